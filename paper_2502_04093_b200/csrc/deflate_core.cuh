@@ -1,0 +1,539 @@
+// deflate_core.cuh -- the zlib-1.3 `compress2(level 6)` semantics the reference's
+// lossless stage produces (proj/src/backend.cpp:15-22), restated as position-
+// parallel pieces so the GPU can produce the identical byte stream.
+//
+// The sequential algorithm (deflate_slow + longest_match + trees.c) is split into
+//   1. per-position hash-chain links           (prev distance, u16)
+//   2. per-position longest-match results      for chain limits 128 and 32
+//   3. a lazy-parse *tag graph*: the parser state at a loop top is one of 4 tags
+//      {A: after a match, B: literal pending, C128/C32: match pending, found with
+//      chain 128/32}, so the parse is a functional graph over (position, tag);
+//      "anchor" positions no match can jump over split it into chunks whose 4-entry
+//      transfer maps compose associatively (parallel scan), then every chunk re-runs
+//      from its true entry tag and emits its symbols
+//   4. blocks of 16383 symbols, zlib's Huffman construction (build_tree/gen_bitlen/
+//      gen_codes, build_bl_tree/scan_tree/send_tree), the stored/static/dynamic
+//      choice including window-slide limits on stored blocks, bit emission.
+// Everything here is __host__ __device__ so tests/native/zmodel.cpp can run the
+// same code on the CPU and diff it against the system libz.
+#pragma once
+#include <stdint.h>
+
+#if defined(__CUDACC__)
+#define HD __host__ __device__ __forceinline__
+#else
+#define HD inline
+#endif
+
+namespace ipz {
+
+constexpr int WSIZE = 32768;
+constexpr int MIN_LOOKAHEAD = 262;
+constexpr int MAX_DIST = WSIZE - MIN_LOOKAHEAD;  // 32506
+constexpr int MIN_MATCH = 3, MAX_MATCH = 258;
+constexpr int GOOD_LENGTH = 8, MAX_LAZY = 16, NICE_LENGTH = 128, MAX_CHAIN = 128;  // configuration_table[6]
+constexpr int TOO_FAR = 4096;
+constexpr int BLOCK_SYMS = 16383;  // lit_bufsize - 1 (memLevel 8)
+constexpr int L_CODES = 286, D_CODES = 30, BL_CODES = 19, END_BLOCK = 256;
+constexpr int HEAP_SIZE = 2 * L_CODES + 1;
+constexpr int MAX_BITS = 15, MAX_BL_BITS = 7;
+
+enum Tag : int { TAG_A = 0, TAG_B = 1, TAG_C128 = 2, TAG_C32 = 3 };
+
+HD uint32_t hash3(uint32_t a, uint32_t b, uint32_t c) { return ((a << 10) ^ (b << 5) ^ c) & 0x7fffu; }
+
+// ----------------------------------------------------------------- match record
+// bits 0-8 L128 | 9-23 D128 | 24-32 L32 | 33-47 D32 | 48 head at exactly MAX_DIST
+HD uint64_t mrec_pack(uint32_t l128, uint32_t d128, uint32_t l32, uint32_t d32, uint32_t flag) {
+    return (uint64_t)l128 | ((uint64_t)d128 << 9) | ((uint64_t)l32 << 24) | ((uint64_t)d32 << 33) | ((uint64_t)flag << 48);
+}
+HD uint32_t mrec_l128(uint64_t r) { return (uint32_t)(r & 0x1ff); }
+HD uint32_t mrec_d128(uint64_t r) { return (uint32_t)((r >> 9) & 0x7fff); }
+HD uint32_t mrec_l32(uint64_t r) { return (uint32_t)((r >> 24) & 0x1ff); }
+HD uint32_t mrec_d32(uint64_t r) { return (uint32_t)((r >> 33) & 0x7fff); }
+HD uint32_t mrec_flag(uint64_t r) { return (uint32_t)((r >> 48) & 1); }
+
+// longest_match (deflate.c) for chain limits 128 and 32 at once.  `prevd[q]` is the
+// distance from q to the previous position with the same hash (0 = none).  Lengths
+// are capped at the lookahead, which is equivalent to zlib's garbage-tolerant scan
+// because nice_match is capped at the lookahead too (the first candidate reaching
+// the data end always terminates the search).
+template <class Bytes, class Prev>
+HD uint64_t match_search(int64_t p, int64_t n, const Bytes &bytes, const Prev &prevd) {
+    if (p + MIN_MATCH > n) return 0;  // not inserted: hash_head = NIL
+    const uint32_t d0 = prevd(p);
+    if (d0 == 0) return 0;
+    int64_t q = p - (int64_t)d0;
+    if (q == 0 || d0 > (uint32_t)MAX_DIST) return 0;  // NIL / too far for the head check
+    const uint32_t flag = d0 == (uint32_t)MAX_DIST;
+    const int64_t maxlen = (n - p) < MAX_MATCH ? (n - p) : MAX_MATCH;
+    const int64_t nice = (n - p) < NICE_LENGTH ? (n - p) : NICE_LENGTH;
+    const int64_t limit = p - MAX_DIST > 0 ? p - MAX_DIST : 0;
+    uint32_t best = 0, bestd = 0, l32 = 0, d32 = 0;
+    for (int i = 1; i <= MAX_CHAIN; ++i) {
+        // match length between p and q (>= 3 only when bytes 0,1 agree: hash implies byte 2)
+        int64_t len = 0;
+        while (len < maxlen && bytes(p + len) == bytes(q + len)) ++len;
+        if (len < MIN_MATCH) len = 0;
+        bool stop = false;
+        if ((uint32_t)len > best) {
+            best = (uint32_t)len;
+            bestd = (uint32_t)(p - q);
+            if (len >= nice) stop = true;
+        }
+        if (i <= 32) {
+            l32 = best;
+            d32 = bestd;
+        }
+        if (stop) break;
+        const uint32_t dq = prevd(q);
+        if (dq == 0) break;
+        const int64_t q2 = q - (int64_t)dq;
+        if (!(q2 > limit)) break;
+        q = q2;
+    }
+    return mrec_pack(best, bestd, l32, d32, flag);
+}
+
+// ------------------------------------------------------------- window slides
+// fill_window slides the 64 KiB window by WSIZE at loop tops; with the whole input
+// available, the k-th slide happens at the first loop top >= slide_threshold(k).
+HD int64_t tail_slide_index(int64_t n) { return n >= 65536 ? (n - 65536) / 32768 + 1 : 0; }
+HD int64_t slides_before(int64_t p, int64_t n) {  // slides done by the loop top at p (inclusive)
+    const int64_t kt = tail_slide_index(n);
+    int64_t c = 0;
+    if (p >= 65275) {
+        c = (p - 65275) / 32768 + 1;
+        if (c > kt) c = kt;
+    }
+    if (p >= n - 261 && p >= 32768 * kt + 65274) c = kt + 1;
+    return c;
+}
+// the head candidate at window index 0 is NIL: only reachable right after a tail slide
+HD bool tail_slide_nil(int64_t p, int64_t n) {
+    const int64_t kt = tail_slide_index(n);
+    return p == 32768 * kt + 65274 && p >= n - 261;
+}
+
+// -------------------------------------------------------------- parse step
+struct Step {
+    int64_t next_p;
+    int next_tag;
+    int emit;          // 0 none, 1 literal, 2 match
+    uint32_t len, dist;  // match length / distance, or literal byte in len
+};
+
+// One iteration of deflate_slow's loop at loop top p entered with `tag`.
+// rp = match record at p, rpm1 = match record at p-1 (only read for tags C*).
+template <class Bytes>
+HD Step parse_step(int64_t p, int tag, int64_t n, uint64_t rp, uint64_t rpm1, const Bytes &bytes) {
+    Step s;
+    uint32_t pl = 2, pd = 0;
+    if (tag == TAG_C128) {
+        pl = mrec_l128(rpm1);
+        pd = mrec_d128(rpm1);
+    } else if (tag == TAG_C32) {
+        pl = mrec_l32(rpm1);
+        pd = mrec_d32(rpm1);
+    }
+    const bool avail = tag != TAG_A;
+    uint32_t ml = 2;
+    int ktag = TAG_C128;
+    if (p + MIN_MATCH <= n && pl < (uint32_t)MAX_LAZY && mrec_l128(rp) != 0 &&
+        !(mrec_flag(rp) && tail_slide_nil(p, n))) {
+        const bool short_chain = pl >= (uint32_t)GOOD_LENGTH;
+        ktag = short_chain ? TAG_C32 : TAG_C128;
+        const uint32_t M = short_chain ? mrec_l32(rp) : mrec_l128(rp);
+        const uint32_t D = short_chain ? mrec_d32(rp) : mrec_d128(rp);
+        if (M > pl) {
+            ml = M;
+            if (ml == MIN_MATCH && D > (uint32_t)TOO_FAR) ml = 2;
+        } else {
+            ml = pl;  // min(pl, lookahead): only used for the emit test below
+        }
+    }
+    if (pl >= MIN_MATCH && ml <= pl) {
+        s.emit = 2;
+        s.len = pl;
+        s.dist = pd;
+        s.next_p = p - 1 + pl;
+        s.next_tag = TAG_A;
+        return s;
+    }
+    s.next_p = p + 1;
+    s.next_tag = ml >= MIN_MATCH ? ktag : TAG_B;
+    if (avail) {
+        s.emit = 1;
+        s.len = bytes(p - 1);
+        s.dist = 0;
+    } else {
+        s.emit = 0;
+        s.len = s.dist = 0;
+    }
+    return s;
+}
+
+// symbol encoding in the symbol stream: literal = byte; match = 1<<31 | (len-3)<<16 | (dist-1)
+HD uint32_t sym_literal(uint32_t c) { return c; }
+HD uint32_t sym_match(uint32_t len, uint32_t dist) { return 0x80000000u | ((len - 3) << 16) | (dist - 1); }
+HD bool sym_is_match(uint32_t s) { return (s & 0x80000000u) != 0; }
+HD uint32_t sym_lc(uint32_t s) { return (s >> 16) & 0xff; }     // len - 3
+HD uint32_t sym_dist1(uint32_t s) { return s & 0xffff; }        // dist - 1
+HD uint32_t sym_bytes(uint32_t s) { return sym_is_match(s) ? sym_lc(s) + 3 : 1; }
+
+// ------------------------------------------------------------ static tables
+HD int ilog2(uint32_t v) {
+    int r = 0;
+    while (v >>= 1) ++r;
+    return r;
+}
+HD uint32_t length_code(uint32_t lc) {  // _length_code[len-3]
+    if (lc < 8) return lc;
+    if (lc == 255) return 28;
+    const int e = ilog2(lc) - 2;
+    return 4u * (uint32_t)e + 4u + ((lc >> e) & 3u);
+}
+HD int extra_lbits(uint32_t code) { return (code < 8 || code == 28) ? 0 : (int)(code - 4) / 4; }
+HD uint32_t base_length(uint32_t code) {
+    if (code < 8) return code;
+    if (code == 28) return 0;
+    const int e = (int)(code - 4) / 4;
+    return (4u + (code & 3u)) << e;
+}
+HD uint32_t dist_code(uint32_t d) {  // d = dist - 1
+    if (d < 4) return d;
+    const int e = ilog2(d) - 1;
+    return 2u * (uint32_t)e + 2u + ((d >> e) & 1u);
+}
+HD int extra_dbits(uint32_t code) { return code < 4 ? 0 : (int)code / 2 - 1; }
+HD uint32_t base_dist(uint32_t code) {
+    if (code < 4) return code;
+    const int e = (int)code / 2 - 1;
+    return (2u + (code & 1u)) << e;
+}
+HD int extra_blbits(int code) { return code == 16 ? 2 : code == 17 ? 3 : code == 18 ? 7 : 0; }
+HD int bl_order(int i) {
+    const int8_t t[19] = {16, 17, 18, 0, 8, 7, 9, 6, 10, 5, 11, 4, 12, 3, 13, 2, 14, 1, 15};
+    return t[i];
+}
+HD uint32_t bi_reverse(uint32_t code, int len) {
+    uint32_t r = 0;
+    for (int i = 0; i < len; ++i) {
+        r = (r << 1) | (code & 1u);
+        code >>= 1;
+    }
+    return r;
+}
+HD int static_llen(int n) { return n < 144 ? 8 : n < 256 ? 9 : n < 280 ? 7 : 8; }
+HD uint32_t static_lcode(int n) {
+    if (n < 144) return bi_reverse(48u + (uint32_t)n, 8);
+    if (n < 256) return bi_reverse(400u + (uint32_t)(n - 144), 9);
+    if (n < 280) return bi_reverse((uint32_t)(n - 256), 7);
+    return bi_reverse(192u + (uint32_t)(n - 280), 8);
+}
+HD uint32_t static_dcode(int n) { return bi_reverse((uint32_t)n, 5); }
+
+// ------------------------------------------------------------- Huffman trees
+struct BlockTrees {
+    uint16_t lcode[L_CODES + 2];
+    uint8_t llen[L_CODES + 2];
+    uint16_t dcode[D_CODES + 2];
+    uint8_t dlen[D_CODES + 2];
+    uint16_t blcode[BL_CODES];
+    uint8_t bllen[BL_CODES];
+    int16_t lmax, dmax, max_blindex;
+    uint8_t type;      // 0 stored, 1 static, 2 dynamic
+    uint8_t last;
+    uint64_t opt_len, static_len;
+    uint64_t body_bits;  // bits after the 3-bit header (stored: 32 + 8*len, alignment not included)
+};
+
+struct TreeScratch {
+    uint16_t freq[HEAP_SIZE];
+    uint16_t dad_len[HEAP_SIZE];  // zlib's dl union: Dad during build, Len after gen_bitlen
+    uint8_t depth[HEAP_SIZE];
+    int16_t heap[HEAP_SIZE];
+    uint16_t bl_count[MAX_BITS + 1];
+    int heap_len, heap_max;
+};
+
+HD bool tr_smaller(const TreeScratch &t, int n, int m) {
+    return t.freq[n] < t.freq[m] || (t.freq[n] == t.freq[m] && t.depth[n] <= t.depth[m]);
+}
+HD void pqdownheap(TreeScratch &t, int k) {
+    const int v = t.heap[k];
+    int j = k << 1;
+    while (j <= t.heap_len) {
+        if (j < t.heap_len && tr_smaller(t, t.heap[j + 1], t.heap[j])) j++;
+        if (tr_smaller(t, v, t.heap[j])) break;
+        t.heap[k] = t.heap[j];
+        k = j;
+        j <<= 1;
+    }
+    t.heap[k] = (int16_t)v;
+}
+
+// build_tree + gen_bitlen + gen_codes (trees.c).  kind: 0 lit/len, 1 dist, 2 bit-length.
+// freq[] of the `elems` leaves must be loaded into t.freq; returns max_code, writes
+// lengths/codes; accumulates opt_len/static_len exactly as zlib does.
+HD int build_tree(TreeScratch &t, int kind, int elems, uint8_t *len_out, uint16_t *code_out, uint64_t &opt_len,
+                  uint64_t &static_len) {
+    const int max_length = kind == 2 ? MAX_BL_BITS : MAX_BITS;
+    int max_code = -1;
+    t.heap_len = 0;
+    t.heap_max = HEAP_SIZE;
+    for (int n = 0; n < elems; n++) {
+        if (t.freq[n] != 0) {
+            t.heap[++t.heap_len] = (int16_t)(max_code = n);
+            t.depth[n] = 0;
+        } else {
+            t.dad_len[n] = 0;
+        }
+    }
+    while (t.heap_len < 2) {
+        const int node = max_code < 2 ? ++max_code : 0;
+        t.heap[++t.heap_len] = (int16_t)node;
+        t.freq[node] = 1;
+        t.depth[node] = 0;
+        opt_len--;
+        if (kind == 0) static_len -= (uint64_t)static_llen(node);
+        else if (kind == 1) static_len -= 5;
+    }
+    for (int n = t.heap_len / 2; n >= 1; n--) pqdownheap(t, n);
+    int node = elems;
+    do {
+        const int n = t.heap[1];  // pqremove
+        t.heap[1] = t.heap[t.heap_len--];
+        pqdownheap(t, 1);
+        const int m = t.heap[1];
+        t.heap[--t.heap_max] = (int16_t)n;
+        t.heap[--t.heap_max] = (int16_t)m;
+        t.freq[node] = (uint16_t)(t.freq[n] + t.freq[m]);
+        t.depth[node] = (uint8_t)((t.depth[n] >= t.depth[m] ? t.depth[n] : t.depth[m]) + 1);
+        t.dad_len[n] = t.dad_len[m] = (uint16_t)node;
+        t.heap[1] = (int16_t)node++;
+        pqdownheap(t, 1);
+    } while (t.heap_len >= 2);
+    t.heap[--t.heap_max] = t.heap[1];
+
+    // gen_bitlen
+    for (int b = 0; b <= MAX_BITS; b++) t.bl_count[b] = 0;
+    t.dad_len[t.heap[t.heap_max]] = 0;
+    int overflow = 0;
+    int h;
+    for (h = t.heap_max + 1; h < HEAP_SIZE; h++) {
+        const int n = t.heap[h];
+        int bits = t.dad_len[t.dad_len[n]] + 1;
+        if (bits > max_length) bits = max_length, overflow++;
+        t.dad_len[n] = (uint16_t)bits;
+        if (n > max_code) continue;
+        t.bl_count[bits]++;
+        int xbits = 0;
+        if (kind == 0 && n >= 257) xbits = extra_lbits((uint32_t)(n - 257));
+        else if (kind == 1) xbits = extra_dbits((uint32_t)n);
+        else if (kind == 2) xbits = extra_blbits(n);
+        const uint64_t f = t.freq[n];
+        opt_len += f * (uint64_t)(bits + xbits);
+        if (kind == 0) static_len += f * (uint64_t)(static_llen(n) + xbits);
+        else if (kind == 1) static_len += f * (uint64_t)(5 + xbits);
+    }
+    if (overflow != 0) {
+        do {
+            int bits = max_length - 1;
+            while (t.bl_count[bits] == 0) bits--;
+            t.bl_count[bits]--;
+            t.bl_count[bits + 1] += 2;
+            t.bl_count[max_length]--;
+            overflow -= 2;
+        } while (overflow > 0);
+        h = HEAP_SIZE;
+        for (int bits = max_length; bits != 0; bits--) {
+            int n = t.bl_count[bits];
+            while (n != 0) {
+                const int m = t.heap[--h];
+                if (m > max_code) continue;
+                if ((unsigned)t.dad_len[m] != (unsigned)bits) {
+                    opt_len += ((uint64_t)bits - (uint64_t)t.dad_len[m]) * (uint64_t)t.freq[m];
+                    t.dad_len[m] = (uint16_t)bits;
+                }
+                n--;
+            }
+        }
+    }
+    // gen_codes
+    uint16_t next_code[MAX_BITS + 1];
+    uint32_t code = 0;
+    for (int bits = 1; bits <= MAX_BITS; bits++) {
+        code = (code + t.bl_count[bits - 1]) << 1;
+        next_code[bits] = (uint16_t)code;
+    }
+    for (int n = 0; n < elems; n++) {
+        const int len = n <= max_code ? t.dad_len[n] : 0;
+        len_out[n] = (uint8_t)len;
+        code_out[n] = len ? (uint16_t)bi_reverse(next_code[len]++, len) : 0;
+    }
+    return max_code;
+}
+
+// scan_tree (counting) / send_tree (emitting) share this run-length walk.
+template <class Visit>
+HD void walk_tree_lengths(const uint8_t *len, int max_code, Visit &&visit) {
+    int prevlen = -1, curlen, nextlen = len[0];
+    int count = 0, max_count = 7, min_count = 4;
+    if (nextlen == 0) max_count = 138, min_count = 3;
+    for (int n = 0; n <= max_code; n++) {
+        curlen = nextlen;
+        nextlen = n + 1 <= max_code ? len[n + 1] : 0xffff;  // guard tree[max_code+1].Len = 0xffff
+        if (++count < max_count && curlen == nextlen) {
+            continue;
+        } else if (count < min_count) {
+            for (int c = 0; c < count; ++c) visit(curlen, 0);
+        } else if (curlen != 0) {
+            if (curlen != prevlen) {
+                visit(curlen, 0);
+                count--;
+            }
+            visit(16, count - 3);
+        } else if (count <= 10) {
+            visit(17, count - 3);
+        } else {
+            visit(18, count - 11);
+        }
+        count = 0;
+        prevlen = curlen;
+        if (nextlen == 0) {
+            max_count = 138, min_count = 3;
+        } else if (curlen == nextlen) {
+            max_count = 6, min_count = 3;
+        } else {
+            max_count = 7, min_count = 4;
+        }
+    }
+}
+// NOTE: scan_tree increments bl_tree[curlen].Freq += count in the count<min_count case,
+// which the per-call visit above reproduces one at a time.
+
+// Build the trees of one block from its symbol histogram (lfreq[286] incl. END_BLOCK=1,
+// dfreq[30]) and choose stored / static / dynamic as _tr_flush_block does.
+HD void plan_block(const uint32_t *lfreq, const uint32_t *dfreq, uint64_t stored_len, bool stored_ok, bool last,
+                   TreeScratch &t, BlockTrees &bt) {
+    uint64_t opt_len = 0, static_len = 0;
+    for (int i = 0; i < HEAP_SIZE; ++i) t.freq[i] = 0;
+    for (int i = 0; i < L_CODES; ++i) t.freq[i] = (uint16_t)lfreq[i];
+    bt.lmax = (int16_t)build_tree(t, 0, L_CODES, bt.llen, bt.lcode, opt_len, static_len);
+    for (int i = 0; i < HEAP_SIZE; ++i) t.freq[i] = 0;
+    for (int i = 0; i < D_CODES; ++i) t.freq[i] = (uint16_t)dfreq[i];
+    bt.dmax = (int16_t)build_tree(t, 1, D_CODES, bt.dlen, bt.dcode, opt_len, static_len);
+    // build_bl_tree
+    uint32_t blf[BL_CODES];
+    for (int i = 0; i < BL_CODES; ++i) blf[i] = 0;
+    auto count_visit = [&](int sym, int) { blf[sym]++; };
+    walk_tree_lengths(bt.llen, bt.lmax, count_visit);
+    walk_tree_lengths(bt.dlen, bt.dmax, count_visit);
+    for (int i = 0; i < HEAP_SIZE; ++i) t.freq[i] = 0;
+    for (int i = 0; i < BL_CODES; ++i) t.freq[i] = (uint16_t)blf[i];
+    build_tree(t, 2, BL_CODES, bt.bllen, bt.blcode, opt_len, static_len);
+    int max_blindex;
+    for (max_blindex = BL_CODES - 1; max_blindex >= 3; max_blindex--)
+        if (bt.bllen[bl_order(max_blindex)] != 0) break;
+    opt_len += 3 * ((uint64_t)max_blindex + 1) + 5 + 5 + 4;
+    bt.max_blindex = (int16_t)max_blindex;
+    bt.opt_len = opt_len;
+    bt.static_len = static_len;
+    bt.last = last ? 1 : 0;
+    uint64_t opt_lenb = (opt_len + 3 + 7) >> 3;
+    const uint64_t static_lenb = (static_len + 3 + 7) >> 3;
+    if (static_lenb <= opt_lenb) opt_lenb = static_lenb;
+    if (stored_len + 4 <= opt_lenb && stored_ok) {
+        bt.type = 0;
+        bt.body_bits = 32 + 8 * stored_len;
+    } else if (static_lenb == opt_lenb) {
+        bt.type = 1;
+        bt.body_bits = static_len;
+    } else {
+        bt.type = 2;
+        // exact emitted bits: counts + bl lengths + tree runs + data (opt_len accounts the same)
+        uint64_t bits = 5 + 5 + 4 + 3 * (uint64_t)(max_blindex + 1);
+        auto size_visit = [&](int sym, int) { bits += bt.bllen[sym] + extra_blbits(sym); };
+        walk_tree_lengths(bt.llen, bt.lmax, size_visit);
+        walk_tree_lengths(bt.dlen, bt.dmax, size_visit);
+        for (int i = 0; i < L_CODES; ++i) {
+            if (!lfreq[i]) continue;
+            const int xb = i >= 257 ? extra_lbits((uint32_t)(i - 257)) : 0;
+            bits += (uint64_t)lfreq[i] * (uint64_t)(bt.llen[i] + xb);
+        }
+        for (int i = 0; i < D_CODES; ++i) {
+            if (!dfreq[i]) continue;
+            bits += (uint64_t)dfreq[i] * (uint64_t)(bt.dlen[i] + extra_dbits((uint32_t)i));
+        }
+        bt.body_bits = bits;
+    }
+}
+
+// bits one symbol costs under the block's chosen (static or dynamic) trees
+HD uint32_t symbol_bits(uint32_t s, const BlockTrees &bt) {
+    if (!sym_is_match(s)) return bt.type == 1 ? (uint32_t)static_llen((int)s) : bt.llen[s];
+    const uint32_t lc = sym_lc(s), code = length_code(lc), d = sym_dist1(s), dc = dist_code(d);
+    const uint32_t ll = bt.type == 1 ? (uint32_t)static_llen((int)(code + 257)) : bt.llen[code + 257];
+    const uint32_t dl = bt.type == 1 ? 5u : bt.dlen[dc];
+    return ll + (uint32_t)extra_lbits(code) + dl + (uint32_t)extra_dbits(dc);
+}
+
+// the (up to 48) bits of one symbol, LSB-first, and their count
+HD uint64_t symbol_code(uint32_t s, const BlockTrees &bt, uint32_t &nbits) {
+    const bool st = bt.type == 1;
+    if (!sym_is_match(s)) {
+        nbits = st ? (uint32_t)static_llen((int)s) : bt.llen[s];
+        return st ? static_lcode((int)s) : bt.lcode[s];
+    }
+    const uint32_t lc = sym_lc(s), code = length_code(lc), d = sym_dist1(s), dc = dist_code(d);
+    uint64_t v = 0;
+    uint32_t pos = 0;
+    const int lsym = (int)code + 257;
+    const uint32_t ll = st ? (uint32_t)static_llen(lsym) : bt.llen[lsym];
+    v |= (uint64_t)(st ? static_lcode(lsym) : bt.lcode[lsym]) << pos;
+    pos += ll;
+    const int xl = extra_lbits(code);
+    if (xl) {
+        v |= (uint64_t)(lc - base_length(code)) << pos;
+        pos += (uint32_t)xl;
+    }
+    const uint32_t dl = st ? 5u : bt.dlen[dc];
+    v |= (uint64_t)(st ? static_dcode((int)dc) : bt.dcode[dc]) << pos;
+    pos += dl;
+    const int xd = extra_dbits(dc);
+    if (xd) {
+        v |= (uint64_t)(d - base_dist(dc)) << pos;
+        pos += (uint32_t)xd;
+    }
+    nbits = pos;
+    return v;
+}
+
+// ------------------------------------------------------------------ checksums
+HD uint32_t crc_multmodp(uint32_t a, uint32_t b) {  // crc32.c multmodp
+    uint32_t m = 1u << 31, p = 0;
+    for (;;) {
+        if (a & m) {
+            p ^= b;
+            if ((a & (m - 1)) == 0) break;
+        }
+        m >>= 1;
+        b = b & 1 ? (b >> 1) ^ 0xedb88320u : b >> 1;
+    }
+    return p;
+}
+// x^(8*len) mod P, by square-and-multiply on x^(2^k)
+HD uint32_t crc_x8n(uint64_t len) {
+    uint32_t p = 1u << 31;     // x^0
+    uint32_t sq = 1u << 27;    // x^8 (x^1 is 1<<30)
+    while (len) {
+        if (len & 1) p = crc_multmodp(sq, p);
+        sq = crc_multmodp(sq, sq);
+        len >>= 1;
+    }
+    return p;
+}
+HD uint32_t crc_combine(uint32_t crc1, uint32_t crc2, uint64_t len2) { return crc_multmodp(crc_x8n(len2), crc1) ^ crc2; }
+
+}  // namespace ipz
