@@ -1,0 +1,121 @@
+/*
+ * ipcomp_b200.h -- the C-ABI drop-in boundary of the B200-native IPComp hot path.
+ *
+ * Plain pointers and sizes only; no torch or C++ types cross this boundary.  Every
+ * call returns an IPCG_* status; the message of the last failure is available from
+ * ipcg_last_error().  The status codes map one-to-one onto the exception types the
+ * reference throws (std::invalid_argument, std::runtime_error, std::domain_error,
+ * ipcomp::InfeasibleRequest), so the C++ host layer (include/ipcomp/pipeline.hpp)
+ * rethrows exactly what the reference would.
+ *
+ * Each entry point names the reference interface it replaces
+ * (paths relative to /root/reference/proj).
+ */
+#ifndef IPCOMP_B200_H
+#define IPCOMP_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define IPCG_OK 0
+#define IPCG_EINVAL 1      /* std::invalid_argument */
+#define IPCG_ERUNTIME 2    /* std::runtime_error    */
+#define IPCG_EDOMAIN 3     /* std::domain_error     */
+#define IPCG_EINFEASIBLE 4 /* ipcomp::InfeasibleRequest (common.hpp:23-25) */
+#define IPCG_ECUDA 5       /* device failure (no reference counterpart) */
+
+#define IPCG_MAX_LEVELS 16
+
+typedef struct ipcg_ctx ipcg_ctx;         /* one CUDA device + stream + workspace  */
+typedef struct ipcg_archive ipcg_archive; /* parsed index + payload (host or device) */
+typedef struct ipcg_session ipcg_session; /* device-resident RetrievalSession        */
+
+/* ArchiveHeader + LevelRecord (include/ipcomp/archive.hpp:19-46), records[l-1] = level l */
+typedef struct {
+    uint64_t count;
+    double delta[33];
+    uint64_t outlier_offset, outlier_length, outlier_count;
+    uint64_t plane_offset[32], plane_length[32];
+} ipcg_level_record;
+
+typedef struct {
+    uint16_t version;
+    uint8_t scalar; /* 0 f32, 1 f64 (common.hpp:14) */
+    uint8_t interp; /* 0 linear, 1 cubic */
+    uint8_t ndims, levels, progressive_levels, anchor_cap;
+    uint64_t dims[4];
+    double eb, range;
+    uint64_t payload_bytes, index_bytes;
+    uint32_t identity; /* crc32 of the index bytes (archive.cpp:161-162) */
+    ipcg_level_record records[IPCG_MAX_LEVELS];
+} ipcg_index;
+
+/* context ---------------------------------------------------------------- */
+int ipcg_ctx_create(int device, ipcg_ctx **out);
+void ipcg_ctx_destroy(ipcg_ctx *ctx);
+const char *ipcg_last_error(const ipcg_ctx *ctx);
+/* CUDA stream all work of this context is ordered on (cudaStream_t, may be 0) */
+int ipcg_set_stream(ipcg_ctx *ctx, void *cuda_stream);
+int ipcg_synchronize(ipcg_ctx *ctx);
+
+/* compress_field<T> (include/ipcomp/pipeline.hpp:140-223).  `values` is a host or
+ * device pointer (values_on_device); the archive is produced device-resident. */
+int ipcg_compress(ipcg_ctx *ctx, int scalar, const void *values, int values_on_device, const uint64_t *dims,
+                  int ndims, double eb, int interp, int progressive_levels, uint64_t anchor_cap, ipcg_archive **out);
+
+/* ArchiveReader(std::istream&) (src/archive.cpp:117-170): parse the index of an
+ * archive held in caller memory (host or device).  The bytes are borrowed, like
+ * the reference's istream, and must outlive the handle. */
+int ipcg_archive_open(ipcg_ctx *ctx, const void *bytes, uint64_t size, int on_device, ipcg_archive **out);
+int ipcg_archive_index(const ipcg_archive *a, ipcg_index *out);
+/* write_archive (src/archive.cpp:72-81): serialized size and copy-out */
+uint64_t ipcg_archive_size(const ipcg_archive *a);
+int ipcg_archive_write(ipcg_ctx *ctx, const ipcg_archive *a, void *dst, int dst_on_device, uint64_t capacity);
+/* ArchiveReader::payload_bytes_read (archive.hpp:81) */
+uint64_t ipcg_archive_payload_bytes_read(const ipcg_archive *a);
+void ipcg_archive_free(ipcg_archive *a);
+
+/* reconstruct_field<T> (pipeline.hpp:260-287): plan k[levels] (RetrievalPlan,
+ * archive.hpp:59-61); out is host or device; *session_out may be NULL. */
+int ipcg_reconstruct(ipcg_ctx *ctx, ipcg_archive *a, int scalar, const int *k, void *out, int out_on_device,
+                     ipcg_session **session_out, uint64_t *payload_bytes_loaded);
+
+/* refine_field<T> (pipeline.hpp:294-352) */
+int ipcg_refine(ipcg_ctx *ctx, ipcg_archive *a, int scalar, const ipcg_session *session, const void *previous,
+                int previous_on_device, const int *k, void *out, int out_on_device, ipcg_session **session_out,
+                uint64_t *payload_bytes_loaded);
+
+/* RetrievalSession (session.hpp:19-34) */
+int ipcg_session_create(ipcg_ctx *ctx, const ipcg_archive *a, const int *planes_loaded,
+                        const uint32_t *const *merged /* [levels], host, NULL for non-progressive */,
+                        ipcg_session **out);
+int ipcg_session_levels(const ipcg_session *s);
+uint32_t ipcg_session_archive_crc(const ipcg_session *s);
+int ipcg_session_planes_loaded(const ipcg_session *s, int *k_out);
+uint64_t ipcg_session_count(const ipcg_session *s, int level);
+int ipcg_session_merged(ipcg_ctx *ctx, const ipcg_session *s, int level, uint32_t *dst, int dst_on_device);
+void ipcg_session_free(ipcg_session *s);
+
+/* planner (src/planner.cpp:30-290) over the index */
+int ipcg_plan_for_error(ipcg_ctx *ctx, const ipcg_archive *a, double max_error, int *k_out);
+int ipcg_plan_for_size(ipcg_ctx *ctx, const ipcg_archive *a, uint64_t byte_budget, int *k_out);
+double ipcg_bound_for_plan(const ipcg_archive *a, const int *k);
+uint64_t ipcg_plan_payload_bytes(const ipcg_archive *a, const int *k);
+
+/* backend_encode (src/backend.cpp:34-53) for `count` equal-length raw planes laid out
+ * at raw + i*raw_stride (host or device).  Payloads are written to out_payload
+ * (host, capacity count*plane_bytes), with per-plane backend id / length / crc32. */
+int ipcg_backend_encode(ipcg_ctx *ctx, const uint8_t *raw, int raw_on_device, uint64_t plane_bytes,
+                        uint64_t raw_stride, int count, uint8_t *backend, uint64_t *length, uint32_t *crc,
+                        uint8_t *out_payload, uint64_t out_capacity);
+
+/* number of kernels this context launched so far (evidence for bench.py) */
+uint64_t ipcg_kernel_launches(const ipcg_ctx *ctx);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

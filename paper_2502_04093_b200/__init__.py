@@ -1,0 +1,480 @@
+"""B200-native IPComp hot path (arXiv 2502.04093) -- Python binding of the C-ABI.
+
+Mirrors the reference's public interface (proj/include/ipcomp/pipeline.hpp, archive.hpp,
+planner.hpp, session.hpp): ``compress_field``, ``ArchiveReader``, ``build_error_model``,
+``plan_for_error``, ``plan_for_size``, ``bound_for_plan``, ``plan_payload_bytes``,
+``full_plan``, ``reconstruct_field``, ``refine_field``; errors raise the Python
+counterparts of the reference's exception types.  All compute runs in the in-tree
+sm_100a library ``libipcomp_b200.so`` (include/ipcomp_b200.h); there is no CPU path --
+importing works without a GPU, but every compute call fails loudly without one.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from dataclasses import dataclass, field
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libipcomp_b200.so")
+MAX_LEVELS = 16
+
+
+class InvalidArgument(ValueError):
+    """std::invalid_argument"""
+
+
+class DomainError(ArithmeticError):
+    """std::domain_error"""
+
+
+class InfeasibleRequest(RuntimeError):
+    """ipcomp::InfeasibleRequest (common.hpp:23-25)"""
+
+
+class CudaError(RuntimeError):
+    """device failure (no reference counterpart)"""
+
+
+_KIND = {1: InvalidArgument, 2: RuntimeError, 3: DomainError, 4: InfeasibleRequest, 5: CudaError}
+
+LINEAR, CUBIC = 0, 1
+
+
+class LevelRecord(C.Structure):
+    _fields_ = [("count", C.c_uint64), ("delta", C.c_double * 33), ("outlier_offset", C.c_uint64),
+                ("outlier_length", C.c_uint64), ("outlier_count", C.c_uint64),
+                ("plane_offset", C.c_uint64 * 32), ("plane_length", C.c_uint64 * 32)]
+
+
+class Index(C.Structure):
+    _fields_ = [("version", C.c_uint16), ("scalar", C.c_uint8), ("interp", C.c_uint8), ("ndims", C.c_uint8),
+                ("levels", C.c_uint8), ("progressive_levels", C.c_uint8), ("anchor_cap", C.c_uint8),
+                ("dims", C.c_uint64 * 4), ("eb", C.c_double), ("range", C.c_double),
+                ("payload_bytes", C.c_uint64), ("index_bytes", C.c_uint64), ("identity", C.c_uint32),
+                ("records", LevelRecord * MAX_LEVELS)]
+
+
+_lib = None
+
+
+def library() -> C.CDLL:
+    """Load the sm_100a library; raises if it was not built (no fallback path exists)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise RuntimeError(f"{LIB_PATH} missing: run paper_2502_04093_b200.build.build() (nvcc, sm_100a)")
+    lib = C.CDLL(LIB_PATH)
+    vp, u64, i32, dbl = C.c_void_p, C.c_uint64, C.c_int, C.c_double
+    P = C.POINTER
+    sig = {
+        "ipcg_ctx_create": (i32, [i32, P(vp)]),
+        "ipcg_ctx_destroy": (None, [vp]),
+        "ipcg_last_error": (C.c_char_p, [vp]),
+        "ipcg_set_stream": (i32, [vp, vp]),
+        "ipcg_synchronize": (i32, [vp]),
+        "ipcg_compress": (i32, [vp, i32, vp, i32, P(u64), i32, dbl, i32, i32, u64, P(vp)]),
+        "ipcg_archive_open": (i32, [vp, vp, u64, i32, P(vp)]),
+        "ipcg_archive_index": (i32, [vp, P(Index)]),
+        "ipcg_archive_size": (u64, [vp]),
+        "ipcg_archive_write": (i32, [vp, vp, vp, i32, u64]),
+        "ipcg_archive_payload_bytes_read": (u64, [vp]),
+        "ipcg_archive_free": (None, [vp]),
+        "ipcg_reconstruct": (i32, [vp, vp, i32, P(i32), vp, i32, P(vp), P(u64)]),
+        "ipcg_refine": (i32, [vp, vp, i32, vp, vp, i32, P(i32), vp, i32, P(vp), P(u64)]),
+        "ipcg_session_create": (i32, [vp, vp, P(i32), P(P(C.c_uint32)), P(vp)]),
+        "ipcg_session_levels": (i32, [vp]),
+        "ipcg_session_archive_crc": (C.c_uint32, [vp]),
+        "ipcg_session_planes_loaded": (i32, [vp, P(i32)]),
+        "ipcg_session_count": (u64, [vp, i32]),
+        "ipcg_session_merged": (i32, [vp, vp, i32, vp, i32]),
+        "ipcg_session_free": (None, [vp]),
+        "ipcg_plan_for_error": (i32, [vp, vp, dbl, P(i32)]),
+        "ipcg_plan_for_size": (i32, [vp, vp, u64, P(i32)]),
+        "ipcg_bound_for_plan": (dbl, [vp, P(i32)]),
+        "ipcg_plan_payload_bytes": (u64, [vp, P(i32)]),
+        "ipcg_backend_encode": (i32, [vp, vp, i32, u64, u64, i32, vp, vp, vp, vp, u64]),
+        "ipcg_kernel_launches": (u64, [vp]),
+    }
+    for name, (res, args) in sig.items():
+        f = getattr(lib, name)
+        f.restype = res
+        f.argtypes = args
+    _lib = lib
+    return lib
+
+
+EXPORTED_SYMBOLS = [
+    "ipcg_ctx_create", "ipcg_ctx_destroy", "ipcg_last_error", "ipcg_set_stream", "ipcg_synchronize",
+    "ipcg_compress", "ipcg_archive_open", "ipcg_archive_index", "ipcg_archive_size", "ipcg_archive_write",
+    "ipcg_archive_payload_bytes_read", "ipcg_archive_free", "ipcg_reconstruct", "ipcg_refine",
+    "ipcg_session_create", "ipcg_session_levels", "ipcg_session_archive_crc", "ipcg_session_planes_loaded",
+    "ipcg_session_count", "ipcg_session_merged", "ipcg_session_free", "ipcg_plan_for_error",
+    "ipcg_plan_for_size", "ipcg_bound_for_plan", "ipcg_plan_payload_bytes", "ipcg_backend_encode",
+    "ipcg_kernel_launches",
+]
+
+
+class Context:
+    """One CUDA device + stream (ipcg_ctx)."""
+
+    _default: dict = {}
+
+    def __init__(self, device: int = 0):
+        lib = library()
+        h = C.c_void_p()
+        rc = lib.ipcg_ctx_create(device, C.byref(h))
+        if rc:
+            raise CudaError(f"cannot create context on cuda:{device} (rc={rc})")
+        self.h = h
+        self.device = device
+
+    @classmethod
+    def default(cls, device: int = 0) -> "Context":
+        if device not in cls._default:
+            cls._default[device] = Context(device)
+        return cls._default[device]
+
+    def check(self, rc: int) -> None:
+        if rc:
+            msg = library().ipcg_last_error(self.h).decode(errors="replace")
+            raise _KIND.get(rc, RuntimeError)(msg)
+
+    def set_stream(self, stream_ptr: int) -> None:
+        self.check(library().ipcg_set_stream(self.h, C.c_void_p(stream_ptr)))
+
+    def synchronize(self) -> None:
+        self.check(library().ipcg_synchronize(self.h))
+
+    def kernel_launches(self) -> int:
+        return int(library().ipcg_kernel_launches(self.h))
+
+    def __del__(self):
+        try:
+            if getattr(self, "h", None) and _lib is not None:
+                _lib.ipcg_ctx_destroy(self.h)
+        except Exception:
+            pass
+
+
+class HostContext:
+    """Context-free handle for host-only calls (index parsing, planning): no device needed."""
+
+    h = None
+    device = 0
+
+    def check(self, rc: int) -> None:
+        if rc:
+            msg = library().ipcg_last_error(None).decode(errors="replace")
+            raise _KIND.get(rc, RuntimeError)(msg)
+
+
+def _ptr(x):
+    """(address, on_device, nbytes) of a numpy array or torch tensor."""
+    if isinstance(x, np.ndarray):
+        assert x.flags.c_contiguous
+        return x.ctypes.data, 0, x.nbytes
+    try:
+        import torch
+
+        if isinstance(x, torch.Tensor):
+            assert x.is_contiguous()
+            return x.data_ptr(), 1 if x.is_cuda else 0, x.numel() * x.element_size()
+    except ImportError:
+        pass
+    if isinstance(x, (bytes, bytearray)):
+        buf = np.frombuffer(x, dtype=np.uint8)
+        return buf.ctypes.data, 0, len(x)
+    raise TypeError(f"unsupported buffer type {type(x)}")
+
+
+def _scalar_of(x) -> int:
+    dt = getattr(x, "dtype", None)
+    s = str(dt)
+    if "float32" in s:
+        return 0
+    if "float64" in s:
+        return 1
+    raise InvalidArgument("field scalars must be f32 or f64")
+
+
+@dataclass
+class ArchiveHeader:
+    scalar: int
+    interp: int
+    dims: tuple
+    eb: float
+    range: float
+    levels: int
+    progressive_levels: int
+    anchor_cap: int
+    payload_bytes: int
+    version: int = 1
+
+
+class ArchiveReader:
+    """ArchiveReader (archive.hpp:63-113): parsed index over archive bytes held in host
+    memory (bytes / numpy) or device memory (torch CUDA tensor).  The bytes are borrowed
+    and kept alive by this object.  Also the owner of a freshly compressed archive."""
+
+    def __init__(self, data=None, ctx: Context | None = None, _handle=None):
+        self.ctx = ctx or Context.default()
+        lib = library()
+        self._keep = data
+        if _handle is not None:
+            self.h = _handle
+        else:
+            if isinstance(data, (bytes, bytearray)):
+                data = np.frombuffer(bytes(data), dtype=np.uint8)
+                self._keep = data
+            addr, on_dev, nbytes = _ptr(data)
+            h = C.c_void_p()
+            self.ctx.check(lib.ipcg_archive_open(self.ctx.h, C.c_void_p(addr), nbytes, on_dev, C.byref(h)))
+            self.h = h
+        self._ix = Index()
+        lib.ipcg_archive_index(self.h, C.byref(self._ix))
+
+    # -- reference accessors
+    def header(self) -> ArchiveHeader:
+        ix = self._ix
+        return ArchiveHeader(ix.scalar, ix.interp, tuple(ix.dims[: ix.ndims]), ix.eb, ix.range, ix.levels,
+                             ix.progressive_levels, ix.anchor_cap, ix.payload_bytes, ix.version)
+
+    def record(self, level: int) -> LevelRecord:
+        return self._ix.records[level - 1]
+
+    def identity(self) -> int:
+        return int(self._ix.identity)
+
+    def index_bytes(self) -> int:
+        return int(self._ix.index_bytes)
+
+    def payload_bytes_read(self) -> int:
+        return int(library().ipcg_archive_payload_bytes_read(self.h))
+
+    @property
+    def levels(self) -> int:
+        return int(self._ix.levels)
+
+    @property
+    def dims(self) -> tuple:
+        return tuple(self._ix.dims[: self._ix.ndims])
+
+    @property
+    def dtype(self):
+        return np.float32 if self._ix.scalar == 0 else np.float64
+
+    def size(self) -> int:
+        return int(library().ipcg_archive_size(self.h))
+
+    def to_bytes(self) -> bytes:
+        """write_archive (archive.cpp:72-81)"""
+        n = self.size()
+        out = np.empty(n, dtype=np.uint8)
+        self.ctx.check(library().ipcg_archive_write(self.ctx.h, self.h, C.c_void_p(out.ctypes.data), 0, n))
+        return out.tobytes()
+
+    def write_to(self, dst) -> None:
+        addr, on_dev, nbytes = _ptr(dst)
+        self.ctx.check(library().ipcg_archive_write(self.ctx.h, self.h, C.c_void_p(addr), on_dev, nbytes))
+
+    def __del__(self):
+        try:
+            if getattr(self, "h", None) and _lib is not None:
+                _lib.ipcg_archive_free(self.h)
+        except Exception:
+            pass
+
+
+def compress_field(values, dims, eb: float, interp: int = CUBIC, progressive_levels: int = 0,
+                   anchor_cap: int = 64, ctx: Context | None = None) -> ArchiveReader:
+    """compress_field<T> (pipeline.hpp:140-223); values: numpy (host) or torch CUDA tensor."""
+    ctx = ctx or Context.default()
+    addr, on_dev, nbytes = _ptr(values)
+    d = (C.c_uint64 * len(dims))(*[int(x) for x in dims])
+    h = C.c_void_p()
+    ctx.check(library().ipcg_compress(ctx.h, _scalar_of(values), C.c_void_p(addr), on_dev, d, len(dims), float(eb),
+                                      int(interp), int(progressive_levels), int(anchor_cap), C.byref(h)))
+    return ArchiveReader(ctx=ctx, _handle=h)
+
+
+@dataclass
+class RetrievalPlan:
+    k: list
+
+
+@dataclass
+class ReconstructStats:
+    level_visits: list
+    payload_bytes_loaded: int
+
+
+class RetrievalSession:
+    """RetrievalSession (session.hpp:19-34); merged codewords stay device-resident."""
+
+    def __init__(self, h, ctx: Context):
+        self.h = h
+        self.ctx = ctx
+
+    @property
+    def archive_crc(self) -> int:
+        return int(library().ipcg_session_archive_crc(self.h))
+
+    def planes_loaded(self) -> list:
+        n = library().ipcg_session_levels(self.h)
+        k = (C.c_int * n)()
+        library().ipcg_session_planes_loaded(self.h, k)
+        return list(k)
+
+    def plan(self) -> RetrievalPlan:
+        return RetrievalPlan(self.planes_loaded())
+
+    def merged(self, level: int):
+        cnt = library().ipcg_session_count(self.h, level)
+        out = np.empty(cnt, dtype=np.uint32)
+        if cnt:
+            self.ctx.check(library().ipcg_session_merged(self.ctx.h, self.h, level, C.c_void_p(out.ctypes.data), 0))
+            return out
+        return None
+
+    @classmethod
+    def from_host(cls, reader: ArchiveReader, planes_loaded, merged) -> "RetrievalSession":
+        L = reader.levels
+        k = (C.c_int * L)(*planes_loaded)
+        arr = (C.POINTER(C.c_uint32) * L)()
+        keep = []
+        for i, m in enumerate(merged):
+            if m is not None:
+                a = np.ascontiguousarray(m, dtype=np.uint32)
+                keep.append(a)
+                arr[i] = a.ctypes.data_as(C.POINTER(C.c_uint32))
+        h = C.c_void_p()
+        reader.ctx.check(library().ipcg_session_create(reader.ctx.h, reader.h, k, arr, C.byref(h)))
+        return cls(h, reader.ctx)
+
+    def __del__(self):
+        try:
+            if getattr(self, "h", None) and _lib is not None:
+                _lib.ipcg_session_free(self.h)
+        except Exception:
+            pass
+
+
+@dataclass
+class Retrieved:
+    values: object
+    session: RetrievalSession | None
+    stats: ReconstructStats = field(default_factory=lambda: ReconstructStats([], 0))
+
+
+def _plan_arr(plan, L):
+    k = plan.k if isinstance(plan, RetrievalPlan) else list(plan)
+    if len(k) != L:
+        raise InvalidArgument("plan level count does not match archive")
+    return (C.c_int * L)(*[int(x) for x in k])
+
+
+def _out_buffer(reader: ArchiveReader, out, device: bool):
+    n = int(np.prod(reader.dims))
+    if out is not None:
+        return out
+    if device:
+        import torch
+
+        return torch.empty(n, dtype=torch.float32 if reader.dtype == np.float32 else torch.float64,
+                           device=f"cuda:{reader.ctx.device}")
+    return np.empty(n, dtype=reader.dtype)
+
+
+def reconstruct_field(reader: ArchiveReader, plan, dtype=None, out=None, device: bool = False,
+                      keep_session: bool = True) -> Retrieved:
+    """reconstruct_field<T> (pipeline.hpp:260-287)."""
+    lib = library()
+    scalar = reader._ix.scalar if dtype is None else (0 if np.dtype(dtype) == np.float32 else 1)
+    k = _plan_arr(plan, reader.levels)
+    out = _out_buffer(reader, out, device)
+    addr, on_dev, _ = _ptr(out)
+    sess = C.c_void_p()
+    loaded = C.c_uint64()
+    reader.ctx.check(lib.ipcg_reconstruct(reader.ctx.h, reader.h, scalar, k, C.c_void_p(addr), on_dev,
+                                          C.byref(sess) if keep_session else None, C.byref(loaded)))
+    s = RetrievalSession(sess, reader.ctx) if keep_session else None
+    return Retrieved(out, s, ReconstructStats([1] * reader.levels, int(loaded.value)))
+
+
+def refine_field(reader: ArchiveReader, session: RetrievalSession, previous, plan, out=None,
+                 keep_session: bool = True) -> Retrieved:
+    """refine_field<T> (pipeline.hpp:294-352)."""
+    lib = library()
+    k = _plan_arr(plan, reader.levels)
+    paddr, pdev, _ = _ptr(previous)
+    if out is None:
+        out = np.empty_like(previous) if isinstance(previous, np.ndarray) else previous.clone()
+    addr, on_dev, _ = _ptr(out)
+    sess = C.c_void_p()
+    loaded = C.c_uint64()
+    scalar = _scalar_of(previous)
+    reader.ctx.check(lib.ipcg_refine(reader.ctx.h, reader.h, scalar, session.h, C.c_void_p(paddr), pdev, k,
+                                     C.c_void_p(addr), on_dev, C.byref(sess) if keep_session else None,
+                                     C.byref(loaded)))
+    s = RetrievalSession(sess, reader.ctx) if keep_session else None
+    visits = [0] * reader.levels
+    for l in range(1, reader._ix.progressive_levels + 1):
+        visits[l - 1] = 1
+    return Retrieved(out, s, ReconstructStats(visits, int(loaded.value)))
+
+
+# ------------------------------------------------------------------ planner
+def build_error_model(reader: ArchiveReader) -> ArchiveReader:
+    """build_error_model (planner.cpp:30-45): the model is the parsed index itself."""
+    return reader
+
+
+def full_plan(model: ArchiveReader) -> RetrievalPlan:
+    return RetrievalPlan([32] * model.levels)
+
+
+def plan_for_error(model: ArchiveReader, max_error: float) -> RetrievalPlan:
+    k = (C.c_int * model.levels)()
+    model.ctx.check(library().ipcg_plan_for_error(model.ctx.h, model.h, float(max_error), k))
+    return RetrievalPlan(list(k))
+
+
+def plan_for_size(model: ArchiveReader, byte_budget: int) -> RetrievalPlan:
+    k = (C.c_int * model.levels)()
+    model.ctx.check(library().ipcg_plan_for_size(model.ctx.h, model.h, int(byte_budget), k))
+    return RetrievalPlan(list(k))
+
+
+def bound_for_plan(model: ArchiveReader, plan) -> float:
+    return float(library().ipcg_bound_for_plan(model.h, _plan_arr(plan, model.levels)))
+
+
+def plan_payload_bytes(model: ArchiveReader, plan) -> int:
+    return int(library().ipcg_plan_payload_bytes(model.h, _plan_arr(plan, model.levels)))
+
+
+def backend_encode(planes: np.ndarray, ctx: Context | None = None):
+    """backend_encode (backend.cpp:34-53) for a (count, plane_bytes) uint8 array of planes.
+    Returns a list of (backend, payload bytes, crc32)."""
+    ctx = ctx or Context.default()
+    planes = np.ascontiguousarray(planes, dtype=np.uint8)
+    if planes.ndim == 1:
+        planes = planes[None, :]
+    count, nbytes = planes.shape
+    be = np.zeros(count, np.uint8)
+    ln = np.zeros(count, np.uint64)
+    cr = np.zeros(count, np.uint32)
+    cap = max(1, count * nbytes)
+    out = np.empty(cap, np.uint8)
+    ctx.check(library().ipcg_backend_encode(ctx.h, C.c_void_p(planes.ctypes.data), 0, nbytes, nbytes, count,
+                                            C.c_void_p(be.ctypes.data), C.c_void_p(ln.ctypes.data),
+                                            C.c_void_p(cr.ctypes.data), C.c_void_p(out.ctypes.data), cap))
+    res, o = [], 0
+    for i in range(count):
+        L = int(ln[i])
+        res.append((int(be[i]), out[o:o + L].tobytes(), int(cr[i])))
+        o += L
+    return res

@@ -1,0 +1,732 @@
+// deflate.cu -- sm_100a implementation of DeflateBatch: the zlib-1.3 compress2(level 6)
+// byte stream for many equal-length bitplanes at once.  Stage semantics live in
+// deflate_core.cuh (shared with the CPU model in tests/native/zmodel.cpp, which is
+// diffed against libz); this file only maps the stages onto the GPU:
+//   scan (zero test, Adler-32) -> prevlinks (warp-serial hash heads in smem) ->
+//   match search (thread/position) -> anchors (block max-scan) -> chunk bounds ->
+//   chunk transfer maps (thread per chunk x tag) -> resolve (warp scan of 4->4 maps) ->
+//   symbol emission -> per-block Huffman plans -> bit layout -> bit emission ->
+//   CRC-32 (chunked + GF(2) combine).
+// All-zero planes (most high planes) are compressed once per batch and shared.
+#include "deflate.cuh"
+#include "deflate_core.cuh"
+
+namespace ipcg {
+
+using namespace ipz;
+
+namespace {
+
+constexpr int CH = DeflateBatch::CH;
+constexpr int PL_WARPS = 3;  // prevlink warps per CTA (64 KiB head table each)
+constexpr int CRC_CHUNK = 4096;
+
+struct StreamMeta {
+    unsigned long long nonzero, adA, adB;
+    uint32_t adler;
+    int active, rep, final_tag;
+    unsigned long long S_loop, nsyms, nblocks, total_bits, comp_len;
+};
+
+struct Bump {
+    uint8_t *p;
+    size_t off = 0;
+    template <class T>
+    T *take(size_t count) {
+        off = (off + 255) & ~size_t(255);
+        T *r = reinterpret_cast<T *>(p + off);
+        off += count * sizeof(T) + 16;
+        return r;
+    }
+};
+
+struct Work {
+    StreamMeta *meta;
+    uint16_t *prevd;
+    uint64_t *rec;
+    uint64_t *first_anchor, *bnd;
+    uint8_t *exit4;
+    uint32_t *cnt4;
+    uint8_t *entry;
+    uint64_t *symoff;
+    uint32_t *syms;
+    uint64_t *blk_top, *blk_start, *blk_bitpos;
+    BlockTrees *trees;
+    uint32_t *crc_part;
+    uint32_t *crc_tab;
+    uint64_t nchunks, maxb, ncrc;
+};
+
+Work carve(void *ws, int S, uint64_t n) {
+    Bump b{static_cast<uint8_t *>(ws)};
+    Work w;
+    w.nchunks = (n + CH - 1) / CH;
+    w.maxb = n / BLOCK_SYMS + 2;
+    w.ncrc = (n + 64 + CRC_CHUNK - 1) / CRC_CHUNK + 1;
+    w.meta = b.take<StreamMeta>(S);
+    w.prevd = b.take<uint16_t>((size_t)S * n);
+    w.rec = b.take<uint64_t>((size_t)S * n);
+    w.first_anchor = b.take<uint64_t>((size_t)S * w.nchunks);
+    w.bnd = b.take<uint64_t>((size_t)S * (w.nchunks + 1));
+    w.exit4 = b.take<uint8_t>((size_t)S * w.nchunks * 4);
+    w.cnt4 = b.take<uint32_t>((size_t)S * w.nchunks * 4);
+    w.entry = b.take<uint8_t>((size_t)S * (w.nchunks + 1));
+    w.symoff = b.take<uint64_t>((size_t)S * w.nchunks);
+    w.syms = b.take<uint32_t>((size_t)S * (n + 1));
+    w.blk_top = b.take<uint64_t>((size_t)S * w.maxb);
+    w.blk_start = b.take<uint64_t>((size_t)S * w.maxb);
+    w.blk_bitpos = b.take<uint64_t>((size_t)S * w.maxb);
+    w.trees = b.take<BlockTrees>((size_t)S * w.maxb);
+    w.crc_part = b.take<uint32_t>((size_t)S * w.ncrc);
+    w.crc_tab = b.take<uint32_t>(8 * 256);
+    (void)b;
+    return w;
+}
+
+size_t carve_size(int S, uint64_t n) {
+    Bump b{nullptr};
+    Work w;
+    w.nchunks = (n + CH - 1) / CH;
+    w.maxb = n / BLOCK_SYMS + 2;
+    w.ncrc = (n + 64 + CRC_CHUNK - 1) / CRC_CHUNK + 1;
+    b.take<StreamMeta>(S);
+    b.take<uint16_t>((size_t)S * n);
+    b.take<uint64_t>((size_t)S * n);
+    b.take<uint64_t>((size_t)S * w.nchunks);
+    b.take<uint64_t>((size_t)S * (w.nchunks + 1));
+    b.take<uint8_t>((size_t)S * w.nchunks * 4);
+    b.take<uint32_t>((size_t)S * w.nchunks * 4);
+    b.take<uint8_t>((size_t)S * (w.nchunks + 1));
+    b.take<uint64_t>((size_t)S * w.nchunks);
+    b.take<uint32_t>((size_t)S * (n + 1));
+    b.take<uint64_t>((size_t)S * w.maxb);
+    b.take<uint64_t>((size_t)S * w.maxb);
+    b.take<uint64_t>((size_t)S * w.maxb);
+    b.take<BlockTrees>((size_t)S * w.maxb);
+    b.take<uint32_t>((size_t)S * w.ncrc);
+    b.take<uint32_t>(8 * 256);
+    return b.off + 256;
+}
+
+struct InBytes {
+    const uint8_t *p;
+    __device__ __forceinline__ uint32_t operator()(int64_t i) const { return __ldg(p + i); }
+};
+struct PrevD {
+    const uint16_t *p;
+    __device__ __forceinline__ uint32_t operator()(int64_t i) const { return __ldg(p + i); }
+};
+
+// ------------------------------------------------------------------ 1. scan
+__global__ void k_scan(const uint8_t *in, uint64_t in_stride, uint64_t n, StreamMeta *meta) {
+    const int j = blockIdx.y;
+    const uint8_t *p = in + (uint64_t)j * in_stride;
+    unsigned long long nz = 0, A = 0, B = 0;
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
+        const uint32_t b = p[i];
+        nz |= b;
+        A += b;
+        B += (unsigned long long)(n - i) % 65521u * b;
+    }
+    B %= 65521u;
+    nz = __reduce_or_sync(0xffffffffu, (unsigned)nz);
+    for (int o = 16; o > 0; o >>= 1) {
+        A += __shfl_down_sync(0xffffffffu, A, o);
+        B += __shfl_down_sync(0xffffffffu, B, o);
+    }
+    if ((threadIdx.x & 31) == 0) {
+        if (nz) atomicOr(&meta[j].nonzero, 1ull);
+        atomicAdd(&meta[j].adA, A);
+        atomicAdd(&meta[j].adB, B % 65521u);
+    }
+}
+
+__global__ void k_select(StreamMeta *meta, int S, uint64_t n) {
+    if (threadIdx.x != 0 || blockIdx.x != 0) return;
+    int rep = -1;
+    for (int j = 0; j < S; ++j)
+        if (!meta[j].nonzero) {
+            rep = j;
+            break;
+        }
+    for (int j = 0; j < S; ++j) {
+        StreamMeta &m = meta[j];
+        m.rep = rep;
+        m.active = (m.nonzero || j == rep) && n > 0;
+        const uint32_t a = (uint32_t)((1 + m.adA) % 65521u);
+        const uint32_t b = (uint32_t)((m.adB + n) % 65521u);
+        m.adler = (b << 16) | a;
+    }
+}
+
+// ------------------------------------------------------------- 2. prevlinks
+// zlib's head/prev insertion order is sequential; one warp walks 32 positions per
+// step through a 64 KiB shared-memory head table (match_any resolves same-step
+// collisions).  Each warp owns a 32 KiB block and warms up on the block before it.
+__global__ void __launch_bounds__(PL_WARPS * 32) k_prevlinks(const uint8_t *in, uint64_t in_stride, uint64_t n,
+                                                           const StreamMeta *meta, uint16_t *prevd_all) {
+    extern __shared__ uint16_t heads[];
+    const int j = blockIdx.y;
+    if (!meta[j].active) return;
+    const unsigned warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint64_t blk = (uint64_t)blockIdx.x * PL_WARPS + warp;
+    if (blk * WSIZE >= n) return;
+    uint16_t *head = heads + (size_t)warp * 32768;
+    for (int i = lane; i < 32768; i += 32) head[i] = 0xFFFF;
+    __syncwarp();
+    const uint8_t *p = in + (uint64_t)j * in_stride;
+    uint16_t *prevd = prevd_all + (uint64_t)j * n;
+    const uint64_t base = blk == 0 ? 0 : (blk - 1) * WSIZE;
+    const uint64_t out0 = blk * WSIZE, end = min(n, (blk + 1) * WSIZE);
+    for (uint64_t pos = base; pos < end; pos += 32) {
+        const uint64_t q = pos + lane;
+        const bool valid = q + MIN_MATCH <= n && q < end;
+        const uint32_t h = valid ? hash3(p[q], p[q + 1], p[q + 2]) : (0x10000u + lane);
+        const uint32_t rel = (uint32_t)(q - base);
+        const unsigned mask = __match_any_sync(0xffffffffu, h);
+        const unsigned lower = mask & ((1u << lane) - 1u);
+        uint32_t prel = 0xFFFF;
+        if (lower) prel = rel - (lane - (31u - __clz(lower)));
+        else if (valid) prel = head[h];
+        __syncwarp();
+        if (valid && lane == 31u - __clz(mask)) head[h] = (uint16_t)rel;
+        __syncwarp();
+        if (q >= out0 && q < end) {
+            uint32_t d = 0;
+            if (valid && prel != 0xFFFF && rel - prel < (uint32_t)WSIZE) d = rel - prel;
+            prevd[q] = (uint16_t)d;
+        }
+    }
+}
+
+// ------------------------------------------------------------ 3. match search
+__global__ void __launch_bounds__(256) k_match(const uint8_t *in, uint64_t in_stride, uint64_t n,
+                                              const StreamMeta *meta, const uint16_t *prevd_all, uint64_t *rec_all) {
+    const int j = blockIdx.y;
+    if (!meta[j].active) return;
+    const InBytes bytes{in + (uint64_t)j * in_stride};
+    const PrevD prev{prevd_all + (uint64_t)j * n};
+    uint64_t *rec = rec_all + (uint64_t)j * n;
+    for (uint64_t p = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; p < n; p += (uint64_t)gridDim.x * blockDim.x)
+        rec[p] = match_search((int64_t)p, (int64_t)n, bytes, prev);
+}
+
+// ---------------------------------------------------------------- 4. anchors
+// p is an anchor iff no match found at q < p reaches past p: max_{q<p}(q+max(L128,1)) <= p
+__global__ void __launch_bounds__(256) k_anchor(uint64_t n, const StreamMeta *meta, const uint64_t *rec_all,
+                                               uint64_t nchunks, uint64_t *first_anchor) {
+    const int j = blockIdx.y;
+    const uint64_t c = blockIdx.x;
+    if (c >= nchunks) return;
+    if (!meta[j].active) return;
+    const uint64_t *rec = rec_all + (uint64_t)j * n;
+    const uint64_t c0 = c * CH, c1 = min(n, c0 + CH);
+    const uint64_t r0 = c0 >= MAX_MATCH ? c0 - MAX_MATCH : 0;
+    const uint64_t len = c1 - r0;
+    const uint64_t per = (len + blockDim.x - 1) / blockDim.x;
+    const uint64_t s0 = r0 + threadIdx.x * per, s1 = min(c1, s0 + per);
+    uint64_t mx = 0;
+    for (uint64_t q = s0; q < s1; ++q) {
+        const uint32_t l = mrec_l128(rec[q]);
+        const uint64_t r = q + (l ? l : 1);
+        mx = r > mx ? r : mx;
+    }
+    __shared__ uint64_t scan[256];
+    __shared__ unsigned long long best;
+    scan[threadIdx.x] = mx;
+    if (threadIdx.x == 0) best = ~0ull;
+    __syncthreads();
+    for (unsigned o = 1; o < blockDim.x; o <<= 1) {  // inclusive max-scan
+        const uint64_t v = threadIdx.x >= o ? scan[threadIdx.x - o] : 0;
+        __syncthreads();
+        if (v > scan[threadIdx.x]) scan[threadIdx.x] = v;
+        __syncthreads();
+    }
+    uint64_t run = threadIdx.x ? scan[threadIdx.x - 1] : 0;
+    for (uint64_t q = s0; q < s1; ++q) {
+        if (q >= c0 && run <= q) {
+            atomicMin(&best, (unsigned long long)q);
+            break;
+        }
+        const uint32_t l = mrec_l128(rec[q]);
+        const uint64_t r = q + (l ? l : 1);
+        run = r > run ? r : run;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) first_anchor[(uint64_t)j * nchunks + c] = best;
+}
+
+// chunk boundaries: bnd[k] = first anchor >= k*CH (suffix-min over chunks)
+__global__ void k_bounds(uint64_t n, const StreamMeta *meta, uint64_t nchunks, const uint64_t *first_anchor,
+                         uint64_t *bnd_all) {
+    const int j = blockIdx.x;
+    if (!meta[j].active) return;
+    const unsigned lane = threadIdx.x;
+    const uint64_t *fa = first_anchor + (uint64_t)j * nchunks;
+    uint64_t *bnd = bnd_all + (uint64_t)j * (nchunks + 1);
+    uint64_t carry = n;
+    if (lane == 0) bnd[nchunks] = n;
+    for (int64_t g = (int64_t)((nchunks + 31) / 32) - 1; g >= 0; --g) {
+        const uint64_t k = (uint64_t)g * 32 + lane;
+        uint64_t v = k < nchunks ? fa[k] : ~0ull;
+        for (int o = 1; o < 32; o <<= 1) {  // suffix min
+            const uint64_t w = __shfl_down_sync(0xffffffffu, v, o);
+            if (lane + o < 32 && w < v) v = w;
+        }
+        v = v < carry ? v : carry;
+        if (k < nchunks) bnd[k] = k == 0 ? 0 : v;
+        carry = __shfl_sync(0xffffffffu, v, 0);
+    }
+}
+
+// ------------------------------------------------------ 5. chunk transfer maps
+__global__ void __launch_bounds__(128) k_sim(const uint8_t *in, uint64_t in_stride, uint64_t n, const StreamMeta *meta,
+                                            const uint64_t *rec_all, uint64_t nchunks, const uint64_t *bnd_all,
+                                            uint8_t *exit4, uint32_t *cnt4) {
+    const int j = blockIdx.y;
+    if (!meta[j].active) return;
+    const uint64_t t = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+    if (t >= nchunks * 4) return;
+    const uint64_t k = t >> 2;
+    int tag = (int)(t & 3);
+    const uint64_t *bnd = bnd_all + (uint64_t)j * (nchunks + 1);
+    const uint64_t b0 = bnd[k], b1 = bnd[k + 1];
+    const uint64_t *rec = rec_all + (uint64_t)j * n;
+    const InBytes bytes{in + (uint64_t)j * in_stride};
+    uint32_t count = 0;
+    int64_t p = (int64_t)b0;
+    while (p < (int64_t)b1) {
+        const Step s = parse_step(p, tag, (int64_t)n, rec[p], p > 0 ? rec[p - 1] : 0ull, bytes);
+        count += s.emit != 0;
+        p = s.next_p;
+        tag = s.next_tag;
+    }
+    exit4[(uint64_t)j * nchunks * 4 + t] = (uint8_t)tag;
+    cnt4[(uint64_t)j * nchunks * 4 + t] = count;
+}
+
+// ---------------------------------------------------------------- 6. resolve
+__device__ __forceinline__ uint32_t map_apply(uint32_t m, int t) { return (m >> (2 * t)) & 3u; }
+__device__ __forceinline__ uint32_t map_then(uint32_t f, uint32_t g) {  // g(f(t))
+    uint32_t r = 0;
+    for (int t = 0; t < 4; ++t) r |= map_apply(g, (int)map_apply(f, t)) << (2 * t);
+    return r;
+}
+
+__global__ void k_resolve(const uint8_t *in, uint64_t in_stride, uint64_t n, StreamMeta *meta, uint64_t nchunks,
+                          const uint8_t *exit4_all, const uint32_t *cnt4_all, uint8_t *entry_all, uint64_t *symoff_all,
+                          uint32_t *syms_all, uint64_t maxb, uint64_t *blk_start_all) {
+    const int j = blockIdx.x;
+    StreamMeta &m = meta[j];
+    if (!m.active) return;
+    const unsigned lane = threadIdx.x;
+    const uint8_t *ex = exit4_all + (uint64_t)j * nchunks * 4;
+    const uint32_t *cn = cnt4_all + (uint64_t)j * nchunks * 4;
+    uint8_t *entry = entry_all + (uint64_t)j * (nchunks + 1);
+    uint64_t *symoff = symoff_all + (uint64_t)j * nchunks;
+    int carry_tag = TAG_A;
+    uint64_t carry_sym = 0;
+    for (uint64_t g = 0; g < nchunks; g += 32) {
+        const uint64_t k = g + lane;
+        uint32_t mp = 0xE4;  // identity map (0,1,2,3)
+        if (k < nchunks) mp = ex[k * 4] | (ex[k * 4 + 1] << 2) | (ex[k * 4 + 2] << 4) | (ex[k * 4 + 3] << 6);
+        uint32_t incl = mp;
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t other = __shfl_up_sync(0xffffffffu, incl, o);
+            if ((int)lane >= o) incl = map_then(other, incl);
+        }
+        uint32_t excl = __shfl_up_sync(0xffffffffu, incl, 1);
+        if (lane == 0) excl = 0xE4;
+        const int my_entry = (int)map_apply(excl, carry_tag);
+        const uint64_t c = k < nchunks ? cn[k * 4 + my_entry] : 0;
+        uint64_t cs = c;
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint64_t other = __shfl_up_sync(0xffffffffu, cs, o);
+            if ((int)lane >= o) cs += other;
+        }
+        if (k < nchunks) {
+            entry[k] = (uint8_t)my_entry;
+            symoff[k] = carry_sym + cs - c;
+        }
+        const uint32_t last_incl = __shfl_sync(0xffffffffu, incl, 31);
+        carry_tag = (int)map_apply(last_incl, carry_tag);
+        carry_sym += __shfl_sync(0xffffffffu, cs, 31);
+    }
+    if (lane == 0) {
+        entry[nchunks] = (uint8_t)carry_tag;
+        m.S_loop = carry_sym;
+        m.final_tag = carry_tag;
+        const bool fin = carry_tag != TAG_A && n > 0;
+        m.nsyms = carry_sym + (fin ? 1 : 0);
+        m.nblocks = carry_sym / BLOCK_SYMS + 1;
+        uint64_t *bs = blk_start_all + (uint64_t)j * maxb;
+        if (fin) {
+            syms_all[(uint64_t)j * (n + 1) + carry_sym] = sym_literal(in[(uint64_t)j * in_stride + n - 1]);
+            if (carry_sym % BLOCK_SYMS == 0) bs[carry_sym / BLOCK_SYMS] = n - 1;
+        }
+        if (m.nsyms == (m.nblocks - 1) * BLOCK_SYMS) bs[m.nblocks - 1] = n;  // empty final block
+    }
+}
+
+// ------------------------------------------------------------ 7. emit symbols
+__global__ void __launch_bounds__(128) k_emit_syms(const uint8_t *in, uint64_t in_stride, uint64_t n,
+                                                  const StreamMeta *meta, const uint64_t *rec_all, uint64_t nchunks,
+                                                  const uint64_t *bnd_all, const uint8_t *entry_all,
+                                                  const uint64_t *symoff_all, uint32_t *syms_all, uint64_t maxb,
+                                                  uint64_t *blk_top_all, uint64_t *blk_start_all) {
+    const int j = blockIdx.y;
+    if (!meta[j].active) return;
+    const uint64_t k = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+    if (k >= nchunks) return;
+    const uint64_t *bnd = bnd_all + (uint64_t)j * (nchunks + 1);
+    const uint64_t b0 = bnd[k], b1 = bnd[k + 1];
+    if (b0 >= b1) return;
+    const uint64_t *rec = rec_all + (uint64_t)j * n;
+    const InBytes bytes{in + (uint64_t)j * in_stride};
+    uint32_t *syms = syms_all + (uint64_t)j * (n + 1);
+    uint64_t *btop = blk_top_all + (uint64_t)j * maxb;
+    uint64_t *bstart = blk_start_all + (uint64_t)j * maxb;
+    int tag = entry_all[(uint64_t)j * (nchunks + 1) + k];
+    uint64_t g = symoff_all[(uint64_t)j * nchunks + k];
+    int64_t p = (int64_t)b0;
+    while (p < (int64_t)b1) {
+        const Step s = parse_step(p, tag, (int64_t)n, rec[p], p > 0 ? rec[p - 1] : 0ull, bytes);
+        if (s.emit) {
+            syms[g] = s.emit == 2 ? sym_match(s.len, s.dist) : sym_literal(s.len);
+            if (g % BLOCK_SYMS == 0) bstart[g / BLOCK_SYMS] = (uint64_t)p - 1;
+            if (g % BLOCK_SYMS == BLOCK_SYMS - 1) btop[g / BLOCK_SYMS] = (uint64_t)p;
+            ++g;
+        }
+        p = s.next_p;
+        tag = s.next_tag;
+    }
+}
+
+// ------------------------------------------------------------ 8. block plans
+__global__ void __launch_bounds__(256) k_plan(uint64_t n, const StreamMeta *meta, const uint32_t *syms_all,
+                                             uint64_t maxb, const uint64_t *blk_top_all,
+                                             const uint64_t *blk_start_all, BlockTrees *trees_all) {
+    const int j = blockIdx.y;
+    const StreamMeta &m = meta[j];
+    const uint64_t b = blockIdx.x;
+    if (!m.active || b >= m.nblocks) return;
+    __shared__ uint32_t lf[L_CODES], df[D_CODES];
+    __shared__ TreeScratch ts;
+    for (int i = threadIdx.x; i < L_CODES; i += blockDim.x) lf[i] = 0;
+    for (int i = threadIdx.x; i < D_CODES; i += blockDim.x) df[i] = 0;
+    __syncthreads();
+    const uint32_t *syms = syms_all + (uint64_t)j * (n + 1);
+    const uint64_t s0 = b * BLOCK_SYMS, s1 = min((uint64_t)m.nsyms, (uint64_t)(s0 + BLOCK_SYMS));
+    for (uint64_t i = s0 + threadIdx.x; i < s1; i += blockDim.x) {
+        const uint32_t s = syms[i];
+        if (sym_is_match(s)) {
+            atomicAdd(&lf[length_code(sym_lc(s)) + 257], 1u);
+            atomicAdd(&df[dist_code(sym_dist1(s))], 1u);
+        } else {
+            atomicAdd(&lf[s], 1u);
+        }
+    }
+    __syncthreads();
+    if (threadIdx.x != 0) return;
+    lf[END_BLOCK] = 1;
+    const bool last = b + 1 == m.nblocks;
+    const uint64_t *bstart = blk_start_all + (uint64_t)j * maxb;
+    const uint64_t start = bstart[b];
+    const uint64_t stop = last ? n : bstart[b + 1];
+    const uint64_t pf = last ? n : blk_top_all[(uint64_t)j * maxb + b];
+    const int64_t offset = 32768 * slides_before((int64_t)pf, (int64_t)n);
+    plan_block(lf, df, stop - start, (int64_t)start >= offset, last, ts, trees_all[(uint64_t)j * maxb + b]);
+}
+
+// --------------------------------------------------------------- 9. layout
+__global__ void k_layout(uint64_t n, StreamMeta *meta, int S, uint64_t maxb, const BlockTrees *trees_all,
+                         uint64_t *bitpos_all) {
+    const int j = blockIdx.x * blockDim.x + threadIdx.x;
+    if (j >= S) return;
+    StreamMeta &m = meta[j];
+    if (!m.active) return;
+    const BlockTrees *tr = trees_all + (uint64_t)j * maxb;
+    uint64_t *bp = bitpos_all + (uint64_t)j * maxb;
+    uint64_t pos = 16;
+    for (uint64_t b = 0; b < m.nblocks; ++b) {
+        bp[b] = pos;
+        if (tr[b].type == 0) pos = ((pos + 3 + 7) & ~7ull) + tr[b].body_bits;
+        else pos += 3 + tr[b].body_bits;
+    }
+    m.total_bits = pos;
+    m.comp_len = (pos + 7) / 8 + 4;
+}
+
+__global__ void k_zero_out(uint64_t n, const StreamMeta *meta, uint8_t *out, uint64_t out_stride) {
+    const int j = blockIdx.y;
+    const StreamMeta &m = meta[j];
+    if (!m.active || m.comp_len >= n) return;
+    uint64_t *o = reinterpret_cast<uint64_t *>(out + (uint64_t)j * out_stride);
+    const uint64_t words = (m.comp_len + 15) / 8;
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < words; i += (uint64_t)gridDim.x * blockDim.x)
+        o[i] = 0;
+}
+
+// -------------------------------------------------------------- 10. emission
+__device__ __forceinline__ void put_bits(unsigned long long *w, uint64_t pos, uint64_t v, uint32_t nb) {
+    if (nb == 0) return;
+    const uint64_t word = pos >> 6;
+    const uint32_t sh = (uint32_t)(pos & 63);
+    atomicOr(&w[word], (unsigned long long)(v << sh));
+    if (sh + nb > 64) atomicOr(&w[word + 1], (unsigned long long)(v >> (64 - sh)));
+}
+
+__global__ void __launch_bounds__(256) k_emit(const uint8_t *in, uint64_t in_stride, uint64_t n, const StreamMeta *meta,
+                                             const uint32_t *syms_all, uint64_t maxb, const uint64_t *blk_start_all,
+                                             const BlockTrees *trees_all, const uint64_t *bitpos_all, uint8_t *out,
+                                             uint64_t out_stride) {
+    const int j = blockIdx.y;
+    const StreamMeta &m = meta[j];
+    const uint64_t b = blockIdx.x;
+    if (!m.active || m.comp_len >= n || b >= m.nblocks) return;
+    unsigned long long *w = reinterpret_cast<unsigned long long *>(out + (uint64_t)j * out_stride);
+    const BlockTrees &bt = trees_all[(uint64_t)j * maxb + b];
+    const bool last = b + 1 == m.nblocks;
+    const uint64_t start = bitpos_all[(uint64_t)j * maxb + b];
+    const uint64_t *bstart = blk_start_all + (uint64_t)j * maxb;
+    const uint64_t byte0 = bstart[b], byte1 = last ? n : bstart[b + 1];
+    __shared__ uint64_t hdr_end;
+    if (threadIdx.x == 0) {
+        if (b == 0) put_bits(w, 0, 0x9c78ull, 16);
+        if (last) {
+            const uint64_t tb = (m.total_bits + 7) / 8;
+            const uint32_t a = m.adler;
+            const uint64_t v = ((uint64_t)(a >> 24) & 0xff) | (((uint64_t)(a >> 16) & 0xff) << 8) |
+                               (((uint64_t)(a >> 8) & 0xff) << 16) | (((uint64_t)a & 0xff) << 24);
+            put_bits(w, tb * 8, v, 32);
+        }
+        uint64_t pos = start;
+        const uint32_t type = bt.type == 0 ? 0u : bt.type == 1 ? 1u : 2u;
+        put_bits(w, pos, type * 2 + (last ? 1 : 0), 3);
+        pos += 3;
+        if (bt.type == 0) {
+            pos = (pos + 7) & ~7ull;
+            const uint64_t len = byte1 - byte0;
+            put_bits(w, pos, (len & 0xffff) | ((~len & 0xffff) << 16), 32);
+            pos += 32;
+        } else if (bt.type == 2) {
+            const int lcodes = bt.lmax + 1, dcodes = bt.dmax + 1, blcodes = bt.max_blindex + 1;
+            put_bits(w, pos, (uint64_t)(lcodes - 257) | ((uint64_t)(dcodes - 1) << 5) | ((uint64_t)(blcodes - 4) << 10), 14);
+            pos += 14;
+            for (int r = 0; r < blcodes; ++r, pos += 3) put_bits(w, pos, bt.bllen[bl_order(r)], 3);
+            auto send = [&](int sym, int extra) {
+                put_bits(w, pos, bt.blcode[sym], bt.bllen[sym]);
+                pos += bt.bllen[sym];
+                const int xb = extra_blbits(sym);
+                if (xb) {
+                    put_bits(w, pos, (uint64_t)extra, (uint32_t)xb);
+                    pos += (uint32_t)xb;
+                }
+            };
+            walk_tree_lengths(bt.llen, bt.lmax, send);
+            walk_tree_lengths(bt.dlen, bt.dmax, send);
+        }
+        hdr_end = pos;
+    }
+    __syncthreads();
+    if (bt.type == 0) {
+        const uint8_t *src = in + (uint64_t)j * in_stride + byte0;
+        uint8_t *dst = out + (uint64_t)j * out_stride + hdr_end / 8;
+        for (uint64_t i = threadIdx.x; i < byte1 - byte0; i += blockDim.x) dst[i] = src[i];
+        return;
+    }
+    // symbols: per-thread contiguous slices, block exclusive scan of their bit counts
+    const uint32_t *syms = syms_all + (uint64_t)j * (n + 1);
+    const uint64_t s0 = b * BLOCK_SYMS, s1 = min((uint64_t)m.nsyms, (uint64_t)(s0 + BLOCK_SYMS));
+    const uint64_t cnt = s1 - s0;
+    const uint64_t per = (cnt + blockDim.x - 1) / blockDim.x;
+    const uint64_t t0 = s0 + threadIdx.x * per, t1 = min(s1, t0 + per);
+    uint64_t mybits = 0;
+    for (uint64_t i = t0; i < t1; ++i) mybits += symbol_bits(syms[i], bt);
+    __shared__ uint64_t scan[256];
+    scan[threadIdx.x] = mybits;
+    __syncthreads();
+    for (unsigned o = 1; o < blockDim.x; o <<= 1) {
+        const uint64_t v = threadIdx.x >= o ? scan[threadIdx.x - o] : 0;
+        __syncthreads();
+        scan[threadIdx.x] += v;
+        __syncthreads();
+    }
+    uint64_t pos = hdr_end + scan[threadIdx.x] - mybits;
+    for (uint64_t i = t0; i < t1; ++i) {
+        uint32_t nb;
+        const uint64_t v = symbol_code(syms[i], bt, nb);
+        put_bits(w, pos, v, nb);
+        pos += nb;
+    }
+    if (threadIdx.x == blockDim.x - 1) {
+        const uint64_t e = hdr_end + scan[blockDim.x - 1];
+        if (bt.type == 1) put_bits(w, e, static_lcode(END_BLOCK), 7);
+        else put_bits(w, e, bt.lcode[END_BLOCK], bt.llen[END_BLOCK]);
+    }
+}
+
+// -------------------------------------------------------------- 11. CRC-32
+__global__ void k_crc_table(uint32_t *tab) {
+    const int i = threadIdx.x;
+    uint32_t c = (uint32_t)i;
+    for (int k = 0; k < 8; ++k) c = c & 1 ? (c >> 1) ^ 0xedb88320u : c >> 1;
+    tab[i] = c;
+    __syncthreads();
+    for (int t = 1; t < 8; ++t) {
+        const uint32_t prev = tab[(t - 1) * 256 + i];
+        tab[t * 256 + i] = (prev >> 8) ^ tab[prev & 0xff];
+        __syncthreads();
+    }
+}
+
+__device__ uint32_t crc_bytes(const uint8_t *p, uint64_t len, const uint32_t *T) {
+    uint32_t c = 0xffffffffu;
+    uint64_t i = 0;
+    while (i < len && (((uintptr_t)(p + i)) & 7)) c = T[(c ^ p[i++]) & 0xff] ^ (c >> 8);
+    for (; i + 8 <= len; i += 8) {
+        const uint64_t v = *reinterpret_cast<const uint64_t *>(p + i);
+        const uint32_t lo = (uint32_t)v ^ c, hi = (uint32_t)(v >> 32);
+        c = T[7 * 256 + (lo & 0xff)] ^ T[6 * 256 + ((lo >> 8) & 0xff)] ^ T[5 * 256 + ((lo >> 16) & 0xff)] ^
+            T[4 * 256 + (lo >> 24)] ^ T[3 * 256 + (hi & 0xff)] ^ T[2 * 256 + ((hi >> 8) & 0xff)] ^
+            T[1 * 256 + ((hi >> 16) & 0xff)] ^ T[hi >> 24];
+    }
+    while (i < len) c = T[(c ^ p[i++]) & 0xff] ^ (c >> 8);
+    return c ^ 0xffffffffu;
+}
+
+__global__ void __launch_bounds__(128) k_crc_chunks(const uint8_t *const *ptrs, const uint64_t *lens,
+                                                   const uint32_t *tab_g, uint64_t ncrc, uint32_t *part) {
+    __shared__ uint32_t T[8 * 256];
+    for (int i = threadIdx.x; i < 8 * 256; i += blockDim.x) T[i] = tab_g[i];
+    __syncthreads();
+    const int j = blockIdx.y;
+    const uint64_t len = lens[j];
+    const uint8_t *p = ptrs[j];
+    const uint64_t c = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+    if (c >= ncrc) return;
+    const uint64_t a = c * CRC_CHUNK;
+    if (a >= len && !(a == 0)) return;
+    const uint64_t e = min(len, a + CRC_CHUNK);
+    part[(uint64_t)j * ncrc + c] = a < len ? crc_bytes(p + a, e - a, T) : 0u;
+}
+
+__global__ void __launch_bounds__(1024) k_crc_combine(const uint64_t *lens, uint64_t ncrc, uint32_t *part,
+                                                     uint32_t *out) {
+    const int j = blockIdx.x;
+    const uint64_t len = lens[j];
+    const uint64_t nc = len ? (len + CRC_CHUNK - 1) / CRC_CHUNK : 0;
+    uint32_t *pp = part + (uint64_t)j * ncrc;
+    // pairwise tree: chunk i covers [i*CH, min(len,(i+1)*CH)); combine right into left
+    for (uint64_t stride = 1; stride < nc; stride <<= 1) {
+        const uint64_t pairs = (nc + 2 * stride - 1) / (2 * stride);
+        for (uint64_t q = threadIdx.x; q < pairs; q += blockDim.x) {
+            const uint64_t l = q * 2 * stride, r = l + stride;
+            if (r < nc) {
+                const uint64_t rend = min(len, (r + stride) * (uint64_t)CRC_CHUNK);
+                pp[l] = crc_combine(pp[l], pp[r], rend - r * (uint64_t)CRC_CHUNK);
+            }
+        }
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) out[j] = nc ? pp[0] : 0u;
+}
+
+// ------------------------------------------------------------- 12. finalize
+__global__ void k_results(const uint8_t *in, uint64_t in_stride, uint64_t n, const StreamMeta *meta, int S,
+                          uint8_t *out, uint64_t out_stride, BackendResults res) {
+    const int j = blockIdx.x * blockDim.x + threadIdx.x;
+    if (j >= S) return;
+    const StreamMeta &m = meta[j];
+    const int src = m.active ? j : m.rep;  // inactive = duplicate all-zero plane
+    const StreamMeta &ms = meta[src];
+    const bool defl = n > 0 && ms.comp_len < n;
+    res.backend[j] = defl ? 1 : 0;
+    res.length[j] = defl ? ms.comp_len : n;
+    res.payload[j] = defl ? out + (uint64_t)src * out_stride : in + (uint64_t)j * in_stride;
+}
+
+__global__ void k_copy_crc(const StreamMeta *meta, int S, BackendResults res) {
+    const int j = blockIdx.x * blockDim.x + threadIdx.x;
+    if (j >= S) return;
+    if (!meta[j].active && meta[j].rep >= 0 && res.backend[j] == 1) res.crc[j] = res.crc[meta[j].rep];
+}
+
+}  // namespace
+
+size_t DeflateBatch::workspace_bytes(int S, uint64_t n) { return carve_size(S, n); }
+
+size_t crc32_batch_workspace(int S, uint64_t max_len) {
+    const uint64_t ncrc = (max_len + 64 + CRC_CHUNK - 1) / CRC_CHUNK + 1;
+    return (size_t)S * ncrc * 4 + 8 * 256 * 4 + 1024;
+}
+
+void crc32_batch(const uint8_t *const *ptrs, const uint64_t *lens, int S, uint64_t max_len, uint32_t *out,
+                 void *workspace, size_t, cudaStream_t st) {
+    const uint64_t ncrc = (max_len + 64 + CRC_CHUNK - 1) / CRC_CHUNK + 1;
+    uint32_t *tab = reinterpret_cast<uint32_t *>(workspace);
+    uint32_t *part = tab + 8 * 256;
+    k_crc_table<<<1, 256, 0, st>>>(tab);
+    CKL();
+    k_crc_chunks<<<dim3((unsigned)((ncrc + 127) / 128), S), 128, 0, st>>>(ptrs, lens, tab, ncrc, part);
+    CKL();
+    k_crc_combine<<<S, 1024, 0, st>>>(lens, ncrc, part, out);
+    CKL();
+}
+
+void DeflateBatch::run(const uint8_t *in, uint64_t in_stride, int S, uint64_t n, uint8_t *out, uint64_t out_stride,
+                       void *workspace, BackendResults res, cudaStream_t st) {
+    Work w = carve(workspace, S, n);
+    CK(cudaMemsetAsync(w.meta, 0, sizeof(StreamMeta) * S, st));
+    if (n > 0) {
+        k_scan<<<dim3(grid_for(n, 256, 256), S), 256, 0, st>>>(in, in_stride, n, w.meta);
+        CKL();
+    }
+    k_select<<<1, 32, 0, st>>>(w.meta, S, n);
+    CKL();
+    if (n > 0) {
+        const uint64_t nblk = (n + WSIZE - 1) / WSIZE;
+        const size_t smem = (size_t)PL_WARPS * 32768 * sizeof(uint16_t);
+        static bool attr = false;
+        if (!attr) {
+            CK(cudaFuncSetAttribute(k_prevlinks, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+            attr = true;
+        }
+        k_prevlinks<<<dim3((unsigned)((nblk + PL_WARPS - 1) / PL_WARPS), S), PL_WARPS * 32, smem, st>>>(in, in_stride, n, w.meta, w.prevd);
+        CKL();
+        k_match<<<dim3(grid_for(n, 256, 4096), S), 256, 0, st>>>(in, in_stride, n, w.meta, w.prevd, w.rec);
+        CKL();
+        k_anchor<<<dim3((unsigned)w.nchunks, S), 256, 0, st>>>(n, w.meta, w.rec, w.nchunks, w.first_anchor);
+        CKL();
+        k_bounds<<<S, 32, 0, st>>>(n, w.meta, w.nchunks, w.first_anchor, w.bnd);
+        CKL();
+        k_sim<<<dim3((unsigned)((w.nchunks * 4 + 127) / 128), S), 128, 0, st>>>(in, in_stride, n, w.meta, w.rec, w.nchunks, w.bnd, w.exit4, w.cnt4);
+        CKL();
+        k_resolve<<<S, 32, 0, st>>>(in, in_stride, n, w.meta, w.nchunks, w.exit4, w.cnt4, w.entry, w.symoff, w.syms,
+                                    w.maxb, w.blk_start);
+        CKL();
+        k_emit_syms<<<dim3((unsigned)((w.nchunks + 127) / 128), S), 128, 0, st>>>(in, in_stride, n, w.meta, w.rec, w.nchunks, w.bnd, w.entry, w.symoff, w.syms, w.maxb, w.blk_top, w.blk_start);
+        CKL();
+        k_plan<<<dim3((unsigned)w.maxb, S), 256, 0, st>>>(n, w.meta, w.syms, w.maxb, w.blk_top, w.blk_start, w.trees);
+        CKL();
+        k_layout<<<(S + 31) / 32, 32, 0, st>>>(n, w.meta, S, w.maxb, w.trees, w.blk_bitpos);
+        CKL();
+        k_zero_out<<<dim3(grid_for(n / 8 + 2, 256, 512), S), 256, 0, st>>>(n, w.meta, out, out_stride);
+        CKL();
+        k_emit<<<dim3((unsigned)w.maxb, S), 256, 0, st>>>(in, in_stride, n, w.meta, w.syms, w.maxb, w.blk_start, w.trees, w.blk_bitpos, out, out_stride);
+        CKL();
+    }
+    k_results<<<(S + 31) / 32, 32, 0, st>>>(in, in_stride, n, w.meta, S, out, out_stride, res);
+    CKL();
+    // CRC over each payload (duplicate all-zero deflate planes reuse their representative's)
+    k_crc_table<<<1, 256, 0, st>>>(w.crc_tab);
+    CKL();
+    k_crc_chunks<<<dim3((unsigned)((w.ncrc + 127) / 128), S), 128, 0, st>>>(res.payload, res.length, w.crc_tab, w.ncrc, w.crc_part);
+    CKL();
+    k_crc_combine<<<S, 1024, 0, st>>>(res.length, w.ncrc, w.crc_part, res.crc);
+    CKL();
+    k_copy_crc<<<(S + 31) / 32, 32, 0, st>>>(w.meta, S, res);
+    CKL();
+}
+
+}  // namespace ipcg

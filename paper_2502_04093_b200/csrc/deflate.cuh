@@ -1,0 +1,32 @@
+// deflate.cuh -- batched, zlib-1.3-exact `compress2(level 6)` on the GPU for the
+// reference's lossless stage (backend_encode, proj/src/backend.cpp:34-53).
+#pragma once
+#include <stdint.h>
+
+#include "util.cuh"
+
+namespace ipcg {
+
+// results of backend_encode for S streams (device arrays of S entries)
+struct BackendResults {
+    uint8_t *backend;          // 0 identity, 1 deflate
+    uint64_t *length;          // payload bytes
+    uint32_t *crc;             // crc32(payload)
+    const uint8_t **payload;   // device address of the payload bytes
+};
+
+// S equal-length streams in[j*in_stride .. +n); outputs land in out[j*out_stride ..],
+// out_stride >= n + 16.  Workspace from DeflateBatch::workspace_bytes.
+struct DeflateBatch {
+    static constexpr int CH = 2048;  // nominal parse chunk
+    static size_t workspace_bytes(int S, uint64_t n);
+    static void run(const uint8_t *in, uint64_t in_stride, int S, uint64_t n, uint8_t *out, uint64_t out_stride,
+                    void *workspace, BackendResults res, cudaStream_t st);
+};
+
+// standalone CRC-32 (zlib polynomial) of S (ptr, len) device ranges
+void crc32_batch(const uint8_t *const *ptrs, const uint64_t *lens, int S, uint64_t max_len, uint32_t *out,
+                 void *workspace, size_t workspace_bytes, cudaStream_t st);
+size_t crc32_batch_workspace(int S, uint64_t max_len);
+
+}  // namespace ipcg

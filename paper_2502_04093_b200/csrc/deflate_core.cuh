@@ -526,7 +526,7 @@ HD uint32_t crc_multmodp(uint32_t a, uint32_t b) {  // crc32.c multmodp
 // x^(8*len) mod P, by square-and-multiply on x^(2^k)
 HD uint32_t crc_x8n(uint64_t len) {
     uint32_t p = 1u << 31;     // x^0
-    uint32_t sq = 1u << 27;    // x^8 (x^1 is 1<<30)
+    uint32_t sq = 1u << 23;    // x^8 (reflected: x^k is 1 << (31-k))
     while (len) {
         if (len & 1) p = crc_multmodp(sq, p);
         sq = crc_multmodp(sq, sq);

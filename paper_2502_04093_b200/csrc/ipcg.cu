@@ -1,0 +1,848 @@
+// ipcg.cu -- orchestration of the B200 hot path behind the C-ABI (include/ipcomp_b200.h).
+//
+//   compress_field   (pipeline.hpp:140-223): range scan -> per level L..1: one
+//                    predict+quantize launch per (level, axis) pass -> loss-table replay
+//                    -> ballot bitplanes + XOR -> DeflateBatch (32 planes) -> one sync ->
+//                    host index (archive.cpp:31-65) -> device payload gather.
+//   reconstruct_field (pipeline.hpp:227-287) / refine_field (:294-352): host plans the
+//                    block reads (partial-bitplane fetch, byte accounting), device gathers
+//                    the blocks, CRC-32 + inflate, XOR-decode+merge, per-pass reconstruction
+//                    with in-traversal outlier overwrite.
+// All device work of a call is ordered on the context's stream; temporaries come from
+// the stream-ordered allocator (cudaMallocAsync), whose pool keeps memory across calls.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/ipcomp_b200.h"
+#include "deflate.cuh"
+#include "grid.h"
+#include "host.h"
+#include "inflate.cuh"
+#include "numerics.cuh"
+
+using namespace ipcg;
+
+struct ipcg_ctx {
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    std::string err;
+    void *pinned = nullptr;
+    size_t pinned_cap = 0;
+};
+
+struct ipcg_archive {
+    ipcg_index ix{};
+    const uint8_t *bytes = nullptr;
+    uint64_t size = 0;
+    bool on_device = false;
+    uint8_t *owned = nullptr;  // device buffer when produced by ipcg_compress
+    uint64_t payload_read = 0;
+    int device = 0;
+};
+
+struct ipcg_session {
+    uint32_t archive_crc = 0;
+    int levels = 0, lp = 0;
+    int k[IPCG_MAX_LEVELS] = {0};
+    uint64_t count[IPCG_MAX_LEVELS] = {0};
+    uint32_t *merged[IPCG_MAX_LEVELS] = {nullptr};  // device, progressive levels only
+};
+
+namespace {
+
+// ------------------------------------------------------------------ helpers
+struct DBuf {  // stream-ordered device allocation
+    void *p = nullptr;
+    cudaStream_t st = nullptr;
+    DBuf() = default;
+    DBuf(size_t bytes, cudaStream_t s) : st(s) {
+        if (bytes) CK(cudaMallocAsync(&p, bytes, s));
+    }
+    DBuf(const DBuf &) = delete;
+    DBuf &operator=(const DBuf &) = delete;
+    DBuf(DBuf &&o) noexcept : p(o.p), st(o.st) { o.p = nullptr; }
+    DBuf &operator=(DBuf &&o) noexcept {
+        release();
+        p = o.p;
+        st = o.st;
+        o.p = nullptr;
+        return *this;
+    }
+    ~DBuf() { release(); }
+    void release() {
+        if (p) cudaFreeAsync(p, st);
+        p = nullptr;
+    }
+    template <class T>
+    T *as() const {
+        return static_cast<T *>(p);
+    }
+};
+
+void *pinned(ipcg_ctx *c, size_t bytes) {
+    if (bytes > c->pinned_cap) {
+        if (c->pinned) CK(cudaFreeHost(c->pinned));
+        size_t cap = std::max<size_t>(bytes, 1 << 20);
+        CK(cudaMallocHost(&c->pinned, cap));
+        c->pinned_cap = cap;
+    }
+    return c->pinned;
+}
+
+thread_local std::string g_host_err;  // errors of context-free (host-only) calls
+
+template <class F>
+int guarded(ipcg_ctx *c, F &&f) {
+    std::string &err = c ? c->err : g_host_err;
+    try {
+        if (c) CK(cudaSetDevice(c->device));
+        f();
+        return IPCG_OK;
+    } catch (const Error &e) {
+        err = e.what();
+        return e.kind;
+    } catch (const std::bad_alloc &) {
+        err = "out of host memory";
+        return IPCG_ERUNTIME;
+    } catch (const std::exception &e) {
+        err = e.what();
+        return IPCG_ERUNTIME;
+    }
+}
+
+void validate_dims(const uint64_t *dims, int nd) {  // common.hpp:35-42
+    if (nd < 1 || nd > 4) throw Error(EINVAL_, "grid must have between 1 and 4 dimensions");
+    for (int i = 0; i < nd; ++i)
+        if (dims[i] < 1) throw Error(EINVAL_, "grid extents must be positive");
+}
+
+uint64_t round_up(uint64_t v, uint64_t a) { return (v + a - 1) / a * a; }
+
+// ------------------------------------------------------------- byte gather
+struct CopyDesc {
+    const uint8_t *src;
+    uint64_t dst_off;
+    uint64_t len;
+};
+
+__global__ void k_gather(const CopyDesc *d, int nd, uint8_t *dst) {
+    const int i = blockIdx.x;
+    if (i >= nd) return;
+    const CopyDesc c = d[i];
+    uint8_t *o = dst + c.dst_off;
+    const uint8_t *s = c.src;
+    // 16-byte vector path when both ends align, else bytes (coalesced per warp)
+    if ((((uintptr_t)o | (uintptr_t)s) & 15) == 0) {
+        const uint64_t v = c.len / 16;
+        const uint4 *s4 = reinterpret_cast<const uint4 *>(s);
+        uint4 *o4 = reinterpret_cast<uint4 *>(o);
+        for (uint64_t k = threadIdx.x; k < v; k += blockDim.x) o4[k] = s4[k];
+        for (uint64_t k = v * 16 + threadIdx.x; k < c.len; k += blockDim.x) o[k] = s[k];
+    } else {
+        for (uint64_t k = threadIdx.x; k < c.len; k += blockDim.x) o[k] = s[k];
+    }
+}
+
+// dst == nullptr: dst_off are absolute device addresses
+void gather(ipcg_ctx *c, std::vector<CopyDesc> descs, uint8_t *dst) {
+    // split long copies so every SM participates
+    std::vector<CopyDesc> pieces;
+    pieces.reserve(descs.size());
+    const uint64_t piece = 1 << 20;
+    for (const CopyDesc &d : descs)
+        for (uint64_t o = 0; o < d.len; o += piece)
+            pieces.push_back(CopyDesc{d.src + o, d.dst_off + o, std::min(piece, d.len - o)});
+    if (pieces.empty()) return;
+    DBuf dd(pieces.size() * sizeof(CopyDesc), c->stream);
+    CopyDesc *h = static_cast<CopyDesc *>(pinned(c, pieces.size() * sizeof(CopyDesc)));
+    std::memcpy(h, pieces.data(), pieces.size() * sizeof(CopyDesc));
+    CK(cudaMemcpyAsync(dd.p, h, pieces.size() * sizeof(CopyDesc), cudaMemcpyHostToDevice, c->stream));
+    k_gather<<<(unsigned)pieces.size(), 256, 0, c->stream>>>(dd.as<CopyDesc>(), (int)pieces.size(), dst);
+    CKL();
+    CK(cudaStreamSynchronize(c->stream));  // the pinned staging is reused by the next call
+}
+
+// ---------------------------------------------------------------- compress
+ipcg_archive *compress_impl(ipcg_ctx *c, int scalar, const void *values, int on_dev, const uint64_t *dims, int nd,
+                            double eb, int interp, int lp_opt, uint64_t cap) {
+    validate_dims(dims, nd);
+    if (scalar != 0 && scalar != 1) throw Error(EINVAL_, "field scalars must be f32 or f64");
+    if (!(eb > 0.0) || !std::isfinite(eb)) throw Error(EINVAL_, "error bound must be positive and finite");
+    const Geometry G = make_geometry(dims, nd, max_levels_for_cap(cap));
+    const int L = G.levels;
+    const int lp = lp_opt == 0 ? L : lp_opt;
+    if (lp < 1 || lp > L) throw Error(EINVAL_, "first progressive level out of range");
+    if (L > IPCG_MAX_LEVELS) throw Error(EINVAL_, "too many levels for this build");
+    const bool cubic = interp == 1;
+    const int w = scalar == 0 ? 4 : 8;
+    const uint64_t n = G.n;
+    cudaStream_t st = c->stream;
+
+    DBuf vals_buf;
+    const void *vals = values;
+    if (!on_dev) {
+        vals_buf = DBuf(n * w, st);
+        CK(cudaMemcpyAsync(vals_buf.p, values, n * w, cudaMemcpyHostToDevice, st));
+        vals = vals_buf.p;
+    }
+    DBuf state(n * w, st), dev(n * 8, st);
+    CK(cudaMemsetAsync(state.p, 0, n * w, st));
+    CK(cudaMemsetAsync(dev.p, 0, n * 8, st));
+    // small per-call device state
+    struct Small {
+        double rng[2];
+        uint32_t lowor[IPCG_MAX_LEVELS];
+        unsigned long long raw[IPCG_MAX_LEVELS][33];
+        double delta[IPCG_MAX_LEVELS][33];
+        unsigned long long ocount[IPCG_MAX_LEVELS];
+        uint8_t backend[IPCG_MAX_LEVELS][32];
+        uint64_t length[IPCG_MAX_LEVELS][32];
+        uint32_t crc[IPCG_MAX_LEVELS][32];
+        const uint8_t *payload[IPCG_MAX_LEVELS][32];
+        double range_part[2 * 1024];
+    };
+    DBuf small(sizeof(Small), st);
+    Small *sd = small.as<Small>();
+    CK(cudaMemsetAsync(small.p, 0, sizeof(Small), st));
+    DBuf ord(n * 8, st), bits(n * 8, st);
+    launch_range(vals, scalar, n, sd->range_part, sd->rng, st);
+
+    uint64_t maxcount = 0;
+    size_t ws_bytes = 0;
+    for (int l = 1; l <= L; ++l) {
+        maxcount = std::max(maxcount, G.level[l - 1].count);
+        ws_bytes = std::max(ws_bytes, DeflateBatch::workspace_bytes(32, (G.level[l - 1].count + 7) / 8));
+    }
+    DBuf nb(std::max<uint64_t>(maxcount, 1) * 4, st), ws(ws_bytes, st);
+    std::vector<DBuf> planes(L), outs(L);
+    std::vector<uint64_t> pb(L), plane_stride(L), out_stride(L), sink_base(L);
+    uint64_t base = 0;
+    for (int level = L; level >= 1; --level) {
+        const LevelGeom &lg = G.level[level - 1];
+        const int li = level - 1;
+        sink_base[li] = base;
+        base += lg.count;
+        pb[li] = (lg.count + 7) / 8;
+        const uint64_t words = (lg.count + 31) / 32;
+        plane_stride[li] = round_up(std::max<uint64_t>(words, 1), 4);  // words, 16-byte rows
+        out_stride[li] = round_up(pb[li] + 16, 16);
+        planes[li] = DBuf(32 * plane_stride[li] * 4, st);
+        outs[li] = DBuf(32 * out_stride[li], st);
+        const OutlierSink sink{&sd->ocount[li], ord.as<uint64_t>() + sink_base[li], bits.as<uint64_t>() + sink_base[li]};
+        for (const PassDesc &pd : lg.passes)
+            launch_quant_pass(vals, state.p, scalar, cubic, pd, eb, nb.as<uint32_t>(), &sd->lowor[li], sink, st);
+        // loss table (measure_loss_table): replay per dropped-digit count d
+        for (int d = 1; d <= 32; ++d)
+            for (const PassDesc &pd : lg.passes)
+                launch_loss_pass(nb.as<uint32_t>(), dev.as<double>(), pd, cubic, 2.0 * eb, d, &sd->lowor[li],
+                                 sd->raw[li], st);
+        for (const PassDesc &pd : lg.passes) launch_zero_pass(dev.as<double>(), pd, st);
+        launch_loss_finalize(sd->raw[li], &sd->lowor[li], sd->delta[li], st);
+        if (planes[li].p) CK(cudaMemsetAsync(planes[li].p, 0, 32 * plane_stride[li] * 4, st));
+        launch_bitplanes(nb.as<uint32_t>(), lg.count, planes[li].as<uint32_t>(), plane_stride[li], st);
+        const BackendResults res{sd->backend[li], sd->length[li], sd->crc[li], sd->payload[li]};
+        DeflateBatch::run(planes[li].as<uint8_t>(), plane_stride[li] * 4, 32, pb[li], outs[li].as<uint8_t>(),
+                          out_stride[li], ws.p, res, st);
+    }
+    Small *sh = static_cast<Small *>(pinned(c, sizeof(Small)));
+    CK(cudaMemcpyAsync(sh, small.p, sizeof(Small), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    Small hs;
+    std::memcpy(&hs, sh, sizeof(Small));
+
+    // index (pipeline.hpp:158-217 + archive.cpp:31-65)
+    ipcg_index ix{};
+    ix.version = 1;
+    ix.scalar = (uint8_t)scalar;
+    ix.interp = (uint8_t)interp;
+    ix.ndims = (uint8_t)nd;
+    for (int i = 0; i < nd; ++i) ix.dims[i] = dims[i];
+    ix.eb = eb;
+    ix.range = hs.rng[1] - hs.rng[0];
+    ix.levels = (uint8_t)L;
+    ix.progressive_levels = (uint8_t)lp;
+    ix.anchor_cap = (uint8_t)cap;
+    uint64_t cursor = 0;
+    for (int level = L; level >= 1; --level) {
+        const int li = level - 1;
+        ipcg_level_record &r = ix.records[li];
+        r.count = G.level[li].count;
+        for (int d = 0; d < 33; ++d) r.delta[d] = hs.delta[li][d];
+        r.outlier_offset = cursor;
+        r.outlier_count = hs.ocount[li];
+        r.outlier_length = hs.ocount[li] * (uint64_t)(8 + w);
+        cursor += r.outlier_length;
+        for (int p = 0; p < 32; ++p) {
+            r.plane_offset[p] = cursor;
+            r.plane_length[p] = 21 + hs.length[li][p];
+            cursor += r.plane_length[p];
+        }
+    }
+    ix.payload_bytes = cursor;
+    const std::vector<uint8_t> index = serialize_index(ix);
+    ix.index_bytes = index.size();
+    ix.identity = crc32_host(index.data(), index.size());
+    const uint64_t total = index.size() + cursor;
+
+    ipcg_archive *a = new ipcg_archive;
+    a->device = c->device;
+    CK(cudaMalloc(&a->owned, std::max<uint64_t>(total, 1)));
+    a->bytes = a->owned;
+    a->size = total;
+    a->on_device = true;
+    a->ix = ix;
+    // index + block headers staged in one pinned blob, payloads copied device-to-device
+    std::vector<uint8_t> blob(index.begin(), index.end());
+    std::vector<CopyDesc> descs;
+    std::vector<std::pair<uint64_t, uint64_t>> blob_spans;  // (blob offset, archive offset, len) for headers
+    blob_spans.push_back({0, 0});
+    const uint64_t payload0 = index.size();
+    for (int level = L; level >= 1; --level) {
+        const int li = level - 1;
+        const ipcg_level_record &r = ix.records[li];
+        for (int p = 0; p < 32; ++p) {
+            const uint64_t hb = blob.size();
+            const uint64_t len = hs.length[li][p];
+            uint8_t h[21];
+            h[0] = hs.backend[li][p];
+            for (int i = 0; i < 8; ++i) h[1 + i] = (uint8_t)(r.count >> (8 * i));
+            for (int i = 0; i < 8; ++i) h[9 + i] = (uint8_t)(len >> (8 * i));
+            for (int i = 0; i < 4; ++i) h[17 + i] = (uint8_t)(hs.crc[li][p] >> (8 * i));
+            blob.insert(blob.end(), h, h + 21);
+            descs.push_back(CopyDesc{nullptr, payload0 + r.plane_offset[p], 21});
+            blob_spans.push_back({hb, 21});
+            descs.push_back(CopyDesc{hs.payload[li][p], payload0 + r.plane_offset[p] + 21, len});
+        }
+    }
+    DBuf blob_d(blob.size(), st);
+    uint8_t *bh = static_cast<uint8_t *>(pinned(c, blob.size()));
+    std::memcpy(bh, blob.data(), blob.size());
+    CK(cudaMemcpyAsync(blob_d.p, bh, blob.size(), cudaMemcpyHostToDevice, st));
+    // index copy
+    std::vector<CopyDesc> all;
+    all.push_back(CopyDesc{blob_d.as<uint8_t>(), 0, index.size()});
+    size_t hi = 1;
+    for (CopyDesc &d : descs) {
+        if (!d.src) {
+            d.src = blob_d.as<uint8_t>() + blob_spans[hi].first;
+            ++hi;
+        }
+        all.push_back(d);
+    }
+    CK(cudaStreamSynchronize(st));  // pinned blob consumed before reuse
+    gather(c, all, a->owned);
+    // outlier blocks, sorted by ordinal (pipeline.hpp:185-188)
+    uint64_t maxo = 0;
+    for (int l = 0; l < L; ++l) maxo = std::max<uint64_t>(maxo, hs.ocount[l]);
+    if (maxo) {
+        const size_t tb = sort_outliers_temp_bytes(maxo);
+        DBuf temp(tb, st), os(maxo * 8, st), bs(maxo * 8, st);
+        for (int level = L; level >= 1; --level) {
+            const int li = level - 1;
+            if (!hs.ocount[li]) continue;
+            const OutlierSink sink{&sd->ocount[li], ord.as<uint64_t>() + sink_base[li], bits.as<uint64_t>() + sink_base[li]};
+            launch_sort_outliers(sink, hs.ocount[li], os.as<uint64_t>(), bs.as<uint64_t>(), temp.p, tb, st);
+            launch_outlier_block(os.as<uint64_t>(), bs.as<uint64_t>(), &sd->ocount[li], scalar,
+                                 a->owned + payload0 + ix.records[li].outlier_offset, st);
+        }
+    }
+    CK(cudaStreamSynchronize(st));
+    return a;
+}
+
+// ---------------------------------------------------------------- retrieval
+struct PlaneRef {
+    int level, plane;
+    uint64_t block_off;  // offset of the block (header) in the staged/device source
+    uint8_t backend;
+    uint64_t plen;
+    uint32_t crc;
+};
+
+__global__ void k_copy_headers(const uint8_t *src, const uint64_t *offs, int n, uint8_t *dst) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    for (int k = 0; k < 21; ++k) dst[i * 21 + k] = src[offs[i] + k];
+}
+
+void retrieve_impl(ipcg_ctx *c, ipcg_archive *a, int scalar, const int *k, void *out, int out_on_dev,
+                   const ipcg_session *prev_sess, const void *previous, int prev_on_dev, ipcg_session **sess_out,
+                   uint64_t *loaded) {
+    const ipcg_index &ix = a->ix;
+    if (ix.scalar != scalar) throw Error(EINVAL_, "scalar kind does not match archive");
+    validate_plan(ix, k);
+    const bool refine = prev_sess != nullptr;
+    if (refine) {
+        if (prev_sess->archive_crc != ix.identity) throw Error(ERUNTIME, "session does not belong to this archive");
+        if (prev_sess->levels != ix.levels) throw Error(ERUNTIME, "session level count does not match archive");
+    }
+    const Geometry G = make_geometry(ix.dims, ix.ndims, max_levels_for_cap(ix.anchor_cap));
+    if (!refine && G.levels != ix.levels) throw Error(ERUNTIME, "archive level count does not match its dimensions");
+    const int L = ix.levels;
+    const int w = scalar == 0 ? 4 : 8;
+    const uint64_t n = G.n;
+    if (refine) {
+        for (int level = 1; level <= L; ++level)
+            if (k[level - 1] < prev_sess->k[level - 1])
+                throw Error(EINVAL_, "refinement plan must not drop planes the session already loaded");
+    }
+    cudaStream_t st = c->stream;
+    // ---- plan the block reads (read_range accounting, archive.cpp:172-200)
+    struct LevelPlan {
+        int p0, p1;
+        bool active;
+        uint64_t ob_off;  // outlier block source offset (staged or archive payload)
+    };
+    std::vector<LevelPlan> lv(L);
+    std::vector<PlaneRef> refs;
+    uint64_t read = 0;
+    auto range_ok = [&](uint64_t off, uint64_t len) {
+        if (off + len > ix.payload_bytes) throw Error(ERUNTIME, "block offset outside payload");
+        if (ix.index_bytes + off + len > a->size) throw Error(ERUNTIME, "truncated archive payload");
+    };
+    std::vector<std::pair<uint64_t, uint64_t>> spans;  // payload-relative (off, len) in read order
+    for (int level = L; level >= 1; --level) {
+        const int li = level - 1;
+        const ipcg_level_record &r = ix.records[li];
+        LevelPlan &p = lv[li];
+        p.active = !refine || level <= ix.progressive_levels;
+        p.p0 = refine ? prev_sess->k[li] : 0;
+        p.p1 = k[li];
+        if (!p.active) continue;
+        if (refine) {
+            if (prev_sess->count[li] != r.count) throw Error(ERUNTIME, "session codeword array has wrong length");
+        } else if (r.count != G.level[li].count) {
+            throw Error(ERUNTIME, "level point count does not match its dimensions");
+        }
+        for (int q = p.p0; q < p.p1; ++q) {
+            range_ok(r.plane_offset[q], r.plane_length[q]);
+            spans.push_back({r.plane_offset[q], r.plane_length[q]});
+            refs.push_back(PlaneRef{level, q, 0, 0, 0, 0});
+            read += r.plane_length[q];
+        }
+        const uint64_t e = 8 + (uint64_t)w;
+        if (r.outlier_length != r.outlier_count * e) throw Error(ERUNTIME, "outlier block length does not match its count");
+        range_ok(r.outlier_offset, r.outlier_length);
+        spans.push_back({r.outlier_offset, r.outlier_length});
+        read += r.outlier_length;
+    }
+    // ---- bring the blocks to the device
+    uint64_t staged = 0;
+    for (auto &s : spans) staged += s.second;
+    DBuf stage;
+    const uint8_t *src_dev;  // device base the block offsets below refer to
+    std::vector<uint64_t> src_off(spans.size());
+    std::vector<uint8_t> headers(refs.size() * 21);
+    if (a->on_device) {
+        src_dev = a->bytes + ix.index_bytes;
+        for (size_t i = 0; i < spans.size(); ++i) src_off[i] = spans[i].first;
+        if (!refs.empty()) {
+            // plane spans are every span except each level's trailing outlier block
+            std::vector<uint64_t> hoffs;
+            size_t si = 0;
+            for (int level = L; level >= 1; --level) {
+                const LevelPlan &p = lv[level - 1];
+                if (!p.active) continue;
+                for (int q = p.p0; q < p.p1; ++q) hoffs.push_back(src_off[si++]);
+                ++si;  // outlier
+            }
+            DBuf ho(hoffs.size() * 8, st), hd(hoffs.size() * 21, st);
+            uint64_t *hp = static_cast<uint64_t *>(pinned(c, hoffs.size() * 8));
+            std::memcpy(hp, hoffs.data(), hoffs.size() * 8);
+            CK(cudaMemcpyAsync(ho.p, hp, hoffs.size() * 8, cudaMemcpyHostToDevice, st));
+            k_copy_headers<<<(unsigned)((hoffs.size() + 127) / 128), 128, 0, st>>>(src_dev, ho.as<uint64_t>(),
+                                                                                (int)hoffs.size(), hd.as<uint8_t>());
+            CKL();
+            CK(cudaMemcpyAsync(headers.data(), hd.p, headers.size(), cudaMemcpyDeviceToHost, st));
+            CK(cudaStreamSynchronize(st));
+        }
+    } else {
+        stage = DBuf(std::max<uint64_t>(staged, 1), st);
+        uint8_t *hp = static_cast<uint8_t *>(pinned(c, std::max<uint64_t>(staged, 1)));
+        uint64_t o = 0;
+        for (size_t i = 0; i < spans.size(); ++i) {
+            std::memcpy(hp + o, a->bytes + ix.index_bytes + spans[i].first, spans[i].second);
+            src_off[i] = o;
+            o += spans[i].second;
+        }
+        size_t si = 0, ri = 0;
+        for (int level = L; level >= 1; --level) {
+            const LevelPlan &p = lv[level - 1];
+            if (!p.active) continue;
+            for (int q = p.p0; q < p.p1; ++q, ++ri) std::memcpy(&headers[ri * 21], hp + src_off[si++], 21);
+            ++si;
+        }
+        CK(cudaMemcpyAsync(stage.p, hp, staged, cudaMemcpyHostToDevice, st));
+        CK(cudaStreamSynchronize(st));  // the pinned staging buffer is reused below
+        src_dev = stage.as<uint8_t>();
+    }
+    a->payload_read += read;
+    // ---- block headers (read_block + load_plane checks, backend.cpp:75-86, archive.cpp:183-191)
+    {
+        size_t si = 0, ri = 0;
+        for (int level = L; level >= 1; --level) {
+            LevelPlan &p = lv[level - 1];
+            if (!p.active) continue;
+            const ipcg_level_record &r = ix.records[level - 1];
+            for (int q = p.p0; q < p.p1; ++q, ++ri, ++si) {
+                const uint64_t blen = r.plane_length[q];
+                const uint8_t *h = &headers[ri * 21];
+                if (blen < 1) throw Error(ERUNTIME, "truncated input while parsing");
+                if (h[0] > 1) throw Error(ERUNTIME, "unknown backend id");
+                if (blen < 21) throw Error(ERUNTIME, "truncated input while parsing");
+                uint64_t raw_bits = 0, plen = 0;
+                uint32_t crc = 0;
+                for (int i = 0; i < 8; ++i) raw_bits |= (uint64_t)h[1 + i] << (8 * i);
+                for (int i = 0; i < 8; ++i) plen |= (uint64_t)h[9 + i] << (8 * i);
+                for (int i = 0; i < 4; ++i) crc |= (uint32_t)h[17 + i] << (8 * i);
+                if (blen - 21 < plen) throw Error(ERUNTIME, "truncated input while parsing");
+                if (blen - 21 != plen) throw Error(ERUNTIME, "plane block has trailing bytes");
+                if (raw_bits != r.count) throw Error(ERUNTIME, "plane bit count does not match level");
+                refs[ri].block_off = src_off[si];
+                refs[ri].backend = h[0];
+                refs[ri].plen = plen;
+                refs[ri].crc = crc;
+            }
+            p.ob_off = src_off[si++];
+        }
+    }
+    // ---- CRC-32 of every payload, then identity copies / inflate into plane rows
+    const size_t R = refs.size();
+    uint64_t maxp = 1;
+    for (const PlaneRef &r : refs) maxp = std::max(maxp, r.plen);
+    std::vector<DBuf> planes(L);
+    std::vector<uint64_t> stride(L, 0);
+    for (int level = 1; level <= L; ++level) {
+        const LevelPlan &p = lv[level - 1];
+        if (!p.active) continue;
+        const uint64_t count = ix.records[level - 1].count;
+        stride[level - 1] = round_up(std::max<uint64_t>((count + 31) / 32, 1), 4);
+        planes[level - 1] = DBuf(32 * stride[level - 1] * 4, st);
+    }
+    if (R) {
+        std::vector<const uint8_t *> ptrs(R);
+        std::vector<uint64_t> lens(R);
+        std::vector<InflateJob> jobs;
+        std::vector<CopyDesc> copies;
+        for (size_t i = 0; i < R; ++i) {
+            const PlaneRef &r = refs[i];
+            ptrs[i] = src_dev + r.block_off + 21;
+            lens[i] = r.plen;
+            const int li = r.level - 1;
+            const uint64_t pbytes = (ix.records[li].count + 7) / 8;
+            uint8_t *row = planes[li].as<uint8_t>() + (uint64_t)r.plane * stride[li] * 4;
+            if (r.backend == 0) {  // identity: the length check follows the CRC check, as in backend_decode
+                copies.push_back(CopyDesc{ptrs[i], (uint64_t)reinterpret_cast<uintptr_t>(row), std::min(r.plen, pbytes)});
+            } else {
+                jobs.push_back(InflateJob{ptrs[i], r.plen, row, pbytes});
+            }
+        }
+        const size_t cw = crc32_batch_workspace((int)R, maxp);
+        DBuf crcws(cw, st), crcs(R * 4, st), pd(R * 8, st), ld(R * 8, st);
+        uint8_t *hp = static_cast<uint8_t *>(pinned(c, R * 16));
+        std::memcpy(hp, ptrs.data(), R * 8);
+        std::memcpy(hp + R * 8, lens.data(), R * 8);
+        CK(cudaMemcpyAsync(pd.p, hp, R * 8, cudaMemcpyHostToDevice, st));
+        CK(cudaMemcpyAsync(ld.p, hp + R * 8, R * 8, cudaMemcpyHostToDevice, st));
+        CK(cudaStreamSynchronize(st));  // pinned ptr/len table consumed
+        crc32_batch(pd.as<const uint8_t *>(), ld.as<uint64_t>(), (int)R, maxp, crcs.as<uint32_t>(), crcws.p, cw, st);
+        std::vector<uint32_t> hcrc(R);
+        CK(cudaMemcpyAsync(hcrc.data(), crcs.p, R * 4, cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
+        for (size_t i = 0; i < R; ++i)
+            if (hcrc[i] != refs[i].crc) throw Error(ERUNTIME, "block checksum mismatch");
+        for (size_t i = 0; i < R; ++i) {
+            const uint64_t pbytes = (ix.records[refs[i].level - 1].count + 7) / 8;
+            if (refs[i].backend == 0 && refs[i].plen != pbytes) throw Error(ERUNTIME, "identity block has wrong length");
+        }
+        if (!copies.empty()) gather(c, copies, nullptr);
+        if (!jobs.empty()) {
+            DBuf jd(jobs.size() * sizeof(InflateJob), st), sd(jobs.size() * 4, st);
+            InflateJob *jh = static_cast<InflateJob *>(pinned(c, jobs.size() * sizeof(InflateJob)));
+            std::memcpy(jh, jobs.data(), jobs.size() * sizeof(InflateJob));
+            CK(cudaMemcpyAsync(jd.p, jh, jobs.size() * sizeof(InflateJob), cudaMemcpyHostToDevice, st));
+            inflate_batch(jd.as<InflateJob>(), (int)jobs.size(), sd.as<int>(), st);
+            std::vector<int> status(jobs.size());
+            CK(cudaMemcpyAsync(status.data(), sd.p, jobs.size() * 4, cudaMemcpyDeviceToHost, st));
+            CK(cudaStreamSynchronize(st));
+            for (int s : status)
+                if (s) throw Error(ERUNTIME, "deflate backend failed to decompress block");
+        }
+    }
+    // ---- merge + reconstruct, coarsest first
+    DBuf out_buf;
+    void *state = out;
+    if (!out_on_dev) {
+        out_buf = DBuf(n * w, st);
+        state = out_buf.p;
+    }
+    if (refine) {
+        CK(cudaMemcpyAsync(state, previous, n * w, prev_on_dev ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, st));
+    }
+    ipcg_session *ns = new ipcg_session;
+    ns->archive_crc = ix.identity;
+    ns->levels = L;
+    ns->lp = ix.progressive_levels;
+    DBuf napplied(8 * IPCG_MAX_LEVELS, st);
+    try {
+        for (int level = L; level >= 1; --level) {
+            const int li = level - 1;
+            const LevelPlan &p = lv[li];
+            ns->k[li] = k[li];
+            ns->count[li] = ix.records[li].count;
+            if (!p.active) {
+                if (refine) ns->k[li] = prev_sess->k[li];
+                continue;
+            }
+            const uint64_t count = ix.records[li].count;
+            uint32_t *merged = nullptr;
+            CK(cudaMallocAsync((void **)&merged, std::max<uint64_t>(count, 1) * 4, st));
+            const uint32_t *min = refine ? prev_sess->merged[li] : nullptr;
+            launch_merge(planes[li].as<uint32_t>(), stride[li], min, merged, count, p.p0, p.p1, st);
+            const uint8_t *ob = src_dev + p.ob_off;
+            const uint64_t no = ix.records[li].outlier_count;
+            if (no) launch_outlier_prefix(ob, no, scalar, count, napplied.as<uint64_t>() + li, st);
+            for (const PassDesc &pd : G.level[li].passes) {
+                launch_recon_pass(state, scalar, ix.interp == 1, pd, ix.eb, merged, st);
+                if (no) launch_outlier_apply(state, scalar, pd, ob, napplied.as<uint64_t>() + li, no, st);
+            }
+            if (level <= ix.progressive_levels) ns->merged[li] = merged;
+            else CK(cudaFreeAsync(merged, st));
+        }
+        if (!out_on_dev) CK(cudaMemcpyAsync(out, state, n * w, cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
+    } catch (...) {
+        for (int l = 0; l < IPCG_MAX_LEVELS; ++l)
+            if (ns->merged[l]) cudaFree(ns->merged[l]);
+        delete ns;
+        throw;
+    }
+    if (loaded) *loaded = read;
+    if (sess_out) *sess_out = ns;
+    else {
+        for (int l = 0; l < IPCG_MAX_LEVELS; ++l)
+            if (ns->merged[l]) cudaFreeAsync(ns->merged[l], st);
+        delete ns;
+    }
+}
+
+}  // namespace
+
+// ================================================================== C-ABI
+extern "C" {
+
+int ipcg_ctx_create(int device, ipcg_ctx **out) {
+    ipcg_ctx *c = new ipcg_ctx;
+    c->device = device;
+    const int rc = guarded(c, [&] {
+        int cnt = 0;
+        CK(cudaGetDeviceCount(&cnt));
+        if (device < 0 || device >= cnt) throw Error(ECUDA, "no such CUDA device");
+        CK(cudaSetDevice(device));
+        cudaMemPool_t pool;
+        CK(cudaDeviceGetDefaultMemPool(&pool, device));
+        uint64_t thr = UINT64_MAX;
+        CK(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr));
+        CK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+    });
+    if (rc != IPCG_OK) {
+        *out = nullptr;
+        delete c;
+        return rc;
+    }
+    *out = c;
+    return IPCG_OK;
+}
+
+void ipcg_ctx_destroy(ipcg_ctx *c) {
+    if (!c) return;
+    cudaSetDevice(c->device);
+    if (c->stream) cudaStreamSynchronize(c->stream);
+    if (c->pinned) cudaFreeHost(c->pinned);
+    if (c->stream) cudaStreamDestroy(c->stream);
+    delete c;
+}
+
+const char *ipcg_last_error(const ipcg_ctx *c) { return c ? c->err.c_str() : g_host_err.c_str(); }
+
+int ipcg_set_stream(ipcg_ctx *c, void *s) {
+    return guarded(c, [&] {
+        CK(cudaStreamSynchronize(c->stream));
+        c->stream = static_cast<cudaStream_t>(s);
+    });
+}
+
+int ipcg_synchronize(ipcg_ctx *c) {
+    return guarded(c, [&] { CK(cudaStreamSynchronize(c->stream)); });
+}
+
+int ipcg_compress(ipcg_ctx *c, int scalar, const void *values, int on_dev, const uint64_t *dims, int nd, double eb,
+                  int interp, int lp, uint64_t cap, ipcg_archive **out) {
+    return guarded(c, [&] { *out = compress_impl(c, scalar, values, on_dev, dims, nd, eb, interp, lp, cap); });
+}
+
+int ipcg_archive_open(ipcg_ctx *c, const void *bytes, uint64_t size, int on_device, ipcg_archive **out) {
+    if (!c && on_device) return IPCG_EINVAL;
+    return guarded(c, [&] {
+        std::vector<uint8_t> head(std::min<uint64_t>(size, kMaxIndexBytes));
+        if (on_device) {
+            if (!head.empty()) CK(cudaMemcpy(head.data(), bytes, head.size(), cudaMemcpyDeviceToHost));
+        } else if (!head.empty()) {
+            std::memcpy(head.data(), bytes, head.size());
+        }
+        ipcg_archive *a = new ipcg_archive;
+        try {
+            parse_index(head.data(), head.size(), a->ix);
+        } catch (...) {
+            delete a;
+            throw;
+        }
+        a->bytes = static_cast<const uint8_t *>(bytes);
+        a->size = size;
+        a->on_device = on_device != 0;
+        a->device = c ? c->device : 0;
+        *out = a;
+    });
+}
+
+int ipcg_archive_index(const ipcg_archive *a, ipcg_index *out) {
+    if (!a || !out) return IPCG_EINVAL;
+    *out = a->ix;
+    return IPCG_OK;
+}
+
+uint64_t ipcg_archive_size(const ipcg_archive *a) { return a ? a->size : 0; }
+
+int ipcg_archive_write(ipcg_ctx *c, const ipcg_archive *a, void *dst, int dst_on_device, uint64_t capacity) {
+    return guarded(c, [&] {
+        if (capacity < a->size) throw Error(EINVAL_, "destination too small for the archive");
+        const cudaMemcpyKind kind = a->on_device ? (dst_on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost)
+                                                 : (dst_on_device ? cudaMemcpyHostToDevice : cudaMemcpyHostToHost);
+        CK(cudaMemcpyAsync(dst, a->bytes, a->size, kind, c->stream));
+        CK(cudaStreamSynchronize(c->stream));
+    });
+}
+
+uint64_t ipcg_archive_payload_bytes_read(const ipcg_archive *a) { return a ? a->payload_read : 0; }
+
+void ipcg_archive_free(ipcg_archive *a) {
+    if (!a) return;
+    if (a->owned) {
+        cudaSetDevice(a->device);
+        cudaFree(a->owned);
+    }
+    delete a;
+}
+
+int ipcg_reconstruct(ipcg_ctx *c, ipcg_archive *a, int scalar, const int *k, void *out, int out_on_device,
+                     ipcg_session **session_out, uint64_t *loaded) {
+    if (session_out) *session_out = nullptr;
+    return guarded(c, [&] { retrieve_impl(c, a, scalar, k, out, out_on_device, nullptr, nullptr, 0, session_out, loaded); });
+}
+
+int ipcg_refine(ipcg_ctx *c, ipcg_archive *a, int scalar, const ipcg_session *s, const void *previous, int prev_on_dev,
+                const int *k, void *out, int out_on_device, ipcg_session **session_out, uint64_t *loaded) {
+    if (session_out) *session_out = nullptr;
+    return guarded(c, [&] {
+        if (!s) throw Error(EINVAL_, "refinement needs a session");
+        retrieve_impl(c, a, scalar, k, out, out_on_device, s, previous, prev_on_dev, session_out, loaded);
+    });
+}
+
+int ipcg_session_create(ipcg_ctx *c, const ipcg_archive *a, const int *planes_loaded, const uint32_t *const *merged,
+                        ipcg_session **out) {
+    return guarded(c, [&] {
+        ipcg_session *s = new ipcg_session;
+        s->archive_crc = a->ix.identity;
+        s->levels = a->ix.levels;
+        s->lp = a->ix.progressive_levels;
+        for (int l = 0; l < s->levels; ++l) {
+            s->k[l] = planes_loaded[l];
+            s->count[l] = a->ix.records[l].count;
+            if (l + 1 <= s->lp && merged && merged[l]) {
+                const uint64_t cnt = s->count[l];
+                CK(cudaMalloc((void **)&s->merged[l], std::max<uint64_t>(cnt, 1) * 4));
+                CK(cudaMemcpy(s->merged[l], merged[l], cnt * 4, cudaMemcpyHostToDevice));
+            }
+        }
+        *out = s;
+    });
+}
+
+int ipcg_session_levels(const ipcg_session *s) { return s ? s->levels : 0; }
+uint32_t ipcg_session_archive_crc(const ipcg_session *s) { return s ? s->archive_crc : 0; }
+int ipcg_session_planes_loaded(const ipcg_session *s, int *k_out) {
+    if (!s) return IPCG_EINVAL;
+    for (int l = 0; l < s->levels; ++l) k_out[l] = s->k[l];
+    return IPCG_OK;
+}
+uint64_t ipcg_session_count(const ipcg_session *s, int level) {
+    if (!s || level < 1 || level > s->levels || !s->merged[level - 1]) return 0;
+    return s->count[level - 1];
+}
+int ipcg_session_merged(ipcg_ctx *c, const ipcg_session *s, int level, uint32_t *dst, int dst_on_device) {
+    return guarded(c, [&] {
+        if (level < 1 || level > s->levels) throw Error(EINVAL_, "level index out of range");
+        const uint32_t *m = s->merged[level - 1];
+        if (!m) return;
+        CK(cudaMemcpyAsync(dst, m, s->count[level - 1] * 4, dst_on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost,
+                           c->stream));
+        CK(cudaStreamSynchronize(c->stream));
+    });
+}
+void ipcg_session_free(ipcg_session *s) {
+    if (!s) return;
+    for (int l = 0; l < IPCG_MAX_LEVELS; ++l)
+        if (s->merged[l]) cudaFree(s->merged[l]);
+    delete s;
+}
+
+int ipcg_plan_for_error(ipcg_ctx *c, const ipcg_archive *a, double max_error, int *k_out) {
+    return guarded(c, [&] { plan_for_error(a->ix, max_error, k_out); });
+}
+int ipcg_plan_for_size(ipcg_ctx *c, const ipcg_archive *a, uint64_t budget, int *k_out) {
+    return guarded(c, [&] { plan_for_size(a->ix, budget, k_out); });
+}
+double ipcg_bound_for_plan(const ipcg_archive *a, const int *k) { return bound_for_plan(a->ix, k); }
+uint64_t ipcg_plan_payload_bytes(const ipcg_archive *a, const int *k) { return plan_payload_bytes(a->ix, k); }
+
+int ipcg_backend_encode(ipcg_ctx *c, const uint8_t *raw, int raw_on_device, uint64_t plane_bytes, uint64_t raw_stride,
+                        int count, uint8_t *backend, uint64_t *length, uint32_t *crc, uint8_t *out_payload,
+                        uint64_t out_capacity) {
+    return guarded(c, [&] {
+        if (count <= 0) return;
+        cudaStream_t st = c->stream;
+        const uint64_t in_stride = round_up(std::max<uint64_t>(plane_bytes, 1), 16);
+        DBuf in((uint64_t)count * in_stride, st);
+        for (int i = 0; i < count; ++i)
+            CK(cudaMemcpyAsync(in.as<uint8_t>() + i * in_stride, raw + i * raw_stride, plane_bytes,
+                               raw_on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, st));
+        const uint64_t out_stride = round_up(plane_bytes + 16, 16);
+        DBuf outb((uint64_t)count * out_stride, st), ws(DeflateBatch::workspace_bytes(count, plane_bytes), st);
+        DBuf be(count, st), ln(count * 8, st), cr(count * 4, st), pl(count * 8, st);
+        const BackendResults res{be.as<uint8_t>(), ln.as<uint64_t>(), cr.as<uint32_t>(), pl.as<const uint8_t *>()};
+        DeflateBatch::run(in.as<uint8_t>(), in_stride, count, plane_bytes, outb.as<uint8_t>(), out_stride, ws.p, res, st);
+        std::vector<const uint8_t *> ptrs(count);
+        CK(cudaMemcpyAsync(backend, be.p, count, cudaMemcpyDeviceToHost, st));
+        CK(cudaMemcpyAsync(length, ln.p, count * 8, cudaMemcpyDeviceToHost, st));
+        CK(cudaMemcpyAsync(crc, cr.p, count * 4, cudaMemcpyDeviceToHost, st));
+        CK(cudaMemcpyAsync(ptrs.data(), pl.p, count * 8, cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
+        uint64_t o = 0;
+        for (int i = 0; i < count; ++i) {
+            if (o + length[i] > out_capacity) throw Error(EINVAL_, "output capacity too small");
+            CK(cudaMemcpyAsync(out_payload + o, ptrs[i], length[i], cudaMemcpyDeviceToHost, st));
+            o += length[i];
+        }
+        CK(cudaStreamSynchronize(st));
+    });
+}
+
+uint64_t ipcg_kernel_launches(const ipcg_ctx *) { return launch_counter(); }
+
+}  // extern "C"

@@ -1,0 +1,478 @@
+// numerics.cu -- sm_100a kernels for prediction, quantization, bitplanes, loss tables,
+// merge and reconstruction.  See numerics.cuh for the reference citations.
+#include <cub/device/device_radix_sort.cuh>
+
+#include "numerics.cuh"
+
+namespace ipcg {
+
+namespace {
+
+constexpr unsigned kBlock = 256;
+
+// row-major unravel of a pass-box index into (flat, coordinate along the pass axis)
+template <bool Small>
+__device__ __forceinline__ uint64_t pass_flat(const PassDesc &p, uint64_t i, uint64_t &axis_idx) {
+    uint64_t flat = p.start_flat;
+    axis_idx = 0;
+    if (Small) {
+        uint32_t r32 = (uint32_t)i;
+        for (int d = p.nd - 1; d >= 0; --d) {
+            const uint32_t c = (uint32_t)p.cnt[d];
+            const uint32_t q = r32 / c, r = r32 - q * c;
+            r32 = q;
+            flat += (uint64_t)r * p.step_flat[d];
+            if (d == p.axis) axis_idx = r;
+        }
+    } else {
+        for (int d = p.nd - 1; d >= 0; --d) {
+            const uint64_t c = p.cnt[d];
+            const uint64_t q = i / c, r = i - q * c;
+            i = q;
+            flat += r * p.step_flat[d];
+            if (d == p.axis) axis_idx = r;
+        }
+    }
+    return flat;
+}
+
+// predict_point<T>, predictor.hpp:27-38 (cubic -> linear -> copy fallback)
+template <class T>
+__device__ __forceinline__ T predict(const T *__restrict__ st, uint64_t flat, uint64_t coord, const PassDesc &p,
+                                     bool cubic) {
+    const uint64_t s = p.s, stp = p.st;
+    if (cubic && coord >= 3 * s && coord + 3 * s < p.extent) {
+        const T a = st[flat - 3 * stp], b = st[flat - stp], c = st[flat + stp], d = st[flat + 3 * stp];
+        return ((T)9 * (b + c) - (a + d)) / (T)16;
+    }
+    if (coord + s < p.extent) return (st[flat - stp] + st[flat + stp]) / (T)2;
+    return st[flat - stp];
+}
+
+template <class T>
+__device__ __forceinline__ T reconstruct_value(T pred, double eb, int64_t code) {  // quantizer.hpp:57-60
+    return (T)((double)pred + 2.0 * eb * (double)code);
+}
+
+// quantize_residual, quantizer.hpp:65-81: returns true for an outlier
+template <class T>
+__device__ __forceinline__ bool quantize_residual(T value, T pred, double eb, int32_t &code, T &recon) {
+    const double y = (double)value - (double)pred;
+    if (isfinite(y)) {
+        const double q = round(y / (2.0 * eb));
+        if (fabs(q) <= (double)kMaxCode) {
+            const int32_t q0 = (int32_t)q;
+#pragma unroll
+            for (int c = 0; c < 3; ++c) {
+                const int64_t cand = c == 0 ? (int64_t)q0 : c == 1 ? (int64_t)q0 - 1 : (int64_t)q0 + 1;
+                if (cand < -kMaxCode || cand > kMaxCode) continue;
+                const T r = reconstruct_value(pred, eb, cand);
+                if (fabs((double)value - (double)r) <= eb) {
+                    code = (int32_t)cand;
+                    recon = r;
+                    return false;
+                }
+            }
+        }
+    }
+    code = 0;
+    recon = value;
+    return true;
+}
+
+template <class T>
+__device__ __forceinline__ uint64_t bits_of(T v) {
+    if constexpr (sizeof(T) == 4) return (uint64_t)__float_as_uint(v);
+    else return (uint64_t)__double_as_longlong(v);
+}
+
+// ------------------------------------------------------------------ range scan
+// std::min/std::max seeded with +/-inf: NaN never wins (pipeline.hpp:151-155)
+template <class T>
+__global__ void k_range_partial(const T *__restrict__ v, uint64_t n, double *part) {
+    double lo = INFINITY, hi = -INFINITY;
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
+        const double x = (double)v[i];
+        lo = (x < lo) ? x : lo;
+        hi = (hi < x) ? x : hi;
+    }
+    __shared__ double slo[kBlock], shi[kBlock];
+    slo[threadIdx.x] = lo;
+    shi[threadIdx.x] = hi;
+    __syncthreads();
+    for (unsigned s = blockDim.x / 2; s > 0; s >>= 1) {
+        if (threadIdx.x < s) {
+            const double a = slo[threadIdx.x + s], b = shi[threadIdx.x + s];
+            slo[threadIdx.x] = (a < slo[threadIdx.x]) ? a : slo[threadIdx.x];
+            shi[threadIdx.x] = (shi[threadIdx.x] < b) ? b : shi[threadIdx.x];
+        }
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+        part[2 * blockIdx.x] = slo[0];
+        part[2 * blockIdx.x + 1] = shi[0];
+    }
+}
+__global__ void k_range_final(const double *part, int nparts, double *out2) {
+    if (threadIdx.x != 0 || blockIdx.x != 0) return;
+    double lo = INFINITY, hi = -INFINITY;
+    for (int i = 0; i < nparts; ++i) {
+        lo = (part[2 * i] < lo) ? part[2 * i] : lo;
+        hi = (hi < part[2 * i + 1]) ? part[2 * i + 1] : hi;
+    }
+    out2[0] = lo;
+    out2[1] = hi;
+}
+
+// --------------------------------------------------------- predict + quantize
+// One launch per (level, axis) pass: every target reads only coarser levels and
+// earlier passes, so all targets of the pass are independent (grid.hpp:40-46).
+template <class T, bool Small>
+__global__ void __launch_bounds__(kBlock) k_quant_pass(const T *__restrict__ values, T *__restrict__ state, PassDesc p,
+                                                       double eb, bool cubic, uint32_t *__restrict__ nb,
+                                                       uint32_t *lowor, OutlierSink sink) {
+    uint32_t orv = 0;
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < p.size; i += (uint64_t)gridDim.x * blockDim.x) {
+        uint64_t aidx;
+        const uint64_t flat = pass_flat<Small>(p, i, aidx);
+        const T v = values[flat];
+        T pred = (T)0;
+        if (p.axis >= 0) pred = predict<T>(state, flat, p.axis_start + aidx * p.axis_step, p, cubic);
+        int32_t code;
+        T recon;
+        const bool outl = quantize_residual<T>(v, pred, eb, code, recon);
+        state[flat] = outl ? v : recon;
+        const uint32_t w = to_negabinary(code);
+        nb[p.ordinal_base + i] = w;
+        orv |= w;
+        if (outl) {
+            const unsigned long long slot = atomicAdd(sink.count, 1ull);
+            sink.ordinal[slot] = p.ordinal_base + i;
+            sink.bits[slot] = bits_of<T>(v);
+        }
+    }
+    orv = __reduce_or_sync(0xffffffffu, orv);
+    if (lane_id() == 0 && orv) atomicOr(lowor, orv);
+}
+
+// ------------------------------------------------------- bitplanes + XOR code
+// split + xor_encode (bitplane.cpp:7-22,44-49): a warp ballot turns 32 codewords
+// into one 32-bit word of plane p (bit i = codeword i, i.e. byte i/8 bit i%8 when
+// stored little-endian), the 2-plane XOR runs on those words, and a shared-memory
+// transpose makes every plane's store a 128-byte coalesced row.
+__global__ void __launch_bounds__(1024) k_bitplanes(const uint32_t *__restrict__ nb, uint64_t count,
+                                                    uint32_t *__restrict__ planes, uint64_t stride) {
+    __shared__ uint32_t tile[32][33];
+    const unsigned warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint64_t word0 = (uint64_t)blockIdx.x * 32;
+    const uint64_t i = (word0 + warp) * 32 + lane;
+    const uint32_t v = i < count ? nb[i] : 0u;
+    uint32_t prev1 = 0, prev2 = 0, mine = 0;
+#pragma unroll
+    for (int p = 0; p < 32; ++p) {
+        const uint32_t b = __ballot_sync(0xffffffffu, (v >> (31 - p)) & 1u);
+        const uint32_t e = b ^ prev1 ^ prev2;
+        prev2 = prev1;
+        prev1 = b;
+        if ((int)lane == p) mine = e;
+    }
+    tile[lane][warp] = mine;  // tile[plane][word]
+    __syncthreads();
+    const unsigned p = threadIdx.x >> 5, w = threadIdx.x & 31;
+    const uint64_t words = (count + 31) / 32;
+    if (word0 + w < words) planes[(uint64_t)p * stride + word0 + w] = tile[p][w];
+}
+
+}  // namespace
+
+namespace {
+// ------------------------------------------------------------ loss table
+// measure_loss_table (pipeline.hpp:85-124) for one dropped-digit count d and one
+// pass: replays the level on the double deviation field `dev` (zero at coarser
+// levels) and folds max|v| into rawbits[d] as an order-independent atomicMax on
+// the IEEE bit patterns of non-negative doubles (exact).  d beyond the highest set
+// digit of the level's OR equals d = hb+1, so those launches exit immediately.
+template <bool Small, bool Cubic>
+__global__ void __launch_bounds__(kBlock) k_loss_pass2(const uint32_t *__restrict__ nb, double *__restrict__ dev,
+                                                       PassDesc p, double unit, int d, const uint32_t *lowor,
+                                                       unsigned long long *rawbits) {
+    const uint32_t lo = *lowor;
+    const uint32_t mask = d == 32 ? 0xFFFFFFFFu : ((1u << d) - 1u);
+    if ((lo & mask) == 0) return;
+    const int hb = 31 - __clz(lo);
+    if (d > hb + 1) return;
+    double worst = 0.0;
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < p.size; i += (uint64_t)gridDim.x * blockDim.x) {
+        uint64_t aidx;
+        const uint64_t flat = pass_flat<Small>(p, i, aidx);
+        const uint32_t w = nb[p.ordinal_base + i];
+        const int64_t truncated = from_negabinary(w & ~mask);
+        const double own = unit * (double)(truncated - (int64_t)from_negabinary(w));
+        const double v = p.axis < 0 ? own : predict<double>(dev, flat, p.axis_start + aidx * p.axis_step, p, Cubic) + own;
+        dev[flat] = v;
+        const double a = fabs(v);
+        worst = (worst < a) ? a : worst;  // NaN never wins, as std::max(worst, NaN)
+    }
+    __shared__ double red[kBlock];
+    red[threadIdx.x] = worst;
+    __syncthreads();
+    for (unsigned s = blockDim.x / 2; s > 0; s >>= 1) {
+        if (threadIdx.x < s) red[threadIdx.x] = (red[threadIdx.x] < red[threadIdx.x + s]) ? red[threadIdx.x + s] : red[threadIdx.x];
+        __syncthreads();
+    }
+    if (threadIdx.x == 0 && red[0] > 0.0) atomicMax(&rawbits[d], (unsigned long long)__double_as_longlong(red[0]));
+}
+
+template <bool Small>
+__global__ void k_zero_pass(double *__restrict__ dev, PassDesc p) {
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < p.size; i += (uint64_t)gridDim.x * blockDim.x) {
+        uint64_t aidx;
+        dev[pass_flat<Small>(p, i, aidx)] = 0.0;
+    }
+}
+
+__global__ void k_loss_finalize(const unsigned long long *rawbits, const uint32_t *lowor, double *delta) {
+    if (threadIdx.x != 0 || blockIdx.x != 0) return;
+    const uint32_t lo = *lowor;
+    double raw[33];
+    raw[0] = 0.0;
+    const int hb = lo ? 31 - __clz(lo) : -1;
+    for (int d = 1; d <= 32; ++d) {
+        const uint32_t mask = d == 32 ? 0xFFFFFFFFu : ((1u << d) - 1u);
+        if ((lo & mask) == 0) {
+            raw[d] = 0.0;
+            continue;
+        }
+        const int src = d > hb + 1 ? hb + 1 : d;
+        raw[d] = __longlong_as_double((long long)rawbits[src]);
+    }
+    delta[0] = 0.0;
+    for (int d = 1; d <= 32; ++d) delta[d] = (delta[d - 1] < raw[d]) ? raw[d] : delta[d - 1];
+}
+
+// ------------------------------------------------------------- outlier block
+// (u64 ordinal, T) pairs in ordinal order (pipeline.hpp:126-136)
+__global__ void k_outlier_block(const uint64_t *ord, const uint64_t *bits, const unsigned long long *count, int scalar,
+                                uint8_t *out) {
+    const uint64_t n = *count;
+    const int w = scalar == 0 ? 4 : 8, e = 8 + w;
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
+        uint8_t *dst = out + i * (uint64_t)e;
+        const uint64_t o = ord[i], b = bits[i];
+        for (int k = 0; k < 8; ++k) dst[k] = (uint8_t)(o >> (8 * k));
+        for (int k = 0; k < w; ++k) dst[8 + k] = (uint8_t)(b >> (8 * k));
+    }
+}
+
+// ------------------------------------------------------------------- merge
+// xor_decode + merge (bitplane.cpp:24-59), and refine's digit folding with the XOR
+// prefix taken from already-merged codewords (pipeline.hpp:328-339): one warp per
+// 32 codewords; lane p owns plane p's word.
+__global__ void __launch_bounds__(256) k_merge(const uint32_t *__restrict__ planes, uint64_t stride,
+                                               const uint32_t *__restrict__ merged_in, uint32_t *__restrict__ merged_out,
+                                               uint64_t count, int k0, int k1) {
+    const unsigned lane = threadIdx.x & 31;
+    const uint64_t words = (count + 31) / 32;
+    for (uint64_t w = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5; w < words;
+         w += ((uint64_t)gridDim.x * blockDim.x) >> 5) {
+        const uint64_t i = w * 32 + lane;
+        const uint32_t mi = (merged_in && i < count) ? merged_in[i] : 0u;
+        uint32_t bp = 0;
+        for (int p = 0; p < k0; ++p) {
+            const uint32_t m = __ballot_sync(0xffffffffu, (mi >> (31 - p)) & 1u);
+            if ((int)lane == p) bp = m;
+        }
+        const uint32_t e = ((int)lane >= k0 && (int)lane < k1) ? planes[(uint64_t)lane * stride + w] : 0u;
+        for (int p = k0; p < k1; ++p) {
+            const uint32_t b1 = __shfl_sync(0xffffffffu, bp, (p - 1) & 31);
+            const uint32_t b2 = __shfl_sync(0xffffffffu, bp, (p - 2) & 31);
+            if ((int)lane == p) bp = e ^ (p >= 1 ? b1 : 0u) ^ (p >= 2 ? b2 : 0u);
+        }
+        uint32_t out = 0;
+#pragma unroll
+        for (int b = 0; b < 32; ++b) {
+            const uint32_t m = __ballot_sync(0xffffffffu, (bp >> b) & 1u);
+            if ((int)lane == b) out = __brev(m);
+        }
+        if (i < count) merged_out[i] = out;
+    }
+}
+
+// ------------------------------------------------------------- reconstruction
+// apply_level (pipeline.hpp:61-78) for one pass
+template <class T, bool Small>
+__global__ void __launch_bounds__(kBlock) k_recon_pass(T *__restrict__ state, PassDesc p, double eb, bool cubic,
+                                                       const uint32_t *__restrict__ merged) {
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < p.size; i += (uint64_t)gridDim.x * blockDim.x) {
+        uint64_t aidx;
+        const uint64_t flat = pass_flat<Small>(p, i, aidx);
+        T pred = (T)0;
+        if (p.axis >= 0) pred = predict<T>(state, flat, p.axis_start + aidx * p.axis_step, p, cubic);
+        state[flat] = reconstruct_value<T>(pred, eb, (int64_t)from_negabinary(merged[p.ordinal_base + i]));
+    }
+}
+
+// strictly increasing prefix of in-range ordinals = what the in-order matcher applies
+__global__ void k_outlier_prefix(const uint8_t *block, uint64_t entries, int scalar, uint64_t count, uint64_t *napplied) {
+    __shared__ unsigned long long first_bad;
+    if (threadIdx.x == 0) first_bad = entries;
+    __syncthreads();
+    const int e = 8 + (scalar == 0 ? 4 : 8);
+    auto ord = [&](uint64_t k) {
+        uint64_t o = 0;
+        for (int b = 0; b < 8; ++b) o |= (uint64_t)block[k * e + b] << (8 * b);
+        return o;
+    };
+    for (uint64_t k = threadIdx.x; k < entries; k += blockDim.x) {
+        const uint64_t o = ord(k);
+        const bool bad = o >= count || (k > 0 && ord(k - 1) >= o);
+        if (bad) atomicMin(&first_bad, (unsigned long long)k);
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) *napplied = first_bad;
+}
+
+template <class T, bool Small>
+__global__ void k_outlier_apply(T *__restrict__ state, PassDesc p, const uint8_t *__restrict__ block,
+                                const uint64_t *napplied) {
+    const uint64_t n = *napplied;
+    const int e = 8 + (int)sizeof(T);
+    for (uint64_t k = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; k < n; k += (uint64_t)gridDim.x * blockDim.x) {
+        const uint8_t *q = block + k * e;
+        uint64_t o = 0, b = 0;
+        for (int j = 0; j < 8; ++j) o |= (uint64_t)q[j] << (8 * j);
+        if (o < p.ordinal_base || o >= p.ordinal_base + p.size) continue;
+        for (int j = 0; j < (int)sizeof(T); ++j) b |= (uint64_t)q[8 + j] << (8 * j);
+        uint64_t aidx;
+        const uint64_t flat = pass_flat<Small>(p, o - p.ordinal_base, aidx);
+        if constexpr (sizeof(T) == 4) state[flat] = __uint_as_float((uint32_t)b);
+        else state[flat] = __longlong_as_double((long long)b);
+    }
+}
+
+}  // namespace
+
+// ============================================================= host launchers
+
+void launch_range(const void *values, int scalar, uint64_t n, double *scratch, double *out2, cudaStream_t st) {
+    const unsigned g = grid_for(n, kBlock, 1024);
+    if (scalar == 0) k_range_partial<float><<<g, kBlock, 0, st>>>((const float *)values, n, scratch);
+    else k_range_partial<double><<<g, kBlock, 0, st>>>((const double *)values, n, scratch);
+    CKL();
+    k_range_final<<<1, 32, 0, st>>>(scratch, (int)g, out2);
+    CKL();
+}
+
+void launch_quant_pass(const void *values, void *state, int scalar, bool cubic, const PassDesc &pd, double eb,
+                       uint32_t *nb, uint32_t *lowor, OutlierSink sink, cudaStream_t st) {
+    const unsigned g = grid_for(pd.size, kBlock);
+    const bool small = pd.size < (uint64_t(1) << 32);
+    if (scalar == 0) {
+        if (small) k_quant_pass<float, true><<<g, kBlock, 0, st>>>((const float *)values, (float *)state, pd, eb, cubic, nb, lowor, sink);
+        else k_quant_pass<float, false><<<g, kBlock, 0, st>>>((const float *)values, (float *)state, pd, eb, cubic, nb, lowor, sink);
+    } else {
+        if (small) k_quant_pass<double, true><<<g, kBlock, 0, st>>>((const double *)values, (double *)state, pd, eb, cubic, nb, lowor, sink);
+        else k_quant_pass<double, false><<<g, kBlock, 0, st>>>((const double *)values, (double *)state, pd, eb, cubic, nb, lowor, sink);
+    }
+    CKL();
+}
+
+void launch_bitplanes(const uint32_t *nb, uint64_t count, uint32_t *planes, uint64_t stride, cudaStream_t st) {
+    const uint64_t words = (count + 31) / 32;
+    if (words == 0) return;
+    const uint64_t blocks = (words + 31) / 32;
+    k_bitplanes<<<(unsigned)blocks, 1024, 0, st>>>(nb, count, planes, stride);
+    CKL();
+}
+
+void launch_loss_pass(const uint32_t *nb, double *dev, const PassDesc &pd, bool cubic, double u, int d,
+                      const uint32_t *lowor, unsigned long long *rawbits, cudaStream_t st) {
+    const unsigned g = grid_for(pd.size, kBlock);
+    const bool small = pd.size < (uint64_t(1) << 32);
+    if (small) {
+        if (cubic) k_loss_pass2<true, true><<<g, kBlock, 0, st>>>(nb, dev, pd, u, d, lowor, rawbits);
+        else k_loss_pass2<true, false><<<g, kBlock, 0, st>>>(nb, dev, pd, u, d, lowor, rawbits);
+    } else {
+        if (cubic) k_loss_pass2<false, true><<<g, kBlock, 0, st>>>(nb, dev, pd, u, d, lowor, rawbits);
+        else k_loss_pass2<false, false><<<g, kBlock, 0, st>>>(nb, dev, pd, u, d, lowor, rawbits);
+    }
+    CKL();
+}
+
+void launch_zero_pass(double *dev, const PassDesc &pd, cudaStream_t st) {
+    const unsigned g = grid_for(pd.size, kBlock);
+    if (pd.size < (uint64_t(1) << 32)) k_zero_pass<true><<<g, kBlock, 0, st>>>(dev, pd);
+    else k_zero_pass<false><<<g, kBlock, 0, st>>>(dev, pd);
+    CKL();
+}
+
+void launch_loss_finalize(const unsigned long long *rawbits, const uint32_t *lowor, double *delta, cudaStream_t st) {
+    k_loss_finalize<<<1, 32, 0, st>>>(rawbits, lowor, delta);
+    CKL();
+}
+
+size_t sort_outliers_temp_bytes(uint64_t capacity) {
+    size_t bytes = 0;
+    cub::DeviceRadixSort::SortPairs(nullptr, bytes, (const uint64_t *)nullptr, (uint64_t *)nullptr,
+                                    (const uint64_t *)nullptr, (uint64_t *)nullptr, (int)capacity);
+    return bytes;
+}
+
+void launch_sort_outliers(OutlierSink sink, uint64_t count, uint64_t *ord_sorted, uint64_t *bits_sorted, void *temp,
+                          size_t temp_bytes, cudaStream_t st) {
+    if (count == 0) return;
+    CK(cub::DeviceRadixSort::SortPairs(temp, temp_bytes, sink.ordinal, ord_sorted, sink.bits, bits_sorted, (int)count,
+                                       0, 64, st));
+}
+
+void launch_outlier_block(const uint64_t *ord_sorted, const uint64_t *bits_sorted, const unsigned long long *count,
+                          int scalar, uint8_t *out, cudaStream_t st) {
+    k_outlier_block<<<64, 256, 0, st>>>(ord_sorted, bits_sorted, count, scalar, out);
+    CKL();
+}
+
+void launch_merge(const uint32_t *planes, uint64_t stride, const uint32_t *merged_in, uint32_t *merged_out,
+                  uint64_t count, int k0, int k1, cudaStream_t st) {
+    const uint64_t words = (count + 31) / 32;
+    if (words == 0) return;
+    const unsigned g = grid_for(words * 32, 256);
+    k_merge<<<g, 256, 0, st>>>(planes, stride, merged_in, merged_out, count, k0, k1);
+    CKL();
+}
+
+void launch_recon_pass(void *state, int scalar, bool cubic, const PassDesc &pd, double eb, const uint32_t *merged,
+                       cudaStream_t st) {
+    const unsigned g = grid_for(pd.size, kBlock);
+    const bool small = pd.size < (uint64_t(1) << 32);
+    if (scalar == 0) {
+        if (small) k_recon_pass<float, true><<<g, kBlock, 0, st>>>((float *)state, pd, eb, cubic, merged);
+        else k_recon_pass<float, false><<<g, kBlock, 0, st>>>((float *)state, pd, eb, cubic, merged);
+    } else {
+        if (small) k_recon_pass<double, true><<<g, kBlock, 0, st>>>((double *)state, pd, eb, cubic, merged);
+        else k_recon_pass<double, false><<<g, kBlock, 0, st>>>((double *)state, pd, eb, cubic, merged);
+    }
+    CKL();
+}
+
+void launch_outlier_prefix(const uint8_t *block, uint64_t entries, int scalar, uint64_t count, uint64_t *napplied,
+                           cudaStream_t st) {
+    k_outlier_prefix<<<1, 1024, 0, st>>>(block, entries, scalar, count, napplied);
+    CKL();
+}
+
+void launch_outlier_apply(void *state, int scalar, const PassDesc &pd, const uint8_t *block, const uint64_t *napplied,
+                          uint64_t max_entries, cudaStream_t st) {
+    if (max_entries == 0) return;
+    const unsigned g = grid_for(max_entries, 256, 1024);
+    const bool small = pd.size < (uint64_t(1) << 32);
+    if (scalar == 0) {
+        if (small) k_outlier_apply<float, true><<<g, 256, 0, st>>>((float *)state, pd, block, napplied);
+        else k_outlier_apply<float, false><<<g, 256, 0, st>>>((float *)state, pd, block, napplied);
+    } else {
+        if (small) k_outlier_apply<double, true><<<g, 256, 0, st>>>((double *)state, pd, block, napplied);
+        else k_outlier_apply<double, false><<<g, 256, 0, st>>>((double *)state, pd, block, napplied);
+    }
+    CKL();
+}
+
+}  // namespace ipcg

@@ -1,0 +1,56 @@
+// numerics.cuh -- sm_100a kernels for the interpolation/quantization hot path
+// (reference: predictor.hpp:14-38, quantizer.hpp:29-81, bitplane.cpp:7-59,
+// pipeline.hpp:61-124,172-193).  All floating point follows the reference's
+// operation order; the build uses -fmad=false -prec-div=true -ftz=false so every
+// operation rounds exactly like the -ffp-contract=off CPU build.
+#pragma once
+#include <stdint.h>
+
+#include "grid.h"
+#include "util.cuh"
+
+namespace ipcg {
+
+constexpr int32_t kMaxCode = int32_t(1) << 30;  // quantizer.hpp:11
+constexpr uint32_t kNbMask = 0xAAAAAAAAu;       // quantizer.hpp:12
+
+__host__ __device__ __forceinline__ uint32_t to_negabinary(int32_t q) {
+    return (uint32_t)((int64_t)q + (int64_t)kNbMask) ^ kNbMask;
+}
+__host__ __device__ __forceinline__ int32_t from_negabinary(uint32_t w) { return (int32_t)((w ^ kNbMask) - kNbMask); }
+
+struct OutlierSink {
+    unsigned long long *count;
+    uint64_t *ordinal;
+    uint64_t *bits;
+};
+
+// ---- host launchers (numerics.cu) ----
+void launch_range(const void *values, int scalar, uint64_t n, double *scratch /*2*1024*/, double *out2,
+                  cudaStream_t st);
+void launch_quant_pass(const void *values, void *state, int scalar, bool cubic, const PassDesc &pd, double eb,
+                       uint32_t *nb, uint32_t *lowor, OutlierSink sink, cudaStream_t st);
+void launch_bitplanes(const uint32_t *nb, uint64_t count, uint32_t *planes, uint64_t plane_stride_words,
+                      cudaStream_t st);
+void launch_loss_pass(const uint32_t *nb, double *dev, const PassDesc &pd, bool cubic, double unit, int d,
+                      const uint32_t *lowor, unsigned long long *rawbits, cudaStream_t st);
+void launch_zero_pass(double *dev, const PassDesc &pd, cudaStream_t st);
+void launch_loss_finalize(const unsigned long long *rawbits, const uint32_t *lowor, double *delta, cudaStream_t st);
+void launch_sort_outliers(OutlierSink sink, uint64_t count, uint64_t *ord_sorted, uint64_t *bits_sorted,
+                          void *temp, size_t temp_bytes, cudaStream_t st);
+size_t sort_outliers_temp_bytes(uint64_t capacity);
+void launch_outlier_block(const uint64_t *ord_sorted, const uint64_t *bits_sorted, const unsigned long long *count,
+                          int scalar, uint8_t *out, cudaStream_t st);
+
+void launch_merge(const uint32_t *planes, uint64_t plane_stride_words, const uint32_t *merged_in, uint32_t *merged_out,
+                  uint64_t count, int k0, int k1, cudaStream_t st);
+void launch_recon_pass(void *state, int scalar, bool cubic, const PassDesc &pd, double eb, const uint32_t *merged,
+                       cudaStream_t st);
+// outlier block bytes (u64 ordinal, T) -> overwrite inside one pass's ordinal range
+void launch_outlier_apply(void *state, int scalar, const PassDesc &pd, const uint8_t *block, const uint64_t *napplied,
+                          uint64_t max_entries, cudaStream_t st);
+// number of leading entries the reference's in-order matcher applies (pipeline.hpp:71-75)
+void launch_outlier_prefix(const uint8_t *block, uint64_t entries, int scalar, uint64_t count, uint64_t *napplied,
+                           cudaStream_t st);
+
+}  // namespace ipcg

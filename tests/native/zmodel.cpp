@@ -221,3 +221,5 @@ extern "C" int zmodel_compress(const uint8_t *in, uint64_t n, int chunk, uint8_t
     }
     return 0;
 }
+
+extern "C" uint32_t zmodel_crc_combine(uint32_t crc1, uint32_t crc2, uint64_t len2) { return crc_combine(crc1, crc2, len2); }

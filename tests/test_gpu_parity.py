@@ -1,0 +1,196 @@
+"""GPU parity: the sm_100a path against the CPU oracle (oracle/), bit for bit.
+
+Compares, on the same seeded inputs: whole archive bytes (codes, outliers, loss
+tables, every bitplane block incl. the zlib-1.3 deflate streams and CRCs), the
+reconstructed values for random plans, refine chains, planner outputs and error
+behaviour.  Mirrors the reference's own tests (proj/tests/test_pipeline.cpp).
+"""
+import numpy as np
+import pytest
+
+import oracle
+import paper_2502_04093_b200 as ipc
+from paper_2502_04093_b200 import synth
+
+pytestmark = pytest.mark.gpu
+
+SHAPES = [(1,), (2,), (3, 1), (1, 1, 1, 5), (9,), (17, 9), (65,), (257,), (33, 21), (17, 18, 19), (5, 6, 7),
+          (2, 3, 4, 5), (31, 22), (129,), (513,), (64, 64), (9, 7, 33)]
+
+
+def _field(dims, seed, dtype):
+    f = synth.smooth_field(dims, seed).astype(dtype)
+    return f
+
+
+def _eb(f, rel):
+    r = float(np.max(f)) - float(np.min(f))
+    return rel * r if r > 0 else 1e-3
+
+
+@pytest.mark.parametrize("dims", SHAPES)
+@pytest.mark.parametrize("interp", [0, 1])
+@pytest.mark.parametrize("dtype", [np.float32, np.float64])
+def test_archive_bytes_match_oracle(dims, interp, dtype, oracle_lib, ctx):
+    f = _field(dims, 17 + len(dims), dtype)
+    eb = _eb(f, 1e-4)
+    want = oracle_lib.compress(f, dims, eb, interp)
+    got = ipc.compress_field(f, dims, eb, interp, ctx=ctx).to_bytes()
+    assert got == want
+
+
+@pytest.mark.parametrize("rel", [1e-1, 1e-3, 1e-6])
+@pytest.mark.parametrize("lp", [0, 1, 2])
+def test_archive_bytes_eb_and_progressive_levels(rel, lp, oracle_lib, ctx):
+    dims = (24, 40, 36)
+    f = _field(dims, 5, np.float32)
+    eb = _eb(f, rel)
+    want = oracle_lib.compress(f, dims, eb, 1, lp)
+    got = ipc.compress_field(f, dims, eb, 1, lp, ctx=ctx).to_bytes()
+    assert got == want
+
+
+@pytest.mark.parametrize("cfg,dims", [(1, (64, 64, 64)), (2, (64, 64, 64)), (3, (90, 180)), (4, (20, 60, 60)),
+                                      (5, (24, 36, 36))])
+def test_baseline_config_generators_match(cfg, dims, oracle_lib, ctx):
+    c = synth.CONFIGS[cfg]
+    f = synth.make_field(cfg, dims=dims)
+    eb = synth.abs_eb(f, c["rel_eb"])
+    want = oracle_lib.compress(f, dims, eb, c["interp"])
+    got = ipc.compress_field(f, dims, eb, c["interp"], ctx=ctx).to_bytes()
+    assert got == want
+
+
+def test_outliers_nonfinite_and_spikes(oracle_lib, ctx):
+    for dt in (np.float32, np.float64):
+        v = np.ones(40, dtype=dt)
+        v[7] = np.inf
+        v[21] = 1e30 if dt == np.float32 else 1e60
+        v[22] = -v[21]
+        v[30] = np.nan
+        want = oracle_lib.compress(v, (40,), 1e-6, 1)
+        got = ipc.compress_field(v, (40,), 1e-6, 1, ctx=ctx).to_bytes()
+        assert got == want
+
+
+def _random_plan(rng, L, lp):
+    return [32 if l + 1 > lp else int(rng.integers(0, 33)) for l in range(L)]
+
+
+def _widen(rng, k, lp):
+    return [x + (int(rng.integers(0, 33 - x)) if i + 1 <= lp else 0) for i, x in enumerate(k)]
+
+
+@pytest.mark.parametrize("dims,interp,dtype", [((65, 33), 0, np.float64), ((17, 13, 11), 1, np.float64),
+                                               ((64, 64, 64), 1, np.float32), ((33,), 1, np.float32),
+                                               ((2, 3, 4, 5), 0, np.float32)])
+def test_reconstruct_and_refine_match_oracle(dims, interp, dtype, oracle_lib, ctx):
+    f = _field(dims, 606, dtype)
+    eb = _eb(f, 1e-4)
+    arch = oracle_lib.compress(f, dims, eb, interp)
+    reader = ipc.ArchiveReader(arch, ctx=ctx)
+    info = oracle_lib.info(arch)
+    L, lp = info.levels, info.progressive_levels
+    rng = np.random.default_rng(7)
+    n = f.size
+    for trial in range(4):
+        k1 = _random_plan(rng, L, lp)
+        k2 = _widen(rng, k1, lp)
+        want1, m1, loaded1 = oracle_lib.reconstruct(arch, k1, dtype, n)
+        got1 = ipc.reconstruct_field(reader, k1)
+        assert got1.values.tobytes() == want1.tobytes()
+        assert got1.stats.payload_bytes_loaded == loaded1
+        for l in range(L):
+            if m1[l] is not None:
+                assert np.array_equal(got1.session.merged(l + 1), m1[l])
+        want2, _, loaded2 = oracle_lib.refine(arch, k1, m1, want1, k2)
+        got2 = ipc.refine_field(reader, got1.session, got1.values, k2)
+        assert got2.values.tobytes() == want2.tobytes()
+        assert got2.stats.payload_bytes_loaded == loaded2
+        direct2, _, _ = oracle_lib.reconstruct(arch, k2, dtype, n)
+        assert got2.values.tobytes() == direct2.tobytes()
+
+
+def test_gpu_archive_round_trip_device_resident(oracle_lib, ctx):
+    import torch
+
+    dims = (48, 40, 32)
+    f = _field(dims, 3, np.float32)
+    eb = _eb(f, 1e-3)
+    ft = torch.from_numpy(f).cuda()
+    reader = ipc.compress_field(ft, dims, eb, 1, ctx=ctx)  # device in, device archive
+    arch = reader.to_bytes()
+    assert arch == oracle_lib.compress(f, dims, eb, 1)
+    k = ipc.full_plan(reader).k
+    out = ipc.reconstruct_field(reader, k, device=True)
+    want, _, _ = oracle_lib.reconstruct(arch, k, np.float32, f.size)
+    assert out.values.cpu().numpy().tobytes() == want.tobytes()
+    assert float(np.max(np.abs(out.values.cpu().numpy().astype(np.float64) - f))) <= eb
+
+
+def test_planner_matches_oracle(oracle_lib, ctx):
+    dims = (33, 29, 17)
+    f = _field(dims, 42, np.float64)
+    eb = _eb(f, 1e-4)
+    arch = oracle_lib.compress(f, dims, eb, 0)
+    reader = ipc.ArchiveReader(arch, ctx=ctx)
+    for factor in (4.0, 64.0, 1024.0, 65536.0):
+        assert ipc.plan_for_error(reader, factor * eb).k == oracle_lib.plan_for_error(arch, factor * eb)
+    total = oracle_lib.plan_payload_bytes(arch, [32] * reader.levels)
+    for frac in (0.2, 0.5, 0.9, 1.0):
+        b = int(total * frac)
+        try:
+            want = oracle_lib.plan_for_size(arch, b)
+        except oracle.InfeasibleRequest:
+            with pytest.raises(ipc.InfeasibleRequest):
+                ipc.plan_for_size(reader, b)
+            continue
+        assert ipc.plan_for_size(reader, b).k == want
+    with pytest.raises(ipc.InfeasibleRequest):
+        ipc.plan_for_error(reader, eb * 0.5)
+
+
+def test_backend_encode_matches_zlib(ctx):
+    import zlib
+
+    rng = np.random.default_rng(0)
+    cases = [bytes(1), bytes(100), bytes(70000), rng.integers(0, 256, 5000, dtype=np.uint8).tobytes(),
+             np.packbits((rng.random(8 * 200000) < 0.05).astype(np.uint8), bitorder="little").tobytes(),
+             (b"abcabcabd" * 30000)[:250000]]
+    for raw in cases:
+        (be, payload, crc), = ipc.backend_encode(np.frombuffer(raw, np.uint8), ctx=ctx)
+        z = zlib.compress(raw, 6)
+        if len(z) < len(raw):
+            assert be == 1 and payload == z
+        else:
+            assert be == 0 and payload == raw
+        assert crc == zlib.crc32(payload)
+
+
+def test_errors_mirror_reference(oracle_lib, ctx):
+    f = _field((33,), 3, np.float64)
+    with pytest.raises(ipc.InvalidArgument, match="error bound must be positive and finite"):
+        ipc.compress_field(f, (33,), 0.0, ctx=ctx)
+    with pytest.raises(ipc.InvalidArgument, match="grid must have between 1 and 4 dimensions"):
+        ipc.compress_field(np.zeros(243), (3, 3, 3, 3, 3), 1e-3, ctx=ctx)
+    arch = oracle_lib.compress(f, (33,), 1e-3, 1)
+    reader = ipc.ArchiveReader(arch, ctx=ctx)
+    with pytest.raises(ipc.InvalidArgument, match="scalar kind does not match archive"):
+        ipc.reconstruct_field(reader, ipc.full_plan(reader), dtype=np.float32)
+    with pytest.raises(ipc.InvalidArgument, match="plan plane count out of range"):
+        ipc.reconstruct_field(reader, [33] * reader.levels)
+    bad = bytearray(arch)
+    bad[0] = ord("X")
+    with pytest.raises(RuntimeError, match="not an archive: bad magic"):
+        ipc.ArchiveReader(bytes(bad), ctx=ctx)
+    # corrupt one payload byte of the finest level's plane 0 -> checksum mismatch
+    info = oracle_lib.info(arch)
+    off = info.index_bytes + info.plane_offset[0][31] + 21
+    bad = bytearray(arch)
+    bad[off] ^= 0xFF
+    r2 = ipc.ArchiveReader(bytes(bad), ctx=ctx)
+    with pytest.raises(RuntimeError, match="block checksum mismatch"):
+        ipc.reconstruct_field(r2, ipc.full_plan(r2))
+    out = ipc.reconstruct_field(reader, [16] * reader.levels)
+    with pytest.raises(ipc.InvalidArgument, match="refinement plan must not drop planes"):
+        ipc.refine_field(reader, out.session, out.values, [8] + [16] * (reader.levels - 1))
