@@ -114,6 +114,9 @@ int ipcg_backend_encode(ipcg_ctx *ctx, const uint8_t *raw, int raw_on_device, ui
 
 /* number of kernels this context launched so far (evidence for bench.py) */
 uint64_t ipcg_kernel_launches(const ipcg_ctx *ctx);
+/* per-kernel-family CUDA-event timing on the launching stream (bench.py roofline) */
+int ipcg_profile_enable(ipcg_ctx *ctx, int enable);
+int ipcg_profile_read(ipcg_ctx *ctx, char *json, uint64_t capacity);
 
 #ifdef __cplusplus
 }

@@ -97,6 +97,8 @@ def library() -> C.CDLL:
         "ipcg_plan_payload_bytes": (u64, [vp, P(i32)]),
         "ipcg_backend_encode": (i32, [vp, vp, i32, u64, u64, i32, vp, vp, vp, vp, u64]),
         "ipcg_kernel_launches": (u64, [vp]),
+        "ipcg_profile_enable": (i32, [vp, i32]),
+        "ipcg_profile_read": (i32, [vp, C.c_char_p, u64]),
     }
     for name, (res, args) in sig.items():
         f = getattr(lib, name)
@@ -113,7 +115,7 @@ EXPORTED_SYMBOLS = [
     "ipcg_session_create", "ipcg_session_levels", "ipcg_session_archive_crc", "ipcg_session_planes_loaded",
     "ipcg_session_count", "ipcg_session_merged", "ipcg_session_free", "ipcg_plan_for_error",
     "ipcg_plan_for_size", "ipcg_bound_for_plan", "ipcg_plan_payload_bytes", "ipcg_backend_encode",
-    "ipcg_kernel_launches",
+    "ipcg_kernel_launches", "ipcg_profile_enable", "ipcg_profile_read",
 ]
 
 
@@ -150,6 +152,16 @@ class Context:
 
     def kernel_launches(self) -> int:
         return int(library().ipcg_kernel_launches(self.h))
+
+    def profile(self, enable: bool = True) -> None:
+        self.check(library().ipcg_profile_enable(self.h, 1 if enable else 0))
+
+    def profile_read(self) -> dict:
+        import json
+
+        buf = C.create_string_buffer(1 << 16)
+        self.check(library().ipcg_profile_read(self.h, buf, 1 << 16))
+        return {k: {"ms": v[0], "scopes": v[1], "bytes": v[2]} for k, v in json.loads(buf.value.decode()).items()}
 
     def __del__(self):
         try:

@@ -210,7 +210,10 @@ ipcg_archive *compress_impl(ipcg_ctx *c, int scalar, const void *values, int on_
     Small *sd = small.as<Small>();
     CK(cudaMemsetAsync(small.p, 0, sizeof(Small), st));
     DBuf ord(n * 8, st), bits(n * 8, st);
-    launch_range(vals, scalar, n, sd->range_part, sd->rng, st);
+    {
+        ProfScope ps("range", st, n * w);
+        launch_range(vals, scalar, n, sd->range_part, sd->rng, st);
+    }
 
     uint64_t maxcount = 0;
     size_t ws_bytes = 0;
@@ -234,9 +237,13 @@ ipcg_archive *compress_impl(ipcg_ctx *c, int scalar, const void *values, int on_
         planes[li] = DBuf(32 * plane_stride[li] * 4, st);
         outs[li] = DBuf(32 * out_stride[li], st);
         const OutlierSink sink{&sd->ocount[li], ord.as<uint64_t>() + sink_base[li], bits.as<uint64_t>() + sink_base[li]};
-        for (const PassDesc &pd : lg.passes)
-            launch_quant_pass(vals, state.p, scalar, cubic, pd, eb, nb.as<uint32_t>(), &sd->lowor[li], sink, st);
+        {
+            ProfScope ps("quant_pass", st, lg.count * (uint64_t)(2 * w + 4) + lg.count * (uint64_t)w);
+            for (const PassDesc &pd : lg.passes)
+                launch_quant_pass(vals, state.p, scalar, cubic, pd, eb, nb.as<uint32_t>(), &sd->lowor[li], sink, st);
+        }
         // loss table (measure_loss_table): replay per dropped-digit count d
+        ProfScope psl("loss_table", st, lg.count * 4);
         for (int d = 1; d <= 32; ++d)
             for (const PassDesc &pd : lg.passes)
                 launch_loss_pass(nb.as<uint32_t>(), dev.as<double>(), pd, cubic, 2.0 * eb, d, &sd->lowor[li],
@@ -244,7 +251,10 @@ ipcg_archive *compress_impl(ipcg_ctx *c, int scalar, const void *values, int on_
         for (const PassDesc &pd : lg.passes) launch_zero_pass(dev.as<double>(), pd, st);
         launch_loss_finalize(sd->raw[li], &sd->lowor[li], sd->delta[li], st);
         if (planes[li].p) CK(cudaMemsetAsync(planes[li].p, 0, 32 * plane_stride[li] * 4, st));
-        launch_bitplanes(nb.as<uint32_t>(), lg.count, planes[li].as<uint32_t>(), plane_stride[li], st);
+        {
+            ProfScope ps("bitplanes", st, lg.count * 8);
+            launch_bitplanes(nb.as<uint32_t>(), lg.count, planes[li].as<uint32_t>(), plane_stride[li], st);
+        }
         const BackendResults res{sd->backend[li], sd->length[li], sd->crc[li], sd->payload[li]};
         DeflateBatch::run(planes[li].as<uint8_t>(), plane_stride[li] * 4, 32, pb[li], outs[li].as<uint8_t>(),
                           out_stride[li], ws.p, res, st);
@@ -550,7 +560,12 @@ void retrieve_impl(ipcg_ctx *c, ipcg_archive *a, int scalar, const int *k, void 
         CK(cudaMemcpyAsync(pd.p, hp, R * 8, cudaMemcpyHostToDevice, st));
         CK(cudaMemcpyAsync(ld.p, hp + R * 8, R * 8, cudaMemcpyHostToDevice, st));
         CK(cudaStreamSynchronize(st));  // pinned ptr/len table consumed
-        crc32_batch(pd.as<const uint8_t *>(), ld.as<uint64_t>(), (int)R, maxp, crcs.as<uint32_t>(), crcws.p, cw, st);
+        {
+            uint64_t cb = 0;
+            for (uint64_t x : lens) cb += x;
+            ProfScope ps("crc_check", st, cb);
+            crc32_batch(pd.as<const uint8_t *>(), ld.as<uint64_t>(), (int)R, maxp, crcs.as<uint32_t>(), crcws.p, cw, st);
+        }
         std::vector<uint32_t> hcrc(R);
         CK(cudaMemcpyAsync(hcrc.data(), crcs.p, R * 4, cudaMemcpyDeviceToHost, st));
         CK(cudaStreamSynchronize(st));
@@ -566,7 +581,12 @@ void retrieve_impl(ipcg_ctx *c, ipcg_archive *a, int scalar, const int *k, void 
             InflateJob *jh = static_cast<InflateJob *>(pinned(c, jobs.size() * sizeof(InflateJob)));
             std::memcpy(jh, jobs.data(), jobs.size() * sizeof(InflateJob));
             CK(cudaMemcpyAsync(jd.p, jh, jobs.size() * sizeof(InflateJob), cudaMemcpyHostToDevice, st));
-            inflate_batch(jd.as<InflateJob>(), (int)jobs.size(), sd.as<int>(), st);
+            {
+                uint64_t ib = 0;
+                for (const InflateJob &j : jobs) ib += j.src_len + j.dst_len;
+                ProfScope ps("inflate", st, ib);
+                inflate_batch(jd.as<InflateJob>(), (int)jobs.size(), sd.as<int>(), st);
+            }
             std::vector<int> status(jobs.size());
             CK(cudaMemcpyAsync(status.data(), sd.p, jobs.size() * 4, cudaMemcpyDeviceToHost, st));
             CK(cudaStreamSynchronize(st));
@@ -603,10 +623,14 @@ void retrieve_impl(ipcg_ctx *c, ipcg_archive *a, int scalar, const int *k, void 
             uint32_t *merged = nullptr;
             CK(cudaMallocAsync((void **)&merged, std::max<uint64_t>(count, 1) * 4, st));
             const uint32_t *min = refine ? prev_sess->merged[li] : nullptr;
-            launch_merge(planes[li].as<uint32_t>(), stride[li], min, merged, count, p.p0, p.p1, st);
+            {
+                ProfScope ps("merge", st, count * 4 + (uint64_t)(p.p1 - p.p0) * ((count + 7) / 8));
+                launch_merge(planes[li].as<uint32_t>(), stride[li], min, merged, count, p.p0, p.p1, st);
+            }
             const uint8_t *ob = src_dev + p.ob_off;
             const uint64_t no = ix.records[li].outlier_count;
             if (no) launch_outlier_prefix(ob, no, scalar, count, napplied.as<uint64_t>() + li, st);
+            ProfScope psr("recon_pass", st, count * (uint64_t)(4 + 2 * w));
             for (const PassDesc &pd : G.level[li].passes) {
                 launch_recon_pass(state, scalar, ix.interp == 1, pd, ix.eb, merged, st);
                 if (no) launch_outlier_apply(state, scalar, pd, ob, napplied.as<uint64_t>() + li, no, st);
@@ -844,5 +868,49 @@ int ipcg_backend_encode(ipcg_ctx *c, const uint8_t *raw, int raw_on_device, uint
 }
 
 uint64_t ipcg_kernel_launches(const ipcg_ctx *) { return launch_counter(); }
+
+int ipcg_profile_enable(ipcg_ctx *c, int enable) {
+    return guarded(c, [&] {
+        CK(cudaStreamSynchronize(c->stream));
+        Profiler &p = profiler();
+        for (auto &r : p.recs) p.pool.push_back(r.a), p.pool.push_back(r.b);
+        p.recs.clear();
+        p.enabled = enable != 0;
+    });
+}
+
+// JSON object {family: [total_ms, scopes, algorithmic_bytes], ...}; clears the records
+int ipcg_profile_read(ipcg_ctx *c, char *json, uint64_t capacity) {
+    return guarded(c, [&] {
+        CK(cudaStreamSynchronize(c->stream));
+        Profiler &p = profiler();
+        std::vector<std::string> names;
+        std::vector<double> ms;
+        std::vector<uint64_t> cnt, bytes;
+        for (auto &r : p.recs) {
+            float t = 0.f;
+            CK(cudaEventElapsedTime(&t, r.a, r.b));
+            size_t i = 0;
+            while (i < names.size() && names[i] != r.name) ++i;
+            if (i == names.size()) names.push_back(r.name), ms.push_back(0), cnt.push_back(0), bytes.push_back(0);
+            ms[i] += t;
+            cnt[i] += 1;
+            bytes[i] += r.bytes;
+            p.pool.push_back(r.a);
+            p.pool.push_back(r.b);
+        }
+        p.recs.clear();
+        std::string out = "{";
+        for (size_t i = 0; i < names.size(); ++i) {
+            char buf[256];
+            std::snprintf(buf, sizeof buf, "%s\"%s\": [%.6f, %llu, %llu]", i ? ", " : "", names[i].c_str(), ms[i],
+                          (unsigned long long)cnt[i], (unsigned long long)bytes[i]);
+            out += buf;
+        }
+        out += "}";
+        if (out.size() + 1 > capacity) throw Error(EINVAL_, "profile buffer too small");
+        std::memcpy(json, out.c_str(), out.size() + 1);
+    });
+}
 
 }  // extern "C"

@@ -5,6 +5,7 @@
 
 #include <stdexcept>
 #include <string>
+#include <vector>
 
 namespace ipcg {
 
@@ -35,6 +36,48 @@ inline unsigned long long &launch_counter() {
         ++::ipcg::launch_counter();        \
         CK(cudaGetLastError());            \
     } while (0)
+
+// Optional per-kernel-family timing: CUDA events recorded on the launching stream
+// around each family (enabled by ipcg_profile_enable); read back by ipcg_profile_read.
+struct Profiler {
+    bool enabled = false;
+    struct Rec {
+        const char *name;
+        cudaEvent_t a, b;
+        uint64_t bytes;
+    };
+    std::vector<Rec> recs;
+    std::vector<cudaEvent_t> pool;
+    cudaEvent_t ev() {
+        if (pool.empty()) {
+            cudaEvent_t e;
+            cudaEventCreate(&e);
+            return e;
+        }
+        cudaEvent_t e = pool.back();
+        pool.pop_back();
+        return e;
+    }
+};
+inline Profiler &profiler() {
+    static Profiler p;
+    return p;
+}
+struct ProfScope {
+    int idx = -1;
+    cudaStream_t st;
+    ProfScope(const char *name, cudaStream_t s, uint64_t bytes = 0) : st(s) {
+        Profiler &p = profiler();
+        if (!p.enabled) return;
+        Profiler::Rec r{name, p.ev(), p.ev(), bytes};
+        cudaEventRecord(r.a, s);
+        p.recs.push_back(r);
+        idx = (int)p.recs.size() - 1;
+    }
+    ~ProfScope() {
+        if (idx >= 0) cudaEventRecord(profiler().recs[idx].b, st);
+    }
+};
 
 inline unsigned grid_for(uint64_t n, unsigned block, unsigned cap = 148u * 32u) {
     uint64_t g = (n + block - 1) / block;
