@@ -1,0 +1,388 @@
+#!/usr/bin/env python
+"""bench.py -- compress & progressive-retrieve throughput of the B200 IPComp hot path.
+
+One step = compress_field of the BASELINE.json workload (config 2: 512^3 float32 GRF,
+cubic, relative eb 1e-4) followed by its progressive retrieval chain: reconstruct at
+relative eb 1e-1, then refine to 1e-2, 1e-3, 1e-4 (pipeline.hpp:140,260,294).
+`value` = uncompressed GB/s of that cycle with the field and the archive resident in HBM
+(timed by CUDA events on the launching stream, max over ranks); `e2e` = the same cycle
+through the C-ABI with HOST buffers (pinned field in, archive out to host, retrieval from
+the host archive with host outputs), host<->device copies inside the timed region.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config C]
+
+Multi-GPU (torchrun): independent replicas, one field per rank ("replicas only", weak scaling).
+`--impl reference` times the reference's own CPU code (oracle/_ref, compiled from the
+reference sources) on a bounded sample of the same workload, rank 0 only.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+from paper_2502_04093_b200 import synth  # noqa: E402
+
+METRIC = "compress & progressive-retrieve GB/s (uncompressed) on 1 B200; % of HBM roofline"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", type=int, default=2)
+    ap.add_argument("--dims", default=None, help="override dims, e.g. 256x256x256 (parity/debug only)")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    return ap.parse_args()
+
+
+def measured_peak():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+class Clocks:
+    """nvidia-smi sampling DURING the timed region (B200_PROFILING.md clocks line)."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device = device
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+        return self
+
+    def __exit__(self, *a):
+        self.lines = []
+        if self.proc:
+            self.proc.terminate()
+            try:
+                out, _ = self.proc.communicate(timeout=5)
+            except Exception:
+                self.proc.kill()
+                out = ""
+            self.lines = [ln.split(",") for ln in out.strip().splitlines() if ln.strip()]
+
+    def summary(self):
+        sm, mx, reasons = [], 0.0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for f in getattr(self, "lines", []):
+            try:
+                sm.append(float(f[1]))
+                mx = max(mx, float(f[2]))
+                for i, nm in enumerate(names):
+                    if f[5 + i].strip().lower() == "active":
+                        reasons.add(nm)
+            except (ValueError, IndexError):
+                continue
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx or None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def dist_setup(gpus: int):
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if ws > 1:
+        import torch.distributed as dist
+
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        dist.init_process_group("nccl" if os.environ.get("BENCH_BACKEND", "nccl") == "nccl" else "gloo")
+    return ws, rank, local
+
+
+def max_over_ranks(x: float, ws: int, device=None) -> float:
+    if ws == 1:
+        return x
+    import torch
+    import torch.distributed as dist
+
+    t = torch.tensor([x], dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def barrier(ws: int):
+    if ws > 1:
+        import torch.distributed as dist
+
+        dist.barrier()
+
+
+def retrieval_targets(cfg: int):
+    return synth.CONFIGS[cfg]["retrieve"].get("rel", [1e-2])
+
+
+# ------------------------------------------------------------------ our arm
+def run_ours(args, ws, rank, local):
+    import torch
+
+    import paper_2502_04093_b200 as ipc
+
+    torch.cuda.set_device(local)
+    c = synth.CONFIGS[args.config]
+    dims = tuple(int(x) for x in args.dims.split("x")) if args.dims else c["dims"]
+    f = synth.make_field(args.config, seed=0, dims=dims, device=f"cuda:{local}")
+    eb = synth.abs_eb(f, c["rel_eb"])
+    n, w = f.size, f.itemsize
+    nbytes = n * w
+    ctx = ipc.Context(local)
+    stream = torch.cuda.current_stream()
+    ctx.set_stream(stream.cuda_stream)
+    ft = torch.from_numpy(f).to(f"cuda:{local}")
+    rels = retrieval_targets(args.config)
+
+    def step_device():
+        reader = ipc.compress_field(ft, dims, eb, c["interp"], ctx=ctx)
+        rng = reader.header().range
+        out = ipc.reconstruct_field(reader, ipc.plan_for_error(reader, rels[0] * rng), device=True)
+        for rel in rels[1:]:
+            out = ipc.refine_field(reader, out.session, out.values, ipc.plan_for_error(reader, rel * rng))
+        return reader, out
+
+    # correctness guard on the benchmarked workload itself: full-fidelity bound holds
+    reader, out = step_device()
+    err = float((out.values.double() - ft.double()).abs().max())
+    assert err <= eb, f"error bound violated: {err} > {eb}"
+    archive_bytes = reader.size()
+    del reader, out
+    for _ in range(max(0, args.warmup - 1)):
+        step_device()
+    torch.cuda.synchronize()
+    barrier(ws)
+    launches0 = ctx.kernel_launches()
+    with Clocks(local) as clk:
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(args.steps):
+            step_device()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        barrier(ws)
+    launches = ctx.kernel_launches() - launches0
+    ms = e0.elapsed_time(e1)
+    ms_max = max_over_ranks(ms, ws, f"cuda:{local}")
+    value = ws * nbytes * args.steps / (ms_max / 1e3) / 1e9
+
+    # component timings (device-resident) for the report
+    comp = {}
+    torch.cuda.synchronize()
+    t0 = torch.cuda.Event(enable_timing=True)
+    t1 = torch.cuda.Event(enable_timing=True)
+    t0.record(stream)
+    reader = ipc.compress_field(ft, dims, eb, c["interp"], ctx=ctx)
+    t1.record(stream)
+    torch.cuda.synchronize()
+    comp["compress_gbs"] = nbytes / (t0.elapsed_time(t1) / 1e3) / 1e9
+    rng = reader.header().range
+    fresh = {}
+    for rel in rels:
+        plan = ipc.plan_for_error(reader, rel * rng)
+        t0.record(stream)
+        out = ipc.reconstruct_field(reader, plan, device=True, keep_session=False)
+        t1.record(stream)
+        torch.cuda.synchronize()
+        fresh[str(rel)] = round(nbytes / (t0.elapsed_time(t1) / 1e3) / 1e9, 3)
+    comp["retrieve_gbs"] = fresh
+    comp["archive_bytes"] = archive_bytes
+    comp["compression_ratio"] = round(nbytes / archive_bytes, 3)
+
+    # roofline of the dominant kernel family, from CUDA events around each family
+    ctx.profile(True)
+    step_device()
+    prof = ctx.profile_read()
+    ctx.profile(False)
+    peak, peak_src = measured_peak()
+    top = max(prof.items(), key=lambda kv: kv[1]["ms"])
+    step_ms = sum(v["ms"] for v in prof.values())
+    achieved = top[1]["bytes"] / (top[1]["ms"] / 1e3) / 1e9 if top[1]["ms"] > 0 else 0.0
+    roofline = {"bound": "hbm", "kernel": top[0], "achieved": round(achieved, 2), "peak": peak,
+                "unit": "GB/s", "frac": round(achieved / peak, 5), "traffic": None,
+                "share_of_step": round(top[1]["ms"] / step_ms, 4) if step_ms else None,
+                "peak_source": peak_src,
+                "families_ms": {k: round(v["ms"], 3) for k, v in sorted(prof.items(), key=lambda kv: -kv[1]["ms"])}}
+
+    # e2e through the C-ABI with host buffers
+    e2e = None
+    if not args.no_e2e:
+        host_f = torch.from_numpy(f).pin_memory()
+        host_arch = torch.empty(archive_bytes + (1 << 20), dtype=torch.uint8).pin_memory()
+        host_out = torch.empty(n, dtype=ft.dtype).pin_memory()
+        h2d = d2h = 0
+
+        def step_host():
+            nonlocal h2d, d2h
+            r = ipc.compress_field(host_f, dims, eb, c["interp"], ctx=ctx)
+            size = r.size()
+            r.write_to(host_arch[:size])
+            del r
+            rh = ipc.ArchiveReader(host_arch[:size], ctx=ctx)
+            rng_ = rh.header().range
+            o = ipc.reconstruct_field(rh, ipc.plan_for_error(rh, rels[0] * rng_), out=host_out)
+            for rel in rels[1:]:
+                o = ipc.refine_field(rh, o.session, host_out, ipc.plan_for_error(rh, rel * rng_), out=host_out)
+            h2d = nbytes + rh.payload_bytes_read()
+            d2h = size + nbytes * len(rels)
+            return o
+
+        step_host()
+        torch.cuda.synchronize()
+        barrier(ws)
+        g0, g1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        g0.record(stream)
+        for _ in range(max(1, args.steps // 2)):
+            step_host()
+        g1.record(stream)
+        torch.cuda.synchronize()
+        ems = max_over_ranks(g0.elapsed_time(g1), ws, f"cuda:{local}") / max(1, args.steps // 2)
+        e2e = {"value": round(ws * nbytes / (ems / 1e3) / 1e9, 4), "unit": "GB/s",
+               "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h)}
+
+    cpu = None
+    if rank == 0 and not args.no_cpu_baseline:
+        cpu = cpu_baseline(args.config, f, dims, c)
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": round(value, 4), "unit": "GB/s", "n_gpus": ws, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": round(ms_max / args.steps, 3), "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f32" if w == 4 else "f64",
+            "data": "synthetic: seeded Gaussian random field P(k)~k^-11/3 by FFT synthesis, normalised to [0,1] "
+                    "(stands in for the paper's SDRBench fields)",
+            "config": {"workload": f"cfg{args.config}: {'x'.join(map(str, dims))} {np.dtype(f.dtype).name} "
+                                   f"{'cubic' if c['interp'] else 'linear'} rel eb {c['rel_eb']}; step = compress + "
+                                   f"progressive retrieve rel {rels[0]} then refine {rels[1:]}",
+                       "dims": list(dims), "rel_eb": c["rel_eb"], "abs_eb": eb,
+                       "l2": f"inputs {nbytes >> 20} MiB > 126 MB L2 (no flush needed)",
+                       "parallelism": f"replicas x{ws}"},
+            "e2e": e2e, "roofline": roofline, "cpu_baseline": cpu, "gpu_launches": int(launches),
+            "clocks": clk.summary(), "detail": comp,
+        }
+        print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------------ CPU reference
+def _sample(f, dims, frac_dims=(128, 256, 256)):
+    d = tuple(min(a, b) for a, b in zip(dims, frac_dims)) if len(dims) == 3 else dims
+    v = f.reshape(dims)[tuple(slice(0, x) for x in d)]
+    return np.ascontiguousarray(v).reshape(-1), d
+
+
+def reference_cycle(ref, v, d, c, eb, rels):
+    """compress + progressive retrieve chain with the reference's own CPU code."""
+    t0 = time.perf_counter()
+    arch = ref.compress(v, d, eb, c["interp"])
+    import oracle
+
+    info = oracle.load("oracle").info(arch)
+    rng = info.range
+    k = ref.plan_for_error(arch, rels[0] * rng)
+    vals, merged, _ = ref.reconstruct(arch, k, v.dtype, v.size)
+    for rel in rels[1:]:
+        k2 = ref.plan_for_error(arch, rel * rng)
+        vals, merged, _ = ref.refine(arch, k, merged, vals, k2)
+        k = k2
+    return time.perf_counter() - t0, len(arch)
+
+
+def cpu_baseline(cfg, f, dims, c):
+    try:
+        import oracle
+
+        ref = oracle.load("ref")
+        kind = "reference"
+    except Exception:
+        import oracle
+
+        ref = oracle.load("oracle")
+        kind = "port"
+    v, d = _sample(f, dims)
+    eb = synth.abs_eb(v, c["rel_eb"])
+    threads = int(os.environ.get("IPCOMP_THREADS", "0")) or min(os.cpu_count() or 1, 16)
+    t, _ = reference_cycle(ref, v, d, c, eb, retrieval_targets(cfg))
+    return {"value": round(v.nbytes / t / 1e9, 5), "unit": "GB/s", "cores": threads, "kind": kind,
+            "sample": f"compress + progressive retrieve chain of a {'x'.join(map(str, d))} sub-volume "
+                      f"({v.nbytes >> 20} MiB) of the same field, one run, {t:.1f} s"}
+
+
+def run_reference(args, ws, rank):
+    if rank != 0:
+        return
+    import oracle
+
+    c = synth.CONFIGS[args.config]
+    dims = tuple(int(x) for x in args.dims.split("x")) if args.dims else c["dims"]
+    try:
+        ref = oracle.load("ref")
+        kind = "reference"
+    except Exception:
+        ref = oracle.load("oracle")
+        kind = "port"
+    threads = os.cpu_count() or 1
+    os.environ["IPCOMP_THREADS"] = str(threads)
+    f = synth.make_field(args.config, seed=0, dims=dims, device="cpu")
+    v, d = _sample(f, dims)
+    eb = synth.abs_eb(v, c["rel_eb"])
+    rels = retrieval_targets(args.config)
+    for _ in range(args.warmup):
+        reference_cycle(ref, v, d, c, eb, rels)
+    times = []
+    for _ in range(args.steps):
+        t, _ = reference_cycle(ref, v, d, c, eb, rels)
+        times.append(t)
+    total = sum(times)
+    value = v.nbytes * args.steps / total / 1e9
+    sample = (f"each step: compress + progressive retrieve chain of a {'x'.join(map(str, d))} sub-volume "
+              f"({v.nbytes >> 20} MiB) of the cfg{args.config} field")
+    line = {"metric": METRIC, "value": round(value, 5), "unit": "GB/s", "n_gpus": ws, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": round(1e3 * total / args.steps, 3), "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f32" if f.itemsize == 4 else "f64",
+            "data": "synthetic", "impl": "reference",
+            "config": {"workload": f"cfg{args.config}: {'x'.join(map(str, dims))} (sampled)", "dims": list(dims)},
+            "cpu_baseline": {"value": round(value, 5), "unit": "GB/s", "cores": threads, "kind": kind,
+                             "sample": sample},
+            "e2e": {"value": round(value, 5), "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    args = parse()
+    ws, rank, local = dist_setup(args.gpus)
+    if args.impl == "reference":
+        run_reference(args, ws, rank)
+    else:
+        run_ours(args, ws, rank, local)
+    if ws > 1:
+        import torch.distributed as dist
+
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

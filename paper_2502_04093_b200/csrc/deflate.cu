@@ -679,9 +679,11 @@ void DeflateBatch::run(const uint8_t *in, uint64_t in_stride, int S, uint64_t n,
     Work w = carve(workspace, S, n);
     CK(cudaMemsetAsync(w.meta, 0, sizeof(StreamMeta) * S, st));
     if (n > 0) {
+        {
         ProfScope ps("deflate.scan", st, (uint64_t)S * n);
         k_scan<<<dim3(grid_for(n, 256, 256), S), 256, 0, st>>>(in, in_stride, n, w.meta);
         CKL();
+        }
     }
     k_select<<<1, 32, 0, st>>>(w.meta, S, n);
     CKL();
@@ -693,12 +695,17 @@ void DeflateBatch::run(const uint8_t *in, uint64_t in_stride, int S, uint64_t n,
             CK(cudaFuncSetAttribute(k_prevlinks, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
             attr = true;
         }
+        {
         ProfScope ps1("deflate.prevlinks", st, (uint64_t)S * n * 3);
         k_prevlinks<<<dim3((unsigned)((nblk + PL_WARPS - 1) / PL_WARPS), S), PL_WARPS * 32, smem, st>>>(in, in_stride, n, w.meta, w.prevd);
         CKL();
+        }
+        {
         ProfScope ps2("deflate.match", st, (uint64_t)S * n * 11);
         k_match<<<dim3(grid_for(n, 256, 4096), S), 256, 0, st>>>(in, in_stride, n, w.meta, w.prevd, w.rec);
         CKL();
+        }
+        {
         ProfScope ps3("deflate.parse", st, (uint64_t)S * n * 20);
         k_anchor<<<dim3((unsigned)w.nchunks, S), 256, 0, st>>>(n, w.meta, w.rec, w.nchunks, w.first_anchor);
         CKL();
@@ -711,16 +718,21 @@ void DeflateBatch::run(const uint8_t *in, uint64_t in_stride, int S, uint64_t n,
         CKL();
         k_emit_syms<<<dim3((unsigned)((w.nchunks + 127) / 128), S), 128, 0, st>>>(in, in_stride, n, w.meta, w.rec, w.nchunks, w.bnd, w.entry, w.symoff, w.syms, w.maxb, w.blk_top, w.blk_start);
         CKL();
+        }
+        {
         ProfScope ps4("deflate.blocks", st, (uint64_t)S * n * 4);
         k_plan<<<dim3((unsigned)w.maxb, S), 256, 0, st>>>(n, w.meta, w.syms, w.maxb, w.blk_top, w.blk_start, w.trees);
         CKL();
         k_layout<<<(S + 31) / 32, 32, 0, st>>>(n, w.meta, S, w.maxb, w.trees, w.blk_bitpos);
         CKL();
+        }
+        {
         ProfScope ps5("deflate.emit", st, (uint64_t)S * n * 4);
         k_zero_out<<<dim3(grid_for(n / 8 + 2, 256, 512), S), 256, 0, st>>>(n, w.meta, out, out_stride);
         CKL();
         k_emit<<<dim3((unsigned)w.maxb, S), 256, 0, st>>>(in, in_stride, n, w.meta, w.syms, w.maxb, w.blk_start, w.trees, w.blk_bitpos, out, out_stride);
         CKL();
+        }
     }
     k_results<<<(S + 31) / 32, 32, 0, st>>>(in, in_stride, n, w.meta, S, out, out_stride, res);
     CKL();

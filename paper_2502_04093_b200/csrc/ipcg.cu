@@ -243,13 +243,15 @@ ipcg_archive *compress_impl(ipcg_ctx *c, int scalar, const void *values, int on_
                 launch_quant_pass(vals, state.p, scalar, cubic, pd, eb, nb.as<uint32_t>(), &sd->lowor[li], sink, st);
         }
         // loss table (measure_loss_table): replay per dropped-digit count d
-        ProfScope psl("loss_table", st, lg.count * 4);
-        for (int d = 1; d <= 32; ++d)
-            for (const PassDesc &pd : lg.passes)
-                launch_loss_pass(nb.as<uint32_t>(), dev.as<double>(), pd, cubic, 2.0 * eb, d, &sd->lowor[li],
-                                 sd->raw[li], st);
-        for (const PassDesc &pd : lg.passes) launch_zero_pass(dev.as<double>(), pd, st);
-        launch_loss_finalize(sd->raw[li], &sd->lowor[li], sd->delta[li], st);
+        {
+            ProfScope psl("loss_table", st, lg.count * 4);
+            for (int d = 1; d <= 32; ++d)
+                for (const PassDesc &pd : lg.passes)
+                    launch_loss_pass(nb.as<uint32_t>(), dev.as<double>(), pd, cubic, 2.0 * eb, d, &sd->lowor[li],
+                                     sd->raw[li], st);
+            for (const PassDesc &pd : lg.passes) launch_zero_pass(dev.as<double>(), pd, st);
+            launch_loss_finalize(sd->raw[li], &sd->lowor[li], sd->delta[li], st);
+        }
         if (planes[li].p) CK(cudaMemsetAsync(planes[li].p, 0, 32 * plane_stride[li] * 4, st));
         {
             ProfScope ps("bitplanes", st, lg.count * 8);
@@ -630,10 +632,12 @@ void retrieve_impl(ipcg_ctx *c, ipcg_archive *a, int scalar, const int *k, void 
             const uint8_t *ob = src_dev + p.ob_off;
             const uint64_t no = ix.records[li].outlier_count;
             if (no) launch_outlier_prefix(ob, no, scalar, count, napplied.as<uint64_t>() + li, st);
-            ProfScope psr("recon_pass", st, count * (uint64_t)(4 + 2 * w));
-            for (const PassDesc &pd : G.level[li].passes) {
-                launch_recon_pass(state, scalar, ix.interp == 1, pd, ix.eb, merged, st);
-                if (no) launch_outlier_apply(state, scalar, pd, ob, napplied.as<uint64_t>() + li, no, st);
+            {
+                ProfScope psr("recon_pass", st, count * (uint64_t)(4 + 2 * w));
+                for (const PassDesc &pd : G.level[li].passes) {
+                    launch_recon_pass(state, scalar, ix.interp == 1, pd, ix.eb, merged, st);
+                    if (no) launch_outlier_apply(state, scalar, pd, ob, napplied.as<uint64_t>() + li, no, st);
+                }
             }
             if (level <= ix.progressive_levels) ns->merged[li] = merged;
             else CK(cudaFreeAsync(merged, st));
