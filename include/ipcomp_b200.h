@@ -112,6 +112,13 @@ int ipcg_backend_encode(ipcg_ctx *ctx, const uint8_t *raw, int raw_on_device, ui
                         uint64_t raw_stride, int count, uint8_t *backend, uint64_t *length, uint32_t *crc,
                         uint8_t *out_payload, uint64_t out_capacity);
 
+/* backend_decode (src/backend.cpp:55-65) for `count` blocks whose payloads are concatenated
+ * in host memory; outputs are concatenated (raw_bytes[i] each) into out.  status[i]:
+ * 0 ok, 1 "block checksum mismatch", 2 "deflate backend failed to decompress block",
+ * 3 "identity block has wrong length". */
+int ipcg_backend_decode(ipcg_ctx *ctx, const uint8_t *payloads, const uint64_t *payload_len, const uint8_t *backend,
+                        const uint32_t *crc, const uint64_t *raw_bytes, int count, uint8_t *out, int *status);
+
 /* number of kernels this context launched so far (evidence for bench.py) */
 uint64_t ipcg_kernel_launches(const ipcg_ctx *ctx);
 /* per-kernel-family CUDA-event timing on the launching stream (bench.py roofline) */

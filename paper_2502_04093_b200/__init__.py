@@ -98,6 +98,7 @@ def library() -> C.CDLL:
         "ipcg_backend_encode": (i32, [vp, vp, i32, u64, u64, i32, vp, vp, vp, vp, u64]),
         "ipcg_kernel_launches": (u64, [vp]),
         "ipcg_profile_enable": (i32, [vp, i32]),
+        "ipcg_backend_decode": (i32, [vp, vp, vp, vp, vp, vp, i32, vp, vp]),
         "ipcg_profile_read": (i32, [vp, C.c_char_p, u64]),
     }
     for name, (res, args) in sig.items():
@@ -115,7 +116,7 @@ EXPORTED_SYMBOLS = [
     "ipcg_session_create", "ipcg_session_levels", "ipcg_session_archive_crc", "ipcg_session_planes_loaded",
     "ipcg_session_count", "ipcg_session_merged", "ipcg_session_free", "ipcg_plan_for_error",
     "ipcg_plan_for_size", "ipcg_bound_for_plan", "ipcg_plan_payload_bytes", "ipcg_backend_encode",
-    "ipcg_kernel_launches", "ipcg_profile_enable", "ipcg_profile_read",
+    "ipcg_kernel_launches", "ipcg_profile_enable", "ipcg_profile_read", "ipcg_backend_decode",
 ]
 
 
@@ -489,4 +490,34 @@ def backend_encode(planes: np.ndarray, ctx: Context | None = None):
         L = int(ln[i])
         res.append((int(be[i]), out[o:o + L].tobytes(), int(cr[i])))
         o += L
+    return res
+
+
+DECODE_ERRORS = {1: "block checksum mismatch", 2: "deflate backend failed to decompress block",
+                 3: "identity block has wrong length"}
+
+
+def backend_decode(blocks, ctx: Context | None = None):
+    """backend_decode (backend.cpp:55-65) for a list of (backend, payload bytes, crc32, raw_bytes).
+    Returns a list of decoded byte strings, or raises RuntimeError with the reference's message."""
+    ctx = ctx or Context.default()
+    n = len(blocks)
+    payload = np.frombuffer(b"".join(b[1] for b in blocks) + b"\0", dtype=np.uint8)
+    plen = np.array([len(b[1]) for b in blocks], np.uint64)
+    be = np.array([b[0] for b in blocks], np.uint8)
+    crc = np.array([b[2] for b in blocks], np.uint32)
+    raw = np.array([b[3] for b in blocks], np.uint64)
+    out = np.empty(int(raw.sum()) + 1, np.uint8)
+    status = np.zeros(n, np.int32)
+    ctx.check(library().ipcg_backend_decode(ctx.h, C.c_void_p(payload.ctypes.data), C.c_void_p(plen.ctypes.data),
+                                            C.c_void_p(be.ctypes.data), C.c_void_p(crc.ctypes.data),
+                                            C.c_void_p(raw.ctypes.data), n, C.c_void_p(out.ctypes.data),
+                                            C.c_void_p(status.ctypes.data)))
+    res, o = [], 0
+    for i in range(n):
+        if status[i]:
+            res.append(RuntimeError(DECODE_ERRORS[int(status[i])]))
+        else:
+            res.append(out[o:o + int(raw[i])].tobytes())
+        o += int(raw[i])
     return res

@@ -1,35 +1,57 @@
-// inflate.cu -- GPU uncompress (RFC 1950/1951) for backend_decode
-// (proj/src/backend.cpp:24-30).  One warp per stream: the Huffman decode runs
-// warp-uniformly (every lane decodes the same symbol, so control flow never
-// diverges and table reads broadcast), lane 0 stores literals and the whole warp
-// performs match and stored-block copies.  Error behaviour follows zlib's
-// inflate/inflate_table: over-subscribed or incomplete codes, missing end-of-block,
-// distances too far back, bad header, Adler-32 mismatch and output-size mismatch
-// all fail the stream, as uncompress() would.
+// inflate.cu -- block-parallel GPU `uncompress` (RFC 1950/1951) for backend_decode
+// (proj/src/backend.cpp:24-30,55-65).
+//
+// A deflate stream is a chain of blocks whose boundaries are only known after
+// decoding.  To decode the blocks of one stream in parallel:
+//   1. scan     every bit offset of every stream for a *dynamic block header* that is
+//               valid the way zlib's inflate/inflate_table check it (complete code-length
+//               code, decodable length sequence, complete lit/len code with an end-of-block
+//               code, admissible distance code); hits go into a per-stream hash table.
+//   2. decode   every candidate block, one warp each (warp-uniform Huffman decode, tables
+//               in shared memory), to its end-of-block: symbols, end bit, output size.
+//   3. chain    one thread per stream walks the real block sequence from the zlib header:
+//               stored blocks are parsed in place, dynamic blocks are looked up among the
+//               candidates, fixed (and any unmatched) blocks are decoded on the spot.
+//   4. emit     one warp per real block writes literals and intra-block copies; bytes whose
+//               copy source lies in an earlier block get a pointer to that source instead.
+//   5. resolve  follow those pointers (they always point into earlier blocks) to bytes
+//               that hold values.
+//   6. check    Adler-32 trailer and exact output length, as uncompress() does.
+// Any stream that fails any zlib rule is reported, like uncompress() != Z_OK.
+#include <algorithm>
+#include <cstring>
+#include <vector>
+
 #include "inflate.cuh"
 
 namespace ipcg {
 
 namespace {
 
-constexpr int WARPS = 4;
 constexpr int FASTBITS = 9;
+constexpr int MAXSYM = 16400;  // symbols stored per candidate block (zlib blocks: <= 16383)
+constexpr int WARPS = 4;
 
-struct Huff {
-    uint16_t count[16];
-    uint16_t first[16];   // canonical first code per length
-    uint16_t offs[16];    // index of the first symbol of each length in sym[]
-    uint16_t sym[320];
-    uint16_t fast[1 << FASTBITS];  // (len << 12) | symbol, 0 = slow path
-    int max;
-};
-
+// ------------------------------------------------------------------ bit reader
 struct Bits {
     const uint8_t *src;
     uint64_t len, pos;  // next byte to load
     uint64_t buf;
     int cnt;
-    uint64_t used;      // bits consumed
+    uint64_t used;  // absolute bit position of the next unread bit
+    __device__ __forceinline__ void init(const uint8_t *s, uint64_t l, uint64_t bit) {
+        src = s;
+        len = l;
+        pos = bit >> 3;
+        buf = 0;
+        cnt = 0;
+        used = bit & ~7ull;
+        const int r = (int)(bit & 7);
+        if (r) {
+            refill();
+            drop(r);
+        }
+    }
     __device__ __forceinline__ void refill() {
         while (cnt <= 56) {
             const uint64_t b = pos < len ? src[pos] : 0u;
@@ -54,79 +76,47 @@ struct Bits {
         return v;
     }
     __device__ __forceinline__ bool overrun() const { return used > 8 * len; }
-    __device__ __forceinline__ void align() {
-        const int r = (int)(used & 7);
-        if (r) drop(8 - r);
-    }
-    __device__ __forceinline__ uint64_t byte_pos() const { return used >> 3; }
-    __device__ __forceinline__ void seek_byte(uint64_t p) {
-        pos = p;
-        buf = 0;
-        cnt = 0;
-        used = p * 8;
-    }
 };
 
-// inflate_table semantics: returns false on over-subscribed / disallowed incomplete sets.
-// type 0 = code lengths, 1 = literal/length, 2 = distance.  Runs on the whole warp.
-__device__ bool build(Huff &h, const uint8_t *lens, int n, int type, unsigned lane) {
-    __shared__ int ok_s[WARPS];
-    const unsigned w = threadIdx.x >> 5;
-    if (lane == 0) {
-        for (int i = 0; i < 16; ++i) h.count[i] = 0;
-        for (int i = 0; i < n; ++i) h.count[lens[i]]++;
-        int max = 15;
-        while (max >= 1 && h.count[max] == 0) --max;
-        h.max = max;
-        int left = 1;
-        bool ok = true;
-        for (int l = 1; l <= 15; ++l) {
-            left <<= 1;
-            left -= h.count[l];
-            if (left < 0) ok = false;
-        }
-        if (ok && max > 0 && left > 0 && (type == 0 || max != 1)) ok = false;
-        h.offs[1] = 0;
-        for (int l = 1; l < 15; ++l) h.offs[l + 1] = (uint16_t)(h.offs[l] + h.count[l]);
-        uint16_t code = 0;
-        h.count[0] = 0;
-        for (int l = 1; l <= 15; ++l) {
-            code = (uint16_t)((code + h.count[l - 1]) << 1);
-            h.first[l] = code;
-        }
-        uint16_t o[16];
-        for (int l = 0; l < 16; ++l) o[l] = h.offs[l];
-        for (int i = 0; i < n; ++i)
-            if (lens[i]) h.sym[o[lens[i]]++] = (uint16_t)i;
-        ok_s[w] = ok;
+__constant__ uint16_t kLBase[29] = {3, 4, 5, 6, 7, 8, 9, 10, 11, 13, 15, 17, 19, 23, 27, 31,
+                                    35, 43, 51, 59, 67, 83, 99, 115, 131, 163, 195, 227, 258};
+__constant__ uint8_t kLExt[29] = {0, 0, 0, 0, 0, 0, 0, 0, 1, 1, 1, 1, 2, 2, 2, 2, 3, 3, 3, 3, 4, 4, 4, 4, 5, 5, 5, 5, 0};
+__constant__ uint16_t kDBase[30] = {1, 2, 3, 4, 5, 7, 9, 13, 17, 25, 33, 49, 65, 97, 129, 193,
+                                    257, 385, 513, 769, 1025, 1537, 2049, 3073, 4097, 6145, 8193, 12289, 16385, 24577};
+__constant__ uint8_t kDExt[30] = {0, 0, 0, 0, 1, 1, 2, 2, 3, 3, 4, 4, 5, 5, 6, 6, 7, 7, 8, 8, 9, 9, 10, 10, 11, 11, 12, 12, 13, 13};
+__constant__ uint8_t kOrder[19] = {16, 17, 18, 0, 8, 7, 9, 6, 10, 5, 11, 4, 12, 3, 13, 2, 14, 1, 15};
+
+// ------------------------------------------------------------ canonical codes
+struct Canon {  // puff-style: count per length + symbols in canonical order
+    uint16_t count[16];
+    uint16_t sym[320];
+};
+
+// inflate_table's acceptance rule: no over-subscription; incomplete only when allowed
+// (never for code lengths; lit/len and dist only with a single 1-bit code).  max==0 is
+// accepted (zlib builds an all-invalid table).  type 0 = code lengths, 1 = lit/len, 2 = dist.
+__device__ bool canon_build(Canon &h, const uint8_t *lens, int n, int type) {
+    for (int i = 0; i < 16; ++i) h.count[i] = 0;
+    for (int i = 0; i < n; ++i) h.count[lens[i]]++;
+    h.count[0] = 0;
+    int max = 15;
+    while (max >= 1 && h.count[max] == 0) --max;
+    int left = 1;
+    for (int l = 1; l <= 15; ++l) {
+        left <<= 1;
+        left -= h.count[l];
+        if (left < 0) return false;
     }
-    __syncwarp();
-    for (int i = lane; i < (1 << FASTBITS); i += 32) h.fast[i] = 0;
-    __syncwarp();
-    // fill the fast table: symbol index t of length L has code first[L] + (t - offs[L])
-    int total = 0;
-    for (int l = 1; l <= 15; ++l) total += h.count[l];
-    for (int t = lane; t < total; t += 32) {
-        int L = 1;
-        while (L < 15 && !(t >= h.offs[L] && t < h.offs[L] + h.count[L])) ++L;
-        if (L > FASTBITS) continue;
-        const uint32_t code = h.first[L] + (uint32_t)(t - h.offs[L]);
-        const uint32_t rev = __brev(code) >> (32 - L);
-        for (uint32_t e = 0; e < (1u << (FASTBITS - L)); ++e)
-            h.fast[rev | (e << L)] = (uint16_t)((L << 12) | h.sym[t]);
-    }
-    __syncwarp();
-    return ok_s[w] != 0;
+    if (max > 0 && left > 0 && (type == 0 || max != 1)) return false;
+    uint16_t offs[16];
+    offs[1] = 0;
+    for (int l = 1; l < 15; ++l) offs[l + 1] = (uint16_t)(offs[l] + h.count[l]);
+    for (int i = 0; i < n; ++i)
+        if (lens[i]) h.sym[offs[lens[i]]++] = (uint16_t)i;
+    return true;
 }
 
-// returns symbol or -1 (invalid code)
-__device__ __forceinline__ int decode(const Huff &h, Bits &b) {
-    const uint32_t e = h.fast[b.peek(FASTBITS)];
-    if (e) {
-        b.drop((int)(e >> 12));
-        return (int)(e & 0xfff);
-    }
-    // canonical slow path (puff)
+__device__ __forceinline__ int canon_decode(const Canon &h, Bits &b) {
     int code = 0, first = 0, index = 0;
     for (int len = 1; len <= 15; ++len) {
         code |= (int)b.get(1);
@@ -140,213 +130,709 @@ __device__ __forceinline__ int decode(const Huff &h, Bits &b) {
     return -1;
 }
 
-__constant__ uint16_t kLBase[29] = {3, 4, 5, 6, 7, 8, 9, 10, 11, 13, 15, 17, 19, 23, 27, 31,
-                                    35, 43, 51, 59, 67, 83, 99, 115, 131, 163, 195, 227, 258};
-__constant__ uint8_t kLExt[29] = {0, 0, 0, 0, 0, 0, 0, 0, 1, 1, 1, 1, 2, 2, 2, 2, 3, 3, 3, 3, 4, 4, 4, 4, 5, 5, 5, 5, 0};
-__constant__ uint16_t kDBase[30] = {1, 2, 3, 4, 5, 7, 9, 13, 17, 25, 33, 49, 65, 97, 129, 193,
-                                    257, 385, 513, 769, 1025, 1537, 2049, 3073, 4097, 6145, 8193, 12289, 16385, 24577};
-__constant__ uint8_t kDExt[30] = {0, 0, 0, 0, 1, 1, 2, 2, 3, 3, 4, 4, 5, 5, 6, 6, 7, 7, 8, 8, 9, 9, 10, 10, 11, 11, 12, 12, 13, 13};
-__constant__ uint8_t kOrder[19] = {16, 17, 18, 0, 8, 7, 9, 6, 10, 5, 11, 4, 12, 3, 13, 2, 14, 1, 15};
+// read a dynamic header at the bit reader's position into lens (lit/len then dist);
+// returns false on any zlib rejection.  Leaves b after the header.
+__device__ bool read_dynamic_header(Bits &b, uint8_t *lens, int &nlen, int &ndist, Canon &scratch) {
+    nlen = (int)b.get(5) + 257;
+    ndist = (int)b.get(5) + 1;
+    const int ncode = (int)b.get(4) + 4;
+    if (nlen > 286 || ndist > 30) return false;
+    uint8_t cll[19];
+    for (int i = 0; i < 19; ++i) cll[i] = 0;
+    for (int i = 0; i < ncode; ++i) cll[kOrder[i]] = (uint8_t)b.get(3);
+    if (!canon_build(scratch, cll, 19, 0)) return false;
+    int idx = 0;
+    uint8_t prev = 0;
+    while (idx < nlen + ndist) {
+        const int sym = canon_decode(scratch, b);
+        if (sym < 0) return false;
+        if (sym < 16) {
+            lens[idx++] = (uint8_t)sym;
+            prev = (uint8_t)sym;
+            continue;
+        }
+        int rep;
+        uint8_t v = 0;
+        if (sym == 16) {
+            if (idx == 0) return false;
+            v = prev;
+            rep = 3 + (int)b.get(2);
+        } else if (sym == 17) {
+            rep = 3 + (int)b.get(3);
+        } else {
+            rep = 11 + (int)b.get(7);
+        }
+        if (idx + rep > nlen + ndist) return false;
+        for (int r = 0; r < rep; ++r) lens[idx + r] = v;
+        prev = v;
+        idx += rep;
+    }
+    if (lens[256] == 0) return false;
+    if (b.overrun()) return false;
+    return true;
+}
 
-__global__ void __launch_bounds__(WARPS * 32) k_inflate(const InflateJob *jobs, int count, int *status) {
-    __shared__ Huff lit_s[WARPS], dist_s[WARPS], cl_s[WARPS];
+// ----------------------------------------------------------- fast warp tables
+struct Huff {
+    uint16_t count[16];
+    uint16_t first[16];
+    uint16_t offs[16];
+    uint16_t sym[320];
+    uint16_t fast[1 << FASTBITS];  // (len << 12) | symbol, 0 = slow path
+};
+
+// build from lengths on the whole warp (lengths already validated)
+__device__ void huff_build(Huff &h, const uint8_t *lens, int n, unsigned lane) {
+    if (lane == 0) {
+        for (int i = 0; i < 16; ++i) h.count[i] = 0;
+        for (int i = 0; i < n; ++i) h.count[lens[i]]++;
+        h.count[0] = 0;
+        h.offs[1] = 0;
+        for (int l = 1; l < 15; ++l) h.offs[l + 1] = (uint16_t)(h.offs[l] + h.count[l]);
+        uint16_t code = 0;
+        for (int l = 1; l <= 15; ++l) {
+            code = (uint16_t)((code + h.count[l - 1]) << 1);
+            h.first[l] = code;
+        }
+        uint16_t o[16];
+        for (int l = 0; l < 16; ++l) o[l] = h.offs[l];
+        for (int i = 0; i < n; ++i)
+            if (lens[i]) h.sym[o[lens[i]]++] = (uint16_t)i;
+    }
+    __syncwarp();
+    for (int i = lane; i < (1 << FASTBITS); i += 32) h.fast[i] = 0;
+    __syncwarp();
+    int total = 0;
+    for (int l = 1; l <= 15; ++l) total += h.count[l];
+    for (int t = lane; t < total; t += 32) {
+        int L = 1;
+        while (L < 15 && !(t >= h.offs[L] && t < h.offs[L] + h.count[L])) ++L;
+        if (L > FASTBITS) continue;
+        const uint32_t code = h.first[L] + (uint32_t)(t - h.offs[L]);
+        const uint32_t rev = __brev(code) >> (32 - L);
+        for (uint32_t e = 0; e < (1u << (FASTBITS - L)); ++e) h.fast[rev | (e << L)] = (uint16_t)((L << 12) | h.sym[t]);
+    }
+    __syncwarp();
+}
+
+__device__ __forceinline__ int huff_decode(const Huff &h, Bits &b) {
+    const uint32_t e = h.fast[b.peek(FASTBITS)];
+    if (e) {
+        b.drop((int)(e >> 12));
+        return (int)(e & 0xfff);
+    }
+    int code = 0, first = 0, index = 0;
+    for (int len = 1; len <= 15; ++len) {
+        code |= (int)b.get(1);
+        const int count = h.count[len];
+        if (code - count < first) return h.sym[index + (code - first)];
+        index += count;
+        first += count;
+        first <<= 1;
+        code <<= 1;
+    }
+    return -1;
+}
+
+// symbol words: literal = byte; match = 1<<31 | len << 16 | dist  (len <= 258, dist <= 32768)
+__device__ __forceinline__ uint32_t sym_lit(uint32_t c) { return c; }
+__device__ __forceinline__ uint32_t sym_match(uint32_t len, uint32_t dist) {
+    return 0x80000000u | (len << 16) | (dist - 1);
+}
+
+// ------------------------------------------------------------------ state
+struct JobMeta {
+    int status;          // 0 ok, 1 error
+    int overflow;        // candidate table overflowed -> chain uses the slow path
+    uint32_t adler_want;
+    uint32_t nblocks;
+    unsigned long long ncand;
+};
+
+struct Cand {
+    uint64_t hdr_bit;
+    uint64_t end_bit;
+    uint64_t out_bytes;
+    uint32_t nsyms;
+    int job;
+    int ok;
+};
+
+struct Blk {
+    int type;        // 0 stored, 1 symbols (candidate or fallback)
+    uint32_t nsyms;
+    uint64_t src;    // stored: byte offset in src;  symbols: index into the symbol pool
+    uint64_t out_off;
+    uint64_t out_len;
+};
+
+struct Tables {  // per-job device pointers
+    unsigned long long *hash;  // key = bit+1 (high 40) | cand index (low 24) ... stored as two arrays
+    uint32_t *hval;
+    uint64_t hcap;
+    Blk *blocks;
+    uint64_t bcap;
+    uint32_t *fallback;  // symbols decoded by the chain itself
+    uint64_t fcap;
+    uint32_t *flags;     // unresolved-byte bitmap
+    uint32_t *ptr;       // source pointer of unresolved bytes
+};
+
+__device__ __forceinline__ uint64_t hslot(uint64_t key, uint64_t cap) {
+    key ^= key >> 33;
+    key *= 0xff51afd7ed558ccdull;
+    key ^= key >> 33;
+    return key & (cap - 1);
+}
+
+// ------------------------------------------------------------------ 1. scan
+__device__ __forceinline__ uint64_t load_le64(const uint8_t *p, uint64_t len, uint64_t byte) {
+    uint64_t v = 0;
+    if (byte + 8 <= len) {
+#pragma unroll
+        for (int i = 0; i < 8; ++i) v |= (uint64_t)p[byte + i] << (8 * i);
+    } else {
+        for (int i = 0; i < 8; ++i)
+            if (byte + i < len) v |= (uint64_t)p[byte + i] << (8 * i);
+    }
+    return v;
+}
+
+__global__ void __launch_bounds__(256) k_scan(const InflateJob *jobs, const Tables *tabs, JobMeta *meta,
+                                             Cand *cands, unsigned long long *ncand_total, uint64_t cand_cap) {
+    const int j = blockIdx.y;
+    const InflateJob job = jobs[j];
+    const uint64_t nbits = job.src_len * 8;
+    const Tables T = tabs[j];
+    for (uint64_t byte = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; byte * 8 < nbits;
+         byte += (uint64_t)gridDim.x * blockDim.x) {
+        if (byte < 2) continue;  // zlib header
+        const uint64_t w0 = load_le64(job.src, job.src_len, byte);
+        const uint64_t w1 = load_le64(job.src, job.src_len, byte + 8);
+        for (int k = 0; k < 8; ++k) {
+            const uint64_t lo = k ? (w0 >> k) | (w1 << (64 - k)) : w0;
+            // BFINAL(1) BTYPE(2)=2 HLIT(5)<=29 HDIST(5)<=29 HCLEN(4)
+            if (((lo >> 1) & 3) != 2) continue;
+            const uint32_t hlit = (uint32_t)(lo >> 3) & 31, hdist = (uint32_t)(lo >> 8) & 31;
+            if (hlit > 29 || hdist > 29) continue;
+            const int ncode = (int)((lo >> 13) & 15) + 4;
+            // code-length code must be complete (Kraft sum == 128 at max length 7)
+            const uint64_t hi = k ? (w1 >> k) : w1;  // bits 64.. of the window start
+            uint32_t kraft = 0;
+            bool over = false;
+            for (int i = 0; i < ncode; ++i) {
+                const int bp = 17 + 3 * i;
+                uint32_t l;
+                if (bp + 3 <= 64) l = (uint32_t)(lo >> bp) & 7;
+                else if (bp >= 64) l = (uint32_t)(hi >> (bp - 64)) & 7;
+                else l = (uint32_t)((lo >> bp) | (hi << (64 - bp))) & 7;
+                if (l) kraft += 128u >> l;
+                if (kraft > 128) {
+                    over = true;
+                    break;
+                }
+            }
+            if (over || kraft != 128) continue;
+            // full validation (rare)
+            const uint64_t bit = byte * 8 + (uint64_t)k;
+            Bits b;
+            b.init(job.src, job.src_len, bit + 3);
+            uint8_t lens[320];
+            Canon cs;
+            int nlen, ndist;
+            if (!read_dynamic_header(b, lens, nlen, ndist, cs)) continue;
+            Canon cl;
+            if (!canon_build(cl, lens, nlen, 1) || !canon_build(cl, lens + nlen, ndist, 2)) continue;
+            const unsigned long long ci = atomicAdd(ncand_total, 1ull);
+            if (ci >= cand_cap) {
+                meta[j].overflow = 1;
+                continue;
+            }
+            Cand c;
+            c.hdr_bit = bit;
+            c.end_bit = 0;
+            c.out_bytes = 0;
+            c.nsyms = 0;
+            c.job = j;
+            c.ok = 0;
+            cands[ci] = c;
+            // insert into the job's hash table
+            const unsigned long long key = bit + 1;
+            uint64_t s = hslot(key, T.hcap);
+            bool placed = false;
+            for (uint64_t probe = 0; probe < T.hcap; ++probe, s = (s + 1) & (T.hcap - 1)) {
+                const unsigned long long prev = atomicCAS(&T.hash[s], 0ull, key);
+                if (prev == 0ull || prev == key) {
+                    T.hval[s] = (uint32_t)ci;
+                    placed = true;
+                    break;
+                }
+            }
+            if (!placed) meta[j].overflow = 1;
+        }
+    }
+}
+
+// ------------------------------------------------------------ 2. candidates
+__global__ void __launch_bounds__(WARPS * 32) k_decode_cands(const InflateJob *jobs, Cand *cands,
+                                                           const unsigned long long *ncand_total, uint64_t cand_cap,
+                                                           uint32_t *pool) {
+    __shared__ Huff lit_s[WARPS], dist_s[WARPS];
     __shared__ uint8_t lens_s[WARPS][320];
     const unsigned w = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int jid = blockIdx.x * WARPS + (int)w;
-    if (jid >= count) return;
-    const InflateJob job = jobs[jid];
-    Huff &lit = lit_s[w], &dist = dist_s[w], &cl = cl_s[w];
-    uint8_t *lens = lens_s[w];
-    Bits b{job.src, job.src_len, 0, 0, 0, 0};
-    uint8_t *dst = job.dst;
-    const uint64_t outcap = job.dst_len;
-    uint64_t out = 0;
+    const uint64_t n = min((unsigned long long)cand_cap, *ncand_total);
+    for (uint64_t ci = blockIdx.x * (uint64_t)WARPS + w; ci < n; ci += (uint64_t)gridDim.x * WARPS) {
+        Cand &c = cands[ci];
+        const InflateJob job = jobs[c.job];
+        Bits b;
+        b.init(job.src, job.src_len, c.hdr_bit + 3);
+        int nlen = 0, ndist = 0;
+        uint8_t lens[320];
+        Canon cs;
+        const bool ok = read_dynamic_header(b, lens, nlen, ndist, cs);  // identical on every lane
+        if (!ok) {
+            if (lane == 0) c.ok = 0;
+            continue;
+        }
+        if (lane == 0)
+            for (int i = 0; i < nlen + ndist; ++i) lens_s[w][i] = lens[i];
+        __syncwarp();
+        huff_build(lit_s[w], lens_s[w], nlen, lane);
+        huff_build(dist_s[w], lens_s[w] + nlen, ndist, lane);
+        uint32_t *out = pool + ci * (uint64_t)MAXSYM;
+        uint32_t ns = 0;
+        uint64_t bytes = 0;
+        bool good = true;
+        for (;;) {
+            const int sym = huff_decode(lit_s[w], b);
+            if (sym < 0 || b.overrun()) {
+                good = false;
+                break;
+            }
+            if (sym == 256) break;
+            if (ns >= MAXSYM) {
+                good = false;
+                break;
+            }
+            if (sym < 256) {
+                if (lane == 0) out[ns] = sym_lit((uint32_t)sym);
+                ++ns;
+                ++bytes;
+                continue;
+            }
+            const int li = sym - 257;
+            if (li >= 29) {
+                good = false;
+                break;
+            }
+            const uint32_t len = kLBase[li] + b.get(kLExt[li]);
+            const int ds = huff_decode(dist_s[w], b);
+            if (ds < 0 || ds >= 30) {
+                good = false;
+                break;
+            }
+            const uint32_t d = kDBase[ds] + b.get(kDExt[ds]);
+            if (lane == 0) out[ns] = sym_match(len, d);
+            ++ns;
+            bytes += len;
+        }
+        if (b.overrun()) good = false;
+        if (lane == 0) {
+            c.ok = good ? 1 : 0;
+            c.end_bit = b.used;
+            c.nsyms = ns;
+            c.out_bytes = bytes;
+        }
+        __syncwarp();
+    }
+}
+
+// ------------------------------------------------------------------- 3. chain
+// decode one block at `b` into fallback symbols (slow path, one thread)
+__device__ bool chain_decode_block(Bits &b, int type, uint32_t *fb, uint64_t fcap, uint64_t &fused, uint32_t &nsyms,
+                                   uint64_t &bytes) {
+    uint8_t lens[320];
+    Canon lit, dist, cs;
+    int nlen, ndist;
+    if (type == 1) {
+        for (int i = 0; i < 144; ++i) lens[i] = 8;
+        for (int i = 144; i < 256; ++i) lens[i] = 9;
+        for (int i = 256; i < 280; ++i) lens[i] = 7;
+        for (int i = 280; i < 288; ++i) lens[i] = 8;
+        for (int i = 0; i < 30; ++i) lens[288 + i] = 5;
+        nlen = 288;
+        ndist = 30;
+    } else {
+        if (!read_dynamic_header(b, lens, nlen, ndist, cs)) return false;
+    }
+    if (!canon_build(lit, lens, nlen, 1) || !canon_build(dist, lens + nlen, ndist, 2)) return false;
+    nsyms = 0;
+    bytes = 0;
+    for (;;) {
+        const int sym = canon_decode(lit, b);
+        if (sym < 0 || b.overrun()) return false;
+        if (sym == 256) return true;
+        if (fused >= fcap) return false;
+        if (sym < 256) {
+            fb[fused++] = sym_lit((uint32_t)sym);
+            ++nsyms;
+            ++bytes;
+            continue;
+        }
+        const int li = sym - 257;
+        if (li >= 29) return false;
+        const uint32_t len = kLBase[li] + b.get(kLExt[li]);
+        const int ds = canon_decode(dist, b);
+        if (ds < 0 || ds >= 30) return false;
+        const uint32_t d = kDBase[ds] + b.get(kDExt[ds]);
+        fb[fused++] = sym_match(len, d);
+        ++nsyms;
+        bytes += len;
+    }
+}
+
+__global__ void k_chain(const InflateJob *jobs, int njobs, const Tables *tabs, JobMeta *meta, const Cand *cands) {
+    const int j = blockIdx.x * blockDim.x + threadIdx.x;
+    if (j >= njobs) return;
+    const InflateJob job = jobs[j];
+    const Tables T = tabs[j];
+    JobMeta &m = meta[j];
     bool err = false;
-    // zlib header (inflate.c HEAD state)
-    {
-        const uint32_t cmf = b.get(8), flg = b.get(8);
+    uint64_t out = 0, nb = 0, fused = 0;
+    if (job.src_len < 2) err = true;
+    if (!err) {
+        const uint32_t cmf = job.src[0], flg = job.src[1];
         if (((cmf << 8) | flg) % 31 != 0 || (cmf & 15) != 8 || (cmf >> 4) + 8 > 15 || (flg & 0x20)) err = true;
     }
+    uint64_t e = 16;
     int last = 0;
     while (!err && !last) {
+        Bits b;
+        b.init(job.src, job.src_len, e);
         last = (int)b.get(1);
         const uint32_t type = b.get(2);
+        if (nb >= T.bcap) {
+            err = true;
+            break;
+        }
+        Blk blk;
+        blk.out_off = out;
         if (type == 0) {
-            b.align();
-            const uint64_t bp = b.byte_pos();
-            b.seek_byte(bp);
+            const uint64_t bp = (b.used + 7) >> 3;
             if (bp + 4 > job.src_len) {
                 err = true;
                 break;
             }
             const uint32_t L = job.src[bp] | (job.src[bp + 1] << 8), NL = job.src[bp + 2] | (job.src[bp + 3] << 8);
-            if (L != (~NL & 0xffff) || bp + 4 + L > job.src_len || out + L > outcap) {
+            if (L != (~NL & 0xffff) || bp + 4 + L > job.src_len) {
                 err = true;
                 break;
             }
-            for (uint32_t i = lane; i < L; i += 32) dst[out + i] = job.src[bp + 4 + i];
-            out += L;
-            b.seek_byte(bp + 4 + L);
-            continue;
-        }
-        if (type == 3) {
+            blk.type = 0;
+            blk.src = bp + 4;
+            blk.out_len = L;
+            blk.nsyms = 0;
+            e = (bp + 4 + L) * 8;
+        } else if (type == 3) {
             err = true;
             break;
-        }
-        if (type == 1) {
-            if (lane == 0) {
-                for (int i = 0; i < 144; ++i) lens[i] = 8;
-                for (int i = 144; i < 256; ++i) lens[i] = 9;
-                for (int i = 256; i < 280; ++i) lens[i] = 7;
-                for (int i = 280; i < 288; ++i) lens[i] = 8;
-                for (int i = 0; i < 30; ++i) lens[288 + i] = 5;
-            }
-            __syncwarp();
-            build(lit, lens, 288, 1, lane);
-            build(dist, lens + 288, 30, 2, lane);
         } else {
-            const int nlen = (int)b.get(5) + 257, ndist = (int)b.get(5) + 1, ncode = (int)b.get(4) + 4;
-            if (nlen > 286 || ndist > 30) {
-                err = true;
-                break;
-            }
-            uint8_t cll[19];
-            for (int i = 0; i < 19; ++i) cll[i] = 0;
-            for (int i = 0; i < ncode; ++i) cll[kOrder[i]] = (uint8_t)b.get(3);
-            if (lane == 0)
-                for (int i = 0; i < 19; ++i) lens[i] = cll[i];
-            __syncwarp();
-            if (!build(cl, lens, 19, 0, lane)) {
-                err = true;
-                break;
-            }
-            uint8_t *ll = lens;  // reuse: cl table already built from lens[0..18]
-            __syncwarp();
-            int idx = 0;
-            uint8_t prev = 0;
-            bool bad = false;
-            while (idx < nlen + ndist) {
-                const int sym = decode(cl, b);
-                if (sym < 0) {
-                    bad = true;
-                    break;
-                }
-                if (sym < 16) {
-                    if (lane == 0) ll[idx] = (uint8_t)sym;
-                    prev = (uint8_t)sym;
-                    ++idx;
-                    continue;
-                }
-                int rep;
-                uint8_t v = 0;
-                if (sym == 16) {
-                    if (idx == 0) {
-                        bad = true;
+            bool found = false;
+            if (type == 2 && !m.overflow) {
+                const unsigned long long key = e + 1;
+                uint64_t s = hslot(key, T.hcap);
+                for (uint64_t probe = 0; probe < T.hcap; ++probe, s = (s + 1) & (T.hcap - 1)) {
+                    const unsigned long long k = T.hash[s];
+                    if (k == 0ull) break;
+                    if (k == key) {
+                        const Cand &c = cands[T.hval[s]];
+                        if (c.ok) {
+                            blk.type = 1;
+                            blk.src = (uint64_t)T.hval[s] * MAXSYM;
+                            blk.nsyms = c.nsyms;
+                            blk.out_len = c.out_bytes;
+                            e = c.end_bit;
+                            found = true;
+                        }
                         break;
                     }
-                    v = prev;
-                    rep = 3 + (int)b.get(2);
-                } else if (sym == 17) {
-                    rep = 3 + (int)b.get(3);
-                } else {
-                    rep = 11 + (int)b.get(7);
                 }
-                if (idx + rep > nlen + ndist) {
-                    bad = true;
-                    break;
-                }
-                if (lane == 0)
-                    for (int r = 0; r < rep; ++r) ll[idx + r] = v;
-                prev = v;
-                idx += rep;
             }
-            __syncwarp();
-            if (bad || ll[256] == 0) {
-                err = true;
-                break;
-            }
-            if (!build(lit, ll, nlen, 1, lane) || !build(dist, ll + nlen, ndist, 2, lane)) {
-                err = true;
-                break;
-            }
-        }
-        // symbols
-        for (;;) {
-            const int sym = decode(lit, b);
-            if (sym < 0 || b.overrun()) {
-                err = true;
-                break;
-            }
-            if (sym < 256) {
-                if (out >= outcap) {
+            if (!found) {
+                uint32_t ns;
+                uint64_t bytes;
+                const uint64_t f0 = fused;
+                if (!chain_decode_block(b, (int)type, T.fallback, T.fcap, fused, ns, bytes)) {
                     err = true;
                     break;
                 }
-                if (lane == 0) dst[out] = (uint8_t)sym;
-                ++out;
-                continue;
+                blk.type = 2;  // symbols in the job's fallback buffer
+                blk.src = f0;
+                blk.nsyms = ns;
+                blk.out_len = bytes;
+                e = b.used;
             }
-            if (sym == 256) break;
-            const int li = sym - 257;
-            if (li >= 29) {
-                err = true;
-                break;
-            }
-            const uint32_t len = kLBase[li] + b.get(kLExt[li]);
-            const int ds = decode(dist, b);
-            if (ds < 0 || ds >= 30) {
-                err = true;
-                break;
-            }
-            const uint32_t d = kDBase[ds] + b.get(kDExt[ds]);
-            if (d > out || out + len > outcap) {
-                err = true;
-                break;
-            }
-            __syncwarp();
-            if (d >= len) {
-                for (uint32_t i = lane; i < len; i += 32) dst[out + i] = dst[out - d + i];
-            } else {
-                for (uint32_t i = lane; i < len; i += 32) dst[out + i] = dst[out - d + (i % d)];
-            }
-            __syncwarp();
-            out += len;
         }
-        if (b.overrun()) err = true;
+        out += blk.out_len;
+        if (out > job.dst_len) {
+            err = true;
+            break;
+        }
+        T.blocks[nb++] = blk;
     }
     if (!err) {
-        b.align();
-        const uint64_t bp = b.byte_pos();
-        if (bp + 4 > job.src_len || out != outcap) {
-            err = true;
-        } else {
-            const uint32_t want = ((uint32_t)job.src[bp] << 24) | ((uint32_t)job.src[bp + 1] << 16) |
-                                  ((uint32_t)job.src[bp + 2] << 8) | job.src[bp + 3];
-            __syncwarp();
-            unsigned long long A = 0, B = 0;
-            for (uint64_t i = lane; i < out; i += 32) {
-                const uint32_t v = dst[i];
-                A += v;
-                B += (unsigned long long)((out - i) % 65521u) * v;
+        const uint64_t bp = (e + 7) >> 3;
+        if (bp + 4 > job.src_len || out != job.dst_len) err = true;
+        else
+            m.adler_want = ((uint32_t)job.src[bp] << 24) | ((uint32_t)job.src[bp + 1] << 16) |
+                           ((uint32_t)job.src[bp + 2] << 8) | job.src[bp + 3];
+    }
+    m.nblocks = err ? 0 : (uint32_t)nb;
+    if (err) m.status = 1;
+}
+
+// -------------------------------------------------------------------- 4. emit
+__device__ __forceinline__ bool flag_get(const uint32_t *f, uint64_t i) { return (f[i >> 5] >> (i & 31)) & 1u; }
+
+__global__ void __launch_bounds__(WARPS * 32) k_emit(const InflateJob *jobs, const Tables *tabs, const JobMeta *meta,
+                                                   const uint32_t *pool) {
+    const int j = blockIdx.y;
+    const JobMeta &m = meta[j];
+    if (m.status) return;
+    const unsigned w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint64_t bi = (uint64_t)blockIdx.x * WARPS + w;
+    if (bi >= m.nblocks) return;
+    const InflateJob job = jobs[j];
+    const Tables T = tabs[j];
+    const Blk blk = T.blocks[bi];
+    uint8_t *dst = job.dst;
+    const uint64_t b0 = blk.out_off;
+    if (blk.type == 0) {
+        for (uint64_t i = lane; i < blk.out_len; i += 32) dst[b0 + i] = job.src[blk.src + i];
+        return;
+    }
+    const uint32_t *syms = blk.type == 1 ? pool + blk.src : T.fallback + blk.src;
+    uint64_t o = b0;
+    for (uint32_t s = 0; s < blk.nsyms; ++s) {
+        const uint32_t v = syms[s];
+        if (!(v & 0x80000000u)) {
+            if (lane == 0) dst[o] = (uint8_t)v;
+            ++o;
+            continue;
+        }
+        const uint32_t len = (v >> 16) & 0x1ff, d = (v & 0xffff) + 1;
+        __syncwarp();
+        for (uint32_t i = lane; i < len; i += 32) {
+            const uint64_t src = o - d + (d < len ? (i % d) : i);
+            const uint64_t t = o + i;
+            if (src >= b0) {
+                if (flag_get(T.flags, src)) {
+                    T.ptr[t] = T.ptr[src];
+                    atomicOr(&T.flags[t >> 5], 1u << (t & 31));
+                } else {
+                    dst[t] = dst[src];
+                }
+            } else {
+                T.ptr[t] = (uint32_t)src;
+                atomicOr(&T.flags[t >> 5], 1u << (t & 31));
             }
-            B %= 65521u;
-            for (int o = 16; o > 0; o >>= 1) {
-                A += __shfl_down_sync(0xffffffffu, A, o);
-                B += __shfl_down_sync(0xffffffffu, B, o);
-            }
-            const uint32_t a = (uint32_t)((1 + A) % 65521u), bb = (uint32_t)((B + out) % 65521u);
-            if (((bb << 16) | a) != want) err = true;
+        }
+        __syncwarp();
+        o += len;
+    }
+}
+
+// ------------------------------------------------------------------ 5. resolve
+__global__ void k_resolve(const InflateJob *jobs, const Tables *tabs, const JobMeta *meta) {
+    const int j = blockIdx.y;
+    if (meta[j].status) return;
+    const InflateJob job = jobs[j];
+    const Tables T = tabs[j];
+    const uint64_t words = (job.dst_len + 31) / 32;
+    for (uint64_t wi = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; wi < words;
+         wi += (uint64_t)gridDim.x * blockDim.x) {
+        uint32_t f = T.flags[wi];
+        while (f) {
+            const int bit = __ffs(f) - 1;
+            f &= f - 1;
+            const uint64_t t = wi * 32 + (uint64_t)bit;
+            uint64_t s = T.ptr[t];
+            while (flag_get(T.flags, s)) s = T.ptr[s];
+            job.dst[t] = job.dst[s];
         }
     }
-    if (lane == 0) status[jid] = err ? 1 : 0;
+}
+
+// --------------------------------------------------------------- 6. checks
+__global__ void k_adler(const InflateJob *jobs, JobMeta *meta, unsigned long long *acc) {
+    const int j = blockIdx.y;
+    if (meta[j].status) return;
+    const InflateJob job = jobs[j];
+    const uint64_t n = job.dst_len;
+    unsigned long long A = 0, B = 0;
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
+        const uint32_t v = job.dst[i];
+        A += v;
+        B += (unsigned long long)((n - i) % 65521u) * v;
+    }
+    B %= 65521u;
+    for (int o = 16; o > 0; o >>= 1) {
+        A += __shfl_down_sync(0xffffffffu, A, o);
+        B += __shfl_down_sync(0xffffffffu, B, o);
+    }
+    if ((threadIdx.x & 31) == 0) {
+        atomicAdd(&acc[2 * j], A);
+        atomicAdd(&acc[2 * j + 1], B % 65521u);
+    }
+}
+
+__global__ void k_finish(const InflateJob *jobs, int njobs, JobMeta *meta, const unsigned long long *acc, int *status) {
+    const int j = blockIdx.x * blockDim.x + threadIdx.x;
+    if (j >= njobs) return;
+    JobMeta &m = meta[j];
+    if (!m.status) {
+        const uint64_t n = jobs[j].dst_len;
+        const uint32_t a = (uint32_t)((1 + acc[2 * j]) % 65521u), b = (uint32_t)((acc[2 * j + 1] + n) % 65521u);
+        if (((b << 16) | a) != m.adler_want) m.status = 1;
+    }
+    status[j] = m.status;
+}
+
+// per-job arena: [hash keys | flags] (zeroed) then [hash values | blocks | fallback | ptr]
+__global__ void k_setup(const InflateJob *jobs, int njobs, Tables *tabs, uint8_t *arena, const uint64_t *offs,
+                        const uint64_t *caps) {
+    const int j = blockIdx.x * blockDim.x + threadIdx.x;
+    if (j >= njobs) return;
+    uint8_t *a = arena + offs[j];
+    Tables T;
+    T.hcap = caps[4 * j];
+    T.bcap = caps[4 * j + 1];
+    T.fcap = caps[4 * j + 2];
+    const uint64_t n = jobs[j].dst_len;
+    T.hash = reinterpret_cast<unsigned long long *>(a);
+    a += T.hcap * 8;
+    T.flags = reinterpret_cast<uint32_t *>(a);
+    a += ((n + 31) / 32) * 4 + 16;
+    a = reinterpret_cast<uint8_t *>(((uintptr_t)a + 15) & ~uintptr_t(15));
+    T.hval = reinterpret_cast<uint32_t *>(a);
+    a += T.hcap * 4;
+    a = reinterpret_cast<uint8_t *>(((uintptr_t)a + 15) & ~uintptr_t(15));
+    T.blocks = reinterpret_cast<Blk *>(a);
+    a += T.bcap * sizeof(Blk);
+    T.fallback = reinterpret_cast<uint32_t *>(a);
+    a += T.fcap * 4;
+    T.ptr = reinterpret_cast<uint32_t *>(a);
+    tabs[j] = T;
+}
+
+__global__ void k_zero(const InflateJob *jobs, const Tables *tabs) {
+    const int j = blockIdx.y;
+    const Tables T = tabs[j];
+    const uint64_t words = (T.hcap * 8 + ((jobs[j].dst_len + 31) / 32) * 4 + 16) / 4;
+    uint32_t *z = reinterpret_cast<uint32_t *>(T.hash);
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < words; i += (uint64_t)gridDim.x * blockDim.x)
+        z[i] = 0;
 }
 
 }  // namespace
 
-void inflate_batch(const InflateJob *jobs_dev, int count, int *status_dev, cudaStream_t st) {
-    if (count <= 0) return;
-    k_inflate<<<(count + WARPS - 1) / WARPS, WARPS * 32, 0, st>>>(jobs_dev, count, status_dev);
+// per-job arena layout (host mirror of k_setup)
+static uint64_t pow2_at_least(uint64_t v) {
+    uint64_t p = 64;
+    while (p < v) p <<= 1;
+    return p;
+}
+
+struct InflatePlan {
+    std::vector<uint64_t> offs, caps;
+    uint64_t arena = 0;
+};
+
+static InflatePlan plan_jobs(const std::vector<InflateJob> &jobs) {
+    InflatePlan p;
+    for (const InflateJob &j : jobs) {
+        const uint64_t hcap = pow2_at_least(2 * (j.src_len / 512 + 64));
+        const uint64_t bcap = j.src_len / 16 + 64;  // zlib blocks are >= 2 KiB compressed
+        const uint64_t fcap = j.dst_len + 16;
+        const uint64_t bytes = hcap * 12 + 64 + bcap * sizeof(Blk) + fcap * 4 + ((j.dst_len + 31) / 32) * 4 + 16 +
+                               (j.dst_len + 4) * 4 + 64;
+        p.offs.push_back(p.arena);
+        p.caps.insert(p.caps.end(), {hcap, bcap, fcap, 0});
+        p.arena += (bytes + 255) & ~uint64_t(255);
+    }
+    return p;
+}
+
+void inflate_batch_host(const std::vector<InflateJob> &jobs, int *status_dev, DevAlloc &alloc, cudaStream_t st) {
+    const int n = (int)jobs.size();
+    if (n == 0) return;
+    const InflatePlan P = plan_jobs(jobs);
+    uint64_t max_src = 0, max_dst = 0, total_src = 0;
+    for (const InflateJob &j : jobs) {
+        max_src = std::max(max_src, j.src_len);
+        max_dst = std::max(max_dst, j.dst_len);
+        total_src += j.src_len;
+    }
+    const uint64_t cand_cap = total_src / 256 + 64 * (uint64_t)n;
+    // small tables: jobs, offs, caps, tabs, meta, counters
+    const size_t jb = n * sizeof(InflateJob), ob = n * 8, cb = n * 4 * 8, tb = n * sizeof(Tables),
+                 mb = n * sizeof(JobMeta);
+    uint8_t *small = static_cast<uint8_t *>(alloc.get(jb + ob + cb + tb + mb + 16 * n + 64 + 1024, st));
+    InflateJob *jd = reinterpret_cast<InflateJob *>(small);
+    uint64_t *od = reinterpret_cast<uint64_t *>(small + jb);
+    uint64_t *cd = reinterpret_cast<uint64_t *>(small + jb + ob);
+    Tables *td = reinterpret_cast<Tables *>(((uintptr_t)(small + jb + ob + cb) + 15) & ~uintptr_t(15));
+    JobMeta *md = reinterpret_cast<JobMeta *>(((uintptr_t)(td + n) + 15) & ~uintptr_t(15));
+    unsigned long long *acc = reinterpret_cast<unsigned long long *>(((uintptr_t)(md + n) + 15) & ~uintptr_t(15));
+    unsigned long long *ncand = acc + 2 * n;
+    std::vector<uint8_t> host(jb + ob + cb);
+    std::memcpy(host.data(), jobs.data(), jb);
+    std::memcpy(host.data() + jb, P.offs.data(), ob);
+    std::memcpy(host.data() + jb + ob, P.caps.data(), cb);
+    CK(cudaMemcpyAsync(small, host.data(), host.size(), cudaMemcpyHostToDevice, st));
+    CK(cudaMemsetAsync(md, 0, (uint8_t *)(ncand + 1) - (uint8_t *)md, st));
+    uint8_t *arena = static_cast<uint8_t *>(alloc.get(P.arena + 256, st));
+    Cand *cands = static_cast<Cand *>(alloc.get(cand_cap * sizeof(Cand) + 64, st));
+    k_setup<<<(n + 63) / 64, 64, 0, st>>>(jd, n, td, arena, od, cd);
     CKL();
+    k_zero<<<dim3(grid_for(max_dst / 32 + 1024, 256, 512), n), 256, 0, st>>>(jd, td);
+    CKL();
+    {
+        ProfScope ps("inflate.scan", st, total_src);
+        k_scan<<<dim3(grid_for(max_src, 256, 2048), n), 256, 0, st>>>(jd, td, md, cands, ncand, cand_cap);
+        CKL();
+    }
+    unsigned long long hc = 0;
+    CK(cudaMemcpyAsync(&hc, ncand, 8, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    const uint64_t nc = std::min<uint64_t>(hc, cand_cap);
+    uint32_t *pool = static_cast<uint32_t *>(alloc.get(std::max<uint64_t>(nc, 1) * MAXSYM * 4, st));
+    {
+        ProfScope ps("inflate.decode", st, total_src);
+        if (nc) {
+            const unsigned g = (unsigned)std::min<uint64_t>((nc + WARPS - 1) / WARPS, 148ull * 16);
+            k_decode_cands<<<g, WARPS * 32, 0, st>>>(jd, cands, ncand, cand_cap, pool);
+            CKL();
+        }
+        k_chain<<<(n + 31) / 32, 32, 0, st>>>(jd, n, td, md, cands);
+        CKL();
+    }
+    {
+        ProfScope ps("inflate.emit", st, max_dst * n);
+        std::vector<JobMeta> hm(n);
+        CK(cudaMemcpyAsync(hm.data(), md, n * sizeof(JobMeta), cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
+        uint64_t maxb = 1;
+        for (const JobMeta &m : hm) maxb = std::max<uint64_t>(maxb, m.nblocks);
+        k_emit<<<dim3((unsigned)((maxb + WARPS - 1) / WARPS), n), WARPS * 32, 0, st>>>(jd, td, md, pool);
+        CKL();
+        k_resolve<<<dim3(grid_for((max_dst + 31) / 32, 256, 1024), n), 256, 0, st>>>(jd, td, md);
+        CKL();
+        k_adler<<<dim3(grid_for(max_dst, 256, 256), n), 256, 0, st>>>(jd, md, acc);
+        CKL();
+        k_finish<<<(n + 63) / 64, 64, 0, st>>>(jd, n, md, acc, status_dev);
+        CKL();
+    }
 }
 
 }  // namespace ipcg

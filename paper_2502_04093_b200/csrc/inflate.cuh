@@ -4,6 +4,8 @@
 #pragma once
 #include <stdint.h>
 
+#include <vector>
+
 #include "util.cuh"
 
 namespace ipcg {
@@ -15,7 +17,8 @@ struct InflateJob {
     uint64_t dst_len;  // expected output length (uncompress destLen)
 };
 
-// status[i] = 0 on success, 1 on any zlib error (uncompress != Z_OK or length mismatch)
-void inflate_batch(const InflateJob *jobs_dev, int count, int *status_dev, cudaStream_t st);
+// status_dev[i] = 0 on success, 1 on any zlib error (uncompress != Z_OK or length
+// mismatch).  Temporaries come from `alloc` (stream-ordered, released by its owner).
+void inflate_batch_host(const std::vector<InflateJob> &jobs, int *status_dev, DevAlloc &alloc, cudaStream_t st);
 
 }  // namespace ipcg

@@ -579,15 +579,13 @@ void retrieve_impl(ipcg_ctx *c, ipcg_archive *a, int scalar, const int *k, void 
         }
         if (!copies.empty()) gather(c, copies, nullptr);
         if (!jobs.empty()) {
-            DBuf jd(jobs.size() * sizeof(InflateJob), st), sd(jobs.size() * 4, st);
-            InflateJob *jh = static_cast<InflateJob *>(pinned(c, jobs.size() * sizeof(InflateJob)));
-            std::memcpy(jh, jobs.data(), jobs.size() * sizeof(InflateJob));
-            CK(cudaMemcpyAsync(jd.p, jh, jobs.size() * sizeof(InflateJob), cudaMemcpyHostToDevice, st));
+            DevAlloc tmp;
+            DBuf sd(jobs.size() * 4, st);
             {
                 uint64_t ib = 0;
                 for (const InflateJob &j : jobs) ib += j.src_len + j.dst_len;
                 ProfScope ps("inflate", st, ib);
-                inflate_batch(jd.as<InflateJob>(), (int)jobs.size(), sd.as<int>(), st);
+                inflate_batch_host(jobs, sd.as<int>(), tmp, st);
             }
             std::vector<int> status(jobs.size());
             CK(cudaMemcpyAsync(status.data(), sd.p, jobs.size() * 4, cudaMemcpyDeviceToHost, st));
@@ -867,6 +865,66 @@ int ipcg_backend_encode(ipcg_ctx *c, const uint8_t *raw, int raw_on_device, uint
             CK(cudaMemcpyAsync(out_payload + o, ptrs[i], length[i], cudaMemcpyDeviceToHost, st));
             o += length[i];
         }
+        CK(cudaStreamSynchronize(st));
+    });
+}
+
+int ipcg_backend_decode(ipcg_ctx *c, const uint8_t *payloads, const uint64_t *payload_len, const uint8_t *backend,
+                        const uint32_t *crc, const uint64_t *raw_bytes, int count, uint8_t *out, int *status) {
+    return guarded(c, [&] {
+        if (count <= 0) return;
+        cudaStream_t st = c->stream;
+        uint64_t tin = 0, tout = 0, maxp = 1;
+        std::vector<uint64_t> in_off(count), out_off(count);
+        for (int i = 0; i < count; ++i) {
+            in_off[i] = tin;
+            out_off[i] = tout;
+            tin += payload_len[i];
+            tout += raw_bytes[i];
+            maxp = std::max(maxp, payload_len[i]);
+        }
+        DBuf din(tin + 16, st), dout(tout + 16, st);
+        CK(cudaMemcpyAsync(din.p, payloads, tin, cudaMemcpyHostToDevice, st));
+        std::vector<const uint8_t *> ptrs(count);
+        for (int i = 0; i < count; ++i) ptrs[i] = din.as<uint8_t>() + in_off[i];
+        const size_t cw = crc32_batch_workspace(count, maxp);
+        DBuf crcws(cw, st), crcs(count * 4, st), pd(count * 8, st), ld(count * 8, st);
+        CK(cudaMemcpyAsync(pd.p, ptrs.data(), count * 8, cudaMemcpyHostToDevice, st));
+        CK(cudaMemcpyAsync(ld.p, payload_len, count * 8, cudaMemcpyHostToDevice, st));
+        crc32_batch(pd.as<const uint8_t *>(), ld.as<uint64_t>(), count, maxp, crcs.as<uint32_t>(), crcws.p, cw, st);
+        std::vector<uint32_t> hcrc(count);
+        CK(cudaMemcpyAsync(hcrc.data(), crcs.p, count * 4, cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
+        std::vector<InflateJob> jobs;
+        std::vector<int> job_of;
+        std::vector<CopyDesc> copies;
+        for (int i = 0; i < count; ++i) {
+            status[i] = 0;
+            if (hcrc[i] != crc[i]) {
+                status[i] = 1;
+                continue;
+            }
+            uint8_t *dst = dout.as<uint8_t>() + out_off[i];
+            if (backend[i] == 0) {
+                if (payload_len[i] != raw_bytes[i]) status[i] = 3;
+                else copies.push_back(CopyDesc{ptrs[i], (uint64_t)reinterpret_cast<uintptr_t>(dst), raw_bytes[i]});
+            } else {
+                jobs.push_back(InflateJob{ptrs[i], payload_len[i], dst, raw_bytes[i]});
+                job_of.push_back(i);
+            }
+        }
+        if (!copies.empty()) gather(c, copies, nullptr);
+        if (!jobs.empty()) {
+            DevAlloc tmp;
+            DBuf sd(jobs.size() * 4, st);
+            inflate_batch_host(jobs, sd.as<int>(), tmp, st);
+            std::vector<int> js(jobs.size());
+            CK(cudaMemcpyAsync(js.data(), sd.p, jobs.size() * 4, cudaMemcpyDeviceToHost, st));
+            CK(cudaStreamSynchronize(st));
+            for (size_t k = 0; k < jobs.size(); ++k)
+                if (js[k]) status[job_of[k]] = 2;
+        }
+        CK(cudaMemcpyAsync(out, dout.p, tout, cudaMemcpyDeviceToHost, st));
         CK(cudaStreamSynchronize(st));
     });
 }

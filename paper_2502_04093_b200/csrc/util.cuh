@@ -79,6 +79,22 @@ struct ProfScope {
     }
 };
 
+// stream-ordered temporaries released together (cudaMallocAsync pool keeps the memory)
+struct DevAlloc {
+    std::vector<void *> ptrs;
+    cudaStream_t st = nullptr;
+    void *get(size_t bytes, cudaStream_t s) {
+        void *p = nullptr;
+        CK(cudaMallocAsync(&p, bytes ? bytes : 1, s));
+        ptrs.push_back(p);
+        st = s;
+        return p;
+    }
+    ~DevAlloc() {
+        for (void *p : ptrs) cudaFreeAsync(p, st);
+    }
+};
+
 inline unsigned grid_for(uint64_t n, unsigned block, unsigned cap = 148u * 32u) {
     uint64_t g = (n + block - 1) / block;
     if (g == 0) g = 1;

@@ -194,3 +194,37 @@ def test_errors_mirror_reference(oracle_lib, ctx):
     out = ipc.reconstruct_field(reader, [16] * reader.levels)
     with pytest.raises(ipc.InvalidArgument, match="refinement plan must not drop planes"):
         ipc.refine_field(reader, out.session, out.values, [8] + [16] * (reader.levels - 1))
+
+
+def test_inflate_against_zlib_streams(ctx):
+    """GPU inflate on zlib streams of every level / block mix, stored/fixed/dynamic, and corruptions."""
+    import zlib
+
+    rng = np.random.default_rng(11)
+    datas = [b"", b"a", bytes(10), bytes(100000), rng.integers(0, 256, 70000, dtype=np.uint8).tobytes(),
+             np.packbits((rng.random(8 * 300000) < 0.03).astype(np.uint8), bitorder="little").tobytes(),
+             np.packbits((rng.random(8 * 200000) < 0.3).astype(np.uint8), bitorder="little").tobytes(),
+             (b"the quick brown fox %d " * 20000)[:300000],
+             np.repeat(rng.integers(0, 3, 5000, dtype=np.uint8), rng.integers(1, 300, 5000)).tobytes()]
+    blocks, want = [], []
+    for d in datas:
+        for level in (1, 6, 9):
+            z = zlib.compress(d, level)
+            blocks.append((1, z, zlib.crc32(z), len(d)))
+            want.append(d)
+        blocks.append((0, d, zlib.crc32(d), len(d)))
+        want.append(d)
+    got = ipc.backend_decode(blocks, ctx=ctx)
+    for g, w in zip(got, want):
+        assert g == w
+    z = bytearray(zlib.compress(datas[6], 6))
+    z[len(z) // 2] ^= 0x55
+    bad = [(1, bytes(z), zlib.crc32(bytes(z)), len(datas[6])),          # corrupt stream, valid CRC
+           (1, zlib.compress(datas[6], 6), 123, len(datas[6])),          # CRC mismatch
+           (1, zlib.compress(datas[6], 6)[:-5], zlib.crc32(zlib.compress(datas[6], 6)[:-5]), len(datas[6])),
+           (1, zlib.compress(datas[6], 6), zlib.crc32(zlib.compress(datas[6], 6)), len(datas[6]) - 1),
+           (0, b"abc", zlib.crc32(b"abc"), 4)]
+    got = ipc.backend_decode(bad, ctx=ctx)
+    assert [str(g) for g in got] == ["deflate backend failed to decompress block", "block checksum mismatch",
+                                     "deflate backend failed to decompress block",
+                                     "deflate backend failed to decompress block", "identity block has wrong length"]
