@@ -459,9 +459,9 @@ __device__ bool chain_decode_block(Bits &b, int type, uint32_t *fb, uint64_t fca
         for (int i = 144; i < 256; ++i) lens[i] = 9;
         for (int i = 256; i < 280; ++i) lens[i] = 7;
         for (int i = 280; i < 288; ++i) lens[i] = 8;
-        for (int i = 0; i < 30; ++i) lens[288 + i] = 5;
+        for (int i = 0; i < 32; ++i) lens[288 + i] = 5;  // zlib's fixed distance table has 32 codes
         nlen = 288;
-        ndist = 30;
+        ndist = 32;
     } else {
         if (!read_dynamic_header(b, lens, nlen, ndist, cs)) return false;
     }
