@@ -40,11 +40,19 @@ struct Bump {
     }
 };
 
+struct RunTask {  // a long periodic stretch of match(258) symbols, written in parallel
+    uint64_t a0, g0, m;
+    int j;
+};
+
 struct Work {
     StreamMeta *meta;
+    RunTask *runs;
+    unsigned long long *nruns;
     uint16_t *prevd;
     uint64_t *rec;
     uint64_t *first_anchor, *bnd;
+    uint32_t *nbreak;  // first chunk >= k that is not entirely 258-byte matches
     uint8_t *exit4;
     uint32_t *cnt4;
     uint8_t *entry;
@@ -64,9 +72,12 @@ Work carve(void *ws, int S, uint64_t n) {
     w.maxb = n / BLOCK_SYMS + 2;
     w.ncrc = (n + 64 + CRC_CHUNK - 1) / CRC_CHUNK + 1;
     w.meta = b.take<StreamMeta>(S);
+    w.runs = b.take<RunTask>((size_t)S * (w.nchunks + 2));
+    w.nruns = b.take<unsigned long long>(1);
     w.prevd = b.take<uint16_t>((size_t)S * n);
     w.rec = b.take<uint64_t>((size_t)S * n);
     w.first_anchor = b.take<uint64_t>((size_t)S * w.nchunks);
+    w.nbreak = b.take<uint32_t>((size_t)S * (w.nchunks + 1));
     w.bnd = b.take<uint64_t>((size_t)S * (w.nchunks + 1));
     w.exit4 = b.take<uint8_t>((size_t)S * w.nchunks * 4);
     w.cnt4 = b.take<uint32_t>((size_t)S * w.nchunks * 4);
@@ -90,9 +101,12 @@ size_t carve_size(int S, uint64_t n) {
     w.maxb = n / BLOCK_SYMS + 2;
     w.ncrc = (n + 64 + CRC_CHUNK - 1) / CRC_CHUNK + 1;
     b.take<StreamMeta>(S);
+    b.take<RunTask>((size_t)S * (w.nchunks + 2));
+    b.take<unsigned long long>(1);
     b.take<uint16_t>((size_t)S * n);
     b.take<uint64_t>((size_t)S * n);
     b.take<uint64_t>((size_t)S * w.nchunks);
+    b.take<uint32_t>((size_t)S * (w.nchunks + 1));
     b.take<uint64_t>((size_t)S * (w.nchunks + 1));
     b.take<uint8_t>((size_t)S * w.nchunks * 4);
     b.take<uint32_t>((size_t)S * w.nchunks * 4);
@@ -109,8 +123,25 @@ size_t carve_size(int S, uint64_t n) {
 }
 
 struct InBytes {
-    const uint8_t *p;
+    const uint8_t *p;  // 8-byte aligned stream base; rows are padded to 16 bytes
     __device__ __forceinline__ uint32_t operator()(int64_t i) const { return __ldg(p + i); }
+    __device__ __forceinline__ uint64_t load8(int64_t i) const {
+        const uintptr_t a = reinterpret_cast<uintptr_t>(p + i);
+        const uint64_t *w = reinterpret_cast<const uint64_t *>(a & ~uintptr_t(7));
+        const unsigned sh = (unsigned)(a & 7) * 8;
+        const uint64_t lo = __ldg(w);
+        return sh ? (lo >> sh) | (__ldg(w + 1) << (64 - sh)) : lo;
+    }
+    // common prefix length of the strings at a and b, capped at maxlen (8 bytes per step)
+    __device__ __forceinline__ int64_t match_len(int64_t a, int64_t b, int64_t maxlen) const {
+        int64_t len = 0;
+        for (; len + 8 <= maxlen; len += 8) {
+            const uint64_t x = load8(a + len) ^ load8(b + len);
+            if (x) return len + (__ffsll((long long)x) - 1) / 8;
+        }
+        while (len < maxlen && p[a + len] == p[b + len]) ++len;
+        return len;
+    }
 };
 struct PrevD {
     const uint16_t *p;
@@ -212,29 +243,38 @@ __global__ void __launch_bounds__(256) k_match(const uint8_t *in, uint64_t in_st
 }
 
 // ---------------------------------------------------------------- 4. anchors
-// p is an anchor iff no match found at q < p reaches past p: max_{q<p}(q+max(L128,1)) <= p
+// p is an anchor iff no match found at q < p reaches past p: max_{q<p}(q+max(L128,1)) <= p.
+// One CTA scans a 2048-position tile (plus the 258-position reach-in) and reports the
+// first anchor of each of its CH-sized chunks.
+constexpr int TILE = 2048;
 __global__ void __launch_bounds__(256) k_anchor(uint64_t n, const StreamMeta *meta, const uint64_t *rec_all,
                                                uint64_t nchunks, uint64_t *first_anchor) {
     const int j = blockIdx.y;
-    const uint64_t c = blockIdx.x;
-    if (c >= nchunks) return;
     if (!meta[j].active) return;
+    const uint64_t c0 = (uint64_t)blockIdx.x * TILE;
+    if (c0 >= n) return;
     const uint64_t *rec = rec_all + (uint64_t)j * n;
-    const uint64_t c0 = c * CH, c1 = min(n, c0 + CH);
+    const uint64_t c1 = min(n, c0 + TILE);
     const uint64_t r0 = c0 >= MAX_MATCH ? c0 - MAX_MATCH : 0;
     const uint64_t len = c1 - r0;
     const uint64_t per = (len + blockDim.x - 1) / blockDim.x;
     const uint64_t s0 = r0 + threadIdx.x * per, s1 = min(c1, s0 + per);
+    __shared__ uint64_t scan[256];
+    __shared__ unsigned long long best[TILE / CH];
+    __shared__ unsigned full[TILE / CH];
+    if (threadIdx.x < TILE / CH) {
+        best[threadIdx.x] = ~0ull;
+        full[threadIdx.x] = 1u;
+    }
+    __syncthreads();
     uint64_t mx = 0;
     for (uint64_t q = s0; q < s1; ++q) {
         const uint32_t l = mrec_l128(rec[q]);
         const uint64_t r = q + (l ? l : 1);
         mx = r > mx ? r : mx;
+        if (q >= c0 && l != MAX_MATCH) full[(q - c0) / CH] = 0u;
     }
-    __shared__ uint64_t scan[256];
-    __shared__ unsigned long long best;
     scan[threadIdx.x] = mx;
-    if (threadIdx.x == 0) best = ~0ull;
     __syncthreads();
     for (unsigned o = 1; o < blockDim.x; o <<= 1) {  // inclusive max-scan
         const uint64_t v = threadIdx.x >= o ? scan[threadIdx.x - o] : 0;
@@ -243,66 +283,141 @@ __global__ void __launch_bounds__(256) k_anchor(uint64_t n, const StreamMeta *me
         __syncthreads();
     }
     uint64_t run = threadIdx.x ? scan[threadIdx.x - 1] : 0;
+    int last = -1;
     for (uint64_t q = s0; q < s1; ++q) {
         if (q >= c0 && run <= q) {
-            atomicMin(&best, (unsigned long long)q);
-            break;
+            const int ch = (int)((q - c0) / CH);
+            if (ch != last) {
+                atomicMin(&best[ch], (unsigned long long)q);
+                last = ch;
+            }
         }
         const uint32_t l = mrec_l128(rec[q]);
         const uint64_t r = q + (l ? l : 1);
         run = r > run ? r : run;
     }
     __syncthreads();
-    if (threadIdx.x == 0) first_anchor[(uint64_t)j * nchunks + c] = best;
+    const uint64_t k = c0 / CH + threadIdx.x;
+    if (threadIdx.x < TILE / CH && k < nchunks)
+        first_anchor[(uint64_t)j * nchunks + k] =
+            (best[threadIdx.x] == ~0ull ? (~0ull >> 2) : best[threadIdx.x]) |  // "none" stays huge, bit 63 clear
+            ((uint64_t)(full[threadIdx.x] && k * CH + CH <= n) << 63);
 }
 
 // chunk boundaries: bnd[k] = first anchor >= k*CH (suffix-min over chunks)
 __global__ void k_bounds(uint64_t n, const StreamMeta *meta, uint64_t nchunks, const uint64_t *first_anchor,
-                         uint64_t *bnd_all) {
+                         uint64_t *bnd_all, uint32_t *nbreak_all) {
     const int j = blockIdx.x;
     if (!meta[j].active) return;
     const unsigned lane = threadIdx.x;
     const uint64_t *fa = first_anchor + (uint64_t)j * nchunks;
     uint64_t *bnd = bnd_all + (uint64_t)j * (nchunks + 1);
+    uint32_t *nbreak = nbreak_all + (uint64_t)j * (nchunks + 1);
     uint64_t carry = n;
-    if (lane == 0) bnd[nchunks] = n;
+    uint32_t carry_nb = (uint32_t)nchunks;
+    if (lane == 0) {
+        bnd[nchunks] = n;
+        nbreak[nchunks] = (uint32_t)nchunks;
+    }
     for (int64_t g = (int64_t)((nchunks + 31) / 32) - 1; g >= 0; --g) {
         const uint64_t k = (uint64_t)g * 32 + lane;
-        uint64_t v = k < nchunks ? fa[k] : ~0ull;
+        const uint64_t raw = k < nchunks ? fa[k] : ~0ull;
+        uint64_t v = k < nchunks ? (raw & ~(1ull << 63)) : ~0ull;
+        uint32_t nb = (k < nchunks && !(raw >> 63)) ? (uint32_t)k : 0xffffffffu;
         for (int o = 1; o < 32; o <<= 1) {  // suffix min
             const uint64_t w = __shfl_down_sync(0xffffffffu, v, o);
+            const uint32_t x = __shfl_down_sync(0xffffffffu, nb, o);
             if (lane + o < 32 && w < v) v = w;
+            if (lane + o < 32 && x < nb) nb = x;
         }
         v = v < carry ? v : carry;
-        if (k < nchunks) bnd[k] = k == 0 ? 0 : v;
+        nb = nb < carry_nb ? nb : carry_nb;
+        if (k < nchunks) {
+            bnd[k] = k == 0 ? 0 : v;
+            nbreak[k] = nb;
+        }
         carry = __shfl_sync(0xffffffffu, v, 0);
+        carry_nb = __shfl_sync(0xffffffffu, nb, 0);
     }
 }
 
+// Inside a run of chunks whose every position has a 258-byte chain-128 match, the lazy
+// parse is periodic: (a, A) holds the match found at a, (a+1, C128) emits match(258) and
+// lands on (a+258, A).  Returns how many A-positions a = p + 258*i stay inside the run
+// (kept clear of the last 520 bytes, where lookahead caps and tail slides apply).
+__device__ __forceinline__ int64_t periodic_run(int64_t p, int tag, uint64_t n, const uint32_t *nbreak) {
+    if (tag != TAG_A) return 0;
+    const uint64_t kk = (uint64_t)p / CH;
+    const uint32_t nb = nbreak[kk];
+    if (nb <= kk) return 0;
+    int64_t limit = (int64_t)nb * CH;
+    if (limit > (int64_t)n - 520) limit = (int64_t)n - 520;
+    if (limit <= p) return 0;
+    return (limit - p + MAX_MATCH - 1) / MAX_MATCH;
+}
+
 // ------------------------------------------------------ 5. chunk transfer maps
-__global__ void __launch_bounds__(128) k_sim(const uint8_t *in, uint64_t in_stride, uint64_t n, const StreamMeta *meta,
-                                            const uint64_t *rec_all, uint64_t nchunks, const uint64_t *bnd_all,
-                                            uint8_t *exit4, uint32_t *cnt4) {
+// One warp owns 8 consecutive chunks: it stages their match records (plus the
+// reach-out margin) in shared memory, then its 32 lanes walk the 8 chunks x 4 entry
+// tags from smem.  Walks that run past the staged window read global memory.
+constexpr int SIM_WARPS = 4;
+constexpr int SIM_CHUNKS = 8;
+constexpr int WIN = SIM_CHUNKS * CH + MAX_MATCH + 8;
+
+struct NoBytes {
+    __device__ __forceinline__ uint32_t operator()(int64_t) const { return 0; }
+};
+
+struct RecWin {
+    const uint64_t *win, *rec;
+    uint64_t s0, s1;
+    __device__ __forceinline__ uint64_t operator()(int64_t q) const {
+        return ((uint64_t)q >= s0 && (uint64_t)q < s1) ? win[q - (int64_t)s0] : rec[q];
+    }
+};
+
+__device__ __forceinline__ RecWin stage_window(uint64_t *win, const uint64_t *rec, uint64_t k0, uint64_t n,
+                                               unsigned lane) {
+    const uint64_t s0 = k0 * CH > 0 ? k0 * CH - 1 : 0;
+    const uint64_t s1 = min(n, (k0 + SIM_CHUNKS) * CH + MAX_MATCH);
+    for (uint64_t i = s0 + lane; i < s1; i += 32) win[i - s0] = rec[i];
+    __syncwarp();
+    return RecWin{win, rec, s0, s1};
+}
+
+__global__ void __launch_bounds__(SIM_WARPS * 32) k_sim(uint64_t n, const StreamMeta *meta, const uint64_t *rec_all,
+                                                       uint64_t nchunks, const uint64_t *bnd_all,
+                                                       const uint32_t *nbreak_all, uint8_t *exit4, uint32_t *cnt4) {
+    extern __shared__ uint64_t srec[];
     const int j = blockIdx.y;
     if (!meta[j].active) return;
-    const uint64_t t = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
-    if (t >= nchunks * 4) return;
-    const uint64_t k = t >> 2;
-    int tag = (int)(t & 3);
+    const unsigned warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint64_t k0 = ((uint64_t)blockIdx.x * SIM_WARPS + warp) * SIM_CHUNKS;
+    if (k0 >= nchunks) return;
+    const RecWin R = stage_window(srec + (size_t)warp * WIN, rec_all + (uint64_t)j * n, k0, n, lane);
+    const uint64_t k = k0 + (lane >> 2);
+    int tag = (int)(lane & 3);
+    if (k >= nchunks) return;
     const uint64_t *bnd = bnd_all + (uint64_t)j * (nchunks + 1);
     const uint64_t b0 = bnd[k], b1 = bnd[k + 1];
-    const uint64_t *rec = rec_all + (uint64_t)j * n;
-    const InBytes bytes{in + (uint64_t)j * in_stride};
+    const NoBytes bytes;
+    const uint32_t *nbreak = nbreak_all + (uint64_t)j * (nchunks + 1);
     uint32_t count = 0;
     int64_t p = (int64_t)b0;
     while (p < (int64_t)b1) {
-        const Step s = parse_step(p, tag, (int64_t)n, rec[p], p > 0 ? rec[p - 1] : 0ull, bytes);
+        const int64_t m = periodic_run(p, tag, n, nbreak);
+        if (m > 0) {
+            count += (uint32_t)m;
+            p += MAX_MATCH * m;
+            continue;
+        }
+        const Step s = parse_step(p, tag, (int64_t)n, R(p), p > 0 ? R(p - 1) : 0ull, bytes);
         count += s.emit != 0;
         p = s.next_p;
         tag = s.next_tag;
     }
-    exit4[(uint64_t)j * nchunks * 4 + t] = (uint8_t)tag;
-    cnt4[(uint64_t)j * nchunks * 4 + t] = count;
+    exit4[((uint64_t)j * nchunks + k) * 4 + (lane & 3)] = (uint8_t)tag;
+    cnt4[((uint64_t)j * nchunks + k) * 4 + (lane & 3)] = count;
 }
 
 // ---------------------------------------------------------------- 6. resolve
@@ -369,28 +484,55 @@ __global__ void k_resolve(const uint8_t *in, uint64_t in_stride, uint64_t n, Str
 }
 
 // ------------------------------------------------------------ 7. emit symbols
-__global__ void __launch_bounds__(128) k_emit_syms(const uint8_t *in, uint64_t in_stride, uint64_t n,
-                                                  const StreamMeta *meta, const uint64_t *rec_all, uint64_t nchunks,
-                                                  const uint64_t *bnd_all, const uint8_t *entry_all,
-                                                  const uint64_t *symoff_all, uint32_t *syms_all, uint64_t maxb,
-                                                  uint64_t *blk_top_all, uint64_t *blk_start_all) {
+// same staging as k_sim; lane c < 8 re-walks chunk k0+c from its resolved entry tag
+__global__ void __launch_bounds__(SIM_WARPS * 32) k_emit_syms(const uint8_t *in, uint64_t in_stride, uint64_t n,
+                                                             const StreamMeta *meta, const uint64_t *rec_all,
+                                                             uint64_t nchunks, const uint64_t *bnd_all,
+                                                             const uint32_t *nbreak_all,
+                                                             const uint8_t *entry_all, const uint64_t *symoff_all,
+                                                             uint32_t *syms_all, uint64_t maxb, uint64_t *blk_top_all,
+                                                             uint64_t *blk_start_all, RunTask *runs,
+                                                             unsigned long long *nruns) {
+    extern __shared__ uint64_t srec[];
     const int j = blockIdx.y;
     if (!meta[j].active) return;
-    const uint64_t k = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
-    if (k >= nchunks) return;
+    const unsigned warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint64_t k0 = ((uint64_t)blockIdx.x * SIM_WARPS + warp) * SIM_CHUNKS;
+    if (k0 >= nchunks) return;
+    const RecWin R = stage_window(srec + (size_t)warp * WIN, rec_all + (uint64_t)j * n, k0, n, lane);
+    const uint64_t k = k0 + lane;
+    if (lane >= SIM_CHUNKS || k >= nchunks) return;
     const uint64_t *bnd = bnd_all + (uint64_t)j * (nchunks + 1);
     const uint64_t b0 = bnd[k], b1 = bnd[k + 1];
     if (b0 >= b1) return;
-    const uint64_t *rec = rec_all + (uint64_t)j * n;
     const InBytes bytes{in + (uint64_t)j * in_stride};
     uint32_t *syms = syms_all + (uint64_t)j * (n + 1);
     uint64_t *btop = blk_top_all + (uint64_t)j * maxb;
     uint64_t *bstart = blk_start_all + (uint64_t)j * maxb;
     int tag = entry_all[(uint64_t)j * (nchunks + 1) + k];
     uint64_t g = symoff_all[(uint64_t)j * nchunks + k];
+    const uint32_t *nbreak = nbreak_all + (uint64_t)j * (nchunks + 1);
     int64_t p = (int64_t)b0;
     while (p < (int64_t)b1) {
-        const Step s = parse_step(p, tag, (int64_t)n, rec[p], p > 0 ? rec[p - 1] : 0ull, bytes);
+        const int64_t m = periodic_run(p, tag, n, nbreak);
+        if (m > 64) {  // long stretch: hand it to k_emit_runs
+            const unsigned long long t = atomicAdd(nruns, 1ull);
+            runs[t] = RunTask{(uint64_t)p, g, (uint64_t)m, j};
+            g += (uint64_t)m;
+            p += MAX_MATCH * m;
+            continue;
+        }
+        if (m > 0) {
+            for (int64_t i = 0; i < m; ++i, ++g) {
+                const int64_t a = p + MAX_MATCH * i;
+                syms[g] = sym_match(MAX_MATCH, mrec_d128(R(a)));
+                if (g % BLOCK_SYMS == 0) bstart[g / BLOCK_SYMS] = (uint64_t)a;
+                if (g % BLOCK_SYMS == BLOCK_SYMS - 1) btop[g / BLOCK_SYMS] = (uint64_t)a + 1;
+            }
+            p += MAX_MATCH * m;
+            continue;
+        }
+        const Step s = parse_step(p, tag, (int64_t)n, R(p), p > 0 ? R(p - 1) : 0ull, bytes);
         if (s.emit) {
             syms[g] = s.emit == 2 ? sym_match(s.len, s.dist) : sym_literal(s.len);
             if (g % BLOCK_SYMS == 0) bstart[g / BLOCK_SYMS] = (uint64_t)p - 1;
@@ -399,6 +541,25 @@ __global__ void __launch_bounds__(128) k_emit_syms(const uint8_t *in, uint64_t i
         }
         p = s.next_p;
         tag = s.next_tag;
+    }
+}
+
+__global__ void __launch_bounds__(256) k_emit_runs(uint64_t n, const uint64_t *rec_all, uint32_t *syms_all,
+                                                  uint64_t maxb, uint64_t *blk_top_all, uint64_t *blk_start_all,
+                                                  const RunTask *runs, const unsigned long long *nruns) {
+    const uint64_t nt = *nruns;
+    for (uint64_t t = blockIdx.x; t < nt; t += gridDim.x) {
+        const RunTask r = runs[t];
+        const uint64_t *rec = rec_all + (uint64_t)r.j * n;
+        uint32_t *syms = syms_all + (uint64_t)r.j * (n + 1);
+        uint64_t *btop = blk_top_all + (uint64_t)r.j * maxb;
+        uint64_t *bstart = blk_start_all + (uint64_t)r.j * maxb;
+        for (uint64_t i = threadIdx.x; i < r.m; i += blockDim.x) {
+            const uint64_t a = r.a0 + MAX_MATCH * i, g = r.g0 + i;
+            syms[g] = sym_match(MAX_MATCH, mrec_d128(rec[a]));
+            if (g % BLOCK_SYMS == 0) bstart[g / BLOCK_SYMS] = a;
+            if (g % BLOCK_SYMS == BLOCK_SYMS - 1) btop[g / BLOCK_SYMS] = a + 1;
+        }
     }
 }
 
@@ -678,6 +839,7 @@ void DeflateBatch::run(const uint8_t *in, uint64_t in_stride, int S, uint64_t n,
                        void *workspace, BackendResults res, cudaStream_t st) {
     Work w = carve(workspace, S, n);
     CK(cudaMemsetAsync(w.meta, 0, sizeof(StreamMeta) * S, st));
+    CK(cudaMemsetAsync(w.nruns, 0, sizeof(unsigned long long), st));
     if (n > 0) {
         {
         ProfScope ps("deflate.scan", st, (uint64_t)S * n);
@@ -707,16 +869,26 @@ void DeflateBatch::run(const uint8_t *in, uint64_t in_stride, int S, uint64_t n,
         }
         {
         ProfScope ps3("deflate.parse", st, (uint64_t)S * n * 20);
-        k_anchor<<<dim3((unsigned)w.nchunks, S), 256, 0, st>>>(n, w.meta, w.rec, w.nchunks, w.first_anchor);
+        k_anchor<<<dim3((unsigned)((n + TILE - 1) / TILE), S), 256, 0, st>>>(n, w.meta, w.rec, w.nchunks, w.first_anchor);
         CKL();
-        k_bounds<<<S, 32, 0, st>>>(n, w.meta, w.nchunks, w.first_anchor, w.bnd);
+        k_bounds<<<S, 32, 0, st>>>(n, w.meta, w.nchunks, w.first_anchor, w.bnd, w.nbreak);
         CKL();
-        k_sim<<<dim3((unsigned)((w.nchunks * 4 + 127) / 128), S), 128, 0, st>>>(in, in_stride, n, w.meta, w.rec, w.nchunks, w.bnd, w.exit4, w.cnt4);
+        const size_t sim_smem = (size_t)SIM_WARPS * WIN * sizeof(uint64_t);
+        const unsigned sim_grid = (unsigned)((w.nchunks + SIM_WARPS * SIM_CHUNKS - 1) / (SIM_WARPS * SIM_CHUNKS));
+        static bool sim_attr = false;
+        if (!sim_attr) {
+            CK(cudaFuncSetAttribute(k_sim, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sim_smem));
+            CK(cudaFuncSetAttribute(k_emit_syms, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sim_smem));
+            sim_attr = true;
+        }
+        k_sim<<<dim3(sim_grid, S), SIM_WARPS * 32, sim_smem, st>>>(n, w.meta, w.rec, w.nchunks, w.bnd, w.nbreak, w.exit4, w.cnt4);
         CKL();
         k_resolve<<<S, 32, 0, st>>>(in, in_stride, n, w.meta, w.nchunks, w.exit4, w.cnt4, w.entry, w.symoff, w.syms,
                                     w.maxb, w.blk_start);
         CKL();
-        k_emit_syms<<<dim3((unsigned)((w.nchunks + 127) / 128), S), 128, 0, st>>>(in, in_stride, n, w.meta, w.rec, w.nchunks, w.bnd, w.entry, w.symoff, w.syms, w.maxb, w.blk_top, w.blk_start);
+        k_emit_syms<<<dim3(sim_grid, S), SIM_WARPS * 32, sim_smem, st>>>(in, in_stride, n, w.meta, w.rec, w.nchunks, w.bnd, w.nbreak, w.entry, w.symoff, w.syms, w.maxb, w.blk_top, w.blk_start, w.runs, w.nruns);
+        CKL();
+        k_emit_runs<<<148 * 4, 256, 0, st>>>(n, w.rec, w.syms, w.maxb, w.blk_top, w.blk_start, w.runs, w.nruns);
         CKL();
         }
         {

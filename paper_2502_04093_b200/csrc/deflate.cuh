@@ -18,7 +18,7 @@ struct BackendResults {
 // S equal-length streams in[j*in_stride .. +n); outputs land in out[j*out_stride ..],
 // out_stride >= n + 16.  Workspace from DeflateBatch::workspace_bytes.
 struct DeflateBatch {
-    static constexpr int CH = 2048;  // nominal parse chunk
+    static constexpr int CH = 256;  // nominal parse chunk (boundaries snap to anchors)
     static size_t workspace_bytes(int S, uint64_t n);
     static void run(const uint8_t *in, uint64_t in_stride, int S, uint64_t n, uint8_t *out, uint64_t out_stride,
                     void *workspace, BackendResults res, cudaStream_t st);

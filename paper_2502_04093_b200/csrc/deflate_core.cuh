@@ -71,10 +71,23 @@ HD uint64_t match_search(int64_t p, int64_t n, const Bytes &bytes, const Prev &p
     const int64_t limit = p - MAX_DIST > 0 ? p - MAX_DIST : 0;
     uint32_t best = 0, bestd = 0, l32 = 0, d32 = 0;
     for (int i = 1; i <= MAX_CHAIN; ++i) {
+        // zlib's quick reject: a candidate that differs at best or best-1 cannot beat best
+        if (best >= MIN_MATCH && (int64_t)best < maxlen &&
+            (bytes(q + best) != bytes(p + best) || bytes(q + best - 1) != bytes(p + best - 1))) {
+            if (i <= 32) {
+                l32 = best;
+                d32 = bestd;
+            }
+            const uint32_t dq = prevd(q);
+            if (dq == 0) break;
+            const int64_t q2 = q - (int64_t)dq;
+            if (!(q2 > limit)) break;
+            q = q2;
+            continue;
+        }
         // match length between p and q (>= 3 only when bytes 0,1 agree: hash implies byte 2)
-        int64_t len = 0;
-        while (len < maxlen && bytes(p + len) == bytes(q + len)) ++len;
-        if (len < MIN_MATCH) len = 0;
+        const int64_t len0 = bytes.match_len(p, q, maxlen);
+        const int64_t len = len0 < MIN_MATCH ? 0 : len0;
         bool stop = false;
         if ((uint32_t)len > best) {
             best = (uint32_t)len;

@@ -247,6 +247,7 @@ struct JobMeta {
     uint32_t adler_want;
     uint32_t nblocks;
     unsigned long long ncand;
+    int allzero;         // every literal of every block is 0 -> output is all zero
 };
 
 struct Cand {
@@ -256,6 +257,7 @@ struct Cand {
     uint32_t nsyms;
     int job;
     int ok;
+    int nzlit;  // some literal is non-zero
 };
 
 struct Blk {
@@ -400,7 +402,7 @@ __global__ void __launch_bounds__(WARPS * 32) k_decode_cands(const InflateJob *j
         huff_build(lit_s[w], lens_s[w], nlen, lane);
         huff_build(dist_s[w], lens_s[w] + nlen, ndist, lane);
         uint32_t *out = pool + ci * (uint64_t)MAXSYM;
-        uint32_t ns = 0;
+        uint32_t ns = 0, nz = 0;
         uint64_t bytes = 0;
         bool good = true;
         for (;;) {
@@ -416,6 +418,7 @@ __global__ void __launch_bounds__(WARPS * 32) k_decode_cands(const InflateJob *j
             }
             if (sym < 256) {
                 if (lane == 0) out[ns] = sym_lit((uint32_t)sym);
+                nz |= (uint32_t)sym;
                 ++ns;
                 ++bytes;
                 continue;
@@ -439,6 +442,7 @@ __global__ void __launch_bounds__(WARPS * 32) k_decode_cands(const InflateJob *j
         if (b.overrun()) good = false;
         if (lane == 0) {
             c.ok = good ? 1 : 0;
+            c.nzlit = nz != 0;
             c.end_bit = b.used;
             c.nsyms = ns;
             c.out_bytes = bytes;
@@ -499,6 +503,7 @@ __global__ void k_chain(const InflateJob *jobs, int njobs, const Tables *tabs, J
     JobMeta &m = meta[j];
     bool err = false;
     uint64_t out = 0, nb = 0, fused = 0;
+    bool nonzero = false;
     if (job.src_len < 2) err = true;
     if (!err) {
         const uint32_t cmf = job.src[0], flg = job.src[1];
@@ -533,6 +538,7 @@ __global__ void k_chain(const InflateJob *jobs, int njobs, const Tables *tabs, J
             blk.out_len = L;
             blk.nsyms = 0;
             e = (bp + 4 + L) * 8;
+            if (L) nonzero = true;  // conservative
         } else if (type == 3) {
             err = true;
             break;
@@ -553,6 +559,7 @@ __global__ void k_chain(const InflateJob *jobs, int njobs, const Tables *tabs, J
                             blk.out_len = c.out_bytes;
                             e = c.end_bit;
                             found = true;
+                            if (c.nzlit) nonzero = true;
                         }
                         break;
                     }
@@ -571,6 +578,7 @@ __global__ void k_chain(const InflateJob *jobs, int njobs, const Tables *tabs, J
                 blk.nsyms = ns;
                 blk.out_len = bytes;
                 e = b.used;
+                nonzero = true;  // conservative
             }
         }
         out += blk.out_len;
@@ -588,7 +596,21 @@ __global__ void k_chain(const InflateJob *jobs, int njobs, const Tables *tabs, J
                            ((uint32_t)job.src[bp + 2] << 8) | job.src[bp + 3];
     }
     m.nblocks = err ? 0 : (uint32_t)nb;
+    m.allzero = !nonzero;
     if (err) m.status = 1;
+}
+
+__global__ void k_fill_zero(const InflateJob *jobs, const JobMeta *meta) {
+    const int j = blockIdx.y;
+    if (meta[j].status || !meta[j].allzero) return;
+    const InflateJob job = jobs[j];
+    const uint64_t v = job.dst_len / 16;
+    uint4 *d4 = reinterpret_cast<uint4 *>(job.dst);  // plane rows are 16-byte aligned
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < v; i += (uint64_t)gridDim.x * blockDim.x)
+        d4[i] = make_uint4(0, 0, 0, 0);
+    for (uint64_t i = v * 16 + blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < job.dst_len;
+         i += (uint64_t)gridDim.x * blockDim.x)
+        job.dst[i] = 0;
 }
 
 // -------------------------------------------------------------------- 4. emit
@@ -598,7 +620,7 @@ __global__ void __launch_bounds__(WARPS * 32) k_emit(const InflateJob *jobs, con
                                                    const uint32_t *pool) {
     const int j = blockIdx.y;
     const JobMeta &m = meta[j];
-    if (m.status) return;
+    if (m.status || m.allzero) return;
     const unsigned w = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const uint64_t bi = (uint64_t)blockIdx.x * WARPS + w;
     if (bi >= m.nblocks) return;
@@ -622,19 +644,34 @@ __global__ void __launch_bounds__(WARPS * 32) k_emit(const InflateJob *jobs, con
         }
         const uint32_t len = (v >> 16) & 0x1ff, d = (v & 0xffff) + 1;
         __syncwarp();
-        for (uint32_t i = lane; i < len; i += 32) {
-            const uint64_t src = o - d + (d < len ? (i % d) : i);
-            const uint64_t t = o + i;
-            if (src >= b0) {
-                if (flag_get(T.flags, src)) {
-                    T.ptr[t] = T.ptr[src];
-                    atomicOr(&T.flags[t >> 5], 1u << (t & 31));
+        // every source byte precedes o, so the lanes of one match never depend on each other;
+        // unresolved bytes (sources in earlier blocks) get a pointer, and their flag bits are
+        // set with one ballot-aggregated atomic per 32 bytes
+        for (uint32_t base = 0; base < len; base += 32) {
+            const uint32_t i = base + lane;
+            const bool act = i < len;
+            bool unres = false;
+            if (act) {
+                const uint64_t src = o - d + (d < len ? (i % d) : i);
+                const uint64_t t = o + i;
+                if (src >= b0) {
+                    if (flag_get(T.flags, src)) {
+                        T.ptr[t] = T.ptr[src];
+                        unres = true;
+                    } else {
+                        dst[t] = dst[src];
+                    }
                 } else {
-                    dst[t] = dst[src];
+                    T.ptr[t] = (uint32_t)src;
+                    unres = true;
                 }
-            } else {
-                T.ptr[t] = (uint32_t)src;
-                atomicOr(&T.flags[t >> 5], 1u << (t & 31));
+            }
+            const unsigned m = __ballot_sync(0xffffffffu, unres);
+            if (m) {
+                const uint64_t t0 = o + base;
+                const unsigned sh = (unsigned)(t0 & 31);
+                if (lane == 0) atomicOr(&T.flags[t0 >> 5], m << sh);
+                if (lane == 1 && sh) atomicOr(&T.flags[(t0 >> 5) + 1], m >> (32 - sh));
             }
         }
         __syncwarp();
@@ -645,7 +682,7 @@ __global__ void __launch_bounds__(WARPS * 32) k_emit(const InflateJob *jobs, con
 // ------------------------------------------------------------------ 5. resolve
 __global__ void k_resolve(const InflateJob *jobs, const Tables *tabs, const JobMeta *meta) {
     const int j = blockIdx.y;
-    if (meta[j].status) return;
+    if (meta[j].status || meta[j].allzero) return;
     const InflateJob job = jobs[j];
     const Tables T = tabs[j];
     const uint64_t words = (job.dst_len + 31) / 32;
@@ -824,10 +861,19 @@ void inflate_batch_host(const std::vector<InflateJob> &jobs, int *status_dev, De
         CK(cudaStreamSynchronize(st));
         uint64_t maxb = 1;
         for (const JobMeta &m : hm) maxb = std::max<uint64_t>(maxb, m.nblocks);
-        k_emit<<<dim3((unsigned)((maxb + WARPS - 1) / WARPS), n), WARPS * 32, 0, st>>>(jd, td, md, pool);
-        CKL();
-        k_resolve<<<dim3(grid_for((max_dst + 31) / 32, 256, 1024), n), 256, 0, st>>>(jd, td, md);
-        CKL();
+        {
+            ProfScope ps2("inflate.emit_blocks", st, max_dst * n);
+            k_emit<<<dim3((unsigned)((maxb + WARPS - 1) / WARPS), n), WARPS * 32, 0, st>>>(jd, td, md, pool);
+            CKL();
+            k_fill_zero<<<dim3(grid_for(max_dst / 16 + 1, 256, 512), n), 256, 0, st>>>(jd, md);
+            CKL();
+        }
+        {
+            ProfScope ps3("inflate.resolve", st, max_dst * n / 8);
+            k_resolve<<<dim3(grid_for((max_dst + 31) / 32, 256, 1024), n), 256, 0, st>>>(jd, td, md);
+            CKL();
+        }
+        ProfScope ps4("inflate.adler", st, max_dst * n);
         k_adler<<<dim3(grid_for(max_dst, 256, 256), n), 256, 0, st>>>(jd, md, acc);
         CKL();
         k_finish<<<(n + 63) / 64, 64, 0, st>>>(jd, n, md, acc, status_dev);

@@ -376,6 +376,19 @@ struct PlaneRef {
     uint32_t crc;
 };
 
+// diff[i] = 1 when the two ranges of pair i differ (src vs dst_off-as-address)
+__global__ void k_compare(const CopyDesc *pairs, int n, int *diff) {
+    const int i = blockIdx.x;
+    if (i >= n) return;
+    const CopyDesc c = pairs[i];
+    const uint8_t *b = reinterpret_cast<const uint8_t *>(c.dst_off);
+    for (uint64_t k = threadIdx.x; k < c.len; k += blockDim.x)
+        if (c.src[k] != b[k]) {
+            diff[i] = 1;
+            break;
+        }
+}
+
 __global__ void k_copy_headers(const uint8_t *src, const uint64_t *offs, int n, uint8_t *dst) {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
@@ -536,10 +549,17 @@ void retrieve_impl(ipcg_ctx *c, ipcg_archive *a, int scalar, const int *k, void 
         stride[level - 1] = round_up(std::max<uint64_t>((count + 31) / 32, 1), 4);
         planes[level - 1] = DBuf(32 * stride[level - 1] * 4, st);
     }
+    // plane rows the merge reads (duplicates may alias one decoded row)
+    std::vector<std::vector<const uint32_t *>> rows(L, std::vector<const uint32_t *>(32, nullptr));
+    for (int l = 0; l < L; ++l)
+        if (planes[l].p)
+            for (int q = 0; q < 32; ++q) rows[l][q] = planes[l].as<uint32_t>() + (uint64_t)q * stride[l];
     if (R) {
         std::vector<const uint8_t *> ptrs(R);
         std::vector<uint64_t> lens(R);
         std::vector<InflateJob> jobs;
+        std::vector<int> job_level, job_plane;
+        std::vector<uint32_t> job_crc;
         std::vector<CopyDesc> copies;
         for (size_t i = 0; i < R; ++i) {
             const PlaneRef &r = refs[i];
@@ -552,6 +572,9 @@ void retrieve_impl(ipcg_ctx *c, ipcg_archive *a, int scalar, const int *k, void 
                 copies.push_back(CopyDesc{ptrs[i], (uint64_t)reinterpret_cast<uintptr_t>(row), std::min(r.plen, pbytes)});
             } else {
                 jobs.push_back(InflateJob{ptrs[i], r.plen, row, pbytes});
+                job_level.push_back(li);
+                job_plane.push_back(r.plane);
+                job_crc.push_back(r.crc);
             }
         }
         const size_t cw = crc32_batch_workspace((int)R, maxp);
@@ -578,21 +601,65 @@ void retrieve_impl(ipcg_ctx *c, ipcg_archive *a, int scalar, const int *k, void 
             if (refs[i].backend == 0 && refs[i].plen != pbytes) throw Error(ERUNTIME, "identity block has wrong length");
         }
         if (!copies.empty()) gather(c, copies, nullptr);
-        if (!jobs.empty()) {
+        // identical deflate payloads (typically the all-zero high planes) decode once:
+        // same (length, crc, plane size) and byte-equal on the device -> alias the row
+        std::vector<int> rep_of(jobs.size(), -1);
+        {
+            std::vector<std::pair<int, int>> pairs;  // (dup job, rep job)
+            for (size_t a = 0; a < jobs.size(); ++a) {
+                for (size_t b = 0; b < a; ++b) {
+                    if (rep_of[b] >= 0) continue;
+                    if (jobs[a].src_len == jobs[b].src_len && jobs[a].dst_len == jobs[b].dst_len &&
+                        job_crc[a] == job_crc[b]) {
+                        pairs.push_back({(int)a, (int)b});
+                        break;
+                    }
+                }
+            }
+            if (!pairs.empty()) {
+                std::vector<CopyDesc> cmp;
+                for (auto &pr : pairs)
+                    cmp.push_back(CopyDesc{jobs[pr.first].src, (uint64_t)reinterpret_cast<uintptr_t>(jobs[pr.second].src),
+                                           jobs[pr.first].src_len});
+                DBuf cd(cmp.size() * sizeof(CopyDesc), st), diff(cmp.size() * 4, st);
+                CK(cudaMemcpyAsync(cd.p, cmp.data(), cmp.size() * sizeof(CopyDesc), cudaMemcpyHostToDevice, st));
+                CK(cudaMemsetAsync(diff.p, 0, cmp.size() * 4, st));
+                k_compare<<<(unsigned)cmp.size(), 256, 0, st>>>(cd.as<CopyDesc>(), (int)cmp.size(), diff.as<int>());
+                CKL();
+                std::vector<int> hd(cmp.size());
+                CK(cudaMemcpyAsync(hd.data(), diff.p, cmp.size() * 4, cudaMemcpyDeviceToHost, st));
+                CK(cudaStreamSynchronize(st));
+                for (size_t q = 0; q < pairs.size(); ++q)
+                    if (!hd[q]) rep_of[pairs[q].first] = pairs[q].second;
+            }
+        }
+        std::vector<InflateJob> todo;
+        for (size_t a = 0; a < jobs.size(); ++a)
+            if (rep_of[a] < 0) todo.push_back(jobs[a]);
+            else rows[job_level[a]][job_plane[a]] = rows[job_level[rep_of[a]]][job_plane[rep_of[a]]];
+        if (!todo.empty()) {
             DevAlloc tmp;
-            DBuf sd(jobs.size() * 4, st);
+            DBuf sd(todo.size() * 4, st);
             {
                 uint64_t ib = 0;
-                for (const InflateJob &j : jobs) ib += j.src_len + j.dst_len;
+                for (const InflateJob &j : todo) ib += j.src_len + j.dst_len;
                 ProfScope ps("inflate", st, ib);
-                inflate_batch_host(jobs, sd.as<int>(), tmp, st);
+                inflate_batch_host(todo, sd.as<int>(), tmp, st);
             }
-            std::vector<int> status(jobs.size());
-            CK(cudaMemcpyAsync(status.data(), sd.p, jobs.size() * 4, cudaMemcpyDeviceToHost, st));
+            std::vector<int> status(todo.size());
+            CK(cudaMemcpyAsync(status.data(), sd.p, todo.size() * 4, cudaMemcpyDeviceToHost, st));
             CK(cudaStreamSynchronize(st));
             for (int s : status)
                 if (s) throw Error(ERUNTIME, "deflate backend failed to decompress block");
         }
+    }
+    DBuf rows_d((size_t)L * 32 * sizeof(void *), st);
+    {
+        std::vector<const uint32_t *> flat((size_t)L * 32, nullptr);
+        for (int l = 0; l < L; ++l)
+            for (int q = 0; q < 32; ++q) flat[(size_t)l * 32 + q] = rows[l][q];
+        CK(cudaMemcpyAsync(rows_d.p, flat.data(), flat.size() * sizeof(void *), cudaMemcpyHostToDevice, st));
+        CK(cudaStreamSynchronize(st));
     }
     // ---- merge + reconstruct, coarsest first
     DBuf out_buf;
@@ -625,7 +692,7 @@ void retrieve_impl(ipcg_ctx *c, ipcg_archive *a, int scalar, const int *k, void 
             const uint32_t *min = refine ? prev_sess->merged[li] : nullptr;
             {
                 ProfScope ps("merge", st, count * 4 + (uint64_t)(p.p1 - p.p0) * ((count + 7) / 8));
-                launch_merge(planes[li].as<uint32_t>(), stride[li], min, merged, count, p.p0, p.p1, st);
+                launch_merge(rows_d.as<const uint32_t *>() + (size_t)li * 32, min, merged, count, p.p0, p.p1, st);
             }
             const uint8_t *ob = src_dev + p.ob_off;
             const uint64_t no = ix.records[li].outlier_count;

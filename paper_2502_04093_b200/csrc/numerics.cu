@@ -268,7 +268,7 @@ __global__ void k_outlier_block(const uint64_t *ord, const uint64_t *bits, const
 // xor_decode + merge (bitplane.cpp:24-59), and refine's digit folding with the XOR
 // prefix taken from already-merged codewords (pipeline.hpp:328-339): one warp per
 // 32 codewords; lane p owns plane p's word.
-__global__ void __launch_bounds__(256) k_merge(const uint32_t *__restrict__ planes, uint64_t stride,
+__global__ void __launch_bounds__(256) k_merge(const uint32_t *const *__restrict__ rows,
                                                const uint32_t *__restrict__ merged_in, uint32_t *__restrict__ merged_out,
                                                uint64_t count, int k0, int k1) {
     const unsigned lane = threadIdx.x & 31;
@@ -282,7 +282,7 @@ __global__ void __launch_bounds__(256) k_merge(const uint32_t *__restrict__ plan
             const uint32_t m = __ballot_sync(0xffffffffu, (mi >> (31 - p)) & 1u);
             if ((int)lane == p) bp = m;
         }
-        const uint32_t e = ((int)lane >= k0 && (int)lane < k1) ? planes[(uint64_t)lane * stride + w] : 0u;
+        const uint32_t e = ((int)lane >= k0 && (int)lane < k1) ? rows[lane][w] : 0u;
         for (int p = k0; p < k1; ++p) {
             const uint32_t b1 = __shfl_sync(0xffffffffu, bp, (p - 1) & 31);
             const uint32_t b2 = __shfl_sync(0xffffffffu, bp, (p - 2) & 31);
@@ -431,12 +431,12 @@ void launch_outlier_block(const uint64_t *ord_sorted, const uint64_t *bits_sorte
     CKL();
 }
 
-void launch_merge(const uint32_t *planes, uint64_t stride, const uint32_t *merged_in, uint32_t *merged_out,
-                  uint64_t count, int k0, int k1, cudaStream_t st) {
+void launch_merge(const uint32_t *const *rows, const uint32_t *merged_in, uint32_t *merged_out, uint64_t count, int k0,
+                  int k1, cudaStream_t st) {
     const uint64_t words = (count + 31) / 32;
     if (words == 0) return;
     const unsigned g = grid_for(words * 32, 256);
-    k_merge<<<g, 256, 0, st>>>(planes, stride, merged_in, merged_out, count, k0, k1);
+    k_merge<<<g, 256, 0, st>>>(rows, merged_in, merged_out, count, k0, k1);
     CKL();
 }
 

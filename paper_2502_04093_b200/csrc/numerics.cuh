@@ -42,8 +42,9 @@ size_t sort_outliers_temp_bytes(uint64_t capacity);
 void launch_outlier_block(const uint64_t *ord_sorted, const uint64_t *bits_sorted, const unsigned long long *count,
                           int scalar, uint8_t *out, cudaStream_t st);
 
-void launch_merge(const uint32_t *planes, uint64_t plane_stride_words, const uint32_t *merged_in, uint32_t *merged_out,
-                  uint64_t count, int k0, int k1, cudaStream_t st);
+// rows: device array of 32 plane-row pointers (rows[p] used for k0 <= p < k1)
+void launch_merge(const uint32_t *const *rows, const uint32_t *merged_in, uint32_t *merged_out, uint64_t count, int k0,
+                  int k1, cudaStream_t st);
 void launch_recon_pass(void *state, int scalar, bool cubic, const PassDesc &pd, double eb, const uint32_t *merged,
                        cudaStream_t st);
 // outlier block bytes (u64 ordinal, T) -> overwrite inside one pass's ordinal range

@@ -33,7 +33,15 @@ struct Stats {
 
 extern "C" int zmodel_compress(const uint8_t *in, uint64_t n, int chunk, uint8_t *out, uint64_t cap,
                                uint64_t *out_len, uint64_t *stats) {
-    auto bytes = [&](int64_t i) -> uint32_t { return in[i]; };
+    struct HostBytes {
+        const uint8_t *in;
+        uint32_t operator()(int64_t i) const { return in[i]; }
+        int64_t match_len(int64_t a, int64_t b, int64_t maxlen) const {
+            int64_t len = 0;
+            while (len < maxlen && in[a + len] == in[b + len]) ++len;
+            return len;
+        }
+    } bytes{in};
     // 1. hash-chain links
     std::vector<uint16_t> prevd(n + 1, 0);
     {
