@@ -19,6 +19,8 @@
 //   6. check    Adler-32 trailer and exact output length, as uncompress() does.
 // Any stream that fails any zlib rule is reported, like uncompress() != Z_OK.
 #include <algorithm>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <vector>
 
@@ -31,6 +33,8 @@ namespace {
 constexpr int FASTBITS = 9;
 constexpr int MAXSYM = 16400;  // symbols stored per candidate block (zlib blocks: <= 16383)
 constexpr int WARPS = 4;
+constexpr int SEG = 512;                  // symbols per emit segment
+constexpr int NCKPT = MAXSYM / SEG + 2;   // output-offset checkpoints per candidate
 
 // ------------------------------------------------------------------ bit reader
 struct Bits {
@@ -248,6 +252,7 @@ struct JobMeta {
     uint32_t nblocks;
     unsigned long long ncand;
     int allzero;         // every literal of every block is 0 -> output is all zero
+    uint32_t nseg;       // emit segments over all blocks
 };
 
 struct Cand {
@@ -266,6 +271,8 @@ struct Blk {
     uint64_t src;    // stored: byte offset in src;  symbols: index into the symbol pool
     uint64_t out_off;
     uint64_t out_len;
+    uint32_t seg_base, nseg;  // emit segments (SEG symbols each) of this block
+    uint64_t ckpt;            // candidate index for output checkpoints, ~0 = none (one segment)
 };
 
 struct Tables {  // per-job device pointers
@@ -378,7 +385,7 @@ __global__ void __launch_bounds__(256) k_scan(const InflateJob *jobs, const Tabl
 // ------------------------------------------------------------ 2. candidates
 __global__ void __launch_bounds__(WARPS * 32) k_decode_cands(const InflateJob *jobs, Cand *cands,
                                                            const unsigned long long *ncand_total, uint64_t cand_cap,
-                                                           uint32_t *pool) {
+                                                           uint32_t *pool, uint32_t *ckpt_pool) {
     __shared__ Huff lit_s[WARPS], dist_s[WARPS];
     __shared__ uint8_t lens_s[WARPS][320];
     const unsigned w = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -416,6 +423,7 @@ __global__ void __launch_bounds__(WARPS * 32) k_decode_cands(const InflateJob *j
                 good = false;
                 break;
             }
+            if (lane == 0 && ns % SEG == 0) ckpt_pool[ci * NCKPT + ns / SEG] = (uint32_t)bytes;
             if (sym < 256) {
                 if (lane == 0) out[ns] = sym_lit((uint32_t)sym);
                 nz |= (uint32_t)sym;
@@ -504,6 +512,7 @@ __global__ void k_chain(const InflateJob *jobs, int njobs, const Tables *tabs, J
     bool err = false;
     uint64_t out = 0, nb = 0, fused = 0;
     bool nonzero = false;
+    uint32_t segs = 0;
     if (job.src_len < 2) err = true;
     if (!err) {
         const uint32_t cmf = job.src[0], flg = job.src[1];
@@ -534,6 +543,7 @@ __global__ void k_chain(const InflateJob *jobs, int njobs, const Tables *tabs, J
                 break;
             }
             blk.type = 0;
+            blk.ckpt = ~0ull;
             blk.src = bp + 4;
             blk.out_len = L;
             blk.nsyms = 0;
@@ -554,6 +564,7 @@ __global__ void k_chain(const InflateJob *jobs, int njobs, const Tables *tabs, J
                         const Cand &c = cands[T.hval[s]];
                         if (c.ok) {
                             blk.type = 1;
+                            blk.ckpt = T.hval[s];
                             blk.src = (uint64_t)T.hval[s] * MAXSYM;
                             blk.nsyms = c.nsyms;
                             blk.out_len = c.out_bytes;
@@ -574,6 +585,7 @@ __global__ void k_chain(const InflateJob *jobs, int njobs, const Tables *tabs, J
                     break;
                 }
                 blk.type = 2;  // symbols in the job's fallback buffer
+                blk.ckpt = ~0ull;
                 blk.src = f0;
                 blk.nsyms = ns;
                 blk.out_len = bytes;
@@ -586,6 +598,9 @@ __global__ void k_chain(const InflateJob *jobs, int njobs, const Tables *tabs, J
             err = true;
             break;
         }
+        blk.nseg = (blk.type == 1 && blk.nsyms > 0) ? (blk.nsyms + SEG - 1) / SEG : 1;
+        blk.seg_base = segs;
+        segs += blk.nseg;
         T.blocks[nb++] = blk;
     }
     if (!err) {
@@ -597,6 +612,7 @@ __global__ void k_chain(const InflateJob *jobs, int njobs, const Tables *tabs, J
     }
     m.nblocks = err ? 0 : (uint32_t)nb;
     m.allzero = !nonzero;
+    m.nseg = err ? 0 : segs;
     if (err) m.status = 1;
 }
 
@@ -604,7 +620,7 @@ __global__ void k_fill_zero(const InflateJob *jobs, const JobMeta *meta) {
     const int j = blockIdx.y;
     if (meta[j].status || !meta[j].allzero) return;
     const InflateJob job = jobs[j];
-    const uint64_t v = job.dst_len / 16;
+    const uint64_t v = (reinterpret_cast<uintptr_t>(job.dst) & 15) ? 0 : job.dst_len / 16;
     uint4 *d4 = reinterpret_cast<uint4 *>(job.dst);  // plane rows are 16-byte aligned
     for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < v; i += (uint64_t)gridDim.x * blockDim.x)
         d4[i] = make_uint4(0, 0, 0, 0);
@@ -617,25 +633,35 @@ __global__ void k_fill_zero(const InflateJob *jobs, const JobMeta *meta) {
 __device__ __forceinline__ bool flag_get(const uint32_t *f, uint64_t i) { return (f[i >> 5] >> (i & 31)) & 1u; }
 
 __global__ void __launch_bounds__(WARPS * 32) k_emit(const InflateJob *jobs, const Tables *tabs, const JobMeta *meta,
-                                                   const uint32_t *pool) {
+                                                   const uint32_t *pool, const uint32_t *ckpt_pool) {
+    // one warp per emit segment (SEG symbols of one block, output offset from the
+    // candidate's checkpoints); copies reaching before the segment become pointers
     const int j = blockIdx.y;
-    const JobMeta &m = meta[j];
-    if (m.status || m.allzero) return;
+    const JobMeta &jm = meta[j];
+    if (jm.status || jm.allzero) return;
     const unsigned w = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const uint64_t bi = (uint64_t)blockIdx.x * WARPS + w;
-    if (bi >= m.nblocks) return;
+    const uint64_t gs = (uint64_t)blockIdx.x * WARPS + w;
+    if (gs >= jm.nseg) return;
     const InflateJob job = jobs[j];
     const Tables T = tabs[j];
-    const Blk blk = T.blocks[bi];
+    uint32_t lo = 0, hi = jm.nblocks - 1;
+    while (lo < hi) {
+        const uint32_t mid = (lo + hi + 1) / 2;
+        if (T.blocks[mid].seg_base <= gs) lo = mid;
+        else hi = mid - 1;
+    }
+    const Blk blk = T.blocks[lo];
+    const uint32_t seg = (uint32_t)(gs - blk.seg_base);
     uint8_t *dst = job.dst;
-    const uint64_t b0 = blk.out_off;
     if (blk.type == 0) {
-        for (uint64_t i = lane; i < blk.out_len; i += 32) dst[b0 + i] = job.src[blk.src + i];
+        for (uint64_t i = lane; i < blk.out_len; i += 32) dst[blk.out_off + i] = job.src[blk.src + i];
         return;
     }
+    const uint32_t s_begin = seg * SEG, s_end = min(blk.nsyms, s_begin + SEG);
+    const uint64_t b0 = blk.out_off + (seg ? ckpt_pool[blk.ckpt * NCKPT + seg] : 0);
     const uint32_t *syms = blk.type == 1 ? pool + blk.src : T.fallback + blk.src;
     uint64_t o = b0;
-    for (uint32_t s = 0; s < blk.nsyms; ++s) {
+    for (uint32_t s = s_begin; s < s_end; ++s) {
         const uint32_t v = syms[s];
         if (!(v & 0x80000000u)) {
             if (lane == 0) dst[o] = (uint8_t)v;
@@ -680,6 +706,28 @@ __global__ void __launch_bounds__(WARPS * 32) k_emit(const InflateJob *jobs, con
 }
 
 // ------------------------------------------------------------------ 5. resolve
+// pointer jumping: ptr[t] <- ptr[ptr[t]] while the target is itself unresolved.  Every
+// pointer always names an earlier byte with the same final value, so concurrent updates
+// are benign; each round halves the remaining chain length.
+__global__ void k_jump(const InflateJob *jobs, const Tables *tabs, const JobMeta *meta) {
+    const int j = blockIdx.y;
+    if (meta[j].status || meta[j].allzero) return;
+    const InflateJob job = jobs[j];
+    const Tables T = tabs[j];
+    const uint64_t words = (job.dst_len + 31) / 32;
+    for (uint64_t wi = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; wi < words;
+         wi += (uint64_t)gridDim.x * blockDim.x) {
+        uint32_t f = T.flags[wi];
+        while (f) {
+            const int bit = __ffs(f) - 1;
+            f &= f - 1;
+            const uint64_t t = wi * 32 + (uint64_t)bit;
+            const uint32_t s = T.ptr[t];
+            if (flag_get(T.flags, s)) T.ptr[t] = T.ptr[s];
+        }
+    }
+}
+
 __global__ void k_resolve(const InflateJob *jobs, const Tables *tabs, const JobMeta *meta) {
     const int j = blockIdx.y;
     if (meta[j].status || meta[j].allzero) return;
@@ -844,11 +892,12 @@ void inflate_batch_host(const std::vector<InflateJob> &jobs, int *status_dev, De
     CK(cudaStreamSynchronize(st));
     const uint64_t nc = std::min<uint64_t>(hc, cand_cap);
     uint32_t *pool = static_cast<uint32_t *>(alloc.get(std::max<uint64_t>(nc, 1) * MAXSYM * 4, st));
+    uint32_t *ckpt = static_cast<uint32_t *>(alloc.get(std::max<uint64_t>(nc, 1) * NCKPT * 4, st));
     {
         ProfScope ps("inflate.decode", st, total_src);
         if (nc) {
             const unsigned g = (unsigned)std::min<uint64_t>((nc + WARPS - 1) / WARPS, 148ull * 16);
-            k_decode_cands<<<g, WARPS * 32, 0, st>>>(jd, cands, ncand, cand_cap, pool);
+            k_decode_cands<<<g, WARPS * 32, 0, st>>>(jd, cands, ncand, cand_cap, pool, ckpt);
             CKL();
         }
         k_chain<<<(n + 31) / 32, 32, 0, st>>>(jd, n, td, md, cands);
@@ -859,17 +908,30 @@ void inflate_batch_host(const std::vector<InflateJob> &jobs, int *status_dev, De
         std::vector<JobMeta> hm(n);
         CK(cudaMemcpyAsync(hm.data(), md, n * sizeof(JobMeta), cudaMemcpyDeviceToHost, st));
         CK(cudaStreamSynchronize(st));
-        uint64_t maxb = 1;
-        for (const JobMeta &m : hm) maxb = std::max<uint64_t>(maxb, m.nblocks);
+        uint64_t maxseg = 1;
+        for (const JobMeta &m : hm) maxseg = std::max<uint64_t>(maxseg, m.nseg);
+        if (getenv("IPCG_DEBUG_INFLATE")) {
+            for (int q = 0; q < n; ++q)
+                fprintf(stderr, "inflate job %d: src %llu dst %llu blocks %u allzero %d status %d\n", q,
+                        (unsigned long long)jobs[q].src_len, (unsigned long long)jobs[q].dst_len, hm[q].nblocks,
+                        hm[q].allzero, hm[q].status);
+        }
         {
             ProfScope ps2("inflate.emit_blocks", st, max_dst * n);
-            k_emit<<<dim3((unsigned)((maxb + WARPS - 1) / WARPS), n), WARPS * 32, 0, st>>>(jd, td, md, pool);
+            k_emit<<<dim3((unsigned)((maxseg + WARPS - 1) / WARPS), n), WARPS * 32, 0, st>>>(jd, td, md, pool, ckpt);
             CKL();
             k_fill_zero<<<dim3(grid_for(max_dst / 16 + 1, 256, 512), n), 256, 0, st>>>(jd, md);
             CKL();
         }
         {
             ProfScope ps3("inflate.resolve", st, max_dst * n / 8);
+            // pointers chain backwards through at most maxseg segments: halve the depth per round
+            int rounds = 0;
+            while ((1ull << rounds) < maxseg) ++rounds;
+            for (int r = 0; r < rounds; ++r) {
+                k_jump<<<dim3(grid_for((max_dst + 31) / 32, 256, 1024), n), 256, 0, st>>>(jd, td, md);
+                CKL();
+            }
             k_resolve<<<dim3(grid_for((max_dst + 31) / 32, 256, 1024), n), 256, 0, st>>>(jd, td, md);
             CKL();
         }

@@ -245,11 +245,13 @@ ipcg_archive *compress_impl(ipcg_ctx *c, int scalar, const void *values, int on_
         // loss table (measure_loss_table): replay per dropped-digit count d
         {
             ProfScope psl("loss_table", st, lg.count * 4);
-            for (int d = 1; d <= 32; ++d)
-                for (const PassDesc &pd : lg.passes)
-                    launch_loss_pass(nb.as<uint32_t>(), dev.as<double>(), pd, cubic, 2.0 * eb, d, &sd->lowor[li],
-                                     sd->raw[li], st);
-            for (const PassDesc &pd : lg.passes) launch_zero_pass(dev.as<double>(), pd, st);
+            if (!launch_loss_fused(nb.as<uint32_t>(), G, level, cubic, 2.0 * eb, &sd->lowor[li], sd->raw[li], st)) {
+                for (int d = 1; d <= 32; ++d)
+                    for (const PassDesc &pd : lg.passes)
+                        launch_loss_pass(nb.as<uint32_t>(), dev.as<double>(), pd, cubic, 2.0 * eb, d, &sd->lowor[li],
+                                         sd->raw[li], st);
+                for (const PassDesc &pd : lg.passes) launch_zero_pass(dev.as<double>(), pd, st);
+            }
             launch_loss_finalize(sd->raw[li], &sd->lowor[li], sd->delta[li], st);
         }
         if (planes[li].p) CK(cudaMemsetAsync(planes[li].p, 0, 32 * plane_stride[li] * 4, st));

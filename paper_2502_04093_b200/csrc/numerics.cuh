@@ -35,6 +35,10 @@ void launch_bitplanes(const uint32_t *nb, uint64_t count, uint32_t *planes, uint
 void launch_loss_pass(const uint32_t *nb, double *dev, const PassDesc &pd, bool cubic, double unit, int d,
                       const uint32_t *lowor, unsigned long long *rawbits, cudaStream_t st);
 void launch_zero_pass(double *dev, const PassDesc &pd, cudaStream_t st);
+// one launch per level (levels below the coarsest): all d replayed in shared-memory tiles;
+// returns false when the level's geometry needs the per-pass path
+bool launch_loss_fused(const uint32_t *nb, const Geometry &G, int level, bool cubic, double unit,
+                       const uint32_t *lowor, unsigned long long *raw, cudaStream_t st);
 void launch_loss_finalize(const unsigned long long *rawbits, const uint32_t *lowor, double *delta, cudaStream_t st);
 void launch_sort_outliers(OutlierSink sink, uint64_t count, uint64_t *ord_sorted, uint64_t *bits_sorted,
                           void *temp, size_t temp_bytes, cudaStream_t st);
