@@ -231,15 +231,70 @@ __global__ void __launch_bounds__(PL_WARPS * 32) k_prevlinks(const uint8_t *in, 
 }
 
 // ------------------------------------------------------------ 3. match search
+// One CTA per MT-position tile.  Hash chains mostly point a short way back (dense
+// chains such as the all-zero triple are local), so the tile's bytes and links plus a
+// BACK-position look-back are staged in shared memory; older candidates read global.
+constexpr int MT = 4096, BACK = 8192, MWIN = MT + BACK + MAX_MATCH + 16;
+
+struct TileBytes {
+    const uint8_t *g;     // global stream base (8-byte aligned)
+    const uint64_t *s;    // staged words covering [w0, w1)
+    int64_t w0, w1;       // w0 is a multiple of 8
+    __device__ __forceinline__ uint32_t operator()(int64_t i) const {
+        if (i >= w0 && i < w1) return (uint32_t)((s[(i - w0) >> 3] >> (8 * ((i - w0) & 7))) & 0xff);
+        return __ldg(g + i);
+    }
+    __device__ __forceinline__ uint64_t load8(int64_t i) const {
+        if (i >= w0 && i + 8 <= w1) {
+            const int64_t r = i - w0;
+            const unsigned sh = (unsigned)(r & 7) * 8;
+            const uint64_t lo = s[r >> 3];
+            return sh ? (lo >> sh) | (s[(r >> 3) + 1] << (64 - sh)) : lo;
+        }
+        return InBytes{g}.load8(i);
+    }
+    __device__ __forceinline__ int64_t match_len(int64_t a, int64_t b, int64_t maxlen) const {
+        int64_t len = 0;
+        for (; len + 8 <= maxlen; len += 8) {
+            const uint64_t x = load8(a + len) ^ load8(b + len);
+            if (x) return len + (__ffsll((long long)x) - 1) / 8;
+        }
+        while (len < maxlen && (*this)(a + len) == (*this)(b + len)) ++len;
+        return len;
+    }
+};
+
+struct TilePrev {
+    const uint16_t *g, *s;
+    int64_t w0, w1;
+    __device__ __forceinline__ uint32_t operator()(int64_t i) const {
+        return (i >= w0 && i < w1) ? s[i - w0] : __ldg(g + i);
+    }
+};
+
 __global__ void __launch_bounds__(256) k_match(const uint8_t *in, uint64_t in_stride, uint64_t n,
                                               const StreamMeta *meta, const uint16_t *prevd_all, uint64_t *rec_all) {
+    __shared__ uint64_t sb[MWIN / 8 + 2];
+    __shared__ uint16_t sp[MT + BACK];
     const int j = blockIdx.y;
     if (!meta[j].active) return;
-    const InBytes bytes{in + (uint64_t)j * in_stride};
-    const PrevD prev{prevd_all + (uint64_t)j * n};
+    const int64_t p0 = (int64_t)blockIdx.x * MT;
+    if (p0 >= (int64_t)n) return;
+    const int64_t p1 = min((int64_t)n, p0 + MT);
+    const uint8_t *base = in + (uint64_t)j * in_stride;
+    const uint16_t *prevd = prevd_all + (uint64_t)j * n;
+    const int64_t w0 = p0 - BACK > 0 ? ((p0 - BACK) & ~int64_t(7)) : 0;
+    const int64_t w1 = min((int64_t)n, p1 + MAX_MATCH + 8);
+    const int64_t nw = (w1 - w0 + 7) / 8;
+    const uint64_t *gw = reinterpret_cast<const uint64_t *>(base + w0);
+    for (int64_t i = threadIdx.x; i < nw; i += blockDim.x) sb[i] = __ldg(gw + i);  // rows are padded: safe
+    const int64_t pw0 = w0, pw1 = p1;
+    for (int64_t i = pw0 + threadIdx.x; i < pw1; i += blockDim.x) sp[i - pw0] = __ldg(prevd + i);
+    __syncthreads();
+    const TileBytes bytes{base, sb, w0, w0 + nw * 8 < w1 ? w0 + nw * 8 : w1};
+    const TilePrev prev{prevd, sp, pw0, pw1};
     uint64_t *rec = rec_all + (uint64_t)j * n;
-    for (uint64_t p = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; p < n; p += (uint64_t)gridDim.x * blockDim.x)
-        rec[p] = match_search((int64_t)p, (int64_t)n, bytes, prev);
+    for (int64_t p = p0 + threadIdx.x; p < p1; p += blockDim.x) rec[p] = match_search(p, (int64_t)n, bytes, prev);
 }
 
 // ---------------------------------------------------------------- 4. anchors
@@ -864,7 +919,7 @@ void DeflateBatch::run(const uint8_t *in, uint64_t in_stride, int S, uint64_t n,
         }
         {
         ProfScope ps2("deflate.match", st, (uint64_t)S * n * 11);
-        k_match<<<dim3(grid_for(n, 256, 4096), S), 256, 0, st>>>(in, in_stride, n, w.meta, w.prevd, w.rec);
+        k_match<<<dim3((unsigned)((n + MT - 1) / MT), S), 256, 0, st>>>(in, in_stride, n, w.meta, w.prevd, w.rec);
         CKL();
         }
         {
