@@ -274,27 +274,15 @@ struct TilePrev {
 
 __global__ void __launch_bounds__(256) k_match(const uint8_t *in, uint64_t in_stride, uint64_t n,
                                               const StreamMeta *meta, const uint16_t *prevd_all, uint64_t *rec_all) {
-    __shared__ uint64_t sb[MWIN / 8 + 2];
-    __shared__ uint16_t sp[MT + BACK];
+    // (measured: staging the tile in shared memory was slower than L1-cached __ldg --
+    // the chain walk is latency/instruction bound -- so the kernel reads global memory)
     const int j = blockIdx.y;
     if (!meta[j].active) return;
-    const int64_t p0 = (int64_t)blockIdx.x * MT;
-    if (p0 >= (int64_t)n) return;
-    const int64_t p1 = min((int64_t)n, p0 + MT);
-    const uint8_t *base = in + (uint64_t)j * in_stride;
-    const uint16_t *prevd = prevd_all + (uint64_t)j * n;
-    const int64_t w0 = p0 - BACK > 0 ? ((p0 - BACK) & ~int64_t(7)) : 0;
-    const int64_t w1 = min((int64_t)n, p1 + MAX_MATCH + 8);
-    const int64_t nw = (w1 - w0 + 7) / 8;
-    const uint64_t *gw = reinterpret_cast<const uint64_t *>(base + w0);
-    for (int64_t i = threadIdx.x; i < nw; i += blockDim.x) sb[i] = __ldg(gw + i);  // rows are padded: safe
-    const int64_t pw0 = w0, pw1 = p1;
-    for (int64_t i = pw0 + threadIdx.x; i < pw1; i += blockDim.x) sp[i - pw0] = __ldg(prevd + i);
-    __syncthreads();
-    const TileBytes bytes{base, sb, w0, w0 + nw * 8 < w1 ? w0 + nw * 8 : w1};
-    const TilePrev prev{prevd, sp, pw0, pw1};
+    const InBytes bytes{in + (uint64_t)j * in_stride};
+    const PrevD prev{prevd_all + (uint64_t)j * n};
     uint64_t *rec = rec_all + (uint64_t)j * n;
-    for (int64_t p = p0 + threadIdx.x; p < p1; p += blockDim.x) rec[p] = match_search(p, (int64_t)n, bytes, prev);
+    for (uint64_t p = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; p < n; p += (uint64_t)gridDim.x * blockDim.x)
+        rec[p] = match_search((int64_t)p, (int64_t)n, bytes, prev);
 }
 
 // ---------------------------------------------------------------- 4. anchors
@@ -919,7 +907,7 @@ void DeflateBatch::run(const uint8_t *in, uint64_t in_stride, int S, uint64_t n,
         }
         {
         ProfScope ps2("deflate.match", st, (uint64_t)S * n * 11);
-        k_match<<<dim3((unsigned)((n + MT - 1) / MT), S), 256, 0, st>>>(in, in_stride, n, w.meta, w.prevd, w.rec);
+        k_match<<<dim3(grid_for(n, 256, 4096), S), 256, 0, st>>>(in, in_stride, n, w.meta, w.prevd, w.rec);
         CKL();
         }
         {

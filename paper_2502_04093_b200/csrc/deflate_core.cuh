@@ -99,6 +99,22 @@ HD uint64_t match_search(int64_t p, int64_t n, const Bytes &bytes, const Prev &p
             d32 = bestd;
         }
         if (stop) break;
+        if (i == 1 && q == p - 1 && len >= MIN_MATCH) {
+            // p-1 starts a run of one byte value v covering [p-1, p-1+best].  The chain
+            // continues p-2, p-3, ... down to the run start r (all hash(v,v,v)), and each of
+            // those candidates fails the quick reject (its byte at +best is still v, the byte
+            // at p+best is not).  Consume them in one step; results are unchanged.
+            const uint32_t v = bytes(p - 1);
+            const int64_t floor_ = (limit + 1) > (p - (int64_t)MAX_CHAIN) ? (limit + 1) : (p - (int64_t)MAX_CHAIN);
+            int64_t r = p - 1;
+            while (r - 1 >= floor_ && bytes(r - 1) == v) --r;
+            const int consumed = (int)(p - 1 - r);  // candidates p-2 .. r
+            if (consumed > 0) {
+                i += consumed;
+                if (i >= MAX_CHAIN) break;
+                q = r;
+            }
+        }
         const uint32_t dq = prevd(q);
         if (dq == 0) break;
         const int64_t q2 = q - (int64_t)dq;

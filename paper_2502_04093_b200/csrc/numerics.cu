@@ -266,15 +266,19 @@ __global__ void k_outlier_block(const uint64_t *ord, const uint64_t *bits, const
 
 // ------------------------------------------------------------------- merge
 // xor_decode + merge (bitplane.cpp:24-59), and refine's digit folding with the XOR
-// prefix taken from already-merged codewords (pipeline.hpp:328-339): one warp per
-// 32 codewords; lane p owns plane p's word.
-__global__ void __launch_bounds__(256) k_merge(const uint32_t *const *__restrict__ rows,
-                                               const uint32_t *__restrict__ merged_in, uint32_t *__restrict__ merged_out,
-                                               uint64_t count, int k0, int k1) {
-    const unsigned lane = threadIdx.x & 31;
+// prefix taken from already-merged codewords (pipeline.hpp:328-339).  A CTA takes 32
+// plane words x 32 planes: warp p loads plane p's 128-byte row segment (coalesced) into
+// a padded smem tile, then warp w owns word w with lane p holding plane p's bits.
+__global__ void __launch_bounds__(1024) k_merge(const uint32_t *const *__restrict__ rows,
+                                                const uint32_t *__restrict__ merged_in,
+                                                uint32_t *__restrict__ merged_out, uint64_t count, int k0, int k1) {
+    __shared__ uint32_t tile[32][33];
+    const unsigned warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const uint64_t words = (count + 31) / 32;
-    for (uint64_t w = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5; w < words;
-         w += ((uint64_t)gridDim.x * blockDim.x) >> 5) {
+    for (uint64_t w0 = (uint64_t)blockIdx.x * 32; w0 < words; w0 += (uint64_t)gridDim.x * 32) {
+        tile[warp][lane] = ((int)warp >= k0 && (int)warp < k1 && w0 + lane < words) ? rows[warp][w0 + lane] : 0u;
+        __syncthreads();
+        const uint64_t w = w0 + warp;
         const uint64_t i = w * 32 + lane;
         const uint32_t mi = (merged_in && i < count) ? merged_in[i] : 0u;
         uint32_t bp = 0;
@@ -282,7 +286,7 @@ __global__ void __launch_bounds__(256) k_merge(const uint32_t *const *__restrict
             const uint32_t m = __ballot_sync(0xffffffffu, (mi >> (31 - p)) & 1u);
             if ((int)lane == p) bp = m;
         }
-        const uint32_t e = ((int)lane >= k0 && (int)lane < k1) ? rows[lane][w] : 0u;
+        const uint32_t e = tile[lane][warp];
         for (int p = k0; p < k1; ++p) {
             const uint32_t b1 = __shfl_sync(0xffffffffu, bp, (p - 1) & 31);
             const uint32_t b2 = __shfl_sync(0xffffffffu, bp, (p - 2) & 31);
@@ -294,7 +298,8 @@ __global__ void __launch_bounds__(256) k_merge(const uint32_t *const *__restrict
             const uint32_t m = __ballot_sync(0xffffffffu, (bp >> b) & 1u);
             if ((int)lane == b) out = __brev(m);
         }
-        if (i < count) merged_out[i] = out;
+        if (w < words && i < count) merged_out[i] = out;
+        __syncthreads();
     }
 }
 
@@ -435,8 +440,8 @@ void launch_merge(const uint32_t *const *rows, const uint32_t *merged_in, uint32
                   int k1, cudaStream_t st) {
     const uint64_t words = (count + 31) / 32;
     if (words == 0) return;
-    const unsigned g = grid_for(words * 32, 256);
-    k_merge<<<g, 256, 0, st>>>(rows, merged_in, merged_out, count, k0, k1);
+    const unsigned g = (unsigned)std::min<uint64_t>((words + 31) / 32, 148ull * 2 * 8);
+    k_merge<<<g, 1024, 0, st>>>(rows, merged_in, merged_out, count, k0, k1);
     CKL();
 }
 
