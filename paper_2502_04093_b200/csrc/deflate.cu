@@ -209,23 +209,34 @@ __global__ void __launch_bounds__(PL_WARPS * 32) k_prevlinks(const uint8_t *in, 
     uint16_t *prevd = prevd_all + (uint64_t)j * n;
     const uint64_t base = blk == 0 ? 0 : (blk - 1) * WSIZE;
     const uint64_t out0 = blk * WSIZE, end = min(n, (blk + 1) * WSIZE);
-    for (uint64_t pos = base; pos < end; pos += 32) {
-        const uint64_t q = pos + lane;
-        const bool valid = q + MIN_MATCH <= n && q < end;
-        const uint32_t h = valid ? hash3(p[q], p[q + 1], p[q + 2]) : (0x10000u + lane);
-        const uint32_t rel = (uint32_t)(q - base);
-        const unsigned mask = __match_any_sync(0xffffffffu, h);
-        const unsigned lower = mask & ((1u << lane) - 1u);
-        uint32_t prel = 0xFFFF;
-        if (lower) prel = rel - (lane - (31u - __clz(lower)));
-        else if (valid) prel = head[h];
-        __syncwarp();
-        if (valid && lane == 31u - __clz(mask)) head[h] = (uint16_t)rel;
-        __syncwarp();
-        if (q >= out0 && q < end) {
-            uint32_t d = 0;
-            if (valid && prel != 0xFFFF && rel - prel < (uint32_t)WSIZE) d = rel - prel;
-            prevd[q] = (uint16_t)d;
+    constexpr int AHEAD = 8;  // hashes of 8 steps are loaded up front so their loads overlap
+    for (uint64_t pos0 = base; pos0 < end; pos0 += 32 * AHEAD) {
+        uint32_t hs[AHEAD];
+#pragma unroll
+        for (int k = 0; k < AHEAD; ++k) {
+            const uint64_t q = pos0 + 32 * k + lane;
+            const bool valid = q + MIN_MATCH <= n && q < end;
+            hs[k] = valid ? hash3(__ldg(p + q), __ldg(p + q + 1), __ldg(p + q + 2)) : (0x10000u + lane);
+        }
+#pragma unroll
+        for (int k = 0; k < AHEAD; ++k) {
+            const uint64_t q = pos0 + 32 * k + lane;
+            const uint32_t h = hs[k];
+            const bool valid = h < 0x10000u;
+            const uint32_t rel = (uint32_t)(q - base);
+            const unsigned mask = __match_any_sync(0xffffffffu, h);
+            const unsigned lower = mask & ((1u << lane) - 1u);
+            uint32_t prel = 0xFFFF;
+            if (lower) prel = rel - (lane - (31u - __clz(lower)));
+            else if (valid) prel = head[h];
+            __syncwarp();
+            if (valid && lane == 31u - __clz(mask)) head[h] = (uint16_t)rel;
+            __syncwarp();
+            if (q >= out0 && q < end) {
+                uint32_t d = 0;
+                if (valid && prel != 0xFFFF && rel - prel < (uint32_t)WSIZE) d = rel - prel;
+                prevd[q] = (uint16_t)d;
+            }
         }
     }
 }
@@ -274,15 +285,41 @@ struct TilePrev {
 
 __global__ void __launch_bounds__(256) k_match(const uint8_t *in, uint64_t in_stride, uint64_t n,
                                               const StreamMeta *meta, const uint16_t *prevd_all, uint64_t *rec_all) {
-    // (measured: staging the tile in shared memory was slower than L1-cached __ldg --
-    // the chain walk is latency/instruction bound -- so the kernel reads global memory)
+    // Chain lengths vary from 0 to 128 candidates between neighbouring positions, so a warp
+    // that evaluated one position per lane would run at the pace of its longest chain (ncu:
+    // 30 G warp-instructions for 205 M positions).  Each lane instead runs the search state
+    // machine one candidate per iteration and starts its next position (lane-strided within
+    // the warp's segment) the moment the current one finishes.  (Staging the tile in shared
+    // memory was measured slower than L1-cached __ldg: the walk is not bandwidth bound.)
     const int j = blockIdx.y;
     if (!meta[j].active) return;
     const InBytes bytes{in + (uint64_t)j * in_stride};
     const PrevD prev{prevd_all + (uint64_t)j * n};
     uint64_t *rec = rec_all + (uint64_t)j * n;
-    for (uint64_t p = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; p < n; p += (uint64_t)gridDim.x * blockDim.x)
-        rec[p] = match_search((int64_t)p, (int64_t)n, bytes, prev);
+    const unsigned lane = threadIdx.x & 31;
+    const uint64_t warps_total = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+    const uint64_t seg = 32 * 64;  // positions per warp segment (64 per lane)
+    for (uint64_t s0 = ((blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5) * seg; s0 < n;
+         s0 += warps_total * seg) {
+        uint64_t next = s0 + lane;
+        const uint64_t end = s0 + seg < n ? s0 + seg : n;
+        MatchState st;
+        st.done = 1;
+        bool have = false;
+        for (;;) {
+            if (!have) {
+                if (next >= end) break;
+                match_init(st, (int64_t)next, (int64_t)n, bytes, prev);
+                next += 32;
+                have = true;
+            }
+            if (!st.done) match_step(st, bytes, prev);
+            if (st.done) {
+                rec[st.p] = match_result(st);
+                have = false;
+            }
+        }
+    }
 }
 
 // ---------------------------------------------------------------- 4. anchors
@@ -907,7 +944,7 @@ void DeflateBatch::run(const uint8_t *in, uint64_t in_stride, int S, uint64_t n,
         }
         {
         ProfScope ps2("deflate.match", st, (uint64_t)S * n * 11);
-        k_match<<<dim3(grid_for(n, 256, 4096), S), 256, 0, st>>>(in, in_stride, n, w.meta, w.prevd, w.rec);
+        k_match<<<dim3((unsigned)((n + 8 * 2048 - 1) / (8 * 2048)), S), 256, 0, st>>>(in, in_stride, n, w.meta, w.prevd, w.rec);
         CKL();
         }
         {

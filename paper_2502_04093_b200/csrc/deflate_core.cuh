@@ -58,70 +58,92 @@ HD uint32_t mrec_flag(uint64_t r) { return (uint32_t)((r >> 48) & 1); }
 // are capped at the lookahead, which is equivalent to zlib's garbage-tolerant scan
 // because nice_match is capped at the lookahead too (the first candidate reaching
 // the data end always terminates the search).
+// The search is a small state machine (init + one candidate per step) so a GPU lane can
+// interleave many positions and never idle behind a neighbour's long chain.
+struct MatchState {
+    int64_t p, q, maxlen, nice, limit;
+    uint32_t best, bestd, l32, d32, flag;
+    int i;     // index of the candidate q (1-based)
+    int done;  // 1 once the search has terminated
+};
+
 template <class Bytes, class Prev>
-HD uint64_t match_search(int64_t p, int64_t n, const Bytes &bytes, const Prev &prevd) {
-    if (p + MIN_MATCH > n) return 0;  // not inserted: hash_head = NIL
+HD void match_init(MatchState &s, int64_t p, int64_t n, const Bytes &, const Prev &prevd) {
+    s.p = p;
+    s.best = s.bestd = s.l32 = s.d32 = s.flag = 0;
+    s.i = 1;
+    s.done = 1;
+    if (p + MIN_MATCH > n) return;  // not inserted: hash_head = NIL
     const uint32_t d0 = prevd(p);
-    if (d0 == 0) return 0;
-    int64_t q = p - (int64_t)d0;
-    if (q == 0 || d0 > (uint32_t)MAX_DIST) return 0;  // NIL / too far for the head check
-    const uint32_t flag = d0 == (uint32_t)MAX_DIST;
-    const int64_t maxlen = (n - p) < MAX_MATCH ? (n - p) : MAX_MATCH;
-    const int64_t nice = (n - p) < NICE_LENGTH ? (n - p) : NICE_LENGTH;
-    const int64_t limit = p - MAX_DIST > 0 ? p - MAX_DIST : 0;
-    uint32_t best = 0, bestd = 0, l32 = 0, d32 = 0;
-    for (int i = 1; i <= MAX_CHAIN; ++i) {
-        // zlib's quick reject: a candidate that differs at best or best-1 cannot beat best
-        if (best >= MIN_MATCH && (int64_t)best < maxlen &&
-            (bytes(q + best) != bytes(p + best) || bytes(q + best - 1) != bytes(p + best - 1))) {
-            if (i <= 32) {
-                l32 = best;
-                d32 = bestd;
-            }
-            const uint32_t dq = prevd(q);
-            if (dq == 0) break;
-            const int64_t q2 = q - (int64_t)dq;
-            if (!(q2 > limit)) break;
-            q = q2;
-            continue;
-        }
+    if (d0 == 0) return;
+    s.q = p - (int64_t)d0;
+    if (s.q == 0 || d0 > (uint32_t)MAX_DIST) return;  // NIL / too far for the head check
+    s.flag = d0 == (uint32_t)MAX_DIST;
+    s.maxlen = (n - p) < MAX_MATCH ? (n - p) : MAX_MATCH;
+    s.nice = (n - p) < NICE_LENGTH ? (n - p) : NICE_LENGTH;
+    s.limit = p - MAX_DIST > 0 ? p - MAX_DIST : 0;
+    s.done = 0;
+}
+
+// evaluate candidate s.i at s.q, then move to the next candidate (or finish)
+template <class Bytes, class Prev>
+HD void match_step(MatchState &s, const Bytes &bytes, const Prev &prevd) {
+    const int64_t p = s.p, q = s.q;
+    // zlib's quick reject: a candidate that differs at best or best-1 cannot beat best
+    const bool reject = s.best >= MIN_MATCH && (int64_t)s.best < s.maxlen &&
+                        (bytes(q + s.best) != bytes(p + s.best) || bytes(q + s.best - 1) != bytes(p + s.best - 1));
+    int64_t next_from = q;
+    if (!reject) {
         // match length between p and q (>= 3 only when bytes 0,1 agree: hash implies byte 2)
-        const int64_t len0 = bytes.match_len(p, q, maxlen);
+        const int64_t len0 = bytes.match_len(p, q, s.maxlen);
         const int64_t len = len0 < MIN_MATCH ? 0 : len0;
-        bool stop = false;
-        if ((uint32_t)len > best) {
-            best = (uint32_t)len;
-            bestd = (uint32_t)(p - q);
-            if (len >= nice) stop = true;
+        if ((uint32_t)len > s.best) {
+            s.best = (uint32_t)len;
+            s.bestd = (uint32_t)(p - q);
+            if (len >= s.nice) {
+                if (s.i <= 32) s.l32 = s.best, s.d32 = s.bestd;
+                s.done = 1;
+                return;
+            }
         }
-        if (i <= 32) {
-            l32 = best;
-            d32 = bestd;
-        }
-        if (stop) break;
-        if (i == 1 && q == p - 1 && len >= MIN_MATCH) {
+        if (s.i == 1 && q == p - 1 && len >= MIN_MATCH) {
             // p-1 starts a run of one byte value v covering [p-1, p-1+best].  The chain
             // continues p-2, p-3, ... down to the run start r (all hash(v,v,v)), and each of
             // those candidates fails the quick reject (its byte at +best is still v, the byte
             // at p+best is not).  Consume them in one step; results are unchanged.
+            if (s.i <= 32) s.l32 = s.best, s.d32 = s.bestd;
             const uint32_t v = bytes(p - 1);
-            const int64_t floor_ = (limit + 1) > (p - (int64_t)MAX_CHAIN) ? (limit + 1) : (p - (int64_t)MAX_CHAIN);
+            const int64_t lo = p - (int64_t)MAX_CHAIN;
+            const int64_t floor_ = (s.limit + 1) > lo ? (s.limit + 1) : lo;
             int64_t r = p - 1;
             while (r - 1 >= floor_ && bytes(r - 1) == v) --r;
-            const int consumed = (int)(p - 1 - r);  // candidates p-2 .. r
-            if (consumed > 0) {
-                i += consumed;
-                if (i >= MAX_CHAIN) break;
-                q = r;
+            s.i += (int)(p - 1 - r);  // candidates p-2 .. r consumed
+            if (s.i >= MAX_CHAIN) {
+                s.done = 1;
+                return;
             }
+            next_from = r;
         }
-        const uint32_t dq = prevd(q);
-        if (dq == 0) break;
-        const int64_t q2 = q - (int64_t)dq;
-        if (!(q2 > limit)) break;
-        q = q2;
     }
-    return mrec_pack(best, bestd, l32, d32, flag);
+    if (s.i <= 32) s.l32 = s.best, s.d32 = s.bestd;
+    const uint32_t dq = prevd(next_from);
+    const int64_t q2 = next_from - (int64_t)dq;
+    if (dq == 0 || !(q2 > s.limit) || s.i >= MAX_CHAIN) {
+        s.done = 1;
+        return;
+    }
+    s.q = q2;
+    s.i += 1;
+}
+
+HD uint64_t match_result(const MatchState &s) { return mrec_pack(s.best, s.bestd, s.l32, s.d32, s.flag); }
+
+template <class Bytes, class Prev>
+HD uint64_t match_search(int64_t p, int64_t n, const Bytes &bytes, const Prev &prevd) {
+    MatchState s;
+    match_init(s, p, n, bytes, prevd);
+    while (!s.done) match_step(s, bytes, prevd);
+    return match_result(s);
 }
 
 // ------------------------------------------------------------- window slides
