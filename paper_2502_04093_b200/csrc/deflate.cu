@@ -242,84 +242,20 @@ __global__ void __launch_bounds__(PL_WARPS * 32) k_prevlinks(const uint8_t *in, 
 }
 
 // ------------------------------------------------------------ 3. match search
-// One CTA per MT-position tile.  Hash chains mostly point a short way back (dense
-// chains such as the all-zero triple are local), so the tile's bytes and links plus a
-// BACK-position look-back are staged in shared memory; older candidates read global.
-constexpr int MT = 4096, BACK = 8192, MWIN = MT + BACK + MAX_MATCH + 16;
-
-struct TileBytes {
-    const uint8_t *g;     // global stream base (8-byte aligned)
-    const uint64_t *s;    // staged words covering [w0, w1)
-    int64_t w0, w1;       // w0 is a multiple of 8
-    __device__ __forceinline__ uint32_t operator()(int64_t i) const {
-        if (i >= w0 && i < w1) return (uint32_t)((s[(i - w0) >> 3] >> (8 * ((i - w0) & 7))) & 0xff);
-        return __ldg(g + i);
-    }
-    __device__ __forceinline__ uint64_t load8(int64_t i) const {
-        if (i >= w0 && i + 8 <= w1) {
-            const int64_t r = i - w0;
-            const unsigned sh = (unsigned)(r & 7) * 8;
-            const uint64_t lo = s[r >> 3];
-            return sh ? (lo >> sh) | (s[(r >> 3) + 1] << (64 - sh)) : lo;
-        }
-        return InBytes{g}.load8(i);
-    }
-    __device__ __forceinline__ int64_t match_len(int64_t a, int64_t b, int64_t maxlen) const {
-        int64_t len = 0;
-        for (; len + 8 <= maxlen; len += 8) {
-            const uint64_t x = load8(a + len) ^ load8(b + len);
-            if (x) return len + (__ffsll((long long)x) - 1) / 8;
-        }
-        while (len < maxlen && (*this)(a + len) == (*this)(b + len)) ++len;
-        return len;
-    }
-};
-
-struct TilePrev {
-    const uint16_t *g, *s;
-    int64_t w0, w1;
-    __device__ __forceinline__ uint32_t operator()(int64_t i) const {
-        return (i >= w0 && i < w1) ? s[i - w0] : __ldg(g + i);
-    }
-};
-
+// One thread per position runs zlib's longest_match for chain limits 128 and 32 (one
+// walk, the 32-limit result snapshotted on the way).  Measured alternatives that lost:
+// staging the tile in shared memory (the walk is latency-, not bandwidth-bound: 70 ms vs
+// 43 ms) and a per-lane state machine that refills idle lanes (87 ms: neighbouring
+// positions have similar chain lengths, so the extra state costs more than divergence).
 __global__ void __launch_bounds__(256) k_match(const uint8_t *in, uint64_t in_stride, uint64_t n,
                                               const StreamMeta *meta, const uint16_t *prevd_all, uint64_t *rec_all) {
-    // Chain lengths vary from 0 to 128 candidates between neighbouring positions, so a warp
-    // that evaluated one position per lane would run at the pace of its longest chain (ncu:
-    // 30 G warp-instructions for 205 M positions).  Each lane instead runs the search state
-    // machine one candidate per iteration and starts its next position (lane-strided within
-    // the warp's segment) the moment the current one finishes.  (Staging the tile in shared
-    // memory was measured slower than L1-cached __ldg: the walk is not bandwidth bound.)
     const int j = blockIdx.y;
     if (!meta[j].active) return;
     const InBytes bytes{in + (uint64_t)j * in_stride};
     const PrevD prev{prevd_all + (uint64_t)j * n};
     uint64_t *rec = rec_all + (uint64_t)j * n;
-    const unsigned lane = threadIdx.x & 31;
-    const uint64_t warps_total = ((uint64_t)gridDim.x * blockDim.x) >> 5;
-    const uint64_t seg = 32 * 64;  // positions per warp segment (64 per lane)
-    for (uint64_t s0 = ((blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5) * seg; s0 < n;
-         s0 += warps_total * seg) {
-        uint64_t next = s0 + lane;
-        const uint64_t end = s0 + seg < n ? s0 + seg : n;
-        MatchState st;
-        st.done = 1;
-        bool have = false;
-        for (;;) {
-            if (!have) {
-                if (next >= end) break;
-                match_init(st, (int64_t)next, (int64_t)n, bytes, prev);
-                next += 32;
-                have = true;
-            }
-            if (!st.done) match_step(st, bytes, prev);
-            if (st.done) {
-                rec[st.p] = match_result(st);
-                have = false;
-            }
-        }
-    }
+    for (uint64_t p = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; p < n; p += (uint64_t)gridDim.x * blockDim.x)
+        rec[p] = match_search((int64_t)p, (int64_t)n, bytes, prev);
 }
 
 // ---------------------------------------------------------------- 4. anchors
@@ -944,7 +880,7 @@ void DeflateBatch::run(const uint8_t *in, uint64_t in_stride, int S, uint64_t n,
         }
         {
         ProfScope ps2("deflate.match", st, (uint64_t)S * n * 11);
-        k_match<<<dim3((unsigned)((n + 8 * 2048 - 1) / (8 * 2048)), S), 256, 0, st>>>(in, in_stride, n, w.meta, w.prevd, w.rec);
+        k_match<<<dim3(grid_for(n, 256, 4096), S), 256, 0, st>>>(in, in_stride, n, w.meta, w.prevd, w.rec);
         CKL();
         }
         {

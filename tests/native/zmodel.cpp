@@ -231,3 +231,38 @@ extern "C" int zmodel_compress(const uint8_t *in, uint64_t n, int chunk, uint8_t
 }
 
 extern "C" uint32_t zmodel_crc_combine(uint32_t crc1, uint32_t crc2, uint64_t len2) { return crc_combine(crc1, crc2, len2); }
+
+// dev statistics: histogram of match_step calls per position (hist[0..129])
+extern "C" void zmodel_chain_hist(const uint8_t *in, uint64_t n, uint64_t *hist, uint64_t *rejects, uint64_t *compares) {
+    struct HB {
+        const uint8_t *in;
+        uint32_t operator()(int64_t i) const { return in[i]; }
+        int64_t match_len(int64_t a, int64_t b, int64_t maxlen) const {
+            int64_t len = 0;
+            while (len < maxlen && in[a + len] == in[b + len]) ++len;
+            return len;
+        }
+    } bytes{in};
+    std::vector<uint16_t> prevd(n + 1, 0);
+    std::vector<int64_t> head(1 << 15, -1);
+    for (int64_t p = 0; p + MIN_MATCH <= (int64_t)n; ++p) {
+        const uint32_t h = hash3(in[p], in[p + 1], in[p + 2]);
+        const int64_t q = head[h];
+        prevd[p] = (q >= 0 && p - q < WSIZE) ? (uint16_t)(p - q) : 0;
+        head[h] = p;
+    }
+    auto prevfn = [&](int64_t i) -> uint32_t { return prevd[i]; };
+    for (int64_t p = 0; p < (int64_t)n; ++p) {
+        MatchState s;
+        match_init(s, p, (int64_t)n, bytes, prevfn);
+        int steps = 0;
+        while (!s.done) {
+            const bool rej = s.best >= MIN_MATCH && (int64_t)s.best < s.maxlen &&
+                             (bytes(s.q + s.best) != bytes(p + s.best) || bytes(s.q + s.best - 1) != bytes(p + s.best - 1));
+            if (rej) ++*rejects; else ++*compares;
+            match_step(s, bytes, prevfn);
+            ++steps;
+        }
+        hist[steps > 129 ? 129 : steps]++;
+    }
+}
