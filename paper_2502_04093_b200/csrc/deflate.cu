@@ -147,6 +147,17 @@ struct PrevD {
     const uint16_t *p;
     __device__ __forceinline__ uint32_t operator()(int64_t i) const { return __ldg(p + i); }
 };
+struct PrevD32 {
+    const uint16_t *p;
+    __device__ __forceinline__ uint32_t operator()(uint32_t i) const { return __ldg(p + i); }
+};
+// 4-byte words of a stream whose base is 16-byte aligned and whose row is padded to 16
+// bytes, so a word whose first byte is < n is always inside the allocation.
+struct InWords {
+    const uint8_t *p;
+    __device__ __forceinline__ uint32_t word(uint32_t k) const { return __ldg(reinterpret_cast<const uint32_t *>(p) + k); }
+    __device__ __forceinline__ uint32_t byte(uint32_t i) const { return __ldg(p + i); }
+};
 
 // ------------------------------------------------------------------ 1. scan
 __global__ void k_scan(const uint8_t *in, uint64_t in_stride, uint64_t n, StreamMeta *meta) {
@@ -247,15 +258,23 @@ __global__ void __launch_bounds__(PL_WARPS * 32) k_prevlinks(const uint8_t *in, 
 // staging the tile in shared memory (the walk is latency-, not bandwidth-bound: 70 ms vs
 // 43 ms) and a per-lane state machine that refills idle lanes (87 ms: neighbouring
 // positions have similar chain lengths, so the extra state costs more than divergence).
+template <bool WIDE>  // WIDE: streams of 2^31 bytes or more (64-bit positions)
 __global__ void __launch_bounds__(256) k_match(const uint8_t *in, uint64_t in_stride, uint64_t n,
                                               const StreamMeta *meta, const uint16_t *prevd_all, uint64_t *rec_all) {
     const int j = blockIdx.y;
     if (!meta[j].active) return;
-    const InBytes bytes{in + (uint64_t)j * in_stride};
-    const PrevD prev{prevd_all + (uint64_t)j * n};
     uint64_t *rec = rec_all + (uint64_t)j * n;
-    for (uint64_t p = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; p < n; p += (uint64_t)gridDim.x * blockDim.x)
-        rec[p] = match_search((int64_t)p, (int64_t)n, bytes, prev);
+    if constexpr (!WIDE) {
+        const InWords words{in + (uint64_t)j * in_stride};
+        const PrevD32 prev{prevd_all + (uint64_t)j * n};
+        for (uint32_t p = blockIdx.x * blockDim.x + threadIdx.x; p < (uint32_t)n; p += gridDim.x * blockDim.x)
+            rec[p] = match_search32(p, (uint32_t)n, words, prev);
+    } else {
+        const InBytes bytes{in + (uint64_t)j * in_stride};
+        const PrevD prev{prevd_all + (uint64_t)j * n};
+        for (uint64_t p = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; p < n; p += (uint64_t)gridDim.x * blockDim.x)
+            rec[p] = match_search((int64_t)p, (int64_t)n, bytes, prev);
+    }
 }
 
 // ---------------------------------------------------------------- 4. anchors
@@ -853,6 +872,8 @@ void crc32_batch(const uint8_t *const *ptrs, const uint64_t *lens, int S, uint64
 
 void DeflateBatch::run(const uint8_t *in, uint64_t in_stride, int S, uint64_t n, uint8_t *out, uint64_t out_stride,
                        void *workspace, BackendResults res, cudaStream_t st) {
+    if ((in_stride & 15) || (reinterpret_cast<uintptr_t>(in) & 15))
+        throw Error(EINVAL_, "deflate input rows must be 16-byte aligned with a 16-byte multiple stride");
     Work w = carve(workspace, S, n);
     CK(cudaMemsetAsync(w.meta, 0, sizeof(StreamMeta) * S, st));
     CK(cudaMemsetAsync(w.nruns, 0, sizeof(unsigned long long), st));
@@ -880,7 +901,10 @@ void DeflateBatch::run(const uint8_t *in, uint64_t in_stride, int S, uint64_t n,
         }
         {
         ProfScope ps2("deflate.match", st, (uint64_t)S * n * 11);
-        k_match<<<dim3(grid_for(n, 256, 4096), S), 256, 0, st>>>(in, in_stride, n, w.meta, w.prevd, w.rec);
+        if (n < (1ull << 31))
+            k_match<false><<<dim3(grid_for(n, 256, 4096), S), 256, 0, st>>>(in, in_stride, n, w.meta, w.prevd, w.rec);
+        else
+            k_match<true><<<dim3(grid_for(n, 256, 4096), S), 256, 0, st>>>(in, in_stride, n, w.meta, w.prevd, w.rec);
         CKL();
         }
         {

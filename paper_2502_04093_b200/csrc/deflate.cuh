@@ -15,7 +15,8 @@ struct BackendResults {
     const uint8_t **payload;   // device address of the payload bytes
 };
 
-// S equal-length streams in[j*in_stride .. +n); outputs land in out[j*out_stride ..],
+// S equal-length streams in[j*in_stride .. +n) (in 16-byte aligned, in_stride a multiple
+// of 16: the match search reads whole aligned words of the padded rows); outputs land in out[j*out_stride ..],
 // out_stride >= n + 16.  Workspace from DeflateBatch::workspace_bytes.
 struct DeflateBatch {
     static constexpr int CH = 256;  // nominal parse chunk (boundaries snap to anchors)

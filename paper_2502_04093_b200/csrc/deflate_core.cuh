@@ -146,6 +146,115 @@ HD uint64_t match_search(int64_t p, int64_t n, const Bytes &bytes, const Prev &p
     return match_result(s);
 }
 
+// ---------------------------------------------------- match_search, fast form
+// Same candidates in the same order and the same record as match_search, for streams
+// shorter than 2^31 bytes.  Differences are only in how the work is spent:
+//  * 32-bit positions;
+//  * zlib's scan_end1/scan_end bytes of p live in registers (longest_match keeps them
+//    in locals too), so a quick reject loads two bytes of q only;
+//  * the run skip can only fire on candidate 1, which is peeled; in the loop the next
+//    link prevd(q) does not depend on the compare and is loaded alongside it;
+//  * common-prefix lengths compare 4 bytes per step from 4-byte-aligned words
+//    (Words::word(k) = bytes 4k..4k+3, little-endian; Words::word is only called for
+//    words whose first byte is < n).
+HD uint32_t funnel_r(uint32_t lo, uint32_t hi, uint32_t sh) {
+#if defined(__CUDA_ARCH__)
+    return __funnelshift_r(lo, hi, sh);
+#else
+    return (uint32_t)((((uint64_t)hi << 32) | lo) >> sh);
+#endif
+}
+HD uint32_t first_set_byte(uint32_t x) {  // x != 0
+#if defined(__CUDA_ARCH__)
+    return (uint32_t)(__ffs((int)x) - 1) >> 3;
+#else
+    return (uint32_t)__builtin_ctz(x) >> 3;
+#endif
+}
+
+template <class Words>
+HD uint32_t match_len32(const Words &w, uint32_t n, uint32_t a, uint32_t b, uint32_t maxlen) {
+    const uint32_t sa = (a & 3) * 8, sb = (b & 3) * 8;
+    uint32_t ka = a >> 2, kb = b >> 2;
+    uint32_t a0 = w.word(ka), b0 = w.word(kb);
+    for (uint32_t len = 0;; len += 4) {
+        const uint32_t a1 = 4 * (ka + 1) < n ? w.word(ka + 1) : 0u;
+        const uint32_t b1 = 4 * (kb + 1) < n ? w.word(kb + 1) : 0u;
+        uint32_t x = funnel_r(a0, a1, sa) ^ funnel_r(b0, b1, sb);
+        if (len + 4 >= maxlen) {
+            const uint32_t r = maxlen - len;  // 1..4
+            if (r < 4) x &= (1u << (8 * r)) - 1u;
+            return x ? len + first_set_byte(x) : maxlen;
+        }
+        if (x) return len + first_set_byte(x);
+        ++ka, ++kb;
+        a0 = a1, b0 = b1;
+    }
+}
+
+template <class Words, class Prev>
+HD uint64_t match_search32(uint32_t p, uint32_t n, const Words &w, const Prev &prevd) {
+    if (p + MIN_MATCH > n) return 0;
+    const uint32_t d0 = prevd(p);
+    if (d0 == 0 || d0 == p || d0 > (uint32_t)MAX_DIST) return 0;
+    const uint32_t flag = d0 == (uint32_t)MAX_DIST;
+    const uint32_t maxlen = n - p < (uint32_t)MAX_MATCH ? n - p : (uint32_t)MAX_MATCH;
+    const uint32_t nice = n - p < (uint32_t)NICE_LENGTH ? n - p : (uint32_t)NICE_LENGTH;
+    const uint32_t limit = p > (uint32_t)MAX_DIST ? p - (uint32_t)MAX_DIST : 0u;
+    uint32_t best = 0, bestd = 0;
+    uint32_t q = p - d0, from = q;
+    int i = 1;
+    {  // candidate 1: no quick reject (best == 0); may start a same-byte run
+        uint32_t len = match_len32(w, n, p, q, maxlen);
+        if (len >= (uint32_t)MIN_MATCH) {
+            best = len, bestd = p - q;
+            if (len >= nice) return mrec_pack(best, bestd, best, bestd, flag);
+            if (q == p - 1) {  // see match_step: candidates p-2 .. r all fail the quick reject
+                const uint32_t v = w.byte(p - 1);
+                const uint32_t lo = p > (uint32_t)MAX_CHAIN ? p - (uint32_t)MAX_CHAIN : 0u;
+                const uint32_t floor_ = limit + 1 > lo ? limit + 1 : lo;
+                uint32_t r = p - 1;
+                while (r >= floor_ + 1 && w.byte(r - 1) == v) --r;
+                i += (int)(p - 1 - r);
+                if (i >= MAX_CHAIN) return mrec_pack(best, bestd, best, bestd, flag);
+                from = r;
+            }
+        }
+    }
+    uint32_t l32 = best, d32 = bestd;
+    {
+        const uint32_t dq = prevd(from);
+        if (dq == 0 || from - dq <= limit || i >= MAX_CHAIN) return mrec_pack(best, bestd, l32, d32, flag);
+        q = from - dq;
+        ++i;
+    }
+    // scan_end1 / scan_end (only meaningful while MIN_MATCH <= best < maxlen)
+    uint32_t e0 = best ? w.byte(p + best - 1) : 0u, e1 = best && best < maxlen ? w.byte(p + best) : 0u;
+    for (;;) {
+        const uint32_t dq = prevd(q);
+        const bool reject = best >= (uint32_t)MIN_MATCH && best < maxlen &&
+                            (w.byte(q + best) != e1 || w.byte(q + best - 1) != e0);
+        if (!reject) {
+            uint32_t len = match_len32(w, n, p, q, maxlen);
+            if (len < (uint32_t)MIN_MATCH) len = 0;
+            if (len > best) {
+                best = len, bestd = p - q;
+                if (len >= nice) {
+                    if (i <= 32) l32 = best, d32 = bestd;
+                    return mrec_pack(best, bestd, l32, d32, flag);
+                }
+                e0 = w.byte(p + best - 1);
+                e1 = best < maxlen ? w.byte(p + best) : 0u;
+            }
+        }
+        if (i <= 32) l32 = best, d32 = bestd;
+        if (dq == 0 || q - dq <= limit || i >= MAX_CHAIN) break;
+        q -= dq;
+        ++i;
+    }
+    return mrec_pack(best, bestd, l32, d32, flag);
+}
+
 // ------------------------------------------------------------- window slides
 // fill_window slides the 64 KiB window by WSIZE at loop tops; with the whole input
 // available, the k-th slide happens at the first loop top >= slide_threshold(k).

@@ -25,6 +25,20 @@ struct BitWriter {
     void align() { pos = (pos + 7) & ~uint64_t(7); }
 };
 
+// 4-byte little-endian words; bytes past n read as 0 (the GPU reads padding there, which
+// match_len32 masks off)
+struct HostWords {
+    const uint8_t *in;
+    uint64_t n;
+    uint32_t word(uint32_t k) const {
+        uint32_t v = 0;
+        for (int b = 0; b < 4; ++b)
+            if (4ull * k + b < n) v |= (uint32_t)in[4ull * k + b] << (8 * b);
+        return v;
+    }
+    uint32_t byte(uint32_t i) const { return in[i]; }
+};
+
 struct Stats {
     uint64_t chunks, blocks, stored, fixed, dynamic, symbols;
 };
@@ -54,9 +68,10 @@ extern "C" int zmodel_compress(const uint8_t *in, uint64_t n, int chunk, uint8_t
         }
     }
     auto prevfn = [&](int64_t i) -> uint32_t { return prevd[i]; };
-    // 2. match records
+    // 2. match records (the GPU's fast form; zmodel_match_check pins it to match_search)
     std::vector<uint64_t> rec(n + 1, 0);
-    for (int64_t p = 0; p < (int64_t)n; ++p) rec[p] = match_search(p, (int64_t)n, bytes, prevfn);
+    const HostWords words{in, n};
+    for (int64_t p = 0; p < (int64_t)n; ++p) rec[p] = match_search32((uint32_t)p, (uint32_t)n, words, prevfn);
     // 3. anchors: no match found at q < p can reach past p
     std::vector<uint8_t> anchor(n + 1, 0);
     {
@@ -232,8 +247,9 @@ extern "C" int zmodel_compress(const uint8_t *in, uint64_t n, int chunk, uint8_t
 
 extern "C" uint32_t zmodel_crc_combine(uint32_t crc1, uint32_t crc2, uint64_t len2) { return crc_combine(crc1, crc2, len2); }
 
-// dev statistics: histogram of match_step calls per position (hist[0..129])
-extern "C" void zmodel_chain_hist(const uint8_t *in, uint64_t n, uint64_t *hist, uint64_t *rejects, uint64_t *compares) {
+// match_search32 (the GPU's form) against the reference-shaped match_search at every
+// position; returns the number of positions whose records differ.
+extern "C" uint64_t zmodel_match_check(const uint8_t *in, uint64_t n) {
     struct HB {
         const uint8_t *in;
         uint32_t operator()(int64_t i) const { return in[i]; }
@@ -252,17 +268,9 @@ extern "C" void zmodel_chain_hist(const uint8_t *in, uint64_t n, uint64_t *hist,
         head[h] = p;
     }
     auto prevfn = [&](int64_t i) -> uint32_t { return prevd[i]; };
-    for (int64_t p = 0; p < (int64_t)n; ++p) {
-        MatchState s;
-        match_init(s, p, (int64_t)n, bytes, prevfn);
-        int steps = 0;
-        while (!s.done) {
-            const bool rej = s.best >= MIN_MATCH && (int64_t)s.best < s.maxlen &&
-                             (bytes(s.q + s.best) != bytes(p + s.best) || bytes(s.q + s.best - 1) != bytes(p + s.best - 1));
-            if (rej) ++*rejects; else ++*compares;
-            match_step(s, bytes, prevfn);
-            ++steps;
-        }
-        hist[steps > 129 ? 129 : steps]++;
-    }
+    const HostWords words{in, n};
+    uint64_t bad = 0;
+    for (int64_t p = 0; p < (int64_t)n; ++p)
+        bad += match_search(p, (int64_t)n, bytes, prevfn) != match_search32((uint32_t)p, (uint32_t)n, words, prevfn);
+    return bad;
 }

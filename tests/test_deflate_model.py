@@ -90,3 +90,21 @@ def test_crc_combine(zmodel):
         a = rng.integers(0, 256, la, dtype=np.uint8).tobytes()
         b = rng.integers(0, 256, lb, dtype=np.uint8).tobytes()
         assert zmodel.lib.zmodel_crc_combine(zlib.crc32(a), zlib.crc32(b), lb) == zlib.crc32(a + b)
+
+
+def test_fast_match_search_equals_reference_form(zmodel):
+    """match_search32 (what k_match runs) gives the same record as match_search at every
+    position: runs, sparse bit patterns, periodic text, tails shorter than a word."""
+    lib = zmodel.lib
+    lib.zmodel_match_check.restype = C.c_uint64
+    lib.zmodel_match_check.argtypes = [C.c_char_p, C.c_uint64]
+    rng = np.random.default_rng(11)
+    datas = [d for _, d in CASES if len(d) <= 70000]
+    for n in (5, 6, 7, 9, 258, 259, 261, 263, 1000):
+        for p in (0.01, 0.05, 0.5):
+            bits = (rng.random(n * 8) < p).astype(np.uint8)
+            datas.append(np.packbits(bits, bitorder="little").tobytes())
+        datas.append(bytes([7]) * n)
+        datas.append((b"ab" * n)[:n])
+    for d in datas:
+        assert lib.zmodel_match_check(d, len(d)) == 0, len(d)
