@@ -269,36 +269,57 @@ __global__ void k_outlier_block(const uint64_t *ord, const uint64_t *bits, const
 // prefix taken from already-merged codewords (pipeline.hpp:328-339).  A CTA takes 32
 // plane words x 32 planes: warp p loads plane p's 128-byte row segment (coalesced) into
 // a padded smem tile, then warp w owns word w with lane p holding plane p's bits.
+// 32x32 bit-matrix transpose across a warp: lane r holds row r (bit c = column c) on
+// entry and column r (bit c = row c) on return.  Five block-swap stages.
+__device__ __forceinline__ uint32_t warp_transpose32(uint32_t x, unsigned lane) {
+    const uint32_t masks[5] = {0x0000FFFFu, 0x00FF00FFu, 0x0F0F0F0Fu, 0x33333333u, 0x55555555u};
+#pragma unroll
+    for (int s = 0; s < 5; ++s) {
+        const int j = 16 >> s;
+        const uint32_t m = masks[s];  // columns c with (c & j) == 0
+        const uint32_t y = __shfl_xor_sync(0xffffffffu, x, j);
+        x = (lane & j) ? ((x & ~m) | ((y & ~m) >> j)) : ((x & m) | ((y & m) << j));
+    }
+    return x;
+}
+
+// Solves b_p = e_p ^ b_{p-1} ^ b_{p-2} down a codeword (plane p at bit 31-p): over GF(2)
+// B = E / (1 + S + S^2) = (1 + S) E / (1 + S^3), S = shift toward the LSB, i.e. F = E ^ (E >> 1)
+// followed by a stride-3 prefix XOR.
+__device__ __forceinline__ uint32_t xor_decode_word(uint32_t e) {
+    uint32_t g = e ^ (e >> 1);
+    g ^= g >> 3;
+    g ^= g >> 6;
+    g ^= g >> 12;
+    g ^= g >> 24;
+    return g;
+}
+
+// bitplane.cpp:24-59 (xor decode + merge) for planes [k0, k1) of one level on top of the
+// codewords already merged from planes [0, k0).  A warp owns 32 consecutive codewords:
+// the 32 plane words are staged through shared memory, transposed with shuffles, and the
+// XOR recurrence is solved inside each codeword.
 __global__ void __launch_bounds__(1024) k_merge(const uint32_t *const *__restrict__ rows,
                                                 const uint32_t *__restrict__ merged_in,
                                                 uint32_t *__restrict__ merged_out, uint64_t count, int k0, int k1) {
     __shared__ uint32_t tile[32][33];
     const unsigned warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const uint64_t words = (count + 31) / 32;
+    const uint32_t pre = k0 == 0 ? 0u : ~0u << (32 - k0);            // planes < k0
+    const uint32_t keep = k1 == 0 ? 0u : k1 >= 32 ? ~0u : ~0u << (32 - k1);  // planes < k1
     for (uint64_t w0 = (uint64_t)blockIdx.x * 32; w0 < words; w0 += (uint64_t)gridDim.x * 32) {
-        tile[warp][lane] = ((int)warp >= k0 && (int)warp < k1 && w0 + lane < words) ? rows[warp][w0 + lane] : 0u;
+        tile[warp][lane] = ((int)warp >= k0 && (int)warp < k1 && w0 + lane < words) ? __ldg(rows[warp] + w0 + lane) : 0u;
         __syncthreads();
         const uint64_t w = w0 + warp;
         const uint64_t i = w * 32 + lane;
-        const uint32_t mi = (merged_in && i < count) ? merged_in[i] : 0u;
-        uint32_t bp = 0;
-        for (int p = 0; p < k0; ++p) {
-            const uint32_t m = __ballot_sync(0xffffffffu, (mi >> (31 - p)) & 1u);
-            if ((int)lane == p) bp = m;
+        // lane p: plane p's word for these 32 codewords -> lane c: codeword c's plane bits
+        const uint32_t e_new = __brev(warp_transpose32(tile[lane][warp], lane));
+        uint32_t e = e_new;
+        if (merged_in && k0 > 0 && i < count) {
+            const uint32_t m = merged_in[i] & pre;
+            e |= (m ^ (m >> 1) ^ (m >> 2)) & pre;
         }
-        const uint32_t e = tile[lane][warp];
-        for (int p = k0; p < k1; ++p) {
-            const uint32_t b1 = __shfl_sync(0xffffffffu, bp, (p - 1) & 31);
-            const uint32_t b2 = __shfl_sync(0xffffffffu, bp, (p - 2) & 31);
-            if ((int)lane == p) bp = e ^ (p >= 1 ? b1 : 0u) ^ (p >= 2 ? b2 : 0u);
-        }
-        uint32_t out = 0;
-#pragma unroll
-        for (int b = 0; b < 32; ++b) {
-            const uint32_t m = __ballot_sync(0xffffffffu, (bp >> b) & 1u);
-            if ((int)lane == b) out = __brev(m);
-        }
-        if (w < words && i < count) merged_out[i] = out;
+        if (w < words && i < count) merged_out[i] = xor_decode_word(e) & keep;
         __syncthreads();
     }
 }
