@@ -205,6 +205,10 @@ __global__ void k_select(StreamMeta *meta, int S, uint64_t n) {
 // zlib's head/prev insertion order is sequential; one warp walks 32 positions per
 // step through a 64 KiB shared-memory head table (match_any resolves same-step
 // collisions).  Each warp owns a 32 KiB block and warms up on the block before it.
+// Only the head-table read/write chain is serial: a batch of AHEAD steps has its bytes
+// loaded one batch ahead (one byte per lane + two spill bytes, the rest by shuffles)
+// and all its match_any masks computed before the chain runs (ncu: the byte-load and
+// MATCH.ANY latencies dominated when they sat on the chain).
 __global__ void __launch_bounds__(PL_WARPS * 32) k_prevlinks(const uint8_t *in, uint64_t in_stride, uint64_t n,
                                                            const StreamMeta *meta, uint16_t *prevd_all) {
     extern __shared__ uint16_t heads[];
@@ -220,32 +224,55 @@ __global__ void __launch_bounds__(PL_WARPS * 32) k_prevlinks(const uint8_t *in, 
     uint16_t *prevd = prevd_all + (uint64_t)j * n;
     const uint64_t base = blk == 0 ? 0 : (blk - 1) * WSIZE;
     const uint64_t out0 = blk * WSIZE, end = min(n, (blk + 1) * WSIZE);
-    constexpr int AHEAD = 8;  // hashes of 8 steps are loaded up front so their loads overlap
-    for (uint64_t pos0 = base; pos0 < end; pos0 += 32 * AHEAD) {
-        uint32_t hs[AHEAD];
+    constexpr int AHEAD = 8;
+    uint32_t b0[AHEAD], bx[AHEAD];  // byte at q; lanes 0,1: byte at q + 32
+    auto fetch = [&](uint64_t pos0) {
 #pragma unroll
         for (int k = 0; k < AHEAD; ++k) {
             const uint64_t q = pos0 + 32 * k + lane;
+            b0[k] = q < n ? __ldg(p + q) : 0u;
+            bx[k] = (lane < 2 && q + 32 < n) ? __ldg(p + q + 32) : 0u;
+        }
+    };
+    fetch(base);
+    const unsigned lt_mask = (1u << lane) - 1u;
+    for (uint64_t pos0 = base; pos0 < end; pos0 += 32 * AHEAD) {
+        uint32_t hs[AHEAD], mk[AHEAD];
+#pragma unroll
+        for (int k = 0; k < AHEAD; ++k) {
+            const uint64_t q = pos0 + 32 * k + lane;
+            const uint32_t v1 = __shfl_sync(0xffffffffu, b0[k], (lane + 1) & 31);
+            const uint32_t e1 = __shfl_sync(0xffffffffu, bx[k], (lane + 1) & 31);
+            const uint32_t v2 = __shfl_sync(0xffffffffu, b0[k], (lane + 2) & 31);
+            const uint32_t e2 = __shfl_sync(0xffffffffu, bx[k], (lane + 2) & 31);
+            const uint32_t c1 = lane == 31 ? e1 : v1, c2 = lane >= 30 ? e2 : v2;
             const bool valid = q + MIN_MATCH <= n && q < end;
-            hs[k] = valid ? hash3(__ldg(p + q), __ldg(p + q + 1), __ldg(p + q + 2)) : (0x10000u + lane);
+            hs[k] = valid ? hash3(b0[k], c1, c2) : (0x10000u + lane);
+        }
+        if (pos0 + 32 * AHEAD < end) fetch(pos0 + 32 * AHEAD);
+#pragma unroll
+        for (int k = 0; k < AHEAD; ++k) mk[k] = __match_any_sync(0xffffffffu, hs[k]);
+        uint32_t prel[AHEAD];
+#pragma unroll
+        for (int k = 0; k < AHEAD; ++k) {
+            const uint32_t h = hs[k];
+            const bool valid = h < 0x10000u;
+            const uint32_t rel = (uint32_t)(pos0 + 32 * k + lane - base);
+            const unsigned lower = mk[k] & lt_mask;
+            prel[k] = 0xFFFF;
+            if (lower) prel[k] = rel - (lane - (31u - __clz(lower)));
+            else if (valid) prel[k] = head[h];
+            __syncwarp();
+            if (valid && lane == 31u - __clz(mk[k])) head[h] = (uint16_t)rel;
+            __syncwarp();
         }
 #pragma unroll
         for (int k = 0; k < AHEAD; ++k) {
             const uint64_t q = pos0 + 32 * k + lane;
-            const uint32_t h = hs[k];
-            const bool valid = h < 0x10000u;
-            const uint32_t rel = (uint32_t)(q - base);
-            const unsigned mask = __match_any_sync(0xffffffffu, h);
-            const unsigned lower = mask & ((1u << lane) - 1u);
-            uint32_t prel = 0xFFFF;
-            if (lower) prel = rel - (lane - (31u - __clz(lower)));
-            else if (valid) prel = head[h];
-            __syncwarp();
-            if (valid && lane == 31u - __clz(mask)) head[h] = (uint16_t)rel;
-            __syncwarp();
             if (q >= out0 && q < end) {
+                const uint32_t rel = (uint32_t)(q - base);
                 uint32_t d = 0;
-                if (valid && prel != 0xFFFF && rel - prel < (uint32_t)WSIZE) d = rel - prel;
+                if (hs[k] < 0x10000u && prel[k] != 0xFFFF && rel - prel[k] < (uint32_t)WSIZE) d = rel - prel[k];
                 prevd[q] = (uint16_t)d;
             }
         }
