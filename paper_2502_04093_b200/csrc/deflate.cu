@@ -419,47 +419,30 @@ __device__ __forceinline__ int64_t periodic_run(int64_t p, int tag, uint64_t n, 
 }
 
 // ------------------------------------------------------ 5. chunk transfer maps
-// One warp owns 8 consecutive chunks: it stages their match records (plus the
-// reach-out margin) in shared memory, then its 32 lanes walk the 8 chunks x 4 entry
-// tags from smem.  Walks that run past the staged window read global memory.
-constexpr int SIM_WARPS = 4;
-constexpr int SIM_CHUNKS = 8;
-constexpr int WIN = SIM_CHUNKS * CH + MAX_MATCH + 8;
-
+// Every chunk is walked from each of the 4 entry tags.  (Staging the records of a few
+// chunks in shared memory was measured slower than reading them through L1: the smem
+// footprint capped occupancy and left 3/4 of the lanes of the emit walk idle.)
 struct NoBytes {
     __device__ __forceinline__ uint32_t operator()(int64_t) const { return 0; }
 };
 
-struct RecWin {
-    const uint64_t *win, *rec;
-    uint64_t s0, s1;
-    __device__ __forceinline__ uint64_t operator()(int64_t q) const {
-        return ((uint64_t)q >= s0 && (uint64_t)q < s1) ? win[q - (int64_t)s0] : rec[q];
-    }
+struct RecG {
+    const uint64_t *rec;
+    __device__ __forceinline__ uint64_t operator()(int64_t q) const { return __ldg(rec + q); }
 };
 
-__device__ __forceinline__ RecWin stage_window(uint64_t *win, const uint64_t *rec, uint64_t k0, uint64_t n,
-                                               unsigned lane) {
-    const uint64_t s0 = k0 * CH > 0 ? k0 * CH - 1 : 0;
-    const uint64_t s1 = min(n, (k0 + SIM_CHUNKS) * CH + MAX_MATCH);
-    for (uint64_t i = s0 + lane; i < s1; i += 32) win[i - s0] = rec[i];
-    __syncwarp();
-    return RecWin{win, rec, s0, s1};
-}
-
-__global__ void __launch_bounds__(SIM_WARPS * 32) k_sim(uint64_t n, const StreamMeta *meta, const uint64_t *rec_all,
-                                                       uint64_t nchunks, const uint64_t *bnd_all,
-                                                       const uint32_t *nbreak_all, uint8_t *exit4, uint32_t *cnt4) {
-    extern __shared__ uint64_t srec[];
+// thread = (chunk, entry tag); records are read through L1 (the 4 walks of a chunk read
+// the same lines at about the same time)
+__global__ void __launch_bounds__(256) k_sim(uint64_t n, const StreamMeta *meta, const uint64_t *rec_all,
+                                            uint64_t nchunks, const uint64_t *bnd_all,
+                                            const uint32_t *nbreak_all, uint8_t *exit4, uint32_t *cnt4) {
     const int j = blockIdx.y;
     if (!meta[j].active) return;
-    const unsigned warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const uint64_t k0 = ((uint64_t)blockIdx.x * SIM_WARPS + warp) * SIM_CHUNKS;
-    if (k0 >= nchunks) return;
-    const RecWin R = stage_window(srec + (size_t)warp * WIN, rec_all + (uint64_t)j * n, k0, n, lane);
-    const uint64_t k = k0 + (lane >> 2);
-    int tag = (int)(lane & 3);
+    const uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const uint64_t k = t >> 2;
+    int tag = (int)(t & 3);
     if (k >= nchunks) return;
+    const RecG R{rec_all + (uint64_t)j * n};
     const uint64_t *bnd = bnd_all + (uint64_t)j * (nchunks + 1);
     const uint64_t b0 = bnd[k], b1 = bnd[k + 1];
     const NoBytes bytes;
@@ -478,8 +461,8 @@ __global__ void __launch_bounds__(SIM_WARPS * 32) k_sim(uint64_t n, const Stream
         p = s.next_p;
         tag = s.next_tag;
     }
-    exit4[((uint64_t)j * nchunks + k) * 4 + (lane & 3)] = (uint8_t)tag;
-    cnt4[((uint64_t)j * nchunks + k) * 4 + (lane & 3)] = count;
+    exit4[((uint64_t)j * nchunks + k) * 4 + (t & 3)] = (uint8_t)tag;
+    cnt4[((uint64_t)j * nchunks + k) * 4 + (t & 3)] = count;
 }
 
 // ---------------------------------------------------------------- 6. resolve
@@ -546,24 +529,20 @@ __global__ void k_resolve(const uint8_t *in, uint64_t in_stride, uint64_t n, Str
 }
 
 // ------------------------------------------------------------ 7. emit symbols
-// same staging as k_sim; lane c < 8 re-walks chunk k0+c from its resolved entry tag
-__global__ void __launch_bounds__(SIM_WARPS * 32) k_emit_syms(const uint8_t *in, uint64_t in_stride, uint64_t n,
-                                                             const StreamMeta *meta, const uint64_t *rec_all,
-                                                             uint64_t nchunks, const uint64_t *bnd_all,
-                                                             const uint32_t *nbreak_all,
-                                                             const uint8_t *entry_all, const uint64_t *symoff_all,
-                                                             uint32_t *syms_all, uint64_t maxb, uint64_t *blk_top_all,
-                                                             uint64_t *blk_start_all, RunTask *runs,
-                                                             unsigned long long *nruns) {
-    extern __shared__ uint64_t srec[];
+// thread per chunk: re-walk it from its resolved entry tag, writing the symbols
+__global__ void __launch_bounds__(256) k_emit_syms(const uint8_t *in, uint64_t in_stride, uint64_t n,
+                                                  const StreamMeta *meta, const uint64_t *rec_all,
+                                                  uint64_t nchunks, const uint64_t *bnd_all,
+                                                  const uint32_t *nbreak_all,
+                                                  const uint8_t *entry_all, const uint64_t *symoff_all,
+                                                  uint32_t *syms_all, uint64_t maxb, uint64_t *blk_top_all,
+                                                  uint64_t *blk_start_all, RunTask *runs,
+                                                  unsigned long long *nruns) {
     const int j = blockIdx.y;
     if (!meta[j].active) return;
-    const unsigned warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const uint64_t k0 = ((uint64_t)blockIdx.x * SIM_WARPS + warp) * SIM_CHUNKS;
-    if (k0 >= nchunks) return;
-    const RecWin R = stage_window(srec + (size_t)warp * WIN, rec_all + (uint64_t)j * n, k0, n, lane);
-    const uint64_t k = k0 + lane;
-    if (lane >= SIM_CHUNKS || k >= nchunks) return;
+    const uint64_t k = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= nchunks) return;
+    const RecG R{rec_all + (uint64_t)j * n};
     const uint64_t *bnd = bnd_all + (uint64_t)j * (nchunks + 1);
     const uint64_t b0 = bnd[k], b1 = bnd[k + 1];
     if (b0 >= b1) return;
@@ -940,20 +919,13 @@ void DeflateBatch::run(const uint8_t *in, uint64_t in_stride, int S, uint64_t n,
         CKL();
         k_bounds<<<S, 32, 0, st>>>(n, w.meta, w.nchunks, w.first_anchor, w.bnd, w.nbreak);
         CKL();
-        const size_t sim_smem = (size_t)SIM_WARPS * WIN * sizeof(uint64_t);
-        const unsigned sim_grid = (unsigned)((w.nchunks + SIM_WARPS * SIM_CHUNKS - 1) / (SIM_WARPS * SIM_CHUNKS));
-        static bool sim_attr = false;
-        if (!sim_attr) {
-            CK(cudaFuncSetAttribute(k_sim, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sim_smem));
-            CK(cudaFuncSetAttribute(k_emit_syms, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sim_smem));
-            sim_attr = true;
-        }
-        k_sim<<<dim3(sim_grid, S), SIM_WARPS * 32, sim_smem, st>>>(n, w.meta, w.rec, w.nchunks, w.bnd, w.nbreak, w.exit4, w.cnt4);
+        k_sim<<<dim3((unsigned)((w.nchunks * 4 + 255) / 256), S), 256, 0, st>>>(n, w.meta, w.rec, w.nchunks, w.bnd,
+                                                                              w.nbreak, w.exit4, w.cnt4);
         CKL();
         k_resolve<<<S, 32, 0, st>>>(in, in_stride, n, w.meta, w.nchunks, w.exit4, w.cnt4, w.entry, w.symoff, w.syms,
                                     w.maxb, w.blk_start);
         CKL();
-        k_emit_syms<<<dim3(sim_grid, S), SIM_WARPS * 32, sim_smem, st>>>(in, in_stride, n, w.meta, w.rec, w.nchunks, w.bnd, w.nbreak, w.entry, w.symoff, w.syms, w.maxb, w.blk_top, w.blk_start, w.runs, w.nruns);
+        k_emit_syms<<<dim3((unsigned)((w.nchunks + 255) / 256), S), 256, 0, st>>>(in, in_stride, n, w.meta, w.rec, w.nchunks, w.bnd, w.nbreak, w.entry, w.symoff, w.syms, w.maxb, w.blk_top, w.blk_start, w.runs, w.nruns);
         CKL();
         k_emit_runs<<<148 * 4, 256, 0, st>>>(n, w.rec, w.syms, w.maxb, w.blk_top, w.blk_start, w.runs, w.nruns);
         CKL();
