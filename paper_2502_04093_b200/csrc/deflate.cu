@@ -57,18 +57,24 @@ struct Work {
     uint32_t *cnt4;
     uint8_t *entry;
     uint64_t *symoff;
+    uint8_t *seg_exit4, *seg_entry;  // the same per SEG-chunk segment (two-level resolve)
+    uint32_t *seg_cnt4;
+    uint64_t *seg_symoff;
     uint32_t *syms;
     uint64_t *blk_top, *blk_start, *blk_bitpos;
     BlockTrees *trees;
     uint32_t *crc_part;
     uint32_t *crc_tab;
-    uint64_t nchunks, maxb, ncrc;
+    uint64_t nchunks, nseg, maxb, ncrc;
 };
 
-Work carve(void *ws, int S, uint64_t n) {
+constexpr uint64_t SEG = 32;  // chunks per resolve segment
+
+Work carve(void *ws, int S, uint64_t n, size_t *size_out = nullptr) {
     Bump b{static_cast<uint8_t *>(ws)};
     Work w;
     w.nchunks = (n + CH - 1) / CH;
+    w.nseg = (w.nchunks + SEG - 1) / SEG;
     w.maxb = n / BLOCK_SYMS + 2;
     w.ncrc = (n + 64 + CRC_CHUNK - 1) / CRC_CHUNK + 1;
     w.meta = b.take<StreamMeta>(S);
@@ -83,6 +89,10 @@ Work carve(void *ws, int S, uint64_t n) {
     w.cnt4 = b.take<uint32_t>((size_t)S * w.nchunks * 4);
     w.entry = b.take<uint8_t>((size_t)S * (w.nchunks + 1));
     w.symoff = b.take<uint64_t>((size_t)S * w.nchunks);
+    w.seg_exit4 = b.take<uint8_t>((size_t)S * w.nseg * 4);
+    w.seg_cnt4 = b.take<uint32_t>((size_t)S * w.nseg * 4);
+    w.seg_entry = b.take<uint8_t>((size_t)S * (w.nseg + 1));
+    w.seg_symoff = b.take<uint64_t>((size_t)S * w.nseg);
     w.syms = b.take<uint32_t>((size_t)S * (n + 1));
     w.blk_top = b.take<uint64_t>((size_t)S * w.maxb);
     w.blk_start = b.take<uint64_t>((size_t)S * w.maxb);
@@ -90,36 +100,14 @@ Work carve(void *ws, int S, uint64_t n) {
     w.trees = b.take<BlockTrees>((size_t)S * w.maxb);
     w.crc_part = b.take<uint32_t>((size_t)S * w.ncrc);
     w.crc_tab = b.take<uint32_t>(8 * 256);
-    (void)b;
+    if (size_out) *size_out = b.off + 256;
     return w;
 }
 
 size_t carve_size(int S, uint64_t n) {
-    Bump b{nullptr};
-    Work w;
-    w.nchunks = (n + CH - 1) / CH;
-    w.maxb = n / BLOCK_SYMS + 2;
-    w.ncrc = (n + 64 + CRC_CHUNK - 1) / CRC_CHUNK + 1;
-    b.take<StreamMeta>(S);
-    b.take<RunTask>((size_t)S * (w.nchunks + 2));
-    b.take<unsigned long long>(1);
-    b.take<uint16_t>((size_t)S * n);
-    b.take<uint64_t>((size_t)S * n);
-    b.take<uint64_t>((size_t)S * w.nchunks);
-    b.take<uint32_t>((size_t)S * (w.nchunks + 1));
-    b.take<uint64_t>((size_t)S * (w.nchunks + 1));
-    b.take<uint8_t>((size_t)S * w.nchunks * 4);
-    b.take<uint32_t>((size_t)S * w.nchunks * 4);
-    b.take<uint8_t>((size_t)S * (w.nchunks + 1));
-    b.take<uint64_t>((size_t)S * w.nchunks);
-    b.take<uint32_t>((size_t)S * (n + 1));
-    b.take<uint64_t>((size_t)S * w.maxb);
-    b.take<uint64_t>((size_t)S * w.maxb);
-    b.take<uint64_t>((size_t)S * w.maxb);
-    b.take<BlockTrees>((size_t)S * w.maxb);
-    b.take<uint32_t>((size_t)S * w.ncrc);
-    b.take<uint32_t>(8 * 256);
-    return b.off + 256;
+    size_t sz = 0;
+    carve(nullptr, S, n, &sz);
+    return sz;
 }
 
 struct InBytes {
@@ -431,41 +419,136 @@ struct RecG {
     __device__ __forceinline__ uint64_t operator()(int64_t q) const { return __ldg(rec + q); }
 };
 
-// thread = (chunk, entry tag); records are read through L1 (the 4 walks of a chunk read
-// the same lines at about the same time)
+// Thread per chunk: the walks from the 4 entry tags run together, the one at the lowest
+// position stepping next.  Two walks that reach the same (position, tag) state evolve
+// identically from then on, so the higher-numbered one stops and keeps only its symbol
+// count offset (the lowest-position-first order guarantees a shared state is seen while
+// both walks sit on it; a merge missed across a periodic jump only costs time).  The
+// four walks usually converge within a few steps, so a chunk costs about one walk.
 __global__ void __launch_bounds__(256) k_sim(uint64_t n, const StreamMeta *meta, const uint64_t *rec_all,
                                             uint64_t nchunks, const uint64_t *bnd_all,
                                             const uint32_t *nbreak_all, uint8_t *exit4, uint32_t *cnt4) {
     const int j = blockIdx.y;
     if (!meta[j].active) return;
-    const uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    const uint64_t k = t >> 2;
-    int tag = (int)(t & 3);
+    const uint64_t k = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (k >= nchunks) return;
     const RecG R{rec_all + (uint64_t)j * n};
     const uint64_t *bnd = bnd_all + (uint64_t)j * (nchunks + 1);
-    const uint64_t b0 = bnd[k], b1 = bnd[k + 1];
+    const int64_t b0 = (int64_t)bnd[k], b1 = (int64_t)bnd[k + 1];
     const NoBytes bytes;
     const uint32_t *nbreak = nbreak_all + (uint64_t)j * (nchunks + 1);
-    uint32_t count = 0;
-    int64_t p = (int64_t)b0;
-    while (p < (int64_t)b1) {
+    int64_t P[4];
+    int T[4], A[4];  // A[t]: the walk t merged into (t while live)
+    uint32_t C[4], D[4];
+#pragma unroll
+    for (int t = 0; t < 4; ++t) P[t] = b0, T[t] = t, A[t] = t, C[t] = 0, D[t] = 0;
+    for (;;) {
+        int w = -1;
+        int64_t p = INT64_MAX;
+        int tag = 0;
+        uint32_t cw = 0;
+#pragma unroll
+        for (int t = 0; t < 4; ++t)
+            if (A[t] == t && P[t] < b1 && P[t] < p) p = P[t], w = t, tag = T[t], cw = C[t];
+        if (w < 0) break;
+        int64_t np;
+        int nt;
         const int64_t m = periodic_run(p, tag, n, nbreak);
         if (m > 0) {
-            count += (uint32_t)m;
-            p += MAX_MATCH * m;
-            continue;
+            np = p + MAX_MATCH * m, nt = TAG_A, cw += (uint32_t)m;
+        } else {
+            const Step s = parse_step(p, tag, (int64_t)n, R(p), p > 0 ? R(p - 1) : 0ull, bytes);
+            np = s.next_p, nt = s.next_tag, cw += s.emit != 0;
         }
-        const Step s = parse_step(p, tag, (int64_t)n, R(p), p > 0 ? R(p - 1) : 0ull, bytes);
-        count += s.emit != 0;
-        p = s.next_p;
-        tag = s.next_tag;
+        int u = -1;
+        uint32_t cu = 0;
+#pragma unroll
+        for (int t = 0; t < 4; ++t) {
+            if (t == w) P[t] = np, T[t] = nt, C[t] = cw;
+            else if (A[t] == t && P[t] == np && T[t] == nt) u = t, cu = C[t];
+        }
+        if (u >= 0) {  // merge the higher-numbered walk into the lower
+#pragma unroll
+            for (int t = 0; t < 4; ++t) {
+                if (t == u && u > w) A[t] = w, D[t] = cu - cw;
+                if (t == w && w > u) A[t] = u, D[t] = cw - cu;
+            }
+        }
     }
-    exit4[((uint64_t)j * nchunks + k) * 4 + (t & 3)] = (uint8_t)tag;
-    cnt4[((uint64_t)j * nchunks + k) * 4 + (t & 3)] = count;
+    uint32_t ex[4], cf[4];
+#pragma unroll
+    for (int t = 0; t < 4; ++t) {
+        ex[t] = (uint32_t)T[t], cf[t] = C[t];
+#pragma unroll
+        for (int v = 0; v < t; ++v)
+            if (A[t] == v) ex[t] = ex[v], cf[t] = cf[v] + D[t];
+    }
+    const uint64_t o = ((uint64_t)j * nchunks + k) * 4;
+#pragma unroll
+    for (int t = 0; t < 4; ++t) {
+        exit4[o + t] = (uint8_t)ex[t];
+        cnt4[o + t] = cf[t];
+    }
 }
 
 // ---------------------------------------------------------------- 6. resolve
+// Two levels: threads compose the transfer maps (exit tag + symbol count per entry tag)
+// of SEG consecutive chunks, one warp per stream scans the segments (k_resolve), and
+// threads expand the segment entries back to per-chunk entry tags and symbol offsets.
+__global__ void __launch_bounds__(256) k_seg_compose(const StreamMeta *meta, uint64_t nchunks, uint64_t nseg,
+                                                    const uint8_t *exit4_all, const uint32_t *cnt4_all,
+                                                    uint8_t *seg_exit4_all, uint32_t *seg_cnt4_all) {
+    const int j = blockIdx.y;
+    if (!meta[j].active) return;
+    const uint64_t g = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (g >= nseg) return;
+    const uint8_t *ex = exit4_all + (uint64_t)j * nchunks * 4;
+    const uint32_t *cn = cnt4_all + (uint64_t)j * nchunks * 4;
+    const uint64_t k1 = min(nchunks, (g + 1) * SEG);
+    uint32_t tg[4] = {0, 1, 2, 3}, c[4] = {0, 0, 0, 0};
+    for (uint64_t k = g * SEG; k < k1; ++k) {
+        const uint32_t e = *reinterpret_cast<const uint32_t *>(ex + k * 4);
+        const uint4 cc = *reinterpret_cast<const uint4 *>(cn + k * 4);
+#pragma unroll
+        for (int t = 0; t < 4; ++t) {
+            const uint32_t x = tg[t];
+            c[t] += x == 0 ? cc.x : x == 1 ? cc.y : x == 2 ? cc.z : cc.w;
+            tg[t] = (e >> (8 * x)) & 0xff;
+        }
+    }
+    const uint64_t o = ((uint64_t)j * nseg + g) * 4;
+#pragma unroll
+    for (int t = 0; t < 4; ++t) seg_exit4_all[o + t] = (uint8_t)tg[t], seg_cnt4_all[o + t] = c[t];
+}
+
+__global__ void __launch_bounds__(256) k_seg_expand(const StreamMeta *meta, uint64_t nchunks, uint64_t nseg,
+                                                   const uint8_t *exit4_all, const uint32_t *cnt4_all,
+                                                   const uint8_t *seg_entry_all, const uint64_t *seg_symoff_all,
+                                                   uint8_t *entry_all, uint64_t *symoff_all) {
+    const int j = blockIdx.y;
+    if (!meta[j].active) return;
+    const uint64_t g = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (g > nseg) return;
+    uint8_t *entry = entry_all + (uint64_t)j * (nchunks + 1);
+    if (g == nseg) {
+        entry[nchunks] = seg_entry_all[(uint64_t)j * (nseg + 1) + nseg];
+        return;
+    }
+    const uint8_t *ex = exit4_all + (uint64_t)j * nchunks * 4;
+    const uint32_t *cn = cnt4_all + (uint64_t)j * nchunks * 4;
+    uint64_t *symoff = symoff_all + (uint64_t)j * nchunks;
+    uint32_t tag = seg_entry_all[(uint64_t)j * (nseg + 1) + g];
+    uint64_t sym = seg_symoff_all[(uint64_t)j * nseg + g];
+    const uint64_t k1 = min(nchunks, (g + 1) * SEG);
+    for (uint64_t k = g * SEG; k < k1; ++k) {
+        entry[k] = (uint8_t)tag;
+        symoff[k] = sym;
+        sym += cn[k * 4 + tag];
+        tag = ex[k * 4 + tag];
+    }
+}
+
+
 __device__ __forceinline__ uint32_t map_apply(uint32_t m, int t) { return (m >> (2 * t)) & 3u; }
 __device__ __forceinline__ uint32_t map_then(uint32_t f, uint32_t g) {  // g(f(t))
     uint32_t r = 0;
@@ -473,6 +556,7 @@ __device__ __forceinline__ uint32_t map_then(uint32_t f, uint32_t g) {  // g(f(t
     return r;
 }
 
+// warp scan of the items' 4->4 maps (items = segments here; `nchunks` counts items)
 __global__ void k_resolve(const uint8_t *in, uint64_t in_stride, uint64_t n, StreamMeta *meta, uint64_t nchunks,
                           const uint8_t *exit4_all, const uint32_t *cnt4_all, uint8_t *entry_all, uint64_t *symoff_all,
                           uint32_t *syms_all, uint64_t maxb, uint64_t *blk_start_all) {
@@ -914,17 +998,32 @@ void DeflateBatch::run(const uint8_t *in, uint64_t in_stride, int S, uint64_t n,
         CKL();
         }
         {
-        ProfScope ps3("deflate.parse", st, (uint64_t)S * n * 20);
+        ProfScope ps3("deflate.anchor", st, (uint64_t)S * n * 8);
         k_anchor<<<dim3((unsigned)((n + TILE - 1) / TILE), S), 256, 0, st>>>(n, w.meta, w.rec, w.nchunks, w.first_anchor);
         CKL();
         k_bounds<<<S, 32, 0, st>>>(n, w.meta, w.nchunks, w.first_anchor, w.bnd, w.nbreak);
         CKL();
-        k_sim<<<dim3((unsigned)((w.nchunks * 4 + 255) / 256), S), 256, 0, st>>>(n, w.meta, w.rec, w.nchunks, w.bnd,
+        }
+        {
+        ProfScope ps3("deflate.sim", st, (uint64_t)S * n * 8);
+        k_sim<<<dim3((unsigned)((w.nchunks + 255) / 256), S), 256, 0, st>>>(n, w.meta, w.rec, w.nchunks, w.bnd,
                                                                               w.nbreak, w.exit4, w.cnt4);
         CKL();
-        k_resolve<<<S, 32, 0, st>>>(in, in_stride, n, w.meta, w.nchunks, w.exit4, w.cnt4, w.entry, w.symoff, w.syms,
-                                    w.maxb, w.blk_start);
+        }
+        {
+        ProfScope ps3("deflate.resolve", st, (uint64_t)S * w.nchunks * 8);
+        const dim3 sg((unsigned)((w.nseg + 1 + 255) / 256), S);
+        k_seg_compose<<<sg, 256, 0, st>>>(w.meta, w.nchunks, w.nseg, w.exit4, w.cnt4, w.seg_exit4, w.seg_cnt4);
         CKL();
+        k_resolve<<<S, 32, 0, st>>>(in, in_stride, n, w.meta, w.nseg, w.seg_exit4, w.seg_cnt4, w.seg_entry,
+                                    w.seg_symoff, w.syms, w.maxb, w.blk_start);
+        CKL();
+        k_seg_expand<<<sg, 256, 0, st>>>(w.meta, w.nchunks, w.nseg, w.exit4, w.cnt4, w.seg_entry, w.seg_symoff,
+                                         w.entry, w.symoff);
+        CKL();
+        }
+        {
+        ProfScope ps3("deflate.emit_syms", st, (uint64_t)S * n * 12);
         k_emit_syms<<<dim3((unsigned)((w.nchunks + 255) / 256), S), 256, 0, st>>>(in, in_stride, n, w.meta, w.rec, w.nchunks, w.bnd, w.nbreak, w.entry, w.symoff, w.syms, w.maxb, w.blk_top, w.blk_start, w.runs, w.nruns);
         CKL();
         k_emit_runs<<<148 * 4, 256, 0, st>>>(n, w.rec, w.syms, w.maxb, w.blk_top, w.blk_start, w.runs, w.nruns);
