@@ -57,7 +57,8 @@ struct Work {
     uint32_t *cnt4;
     uint8_t *entry;
     uint64_t *symoff;
-    uint8_t *seg_exit4, *seg_entry;  // the same per SEG-chunk segment (two-level resolve)
+    uint8_t *seg_exit4, *seg_entry;  // the same per SEG-chunk segment (two-level resolve;
+                                     // seg_symoff/seg_cnt4 first serve the bounds scan)
     uint32_t *seg_cnt4;
     uint64_t *seg_symoff;
     uint32_t *syms;
@@ -355,25 +356,50 @@ __global__ void __launch_bounds__(256) k_anchor(uint64_t n, const StreamMeta *me
 }
 
 // chunk boundaries: bnd[k] = first anchor >= k*CH (suffix-min over chunks)
-__global__ void k_bounds(uint64_t n, const StreamMeta *meta, uint64_t nchunks, const uint64_t *first_anchor,
-                         uint64_t *bnd_all, uint32_t *nbreak_all) {
+// bnd[k] = first anchor >= k*CH (suffix min of the per-chunk first anchors), and
+// nbreak[k] = first chunk >= k that is not entirely 258-byte matches (bit 63 of the
+// record).  Three phases like the resolve: per-segment minima, one warp per stream
+// scanning the segments, per-segment expansion.
+__device__ __forceinline__ void bound_item(uint64_t raw, uint64_t k, uint64_t &v, uint32_t &nb) {
+    v = raw & ~(1ull << 63);
+    nb = !(raw >> 63) ? (uint32_t)k : 0xffffffffu;
+}
+
+__global__ void __launch_bounds__(256) k_bounds_seg(const StreamMeta *meta, uint64_t nchunks, uint64_t nseg,
+                                                   const uint64_t *first_anchor, uint64_t *segv_all,
+                                                   uint32_t *segnb_all) {
+    const int j = blockIdx.y;
+    if (!meta[j].active) return;
+    const uint64_t g = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (g >= nseg) return;
+    const uint64_t *fa = first_anchor + (uint64_t)j * nchunks;
+    uint64_t v = ~0ull;
+    uint32_t nb = 0xffffffffu;
+    for (uint64_t k = g * SEG; k < min(nchunks, (g + 1) * SEG); ++k) {
+        uint64_t x;
+        uint32_t y;
+        bound_item(fa[k], k, x, y);
+        v = x < v ? x : v;
+        nb = y < nb ? y : nb;
+    }
+    segv_all[(uint64_t)j * nseg + g] = v;
+    segnb_all[(uint64_t)j * nseg + g] = nb;
+}
+
+// in place: segv[g] <- min(segv[g..], n), segnb[g] <- min(segnb[g..], nchunks)
+__global__ void k_bounds_scan(uint64_t n, const StreamMeta *meta, uint64_t nchunks, uint64_t nseg, uint64_t *segv_all,
+                              uint32_t *segnb_all) {
     const int j = blockIdx.x;
     if (!meta[j].active) return;
     const unsigned lane = threadIdx.x;
-    const uint64_t *fa = first_anchor + (uint64_t)j * nchunks;
-    uint64_t *bnd = bnd_all + (uint64_t)j * (nchunks + 1);
-    uint32_t *nbreak = nbreak_all + (uint64_t)j * (nchunks + 1);
+    uint64_t *segv = segv_all + (uint64_t)j * nseg;
+    uint32_t *segnb = segnb_all + (uint64_t)j * nseg;
     uint64_t carry = n;
     uint32_t carry_nb = (uint32_t)nchunks;
-    if (lane == 0) {
-        bnd[nchunks] = n;
-        nbreak[nchunks] = (uint32_t)nchunks;
-    }
-    for (int64_t g = (int64_t)((nchunks + 31) / 32) - 1; g >= 0; --g) {
+    for (int64_t g = (int64_t)((nseg + 31) / 32) - 1; g >= 0; --g) {
         const uint64_t k = (uint64_t)g * 32 + lane;
-        const uint64_t raw = k < nchunks ? fa[k] : ~0ull;
-        uint64_t v = k < nchunks ? (raw & ~(1ull << 63)) : ~0ull;
-        uint32_t nb = (k < nchunks && !(raw >> 63)) ? (uint32_t)k : 0xffffffffu;
+        uint64_t v = k < nseg ? segv[k] : ~0ull;
+        uint32_t nb = k < nseg ? segnb[k] : 0xffffffffu;
         for (int o = 1; o < 32; o <<= 1) {  // suffix min
             const uint64_t w = __shfl_down_sync(0xffffffffu, v, o);
             const uint32_t x = __shfl_down_sync(0xffffffffu, nb, o);
@@ -382,12 +408,38 @@ __global__ void k_bounds(uint64_t n, const StreamMeta *meta, uint64_t nchunks, c
         }
         v = v < carry ? v : carry;
         nb = nb < carry_nb ? nb : carry_nb;
-        if (k < nchunks) {
-            bnd[k] = k == 0 ? 0 : v;
-            nbreak[k] = nb;
-        }
+        if (k < nseg) segv[k] = v, segnb[k] = nb;
         carry = __shfl_sync(0xffffffffu, v, 0);
         carry_nb = __shfl_sync(0xffffffffu, nb, 0);
+    }
+}
+
+__global__ void __launch_bounds__(256) k_bounds_expand(uint64_t n, const StreamMeta *meta, uint64_t nchunks,
+                                                      uint64_t nseg, const uint64_t *first_anchor,
+                                                      const uint64_t *segv_all, const uint32_t *segnb_all,
+                                                      uint64_t *bnd_all, uint32_t *nbreak_all) {
+    const int j = blockIdx.y;
+    if (!meta[j].active) return;
+    const uint64_t g = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (g > nseg) return;
+    uint64_t *bnd = bnd_all + (uint64_t)j * (nchunks + 1);
+    uint32_t *nbreak = nbreak_all + (uint64_t)j * (nchunks + 1);
+    if (g == nseg) {
+        bnd[nchunks] = n;
+        nbreak[nchunks] = (uint32_t)nchunks;
+        return;
+    }
+    const uint64_t *fa = first_anchor + (uint64_t)j * nchunks;
+    uint64_t carry = g + 1 < nseg ? segv_all[(uint64_t)j * nseg + g + 1] : n;
+    uint32_t carry_nb = g + 1 < nseg ? segnb_all[(uint64_t)j * nseg + g + 1] : (uint32_t)nchunks;
+    for (int64_t k = (int64_t)min(nchunks, (g + 1) * SEG) - 1; k >= (int64_t)(g * SEG); --k) {
+        uint64_t v;
+        uint32_t nb;
+        bound_item(fa[k], (uint64_t)k, v, nb);
+        carry = v < carry ? v : carry;
+        carry_nb = nb < carry_nb ? nb : carry_nb;
+        bnd[k] = k == 0 ? 0 : carry;
+        nbreak[k] = carry_nb;
     }
 }
 
@@ -1001,7 +1053,13 @@ void DeflateBatch::run(const uint8_t *in, uint64_t in_stride, int S, uint64_t n,
         ProfScope ps3("deflate.anchor", st, (uint64_t)S * n * 8);
         k_anchor<<<dim3((unsigned)((n + TILE - 1) / TILE), S), 256, 0, st>>>(n, w.meta, w.rec, w.nchunks, w.first_anchor);
         CKL();
-        k_bounds<<<S, 32, 0, st>>>(n, w.meta, w.nchunks, w.first_anchor, w.bnd, w.nbreak);
+        const dim3 bg((unsigned)((w.nseg + 1 + 255) / 256), S);
+        k_bounds_seg<<<bg, 256, 0, st>>>(w.meta, w.nchunks, w.nseg, w.first_anchor, w.seg_symoff, w.seg_cnt4);
+        CKL();
+        k_bounds_scan<<<S, 32, 0, st>>>(n, w.meta, w.nchunks, w.nseg, w.seg_symoff, w.seg_cnt4);
+        CKL();
+        k_bounds_expand<<<bg, 256, 0, st>>>(n, w.meta, w.nchunks, w.nseg, w.first_anchor, w.seg_symoff, w.seg_cnt4,
+                                            w.bnd, w.nbreak);
         CKL();
         }
         {
