@@ -741,21 +741,29 @@ __global__ void __launch_bounds__(256) k_emit_runs(uint64_t n, const uint64_t *r
 }
 
 // ------------------------------------------------------------ 8. block plans
-__global__ void __launch_bounds__(256) k_plan(uint64_t n, const StreamMeta *meta, const uint32_t *syms_all,
-                                             uint64_t maxb, const uint64_t *blk_top_all,
-                                             const uint64_t *blk_start_all, BlockTrees *trees_all) {
+// zlib's tree construction (build_tree/gen_bitlen/gen_codes) is a sequential chain of
+// dependent shared-memory operations.  A one-warp CTA per block: the warp tallies the
+// block's symbols, lane 0 builds the trees with every array (scratch and the BlockTrees
+// being written) in shared memory, the warp copies the result out.  Small CTAs let 32
+// independent builders share an SM and hide each other's latency.  (A thread per block
+// was measured slower: the builders diverge, so a warp serialises them.)
+__global__ void __launch_bounds__(32) k_plan(uint64_t n, const StreamMeta *meta, const uint32_t *syms_all,
+                                            uint64_t maxb, const uint64_t *blk_top_all,
+                                            const uint64_t *blk_start_all, BlockTrees *trees_all) {
     const int j = blockIdx.y;
     const StreamMeta &m = meta[j];
     const uint64_t b = blockIdx.x;
     if (!m.active || b >= m.nblocks) return;
     __shared__ uint32_t lf[L_CODES], df[D_CODES];
     __shared__ TreeScratch ts;
-    for (int i = threadIdx.x; i < L_CODES; i += blockDim.x) lf[i] = 0;
-    for (int i = threadIdx.x; i < D_CODES; i += blockDim.x) df[i] = 0;
-    __syncthreads();
+    __shared__ BlockTrees bt;
+    const unsigned lane = threadIdx.x;
+    for (int i = lane; i < L_CODES; i += 32) lf[i] = 0;
+    for (int i = lane; i < D_CODES; i += 32) df[i] = 0;
+    __syncwarp();
     const uint32_t *syms = syms_all + (uint64_t)j * (n + 1);
     const uint64_t s0 = b * BLOCK_SYMS, s1 = min((uint64_t)m.nsyms, (uint64_t)(s0 + BLOCK_SYMS));
-    for (uint64_t i = s0 + threadIdx.x; i < s1; i += blockDim.x) {
+    for (uint64_t i = s0 + lane; i < s1; i += 32) {
         const uint32_t s = syms[i];
         if (sym_is_match(s)) {
             atomicAdd(&lf[length_code(sym_lc(s)) + 257], 1u);
@@ -764,16 +772,22 @@ __global__ void __launch_bounds__(256) k_plan(uint64_t n, const StreamMeta *meta
             atomicAdd(&lf[s], 1u);
         }
     }
-    __syncthreads();
-    if (threadIdx.x != 0) return;
-    lf[END_BLOCK] = 1;
-    const bool last = b + 1 == m.nblocks;
-    const uint64_t *bstart = blk_start_all + (uint64_t)j * maxb;
-    const uint64_t start = bstart[b];
-    const uint64_t stop = last ? n : bstart[b + 1];
-    const uint64_t pf = last ? n : blk_top_all[(uint64_t)j * maxb + b];
-    const int64_t offset = 32768 * slides_before((int64_t)pf, (int64_t)n);
-    plan_block(lf, df, stop - start, (int64_t)start >= offset, last, ts, trees_all[(uint64_t)j * maxb + b]);
+    __syncwarp();
+    if (lane == 0) {
+        lf[END_BLOCK] = 1;
+        const bool last = b + 1 == m.nblocks;
+        const uint64_t *bstart = blk_start_all + (uint64_t)j * maxb;
+        const uint64_t start = bstart[b];
+        const uint64_t stop = last ? n : bstart[b + 1];
+        const uint64_t pf = last ? n : blk_top_all[(uint64_t)j * maxb + b];
+        const int64_t offset = 32768 * slides_before((int64_t)pf, (int64_t)n);
+        plan_block(lf, df, stop - start, (int64_t)start >= offset, last, ts, bt);
+    }
+    __syncwarp();
+    static_assert(sizeof(BlockTrees) % 8 == 0, "BlockTrees copied as 8-byte words");
+    const uint64_t *src = reinterpret_cast<const uint64_t *>(&bt);
+    uint64_t *dst = reinterpret_cast<uint64_t *>(trees_all + (uint64_t)j * maxb + b);
+    for (int i = lane; i < (int)(sizeof(BlockTrees) / 8); i += 32) dst[i] = src[i];
 }
 
 // --------------------------------------------------------------- 9. layout
@@ -1089,7 +1103,7 @@ void DeflateBatch::run(const uint8_t *in, uint64_t in_stride, int S, uint64_t n,
         }
         {
         ProfScope ps4("deflate.blocks", st, (uint64_t)S * n * 4);
-        k_plan<<<dim3((unsigned)w.maxb, S), 256, 0, st>>>(n, w.meta, w.syms, w.maxb, w.blk_top, w.blk_start, w.trees);
+        k_plan<<<dim3((unsigned)w.maxb, S), 32, 0, st>>>(n, w.meta, w.syms, w.maxb, w.blk_top, w.blk_start, w.trees);
         CKL();
         k_layout<<<(S + 31) / 32, 32, 0, st>>>(n, w.meta, S, w.maxb, w.trees, w.blk_bitpos);
         CKL();
