@@ -29,7 +29,11 @@ using namespace ipcg;
 
 struct ipcg_ctx {
     int device = 0;
-    cudaStream_t stream = nullptr;
+    cudaStream_t stream = nullptr;  // all work is ordered on this stream (forks join back)
+    cudaStream_t own_stream = nullptr;
+    std::vector<cudaStream_t> side;  // fork targets (per-level chains)
+    std::vector<cudaEvent_t> events;
+    size_t events_used = 0;
     std::string err;
     void *pinned = nullptr;
     size_t pinned_cap = 0;
@@ -83,6 +87,28 @@ struct DBuf {  // stream-ordered device allocation
         return static_cast<T *>(p);
     }
 };
+
+cudaStream_t side_stream(ipcg_ctx *c, size_t i) {
+    while (c->side.size() <= i) {
+        cudaStream_t s;
+        CK(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+        c->side.push_back(s);
+    }
+    return c->side[i];
+}
+
+// `to` waits for everything enqueued on `from` so far (events are reused across calls:
+// a wait captures the event's state at enqueue time)
+void stream_dep(ipcg_ctx *c, cudaStream_t from, cudaStream_t to) {
+    if (c->events_used == c->events.size()) {
+        cudaEvent_t e;
+        CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        c->events.push_back(e);
+    }
+    cudaEvent_t e = c->events[c->events_used++];
+    CK(cudaEventRecord(e, from));
+    CK(cudaStreamWaitEvent(to, e, 0));
+}
 
 void *pinned(ipcg_ctx *c, size_t bytes) {
     if (bytes > c->pinned_cap) {
@@ -215,6 +241,9 @@ ipcg_archive *compress_impl(ipcg_ctx *c, int scalar, const void *values, int on_
         launch_range(vals, scalar, n, sd->range_part, sd->rng, st);
     }
 
+    // (Forking each level's lossless stage and the loss tables onto side streams was
+    // measured: no gain -- level 1's kernels saturate the GPU, so overlap only hides the
+    // small levels' latency tails, and those are a few ms.)
     uint64_t maxcount = 0;
     size_t ws_bytes = 0;
     for (int l = 1; l <= L; ++l) {
@@ -743,7 +772,8 @@ int ipcg_ctx_create(int device, ipcg_ctx **out) {
         CK(cudaDeviceGetDefaultMemPool(&pool, device));
         uint64_t thr = UINT64_MAX;
         CK(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr));
-        CK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+        CK(cudaStreamCreateWithFlags(&c->own_stream, cudaStreamNonBlocking));
+        c->stream = c->own_stream;
     });
     if (rc != IPCG_OK) {
         *out = nullptr;
@@ -758,8 +788,11 @@ void ipcg_ctx_destroy(ipcg_ctx *c) {
     if (!c) return;
     cudaSetDevice(c->device);
     if (c->stream) cudaStreamSynchronize(c->stream);
+    for (cudaStream_t s : c->side) cudaStreamSynchronize(s);
     if (c->pinned) cudaFreeHost(c->pinned);
-    if (c->stream) cudaStreamDestroy(c->stream);
+    for (cudaStream_t s : c->side) cudaStreamDestroy(s);
+    for (cudaEvent_t e : c->events) cudaEventDestroy(e);
+    if (c->own_stream) cudaStreamDestroy(c->own_stream);
     delete c;
 }
 
@@ -768,7 +801,7 @@ const char *ipcg_last_error(const ipcg_ctx *c) { return c ? c->err.c_str() : g_h
 int ipcg_set_stream(ipcg_ctx *c, void *s) {
     return guarded(c, [&] {
         CK(cudaStreamSynchronize(c->stream));
-        c->stream = static_cast<cudaStream_t>(s);
+        c->stream = s ? static_cast<cudaStream_t>(s) : c->own_stream;
     });
 }
 
