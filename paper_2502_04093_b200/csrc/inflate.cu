@@ -295,89 +295,120 @@ __device__ __forceinline__ uint64_t hslot(uint64_t key, uint64_t cap) {
 }
 
 // ------------------------------------------------------------------ 1. scan
-__device__ __forceinline__ uint64_t load_le64(const uint8_t *p, uint64_t len, uint64_t byte) {
-    uint64_t v = 0;
-    if (byte + 8 <= len) {
-#pragma unroll
-        for (int i = 0; i < 8; ++i) v |= (uint64_t)p[byte + i] << (8 * i);
-    } else {
-        for (int i = 0; i < 8; ++i)
-            if (byte + i < len) v |= (uint64_t)p[byte + i] << (8 * i);
+// A CTA stages a tile of the stream in shared memory; each thread tests 32 consecutive bit
+// offsets from four aligned words (funnel shifts), rejecting on BTYPE/HLIT/HDIST and then on
+// the code-length code's Kraft sum, looked up 4 fields (12 bits) at a time.  Survivors
+// (rare) get the full zlib header validation.
+constexpr int SCAN_TILE = 256 * 4;  // bytes per tile: 4 per thread = 32 bit offsets
+constexpr int SCAN_HALO = 16;       // a header's fixed part spans < 80 bits
+
+__device__ __forceinline__ void scan_offset(const InflateJob &job, const Tables &T, JobMeta *meta, int j,
+                                            Cand *cands, unsigned long long *ncand_total, uint64_t cand_cap,
+                                            uint64_t bit) {
+    Bits b;
+    b.init(job.src, job.src_len, bit + 3);
+    uint8_t lens[320];
+    Canon cs;
+    int nlen, ndist;
+    if (!read_dynamic_header(b, lens, nlen, ndist, cs)) return;
+    Canon cl;
+    if (!canon_build(cl, lens, nlen, 1) || !canon_build(cl, lens + nlen, ndist, 2)) return;
+    const unsigned long long ci = atomicAdd(ncand_total, 1ull);
+    if (ci >= cand_cap) {
+        meta[j].overflow = 1;
+        return;
     }
-    return v;
+    Cand c;
+    c.hdr_bit = bit;
+    c.end_bit = 0;
+    c.out_bytes = 0;
+    c.nsyms = 0;
+    c.job = j;
+    c.ok = 0;
+    cands[ci] = c;
+    // insert into the job's hash table
+    const unsigned long long key = bit + 1;
+    uint64_t sl = hslot(key, T.hcap);
+    for (uint64_t probe = 0; probe < T.hcap; ++probe, sl = (sl + 1) & (T.hcap - 1)) {
+        const unsigned long long prev = atomicCAS(&T.hash[sl], 0ull, key);
+        if (prev == 0ull || prev == key) {
+            T.hval[sl] = (uint32_t)ci;
+            return;
+        }
+    }
+    meta[j].overflow = 1;
+}
+
+// survivors of the cheap filters, validated by k_validate with every lane busy (validating
+// in place left 31 lanes waiting on the one running zlib's header decode)
+struct Survivor {
+    uint64_t bit;
+    int job;
+};
+
+__global__ void __launch_bounds__(256) k_validate(const InflateJob *jobs, const Tables *tabs, JobMeta *meta,
+                                                 const Survivor *surv, const unsigned long long *nsurv,
+                                                 uint64_t surv_cap, Cand *cands, unsigned long long *ncand_total,
+                                                 uint64_t cand_cap) {
+    const uint64_t ns = min((unsigned long long)surv_cap, *nsurv);
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < ns; i += (uint64_t)gridDim.x * blockDim.x) {
+        const Survivor sv = surv[i];
+        scan_offset(jobs[sv.job], tabs[sv.job], meta, sv.job, cands, ncand_total, cand_cap, sv.bit);
+    }
 }
 
 __global__ void __launch_bounds__(256) k_scan(const InflateJob *jobs, const Tables *tabs, JobMeta *meta,
-                                             Cand *cands, unsigned long long *ncand_total, uint64_t cand_cap) {
+                                             Survivor *surv, unsigned long long *nsurv, uint64_t surv_cap) {
+    __shared__ uint16_t kraft4[4096];  // sum of 128 >> l over four 3-bit lengths (0 = unused)
+    __shared__ __align__(16) uint8_t tile[SCAN_TILE + SCAN_HALO];
+    for (int i = threadIdx.x; i < 4096; i += blockDim.x) {
+        uint32_t k = 0;
+        for (int q = 0; q < 4; ++q) {
+            const int l = (i >> (3 * q)) & 7;
+            if (l) k += 128u >> l;
+        }
+        kraft4[i] = (uint16_t)k;
+    }
     const int j = blockIdx.y;
     const InflateJob job = jobs[j];
-    const uint64_t nbits = job.src_len * 8;
-    const Tables T = tabs[j];
-    for (uint64_t byte = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; byte * 8 < nbits;
-         byte += (uint64_t)gridDim.x * blockDim.x) {
-        if (byte < 2) continue;  // zlib header
-        const uint64_t w0 = load_le64(job.src, job.src_len, byte);
-        const uint64_t w1 = load_le64(job.src, job.src_len, byte + 8);
-        for (int k = 0; k < 8; ++k) {
-            const uint64_t lo = k ? (w0 >> k) | (w1 << (64 - k)) : w0;
+    const uint32_t *tw = reinterpret_cast<const uint32_t *>(tile);
+    for (uint64_t t0 = (uint64_t)blockIdx.x * SCAN_TILE; t0 < job.src_len; t0 += (uint64_t)gridDim.x * SCAN_TILE) {
+        __syncthreads();
+        for (int i = threadIdx.x; i < SCAN_TILE + SCAN_HALO; i += blockDim.x)
+            tile[i] = t0 + i < job.src_len ? job.src[t0 + i] : 0;
+        __syncthreads();
+        const uint64_t byte0 = t0 + 4 * threadIdx.x;
+        const uint32_t W0 = tw[threadIdx.x], W1 = tw[threadIdx.x + 1], W2 = tw[threadIdx.x + 2],
+                       W3 = tw[threadIdx.x + 3];
+        const unsigned lane = threadIdx.x & 31;
+        for (int k = 0; k < 32; ++k) {  // warp-convergent: survivors appended with one atomic per warp
+            const uint64_t bit = byte0 * 8 + (uint64_t)k;
+            const uint32_t f0 = __funnelshift_r(W0, W1, k), f1 = __funnelshift_r(W1, W2, k),
+                           f2 = __funnelshift_r(W2, W3, k);
             // BFINAL(1) BTYPE(2)=2 HLIT(5)<=29 HDIST(5)<=29 HCLEN(4)
-            if (((lo >> 1) & 3) != 2) continue;
-            const uint32_t hlit = (uint32_t)(lo >> 3) & 31, hdist = (uint32_t)(lo >> 8) & 31;
-            if (hlit > 29 || hdist > 29) continue;
-            const int ncode = (int)((lo >> 13) & 15) + 4;
-            // code-length code must be complete (Kraft sum == 128 at max length 7)
-            const uint64_t hi = k ? (w1 >> k) : w1;  // bits 64.. of the window start
-            uint32_t kraft = 0;
-            bool over = false;
-            for (int i = 0; i < ncode; ++i) {
-                const int bp = 17 + 3 * i;
-                uint32_t l;
-                if (bp + 3 <= 64) l = (uint32_t)(lo >> bp) & 7;
-                else if (bp >= 64) l = (uint32_t)(hi >> (bp - 64)) & 7;
-                else l = (uint32_t)((lo >> bp) | (hi << (64 - bp))) & 7;
-                if (l) kraft += 128u >> l;
-                if (kraft > 128) {
-                    over = true;
-                    break;
-                }
+            bool ok = bit >= 16 && bit < job.src_len * 8 && ((f0 >> 1) & 3) == 2 && ((f0 >> 3) & 31) <= 29 &&
+                      ((f0 >> 8) & 31) <= 29;
+            if (ok) {
+                // code-length lengths: bits 17 .. 17 + 3*ncode of the window; complete code only
+                const int ncode = (int)((f0 >> 13) & 15) + 4;
+                const uint64_t lo = (uint64_t)f0 | ((uint64_t)f1 << 32);
+                uint64_t cl = (lo >> 17) | ((uint64_t)f2 << 47);  // 57 bits = 19 fields
+                cl &= (1ull << (3 * ncode)) - 1;
+                const uint32_t kraft = (uint32_t)kraft4[cl & 4095] + kraft4[(cl >> 12) & 4095] +
+                                       kraft4[(cl >> 24) & 4095] + kraft4[(cl >> 36) & 4095] +
+                                       kraft4[(cl >> 48) & 511];
+                ok = kraft == 128;
             }
-            if (over || kraft != 128) continue;
-            // full validation (rare)
-            const uint64_t bit = byte * 8 + (uint64_t)k;
-            Bits b;
-            b.init(job.src, job.src_len, bit + 3);
-            uint8_t lens[320];
-            Canon cs;
-            int nlen, ndist;
-            if (!read_dynamic_header(b, lens, nlen, ndist, cs)) continue;
-            Canon cl;
-            if (!canon_build(cl, lens, nlen, 1) || !canon_build(cl, lens + nlen, ndist, 2)) continue;
-            const unsigned long long ci = atomicAdd(ncand_total, 1ull);
-            if (ci >= cand_cap) {
-                meta[j].overflow = 1;
-                continue;
+            const unsigned m = __ballot_sync(0xffffffffu, ok);
+            if (!m) continue;
+            unsigned long long base = 0;
+            if (lane == (unsigned)__ffs(m) - 1) base = atomicAdd(nsurv, (unsigned long long)__popc(m));
+            base = __shfl_sync(0xffffffffu, base, __ffs(m) - 1);
+            if (ok) {
+                const unsigned long long si = base + __popc(m & ((1u << lane) - 1u));
+                if (si < surv_cap) surv[si] = Survivor{bit, j};
+                else meta[j].overflow = 1;
             }
-            Cand c;
-            c.hdr_bit = bit;
-            c.end_bit = 0;
-            c.out_bytes = 0;
-            c.nsyms = 0;
-            c.job = j;
-            c.ok = 0;
-            cands[ci] = c;
-            // insert into the job's hash table
-            const unsigned long long key = bit + 1;
-            uint64_t s = hslot(key, T.hcap);
-            bool placed = false;
-            for (uint64_t probe = 0; probe < T.hcap; ++probe, s = (s + 1) & (T.hcap - 1)) {
-                const unsigned long long prev = atomicCAS(&T.hash[s], 0ull, key);
-                if (prev == 0ull || prev == key) {
-                    T.hval[s] = (uint32_t)ci;
-                    placed = true;
-                    break;
-                }
-            }
-            if (!placed) meta[j].overflow = 1;
         }
     }
 }
@@ -878,13 +909,20 @@ void inflate_batch_host(const std::vector<InflateJob> &jobs, int *status_dev, De
     CK(cudaMemsetAsync(md, 0, (uint8_t *)(ncand + 1) - (uint8_t *)md, st));
     uint8_t *arena = static_cast<uint8_t *>(alloc.get(P.arena + 256, st));
     Cand *cands = static_cast<Cand *>(alloc.get(cand_cap * sizeof(Cand) + 64, st));
+    const uint64_t surv_cap = total_src / 32 + 4096;  // measured: ~1 in 1100 bit offsets survives (overflow -> slow chain path)
+    Survivor *surv = static_cast<Survivor *>(alloc.get(surv_cap * sizeof(Survivor), st));
+    unsigned long long *nsurv = static_cast<unsigned long long *>(alloc.get(8, st));
+    CK(cudaMemsetAsync(nsurv, 0, 8, st));
     k_setup<<<(n + 63) / 64, 64, 0, st>>>(jd, n, td, arena, od, cd);
     CKL();
     k_zero<<<dim3(grid_for(max_dst / 32 + 1024, 256, 512), n), 256, 0, st>>>(jd, td);
     CKL();
     {
         ProfScope ps("inflate.scan", st, total_src);
-        k_scan<<<dim3(grid_for(max_src, 256, 2048), n), 256, 0, st>>>(jd, td, md, cands, ncand, cand_cap);
+        k_scan<<<dim3(grid_for((max_src + SCAN_TILE - 1) / SCAN_TILE, 1, 4096), n), 256, 0, st>>>(jd, td, md, surv,
+                                                                                             nsurv, surv_cap);
+        CKL();
+        k_validate<<<148 * 8, 256, 0, st>>>(jd, td, md, surv, nsurv, surv_cap, cands, ncand, cand_cap);
         CKL();
     }
     unsigned long long hc = 0;
@@ -911,6 +949,22 @@ void inflate_batch_host(const std::vector<InflateJob> &jobs, int *status_dev, De
         uint64_t maxseg = 1;
         for (const JobMeta &m : hm) maxseg = std::max<uint64_t>(maxseg, m.nseg);
         if (getenv("IPCG_DEBUG_INFLATE")) {
+            std::vector<Cand> hcands(nc);
+            CK(cudaMemcpy(hcands.data(), cands, nc * sizeof(Cand), cudaMemcpyDeviceToHost));
+            uint64_t ok = 0, okn = 0, badn = 0, hist[6] = {0, 0, 0, 0, 0, 0};
+            for (const Cand &cc : hcands) {
+                if (cc.ok) ++ok, okn += cc.nsyms;
+                else badn += cc.nsyms;
+                const uint32_t v = cc.nsyms;
+                hist[v == 0 ? 0 : v < 16 ? 1 : v < 256 ? 2 : v < 4096 ? 3 : v < 16000 ? 4 : 5]++;
+            }
+            unsigned long long hs = 0;
+            CK(cudaMemcpy(&hs, nsurv, 8, cudaMemcpyDeviceToHost));
+            fprintf(stderr, "inflate: %llu survivors of %llu bit offsets\n", hs, (unsigned long long)total_src * 8);
+            fprintf(stderr, "inflate: %d jobs, %llu candidates (%llu ok, syms ok %llu bad %llu) nsyms hist 0:%llu <16:%llu <256:%llu <4k:%llu <16k:%llu >=16k:%llu\n",
+                    n, (unsigned long long)nc, (unsigned long long)ok, (unsigned long long)okn, (unsigned long long)badn,
+                    (unsigned long long)hist[0], (unsigned long long)hist[1], (unsigned long long)hist[2],
+                    (unsigned long long)hist[3], (unsigned long long)hist[4], (unsigned long long)hist[5]);
             for (int q = 0; q < n; ++q)
                 fprintf(stderr, "inflate job %d: src %llu dst %llu blocks %u allzero %d status %d\n", q,
                         (unsigned long long)jobs[q].src_len, (unsigned long long)jobs[q].dst_len, hm[q].nblocks,
