@@ -238,6 +238,78 @@ __device__ __forceinline__ int huff_decode(const Huff &h, Bits &b) {
     return -1;
 }
 
+// ---------------------------------------------------- word-refill bit reader
+// 64-bit buffer refilled 32 bits at a time from 4-byte-aligned words (the stream may start
+// at any byte; words wholly past its last byte read as 0).  Used by the symbol loops.
+struct WBits {
+    const uint32_t *w;
+    uint64_t nwords;  // words covering [aligned base, src + len)
+    uint64_t wi;      // next word to load
+    uint64_t buf;
+    int cnt;
+    uint64_t pos;     // absolute bit position (relative to the aligned base) of buf bit 0
+    uint64_t endbit;  // absolute bit position of the end of the stream
+    __device__ __forceinline__ void init(const uint8_t *src, uint64_t len, uint64_t bit) {
+        const uintptr_t a = reinterpret_cast<uintptr_t>(src);
+        const uint64_t off = (uint64_t)(a & 3) * 8;
+        w = reinterpret_cast<const uint32_t *>(a & ~uintptr_t(3));
+        nwords = (off / 8 + len + 3) / 4;
+        endbit = off + 8 * len;
+        const uint64_t abs = off + bit;
+        wi = abs >> 5;
+        buf = 0;
+        cnt = 0;
+        pos = abs & ~31ull;
+        refill();
+        refill();
+        drop((int)(abs & 31));
+    }
+    __device__ __forceinline__ void refill() {
+        if (cnt <= 32) {
+            const uint64_t v = wi < nwords ? __ldg(w + wi) : 0u;
+            buf |= v << cnt;
+            ++wi;
+            cnt += 32;
+        }
+    }
+    __device__ __forceinline__ void drop(int k) {
+        buf >>= k;
+        cnt -= k;
+        pos += (uint64_t)k;
+    }
+    __device__ __forceinline__ uint32_t take(int k) {  // k <= cnt
+        const uint32_t v = (uint32_t)(buf & ((1ull << k) - 1));
+        drop(k);
+        return v;
+    }
+    __device__ __forceinline__ bool overrun() const { return pos > endbit; }
+};
+
+// Huffman decode from the buffer (needs >= 15 valid bits)
+__device__ __forceinline__ int huff_decode_w(const Huff &h, WBits &b) {
+    const uint32_t e = h.fast[b.buf & ((1u << FASTBITS) - 1)];
+    if (e) {
+        b.drop((int)(e >> 12));
+        return (int)(e & 0xfff);
+    }
+    int code = 0, first = 0, index = 0;
+    uint64_t bb = b.buf;
+    for (int len = 1; len <= 15; ++len) {
+        code |= (int)(bb & 1);
+        bb >>= 1;
+        const int count = h.count[len];
+        if (code - count < first) {
+            b.drop(len);
+            return h.sym[index + (code - first)];
+        }
+        index += count;
+        first += count;
+        first <<= 1;
+        code <<= 1;
+    }
+    return -1;
+}
+
 // symbol words: literal = byte; match = 1<<31 | len << 16 | dist  (len <= 258, dist <= 32768)
 __device__ __forceinline__ uint32_t sym_lit(uint32_t c) { return c; }
 __device__ __forceinline__ uint32_t sym_match(uint32_t len, uint32_t dist) {
@@ -443,9 +515,12 @@ __global__ void __launch_bounds__(WARPS * 32) k_decode_cands(const InflateJob *j
         uint32_t ns = 0, nz = 0;
         uint64_t bytes = 0;
         bool good = true;
+        WBits wb;
+        wb.init(job.src, job.src_len, b.used);
         for (;;) {
-            const int sym = huff_decode(lit_s[w], b);
-            if (sym < 0 || b.overrun()) {
+            wb.refill();  // >= 33 bits: a literal/length code and its extra bits
+            const int sym = huff_decode_w(lit_s[w], wb);
+            if (sym < 0) {
                 good = false;
                 break;
             }
@@ -454,7 +529,13 @@ __global__ void __launch_bounds__(WARPS * 32) k_decode_cands(const InflateJob *j
                 good = false;
                 break;
             }
-            if (lane == 0 && ns % SEG == 0) ckpt_pool[ci * NCKPT + ns / SEG] = (uint32_t)bytes;
+            if (ns % SEG == 0) {
+                if (lane == 0) ckpt_pool[ci * NCKPT + ns / SEG] = (uint32_t)bytes;
+                if (wb.overrun()) {
+                    good = false;
+                    break;
+                }
+            }
             if (sym < 256) {
                 if (lane == 0) out[ns] = sym_lit((uint32_t)sym);
                 nz |= (uint32_t)sym;
@@ -467,18 +548,20 @@ __global__ void __launch_bounds__(WARPS * 32) k_decode_cands(const InflateJob *j
                 good = false;
                 break;
             }
-            const uint32_t len = kLBase[li] + b.get(kLExt[li]);
-            const int ds = huff_decode(dist_s[w], b);
+            const uint32_t len = kLBase[li] + wb.take(kLExt[li]);
+            wb.refill();  // >= 33 bits: a distance code and its extra bits
+            const int ds = huff_decode_w(dist_s[w], wb);
             if (ds < 0 || ds >= 30) {
                 good = false;
                 break;
             }
-            const uint32_t d = kDBase[ds] + b.get(kDExt[ds]);
+            const uint32_t d = kDBase[ds] + wb.take(kDExt[ds]);
             if (lane == 0) out[ns] = sym_match(len, d);
             ++ns;
             bytes += len;
         }
-        if (b.overrun()) good = false;
+        if (wb.overrun()) good = false;
+        b.used = wb.pos - (uint64_t)(reinterpret_cast<uintptr_t>(job.src) & 3) * 8;
         if (lane == 0) {
             c.ok = good ? 1 : 0;
             c.nzlit = nz != 0;
