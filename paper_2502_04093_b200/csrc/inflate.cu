@@ -325,6 +325,8 @@ struct JobMeta {
     unsigned long long ncand;
     int allzero;         // every literal of every block is 0 -> output is all zero
     uint32_t nseg;       // emit segments over all blocks
+    uint32_t nfallback;  // blocks the chain decoded itself (fixed, stored excluded, unmatched dynamic)
+    uint64_t fb_syms;    // their symbols
 };
 
 struct Cand {
@@ -334,7 +336,9 @@ struct Cand {
     uint32_t nsyms;
     int job;
     int ok;
-    int nzlit;  // some literal is non-zero
+    int nzlit;   // some literal is non-zero
+    int bfinal;  // BFINAL bit of this block's header
+    int next;    // candidate starting at end_bit, -1 if none (set by k_decode_cands)
 };
 
 struct Blk {
@@ -397,6 +401,9 @@ __device__ __forceinline__ void scan_offset(const InflateJob &job, const Tables 
     c.nsyms = 0;
     c.job = j;
     c.ok = 0;
+    c.nzlit = 0;
+    c.bfinal = (job.src[bit >> 3] >> (bit & 7)) & 1;
+    c.next = -1;
     cands[ci] = c;
     // insert into the job's hash table
     const unsigned long long key = bit + 1;
@@ -486,7 +493,7 @@ __global__ void __launch_bounds__(256) k_scan(const InflateJob *jobs, const Tabl
 }
 
 // ------------------------------------------------------------ 2. candidates
-__global__ void __launch_bounds__(WARPS * 32) k_decode_cands(const InflateJob *jobs, Cand *cands,
+__global__ void __launch_bounds__(WARPS * 32) k_decode_cands(const InflateJob *jobs, const Tables *tabs, Cand *cands,
                                                            const unsigned long long *ncand_total, uint64_t cand_cap,
                                                            uint32_t *pool, uint32_t *ckpt_pool) {
     __shared__ Huff lit_s[WARPS], dist_s[WARPS];
@@ -568,6 +575,20 @@ __global__ void __launch_bounds__(WARPS * 32) k_decode_cands(const InflateJob *j
             c.end_bit = b.used;
             c.nsyms = ns;
             c.out_bytes = bytes;
+            // link to the candidate that starts where this block ends (the chain follows it)
+            int nx = -1;
+            const Tables T = tabs[c.job];
+            const unsigned long long key = b.used + 1;
+            uint64_t sl = hslot(key, T.hcap);
+            for (uint64_t probe = 0; probe < T.hcap; ++probe, sl = (sl + 1) & (T.hcap - 1)) {
+                const unsigned long long k = T.hash[sl];
+                if (k == 0ull) break;
+                if (k == key) {
+                    nx = (int)T.hval[sl];
+                    break;
+                }
+            }
+            c.next = nx;
         }
         __syncwarp();
     }
@@ -634,17 +655,41 @@ __global__ void k_chain(const InflateJob *jobs, int njobs, const Tables *tabs, J
     }
     uint64_t e = 16;
     int last = 0;
+    int pending = -1;  // candidate known (linked by k_decode_cands) to start at e
     while (!err && !last) {
-        Bits b;
-        b.init(job.src, job.src_len, e);
-        last = (int)b.get(1);
-        const uint32_t type = b.get(2);
         if (nb >= T.bcap) {
             err = true;
             break;
         }
         Blk blk;
         blk.out_off = out;
+        if (pending >= 0 && cands[pending].ok) {  // fast path: no header read, no hash probe
+            const Cand &c = cands[pending];
+            last = c.bfinal;
+            blk.type = 1;
+            blk.ckpt = (uint64_t)pending;
+            blk.src = (uint64_t)pending * MAXSYM;
+            blk.nsyms = c.nsyms;
+            blk.out_len = c.out_bytes;
+            e = c.end_bit;
+            if (c.nzlit) nonzero = true;
+            pending = c.next;
+            out += blk.out_len;
+            if (out > job.dst_len) {
+                err = true;
+                break;
+            }
+            blk.nseg = blk.nsyms > 0 ? (blk.nsyms + SEG - 1) / SEG : 1;
+            blk.seg_base = segs;
+            segs += blk.nseg;
+            T.blocks[nb++] = blk;
+            continue;
+        }
+        pending = -1;
+        Bits b;
+        b.init(job.src, job.src_len, e);
+        last = (int)b.get(1);
+        const uint32_t type = b.get(2);
         if (type == 0) {
             const uint64_t bp = (b.used + 7) >> 3;
             if (bp + 4 > job.src_len) {
@@ -684,6 +729,7 @@ __global__ void k_chain(const InflateJob *jobs, int njobs, const Tables *tabs, J
                             blk.out_len = c.out_bytes;
                             e = c.end_bit;
                             found = true;
+                            pending = c.next;
                             if (c.nzlit) nonzero = true;
                         }
                         break;
@@ -699,6 +745,8 @@ __global__ void k_chain(const InflateJob *jobs, int njobs, const Tables *tabs, J
                     break;
                 }
                 blk.type = 2;  // symbols in the job's fallback buffer
+                ++m.nfallback;
+                m.fb_syms += ns;
                 blk.ckpt = ~0ull;
                 blk.src = f0;
                 blk.nsyms = ns;
@@ -1018,7 +1066,7 @@ void inflate_batch_host(const std::vector<InflateJob> &jobs, int *status_dev, De
         ProfScope ps("inflate.decode", st, total_src);
         if (nc) {
             const unsigned g = (unsigned)std::min<uint64_t>((nc + WARPS - 1) / WARPS, 148ull * 16);
-            k_decode_cands<<<g, WARPS * 32, 0, st>>>(jd, cands, ncand, cand_cap, pool, ckpt);
+            k_decode_cands<<<g, WARPS * 32, 0, st>>>(jd, td, cands, ncand, cand_cap, pool, ckpt);
             CKL();
         }
         k_chain<<<(n + 31) / 32, 32, 0, st>>>(jd, n, td, md, cands);
@@ -1049,9 +1097,9 @@ void inflate_batch_host(const std::vector<InflateJob> &jobs, int *status_dev, De
                     (unsigned long long)hist[0], (unsigned long long)hist[1], (unsigned long long)hist[2],
                     (unsigned long long)hist[3], (unsigned long long)hist[4], (unsigned long long)hist[5]);
             for (int q = 0; q < n; ++q)
-                fprintf(stderr, "inflate job %d: src %llu dst %llu blocks %u allzero %d status %d\n", q,
+                fprintf(stderr, "inflate job %d: src %llu dst %llu blocks %u allzero %d status %d fallback %u (%llu syms)\n", q,
                         (unsigned long long)jobs[q].src_len, (unsigned long long)jobs[q].dst_len, hm[q].nblocks,
-                        hm[q].allzero, hm[q].status);
+                        hm[q].allzero, hm[q].status, hm[q].nfallback, (unsigned long long)hm[q].fb_syms);
         }
         {
             ProfScope ps2("inflate.emit_blocks", st, max_dst * n);
