@@ -26,6 +26,9 @@
 
 #include "inflate.cuh"
 
+#include <cooperative_groups.h>
+namespace cg = cooperative_groups;
+
 namespace ipcg {
 
 namespace {
@@ -360,6 +363,7 @@ struct Tables {  // per-job device pointers
     uint32_t *fallback;  // symbols decoded by the chain itself
     uint64_t fcap;
     uint32_t *flags;     // unresolved-byte bitmap
+    uint32_t *mark;      // unresolved bytes that some pointer targets (resolve)
     uint32_t *ptr;       // source pointer of unresolved bytes
 };
 
@@ -823,90 +827,135 @@ __global__ void __launch_bounds__(WARPS * 32) k_emit(const InflateJob *jobs, con
     const uint64_t b0 = blk.out_off + (seg ? ckpt_pool[blk.ckpt * NCKPT + seg] : 0);
     const uint32_t *syms = blk.type == 1 ? pool + blk.src : T.fallback + blk.src;
     uint64_t o = b0;
-    for (uint32_t s = s_begin; s < s_end; ++s) {
-        const uint32_t v = syms[s];
-        if (!(v & 0x80000000u)) {
-            if (lane == 0) dst[o] = (uint8_t)v;
-            ++o;
-            continue;
+    // 32 symbols per step: output offsets by a warp prefix sum, literals written in parallel,
+    // then the step's matches in order (a match may read bytes of earlier ones)
+    for (uint32_t sb = s_begin; sb < s_end; sb += 32) {
+        const uint32_t s = sb + lane;
+        const bool valid = s < s_end;
+        const uint32_t v = valid ? syms[s] : 0u;
+        const bool ismatch = valid && (v & 0x80000000u);
+        const uint32_t mylen = !valid ? 0u : ismatch ? ((v >> 16) & 0x1ff) : 1u;
+        uint32_t incl = mylen;
+#pragma unroll
+        for (int off = 1; off < 32; off <<= 1) {
+            const uint32_t t = __shfl_up_sync(0xffffffffu, incl, off);
+            if ((int)lane >= off) incl += t;
         }
-        const uint32_t len = (v >> 16) & 0x1ff, d = (v & 0xffff) + 1;
+        const uint32_t my_rel = incl - mylen;
+        if (valid && !ismatch) dst[o + my_rel] = (uint8_t)v;
         __syncwarp();
-        // every source byte precedes o, so the lanes of one match never depend on each other;
-        // unresolved bytes (sources in earlier blocks) get a pointer, and their flag bits are
-        // set with one ballot-aggregated atomic per 32 bytes
-        for (uint32_t base = 0; base < len; base += 32) {
-            const uint32_t i = base + lane;
-            const bool act = i < len;
-            bool unres = false;
-            if (act) {
-                const uint64_t src = o - d + (d < len ? (i % d) : i);
-                const uint64_t t = o + i;
-                if (src >= b0) {
-                    if (flag_get(T.flags, src)) {
-                        T.ptr[t] = T.ptr[src];
-                        unres = true;
+        unsigned mm = __ballot_sync(0xffffffffu, ismatch);
+        while (mm) {
+            const int l = __ffs(mm) - 1;
+            mm &= mm - 1;
+            const uint32_t mv = __shfl_sync(0xffffffffu, v, l);
+            const uint64_t mo = o + __shfl_sync(0xffffffffu, my_rel, l);
+            const uint32_t len = (mv >> 16) & 0x1ff, d = (mv & 0xffff) + 1;
+            // every source byte precedes mo, so the lanes of one match never depend on each other;
+            // unresolved bytes (sources in earlier segments) get a pointer, and their flag bits
+            // are set with one ballot-aggregated atomic per 32 bytes
+            for (uint32_t base = 0; base < len; base += 32) {
+                const uint32_t i = base + lane;
+                const bool act = i < len;
+                bool unres = false;
+                if (act) {
+                    const uint64_t src = mo - d + (d < len ? (i % d) : i);
+                    const uint64_t t = mo + i;
+                    if (src >= b0) {
+                        if (flag_get(T.flags, src)) {
+                            T.ptr[t] = T.ptr[src];
+                            unres = true;
+                        } else {
+                            dst[t] = dst[src];
+                        }
                     } else {
-                        dst[t] = dst[src];
+                        T.ptr[t] = (uint32_t)src;
+                        unres = true;
                     }
-                } else {
-                    T.ptr[t] = (uint32_t)src;
-                    unres = true;
                 }
-            }
-            const unsigned m = __ballot_sync(0xffffffffu, unres);
-            if (m) {
-                const uint64_t t0 = o + base;
-                const unsigned sh = (unsigned)(t0 & 31);
-                if (lane == 0) atomicOr(&T.flags[t0 >> 5], m << sh);
-                if (lane == 1 && sh) atomicOr(&T.flags[(t0 >> 5) + 1], m >> (32 - sh));
+                const unsigned m = __ballot_sync(0xffffffffu, unres);
+                if (m) {
+                    const uint64_t t0 = mo + base;
+                    const unsigned sh = (unsigned)(t0 & 31);
+                    if (lane == 0) atomicOr(&T.flags[t0 >> 5], m << sh);
+                    if (lane == 1 && sh) atomicOr(&T.flags[(t0 >> 5) + 1], m >> (32 - sh));
+                }
+                __syncwarp();
             }
         }
-        __syncwarp();
-        o += len;
+        o += __shfl_sync(0xffffffffu, incl, 31);
     }
 }
 
 // ------------------------------------------------------------------ 5. resolve
-// pointer jumping: ptr[t] <- ptr[ptr[t]] while the target is itself unresolved.  Every
-// pointer always names an earlier byte with the same final value, so concurrent updates
-// are benign; each round halves the remaining chain length.
-__global__ void k_jump(const InflateJob *jobs, const Tables *tabs, const JobMeta *meta) {
-    const int j = blockIdx.y;
-    if (meta[j].status || meta[j].allzero) return;
-    const InflateJob job = jobs[j];
-    const Tables T = tabs[j];
-    const uint64_t words = (job.dst_len + 31) / 32;
-    for (uint64_t wi = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; wi < words;
-         wi += (uint64_t)gridDim.x * blockDim.x) {
-        uint32_t f = T.flags[wi];
-        while (f) {
-            const int bit = __ffs(f) - 1;
-            f &= f - 1;
-            const uint64_t t = wi * 32 + (uint64_t)bit;
-            const uint32_t s = T.ptr[t];
-            if (flag_get(T.flags, s)) T.ptr[t] = T.ptr[s];
+// Every unresolved byte t points (ptr[t]) to an earlier byte with the same final value.  In
+// run-heavy planes nearly every byte of every segment after the first is unresolved and the
+// chains cross all segments, but they funnel through few distinct bytes (the tails of
+// earlier segments).  So, in one cooperative launch:
+//   A. mark every unresolved byte that some pointer targets (the marked set is closed under
+//      ptr: a marked byte's own target is marked by it);
+//   B. pointer-jump on the marked bytes only, until none targets an unresolved byte;
+//   C. resolve every unresolved byte in one step (its target is resolved or marked).
+// (Jumping on all unresolved bytes cost ~8 rounds x 40 M random updates.)
+template <class F>
+__device__ __forceinline__ void for_each_set(const uint32_t *bits, uint64_t words, uint64_t tid, uint64_t nth, F &&f) {
+    for (uint64_t wi = tid; wi < words; wi += nth) {
+        uint32_t x = bits[wi];
+        while (x) {
+            const int b = __ffs(x) - 1;
+            x &= x - 1;
+            f(wi * 32 + (uint64_t)b);
         }
     }
 }
 
-__global__ void k_resolve(const InflateJob *jobs, const Tables *tabs, const JobMeta *meta) {
-    const int j = blockIdx.y;
-    if (meta[j].status || meta[j].allzero) return;
-    const InflateJob job = jobs[j];
-    const Tables T = tabs[j];
-    const uint64_t words = (job.dst_len + 31) / 32;
-    for (uint64_t wi = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; wi < words;
-         wi += (uint64_t)gridDim.x * blockDim.x) {
-        uint32_t f = T.flags[wi];
-        while (f) {
-            const int bit = __ffs(f) - 1;
-            f &= f - 1;
-            const uint64_t t = wi * 32 + (uint64_t)bit;
-            uint64_t s = T.ptr[t];
-            while (flag_get(T.flags, s)) s = T.ptr[s];
-            job.dst[t] = job.dst[s];
+__global__ void __launch_bounds__(256) k_resolve_all(const InflateJob *jobs, const Tables *tabs, const JobMeta *meta,
+                                                    int njobs, unsigned *changed) {
+    cg::grid_group grid = cg::this_grid();
+    const uint64_t tid = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+    const uint64_t nth = (uint64_t)gridDim.x * blockDim.x;
+    // A
+    for (int j = 0; j < njobs; ++j) {
+        if (meta[j].status || meta[j].allzero) continue;
+        const Tables T = tabs[j];
+        for_each_set(T.flags, (jobs[j].dst_len + 31) / 32, tid, nth, [&](uint64_t t) {
+            const uint32_t s = T.ptr[t];
+            if (flag_get(T.flags, s) && !flag_get(T.mark, s)) atomicOr(&T.mark[s >> 5], 1u << (s & 31));
+        });
+    }
+    grid.sync();
+    // B
+    for (int round = 0;; ++round) {
+        if (tid == 0) changed[(round + 1) % 3] = 0;  // its last reader finished before the previous sync
+        bool any = false;
+        for (int j = 0; j < njobs; ++j) {
+            if (meta[j].status || meta[j].allzero) continue;
+            const Tables T = tabs[j];
+            for_each_set(T.mark, (jobs[j].dst_len + 31) / 32, tid, nth, [&](uint64_t t) {
+                const uint32_t s = T.ptr[t];
+                if (flag_get(T.flags, s)) {
+                    T.ptr[t] = T.ptr[s];
+                    any = true;
+                }
+            });
         }
+        if (__any_sync(0xffffffffu, any) && (threadIdx.x & 31) == 0) atomicOr(&changed[round % 3], 1u);
+        grid.sync();
+        if (*(volatile unsigned *)&changed[round % 3] == 0) {
+            if (tid == 0) changed[3] = (unsigned)round + 1;  // rounds run (diagnostics)
+            break;
+        }
+    }
+    // C
+    for (int j = 0; j < njobs; ++j) {
+        if (meta[j].status || meta[j].allzero) continue;
+        const InflateJob job = jobs[j];
+        const Tables T = tabs[j];
+        for_each_set(T.flags, (job.dst_len + 31) / 32, tid, nth, [&](uint64_t t) {
+            uint32_t s = T.ptr[t];
+            if (flag_get(T.flags, s)) s = T.ptr[s];
+            job.dst[t] = job.dst[s];
+        });
     }
 }
 
@@ -945,7 +994,7 @@ __global__ void k_finish(const InflateJob *jobs, int njobs, JobMeta *meta, const
     status[j] = m.status;
 }
 
-// per-job arena: [hash keys | flags] (zeroed) then [hash values | blocks | fallback | ptr]
+// per-job arena: [hash keys | flags | mark] (zeroed) then [hash values | blocks | fallback | ptr]
 __global__ void k_setup(const InflateJob *jobs, int njobs, Tables *tabs, uint8_t *arena, const uint64_t *offs,
                         const uint64_t *caps) {
     const int j = blockIdx.x * blockDim.x + threadIdx.x;
@@ -959,6 +1008,8 @@ __global__ void k_setup(const InflateJob *jobs, int njobs, Tables *tabs, uint8_t
     T.hash = reinterpret_cast<unsigned long long *>(a);
     a += T.hcap * 8;
     T.flags = reinterpret_cast<uint32_t *>(a);
+    a += ((n + 31) / 32) * 4 + 16;
+    T.mark = reinterpret_cast<uint32_t *>(a);
     a += ((n + 31) / 32) * 4 + 16;
     a = reinterpret_cast<uint8_t *>(((uintptr_t)a + 15) & ~uintptr_t(15));
     T.hval = reinterpret_cast<uint32_t *>(a);
@@ -975,7 +1026,7 @@ __global__ void k_setup(const InflateJob *jobs, int njobs, Tables *tabs, uint8_t
 __global__ void k_zero(const InflateJob *jobs, const Tables *tabs) {
     const int j = blockIdx.y;
     const Tables T = tabs[j];
-    const uint64_t words = (T.hcap * 8 + ((jobs[j].dst_len + 31) / 32) * 4 + 16) / 4;
+    const uint64_t words = (T.hcap * 8 + 2 * (((jobs[j].dst_len + 31) / 32) * 4 + 16)) / 4;
     uint32_t *z = reinterpret_cast<uint32_t *>(T.hash);
     for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < words; i += (uint64_t)gridDim.x * blockDim.x)
         z[i] = 0;
@@ -1001,7 +1052,7 @@ static InflatePlan plan_jobs(const std::vector<InflateJob> &jobs) {
         const uint64_t hcap = pow2_at_least(2 * (j.src_len / 512 + 64));
         const uint64_t bcap = j.src_len / 16 + 64;  // zlib blocks are >= 2 KiB compressed
         const uint64_t fcap = j.dst_len + 16;
-        const uint64_t bytes = hcap * 12 + 64 + bcap * sizeof(Blk) + fcap * 4 + ((j.dst_len + 31) / 32) * 4 + 16 +
+        const uint64_t bytes = hcap * 12 + 64 + bcap * sizeof(Blk) + fcap * 4 + 2 * (((j.dst_len + 31) / 32) * 4 + 16) +
                                (j.dst_len + 4) * 4 + 64;
         p.offs.push_back(p.arena);
         p.caps.insert(p.caps.end(), {hcap, bcap, fcap, 0});
@@ -1110,15 +1161,35 @@ void inflate_batch_host(const std::vector<InflateJob> &jobs, int *status_dev, De
         }
         {
             ProfScope ps3("inflate.resolve", st, max_dst * n / 8);
-            // pointers chain backwards through at most maxseg segments: halve the depth per round
-            int rounds = 0;
-            while ((1ull << rounds) < maxseg) ++rounds;
-            for (int r = 0; r < rounds; ++r) {
-                k_jump<<<dim3(grid_for((max_dst + 31) / 32, 256, 1024), n), 256, 0, st>>>(jd, td, md);
-                CKL();
+            unsigned *changed = static_cast<unsigned *>(alloc.get(4 * sizeof(unsigned), st));
+            CK(cudaMemsetAsync(changed, 0, 4 * sizeof(unsigned), st));
+            static int coop_blocks = 0;
+            if (!coop_blocks) {
+                int dev = 0, sms = 0, per = 0;
+                CK(cudaGetDevice(&dev));
+                CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+                CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_resolve_all, 256, 0));
+                coop_blocks = sms * std::max(1, std::min(per, 4));
             }
-            k_resolve<<<dim3(grid_for((max_dst + 31) / 32, 256, 1024), n), 256, 0, st>>>(jd, td, md);
+            int nj = n;
+            void *args[] = {(void *)&jd, (void *)&td, (void *)&md, (void *)&nj, (void *)&changed};
+            CK(cudaLaunchCooperativeKernel((const void *)k_resolve_all, dim3(coop_blocks), dim3(256), args, 0, st));
             CKL();
+            if (getenv("IPCG_DEBUG_INFLATE")) {
+                unsigned hr[4];
+                CK(cudaStreamSynchronize(st));
+                CK(cudaMemcpy(hr, changed, sizeof(hr), cudaMemcpyDeviceToHost));
+                uint64_t unres = 0;
+                std::vector<Tables> ht(n);
+                CK(cudaMemcpy(ht.data(), td, n * sizeof(Tables), cudaMemcpyDeviceToHost));
+                for (int q = 0; q < n; ++q) {
+                    std::vector<uint32_t> fl((jobs[q].dst_len + 31) / 32);
+                    CK(cudaMemcpy(fl.data(), ht[q].flags, fl.size() * 4, cudaMemcpyDeviceToHost));
+                    for (uint32_t x : fl) unres += __builtin_popcount(x);
+                }
+                fprintf(stderr, "inflate: resolve rounds %u, unresolved bytes %llu of %llu\n", hr[3],
+                        (unsigned long long)unres, (unsigned long long)(max_dst * n));
+            }
         }
         ProfScope ps4("inflate.adler", st, max_dst * n);
         k_adler<<<dim3(grid_for(max_dst, 256, 256), n), 256, 0, st>>>(jd, md, acc);
