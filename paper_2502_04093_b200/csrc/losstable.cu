@@ -27,6 +27,7 @@ struct LossGeom {
     int R[4];      // staged region extents T + 2H
     int NT[4];     // boxes per axis
     int S[4];      // row-major strides of the staged region
+    uint64_t Rm[4];  // ceil(2^32 / R[i]): x / R[i] == (x * Rm[i]) >> 32 for x, R[i] < 2^16
     int region;
     int paxis[4];
     uint64_t pbase[4];
@@ -35,101 +36,86 @@ struct LossGeom {
 
 __device__ __forceinline__ int32_t from_nb(uint32_t w) { return (int32_t)((w ^ kNbMask) - kNbMask); }
 
+// Per CTA: (1) enumerate each pass's evaluation points directly from its sub-lattice
+// (axes < j: the box; axis j: odd coordinates in the box; axes > j: even coordinates in the
+// box widened by the halo), storing (staged position, edge class, interior flag) and the
+// point's codeword; (2) replay the valid d (a contiguous range) two at a time, one
+// deviation array each, so list/code/address work and barriers are shared by the pair.
 template <bool Cubic>
 __global__ void __launch_bounds__(LT_THREADS) k_loss_fused(const uint32_t *__restrict__ nb, LossGeom g, double unit,
                                                           const uint32_t *lowor, unsigned long long *raw) {
-    extern __shared__ unsigned char smem[];
-    double *dev = reinterpret_cast<double *>(smem);
-    uint32_t *code = reinterpret_cast<uint32_t *>(dev + g.region);
-    uint16_t *list = reinterpret_cast<uint16_t *>(code + g.region);  // per-pass work lists
-    __shared__ int cnt[4], off[5];
-    __shared__ double red[LT_THREADS / 32];
+    extern __shared__ __align__(16) unsigned char smem[];
     const uint32_t lo = *lowor;
     if (lo == 0) return;
-    // box origin
+    double *dev0 = reinterpret_cast<double *>(smem);
+    double *dev1 = dev0 + g.region;
+    uint32_t *codes = reinterpret_cast<uint32_t *>(dev1 + g.region);
+    uint16_t *list = reinterpret_cast<uint16_t *>(codes + g.region);  // u | edge << 13 | interior << 15
+    __shared__ int off[5];
+    __shared__ int first[4][4], cnt[4][4];
+    __shared__ uint64_t mag[4][4];  // ceil(2^32 / cnt)
+    __shared__ double red[2][LT_THREADS / 32];
     int tile = blockIdx.x, t0[4];
     for (int i = g.nd - 1; i >= 0; --i) {
         t0[i] = (tile % g.NT[i]) * g.T[i];
         tile /= g.NT[i];
     }
-    if (threadIdx.x < 4) cnt[threadIdx.x] = 0;
-    __syncthreads();
-    // stage codewords, classify every staged position, count per-pass work
-    for (int u = threadIdx.x; u < g.region; u += blockDim.x) {
-        dev[u] = 0.0;
-        int lu[4], m[4], rem = u;
-        for (int i = g.nd - 1; i >= 0; --i) {
-            lu[i] = rem % g.R[i];
-            rem /= g.R[i];
-            m[i] = t0[i] - g.H[i] + lu[i];
-        }
-        bool in = true;
-        int j = -1;
-        for (int i = 0; i < g.nd; ++i) {
-            if (m[i] < 0 || m[i] >= g.M[i]) in = false;
-            if (m[i] & 1) j = i;
-        }
-        uint32_t w = 0;
-        if (in && j >= 0) {
-            int pi = 0;
-            while (g.paxis[pi] != j) ++pi;
-            uint64_t ord = 0;
-            for (int i = 0; i < g.nd; ++i) {
-                const uint32_t idx = i < j ? (uint32_t)m[i] : i == j ? (uint32_t)(m[i] - 1) / 2 : (uint32_t)m[i] / 2;
-                ord = ord * g.pcnt[pi][i] + idx;
-            }
-            w = nb[g.pbase[pi] + ord];
-            // member of pass j's evaluation region: inside the box on axes <= j
-            bool member = true;
-            for (int i = 0; i <= j; ++i)
-                if (lu[i] < g.H[i] || lu[i] >= g.H[i] + g.T[i]) member = false;
-            if (member) atomicAdd(&cnt[pi], 1);
-        }
-        code[u] = w;
-    }
-    __syncthreads();
     if (threadIdx.x == 0) {
         off[0] = 0;
-        for (int p = 0; p < g.npass; ++p) off[p + 1] = off[p] + cnt[p];
-        for (int p = 0; p < 4; ++p) cnt[p] = 0;
+        for (int p = 0; p < g.npass; ++p) {
+            const int j = g.paxis[p];
+            int total = 1;
+            for (int i = 0; i < g.nd; ++i) {
+                int a0, a1, step;
+                if (i < j) a0 = t0[i], a1 = min(t0[i] + g.T[i], g.M[i]), step = 1;
+                else if (i == j) a0 = t0[i] | 1, a1 = min(t0[i] + g.T[i], g.M[i]), step = 2;
+                else a0 = max(t0[i] - g.H[i], 0), a0 += a0 & 1, a1 = min(t0[i] + g.T[i] + g.H[i], g.M[i]), step = 2;
+                const int c = a1 > a0 ? (a1 - a0 + step - 1) / step : 0;
+                first[p][i] = a0;
+                cnt[p][i] = c;
+                mag[p][i] = c ? ((1ull << 32) + (uint64_t)c - 1) / (uint64_t)c : 0;
+                total *= c;
+            }
+            off[p + 1] = off[p] + total;
+        }
     }
+    for (int u = threadIdx.x; u < 2 * g.region; u += blockDim.x) dev0[u] = 0.0;
     __syncthreads();
-    // build the lists: entry = position (13 bits) | edge class << 13 | interior << 15
-    for (int u = threadIdx.x; u < g.region; u += blockDim.x) {
-        int lu[4], m[4], rem = u;
+    const int nent = off[g.npass];
+    for (int e = threadIdx.x; e < nent; e += blockDim.x) {
+        int p = 0;
+        while (e >= off[p + 1]) ++p;
+        const int j = g.paxis[p];
+        int rem = e - off[p], u = 0, mj = 0;
+        uint64_t ord = 0;
+        bool interior = true;
+        int m[4];
         for (int i = g.nd - 1; i >= 0; --i) {
-            lu[i] = rem % g.R[i];
-            rem /= g.R[i];
-            m[i] = t0[i] - g.H[i] + lu[i];
+            const int q = (int)(((uint64_t)rem * mag[p][i]) >> 32);
+            const int k = rem - q * cnt[p][i];
+            rem = q;
+            m[i] = first[p][i] + (i < j ? k : 2 * k);
         }
-        bool in = true;
-        int j = -1;
         for (int i = 0; i < g.nd; ++i) {
-            if (m[i] < 0 || m[i] >= g.M[i]) in = false;
-            if (m[i] & 1) j = i;
+            u += (m[i] - t0[i] + g.H[i]) * g.S[i];
+            if (m[i] < t0[i] || m[i] >= t0[i] + g.T[i]) interior = false;
+            const uint32_t idx = i < j ? (uint32_t)m[i] : i == j ? (uint32_t)(m[i] - 1) / 2 : (uint32_t)m[i] / 2;
+            ord = ord * g.pcnt[p][i] + idx;
+            if (i == j) mj = m[i];
         }
-        if (!in || j < 0) continue;
-        bool member = true, interior = true;
-        for (int i = 0; i < g.nd; ++i) {
-            const bool inbox = lu[i] >= g.H[i] && lu[i] < g.H[i] + g.T[i];
-            if (i <= j && !inbox) member = false;
-            if (!inbox) interior = false;
-        }
-        if (!member) continue;
-        int pi = 0;
-        while (g.paxis[pi] != j) ++pi;
-        const int mj = m[j];
         const int edge = (Cubic && mj >= 3 && mj + 3 < g.M[j]) ? 0 : (mj + 1 < g.M[j]) ? 1 : 2;
-        const int slot = off[pi] + atomicAdd(&cnt[pi], 1);
-        list[slot] = (uint16_t)(u | (edge << 13) | ((interior ? 1 : 0) << 15));
+        codes[e] = __ldg(nb + g.pbase[p] + ord);
+        list[e] = (uint16_t)(u | (edge << 13) | ((interior ? 1 : 0) << 15));
     }
     __syncthreads();
+    const int d0 = __ffs((int)lo);  // first d whose mask reaches a set bit
     const int hb = 31 - __clz(lo);
     const int dmax = hb + 1 < 32 ? hb + 1 : 32;
-    for (int d = 1; d <= dmax; ++d) {
-        const uint32_t mask = d == 32 ? 0xFFFFFFFFu : ((1u << d) - 1u);
-        if ((lo & mask) == 0) continue;
-        double worst = 0.0;
+    for (int da = d0; da <= dmax; da += 2) {
+        const int db = da + 1 <= dmax ? da + 1 : da;  // a lone last d is computed twice
+        const uint32_t ma = da == 32 ? 0xFFFFFFFFu : ((1u << da) - 1u);
+        const uint32_t mb = db == 32 ? 0xFFFFFFFFu : ((1u << db) - 1u);
+        double wa = 0.0, wb = 0.0;
         for (int pi = 0; pi < g.npass; ++pi) {
             const int stp = g.S[g.paxis[pi]];
             // without a halo along the pass axis (the first axis) every source is a coarser
@@ -138,38 +124,46 @@ __global__ void __launch_bounds__(LT_THREADS) k_loss_fused(const uint32_t *__res
             for (int e = off[pi] + threadIdx.x; e < off[pi + 1]; e += blockDim.x) {
                 const uint32_t ent = list[e];
                 const int u = (int)(ent & 0x1fff), edge = (int)((ent >> 13) & 3);
-                const uint32_t w = code[u];
-                const double own = unit * (double)((int64_t)from_nb(w & ~mask) - (int64_t)from_nb(w));
-                double pred;
+                const uint32_t w = codes[e];
+                const int64_t full = (int64_t)from_nb(w);
+                const double oa = unit * (double)((int64_t)from_nb(w & ~ma) - full);
+                const double ob = unit * (double)((int64_t)from_nb(w & ~mb) - full);
+                double pa, pb;
                 if (zero_src) {
-                    pred = edge == 0 ? (9.0 * (0.0 + 0.0) - (0.0 + 0.0)) / 16.0 : edge == 1 ? (0.0 + 0.0) / 2.0 : 0.0;
+                    const double z = edge == 0 ? (9.0 * (0.0 + 0.0) - (0.0 + 0.0)) / 16.0 : edge == 1 ? (0.0 + 0.0) / 2.0 : 0.0;
+                    pa = z, pb = z;
                 } else if (edge == 0) {
-                    const double a = dev[u - 3 * stp], b = dev[u - stp], c = dev[u + stp], dd = dev[u + 3 * stp];
-                    pred = (9.0 * (b + c) - (a + dd)) / 16.0;
+                    pa = (9.0 * (dev0[u - stp] + dev0[u + stp]) - (dev0[u - 3 * stp] + dev0[u + 3 * stp])) / 16.0;
+                    pb = (9.0 * (dev1[u - stp] + dev1[u + stp]) - (dev1[u - 3 * stp] + dev1[u + 3 * stp])) / 16.0;
                 } else if (edge == 1) {
-                    pred = (dev[u - stp] + dev[u + stp]) / 2.0;
+                    pa = (dev0[u - stp] + dev0[u + stp]) / 2.0;
+                    pb = (dev1[u - stp] + dev1[u + stp]) / 2.0;
                 } else {
-                    pred = dev[u - stp];
+                    pa = dev0[u - stp];
+                    pb = dev1[u - stp];
                 }
-                const double v = pred + own;
-                dev[u] = v;
+                const double va = pa + oa, vb = pb + ob;
+                dev0[u] = va;
+                dev1[u] = vb;
                 if (ent >> 15) {
-                    const double a = fabs(v);
-                    worst = (worst < a) ? a : worst;
+                    const double xa = fabs(va), xb = fabs(vb);
+                    wa = (wa < xa) ? xa : wa;
+                    wb = (wb < xb) ? xb : wb;
                 }
             }
             __syncthreads();
         }
         for (int o = 16; o > 0; o >>= 1) {
-            const double x = __shfl_down_sync(0xffffffffu, worst, o);
-            worst = (worst < x) ? x : worst;
+            const double xa = __shfl_down_sync(0xffffffffu, wa, o), xb = __shfl_down_sync(0xffffffffu, wb, o);
+            wa = (wa < xa) ? xa : wa;
+            wb = (wb < xb) ? xb : wb;
         }
-        if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = worst;
+        if ((threadIdx.x & 31) == 0) red[0][threadIdx.x >> 5] = wa, red[1][threadIdx.x >> 5] = wb;
         __syncthreads();
-        if (threadIdx.x == 0) {
-            double m = 0.0;
-            for (int i = 0; i < (int)(blockDim.x >> 5); ++i) m = (m < red[i]) ? red[i] : m;
-            if (m > 0.0) atomicMax(&raw[d], (unsigned long long)__double_as_longlong(m));
+        if (threadIdx.x < 2) {
+            double mx = 0.0;
+            for (int i = 0; i < (int)(blockDim.x >> 5); ++i) mx = (mx < red[threadIdx.x][i]) ? red[threadIdx.x][i] : mx;
+            if (mx > 0.0) atomicMax(&raw[threadIdx.x ? db : da], (unsigned long long)__double_as_longlong(mx));
         }
         __syncthreads();
     }
@@ -184,7 +178,7 @@ bool launch_loss_fused(const uint32_t *nb, const Geometry &G, int level, bool cu
     const uint64_t s = uint64_t(1) << (level - 1);
     LossGeom g{};
     g.nd = G.nd;
-    static const int tiles[5][4] = {{0, 0, 0, 0}, {4096, 1, 1, 1}, {32, 128, 1, 1}, {4, 16, 64, 1}, {1, 4, 8, 32}};
+    static const int tiles[5][4] = {{0, 0, 0, 0}, {2048, 1, 1, 1}, {32, 64, 1, 1}, {4, 16, 32, 1}, {1, 4, 8, 16}};
     uint64_t region = 1, ntiles = 1;
     for (int i = 0; i < g.nd; ++i) {
         const uint64_t M = (G.dims[i] + s - 1) / s;
@@ -193,6 +187,7 @@ bool launch_loss_fused(const uint32_t *nb, const Geometry &G, int level, bool cu
         g.T[i] = (int)std::min<uint64_t>(tiles[g.nd][i], M);
         g.H[i] = (i >= 1 && M > 1) ? 3 : 0;
         g.R[i] = g.T[i] + 2 * g.H[i];
+        g.Rm[i] = ((1ull << 32) + (uint64_t)g.R[i] - 1) / (uint64_t)g.R[i];
         g.NT[i] = (int)((M + g.T[i] - 1) / g.T[i]);
         region *= (uint64_t)g.R[i];
         ntiles *= (uint64_t)g.NT[i];
@@ -210,7 +205,7 @@ bool launch_loss_fused(const uint32_t *nb, const Geometry &G, int level, bool cu
         g.pbase[p] = lg.passes[p].ordinal_base;
         for (int i = 0; i < g.nd; ++i) g.pcnt[p][i] = (uint32_t)lg.passes[p].cnt[i];
     }
-    const size_t smem = region * (8 + 4 + 2) + 64;
+    const size_t smem = region * (2 * 8 + 4 + 2) + 64;
     static bool attr = false;
     if (!attr) {
         CK(cudaFuncSetAttribute(k_loss_fused<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
