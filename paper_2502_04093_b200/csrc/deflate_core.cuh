@@ -408,29 +408,40 @@ struct BlockTrees {
     uint64_t body_bits;  // bits after the 3-bit header (stored: 32 + 8*len, alignment not included)
 };
 
+// zlib's heap orders nodes by smaller(n, m) = freq[n] < freq[m] || (freq[n] == freq[m] &&
+// depth[n] <= depth[m]), i.e. (freq, depth) compared lexicographically with ties counting as
+// "smaller".  Heap entries pack freq << 18 | depth << 10 | node so one load gives the whole
+// key (depth is zlib's uch and wraps the same way).  heap[heap_max..] then holds the nodes
+// in zlib's order for gen_bitlen.
 struct TreeScratch {
-    uint16_t freq[HEAP_SIZE];
+    uint16_t freq[HEAP_SIZE];     // leaf frequencies (input; forced leaves set to 1)
     uint16_t dad_len[HEAP_SIZE];  // zlib's dl union: Dad during build, Len after gen_bitlen
-    uint8_t depth[HEAP_SIZE];
-    int16_t heap[HEAP_SIZE];
+    uint64_t heap[HEAP_SIZE];
     uint16_t bl_count[MAX_BITS + 1];
     int heap_len, heap_max;
 };
 
-HD bool tr_smaller(const TreeScratch &t, int n, int m) {
-    return t.freq[n] < t.freq[m] || (t.freq[n] == t.freq[m] && t.depth[n] <= t.depth[m]);
+HD uint64_t hmake(uint64_t freq, uint32_t depth, int node) {
+    return (freq << 18) | ((uint64_t)(depth & 0xff) << 10) | (uint64_t)node;
 }
+HD uint64_t hkey(uint64_t e) { return e >> 10; }
+HD int hnode(uint64_t e) { return (int)(e & 1023); }
+
 HD void pqdownheap(TreeScratch &t, int k) {
-    const int v = t.heap[k];
+    const uint64_t v = t.heap[k];
     int j = k << 1;
     while (j <= t.heap_len) {
-        if (j < t.heap_len && tr_smaller(t, t.heap[j + 1], t.heap[j])) j++;
-        if (tr_smaller(t, v, t.heap[j])) break;
-        t.heap[k] = t.heap[j];
+        uint64_t hj = t.heap[j];
+        if (j < t.heap_len) {
+            const uint64_t hj1 = t.heap[j + 1];
+            if (hkey(hj1) <= hkey(hj)) j++, hj = hj1;
+        }
+        if (hkey(v) <= hkey(hj)) break;
+        t.heap[k] = hj;
         k = j;
         j <<= 1;
     }
-    t.heap[k] = (int16_t)v;
+    t.heap[k] = v;
 }
 
 // build_tree + gen_bitlen + gen_codes (trees.c).  kind: 0 lit/len, 1 dist, 2 bit-length.
@@ -444,17 +455,15 @@ HD int build_tree(TreeScratch &t, int kind, int elems, uint8_t *len_out, uint16_
     t.heap_max = HEAP_SIZE;
     for (int n = 0; n < elems; n++) {
         if (t.freq[n] != 0) {
-            t.heap[++t.heap_len] = (int16_t)(max_code = n);
-            t.depth[n] = 0;
+            t.heap[++t.heap_len] = hmake(t.freq[n], 0, max_code = n);
         } else {
             t.dad_len[n] = 0;
         }
     }
     while (t.heap_len < 2) {
         const int node = max_code < 2 ? ++max_code : 0;
-        t.heap[++t.heap_len] = (int16_t)node;
+        t.heap[++t.heap_len] = hmake(1, 0, node);
         t.freq[node] = 1;
-        t.depth[node] = 0;
         opt_len--;
         if (kind == 0) static_len -= (uint64_t)static_llen(node);
         else if (kind == 1) static_len -= 5;
@@ -462,27 +471,26 @@ HD int build_tree(TreeScratch &t, int kind, int elems, uint8_t *len_out, uint16_
     for (int n = t.heap_len / 2; n >= 1; n--) pqdownheap(t, n);
     int node = elems;
     do {
-        const int n = t.heap[1];  // pqremove
+        const uint64_t en = t.heap[1];  // pqremove
         t.heap[1] = t.heap[t.heap_len--];
         pqdownheap(t, 1);
-        const int m = t.heap[1];
-        t.heap[--t.heap_max] = (int16_t)n;
-        t.heap[--t.heap_max] = (int16_t)m;
-        t.freq[node] = (uint16_t)(t.freq[n] + t.freq[m]);
-        t.depth[node] = (uint8_t)((t.depth[n] >= t.depth[m] ? t.depth[n] : t.depth[m]) + 1);
-        t.dad_len[n] = t.dad_len[m] = (uint16_t)node;
-        t.heap[1] = (int16_t)node++;
+        const uint64_t em = t.heap[1];
+        t.heap[--t.heap_max] = en;
+        t.heap[--t.heap_max] = em;
+        const uint32_t dn = (uint32_t)(en >> 10) & 0xff, dm = (uint32_t)(em >> 10) & 0xff;
+        t.dad_len[hnode(en)] = t.dad_len[hnode(em)] = (uint16_t)node;
+        t.heap[1] = hmake((en >> 18) + (em >> 18), (dn >= dm ? dn : dm) + 1, node++);
         pqdownheap(t, 1);
     } while (t.heap_len >= 2);
     t.heap[--t.heap_max] = t.heap[1];
 
     // gen_bitlen
     for (int b = 0; b <= MAX_BITS; b++) t.bl_count[b] = 0;
-    t.dad_len[t.heap[t.heap_max]] = 0;
+    t.dad_len[hnode(t.heap[t.heap_max])] = 0;
     int overflow = 0;
     int h;
     for (h = t.heap_max + 1; h < HEAP_SIZE; h++) {
-        const int n = t.heap[h];
+        const int n = hnode(t.heap[h]);
         int bits = t.dad_len[t.dad_len[n]] + 1;
         if (bits > max_length) bits = max_length, overflow++;
         t.dad_len[n] = (uint16_t)bits;
@@ -510,7 +518,7 @@ HD int build_tree(TreeScratch &t, int kind, int elems, uint8_t *len_out, uint16_
         for (int bits = max_length; bits != 0; bits--) {
             int n = t.bl_count[bits];
             while (n != 0) {
-                const int m = t.heap[--h];
+                const int m = hnode(t.heap[--h]);
                 if (m > max_code) continue;
                 if ((unsigned)t.dad_len[m] != (unsigned)bits) {
                     opt_len += ((uint64_t)bits - (uint64_t)t.dad_len[m]) * (uint64_t)t.freq[m];
