@@ -213,7 +213,7 @@ __global__ void __launch_bounds__(PL_WARPS * 32) k_prevlinks(const uint8_t *in, 
     uint16_t *prevd = prevd_all + (uint64_t)j * n;
     const uint64_t base = blk == 0 ? 0 : (blk - 1) * WSIZE;
     const uint64_t out0 = blk * WSIZE, end = min(n, (blk + 1) * WSIZE);
-    constexpr int AHEAD = 8;
+    constexpr int AHEAD = 16;
     uint32_t b0[AHEAD], bx[AHEAD];  // byte at q; lanes 0,1: byte at q + 32
     auto fetch = [&](uint64_t pos0) {
 #pragma unroll

@@ -376,13 +376,17 @@ HD int bl_order(int i) {
     const int8_t t[19] = {16, 17, 18, 0, 8, 7, 9, 6, 10, 5, 11, 4, 12, 3, 13, 2, 14, 1, 15};
     return t[i];
 }
-HD uint32_t bi_reverse(uint32_t code, int len) {
+HD uint32_t bi_reverse(uint32_t code, int len) {  // len in 1..15
+#if defined(__CUDA_ARCH__)
+    return __brev(code) >> (32 - len);
+#else
     uint32_t r = 0;
     for (int i = 0; i < len; ++i) {
         r = (r << 1) | (code & 1u);
         code >>= 1;
     }
     return r;
+#endif
 }
 HD int static_llen(int n) { return n < 144 ? 8 : n < 256 ? 9 : n < 280 ? 7 : 8; }
 HD uint32_t static_lcode(int n) {
