@@ -963,6 +963,38 @@ __global__ void __launch_bounds__(128) k_crc_chunks(const uint8_t *const *ptrs, 
     part[(uint64_t)j * ncrc + c] = a < len ? crc_bytes(p + a, e - a, T) : 0u;
 }
 
+// crc32_combine's shift (multiply by x^(8 len) mod P) is linear: table i holds it for
+// len = 2^i applied to each byte lane, so a shift costs 4 lookups per set bit of len
+// (one for the power-of-two lengths the combine tree mostly uses).  Built once per
+// device from crc_multmodp/crc_x8n (deflate_core.cuh, pinned to zlib by the CPU tests).
+constexpr int CRC_SHIFT_BITS = 40;
+__device__ uint32_t g_crc_shift[CRC_SHIFT_BITS * 1024];
+
+__global__ void k_crc_shift_tables() {
+    const int i = blockIdx.x, e = threadIdx.x;  // e: byte lane (e >> 8) and value (e & 255)
+    const uint32_t op = crc_x8n(1ull << i);
+    g_crc_shift[i * 1024 + e] = crc_multmodp(op, (uint32_t)(e & 255) << (8 * (e >> 8)));
+}
+
+__device__ __forceinline__ uint32_t crc_shift(uint32_t c, uint64_t len) {
+    for (int i = 0; len; ++i, len >>= 1) {
+        if (!(len & 1)) continue;
+        const uint32_t *T = g_crc_shift + i * 1024;
+        c = T[c & 0xff] ^ T[256 + ((c >> 8) & 0xff)] ^ T[512 + ((c >> 16) & 0xff)] ^ T[768 + (c >> 24)];
+    }
+    return c;
+}
+
+void ensure_crc_shift_tables(cudaStream_t st) {
+    static bool done[64] = {false};
+    int dev = 0;
+    CK(cudaGetDevice(&dev));
+    if (dev < 64 && done[dev]) return;
+    k_crc_shift_tables<<<CRC_SHIFT_BITS, 1024, 0, st>>>();
+    CKL();
+    if (dev < 64) done[dev] = true;
+}
+
 __global__ void __launch_bounds__(1024) k_crc_combine(const uint64_t *lens, uint64_t ncrc, uint32_t *part,
                                                      uint32_t *out) {
     const int j = blockIdx.x;
@@ -976,7 +1008,7 @@ __global__ void __launch_bounds__(1024) k_crc_combine(const uint64_t *lens, uint
             const uint64_t l = q * 2 * stride, r = l + stride;
             if (r < nc) {
                 const uint64_t rend = min(len, (r + stride) * (uint64_t)CRC_CHUNK);
-                pp[l] = crc_combine(pp[l], pp[r], rend - r * (uint64_t)CRC_CHUNK);
+                pp[l] = crc_shift(pp[l], rend - r * (uint64_t)CRC_CHUNK) ^ pp[r];
             }
         }
         __syncthreads();
@@ -1020,6 +1052,7 @@ void crc32_batch(const uint8_t *const *ptrs, const uint64_t *lens, int S, uint64
     uint32_t *part = tab + 8 * 256;
     k_crc_table<<<1, 256, 0, st>>>(tab);
     CKL();
+    ensure_crc_shift_tables(st);
     k_crc_chunks<<<dim3((unsigned)((ncrc + 127) / 128), S), 128, 0, st>>>(ptrs, lens, tab, ncrc, part);
     CKL();
     k_crc_combine<<<S, 1024, 0, st>>>(lens, ncrc, part, out);
@@ -1122,6 +1155,7 @@ void DeflateBatch::run(const uint8_t *in, uint64_t in_stride, int S, uint64_t n,
     ProfScope ps6("deflate.crc", st, (uint64_t)S * n);
     k_crc_table<<<1, 256, 0, st>>>(w.crc_tab);
     CKL();
+    ensure_crc_shift_tables(st);
     k_crc_chunks<<<dim3((unsigned)((w.ncrc + 127) / 128), S), 128, 0, st>>>(res.payload, res.length, w.crc_tab, w.ncrc, w.crc_part);
     CKL();
     k_crc_combine<<<S, 1024, 0, st>>>(res.length, w.ncrc, w.crc_part, res.crc);

@@ -274,3 +274,49 @@ extern "C" uint64_t zmodel_match_check(const uint8_t *in, uint64_t n) {
         bad += match_search(p, (int64_t)n, bytes, prevfn) != match_search32((uint32_t)p, (uint32_t)n, words, prevfn);
     return bad;
 }
+
+// dev statistics: parse steps (positions whose match record the lazy parse reads) and the
+// match_step work spent on them vs on all positions
+extern "C" void zmodel_parse_visits(const uint8_t *in, uint64_t n, uint64_t *out3) {
+    struct HB {
+        const uint8_t *in;
+        uint32_t operator()(int64_t i) const { return in[i]; }
+        int64_t match_len(int64_t a, int64_t b, int64_t maxlen) const {
+            int64_t len = 0;
+            while (len < maxlen && in[a + len] == in[b + len]) ++len;
+            return len;
+        }
+    } bytes{in};
+    std::vector<uint16_t> prevd(n + 1, 0);
+    std::vector<int64_t> head(1 << 15, -1);
+    for (int64_t p = 0; p + MIN_MATCH <= (int64_t)n; ++p) {
+        const uint32_t h = hash3(in[p], in[p + 1], in[p + 2]);
+        const int64_t q = head[h];
+        prevd[p] = (q >= 0 && p - q < WSIZE) ? (uint16_t)(p - q) : 0;
+        head[h] = p;
+    }
+    auto prevfn = [&](int64_t i) -> uint32_t { return prevd[i]; };
+    std::vector<uint64_t> rec(n + 1, 0), steps(n + 1, 0);
+    for (int64_t p = 0; p < (int64_t)n; ++p) {
+        MatchState s;
+        match_init(s, p, (int64_t)n, bytes, prevfn);
+        uint64_t k = 0;
+        while (!s.done) match_step(s, bytes, prevfn), ++k;
+        steps[p] = k;
+        rec[p] = match_result(s);
+    }
+    uint64_t visits = 0, vsteps = 0, allsteps = 0;
+    for (int64_t p = 0; p < (int64_t)n; ++p) allsteps += steps[p];
+    int64_t p = 0;
+    int tag = TAG_A;
+    while (p < (int64_t)n) {
+        ++visits;
+        vsteps += steps[p];
+        const Step s = parse_step(p, tag, (int64_t)n, rec[p], p > 0 ? rec[p - 1] : 0, bytes);
+        p = s.next_p;
+        tag = s.next_tag;
+    }
+    out3[0] = visits;
+    out3[1] = vsteps;
+    out3[2] = allsteps;
+}
