@@ -699,7 +699,12 @@ void retrieve_impl(ipcg_ctx *c, ipcg_archive *a, int scalar, const int *k, void 
         out_buf = DBuf(n * w, st);
         state = out_buf.p;
     }
-    if (refine) {
+    // refine_field starts from `previous` and replays the progressive levels (pipeline.hpp:
+    // 310-349); the replay rewrites every point of those levels, so `previous` only
+    // contributes the points of non-progressive levels: copy it only if there are any.
+    bool keeps_previous = false;
+    for (int l = 0; l < L; ++l) keeps_previous |= !lv[l].active;
+    if (refine && keeps_previous) {
         CK(cudaMemcpyAsync(state, previous, n * w, prev_on_dev ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, st));
     }
     ipcg_session *ns = new ipcg_session;
