@@ -222,6 +222,44 @@ __device__ void huff_build(Huff &h, const uint8_t *lens, int n, unsigned lane) {
     __syncwarp();
 }
 
+// the same for a group of G lanes (gl = lane within the group); every lane of the warp
+// calls it (inactive groups pass active = false) so the warp-wide syncs line up
+__device__ void huff_build_group(Huff &h, const uint8_t *lens, int n, unsigned gl, unsigned G, bool active) {
+    if (active && gl == 0) {
+        for (int i = 0; i < 16; ++i) h.count[i] = 0;
+        for (int i = 0; i < n; ++i) h.count[lens[i]]++;
+        h.count[0] = 0;
+        h.offs[1] = 0;
+        for (int l = 1; l < 15; ++l) h.offs[l + 1] = (uint16_t)(h.offs[l] + h.count[l]);
+        uint16_t code = 0;
+        for (int l = 1; l <= 15; ++l) {
+            code = (uint16_t)((code + h.count[l - 1]) << 1);
+            h.first[l] = code;
+        }
+        uint16_t o[16];
+        for (int l = 0; l < 16; ++l) o[l] = h.offs[l];
+        for (int i = 0; i < n; ++i)
+            if (lens[i]) h.sym[o[lens[i]]++] = (uint16_t)i;
+    }
+    __syncwarp();
+    if (active)
+        for (int i = gl; i < (1 << FASTBITS); i += G) h.fast[i] = 0;
+    __syncwarp();
+    if (active) {
+        int total = 0;
+        for (int l = 1; l <= 15; ++l) total += h.count[l];
+        for (int t = gl; t < total; t += G) {
+            int L = 1;
+            while (L < 15 && !(t >= h.offs[L] && t < h.offs[L] + h.count[L])) ++L;
+            if (L > FASTBITS) continue;
+            const uint32_t code = h.first[L] + (uint32_t)(t - h.offs[L]);
+            const uint32_t rev = __brev(code) >> (32 - L);
+            for (uint32_t e = 0; e < (1u << (FASTBITS - L)); ++e) h.fast[rev | (e << L)] = (uint16_t)((L << 12) | h.sym[t]);
+        }
+    }
+    __syncwarp();
+}
+
 __device__ __forceinline__ int huff_decode(const Huff &h, Bits &b) {
     const uint32_t e = h.fast[b.peek(FASTBITS)];
     if (e) {
@@ -497,31 +535,45 @@ __global__ void __launch_bounds__(256) k_scan(const InflateJob *jobs, const Tabl
 }
 
 // ------------------------------------------------------------ 2. candidates
-__global__ void __launch_bounds__(WARPS * 32) k_decode_cands(const InflateJob *jobs, const Tables *tabs, Cand *cands,
+// CPW candidates per warp, one per group of 32/CPW lanes: the decode is inherently
+// sequential per block and every lane of a group does the same work, so packing several
+// blocks into a warp divides the (issue-bound) warp-instruction count.
+constexpr int DWARPS = 4;  // warps per k_decode_cands CTA (static smem: DWARPS * CPW table slots)
+
+template <int CPW>
+__global__ void __launch_bounds__(DWARPS * 32) k_decode_cands(const InflateJob *jobs, const Tables *tabs, Cand *cands,
                                                            const unsigned long long *ncand_total, uint64_t cand_cap,
                                                            uint32_t *pool, uint32_t *ckpt_pool) {
-    __shared__ Huff lit_s[WARPS], dist_s[WARPS];
-    __shared__ uint8_t lens_s[WARPS][320];
+    constexpr unsigned G = 32 / CPW;
+    __shared__ Huff lit_s[DWARPS * CPW], dist_s[DWARPS * CPW];
+    __shared__ uint8_t lens_s[DWARPS * CPW][320];
     const unsigned w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const unsigned sub = lane / G, gl = lane % G, slot = w * CPW + sub;
     const uint64_t n = min((unsigned long long)cand_cap, *ncand_total);
-    for (uint64_t ci = blockIdx.x * (uint64_t)WARPS + w; ci < n; ci += (uint64_t)gridDim.x * WARPS) {
-        Cand &c = cands[ci];
-        const InflateJob job = jobs[c.job];
+    for (uint64_t bw = blockIdx.x * (uint64_t)DWARPS + w; bw * CPW < n; bw += (uint64_t)gridDim.x * DWARPS) {
+        const uint64_t ci = bw * CPW + sub;
+        bool act = ci < n;
+        Cand dummy;
+        Cand &c = act ? cands[ci] : dummy;
+        const InflateJob job = jobs[act ? c.job : 0];
         Bits b;
-        b.init(job.src, job.src_len, c.hdr_bit + 3);
         int nlen = 0, ndist = 0;
         uint8_t lens[320];
-        Canon cs;
-        const bool ok = read_dynamic_header(b, lens, nlen, ndist, cs);  // identical on every lane
-        if (!ok) {
-            if (lane == 0) c.ok = 0;
-            continue;
+        if (act) {
+            b.init(job.src, job.src_len, c.hdr_bit + 3);
+            Canon cs;
+            const bool ok = read_dynamic_header(b, lens, nlen, ndist, cs);  // identical on the group's lanes
+            if (!ok) {
+                if (gl == 0) c.ok = 0;
+                act = false;
+            }
         }
-        if (lane == 0)
-            for (int i = 0; i < nlen + ndist; ++i) lens_s[w][i] = lens[i];
+        if (act && gl == 0)
+            for (int i = 0; i < nlen + ndist; ++i) lens_s[slot][i] = lens[i];
         __syncwarp();
-        huff_build(lit_s[w], lens_s[w], nlen, lane);
-        huff_build(dist_s[w], lens_s[w] + nlen, ndist, lane);
+        huff_build_group(lit_s[slot], lens_s[slot], nlen, gl, G, act);
+        huff_build_group(dist_s[slot], lens_s[slot] + nlen, ndist, gl, G, act);
+        if (act) {  // (no early exits: every lane reaches the syncs below)
         uint32_t *out = pool + ci * (uint64_t)MAXSYM;
         uint32_t ns = 0, nz = 0;
         uint64_t bytes = 0;
@@ -530,7 +582,7 @@ __global__ void __launch_bounds__(WARPS * 32) k_decode_cands(const InflateJob *j
         wb.init(job.src, job.src_len, b.used);
         for (;;) {
             wb.refill();  // >= 33 bits: a literal/length code and its extra bits
-            const int sym = huff_decode_w(lit_s[w], wb);
+            const int sym = huff_decode_w(lit_s[slot], wb);
             if (sym < 0) {
                 good = false;
                 break;
@@ -541,14 +593,14 @@ __global__ void __launch_bounds__(WARPS * 32) k_decode_cands(const InflateJob *j
                 break;
             }
             if (ns % SEG == 0) {
-                if (lane == 0) ckpt_pool[ci * NCKPT + ns / SEG] = (uint32_t)bytes;
+                if (gl == 0) ckpt_pool[ci * NCKPT + ns / SEG] = (uint32_t)bytes;
                 if (wb.overrun()) {
                     good = false;
                     break;
                 }
             }
             if (sym < 256) {
-                if (lane == 0) out[ns] = sym_lit((uint32_t)sym);
+                if (gl == 0) out[ns] = sym_lit((uint32_t)sym);
                 nz |= (uint32_t)sym;
                 ++ns;
                 ++bytes;
@@ -561,19 +613,19 @@ __global__ void __launch_bounds__(WARPS * 32) k_decode_cands(const InflateJob *j
             }
             const uint32_t len = kLBase[li] + wb.take(kLExt[li]);
             wb.refill();  // >= 33 bits: a distance code and its extra bits
-            const int ds = huff_decode_w(dist_s[w], wb);
+            const int ds = huff_decode_w(dist_s[slot], wb);
             if (ds < 0 || ds >= 30) {
                 good = false;
                 break;
             }
             const uint32_t d = kDBase[ds] + wb.take(kDExt[ds]);
-            if (lane == 0) out[ns] = sym_match(len, d);
+            if (gl == 0) out[ns] = sym_match(len, d);
             ++ns;
             bytes += len;
         }
         if (wb.overrun()) good = false;
         b.used = wb.pos - (uint64_t)(reinterpret_cast<uintptr_t>(job.src) & 3) * 8;
-        if (lane == 0) {
+        if (gl == 0) {
             c.ok = good ? 1 : 0;
             c.nzlit = nz != 0;
             c.end_bit = b.used;
@@ -593,6 +645,7 @@ __global__ void __launch_bounds__(WARPS * 32) k_decode_cands(const InflateJob *j
                 }
             }
             c.next = nx;
+        }
         }
         __syncwarp();
     }
@@ -1116,8 +1169,9 @@ void inflate_batch_host(const std::vector<InflateJob> &jobs, int *status_dev, De
     {
         ProfScope ps("inflate.decode", st, total_src);
         if (nc) {
-            const unsigned g = (unsigned)std::min<uint64_t>((nc + WARPS - 1) / WARPS, 148ull * 16);
-            k_decode_cands<<<g, WARPS * 32, 0, st>>>(jd, td, cands, ncand, cand_cap, pool, ckpt);
+            constexpr int CPW = 1;  // measured: 2 or 4 per warp diverge (literal vs match paths) and lose
+            const unsigned g = (unsigned)std::min<uint64_t>((nc + DWARPS * CPW - 1) / (DWARPS * CPW), 148ull * 32);
+            k_decode_cands<CPW><<<g, DWARPS * 32, 0, st>>>(jd, td, cands, ncand, cand_cap, pool, ckpt);
             CKL();
         }
         k_chain<<<(n + 31) / 32, 32, 0, st>>>(jd, n, td, md, cands);
