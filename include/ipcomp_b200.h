@@ -54,10 +54,15 @@ typedef struct {
 } ipcg_index;
 
 /* context ---------------------------------------------------------------- */
+/* A context is used by one host thread at a time.  Its device scratch, archive payloads
+ * and session codewords come from a grow-only pool it owns: destroy archives and sessions
+ * before their context. */
 int ipcg_ctx_create(int device, ipcg_ctx **out);
 void ipcg_ctx_destroy(ipcg_ctx *ctx);
 const char *ipcg_last_error(const ipcg_ctx *ctx);
-/* CUDA stream all work of this context is ordered on (cudaStream_t, may be 0) */
+/* CUDA stream all work of this context is ordered on (cudaStream_t; NULL restores the
+ * context's own stream).  Device buffers of archives and sessions are allocated and freed
+ * stream-ordered on the stream current when they were created, which must outlive them. */
 int ipcg_set_stream(ipcg_ctx *ctx, void *cuda_stream);
 int ipcg_synchronize(ipcg_ctx *ctx);
 

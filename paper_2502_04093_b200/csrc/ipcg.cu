@@ -2,14 +2,15 @@
 //
 //   compress_field   (pipeline.hpp:140-223): range scan -> per level L..1: one
 //                    predict+quantize launch per (level, axis) pass -> loss-table replay
-//                    -> ballot bitplanes + XOR -> DeflateBatch (32 planes) -> one sync ->
+//                    -> transpose bitplanes + XOR -> DeflateBatch (32 planes) -> one sync ->
 //                    host index (archive.cpp:31-65) -> device payload gather.
 //   reconstruct_field (pipeline.hpp:227-287) / refine_field (:294-352): host plans the
 //                    block reads (partial-bitplane fetch, byte accounting), device gathers
 //                    the blocks, CRC-32 + inflate, XOR-decode+merge, per-pass reconstruction
 //                    with in-traversal outlier overwrite.
-// All device work of a call is ordered on the context's stream; temporaries come from
-// the stream-ordered allocator (cudaMallocAsync), whose pool keeps memory across calls.
+// All device work of a call is ordered on the context's stream; temporaries, archive
+// payloads and session codewords come from the context's grow-only ScratchPool
+// (util.cuh), so steady-state calls allocate nothing.
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -17,6 +18,10 @@
 #include <cstring>
 #include <string>
 #include <vector>
+
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
 
 #include "../../include/ipcomp_b200.h"
 #include "deflate.cuh"
@@ -34,6 +39,7 @@ struct ipcg_ctx {
     std::vector<cudaStream_t> side;  // fork targets (per-level chains)
     std::vector<cudaEvent_t> events;
     size_t events_used = 0;
+    ScratchPool scratch;  // per-call device scratch, reused across calls (also archive/session memory)
     std::string err;
     void *pinned = nullptr;
     size_t pinned_cap = 0;
@@ -45,6 +51,8 @@ struct ipcg_archive {
     uint64_t size = 0;
     bool on_device = false;
     uint8_t *owned = nullptr;  // device buffer when produced by ipcg_compress
+    cudaStream_t owner = nullptr;  // stream `owned` was allocated on (reused there, stream-ordered)
+    ScratchPool *pool = nullptr;   // the creating context's pool `owned` returns to
     uint64_t payload_read = 0;
     int device = 0;
 };
@@ -55,6 +63,9 @@ struct ipcg_session {
     int k[IPCG_MAX_LEVELS] = {0};
     uint64_t count[IPCG_MAX_LEVELS] = {0};
     uint32_t *merged[IPCG_MAX_LEVELS] = {nullptr};  // device, progressive levels only
+    cudaStream_t owner = nullptr;                     // stream the merged arrays are released on
+    ScratchPool *pool = nullptr;                      // and the pool they return to
+    int device = 0;
 };
 
 namespace {
@@ -65,7 +76,7 @@ struct DBuf {  // stream-ordered device allocation
     cudaStream_t st = nullptr;
     DBuf() = default;
     DBuf(size_t bytes, cudaStream_t s) : st(s) {
-        if (bytes) CK(cudaMallocAsync(&p, bytes, s));
+        if (bytes) p = scratch_get(bytes, s);
     }
     DBuf(const DBuf &) = delete;
     DBuf &operator=(const DBuf &) = delete;
@@ -79,7 +90,7 @@ struct DBuf {  // stream-ordered device allocation
     }
     ~DBuf() { release(); }
     void release() {
-        if (p) cudaFreeAsync(p, st);
+        scratch_put(p, st);
         p = nullptr;
     }
     template <class T>
@@ -125,6 +136,11 @@ thread_local std::string g_host_err;  // errors of context-free (host-only) call
 template <class F>
 int guarded(ipcg_ctx *c, F &&f) {
     std::string &err = c ? c->err : g_host_err;
+    struct Bind {  // this call's scratch pool
+        ScratchPool *prev;
+        explicit Bind(ipcg_ctx *c) : prev(current_scratch()) { current_scratch() = c ? &c->scratch : nullptr; }
+        ~Bind() { current_scratch() = prev; }
+    } bind(c);
     try {
         if (c) CK(cudaSetDevice(c->device));
         f();
@@ -194,8 +210,28 @@ void gather(ipcg_ctx *c, std::vector<CopyDesc> descs, uint8_t *dst) {
 }
 
 // ---------------------------------------------------------------- compress
+// host-side phase timer (IPCG_DEBUG_TIMING=1): where a call's wall time goes
+struct PhaseTimer {
+    bool on = getenv("IPCG_DEBUG_TIMING") != nullptr;
+    std::chrono::steady_clock::time_point t0 = std::chrono::steady_clock::now(), last = t0;
+    std::string line;
+    void mark(const char *what) {
+        if (!on) return;
+        const auto now = std::chrono::steady_clock::now();
+        char buf[64];
+        snprintf(buf, sizeof(buf), " %s %.2f", what, std::chrono::duration<double, std::milli>(now - last).count());
+        line += buf;
+        last = now;
+    }
+    ~PhaseTimer() {
+        if (on) fprintf(stderr, "[ipcg timing]%s total %.2f ms\n", line.c_str(),
+                        std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count());
+    }
+};
+
 ipcg_archive *compress_impl(ipcg_ctx *c, int scalar, const void *values, int on_dev, const uint64_t *dims, int nd,
                             double eb, int interp, int lp_opt, uint64_t cap) {
+    PhaseTimer tm;
     validate_dims(dims, nd);
     if (scalar != 0 && scalar != 1) throw Error(EINVAL_, "field scalars must be f32 or f64");
     if (!(eb > 0.0) || !std::isfinite(eb)) throw Error(EINVAL_, "error bound must be positive and finite");
@@ -233,6 +269,7 @@ ipcg_archive *compress_impl(ipcg_ctx *c, int scalar, const void *values, int on_
         double range_part[2 * 1024];
     };
     DBuf small(sizeof(Small), st);
+    tm.mark("setup");
     Small *sd = small.as<Small>();
     CK(cudaMemsetAsync(small.p, 0, sizeof(Small), st));
     DBuf ord(n * 8, st), bits(n * 8, st);
@@ -265,12 +302,14 @@ ipcg_archive *compress_impl(ipcg_ctx *c, int scalar, const void *values, int on_
         out_stride[li] = round_up(pb[li] + 16, 16);
         planes[li] = DBuf(32 * plane_stride[li] * 4, st);
         outs[li] = DBuf(32 * out_stride[li], st);
+        tm.mark("alloc_l");
         const OutlierSink sink{&sd->ocount[li], ord.as<uint64_t>() + sink_base[li], bits.as<uint64_t>() + sink_base[li]};
         {
             ProfScope ps("quant_pass", st, lg.count * (uint64_t)(2 * w + 4) + lg.count * (uint64_t)w);
             for (const PassDesc &pd : lg.passes)
                 launch_quant_pass(vals, state.p, scalar, cubic, pd, eb, nb.as<uint32_t>(), &sd->lowor[li], sink, st);
         }
+        tm.mark("quant");
         // loss table (measure_loss_table): replay per dropped-digit count d
         {
             ProfScope psl("loss_table", st, lg.count * 4);
@@ -283,7 +322,9 @@ ipcg_archive *compress_impl(ipcg_ctx *c, int scalar, const void *values, int on_
             }
             launch_loss_finalize(sd->raw[li], &sd->lowor[li], sd->delta[li], st);
         }
-        if (planes[li].p) CK(cudaMemsetAsync(planes[li].p, 0, 32 * plane_stride[li] * 4, st));
+        tm.mark("loss");
+        // (no memset: k_bitplanes writes every word below the row length, zero past `count`;
+        // the deflate stage never reads a row past its n = ceil(count/8) bytes)
         {
             ProfScope ps("bitplanes", st, lg.count * 8);
             launch_bitplanes(nb.as<uint32_t>(), lg.count, planes[li].as<uint32_t>(), plane_stride[li], st);
@@ -291,12 +332,15 @@ ipcg_archive *compress_impl(ipcg_ctx *c, int scalar, const void *values, int on_
         const BackendResults res{sd->backend[li], sd->length[li], sd->crc[li], sd->payload[li]};
         DeflateBatch::run(planes[li].as<uint8_t>(), plane_stride[li] * 4, 32, pb[li], outs[li].as<uint8_t>(),
                           out_stride[li], ws.p, res, st);
+        tm.mark("deflate");
     }
     Small *sh = static_cast<Small *>(pinned(c, sizeof(Small)));
+    tm.mark("enqueue");
     CK(cudaMemcpyAsync(sh, small.p, sizeof(Small), cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
     Small hs;
     std::memcpy(&hs, sh, sizeof(Small));
+    tm.mark("gpu_wait");
 
     // index (pipeline.hpp:158-217 + archive.cpp:31-65)
     ipcg_index ix{};
@@ -331,14 +375,19 @@ ipcg_archive *compress_impl(ipcg_ctx *c, int scalar, const void *values, int on_
     ix.index_bytes = index.size();
     ix.identity = crc32_host(index.data(), index.size());
     const uint64_t total = index.size() + cursor;
+    tm.mark("index");
 
     ipcg_archive *a = new ipcg_archive;
     a->device = c->device;
-    CK(cudaMalloc(&a->owned, std::max<uint64_t>(total, 1)));
+    // stream-ordered: a cudaMalloc/cudaFree pair per call would synchronize the device
+    a->owned = static_cast<uint8_t *>(c->scratch.get(std::max<uint64_t>(total, 1), st));
+    a->owner = st;
+    a->pool = &c->scratch;
     a->bytes = a->owned;
     a->size = total;
     a->on_device = true;
     a->ix = ix;
+    tm.mark("alloc");
     // index + block headers staged in one pinned blob, payloads copied device-to-device
     std::vector<uint8_t> blob(index.begin(), index.end());
     std::vector<CopyDesc> descs;
@@ -379,6 +428,7 @@ ipcg_archive *compress_impl(ipcg_ctx *c, int scalar, const void *values, int on_
     }
     CK(cudaStreamSynchronize(st));  // pinned blob consumed before reuse
     gather(c, all, a->owned);
+    tm.mark("gather");
     // outlier blocks, sorted by ordinal (pipeline.hpp:185-188)
     uint64_t maxo = 0;
     for (int l = 0; l < L; ++l) maxo = std::max<uint64_t>(maxo, hs.ocount[l]);
@@ -395,6 +445,7 @@ ipcg_archive *compress_impl(ipcg_ctx *c, int scalar, const void *values, int on_
         }
     }
     CK(cudaStreamSynchronize(st));
+    tm.mark("outliers");
     return a;
 }
 
@@ -711,6 +762,9 @@ void retrieve_impl(ipcg_ctx *c, ipcg_archive *a, int scalar, const int *k, void 
     ns->archive_crc = ix.identity;
     ns->levels = L;
     ns->lp = ix.progressive_levels;
+    ns->owner = st;
+    ns->pool = &c->scratch;
+    ns->device = c->device;
     DBuf napplied(8 * IPCG_MAX_LEVELS, st);
     try {
         for (int level = L; level >= 1; --level) {
@@ -724,7 +778,7 @@ void retrieve_impl(ipcg_ctx *c, ipcg_archive *a, int scalar, const int *k, void 
             }
             const uint64_t count = ix.records[li].count;
             uint32_t *merged = nullptr;
-            CK(cudaMallocAsync((void **)&merged, std::max<uint64_t>(count, 1) * 4, st));
+            merged = static_cast<uint32_t *>(scratch_get(std::max<uint64_t>(count, 1) * 4, st));
             const uint32_t *min = refine ? prev_sess->merged[li] : nullptr;
             {
                 ProfScope ps("merge", st, count * 4 + (uint64_t)(p.p1 - p.p0) * ((count + 7) / 8));
@@ -741,13 +795,13 @@ void retrieve_impl(ipcg_ctx *c, ipcg_archive *a, int scalar, const int *k, void 
                 }
             }
             if (level <= ix.progressive_levels) ns->merged[li] = merged;
-            else CK(cudaFreeAsync(merged, st));
+            else scratch_put(merged, st);
         }
         if (!out_on_dev) CK(cudaMemcpyAsync(out, state, n * w, cudaMemcpyDeviceToHost, st));
         CK(cudaStreamSynchronize(st));
     } catch (...) {
         for (int l = 0; l < IPCG_MAX_LEVELS; ++l)
-            if (ns->merged[l]) cudaFree(ns->merged[l]);
+            if (ns->merged[l]) scratch_put(ns->merged[l], st);
         delete ns;
         throw;
     }
@@ -755,7 +809,7 @@ void retrieve_impl(ipcg_ctx *c, ipcg_archive *a, int scalar, const int *k, void 
     if (sess_out) *sess_out = ns;
     else {
         for (int l = 0; l < IPCG_MAX_LEVELS; ++l)
-            if (ns->merged[l]) cudaFreeAsync(ns->merged[l], st);
+            if (ns->merged[l]) scratch_put(ns->merged[l], st);
         delete ns;
     }
 }
@@ -794,6 +848,8 @@ void ipcg_ctx_destroy(ipcg_ctx *c) {
     cudaSetDevice(c->device);
     if (c->stream) cudaStreamSynchronize(c->stream);
     for (cudaStream_t s : c->side) cudaStreamSynchronize(s);
+    c->scratch.release_all(c->own_stream);
+    if (c->own_stream) cudaStreamSynchronize(c->own_stream);
     if (c->pinned) cudaFreeHost(c->pinned);
     for (cudaStream_t s : c->side) cudaStreamDestroy(s);
     for (cudaEvent_t e : c->events) cudaEventDestroy(e);
@@ -867,7 +923,8 @@ void ipcg_archive_free(ipcg_archive *a) {
     if (!a) return;
     if (a->owned) {
         cudaSetDevice(a->device);
-        cudaFree(a->owned);
+        if (a->pool) a->pool->put(a->owned);  // reused stream-ordered by the context's next calls
+        else cudaFreeAsync(a->owned, a->owner);
     }
     delete a;
 }
@@ -894,13 +951,17 @@ int ipcg_session_create(ipcg_ctx *c, const ipcg_archive *a, const int *planes_lo
         s->archive_crc = a->ix.identity;
         s->levels = a->ix.levels;
         s->lp = a->ix.progressive_levels;
+        s->owner = c->stream;
+        s->pool = &c->scratch;
+        s->device = c->device;
         for (int l = 0; l < s->levels; ++l) {
             s->k[l] = planes_loaded[l];
             s->count[l] = a->ix.records[l].count;
             if (l + 1 <= s->lp && merged && merged[l]) {
                 const uint64_t cnt = s->count[l];
-                CK(cudaMalloc((void **)&s->merged[l], std::max<uint64_t>(cnt, 1) * 4));
-                CK(cudaMemcpy(s->merged[l], merged[l], cnt * 4, cudaMemcpyHostToDevice));
+                s->merged[l] = static_cast<uint32_t *>(c->scratch.get(std::max<uint64_t>(cnt, 1) * 4, c->stream));
+                CK(cudaMemcpyAsync(s->merged[l], merged[l], cnt * 4, cudaMemcpyHostToDevice, c->stream));
+                CK(cudaStreamSynchronize(c->stream));
             }
         }
         *out = s;
@@ -930,8 +991,12 @@ int ipcg_session_merged(ipcg_ctx *c, const ipcg_session *s, int level, uint32_t 
 }
 void ipcg_session_free(ipcg_session *s) {
     if (!s) return;
+    cudaSetDevice(s->device);
     for (int l = 0; l < IPCG_MAX_LEVELS; ++l)
-        if (s->merged[l]) cudaFree(s->merged[l]);
+        if (s->merged[l]) {
+            if (s->pool) s->pool->put(s->merged[l]);
+            else cudaFreeAsync(s->merged[l], s->owner);
+        }
     delete s;
 }
 

@@ -161,6 +161,23 @@ __global__ void __launch_bounds__(kBlock) k_quant_pass(const T *__restrict__ val
 // into one 32-bit word of plane p (bit i = codeword i, i.e. byte i/8 bit i%8 when
 // stored little-endian), the 2-plane XOR runs on those words, and a shared-memory
 // transpose makes every plane's store a 128-byte coalesced row.
+// 32x32 bit-matrix transpose across a warp: lane r holds row r (bit c = column c) on
+// entry and column r (bit c = row c) on return.  Five block-swap stages.
+__device__ __forceinline__ uint32_t warp_transpose32(uint32_t x, unsigned lane) {
+    const uint32_t masks[5] = {0x0000FFFFu, 0x00FF00FFu, 0x0F0F0F0Fu, 0x33333333u, 0x55555555u};
+#pragma unroll
+    for (int s = 0; s < 5; ++s) {
+        const int j = 16 >> s;
+        const uint32_t m = masks[s];  // columns c with (c & j) == 0
+        const uint32_t y = __shfl_xor_sync(0xffffffffu, x, j);
+        x = (lane & j) ? ((x & ~m) | ((y & ~m) >> j)) : ((x & m) | ((y & m) << j));
+    }
+    return x;
+}
+
+// bitplane.cpp:7-22 split + 44-49 xor: a warp transposes its 32 codewords (lane l: codeword
+// l -> lane 31-p: plane p's word, bit l = codeword l's digit), XORs each plane word with the
+// two planes above it (lanes +1, +2), and the CTA writes the 32 planes x 32 words tile.
 __global__ void __launch_bounds__(1024) k_bitplanes(const uint32_t *__restrict__ nb, uint64_t count,
                                                     uint32_t *__restrict__ planes, uint64_t stride) {
     __shared__ uint32_t tile[32][33];
@@ -168,16 +185,10 @@ __global__ void __launch_bounds__(1024) k_bitplanes(const uint32_t *__restrict__
     const uint64_t word0 = (uint64_t)blockIdx.x * 32;
     const uint64_t i = (word0 + warp) * 32 + lane;
     const uint32_t v = i < count ? nb[i] : 0u;
-    uint32_t prev1 = 0, prev2 = 0, mine = 0;
-#pragma unroll
-    for (int p = 0; p < 32; ++p) {
-        const uint32_t b = __ballot_sync(0xffffffffu, (v >> (31 - p)) & 1u);
-        const uint32_t e = b ^ prev1 ^ prev2;
-        prev2 = prev1;
-        prev1 = b;
-        if ((int)lane == p) mine = e;
-    }
-    tile[lane][warp] = mine;  // tile[plane][word]
+    const uint32_t b = warp_transpose32(v, lane);  // plane 31 - lane
+    const uint32_t b1 = __shfl_down_sync(0xffffffffu, b, 1), b2 = __shfl_down_sync(0xffffffffu, b, 2);
+    const uint32_t e = b ^ (lane < 31 ? b1 : 0u) ^ (lane < 30 ? b2 : 0u);
+    tile[31 - lane][warp] = e;  // tile[plane][word]
     __syncthreads();
     const unsigned p = threadIdx.x >> 5, w = threadIdx.x & 31;
     const uint64_t words = (count + 31) / 32;
@@ -270,20 +281,6 @@ __global__ void k_outlier_block(const uint64_t *ord, const uint64_t *bits, const
 // prefix taken from already-merged codewords (pipeline.hpp:328-339).  A CTA takes 32
 // plane words x 32 planes: warp p loads plane p's 128-byte row segment (coalesced) into
 // a padded smem tile, then warp w owns word w with lane p holding plane p's bits.
-// 32x32 bit-matrix transpose across a warp: lane r holds row r (bit c = column c) on
-// entry and column r (bit c = row c) on return.  Five block-swap stages.
-__device__ __forceinline__ uint32_t warp_transpose32(uint32_t x, unsigned lane) {
-    const uint32_t masks[5] = {0x0000FFFFu, 0x00FF00FFu, 0x0F0F0F0Fu, 0x33333333u, 0x55555555u};
-#pragma unroll
-    for (int s = 0; s < 5; ++s) {
-        const int j = 16 >> s;
-        const uint32_t m = masks[s];  // columns c with (c & j) == 0
-        const uint32_t y = __shfl_xor_sync(0xffffffffu, x, j);
-        x = (lane & j) ? ((x & ~m) | ((y & ~m) >> j)) : ((x & m) | ((y & m) << j));
-    }
-    return x;
-}
-
 // Solves b_p = e_p ^ b_{p-1} ^ b_{p-2} down a codeword (plane p at bit 31-p): over GF(2)
 // B = E / (1 + S + S^2) = (1 + S) E / (1 + S^3), S = shift toward the LSB, i.e. F = E ^ (E >> 1)
 // followed by a stride-3 prefix XOR.

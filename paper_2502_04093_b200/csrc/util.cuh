@@ -3,7 +3,9 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <map>
 #include <stdexcept>
+#include <unordered_map>
 #include <string>
 #include <vector>
 
@@ -79,19 +81,66 @@ struct ProfScope {
     }
 };
 
-// stream-ordered temporaries released together (cudaMallocAsync pool keeps the memory)
+// Grow-only device scratch owned by a context.  Blocks are handed out best-fit (within
+// 25% + 1 MiB of the request) and go back to the pool, not to CUDA: every user enqueues on
+// the context's stream, so a block returned by one call is reused, stream-ordered, by the
+// next.  (cudaMallocAsync of multi-GB buffers per call was measured blocking the host for
+// up to 200 ms whenever the CUDA pool had to map memory again, leaving the GPU idle.)
+struct ScratchPool {
+    std::multimap<size_t, void *> free_;
+    std::unordered_map<void *, size_t> size_;
+    void *get(size_t bytes, cudaStream_t st) {
+        bytes = (bytes + 255) & ~size_t(255);
+        if (bytes == 0) bytes = 256;
+        auto it = free_.lower_bound(bytes);
+        if (it != free_.end() && it->first <= bytes + bytes / 4 + (size_t(1) << 20)) {
+            void *p = it->second;
+            free_.erase(it);
+            return p;
+        }
+        void *p = nullptr;
+        CK(cudaMallocAsync(&p, bytes, st));
+        size_[p] = bytes;
+        return p;
+    }
+    void put(void *p) {
+        if (p) free_.emplace(size_.at(p), p);
+    }
+    void release_all(cudaStream_t st) {  // caller has synchronized
+        for (auto &kv : size_) cudaFreeAsync(kv.first, st);
+        free_.clear();
+        size_.clear();
+    }
+};
+// the pool of the context whose API call is running on this thread (set by the C-ABI entry)
+inline ScratchPool *&current_scratch() {
+    thread_local ScratchPool *p = nullptr;
+    return p;
+}
+inline void *scratch_get(size_t bytes, cudaStream_t st) {
+    if (ScratchPool *sp = current_scratch()) return sp->get(bytes, st);
+    void *p = nullptr;
+    CK(cudaMallocAsync(&p, bytes ? bytes : 1, st));
+    return p;
+}
+inline void scratch_put(void *p, cudaStream_t st) {
+    if (!p) return;
+    if (ScratchPool *sp = current_scratch()) sp->put(p);
+    else cudaFreeAsync(p, st);
+}
+
+// stream-ordered temporaries released together
 struct DevAlloc {
     std::vector<void *> ptrs;
     cudaStream_t st = nullptr;
     void *get(size_t bytes, cudaStream_t s) {
-        void *p = nullptr;
-        CK(cudaMallocAsync(&p, bytes ? bytes : 1, s));
+        void *p = scratch_get(bytes, s);
         ptrs.push_back(p);
         st = s;
         return p;
     }
     ~DevAlloc() {
-        for (void *p : ptrs) cudaFreeAsync(p, st);
+        for (void *p : ptrs) scratch_put(p, st);
     }
 };
 
