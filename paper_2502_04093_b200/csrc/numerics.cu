@@ -294,31 +294,82 @@ __device__ __forceinline__ uint32_t xor_decode_word(uint32_t e) {
 }
 
 // bitplane.cpp:24-59 (xor decode + merge) for planes [k0, k1) of one level on top of the
-// codewords already merged from planes [0, k0).  A warp owns 32 consecutive codewords:
-// the 32 plane words are staged through shared memory, transposed with shuffles, and the
-// XOR recurrence is solved inside each codeword.
-__global__ void __launch_bounds__(1024) k_merge(const uint32_t *const *__restrict__ rows,
-                                                const uint32_t *__restrict__ merged_in,
-                                                uint32_t *__restrict__ merged_out, uint64_t count, int k0, int k1) {
-    __shared__ uint32_t tile[32][33];
-    const unsigned warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const uint64_t words = (count + 31) / 32;
-    const uint32_t pre = k0 == 0 ? 0u : ~0u << (32 - k0);            // planes < k0
+// codewords already merged from planes [0, k0).  Each warp works alone on 32 plane words
+// (1024 codewords): lane p loads plane p's 32 words with four 16-byte loads (rows are
+// 16-byte aligned and padded to a multiple of 4 words), then for each word the warp
+// transposes the 32x32 bit block (lane c: codeword c's plane bits), solves the XOR recurrence
+// inside the codeword and stores 32 codewords coalesced.  No shared memory, no block syncs.
+__global__ void __launch_bounds__(256) k_merge(const uint32_t *const *__restrict__ rows,
+                                               const uint32_t *__restrict__ merged_in,
+                                               uint32_t *__restrict__ merged_out, uint64_t count, int k0, int k1) {
+    const unsigned lane = threadIdx.x & 31;
+    const uint64_t words = (count + 31) / 32, words4 = (words + 3) & ~3ull;
+    const uint32_t pre = k0 == 0 ? 0u : ~0u << (32 - k0);                    // planes < k0
     const uint32_t keep = k1 == 0 ? 0u : k1 >= 32 ? ~0u : ~0u << (32 - k1);  // planes < k1
-    for (uint64_t w0 = (uint64_t)blockIdx.x * 32; w0 < words; w0 += (uint64_t)gridDim.x * 32) {
-        tile[warp][lane] = ((int)warp >= k0 && (int)warp < k1 && w0 + lane < words) ? __ldg(rows[warp] + w0 + lane) : 0u;
-        __syncthreads();
-        const uint64_t w = w0 + warp;
-        const uint64_t i = w * 32 + lane;
-        // lane p: plane p's word for these 32 codewords -> lane c: codeword c's plane bits
-        const uint32_t e_new = __brev(warp_transpose32(tile[lane][warp], lane));
-        uint32_t e = e_new;
-        if (merged_in && k0 > 0 && i < count) {
-            const uint32_t m = merged_in[i] & pre;
-            e |= (m ^ (m >> 1) ^ (m >> 2)) & pre;
+    const uint32_t *row = ((int)lane >= k0 && (int)lane < k1) ? rows[lane] : nullptr;
+    const bool with_prefix = merged_in && k0 > 0;
+    const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+    for (uint64_t w0 = (((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5) * 32; w0 < words; w0 += nwarps * 32) {
+        uint32_t v[32];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+            uint4 q = make_uint4(0u, 0u, 0u, 0u);
+            if (row && w0 + 4 * k < words4) q = __ldg(reinterpret_cast<const uint4 *>(row + w0) + k);
+            v[4 * k] = q.x, v[4 * k + 1] = q.y, v[4 * k + 2] = q.z, v[4 * k + 3] = q.w;
         }
-        if (w < words && i < count) merged_out[i] = xor_decode_word(e) & keep;
-        __syncthreads();
+#pragma unroll
+        for (int wv = 0; wv < 32; ++wv) {
+            const uint64_t w = w0 + wv;
+            if (w >= words) break;  // warp-uniform
+            const uint64_t i = w * 32 + lane;
+            uint32_t e = __brev(warp_transpose32(v[wv], lane));
+            if (with_prefix && i < count) {
+                const uint32_t m = merged_in[i] & pre;
+                e |= (m ^ (m >> 1) ^ (m >> 2)) & pre;
+            }
+            if (i < count) merged_out[i] = xor_decode_word(e) & keep;
+        }
+    }
+}
+
+// Refinement step adding few planes (k1 - k0 <= 8) on top of merged codewords: no transpose;
+// for each word lane c takes bit c of every new plane word (a broadcast load), ORs in the
+// prefix's XOR-encoded digits and solves the recurrence.  One coalesced codeword load and
+// store per word; 4 words per warp iteration for memory-level parallelism.
+__global__ void __launch_bounds__(256) k_merge_few(const uint32_t *const *__restrict__ rows,
+                                                   const uint32_t *__restrict__ merged_in,
+                                                   uint32_t *__restrict__ merged_out, uint64_t count, int k0, int k1) {
+    const unsigned lane = threadIdx.x & 31;
+    const uint64_t words = (count + 31) / 32;
+    const uint32_t pre = k0 == 0 ? 0u : ~0u << (32 - k0);
+    const uint32_t keep = k1 >= 32 ? ~0u : ~0u << (32 - k1);
+    const int np = k1 - k0;
+    const uint32_t *r[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) r[q] = q < np ? rows[k0 + q] : nullptr;
+    const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+    for (uint64_t w0 = (((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5) * 4; w0 < words; w0 += nwarps * 4) {
+        uint32_t m[4], e[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const uint64_t i = (w0 + u) * 32 + lane;
+            m[u] = i < count ? __ldg(merged_in + i) & pre : 0u;
+            e[u] = (m[u] ^ (m[u] >> 1) ^ (m[u] >> 2)) & pre;
+        }
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+            if (q >= np) break;
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const uint32_t x = w0 + u < words ? __ldg(r[q] + w0 + u) : 0u;
+                e[u] |= ((x >> lane) & 1u) << (31 - (k0 + q));
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const uint64_t i = (w0 + u) * 32 + lane;
+            if (i < count) merged_out[i] = xor_decode_word(e[u]) & keep;
+        }
     }
 }
 
@@ -459,8 +510,13 @@ void launch_merge(const uint32_t *const *rows, const uint32_t *merged_in, uint32
                   int k1, cudaStream_t st) {
     const uint64_t words = (count + 31) / 32;
     if (words == 0) return;
-    const unsigned g = (unsigned)std::min<uint64_t>((words + 31) / 32, 148ull * 2 * 8);
-    k_merge<<<g, 1024, 0, st>>>(rows, merged_in, merged_out, count, k0, k1);
+    if (merged_in && k0 > 0 && k1 - k0 <= 8) {
+        const unsigned g = (unsigned)std::min<uint64_t>(((words + 3) / 4 + 7) / 8, 148ull * 16);
+        k_merge_few<<<g, 256, 0, st>>>(rows, merged_in, merged_out, count, k0, k1);
+    } else {
+        const unsigned g = (unsigned)std::min<uint64_t>(((words + 31) / 32 + 7) / 8, 148ull * 8);
+        k_merge<<<g, 256, 0, st>>>(rows, merged_in, merged_out, count, k0, k1);
+    }
     CKL();
 }
 
