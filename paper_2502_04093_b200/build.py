@@ -23,6 +23,7 @@ INCLUDE = os.path.join(os.path.dirname(HERE), "include")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVFLAGS = ["-std=c++17", *ARCH, "-O3", "-lineinfo", "-fmad=false", "-prec-div=true", "-prec-sqrt=true",
            "-ftz=false", "--extended-lambda", "-Xcompiler", "-fPIC,-ffp-contract=off", f"-I{INCLUDE}"]
+PER_FILE: dict = {}  # per-file extra nvcc flags
 
 
 def _newest_dep() -> float:
@@ -34,7 +35,7 @@ def _compile(src: str, force: bool) -> str:
     obj = os.path.join(BUILD, os.path.basename(src) + ".o")
     if not force and os.path.exists(obj) and os.path.getmtime(obj) >= _newest_dep():
         return obj
-    cmd = ["nvcc", *NVFLAGS, "-c", src, "-o", obj]
+    cmd = ["nvcc", *NVFLAGS, *PER_FILE.get(os.path.basename(src), []), "-c", src, "-o", obj]
     if src.endswith(".cpp"):
         cmd = ["nvcc", *NVFLAGS, "-x", "cu", "-c", src, "-o", obj]
     r = subprocess.run(cmd, capture_output=True, text=True)

@@ -10,8 +10,11 @@
 // every level point is counted in exactly one box.  max|v| per d is folded with an
 // atomicMax on the IEEE bits of a non-negative double (exact, order-free).
 #include <algorithm>
+#include <cstdio>
+#include <type_traits>
 
 #include "numerics.cuh"
+#include "tiles.cuh"
 
 namespace ipcg {
 
@@ -19,20 +22,7 @@ namespace {
 
 constexpr int LT_THREADS = 256;
 
-struct LossGeom {
-    int nd, npass;
-    int M[4];      // lattice extents ceil(dims/s)
-    int T[4];      // box extents
-    int H[4];      // halo (0 or 3)
-    int R[4];      // staged region extents T + 2H
-    int NT[4];     // boxes per axis
-    int S[4];      // row-major strides of the staged region
-    uint64_t Rm[4];  // ceil(2^32 / R[i]): x / R[i] == (x * Rm[i]) >> 32 for x, R[i] < 2^16
-    int region;
-    int paxis[4];
-    uint64_t pbase[4];
-    uint32_t pcnt[4][4];
-};
+
 
 __device__ __forceinline__ int32_t from_nb(uint32_t w) { return (int32_t)((w ^ kNbMask) - kNbMask); }
 
@@ -42,7 +32,7 @@ __device__ __forceinline__ int32_t from_nb(uint32_t w) { return (int32_t)((w ^ k
 // point's codeword; (2) replay the valid d (a contiguous range) two at a time, one
 // deviation array each, so list/code/address work and barriers are shared by the pair.
 template <bool Cubic>
-__global__ void __launch_bounds__(LT_THREADS) k_loss_fused(const uint32_t *__restrict__ nb, LossGeom g, double unit,
+__global__ void __launch_bounds__(LT_THREADS) k_loss_fused(const uint32_t *__restrict__ nb, TileGeom g, double unit,
                                                           const uint32_t *lowor, unsigned long long *raw) {
     extern __shared__ __align__(16) unsigned char smem[];
     const uint32_t lo = *lowor;
@@ -169,42 +159,15 @@ __global__ void __launch_bounds__(LT_THREADS) k_loss_fused(const uint32_t *__res
     }
 }
 
+
 }  // namespace
 
 bool launch_loss_fused(const uint32_t *nb, const Geometry &G, int level, bool cubic, double unit,
                        const uint32_t *lowor, unsigned long long *raw, cudaStream_t st) {
-    const LevelGeom &lg = G.level[level - 1];
-    if (level == G.levels || lg.passes.empty()) return false;
-    const uint64_t s = uint64_t(1) << (level - 1);
-    LossGeom g{};
-    g.nd = G.nd;
     static const int tiles[5][4] = {{0, 0, 0, 0}, {2048, 1, 1, 1}, {32, 64, 1, 1}, {4, 16, 32, 1}, {1, 4, 8, 16}};
-    uint64_t region = 1, ntiles = 1;
-    for (int i = 0; i < g.nd; ++i) {
-        const uint64_t M = (G.dims[i] + s - 1) / s;
-        if (M > (1u << 30)) return false;
-        g.M[i] = (int)M;
-        g.T[i] = (int)std::min<uint64_t>(tiles[g.nd][i], M);
-        g.H[i] = (i >= 1 && M > 1) ? 3 : 0;
-        g.R[i] = g.T[i] + 2 * g.H[i];
-        g.Rm[i] = ((1ull << 32) + (uint64_t)g.R[i] - 1) / (uint64_t)g.R[i];
-        g.NT[i] = (int)((M + g.T[i] - 1) / g.T[i]);
-        region *= (uint64_t)g.R[i];
-        ntiles *= (uint64_t)g.NT[i];
-    }
-    if (region >= 8192 || ntiles > 0x7fffffff) return false;  // 13-bit list entries
-    g.region = (int)region;
-    int acc = 1;
-    for (int i = g.nd - 1; i >= 0; --i) {
-        g.S[i] = acc;
-        acc *= g.R[i];
-    }
-    g.npass = (int)lg.passes.size();
-    for (int p = 0; p < g.npass; ++p) {
-        g.paxis[p] = lg.passes[p].axis;
-        g.pbase[p] = lg.passes[p].ordinal_base;
-        for (int i = 0; i < g.nd; ++i) g.pcnt[p][i] = (uint32_t)lg.passes[p].cnt[i];
-    }
+    TileGeom g;
+    uint64_t ntiles, region;
+    if (!tile_geom(G, level, tiles, g, ntiles, region)) return false;
     const size_t smem = region * (2 * 8 + 4 + 2) + 64;
     static bool attr = false;
     if (!attr) {
