@@ -15,7 +15,6 @@ struct PassDesc {
     int nd;
     int axis;                  // -1 for the coarsest level (predicts 0)
     uint64_t cnt[kMaxDims];    // box extent per axis
-    uint64_t rcp[kMaxDims];    // ceil(2^64 / cnt) (0 for cnt <= 1): i / cnt == umulhi64(i, rcp) for i < 2^32
     uint64_t step_flat[kMaxDims];
     uint64_t start_flat;
     uint64_t axis_start, axis_step;  // coordinate along `axis`: axis_start + idx[axis]*axis_step
@@ -82,7 +81,6 @@ inline Geometry make_geometry(const uint64_t *dims, int nd, int max_levels) {
             p.start_flat = 0;
             for (int i = 0; i < nd; ++i) {
                 p.cnt[i] = lattice_count(dims[i], start[i], step[i]);
-                p.rcp[i] = p.cnt[i] > 1 ? ~uint64_t(0) / p.cnt[i] + 1 : 0;
                 p.size *= p.cnt[i];
                 p.step_flat[i] = step[i] * g.strides[i];
                 p.start_flat += start[i] * g.strides[i];

@@ -19,8 +19,7 @@ __device__ __forceinline__ uint64_t pass_flat(const PassDesc &p, uint64_t i, uin
         uint32_t r32 = (uint32_t)i;
         for (int d = p.nd - 1; d >= 0; --d) {
             const uint32_t c = (uint32_t)p.cnt[d];
-            const uint32_t q = c > 1 ? (uint32_t)__umul64hi((uint64_t)r32, p.rcp[d]) : r32;
-            const uint32_t r = r32 - q * c;
+            const uint32_t q = r32 / c, r = r32 - q * c;  // (a 64-bit reciprocal multiply measured slower)
             r32 = q;
             flat += (uint64_t)r * p.step_flat[d];
             if (d == p.axis) axis_idx = r;
