@@ -1060,7 +1060,7 @@ void crc32_batch(const uint8_t *const *ptrs, const uint64_t *lens, int S, uint64
 }
 
 void DeflateBatch::run(const uint8_t *in, uint64_t in_stride, int S, uint64_t n, uint8_t *out, uint64_t out_stride,
-                       void *workspace, BackendResults res, cudaStream_t st) {
+                       void *workspace, BackendResults res, cudaStream_t st, cudaEvent_t after_match) {
     if ((in_stride & 15) || (reinterpret_cast<uintptr_t>(in) & 15))
         throw Error(EINVAL_, "deflate input rows must be 16-byte aligned with a 16-byte multiple stride");
     Work w = carve(workspace, S, n);
@@ -1096,6 +1096,7 @@ void DeflateBatch::run(const uint8_t *in, uint64_t in_stride, int S, uint64_t n,
             k_match<true><<<dim3(grid_for(n, 256, 4096), S), 256, 0, st>>>(in, in_stride, n, w.meta, w.prevd, w.rec);
         CKL();
         }
+        if (after_match) CK(cudaEventRecord(after_match, st));
         {
         ProfScope ps3("deflate.anchor", st, (uint64_t)S * n * 8);
         k_anchor<<<dim3((unsigned)((n + TILE - 1) / TILE), S), 256, 0, st>>>(n, w.meta, w.rec, w.nchunks, w.first_anchor);

@@ -21,8 +21,10 @@ struct BackendResults {
 struct DeflateBatch {
     static constexpr int CH = 256;  // nominal parse chunk (boundaries snap to anchors)
     static size_t workspace_bytes(int S, uint64_t n);
+    // after_match (optional): recorded on `st` once the match search is enqueued, so a caller
+    // can start other work when the throughput-bound phases are over
     static void run(const uint8_t *in, uint64_t in_stride, int S, uint64_t n, uint8_t *out, uint64_t out_stride,
-                    void *workspace, BackendResults res, cudaStream_t st);
+                    void *workspace, BackendResults res, cudaStream_t st, cudaEvent_t after_match = nullptr);
 };
 
 // standalone CRC-32 (zlib polynomial) of S (ptr, len) device ranges

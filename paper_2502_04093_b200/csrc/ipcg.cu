@@ -99,24 +99,33 @@ struct DBuf {  // stream-ordered device allocation
     }
 };
 
+// side stream i: 0 carries work off the critical path (lowest priority), the others the
+// critical chains (highest priority), so the scheduler fills the gaps of the latter with it
 cudaStream_t side_stream(ipcg_ctx *c, size_t i) {
     while (c->side.size() <= i) {
+        int least = 0, greatest = 0;
+        CK(cudaDeviceGetStreamPriorityRange(&least, &greatest));
         cudaStream_t s;
-        CK(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+        CK(cudaStreamCreateWithPriority(&s, cudaStreamNonBlocking, c->side.empty() ? greatest : least));
         c->side.push_back(s);
     }
     return c->side[i];
 }
 
-// `to` waits for everything enqueued on `from` so far (events are reused across calls:
-// a wait captures the event's state at enqueue time)
-void stream_dep(ipcg_ctx *c, cudaStream_t from, cudaStream_t to) {
+// an event from the context's pool (reused across calls: a wait captures the event's
+// state at enqueue time)
+cudaEvent_t pool_event(ipcg_ctx *c) {
     if (c->events_used == c->events.size()) {
         cudaEvent_t e;
         CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
         c->events.push_back(e);
     }
-    cudaEvent_t e = c->events[c->events_used++];
+    return c->events[c->events_used++];
+}
+
+// `to` waits for everything enqueued on `from` so far
+void stream_dep(ipcg_ctx *c, cudaStream_t from, cudaStream_t to) {
+    cudaEvent_t e = pool_event(c);
     CK(cudaEventRecord(e, from));
     CK(cudaStreamWaitEvent(to, e, 0));
 }
@@ -281,14 +290,15 @@ ipcg_archive *compress_impl(ipcg_ctx *c, int scalar, const void *values, int on_
     // (Forking each level's lossless stage and the loss tables onto side streams was
     // measured: no gain -- level 1's kernels saturate the GPU, so overlap only hides the
     // small levels' latency tails, and those are a few ms.)
-    uint64_t maxcount = 0;
-    size_t ws_bytes = 0;
-    for (int l = 1; l <= L; ++l) {
-        maxcount = std::max(maxcount, G.level[l - 1].count);
-        ws_bytes = std::max(ws_bytes, DeflateBatch::workspace_bytes(32, (G.level[l - 1].count + 7) / 8));
-    }
-    DBuf nb(std::max<uint64_t>(maxcount, 1) * 4, st), ws(ws_bytes, st);
-    std::vector<DBuf> planes(L), outs(L);
+    // Only quantization is sequential across levels (level l predicts from the state the
+    // coarser levels left).  Each level's lossless stage (bitplanes + deflate) forks onto its
+    // own side stream and the loss tables onto one shared side stream (the per-pass fallback
+    // shares `dev`): the small levels' latency-bound chains (zlib's serial Huffman builds,
+    // single-CTA scans) then run under level 1's throughput-bound kernels.  Everything joins
+    // back into `st` before the results are read.
+    c->events_used = 0;
+    cudaStream_t loss_st = side_stream(c, 0);
+    std::vector<DBuf> nbs(L), wss(L), planes(L), outs(L);
     std::vector<uint64_t> pb(L), plane_stride(L), out_stride(L), sink_base(L);
     uint64_t base = 0;
     for (int level = L; level >= 1; --level) {
@@ -300,40 +310,51 @@ ipcg_archive *compress_impl(ipcg_ctx *c, int scalar, const void *values, int on_
         const uint64_t words = (lg.count + 31) / 32;
         plane_stride[li] = round_up(std::max<uint64_t>(words, 1), 4);  // words, 16-byte rows
         out_stride[li] = round_up(pb[li] + 16, 16);
+        nbs[li] = DBuf(std::max<uint64_t>(lg.count, 1) * 4, st);
+        wss[li] = DBuf(DeflateBatch::workspace_bytes(32, pb[li]), st);
         planes[li] = DBuf(32 * plane_stride[li] * 4, st);
         outs[li] = DBuf(32 * out_stride[li], st);
         tm.mark("alloc_l");
+        uint32_t *nb = nbs[li].as<uint32_t>();
         const OutlierSink sink{&sd->ocount[li], ord.as<uint64_t>() + sink_base[li], bits.as<uint64_t>() + sink_base[li]};
         {
             ProfScope ps("quant_pass", st, lg.count * (uint64_t)(2 * w + 4) + lg.count * (uint64_t)w);
             for (const PassDesc &pd : lg.passes)
-                launch_quant_pass(vals, state.p, scalar, cubic, pd, eb, nb.as<uint32_t>(), &sd->lowor[li], sink, st);
+                launch_quant_pass(vals, state.p, scalar, cubic, pd, eb, nb, &sd->lowor[li], sink, st);
         }
         tm.mark("quant");
-        // loss table (measure_loss_table): replay per dropped-digit count d
+        // lossless stage.  (No memset: k_bitplanes writes every word below the row length, zero
+        // past `count`; the deflate stage never reads a row past its n = ceil(count/8) bytes.)
+        cudaStream_t ds = side_stream(c, 1 + (size_t)li);
+        stream_dep(c, st, ds);
         {
-            ProfScope psl("loss_table", st, lg.count * 4);
-            if (!launch_loss_fused(nb.as<uint32_t>(), G, level, cubic, 2.0 * eb, &sd->lowor[li], sd->raw[li], st)) {
-                for (int d = 1; d <= 32; ++d)
-                    for (const PassDesc &pd : lg.passes)
-                        launch_loss_pass(nb.as<uint32_t>(), dev.as<double>(), pd, cubic, 2.0 * eb, d, &sd->lowor[li],
-                                         sd->raw[li], st);
-                for (const PassDesc &pd : lg.passes) launch_zero_pass(dev.as<double>(), pd, st);
-            }
-            launch_loss_finalize(sd->raw[li], &sd->lowor[li], sd->delta[li], st);
+            ProfScope ps("bitplanes", ds, lg.count * 8);
+            launch_bitplanes(nb, lg.count, planes[li].as<uint32_t>(), plane_stride[li], ds);
         }
-        tm.mark("loss");
-        // (no memset: k_bitplanes writes every word below the row length, zero past `count`;
-        // the deflate stage never reads a row past its n = ceil(count/8) bytes)
-        {
-            ProfScope ps("bitplanes", st, lg.count * 8);
-            launch_bitplanes(nb.as<uint32_t>(), lg.count, planes[li].as<uint32_t>(), plane_stride[li], st);
-        }
+        cudaEvent_t after_match = pool_event(c);
         const BackendResults res{sd->backend[li], sd->length[li], sd->crc[li], sd->payload[li]};
         DeflateBatch::run(planes[li].as<uint8_t>(), plane_stride[li] * 4, 32, pb[li], outs[li].as<uint8_t>(),
-                          out_stride[li], ws.p, res, st);
+                          out_stride[li], wss[li].p, res, ds, after_match);
+        // loss table (measure_loss_table): replay per dropped-digit count d, started once this
+        // level's match search is done so it overlaps the latency-bound parse/Huffman phases
+        // instead of competing with the throughput-bound ones (measured: 53 vs 60 ms)
+        stream_dep(c, st, loss_st);
+        CK(cudaStreamWaitEvent(loss_st, after_match, 0));
+        {
+            ProfScope psl("loss_table", loss_st, lg.count * 4);
+            if (!launch_loss_fused(nb, G, level, cubic, 2.0 * eb, &sd->lowor[li], sd->raw[li], loss_st)) {
+                for (int d = 1; d <= 32; ++d)
+                    for (const PassDesc &pd : lg.passes)
+                        launch_loss_pass(nb, dev.as<double>(), pd, cubic, 2.0 * eb, d, &sd->lowor[li], sd->raw[li],
+                                         loss_st);
+                for (const PassDesc &pd : lg.passes) launch_zero_pass(dev.as<double>(), pd, loss_st);
+            }
+            launch_loss_finalize(sd->raw[li], &sd->lowor[li], sd->delta[li], loss_st);
+        }
         tm.mark("deflate");
     }
+    stream_dep(c, loss_st, st);
+    for (int li = 0; li < L; ++li) stream_dep(c, side_stream(c, 1 + (size_t)li), st);
     Small *sh = static_cast<Small *>(pinned(c, sizeof(Small)));
     tm.mark("enqueue");
     CK(cudaMemcpyAsync(sh, small.p, sizeof(Small), cudaMemcpyDeviceToHost, st));

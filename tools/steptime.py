@@ -12,7 +12,7 @@ st = torch.cuda.current_stream()
 ctx.set_stream(st.cuda_stream)
 ft = torch.from_numpy(f).cuda()
 rels = c["retrieve"]["rel"]
-for it in range(6):
+for it in range(int(sys.argv[1]) if len(sys.argv) > 1 else 6):
     torch.cuda.synchronize()
     t = [time.perf_counter()]
     r = ipc.compress_field(ft, c["dims"], eb, c["interp"], ctx=ctx); t.append(time.perf_counter())
