@@ -296,8 +296,12 @@ ipcg_archive *compress_impl(ipcg_ctx *c, int scalar, const void *values, int on_
     // shares `dev`): the small levels' latency-bound chains (zlib's serial Huffman builds,
     // single-CTA scans) then run under level 1's throughput-bound kernels.  Everything joins
     // back into `st` before the results are read.
+    // With the per-family profiler on (bench.py's roofline step, never the timed loop) all
+    // of it stays on `st`, so each family's CUDA-event span covers only its own kernels.
     c->events_used = 0;
-    cudaStream_t loss_st = side_stream(c, 0);
+    const bool serial = profiler().enabled;
+    auto fork = [&](size_t i) { return serial ? st : side_stream(c, i); };
+    cudaStream_t loss_st = fork(0);
     std::vector<DBuf> nbs(L), wss(L), planes(L), outs(L);
     std::vector<uint64_t> pb(L), plane_stride(L), out_stride(L), sink_base(L);
     uint64_t base = 0;
@@ -325,8 +329,8 @@ ipcg_archive *compress_impl(ipcg_ctx *c, int scalar, const void *values, int on_
         tm.mark("quant");
         // lossless stage.  (No memset: k_bitplanes writes every word below the row length, zero
         // past `count`; the deflate stage never reads a row past its n = ceil(count/8) bytes.)
-        cudaStream_t ds = side_stream(c, 1 + (size_t)li);
-        stream_dep(c, st, ds);
+        cudaStream_t ds = fork(1 + (size_t)li);
+        if (ds != st) stream_dep(c, st, ds);
         {
             ProfScope ps("bitplanes", ds, lg.count * 8);
             launch_bitplanes(nb, lg.count, planes[li].as<uint32_t>(), plane_stride[li], ds);
@@ -338,8 +342,10 @@ ipcg_archive *compress_impl(ipcg_ctx *c, int scalar, const void *values, int on_
         // loss table (measure_loss_table): replay per dropped-digit count d, started once this
         // level's match search is done so it overlaps the latency-bound parse/Huffman phases
         // instead of competing with the throughput-bound ones (measured: 53 vs 60 ms)
-        stream_dep(c, st, loss_st);
-        CK(cudaStreamWaitEvent(loss_st, after_match, 0));
+        if (loss_st != st) {
+            stream_dep(c, st, loss_st);
+            CK(cudaStreamWaitEvent(loss_st, after_match, 0));
+        }
         {
             ProfScope psl("loss_table", loss_st, lg.count * 4);
             if (!launch_loss_fused(nb, G, level, cubic, 2.0 * eb, &sd->lowor[li], sd->raw[li], loss_st)) {
@@ -353,8 +359,10 @@ ipcg_archive *compress_impl(ipcg_ctx *c, int scalar, const void *values, int on_
         }
         tm.mark("deflate");
     }
-    stream_dep(c, loss_st, st);
-    for (int li = 0; li < L; ++li) stream_dep(c, side_stream(c, 1 + (size_t)li), st);
+    if (!serial) {
+        stream_dep(c, loss_st, st);
+        for (int li = 0; li < L; ++li) stream_dep(c, side_stream(c, 1 + (size_t)li), st);
+    }
     Small *sh = static_cast<Small *>(pinned(c, sizeof(Small)));
     tm.mark("enqueue");
     CK(cudaMemcpyAsync(sh, small.p, sizeof(Small), cudaMemcpyDeviceToHost, st));
