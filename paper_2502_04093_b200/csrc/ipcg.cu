@@ -187,16 +187,23 @@ __global__ void k_gather(const CopyDesc *d, int nd, uint8_t *dst) {
     const CopyDesc c = d[i];
     uint8_t *o = dst + c.dst_off;
     const uint8_t *s = c.src;
-    // 16-byte vector path when both ends align, else bytes (coalesced per warp)
-    if ((((uintptr_t)o | (uintptr_t)s) & 15) == 0) {
-        const uint64_t v = c.len / 16;
-        const uint4 *s4 = reinterpret_cast<const uint4 *>(s);
-        uint4 *o4 = reinterpret_cast<uint4 *>(o);
-        for (uint64_t k = threadIdx.x; k < v; k += blockDim.x) o4[k] = s4[k];
-        for (uint64_t k = v * 16 + threadIdx.x; k < c.len; k += blockDim.x) o[k] = s[k];
+    uint64_t len = c.len;
+    // bytes until the destination is 4-byte aligned, then aligned 32-bit stores whose source
+    // words are funnel-shifted from aligned loads (archive payloads start at arbitrary bytes),
+    // then the tail bytes
+    const uint64_t head = min(len, (uint64_t)((4 - ((uintptr_t)o & 3)) & 3));
+    if (threadIdx.x < head) o[threadIdx.x] = s[threadIdx.x];
+    o += head, s += head, len -= head;
+    const uint64_t nw = len / 4;
+    const unsigned sh = (unsigned)((uintptr_t)s & 3) * 8;
+    const uint32_t *sw = reinterpret_cast<const uint32_t *>((uintptr_t)s & ~uintptr_t(3));
+    uint32_t *ow = reinterpret_cast<uint32_t *>(o);
+    if (sh == 0) {
+        for (uint64_t k = threadIdx.x; k < nw; k += blockDim.x) ow[k] = sw[k];
     } else {
-        for (uint64_t k = threadIdx.x; k < c.len; k += blockDim.x) o[k] = s[k];
+        for (uint64_t k = threadIdx.x; k < nw; k += blockDim.x) ow[k] = __funnelshift_r(sw[k], sw[k + 1], sh);
     }
+    for (uint64_t k = nw * 4 + threadIdx.x; k < len; k += blockDim.x) o[k] = s[k];
 }
 
 // dst == nullptr: dst_off are absolute device addresses
@@ -204,7 +211,7 @@ void gather(ipcg_ctx *c, std::vector<CopyDesc> descs, uint8_t *dst) {
     // split long copies so every SM participates
     std::vector<CopyDesc> pieces;
     pieces.reserve(descs.size());
-    const uint64_t piece = 1 << 20;
+    const uint64_t piece = 256 << 10;
     for (const CopyDesc &d : descs)
         for (uint64_t o = 0; o < d.len; o += piece)
             pieces.push_back(CopyDesc{d.src + o, d.dst_off + o, std::min(piece, d.len - o)});
@@ -509,6 +516,7 @@ __global__ void k_copy_headers(const uint8_t *src, const uint64_t *offs, int n, 
 void retrieve_impl(ipcg_ctx *c, ipcg_archive *a, int scalar, const int *k, void *out, int out_on_dev,
                    const ipcg_session *prev_sess, const void *previous, int prev_on_dev, ipcg_session **sess_out,
                    uint64_t *loaded) {
+    PhaseTimer tm;
     const ipcg_index &ix = a->ix;
     if (ix.scalar != scalar) throw Error(EINVAL_, "scalar kind does not match archive");
     validate_plan(ix, k);
@@ -618,6 +626,7 @@ void retrieve_impl(ipcg_ctx *c, ipcg_archive *a, int scalar, const int *k, void 
         src_dev = stage.as<uint8_t>();
     }
     a->payload_read += read;
+    tm.mark("stage");
     // ---- block headers (read_block + load_plane checks, backend.cpp:75-86, archive.cpp:183-191)
     {
         size_t si = 0, ri = 0;
@@ -707,11 +716,13 @@ void retrieve_impl(ipcg_ctx *c, ipcg_archive *a, int scalar, const int *k, void 
         CK(cudaStreamSynchronize(st));
         for (size_t i = 0; i < R; ++i)
             if (hcrc[i] != refs[i].crc) throw Error(ERUNTIME, "block checksum mismatch");
+    tm.mark("crc");
         for (size_t i = 0; i < R; ++i) {
             const uint64_t pbytes = (ix.records[refs[i].level - 1].count + 7) / 8;
             if (refs[i].backend == 0 && refs[i].plen != pbytes) throw Error(ERUNTIME, "identity block has wrong length");
         }
         if (!copies.empty()) gather(c, copies, nullptr);
+    tm.mark("copies");
         // identical deflate payloads (typically the all-zero high planes) decode once:
         // same (length, crc, plane size) and byte-equal on the device -> alias the row
         std::vector<int> rep_of(jobs.size(), -1);
@@ -745,6 +756,7 @@ void retrieve_impl(ipcg_ctx *c, ipcg_archive *a, int scalar, const int *k, void 
             }
         }
         std::vector<InflateJob> todo;
+    tm.mark("dedupe");
         for (size_t a = 0; a < jobs.size(); ++a)
             if (rep_of[a] < 0) todo.push_back(jobs[a]);
             else rows[job_level[a]][job_plane[a]] = rows[job_level[rep_of[a]]][job_plane[rep_of[a]]];
@@ -763,6 +775,7 @@ void retrieve_impl(ipcg_ctx *c, ipcg_archive *a, int scalar, const int *k, void 
             for (int s : status)
                 if (s) throw Error(ERUNTIME, "deflate backend failed to decompress block");
         }
+    tm.mark("inflate");
     }
     DBuf rows_d((size_t)L * 32 * sizeof(void *), st);
     {
@@ -772,6 +785,7 @@ void retrieve_impl(ipcg_ctx *c, ipcg_archive *a, int scalar, const int *k, void 
         CK(cudaMemcpyAsync(rows_d.p, flat.data(), flat.size() * sizeof(void *), cudaMemcpyHostToDevice, st));
         CK(cudaStreamSynchronize(st));
     }
+    tm.mark("rows");
     // ---- merge + reconstruct, coarsest first
     DBuf out_buf;
     void *state = out;
@@ -828,6 +842,7 @@ void retrieve_impl(ipcg_ctx *c, ipcg_archive *a, int scalar, const int *k, void 
         }
         if (!out_on_dev) CK(cudaMemcpyAsync(out, state, n * w, cudaMemcpyDeviceToHost, st));
         CK(cudaStreamSynchronize(st));
+    tm.mark("recon");
     } catch (...) {
         for (int l = 0; l < IPCG_MAX_LEVELS; ++l)
             if (ns->merged[l]) scratch_put(ns->merged[l], st);
