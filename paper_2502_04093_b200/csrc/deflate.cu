@@ -281,8 +281,13 @@ __global__ void __launch_bounds__(256) k_match(const uint8_t *in, uint64_t in_st
     if (!meta[j].active) return;
     uint64_t *rec = rec_all + (uint64_t)j * n;
     if constexpr (!WIDE) {
-        const InWords words{in + (uint64_t)j * in_stride};
-        const PrevD32 prev{prevd_all + (uint64_t)j * n};
+        // the stream bases go through an empty asm so the compiler keeps them in registers
+        // (it otherwise recomputed prevd_all + j*n from the constant bank on every chain step)
+        const uint8_t *inj = in + (uint64_t)j * in_stride;
+        const uint16_t *pvj = prevd_all + (uint64_t)j * n;
+        asm volatile("" : "+l"(inj), "+l"(pvj));
+        const InWords words{inj};
+        const PrevD32 prev{pvj};
         for (uint32_t p = blockIdx.x * blockDim.x + threadIdx.x; p < (uint32_t)n; p += gridDim.x * blockDim.x)
             rec[p] = match_search32(p, (uint32_t)n, words, prev);
     } else {

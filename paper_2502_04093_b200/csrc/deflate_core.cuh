@@ -200,7 +200,10 @@ HD uint64_t match_search32(uint32_t p, uint32_t n, const Words &w, const Prev &p
     const uint32_t flag = d0 == (uint32_t)MAX_DIST;
     const uint32_t maxlen = n - p < (uint32_t)MAX_MATCH ? n - p : (uint32_t)MAX_MATCH;
     const uint32_t nice = n - p < (uint32_t)NICE_LENGTH ? n - p : (uint32_t)NICE_LENGTH;
-    const uint32_t limit = p > (uint32_t)MAX_DIST ? p - (uint32_t)MAX_DIST : 0u;
+    uint32_t limit = p > (uint32_t)MAX_DIST ? p - (uint32_t)MAX_DIST : 0u;
+#if defined(__CUDA_ARCH__)
+    asm volatile("" : "+r"(limit));  // keep it in a register (it was recomputed every chain step)
+#endif
     uint32_t best = 0, bestd = 0;
     uint32_t q = p - d0, from = q;
     int i = 1;
