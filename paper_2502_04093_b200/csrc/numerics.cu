@@ -36,6 +36,19 @@ __device__ __forceinline__ uint64_t pass_flat(const PassDesc &p, uint64_t i, uin
     return flat;
 }
 
+// Box launch (passes of up to 3 dimensions, leading dims padded with count 1): one element
+// per thread, its coordinates straight from the grid (x: blockIdx.x*blockDim.x+threadIdx.x
+// along the last axis, y: blockIdx.y*blockDim.y+threadIdx.y, z: blockIdx.z), so the index
+// math is multiply-adds instead of the per-axis divisions of pass_flat.
+__device__ __forceinline__ bool box_index(const PassDesc &p, uint64_t &i, uint64_t &flat, uint64_t &aidx) {
+    const uint32_t x = blockIdx.x * blockDim.x + threadIdx.x, y = blockIdx.y * blockDim.y + threadIdx.y, z = blockIdx.z;
+    if (x >= p.cnt[2] || y >= p.cnt[1]) return false;
+    i = ((uint64_t)z * p.cnt[1] + y) * p.cnt[2] + x;
+    flat = p.start_flat + (uint64_t)z * p.step_flat[0] + (uint64_t)y * p.step_flat[1] + (uint64_t)x * p.step_flat[2];
+    aidx = p.axis == 0 ? z : p.axis == 1 ? y : x;
+    return true;
+}
+
 // predict_point<T>, predictor.hpp:27-38 (cubic -> linear -> copy fallback)
 template <class T>
 __device__ __forceinline__ T predict(const T *__restrict__ st, uint64_t flat, uint64_t coord, const PassDesc &p,
@@ -128,13 +141,37 @@ __global__ void k_range_final(const double *part, int nparts, double *out2) {
 // One launch per (level, axis) pass: every target reads only coarser levels and
 // earlier passes, so all targets of the pass are independent (grid.hpp:40-46).
 template <class T, bool Small>
+__device__ __forceinline__ void quant_point(const T *__restrict__ values, T *__restrict__ state, const PassDesc &p,
+                                            double eb, bool cubic, uint32_t *__restrict__ nb, uint32_t &orv,
+                                            OutlierSink sink, uint64_t i, uint64_t flat, uint64_t aidx);
+
+template <class T, bool Small, bool Box>
 __global__ void __launch_bounds__(kBlock) k_quant_pass(const T *__restrict__ values, T *__restrict__ state, PassDesc p,
                                                        double eb, bool cubic, uint32_t *__restrict__ nb,
                                                        uint32_t *lowor, OutlierSink sink) {
     uint32_t orv = 0;
-    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < p.size; i += (uint64_t)gridDim.x * blockDim.x) {
-        uint64_t aidx;
-        const uint64_t flat = pass_flat<Small>(p, i, aidx);
+    if constexpr (Box) {
+        uint64_t i, flat, aidx;
+        if (box_index(p, i, flat, aidx)) quant_point<T, Small>(values, state, p, eb, cubic, nb, orv, sink, i, flat, aidx);
+    } else {
+        for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < p.size; i += (uint64_t)gridDim.x * blockDim.x) {
+            uint64_t aidx;
+            const uint64_t flat = pass_flat<Small>(p, i, aidx);
+            quant_point<T, Small>(values, state, p, eb, cubic, nb, orv, sink, i, flat, aidx);
+        }
+    }
+    orv = __reduce_or_sync(0xffffffffu, orv);
+    // the level's OR saturates after a few warps: skip the same-address atomic when it would
+    // add no bit (one atomic per warp contended heavily with one element per thread)
+    if (lane_id() == 0 && (orv & ~*reinterpret_cast<volatile uint32_t *>(lowor))) atomicOr(lowor, orv);
+}
+
+// predict + quantize + write-back of one pass element (pipeline.hpp:163-180)
+template <class T, bool Small>
+__device__ __forceinline__ void quant_point(const T *__restrict__ values, T *__restrict__ state, const PassDesc &p,
+                                            double eb, bool cubic, uint32_t *__restrict__ nb, uint32_t &orv,
+                                            OutlierSink sink, uint64_t i, uint64_t flat, uint64_t aidx) {
+    {
         const T v = values[flat];
         T pred = (T)0;
         if (p.axis >= 0) pred = predict<T>(state, flat, p.axis_start + aidx * p.axis_step, p, cubic);
@@ -151,8 +188,6 @@ __global__ void __launch_bounds__(kBlock) k_quant_pass(const T *__restrict__ val
             sink.bits[slot] = bits_of<T>(v);
         }
     }
-    orv = __reduce_or_sync(0xffffffffu, orv);
-    if (lane_id() == 0 && orv) atomicOr(lowor, orv);
 }
 
 // ------------------------------------------------------- bitplanes + XOR code
@@ -374,15 +409,23 @@ __global__ void __launch_bounds__(256) k_merge_few(const uint32_t *const *__rest
 
 // ------------------------------------------------------------- reconstruction
 // apply_level (pipeline.hpp:61-78) for one pass
-template <class T, bool Small>
+template <class T, bool Small, bool Box>
 __global__ void __launch_bounds__(kBlock) k_recon_pass(T *__restrict__ state, PassDesc p, double eb, bool cubic,
                                                        const uint32_t *__restrict__ merged) {
-    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < p.size; i += (uint64_t)gridDim.x * blockDim.x) {
-        uint64_t aidx;
-        const uint64_t flat = pass_flat<Small>(p, i, aidx);
+    auto point = [&](uint64_t i, uint64_t flat, uint64_t aidx) {
         T pred = (T)0;
         if (p.axis >= 0) pred = predict<T>(state, flat, p.axis_start + aidx * p.axis_step, p, cubic);
         state[flat] = reconstruct_value<T>(pred, eb, (int64_t)from_negabinary(merged[p.ordinal_base + i]));
+    };
+    if constexpr (Box) {
+        uint64_t i, flat, aidx;
+        if (box_index(p, i, flat, aidx)) point(i, flat, aidx);
+    } else {
+        for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < p.size; i += (uint64_t)gridDim.x * blockDim.x) {
+            uint64_t aidx;
+            const uint64_t flat = pass_flat<Small>(p, i, aidx);
+            point(i, flat, aidx);
+        }
     }
 }
 
@@ -437,16 +480,48 @@ void launch_range(const void *values, int scalar, uint64_t n, double *scratch, d
     CKL();
 }
 
+// the pass as a 3-axis box for the Box kernels (false: more than 3 axes or grid limits)
+static bool pass_box(const PassDesc &pd, PassDesc &q, dim3 &grid, dim3 &block) {
+    if (pd.nd > 3 || pd.size == 0) return false;
+    q = pd;
+    const int pad = 3 - pd.nd;
+    for (int d = 2; d >= 0; --d) {
+        const int sd = d - pad;
+        q.cnt[d] = sd >= 0 ? pd.cnt[sd] : 1;
+        q.step_flat[d] = sd >= 0 ? pd.step_flat[sd] : 0;
+    }
+    q.nd = 3;
+    q.axis = pd.axis >= 0 ? pd.axis + pad : -1;
+    if (q.cnt[2] >= (1ull << 31)) return false;
+    const unsigned bx = (unsigned)std::min<uint64_t>(kBlock, (q.cnt[2] + 31) / 32 * 32);
+    const unsigned by = kBlock / bx;
+    const uint64_t gy = (q.cnt[1] + by - 1) / by;
+    if (gy > 65535 || q.cnt[0] > 65535) return false;
+    block = dim3(bx, by, 1);
+    grid = dim3((unsigned)((q.cnt[2] + bx - 1) / bx), (unsigned)gy, (unsigned)q.cnt[0]);
+    return true;
+}
+
 void launch_quant_pass(const void *values, void *state, int scalar, bool cubic, const PassDesc &pd, double eb,
                        uint32_t *nb, uint32_t *lowor, OutlierSink sink, cudaStream_t st) {
+    PassDesc q;
+    dim3 grid, block;
+    if (pass_box(pd, q, grid, block)) {
+        if (scalar == 0)
+            k_quant_pass<float, true, true><<<grid, block, 0, st>>>((const float *)values, (float *)state, q, eb, cubic, nb, lowor, sink);
+        else
+            k_quant_pass<double, true, true><<<grid, block, 0, st>>>((const double *)values, (double *)state, q, eb, cubic, nb, lowor, sink);
+        CKL();
+        return;
+    }
     const unsigned g = grid_for(pd.size, kBlock);
     const bool small = pd.size < (uint64_t(1) << 32);
     if (scalar == 0) {
-        if (small) k_quant_pass<float, true><<<g, kBlock, 0, st>>>((const float *)values, (float *)state, pd, eb, cubic, nb, lowor, sink);
-        else k_quant_pass<float, false><<<g, kBlock, 0, st>>>((const float *)values, (float *)state, pd, eb, cubic, nb, lowor, sink);
+        if (small) k_quant_pass<float, true, false><<<g, kBlock, 0, st>>>((const float *)values, (float *)state, pd, eb, cubic, nb, lowor, sink);
+        else k_quant_pass<float, false, false><<<g, kBlock, 0, st>>>((const float *)values, (float *)state, pd, eb, cubic, nb, lowor, sink);
     } else {
-        if (small) k_quant_pass<double, true><<<g, kBlock, 0, st>>>((const double *)values, (double *)state, pd, eb, cubic, nb, lowor, sink);
-        else k_quant_pass<double, false><<<g, kBlock, 0, st>>>((const double *)values, (double *)state, pd, eb, cubic, nb, lowor, sink);
+        if (small) k_quant_pass<double, true, false><<<g, kBlock, 0, st>>>((const double *)values, (double *)state, pd, eb, cubic, nb, lowor, sink);
+        else k_quant_pass<double, false, false><<<g, kBlock, 0, st>>>((const double *)values, (double *)state, pd, eb, cubic, nb, lowor, sink);
     }
     CKL();
 }
@@ -521,14 +596,22 @@ void launch_merge(const uint32_t *const *rows, const uint32_t *merged_in, uint32
 
 void launch_recon_pass(void *state, int scalar, bool cubic, const PassDesc &pd, double eb, const uint32_t *merged,
                        cudaStream_t st) {
+    PassDesc q;
+    dim3 grid, block;
+    if (pass_box(pd, q, grid, block)) {
+        if (scalar == 0) k_recon_pass<float, true, true><<<grid, block, 0, st>>>((float *)state, q, eb, cubic, merged);
+        else k_recon_pass<double, true, true><<<grid, block, 0, st>>>((double *)state, q, eb, cubic, merged);
+        CKL();
+        return;
+    }
     const unsigned g = grid_for(pd.size, kBlock);
     const bool small = pd.size < (uint64_t(1) << 32);
     if (scalar == 0) {
-        if (small) k_recon_pass<float, true><<<g, kBlock, 0, st>>>((float *)state, pd, eb, cubic, merged);
-        else k_recon_pass<float, false><<<g, kBlock, 0, st>>>((float *)state, pd, eb, cubic, merged);
+        if (small) k_recon_pass<float, true, false><<<g, kBlock, 0, st>>>((float *)state, pd, eb, cubic, merged);
+        else k_recon_pass<float, false, false><<<g, kBlock, 0, st>>>((float *)state, pd, eb, cubic, merged);
     } else {
-        if (small) k_recon_pass<double, true><<<g, kBlock, 0, st>>>((double *)state, pd, eb, cubic, merged);
-        else k_recon_pass<double, false><<<g, kBlock, 0, st>>>((double *)state, pd, eb, cubic, merged);
+        if (small) k_recon_pass<double, true, false><<<g, kBlock, 0, st>>>((double *)state, pd, eb, cubic, merged);
+        else k_recon_pass<double, false, false><<<g, kBlock, 0, st>>>((double *)state, pd, eb, cubic, merged);
     }
     CKL();
 }
