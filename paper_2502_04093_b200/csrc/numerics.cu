@@ -101,17 +101,36 @@ __device__ __forceinline__ uint64_t bits_of(T v) {
 
 // ------------------------------------------------------------------ range scan
 // std::min/std::max seeded with +/-inf: NaN never wins (pipeline.hpp:151-155)
+// 16-byte vector loads; comparisons in T (float -> double is exact and order-preserving,
+// and NaN loses every comparison either way), widened to double for the result
 template <class T>
 __global__ void k_range_partial(const T *__restrict__ v, uint64_t n, double *part) {
-    double lo = INFINITY, hi = -INFINITY;
-    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
-        const double x = (double)v[i];
+    constexpr int V = 16 / (int)sizeof(T);
+    T lo = (T)INFINITY, hi = (T)-INFINITY;
+    const uint64_t tid = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x, nth = (uint64_t)gridDim.x * blockDim.x;
+    uint64_t done = 0;
+    if ((reinterpret_cast<uintptr_t>(v) & 15) == 0) {
+        const uint64_t nv = n / V;
+        const uint4 *vv = reinterpret_cast<const uint4 *>(v);
+        for (uint64_t k = tid; k < nv; k += nth) {
+            const uint4 q = __ldg(vv + k);
+            const T *e = reinterpret_cast<const T *>(&q);
+#pragma unroll
+            for (int j = 0; j < V; ++j) {
+                lo = (e[j] < lo) ? e[j] : lo;
+                hi = (hi < e[j]) ? e[j] : hi;
+            }
+        }
+        done = nv * V;
+    }
+    for (uint64_t i = done + tid; i < n; i += nth) {
+        const T x = v[i];
         lo = (x < lo) ? x : lo;
         hi = (hi < x) ? x : hi;
     }
     __shared__ double slo[kBlock], shi[kBlock];
-    slo[threadIdx.x] = lo;
-    shi[threadIdx.x] = hi;
+    slo[threadIdx.x] = (double)lo;
+    shi[threadIdx.x] = (double)hi;
     __syncthreads();
     for (unsigned s = blockDim.x / 2; s > 0; s >>= 1) {
         if (threadIdx.x < s) {
@@ -472,7 +491,7 @@ __global__ void k_outlier_apply(T *__restrict__ state, PassDesc p, const uint8_t
 // ============================================================= host launchers
 
 void launch_range(const void *values, int scalar, uint64_t n, double *scratch, double *out2, cudaStream_t st) {
-    const unsigned g = grid_for(n, kBlock, 1024);
+    const unsigned g = grid_for((n + 3) / 4, kBlock, 1024);
     if (scalar == 0) k_range_partial<float><<<g, kBlock, 0, st>>>((const float *)values, n, scratch);
     else k_range_partial<double><<<g, kBlock, 0, st>>>((const double *)values, n, scratch);
     CKL();
