@@ -240,8 +240,17 @@ def run_ours(args, ws, rank, local):
         g = gbs(fam)
         if g is not None:
             hbm[fam] = {"ms": round(prof[fam]["ms"], 3), "achieved": round(g, 1), "frac": round(g / peak, 4)}
+    # measured DRAM traffic of the dominant family (ncu, one compress = one step's launches)
+    traffic, traffic_src = None, None
+    tp = os.path.join(ROOT, "profiles", "r01_traffic.json")
+    if os.path.exists(tp):
+        tj = json.load(open(tp)).get(top[0])
+        if tj:
+            traffic, traffic_src = int(tj["dram_bytes"]), tj["source"]
     roofline = {"bound": "hbm", "kernel": top[0], "achieved": round(achieved, 2), "peak": peak,
-                "unit": "GB/s", "frac": round(achieved / peak, 5), "traffic": None,
+                "unit": "GB/s", "frac": round(achieved / peak, 5), "traffic": traffic,
+                "traffic_basis": "bytes per step for the family (same basis as achieved)", "traffic_source": traffic_src,
+                "algorithmic_bytes": int(top[1]["bytes"]),
                 "share_of_step": round(top[1]["ms"] / step_ms, 4) if step_ms else None,
                 "peak_source": peak_src,
                 "family_timing": "CUDA events per family in one profiled step run serially "
