@@ -580,48 +580,58 @@ __global__ void __launch_bounds__(DWARPS * 32) k_decode_cands(const InflateJob *
         bool good = true;
         WBits wb;
         wb.init(job.src, job.src_len, b.used);
+        // segments of SEG symbols: the checkpoint and the overrun test once per segment, a
+        // tight decode loop inside (same outcome as testing every symbol: an overrun stays
+        // an overrun, and the final test below catches one inside the last segment)
         for (;;) {
-            wb.refill();  // >= 33 bits: a literal/length code and its extra bits
-            const int sym = huff_decode_w(lit_s[slot], wb);
-            if (sym < 0) {
+            if (ns >= MAXSYM) {  // only an end-of-block may follow MAXSYM symbols
+                wb.refill();
+                if (huff_decode_w(lit_s[slot], wb) != 256) good = false;
+                break;
+            }
+            if (gl == 0) ckpt_pool[ci * NCKPT + ns / SEG] = (uint32_t)bytes;
+            if (wb.overrun()) {
                 good = false;
                 break;
             }
-            if (sym == 256) break;
-            if (ns >= MAXSYM) {
-                good = false;
-                break;
-            }
-            if (ns % SEG == 0) {
-                if (gl == 0) ckpt_pool[ci * NCKPT + ns / SEG] = (uint32_t)bytes;
-                if (wb.overrun()) {
+            const uint32_t seg_end = min(ns + (uint32_t)SEG, (uint32_t)MAXSYM);
+            bool eob = false;
+            while (ns < seg_end) {
+                wb.refill();  // >= 33 bits: a literal/length code and its extra bits
+                const int sym = huff_decode_w(lit_s[slot], wb);
+                if (sym < 256) {
+                    if (sym < 0) {
+                        good = false;
+                        break;
+                    }
+                    if (gl == 0) out[ns] = sym_lit((uint32_t)sym);
+                    nz |= (uint32_t)sym;
+                    ++ns;
+                    ++bytes;
+                    continue;
+                }
+                if (sym == 256) {
+                    eob = true;
+                    break;
+                }
+                const int li = sym - 257;
+                if (li >= 29) {
                     good = false;
                     break;
                 }
-            }
-            if (sym < 256) {
-                if (gl == 0) out[ns] = sym_lit((uint32_t)sym);
-                nz |= (uint32_t)sym;
+                const uint32_t len = kLBase[li] + wb.take(kLExt[li]);
+                wb.refill();  // >= 33 bits: a distance code and its extra bits
+                const int ds = huff_decode_w(dist_s[slot], wb);
+                if (ds < 0 || ds >= 30) {
+                    good = false;
+                    break;
+                }
+                const uint32_t d = kDBase[ds] + wb.take(kDExt[ds]);
+                if (gl == 0) out[ns] = sym_match(len, d);
                 ++ns;
-                ++bytes;
-                continue;
+                bytes += len;
             }
-            const int li = sym - 257;
-            if (li >= 29) {
-                good = false;
-                break;
-            }
-            const uint32_t len = kLBase[li] + wb.take(kLExt[li]);
-            wb.refill();  // >= 33 bits: a distance code and its extra bits
-            const int ds = huff_decode_w(dist_s[slot], wb);
-            if (ds < 0 || ds >= 30) {
-                good = false;
-                break;
-            }
-            const uint32_t d = kDBase[ds] + wb.take(kDExt[ds]);
-            if (gl == 0) out[ns] = sym_match(len, d);
-            ++ns;
-            bytes += len;
+            if (!good || eob) break;
         }
         if (wb.overrun()) good = false;
         b.used = wb.pos - (uint64_t)(reinterpret_cast<uintptr_t>(job.src) & 3) * 8;
