@@ -36,7 +36,7 @@ namespace {
 constexpr int FASTBITS = 9;
 constexpr int MAXSYM = 16400;  // symbols stored per candidate block (zlib blocks: <= 16383)
 constexpr int WARPS = 4;
-constexpr int SEG = 512;                  // symbols per emit segment
+constexpr int SEG = 128;                  // symbols per emit segment
 constexpr int NCKPT = MAXSYM / SEG + 2;   // output-offset checkpoints per candidate
 
 // ------------------------------------------------------------------ bit reader
@@ -886,7 +886,8 @@ __global__ void __launch_bounds__(WARPS * 32) k_emit(const InflateJob *jobs, con
         for (uint64_t i = lane; i < blk.out_len; i += 32) dst[blk.out_off + i] = job.src[blk.src + i];
         return;
     }
-    const uint32_t s_begin = seg * SEG, s_end = min(blk.nsyms, s_begin + SEG);
+    // a block without checkpoints (decoded by the chain itself) is one segment of any length
+    const uint32_t s_begin = seg * SEG, s_end = blk.nseg == 1 ? blk.nsyms : min(blk.nsyms, s_begin + SEG);
     const uint64_t b0 = blk.out_off + (seg ? ckpt_pool[blk.ckpt * NCKPT + seg] : 0);
     const uint32_t *syms = blk.type == 1 ? pool + blk.src : T.fallback + blk.src;
     uint64_t o = b0;

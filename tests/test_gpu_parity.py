@@ -207,9 +207,19 @@ def test_inflate_against_zlib_streams(ctx):
              (b"the quick brown fox %d " * 20000)[:300000],
              np.repeat(rng.integers(0, 3, 5000, dtype=np.uint8), rng.integers(1, 300, 5000)).tobytes()]
     blocks, want = [], []
+    def deflate(d, level, strategy):
+        c = zlib.compressobj(level, zlib.DEFLATED, 15, 8, strategy)
+        return c.compress(d) + c.flush()
+
     for d in datas:
         for level in (1, 6, 9):
             z = zlib.compress(d, level)
+            blocks.append((1, z, zlib.crc32(z), len(d)))
+            want.append(d)
+        # fixed-Huffman-only streams (long static blocks the chain decodes itself),
+        # Huffman-only (no matches) and RLE (distance-1 runs)
+        for strategy in (zlib.Z_FIXED, zlib.Z_HUFFMAN_ONLY, zlib.Z_RLE):
+            z = deflate(d, 6, strategy)
             blocks.append((1, z, zlib.crc32(z), len(d)))
             want.append(d)
         blocks.append((0, d, zlib.crc32(d), len(d)))
