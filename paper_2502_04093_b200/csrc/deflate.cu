@@ -8,6 +8,7 @@
 //   symbol emission -> per-block Huffman plans -> bit layout -> bit emission ->
 //   CRC-32 (chunked + GF(2) combine).
 // All-zero planes (most high planes) are compressed once per batch and shared.
+#include <cstdlib>
 #include "deflate.cuh"
 #include "deflate_core.cuh"
 
@@ -191,28 +192,53 @@ __global__ void k_select(StreamMeta *meta, int S, uint64_t n) {
 }
 
 // ------------------------------------------------------------- 2. prevlinks
-// zlib's head/prev insertion order is sequential; one warp walks 32 positions per
-// step through a 64 KiB shared-memory head table (match_any resolves same-step
-// collisions).  Each warp owns a 32 KiB block and warms up on the block before it.
-// Only the head-table read/write chain is serial: a batch of AHEAD steps has its bytes
-// loaded one batch ahead (one byte per lane + two spill bytes, the rest by shuffles)
-// and all its match_any masks computed before the chain runs (ncu: the byte-load and
-// MATCH.ANY latencies dominated when they sat on the chain).
+// zlib's head/prev insertion order is sequential; one warp walks 32 positions per step
+// through a 64 KiB shared-memory head table (match_any resolves same-step collisions).
+// Each warp owns `span` 32 KiB windows (chosen per launch from a wave model: longer spans
+// amortise the warm-up, shorter ones fill the SMs) and warms up on the window before them.  Table
+// entries hold positions (relative to the warm-up start) modulo 65536: at the start of
+// window W every entry older than WSIZE-1 relative to the window start becomes the sentinel
+// S_W = ((W-1)*WSIZE) mod 65536 -- valid entries during W lie in [W*WSIZE - 32767,
+// (W+1)*WSIZE), which covers every residue but that one -- so a lookup's distance is
+// (p - entry) mod 65536.  Only the head-table read/write chain is serial: a batch of AHEAD
+// steps has its bytes loaded one batch ahead (one byte per lane + two spill bytes, the rest
+// by shuffles) and all its match_any masks computed before the chain runs; head reads are
+// consumed only after the batch (ncu: using them inside the chain, packing the two loaded
+// bytes at fetch time, or inlining the sweep each cost 1.5-2.5x).
+// Window-boundary sweep of a prevlinks head table (out of line: it runs once per 32 KiB
+// window and would otherwise cost the chain loop registers).
+__device__ __noinline__ uint32_t prevlinks_sweep(uint16_t *head, unsigned lane, uint32_t rel0, uint32_t sent) {
+    const uint32_t nsent = (rel0 - WSIZE) & 0xFFFF;
+    uint4 *h4 = reinterpret_cast<uint4 *>(head);
+    for (int i = lane; i < 32768 / 8; i += 32) {
+        uint4 v = h4[i];
+        uint32_t *w = reinterpret_cast<uint32_t *>(&v);
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+            const uint32_t sh = (k & 1) * 16, e = (w[k >> 1] >> sh) & 0xFFFF, age = (rel0 - e) & 0xFFFF;
+            if (e == sent || age == 0 || age >= (uint32_t)WSIZE) w[k >> 1] = (w[k >> 1] & ~(0xFFFFu << sh)) | (nsent << sh);
+        }
+        h4[i] = v;
+    }
+    __syncwarp();
+    return nsent;
+}
+
 __global__ void __launch_bounds__(PL_WARPS * 32) k_prevlinks(const uint8_t *in, uint64_t in_stride, uint64_t n,
-                                                           const StreamMeta *meta, uint16_t *prevd_all) {
+                                                           const StreamMeta *meta, uint16_t *prevd_all, int span) {
     extern __shared__ uint16_t heads[];
     const int j = blockIdx.y;
     if (!meta[j].active) return;
     const unsigned warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const uint64_t blk = (uint64_t)blockIdx.x * PL_WARPS + warp;
-    if (blk * WSIZE >= n) return;
+    const uint64_t out0 = ((uint64_t)blockIdx.x * PL_WARPS + warp) * (uint64_t)span * WSIZE;
+    if (out0 >= n) return;
     uint16_t *head = heads + (size_t)warp * 32768;
-    for (int i = lane; i < 32768; i += 32) head[i] = 0xFFFF;
+    for (int i = lane; i < 32768; i += 32) head[i] = 0x8000;  // S_0
     __syncwarp();
     const uint8_t *p = in + (uint64_t)j * in_stride;
     uint16_t *prevd = prevd_all + (uint64_t)j * n;
-    const uint64_t base = blk == 0 ? 0 : (blk - 1) * WSIZE;
-    const uint64_t out0 = blk * WSIZE, end = min(n, (blk + 1) * WSIZE);
+    const uint64_t base = out0 == 0 ? 0 : out0 - WSIZE;
+    const uint64_t end = min(n, out0 + (uint64_t)span * WSIZE);
     constexpr int AHEAD = 16;
     uint32_t b0[AHEAD], bx[AHEAD];  // byte at q; lanes 0,1: byte at q + 32
     auto fetch = [&](uint64_t pos0) {
@@ -225,7 +251,12 @@ __global__ void __launch_bounds__(PL_WARPS * 32) k_prevlinks(const uint8_t *in, 
     };
     fetch(base);
     const unsigned lt_mask = (1u << lane) - 1u;
+    uint32_t sent = 0x8000;
     for (uint64_t pos0 = base; pos0 < end; pos0 += 32 * AHEAD) {
+        const uint32_t rel0 = (uint32_t)(pos0 - base);
+        if (rel0 != 0 && (rel0 & (WSIZE - 1)) == 0) {  // window boundary (32*AHEAD divides WSIZE)
+            sent = prevlinks_sweep(head, lane, rel0, sent);
+        }
         uint32_t hs[AHEAD], mk[AHEAD];
 #pragma unroll
         for (int k = 0; k < AHEAD; ++k) {
@@ -248,7 +279,7 @@ __global__ void __launch_bounds__(PL_WARPS * 32) k_prevlinks(const uint8_t *in, 
             const bool valid = h < 0x10000u;
             const uint32_t rel = (uint32_t)(pos0 + 32 * k + lane - base);
             const unsigned lower = mk[k] & lt_mask;
-            prel[k] = 0xFFFF;
+            prel[k] = sent;
             if (lower) prel[k] = rel - (lane - (31u - __clz(lower)));
             else if (valid) prel[k] = head[h];
             __syncwarp();
@@ -259,10 +290,8 @@ __global__ void __launch_bounds__(PL_WARPS * 32) k_prevlinks(const uint8_t *in, 
         for (int k = 0; k < AHEAD; ++k) {
             const uint64_t q = pos0 + 32 * k + lane;
             if (q >= out0 && q < end) {
-                const uint32_t rel = (uint32_t)(q - base);
-                uint32_t d = 0;
-                if (hs[k] < 0x10000u && prel[k] != 0xFFFF && rel - prel[k] < (uint32_t)WSIZE) d = rel - prel[k];
-                prevd[q] = (uint16_t)d;
+                const uint32_t e = prel[k] & 0xFFFF, d = ((uint32_t)(q - base) - e) & 0xFFFF;
+                prevd[q] = (uint16_t)(hs[k] < 0x10000u && e != sent && d < (uint32_t)WSIZE ? d : 0u);
             }
         }
     }
@@ -1102,7 +1131,18 @@ void DeflateBatch::run(const uint8_t *in, uint64_t in_stride, int S, uint64_t n,
         }
         {
         ProfScope ps1("deflate.prevlinks", st, (uint64_t)S * n * 3);
-        k_prevlinks<<<dim3((unsigned)((nblk + PL_WARPS - 1) / PL_WARPS), S), PL_WARPS * 32, smem, st>>>(in, in_stride, n, w.meta, w.prevd);
+        static int span_env = getenv("IPCG_PL_SPAN") ? atoi(getenv("IPCG_PL_SPAN")) : 0;
+        int span = span_env;
+        if (span <= 0) {
+            // waves of resident warps x per-warp windows (warm-up + span, sweeps ~0.2 window)
+            const uint64_t slots = (uint64_t)num_sms() * PL_WARPS, wtot = nblk * (uint64_t)S;
+            double best = 1e300;
+            for (int s = 1; s <= 6; ++s) {
+                const double t = (double)((wtot + slots * s - 1) / (slots * s)) * (1.0 + 1.2 * s);
+                if (t < best - 1e-9) best = t, span = s;
+            }
+        }
+        k_prevlinks<<<dim3((unsigned)((nblk + span * PL_WARPS - 1) / (span * PL_WARPS)), S), PL_WARPS * 32, smem, st>>>(in, in_stride, n, w.meta, w.prevd, span);
         CKL();
         }
         {

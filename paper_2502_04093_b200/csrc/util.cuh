@@ -144,6 +144,17 @@ struct DevAlloc {
     }
 };
 
+// SM count of the current device (cached; one device per process, see include/ipcomp_b200.h)
+inline int num_sms() {
+    static int sms = [] {
+        int dev = 0, v = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+        return v > 0 ? v : 148;
+    }();
+    return sms;
+}
+
 inline unsigned grid_for(uint64_t n, unsigned block, unsigned cap = 148u * 32u) {
     uint64_t g = (n + block - 1) / block;
     if (g == 0) g = 1;
