@@ -147,6 +147,7 @@ struct InWords {
     const uint8_t *p;
     __device__ __forceinline__ uint32_t word(uint32_t k) const { return __ldg(reinterpret_cast<const uint32_t *>(p) + k); }
     __device__ __forceinline__ uint32_t byte(uint32_t i) const { return __ldg(p + i); }
+    __device__ __forceinline__ const uint8_t *at(uint32_t off) const { return p + off; }
 };
 
 // ------------------------------------------------------------------ 1. scan

@@ -157,6 +157,13 @@ HD uint64_t match_search(int64_t p, int64_t n, const Bytes &bytes, const Prev &p
 //  * common-prefix lengths compare 4 bytes per step from 4-byte-aligned words
 //    (Words::word(k) = bytes 4k..4k+3, little-endian; Words::word is only called for
 //    words whose first byte is < n).
+HD uint32_t ldg_byte(const uint8_t *a) {
+#if defined(__CUDA_ARCH__)
+    return __ldg(a);
+#else
+    return *a;
+#endif
+}
 HD uint32_t funnel_r(uint32_t lo, uint32_t hi, uint32_t sh) {
 #if defined(__CUDA_ARCH__)
     return __funnelshift_r(lo, hi, sh);
@@ -192,26 +199,40 @@ HD uint32_t match_len32(const Words &w, uint32_t n, uint32_t a, uint32_t b, uint
     }
 }
 
+// The walk is resumable: walk32_start examines candidate 1 (and its run skip) and
+// positions the walk on candidate 2; walk32_run examines up to `budget` candidates and
+// either finishes (returns true, record in `rec`) or stops at the top of the next
+// candidate with the state in `s` (tests/native/zmodel.cpp pins stop/resume at every
+// budget).  A k_match that gave every position a short budget and resumed the unfinished
+// walks from a compacted queue was measured slower (25.8 vs 22.1 ms): ncu showed the same
+// 11 active lanes per instruction in the resume pass, so the divergence is within a chain
+// step (quick reject vs. compare), not between chain lengths.
+struct Walk32 {
+    uint32_t p, q, best, bestd, l32, d32, flag;
+    int i;  // index of candidate q
+};
+
 template <class Words, class Prev>
-HD uint64_t match_search32(uint32_t p, uint32_t n, const Words &w, const Prev &prevd) {
-    if (p + MIN_MATCH > n) return 0;
+HD bool walk32_start(uint32_t p, uint32_t n, const Words &w, const Prev &prevd, Walk32 &s, uint64_t &rec) {
+    rec = 0;
+    if (p + MIN_MATCH > n) return true;
     const uint32_t d0 = prevd(p);
-    if (d0 == 0 || d0 == p || d0 > (uint32_t)MAX_DIST) return 0;
+    if (d0 == 0 || d0 == p || d0 > (uint32_t)MAX_DIST) return true;
     const uint32_t flag = d0 == (uint32_t)MAX_DIST;
     const uint32_t maxlen = n - p < (uint32_t)MAX_MATCH ? n - p : (uint32_t)MAX_MATCH;
     const uint32_t nice = n - p < (uint32_t)NICE_LENGTH ? n - p : (uint32_t)NICE_LENGTH;
-    uint32_t limit = p > (uint32_t)MAX_DIST ? p - (uint32_t)MAX_DIST : 0u;
-#if defined(__CUDA_ARCH__)
-    asm volatile("" : "+r"(limit));  // keep it in a register (it was recomputed every chain step)
-#endif
+    const uint32_t limit = p > (uint32_t)MAX_DIST ? p - (uint32_t)MAX_DIST : 0u;
     uint32_t best = 0, bestd = 0;
     uint32_t q = p - d0, from = q;
     int i = 1;
     {  // candidate 1: no quick reject (best == 0); may start a same-byte run
-        uint32_t len = match_len32(w, n, p, q, maxlen);
+        const uint32_t len = match_len32(w, n, p, q, maxlen);
         if (len >= (uint32_t)MIN_MATCH) {
             best = len, bestd = p - q;
-            if (len >= nice) return mrec_pack(best, bestd, best, bestd, flag);
+            if (len >= nice) {
+                rec = mrec_pack(best, bestd, best, bestd, flag);
+                return true;
+            }
             if (q == p - 1) {  // see match_step: candidates p-2 .. r all fail the quick reject
                 const uint32_t v = w.byte(p - 1);
                 const uint32_t lo = p > (uint32_t)MAX_CHAIN ? p - (uint32_t)MAX_CHAIN : 0u;
@@ -219,43 +240,87 @@ HD uint64_t match_search32(uint32_t p, uint32_t n, const Words &w, const Prev &p
                 uint32_t r = p - 1;
                 while (r >= floor_ + 1 && w.byte(r - 1) == v) --r;
                 i += (int)(p - 1 - r);
-                if (i >= MAX_CHAIN) return mrec_pack(best, bestd, best, bestd, flag);
+                if (i >= MAX_CHAIN) {
+                    rec = mrec_pack(best, bestd, best, bestd, flag);
+                    return true;
+                }
                 from = r;
             }
         }
     }
-    uint32_t l32 = best, d32 = bestd;
-    {
-        const uint32_t dq = prevd(from);
-        if (dq == 0 || from - dq <= limit || i >= MAX_CHAIN) return mrec_pack(best, bestd, l32, d32, flag);
-        q = from - dq;
-        ++i;
+    const uint32_t dq = prevd(from);
+    // (from == limit is possible here: the head candidate may sit at exactly MAX_DIST)
+    if (dq == 0 || from - dq <= limit || i >= MAX_CHAIN) {
+        rec = mrec_pack(best, bestd, best, bestd, flag);
+        return true;
     }
-    // scan_end1 / scan_end (only meaningful while MIN_MATCH <= best < maxlen)
-    uint32_t e0 = best ? w.byte(p + best - 1) : 0u, e1 = best && best < maxlen ? w.byte(p + best) : 0u;
+    s = Walk32{p, from - dq, best, bestd, best, bestd, flag, i + 1};
+    return false;
+}
+
+// scan_end1 / scan_end (only meaningful while MIN_MATCH <= best; best < nice <= maxlen holds
+// in the loop).  Both quick-reject bytes of q are loaded unconditionally through
+// qb = stream + best - 1 (at best == 0 they are q, q+1 and unused).  The chain ends when the
+// link is NIL or leaves the window: dq - 1 >= q - lim1 (unsigned; dq <= q and q >= lim1 for
+// every chained candidate).  Candidates up to 32 and beyond run as two phases so the
+// chain-32 snapshot is taken once instead of every step.
+template <class Words, class Prev>
+HD bool walk32_run(uint32_t n, const Words &w, const Prev &prevd, Walk32 &s, int budget, uint64_t &rec) {
+    const uint32_t p = s.p;
+    const uint32_t maxlen = n - p < (uint32_t)MAX_MATCH ? n - p : (uint32_t)MAX_MATCH;
+    const uint32_t nice = n - p < (uint32_t)NICE_LENGTH ? n - p : (uint32_t)NICE_LENGTH;
+    const uint32_t lim1 = (p > (uint32_t)MAX_DIST ? p - (uint32_t)MAX_DIST : 0u) + 1u;
+    uint32_t q = s.q, best = s.best, bestd = s.bestd, l32 = s.l32, d32 = s.d32;
+    int i = s.i;
+    uint32_t e0 = best ? w.byte(p + best - 1) : 0u, e1 = best ? w.byte(p + best) : 0u;
+    const uint8_t *qb = w.at(best ? best - 1 : 0u);
+    int stop = i <= 32 ? 32 : MAX_CHAIN;
     for (;;) {
+        if (budget-- <= 0) {
+            s.q = q, s.best = best, s.bestd = bestd, s.l32 = l32, s.d32 = d32, s.i = i;
+            return false;
+        }
         const uint32_t dq = prevd(q);
-        const bool reject = best >= (uint32_t)MIN_MATCH && best < maxlen &&
-                            (w.byte(q + best) != e1 || w.byte(q + best - 1) != e0);
-        if (!reject) {
-            uint32_t len = match_len32(w, n, p, q, maxlen);
-            if (len < (uint32_t)MIN_MATCH) len = 0;
-            if (len > best) {
+        const uint32_t x0 = ldg_byte(qb + q), x1 = ldg_byte(qb + q + 1);
+        if (best == 0 || (x0 == e0 && x1 == e1)) {
+            const uint32_t len = match_len32(w, n, p, q, maxlen);
+            if (len >= (uint32_t)MIN_MATCH && len > best) {
                 best = len, bestd = p - q;
                 if (len >= nice) {
                     if (i <= 32) l32 = best, d32 = bestd;
-                    return mrec_pack(best, bestd, l32, d32, flag);
+                    break;
                 }
                 e0 = w.byte(p + best - 1);
-                e1 = best < maxlen ? w.byte(p + best) : 0u;
+                e1 = w.byte(p + best);
+                qb = w.at(best - 1);
             }
         }
-        if (i <= 32) l32 = best, d32 = bestd;
-        if (dq == 0 || q - dq <= limit || i >= MAX_CHAIN) break;
+        if (dq - 1u >= q - lim1 || i >= stop) {
+            if (stop == 32) {
+                l32 = best, d32 = bestd;
+                if (i == 32 && dq - 1u < q - lim1) {  // phase 2: candidates 33..MAX_CHAIN
+                    stop = MAX_CHAIN;
+                    q -= dq;
+                    ++i;
+                    continue;
+                }
+            }
+            break;
+        }
         q -= dq;
         ++i;
     }
-    return mrec_pack(best, bestd, l32, d32, flag);
+    rec = mrec_pack(best, bestd, l32, d32, s.flag);
+    return true;
+}
+
+template <class Words, class Prev>
+HD uint64_t match_search32(uint32_t p, uint32_t n, const Words &w, const Prev &prevd) {
+    Walk32 s;
+    uint64_t rec;
+    if (walk32_start(p, n, w, prevd, s, rec)) return rec;
+    walk32_run(n, w, prevd, s, 1 << 30, rec);
+    return rec;
 }
 
 // ------------------------------------------------------------- window slides

@@ -37,6 +37,7 @@ struct HostWords {
         return v;
     }
     uint32_t byte(uint32_t i) const { return in[i]; }
+    const uint8_t *at(uint32_t off) const { return in + off; }
 };
 
 struct Stats {
@@ -270,8 +271,22 @@ extern "C" uint64_t zmodel_match_check(const uint8_t *in, uint64_t n) {
     auto prevfn = [&](int64_t i) -> uint32_t { return prevd[i]; };
     const HostWords words{in, n};
     uint64_t bad = 0;
-    for (int64_t p = 0; p < (int64_t)n; ++p)
-        bad += match_search(p, (int64_t)n, bytes, prevfn) != match_search32((uint32_t)p, (uint32_t)n, words, prevfn);
+    for (int64_t p = 0; p < (int64_t)n; ++p) {
+        const uint64_t ref = match_search(p, (int64_t)n, bytes, prevfn);
+        bad += ref != match_search32((uint32_t)p, (uint32_t)n, words, prevfn);
+        // the resumable walk (k_match's budgeted first pass + queued second pass), stopped
+        // and resumed every `budget` candidates
+        for (int budget : {1, 2, 5, 31}) {
+            Walk32 s;
+            uint64_t rec;
+            if (!walk32_start((uint32_t)p, (uint32_t)n, words, prevfn, s, rec))
+                while (!walk32_run((uint32_t)n, words, prevfn, s, budget, rec)) {
+                    Walk32 t = s;  // the state round-trips through memory
+                    s = t;
+                }
+            bad += rec != ref;
+        }
+    }
     return bad;
 }
 
