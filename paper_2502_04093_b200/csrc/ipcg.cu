@@ -606,23 +606,33 @@ void retrieve_impl(ipcg_ctx *c, ipcg_archive *a, int scalar, const int *k, void 
             CK(cudaStreamSynchronize(st));
         }
     } else {
+        // straight from the caller's buffer (no host-side staging copy): spans that are
+        // adjacent in the archive (a level's planes and its outlier block) go as one copy,
+        // which is a DMA from page-locked memory and a driver-pipelined copy otherwise.  The
+        // call returns only after the stream drains, so the buffer is not read after return.
         stage = DBuf(std::max<uint64_t>(staged, 1), st);
-        uint8_t *hp = static_cast<uint8_t *>(pinned(c, std::max<uint64_t>(staged, 1)));
+        const uint8_t *hb = a->bytes + ix.index_bytes;
         uint64_t o = 0;
-        for (size_t i = 0; i < spans.size(); ++i) {
-            std::memcpy(hp + o, a->bytes + ix.index_bytes + spans[i].first, spans[i].second);
+        for (size_t i = 0; i < spans.size();) {
+            size_t e = i + 1;
             src_off[i] = o;
-            o += spans[i].second;
+            while (e < spans.size() && spans[e].first == spans[e - 1].first + spans[e - 1].second) {
+                src_off[e] = o + (spans[e].first - spans[i].first);
+                ++e;
+            }
+            const uint64_t len = spans[e - 1].first + spans[e - 1].second - spans[i].first;
+            if (len) CK(cudaMemcpyAsync(stage.as<uint8_t>() + o, hb + spans[i].first, len, cudaMemcpyHostToDevice, st));
+            o += len;
+            i = e;
         }
         size_t si = 0, ri = 0;
         for (int level = L; level >= 1; --level) {
             const LevelPlan &p = lv[level - 1];
             if (!p.active) continue;
-            for (int q = p.p0; q < p.p1; ++q, ++ri) std::memcpy(&headers[ri * 21], hp + src_off[si++], 21);
+            for (int q = p.p0; q < p.p1; ++q, ++ri, ++si)  // (a short block fails the length checks below)
+                std::memcpy(&headers[ri * 21], hb + spans[si].first, std::min<uint64_t>(21, spans[si].second));
             ++si;
         }
-        CK(cudaMemcpyAsync(stage.p, hp, staged, cudaMemcpyHostToDevice, st));
-        CK(cudaStreamSynchronize(st));  // the pinned staging buffer is reused below
         src_dev = stage.as<uint8_t>();
     }
     a->payload_read += read;
