@@ -37,6 +37,7 @@ struct ipcg_ctx {
     cudaStream_t stream = nullptr;  // all work is ordered on this stream (forks join back)
     cudaStream_t own_stream = nullptr;
     std::vector<cudaStream_t> side;  // fork targets (per-level chains)
+    std::vector<cudaStream_t> loss;  // per-level loss-table streams (highest priority)
     std::vector<cudaEvent_t> events;
     size_t events_used = 0;
     ScratchPool scratch;  // per-call device scratch, reused across calls (also archive/session memory)
@@ -101,15 +102,34 @@ struct DBuf {  // stream-ordered device allocation
 
 // side stream i: 0 carries work off the critical path (lowest priority), the others the
 // critical chains (highest priority), so the scheduler fills the gaps of the latter with it
+// Stream priorities for compress: level 1's lossless chain (side stream 1) is the critical
+// path but throughput-bound -- it runs at the lowest priority and fills whatever the
+// others leave; the coarser levels' latency-bound chains and the loss tables run at the
+// highest, so their few CTAs are dispatched as soon as an SM frees up instead of queueing
+// behind level 1's kernels.  Measured on cfg2: 46.4 ms per compress and run-to-run stable,
+// vs 57 ms (loss tables on one shared stream) and a bimodal 48-58 ms (level 1 highest).
+static int prio_for(bool low) {
+    int least = 0, greatest = 0;
+    CK(cudaDeviceGetStreamPriorityRange(&least, &greatest));
+    return low ? least : greatest;
+}
+
 cudaStream_t side_stream(ipcg_ctx *c, size_t i) {
     while (c->side.size() <= i) {
-        int least = 0, greatest = 0;
-        CK(cudaDeviceGetStreamPriorityRange(&least, &greatest));
         cudaStream_t s;
-        CK(cudaStreamCreateWithPriority(&s, cudaStreamNonBlocking, c->side.empty() ? greatest : least));
+        CK(cudaStreamCreateWithPriority(&s, cudaStreamNonBlocking, prio_for(c->side.size() == 1)));
         c->side.push_back(s);
     }
     return c->side[i];
+}
+
+cudaStream_t loss_stream(ipcg_ctx *c, size_t i) {
+    while (c->loss.size() <= i) {
+        cudaStream_t s;
+        CK(cudaStreamCreateWithPriority(&s, cudaStreamNonBlocking, prio_for(false)));
+        c->loss.push_back(s);
+    }
+    return c->loss[i];
 }
 
 // an event from the context's pool (reused across calls: a wait captures the event's
@@ -226,6 +246,36 @@ void gather(ipcg_ctx *c, std::vector<CopyDesc> descs, uint8_t *dst) {
 }
 
 // ---------------------------------------------------------------- compress
+// dev timeline (IPCG_DEBUG_TIMELINE=1): when each stream reaches the marked points of a compress
+struct Timeline {
+    bool on = getenv("IPCG_DEBUG_TIMELINE") != nullptr;
+    std::vector<std::pair<std::string, cudaEvent_t>> ev;
+    cudaEvent_t mark(const std::string &name, cudaStream_t s) {
+        if (!on) return nullptr;
+        cudaEvent_t e;
+        CK(cudaEventCreate(&e));
+        CK(cudaEventRecord(e, s));
+        ev.push_back({name, e});
+        return e;
+    }
+    void print() {
+        if (!on || ev.empty()) return;
+        CK(cudaDeviceSynchronize());
+        std::vector<std::pair<float, std::string>> t;
+        for (auto &x : ev) {
+            float ms = 0;
+            CK(cudaEventElapsedTime(&ms, ev[0].second, x.second));
+            t.push_back({ms, x.first});
+        }
+        std::sort(t.begin(), t.end());
+        fprintf(stderr, "[timeline]");
+        for (auto &x : t) fprintf(stderr, " %s@%.1f", x.second.c_str(), x.first);
+        fprintf(stderr, "\n");
+        for (auto &x : ev) cudaEventDestroy(x.second);
+        ev.clear();
+    }
+};
+
 // host-side phase timer (IPCG_DEBUG_TIMING=1): where a call's wall time goes
 struct PhaseTimer {
     bool on = getenv("IPCG_DEBUG_TIMING") != nullptr;
@@ -286,6 +336,8 @@ ipcg_archive *compress_impl(ipcg_ctx *c, int scalar, const void *values, int on_
     };
     DBuf small(sizeof(Small), st);
     tm.mark("setup");
+    Timeline tline;
+    tline.mark("start", st);
     Small *sd = small.as<Small>();
     CK(cudaMemsetAsync(small.p, 0, sizeof(Small), st));
     DBuf ord(n * 8, st), bits(n * 8, st);
@@ -299,16 +351,16 @@ ipcg_archive *compress_impl(ipcg_ctx *c, int scalar, const void *values, int on_
     // small levels' latency tails, and those are a few ms.)
     // Only quantization is sequential across levels (level l predicts from the state the
     // coarser levels left).  Each level's lossless stage (bitplanes + deflate) forks onto its
-    // own side stream and the loss tables onto one shared side stream (the per-pass fallback
-    // shares `dev`): the small levels' latency-bound chains (zlib's serial Huffman builds,
-    // single-CTA scans) then run under level 1's throughput-bound kernels.  Everything joins
-    // back into `st` before the results are read.
+    // own side stream and its loss table onto its own highest-priority stream: the small
+    // levels' latency-bound chains (zlib's serial Huffman builds, single-CTA scans) then run
+    // under level 1's throughput-bound kernels.  Everything joins back into `st` before the
+    // results are read.
     // With the per-family profiler on (bench.py's roofline step, never the timed loop) all
     // of it stays on `st`, so each family's CUDA-event span covers only its own kernels.
     c->events_used = 0;
     const bool serial = profiler().enabled;
     auto fork = [&](size_t i) { return serial ? st : side_stream(c, i); };
-    cudaStream_t loss_st = fork(0);
+    cudaEvent_t fb_done = nullptr;  // last per-pass loss fallback (they share `dev`)
     std::vector<DBuf> nbs(L), wss(L), planes(L), outs(L);
     std::vector<uint64_t> pb(L), plane_stride(L), out_stride(L), sink_base(L);
     uint64_t base = 0;
@@ -334,6 +386,7 @@ ipcg_archive *compress_impl(ipcg_ctx *c, int scalar, const void *values, int on_
                 launch_quant_pass(vals, state.p, scalar, cubic, pd, eb, nb, &sd->lowor[li], sink, st);
         }
         tm.mark("quant");
+        tline.mark("q" + std::to_string(level), st);
         // lossless stage.  (No memset: k_bitplanes writes every word below the row length, zero
         // past `count`; the deflate stage never reads a row past its n = ceil(count/8) bytes.)
         cudaStream_t ds = fork(1 + (size_t)li);
@@ -342,38 +395,56 @@ ipcg_archive *compress_impl(ipcg_ctx *c, int scalar, const void *values, int on_
             ProfScope ps("bitplanes", ds, lg.count * 8);
             launch_bitplanes(nb, lg.count, planes[li].as<uint32_t>(), plane_stride[li], ds);
         }
-        cudaEvent_t after_match = pool_event(c);
+        cudaEvent_t after_match = tline.on ? nullptr : pool_event(c);
+        if (tline.on) {
+            CK(cudaEventCreate(&after_match));
+            tline.ev.push_back({"m" + std::to_string(level), after_match});
+        }
         const BackendResults res{sd->backend[li], sd->length[li], sd->crc[li], sd->payload[li]};
         DeflateBatch::run(planes[li].as<uint8_t>(), plane_stride[li] * 4, 32, pb[li], outs[li].as<uint8_t>(),
                           out_stride[li], wss[li].p, res, ds, after_match);
-        // loss table (measure_loss_table): replay per dropped-digit count d, started once this
-        // level's match search is done so it overlaps the latency-bound parse/Huffman phases
-        // instead of competing with the throughput-bound ones (measured: 53 vs 60 ms)
-        if (loss_st != st) {
-            stream_dep(c, st, loss_st);
-            CK(cudaStreamWaitEvent(loss_st, after_match, 0));
+        tline.mark("d" + std::to_string(level), ds);
+        // loss table (measure_loss_table): replay per dropped-digit count d, on the level's own
+        // highest-priority stream, started once this level's match search is done so it
+        // overlaps the latency-bound parse/Huffman phases instead of competing with the
+        // throughput-bound ones.  (One loss stream shared by all levels put level 1's table
+        // behind level 2's, whose match search finishes late under level 1's kernels:
+        // measured 57 ms per compress vs 39 ms without loss tables.)
+        cudaStream_t ls = serial ? st : loss_stream(c, (size_t)li);
+        if (ls != st) {
+            stream_dep(c, st, ls);
+            CK(cudaStreamWaitEvent(ls, after_match, 0));
         }
         {
-            ProfScope psl("loss_table", loss_st, lg.count * 4);
-            if (!launch_loss_fused(nb, G, level, cubic, 2.0 * eb, &sd->lowor[li], sd->raw[li], loss_st)) {
+            ProfScope psl("loss_table", ls, lg.count * 4);
+            if (!launch_loss_fused(nb, G, level, cubic, 2.0 * eb, &sd->lowor[li], sd->raw[li], ls)) {
+                // the per-pass fallback shares `dev` across levels: chain those in order
+                if (fb_done) CK(cudaStreamWaitEvent(ls, fb_done, 0));
                 for (int d = 1; d <= 32; ++d)
                     for (const PassDesc &pd : lg.passes)
-                        launch_loss_pass(nb, dev.as<double>(), pd, cubic, 2.0 * eb, d, &sd->lowor[li], sd->raw[li],
-                                         loss_st);
-                for (const PassDesc &pd : lg.passes) launch_zero_pass(dev.as<double>(), pd, loss_st);
+                        launch_loss_pass(nb, dev.as<double>(), pd, cubic, 2.0 * eb, d, &sd->lowor[li], sd->raw[li], ls);
+                for (const PassDesc &pd : lg.passes) launch_zero_pass(dev.as<double>(), pd, ls);
+                if (ls != st) {
+                    fb_done = pool_event(c);
+                    CK(cudaEventRecord(fb_done, ls));
+                }
             }
-            launch_loss_finalize(sd->raw[li], &sd->lowor[li], sd->delta[li], loss_st);
+            launch_loss_finalize(sd->raw[li], &sd->lowor[li], sd->delta[li], ls);
         }
+        tline.mark("L" + std::to_string(level), ls);
         tm.mark("deflate");
     }
     if (!serial) {
-        stream_dep(c, loss_st, st);
-        for (int li = 0; li < L; ++li) stream_dep(c, side_stream(c, 1 + (size_t)li), st);
+        for (int li = 0; li < L; ++li) {
+            stream_dep(c, loss_stream(c, (size_t)li), st);
+            stream_dep(c, side_stream(c, 1 + (size_t)li), st);
+        }
     }
     Small *sh = static_cast<Small *>(pinned(c, sizeof(Small)));
     tm.mark("enqueue");
     CK(cudaMemcpyAsync(sh, small.p, sizeof(Small), cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
+    tline.print();
     Small hs;
     std::memcpy(&hs, sh, sizeof(Small));
     tm.mark("gpu_wait");
@@ -902,10 +973,12 @@ void ipcg_ctx_destroy(ipcg_ctx *c) {
     cudaSetDevice(c->device);
     if (c->stream) cudaStreamSynchronize(c->stream);
     for (cudaStream_t s : c->side) cudaStreamSynchronize(s);
+    for (cudaStream_t s : c->loss) cudaStreamSynchronize(s);
     c->scratch.release_all(c->own_stream);
     if (c->own_stream) cudaStreamSynchronize(c->own_stream);
     if (c->pinned) cudaFreeHost(c->pinned);
     for (cudaStream_t s : c->side) cudaStreamDestroy(s);
+    for (cudaStream_t s : c->loss) cudaStreamDestroy(s);
     for (cudaEvent_t e : c->events) cudaEventDestroy(e);
     if (c->own_stream) cudaStreamDestroy(c->own_stream);
     delete c;
