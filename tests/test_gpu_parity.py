@@ -156,7 +156,11 @@ def test_backend_encode_matches_zlib(ctx):
     rng = np.random.default_rng(0)
     cases = [bytes(1), bytes(100), bytes(70000), rng.integers(0, 256, 5000, dtype=np.uint8).tobytes(),
              np.packbits((rng.random(8 * 200000) < 0.05).astype(np.uint8), bitorder="little").tobytes(),
-             (b"abcabcabd" * 30000)[:250000]]
+             (b"abcabcabd" * 30000)[:250000],
+             # stored blocks (random stretches) between compressed ones: every later block's bit
+             # position goes through a byte alignment
+             rng.integers(0, 256, 40000, dtype=np.uint8).tobytes() + bytes(60000) +
+             rng.integers(0, 256, 50000, dtype=np.uint8).tobytes() + b"xyz" * 20000]
     for raw in cases:
         (be, payload, crc), = ipc.backend_encode(np.frombuffer(raw, np.uint8), ctx=ctx)
         z = zlib.compress(raw, 6)
