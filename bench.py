@@ -7,7 +7,8 @@ relative eb 1e-1, then refine to 1e-2, 1e-3, 1e-4 (pipeline.hpp:140,260,294).
 `value` = uncompressed GB/s of that cycle with the field and the archive resident in HBM
 (timed by CUDA events on the launching stream, max over ranks); `e2e` = the same cycle
 through the C-ABI with HOST buffers (pinned field in, archive out to host, retrieval from
-the host archive with host outputs), host<->device copies inside the timed region.
+the host archive with host outputs; host-async mode, so each retrieval's copy-out overlaps
+the calls after it), host<->device copies inside the timed region.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config C]
 
@@ -204,6 +205,9 @@ def run_ours(args, ws, rank, local):
     fresh = {}
     for rel in rels:
         plan = ipc.plan_for_error(reader, rel * rng)
+        # warm once: a fresh retrieval of a deeper plan than any refine decoded grows the
+        # context's scratch pool on its first call
+        ipc.reconstruct_field(reader, plan, device=True, keep_session=False)
         t0.record(stream)
         out = ipc.reconstruct_field(reader, plan, device=True, keep_session=False)
         t1.record(stream)
@@ -281,16 +285,25 @@ def run_ours(args, ws, rank, local):
             d2h = size + nbytes * len(rels)
             return o
 
+        # host-async mode: each retrieval's copy-out into host_out runs on the context's copy
+        # stream under the following calls; ctx.synchronize() lands every copy before the
+        # closing event, so all host<->device traffic stays inside the timed region
+        ctx.set_host_async(True)
         step_host()
+        ctx.synchronize()
         torch.cuda.synchronize()
         barrier(ws)
         g0, g1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         g0.record(stream)
-        for _ in range(max(1, args.steps // 2)):
+        for _ in range(args.steps):
             step_host()
+        ctx.synchronize()
         g1.record(stream)
         torch.cuda.synchronize()
-        ems = max_over_ranks(g0.elapsed_time(g1), ws, f"cuda:{local}") / max(1, args.steps // 2)
+        ctx.set_host_async(False)
+        herr = float(np.max(np.abs(host_out.numpy().astype(np.float64) - f.reshape(-1))))
+        assert herr <= eb, f"e2e result violates the error bound: {herr} > {eb}"
+        ems = max_over_ranks(g0.elapsed_time(g1), ws, f"cuda:{local}") / args.steps
         e2e = {"value": round(ws * nbytes / (ems / 1e3) / 1e9, 4), "unit": "GB/s",
                "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h)}
 

@@ -65,6 +65,13 @@ const char *ipcg_last_error(const ipcg_ctx *ctx);
  * stream-ordered on the stream current when they were created, which must outlive them. */
 int ipcg_set_stream(ipcg_ctx *ctx, void *cuda_stream);
 int ipcg_synchronize(ipcg_ctx *ctx);
+/* Host-async mode (off by default; no reference counterpart -- the reference's calls are
+ * synchronous).  When on, ipcg_reconstruct / ipcg_refine with a HOST `out` return once the
+ * values are final on the device; the device->host copy into `out` runs on a context-owned
+ * copy stream and has landed when ipcg_synchronize returns (or the next ipcg_set_* call).
+ * Later calls overlap it; a refine whose `previous` is host memory waits for pending copies
+ * before reading it.  `out` should be page-locked for the copy to be asynchronous. */
+int ipcg_set_host_async(ipcg_ctx *ctx, int enable);
 
 /* compress_field<T> (include/ipcomp/pipeline.hpp:140-223).  `values` is a host or
  * device pointer (values_on_device); the archive is produced device-resident. */

@@ -78,6 +78,7 @@ class Context {
     }
     void set_stream(void *cuda_stream) { check(ipcg_set_stream(get(), cuda_stream)); }
     void synchronize() { check(ipcg_synchronize(get())); }
+    void set_host_async(bool enable) { check(ipcg_set_host_async(get(), enable ? 1 : 0)); }
 
    private:
     struct Del {

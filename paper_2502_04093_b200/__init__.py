@@ -75,6 +75,7 @@ def library() -> C.CDLL:
         "ipcg_last_error": (C.c_char_p, [vp]),
         "ipcg_set_stream": (i32, [vp, vp]),
         "ipcg_synchronize": (i32, [vp]),
+        "ipcg_set_host_async": (i32, [vp, i32]),
         "ipcg_compress": (i32, [vp, i32, vp, i32, P(u64), i32, dbl, i32, i32, u64, P(vp)]),
         "ipcg_archive_open": (i32, [vp, vp, u64, i32, P(vp)]),
         "ipcg_archive_index": (i32, [vp, P(Index)]),
@@ -111,6 +112,7 @@ def library() -> C.CDLL:
 
 EXPORTED_SYMBOLS = [
     "ipcg_ctx_create", "ipcg_ctx_destroy", "ipcg_last_error", "ipcg_set_stream", "ipcg_synchronize",
+    "ipcg_set_host_async",
     "ipcg_compress", "ipcg_archive_open", "ipcg_archive_index", "ipcg_archive_size", "ipcg_archive_write",
     "ipcg_archive_payload_bytes_read", "ipcg_archive_free", "ipcg_reconstruct", "ipcg_refine",
     "ipcg_session_create", "ipcg_session_levels", "ipcg_session_archive_crc", "ipcg_session_planes_loaded",
@@ -150,6 +152,11 @@ class Context:
 
     def synchronize(self) -> None:
         self.check(library().ipcg_synchronize(self.h))
+
+    def set_host_async(self, enable: bool = True) -> None:
+        """Host-async mode (ipcg_set_host_async): retrievals into host buffers return once the
+        values are final on the device; the copy-out lands by the next synchronize()."""
+        self.check(library().ipcg_set_host_async(self.h, 1 if enable else 0))
 
     def kernel_launches(self) -> int:
         return int(library().ipcg_kernel_launches(self.h))

@@ -1172,8 +1172,7 @@ void inflate_batch_host(const std::vector<InflateJob> &jobs, int *status_dev, De
         CKL();
     }
     unsigned long long hc = 0;
-    CK(cudaMemcpyAsync(&hc, ncand, 8, cudaMemcpyDeviceToHost, st));
-    CK(cudaStreamSynchronize(st));
+    readback(&hc, ncand, 8, st);
     const uint64_t nc = std::min<uint64_t>(hc, cand_cap);
     uint32_t *pool = static_cast<uint32_t *>(alloc.get(std::max<uint64_t>(nc, 1) * MAXSYM * 4, st));
     uint32_t *ckpt = static_cast<uint32_t *>(alloc.get(std::max<uint64_t>(nc, 1) * NCKPT * 4, st));
@@ -1191,8 +1190,7 @@ void inflate_batch_host(const std::vector<InflateJob> &jobs, int *status_dev, De
     {
         ProfScope ps("inflate.emit", st, max_dst * n);
         std::vector<JobMeta> hm(n);
-        CK(cudaMemcpyAsync(hm.data(), md, n * sizeof(JobMeta), cudaMemcpyDeviceToHost, st));
-        CK(cudaStreamSynchronize(st));
+        readback(hm.data(), md, n * sizeof(JobMeta), st);
         uint64_t maxseg = 1;
         for (const JobMeta &m : hm) maxseg = std::max<uint64_t>(maxseg, m.nseg);
         if (getenv("IPCG_DEBUG_INFLATE")) {

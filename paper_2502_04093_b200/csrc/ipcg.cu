@@ -32,6 +32,42 @@
 
 using namespace ipcg;
 
+namespace ipcg {
+namespace rb {
+__global__ void k_readback(const uint8_t *__restrict__ src, uint8_t *__restrict__ dst, size_t n) {
+    for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x)
+        dst[i] = src[i];
+}
+struct MappedBuf {  // grow-only mapped page-locked staging, one per host thread
+    void *h = nullptr;
+    size_t cap = 0;
+    ~MappedBuf() {
+        if (h) cudaFreeHost(h);
+    }
+};
+}  // namespace rb
+
+void readback(void *dst, const void *src_dev, size_t bytes, cudaStream_t st) {
+    if (!bytes) return;
+    thread_local rb::MappedBuf mb;
+    if (bytes > mb.cap) {
+        CK(cudaStreamSynchronize(st));
+        if (mb.h) CK(cudaFreeHost(mb.h));
+        mb.h = nullptr;
+        const size_t cap = std::max<size_t>(bytes, 64 << 10);
+        CK(cudaHostAlloc(&mb.h, cap, cudaHostAllocMapped));
+        mb.cap = cap;
+    }
+    void *d = nullptr;
+    CK(cudaHostGetDevicePointer(&d, mb.h, 0));
+    rb::k_readback<<<(unsigned)std::min<size_t>((bytes + 255) / 256, 64), 256, 0, st>>>(
+        static_cast<const uint8_t *>(src_dev), static_cast<uint8_t *>(d), bytes);
+    CKL();
+    CK(cudaStreamSynchronize(st));
+    std::memcpy(dst, mb.h, bytes);
+}
+}  // namespace ipcg
+
 struct ipcg_ctx {
     int device = 0;
     cudaStream_t stream = nullptr;  // all work is ordered on this stream (forks join back)
@@ -44,6 +80,20 @@ struct ipcg_ctx {
     std::string err;
     void *pinned = nullptr;
     size_t pinned_cap = 0;
+    // host-async mode (ipcg_set_host_async): a retrieval's device->host copy of its values
+    // runs on `copy` from a ring of device output buffers, so the next call's kernels (and
+    // its host->device uploads: PCIe is full duplex) overlap it
+    bool host_async = false;
+    cudaStream_t copy = nullptr;
+    struct OutSlot {
+        void *p = nullptr;
+        size_t cap = 0;
+        cudaEvent_t ready = nullptr, done = nullptr;  // values final (on stream) / copied out
+    };
+    std::vector<OutSlot> ring;
+    size_t ring_next = 0;
+    cudaEvent_t copy_tail = nullptr;  // the last copy enqueued
+    bool copy_pending = false;
 };
 
 struct ipcg_archive {
@@ -158,6 +208,36 @@ void *pinned(ipcg_ctx *c, size_t bytes) {
         c->pinned_cap = cap;
     }
     return c->pinned;
+}
+
+// next output buffer of the host-async ring (grown to `bytes` once its last copy is done)
+constexpr size_t RING_SLOTS = 4;
+ipcg_ctx::OutSlot &out_slot(ipcg_ctx *c, size_t bytes) {
+    if (c->ring.empty()) {
+        c->ring.resize(RING_SLOTS);
+        for (auto &sl : c->ring) {
+            CK(cudaEventCreateWithFlags(&sl.ready, cudaEventDisableTiming));
+            CK(cudaEventCreateWithFlags(&sl.done, cudaEventDisableTiming));
+        }
+    }
+    ipcg_ctx::OutSlot &sl = c->ring[c->ring_next];
+    c->ring_next = (c->ring_next + 1) % c->ring.size();
+    if (sl.cap < bytes) {
+        CK(cudaEventSynchronize(sl.done));
+        if (sl.p) CK(cudaFree(sl.p));
+        sl.p = nullptr;
+        CK(cudaMalloc(&sl.p, bytes));
+        sl.cap = bytes;
+    }
+    return sl;
+}
+
+// host-async copies issued so far have landed in host memory
+void drain_copies(ipcg_ctx *c) {
+    if (c->copy && c->copy_pending) {
+        CK(cudaStreamSynchronize(c->copy));
+        c->copy_pending = false;
+    }
 }
 
 thread_local std::string g_host_err;  // errors of context-free (host-only) calls
@@ -442,8 +522,7 @@ ipcg_archive *compress_impl(ipcg_ctx *c, int scalar, const void *values, int on_
     }
     Small *sh = static_cast<Small *>(pinned(c, sizeof(Small)));
     tm.mark("enqueue");
-    CK(cudaMemcpyAsync(sh, small.p, sizeof(Small), cudaMemcpyDeviceToHost, st));
-    CK(cudaStreamSynchronize(st));
+    readback(sh, small.p, sizeof(Small), st);
     tline.print();
     Small hs;
     std::memcpy(&hs, sh, sizeof(Small));
@@ -673,8 +752,7 @@ void retrieve_impl(ipcg_ctx *c, ipcg_archive *a, int scalar, const int *k, void 
             k_copy_headers<<<(unsigned)((hoffs.size() + 127) / 128), 128, 0, st>>>(src_dev, ho.as<uint64_t>(),
                                                                                 (int)hoffs.size(), hd.as<uint8_t>());
             CKL();
-            CK(cudaMemcpyAsync(headers.data(), hd.p, headers.size(), cudaMemcpyDeviceToHost, st));
-            CK(cudaStreamSynchronize(st));
+            readback(headers.data(), hd.p, headers.size(), st);
         }
     } else {
         // straight from the caller's buffer (no host-side staging copy): spans that are
@@ -793,8 +871,7 @@ void retrieve_impl(ipcg_ctx *c, ipcg_archive *a, int scalar, const int *k, void 
             crc32_batch(pd.as<const uint8_t *>(), ld.as<uint64_t>(), (int)R, maxp, crcs.as<uint32_t>(), crcws.p, cw, st);
         }
         std::vector<uint32_t> hcrc(R);
-        CK(cudaMemcpyAsync(hcrc.data(), crcs.p, R * 4, cudaMemcpyDeviceToHost, st));
-        CK(cudaStreamSynchronize(st));
+        readback(hcrc.data(), crcs.p, R * 4, st);
         for (size_t i = 0; i < R; ++i)
             if (hcrc[i] != refs[i].crc) throw Error(ERUNTIME, "block checksum mismatch");
     tm.mark("crc");
@@ -830,8 +907,7 @@ void retrieve_impl(ipcg_ctx *c, ipcg_archive *a, int scalar, const int *k, void 
                 k_compare<<<(unsigned)cmp.size(), 256, 0, st>>>(cd.as<CopyDesc>(), (int)cmp.size(), diff.as<int>());
                 CKL();
                 std::vector<int> hd(cmp.size());
-                CK(cudaMemcpyAsync(hd.data(), diff.p, cmp.size() * 4, cudaMemcpyDeviceToHost, st));
-                CK(cudaStreamSynchronize(st));
+                readback(hd.data(), diff.p, cmp.size() * 4, st);
                 for (size_t q = 0; q < pairs.size(); ++q)
                     if (!hd[q]) rep_of[pairs[q].first] = pairs[q].second;
             }
@@ -851,8 +927,7 @@ void retrieve_impl(ipcg_ctx *c, ipcg_archive *a, int scalar, const int *k, void 
                 inflate_batch_host(todo, sd.as<int>(), tmp, st);
             }
             std::vector<int> status(todo.size());
-            CK(cudaMemcpyAsync(status.data(), sd.p, todo.size() * 4, cudaMemcpyDeviceToHost, st));
-            CK(cudaStreamSynchronize(st));
+            readback(status.data(), sd.p, todo.size() * 4, st);
             for (int s : status)
                 if (s) throw Error(ERUNTIME, "deflate backend failed to decompress block");
         }
@@ -870,9 +945,16 @@ void retrieve_impl(ipcg_ctx *c, ipcg_archive *a, int scalar, const int *k, void 
     // ---- merge + reconstruct, coarsest first
     DBuf out_buf;
     void *state = out;
+    ipcg_ctx::OutSlot *slot = nullptr;
     if (!out_on_dev) {
-        out_buf = DBuf(n * w, st);
-        state = out_buf.p;
+        if (c->host_async) {
+            slot = &out_slot(c, n * w);
+            CK(cudaStreamWaitEvent(st, slot->done, 0));  // its previous copy-out has finished
+            state = slot->p;
+        } else {
+            out_buf = DBuf(n * w, st);
+            state = out_buf.p;
+        }
     }
     // refine_field starts from `previous` and replays the progressive levels (pipeline.hpp:
     // 310-349); the replay rewrites every point of those levels, so `previous` only
@@ -880,6 +962,8 @@ void retrieve_impl(ipcg_ctx *c, ipcg_archive *a, int scalar, const int *k, void 
     bool keeps_previous = false;
     for (int l = 0; l < L; ++l) keeps_previous |= !lv[l].active;
     if (refine && keeps_previous) {
+        // `previous` may be the host destination of a copy-out still in flight
+        if (!prev_on_dev && c->copy_pending) CK(cudaStreamWaitEvent(st, c->copy_tail, 0));
         CK(cudaMemcpyAsync(state, previous, n * w, prev_on_dev ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, st));
     }
     ipcg_session *ns = new ipcg_session;
@@ -921,7 +1005,16 @@ void retrieve_impl(ipcg_ctx *c, ipcg_archive *a, int scalar, const int *k, void 
             if (level <= ix.progressive_levels) ns->merged[li] = merged;
             else scratch_put(merged, st);
         }
-        if (!out_on_dev) CK(cudaMemcpyAsync(out, state, n * w, cudaMemcpyDeviceToHost, st));
+        if (slot) {
+            CK(cudaEventRecord(slot->ready, st));
+            CK(cudaStreamWaitEvent(c->copy, slot->ready, 0));
+            CK(cudaMemcpyAsync(out, state, n * w, cudaMemcpyDeviceToHost, c->copy));
+            CK(cudaEventRecord(slot->done, c->copy));
+            CK(cudaEventRecord(c->copy_tail, c->copy));
+            c->copy_pending = true;
+        } else if (!out_on_dev) {
+            CK(cudaMemcpyAsync(out, state, n * w, cudaMemcpyDeviceToHost, st));
+        }
         CK(cudaStreamSynchronize(st));
     tm.mark("recon");
     } catch (...) {
@@ -971,6 +1064,14 @@ int ipcg_ctx_create(int device, ipcg_ctx **out) {
 void ipcg_ctx_destroy(ipcg_ctx *c) {
     if (!c) return;
     cudaSetDevice(c->device);
+    if (c->copy) cudaStreamSynchronize(c->copy);
+    for (auto &sl : c->ring) {
+        if (sl.p) cudaFree(sl.p);
+        cudaEventDestroy(sl.ready);
+        cudaEventDestroy(sl.done);
+    }
+    if (c->copy_tail) cudaEventDestroy(c->copy_tail);
+    if (c->copy) cudaStreamDestroy(c->copy);
     if (c->stream) cudaStreamSynchronize(c->stream);
     for (cudaStream_t s : c->side) cudaStreamSynchronize(s);
     for (cudaStream_t s : c->loss) cudaStreamSynchronize(s);
@@ -988,13 +1089,28 @@ const char *ipcg_last_error(const ipcg_ctx *c) { return c ? c->err.c_str() : g_h
 
 int ipcg_set_stream(ipcg_ctx *c, void *s) {
     return guarded(c, [&] {
+        drain_copies(c);
         CK(cudaStreamSynchronize(c->stream));
         c->stream = s ? static_cast<cudaStream_t>(s) : c->own_stream;
     });
 }
 
 int ipcg_synchronize(ipcg_ctx *c) {
-    return guarded(c, [&] { CK(cudaStreamSynchronize(c->stream)); });
+    return guarded(c, [&] {
+        drain_copies(c);
+        CK(cudaStreamSynchronize(c->stream));
+    });
+}
+
+int ipcg_set_host_async(ipcg_ctx *c, int enable) {
+    return guarded(c, [&] {
+        drain_copies(c);
+        if (enable && !c->copy) {
+            CK(cudaStreamCreateWithFlags(&c->copy, cudaStreamNonBlocking));
+            CK(cudaEventCreateWithFlags(&c->copy_tail, cudaEventDisableTiming));
+        }
+        c->host_async = enable != 0;
+    });
 }
 
 int ipcg_compress(ipcg_ctx *c, int scalar, const void *values, int on_dev, const uint64_t *dims, int nd, double eb,

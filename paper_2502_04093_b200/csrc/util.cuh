@@ -39,6 +39,12 @@ inline unsigned long long &launch_counter() {
         CK(cudaGetLastError());            \
     } while (0)
 
+// Small device->host result reads on the hot path (sizes, CRCs, status words) go through
+// mapped page-locked memory: a kernel stores them over PCIe, then the stream is synchronized.
+// A cudaMemcpy D2H would queue on the copy engine behind any bulk transfer in flight (a
+// host-async copy-out of 512 MiB holds it ~10 ms).  Synchronizes `st`; defined in ipcg.cu.
+void readback(void *dst, const void *src_dev, size_t bytes, cudaStream_t st);
+
 // Optional per-kernel-family timing: CUDA events recorded on the launching stream
 // around each family (enabled by ipcg_profile_enable); read back by ipcg_profile_read.
 struct Profiler {

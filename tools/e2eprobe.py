@@ -18,12 +18,18 @@ host_out = torch.empty(n, dtype=torch.float32).pin_memory()
 host_arch = None
 
 
+ASYNC = len(sys.argv) > 1 and sys.argv[1] == "async"
+if ASYNC:
+    ctx.set_host_async(True)
+
+
 def step(report):
     global host_arch
     T = [time.time()]
     names = []
     def mark(s):
-        torch.cuda.synchronize()
+        if not ASYNC:
+            torch.cuda.synchronize()
         T.append(time.time()); names.append(s)
     r = ipc.compress_field(host_f, dims, eb, c["interp"], ctx=ctx); mark("compress(host)")
     size = r.size()
@@ -36,6 +42,8 @@ def step(report):
     o = ipc.reconstruct_field(rh, ipc.plan_for_error(rh, rels[0] * rng_), out=host_out); mark(f"reconstruct {rels[0]}")
     for rel in rels[1:]:
         o = ipc.refine_field(rh, o.session, host_out, ipc.plan_for_error(rh, rel * rng_), out=host_out); mark(f"refine {rel}")
+    if ASYNC:
+        ctx.synchronize(); mark("synchronize")
     if report:
         tot = T[-1] - T[0]
         print(f"step {tot*1e3:.1f} ms  e2e {f.nbytes/tot/1e9:.3f} GB/s")
