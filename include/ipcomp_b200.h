@@ -110,6 +110,26 @@ int ipcg_session_planes_loaded(const ipcg_session *s, int *k_out);
 uint64_t ipcg_session_count(const ipcg_session *s, int level);
 int ipcg_session_merged(ipcg_ctx *ctx, const ipcg_session *s, int level, uint32_t *dst, int dst_on_device);
 void ipcg_session_free(ipcg_session *s);
+/* write_session (src/session.cpp:8-24): the session file, each progressive level's merged
+ * codewords deflated on the device.  dst is host or device memory of `capacity` bytes;
+ * *size_out receives the file size (also when the call fails with IPCG_EINVAL because
+ * capacity is too small or dst is NULL -- a size query).  ipcg_session_write_bound gives a
+ * capacity that always suffices. */
+uint64_t ipcg_session_write_bound(const ipcg_session *s);
+int ipcg_session_write(ipcg_ctx *ctx, const ipcg_session *s, void *dst, int dst_on_device, uint64_t capacity,
+                       uint64_t *size_out);
+/* read_session (src/session.cpp:26-61): parse + CRC-check + inflate on the device into a
+ * device-resident session bound to `a`; errors carry the reference's messages. */
+int ipcg_session_read(ipcg_ctx *ctx, const ipcg_archive *a, const void *bytes, uint64_t size, int on_device,
+                      ipcg_session **out);
+
+/* compute_metrics<T> (pipeline.hpp:354-372): max pointwise error, MSE and PSNR of `decoded`
+ * against `original` (n elements of f32/f64 each, host or device), one device pass.  max_error
+ * is exact; mse/psnr differ from the reference's left-to-right double sum only by summation
+ * order.  Sizes differing -> IPCG_EINVAL "metrics inputs differ in size". */
+int ipcg_compute_metrics(ipcg_ctx *ctx, int scalar, const void *original, int original_on_device, uint64_t n_original,
+                         const void *decoded, int decoded_on_device, uint64_t n_decoded, double *max_error,
+                         double *mse, double *psnr);
 
 /* planner (src/planner.cpp:30-290) over the index */
 int ipcg_plan_for_error(ipcg_ctx *ctx, const ipcg_archive *a, double max_error, int *k_out);

@@ -113,6 +113,18 @@ def _setup(lib: C.CDLL, pfx: str) -> C.CDLL:
     f.argtypes = [C.c_void_p, C.c_uint64, C.c_int, C.POINTER(u8p), C.POINTER(C.c_uint64), C.POINTER(C.c_int),
                   C.POINTER(C.c_uint32)]
     getattr(lib, pfx + "free").argtypes = [C.c_void_p]
+    f = getattr(lib, pfx + "compute_metrics")
+    f.restype = C.c_int
+    f.argtypes = [C.c_int, C.c_void_p, C.c_void_p, C.c_uint64, C.POINTER(C.c_double)]
+    f = getattr(lib, pfx + "read_session")
+    f.restype = C.c_int
+    f.argtypes = [C.c_void_p, C.c_uint64, C.c_void_p, C.c_uint64, C.POINTER(C.c_int),
+                  C.POINTER(C.POINTER(C.c_uint32)), C.c_char_p, C.c_int]
+    if pfx == "ref_":
+        lib.ref_write_session.restype = C.c_int
+        lib.ref_write_session.argtypes = [C.c_void_p, C.c_uint64, C.POINTER(C.c_int),
+                                          C.POINTER(C.POINTER(C.c_uint32)), C.POINTER(u8p), C.POINTER(C.c_uint64),
+                                          C.c_char_p, C.c_int]
     if pfx == "orc_":
         lib.orc_trace_free.argtypes = [C.POINTER(Trace)]
         lib.orc_archive_info.restype = C.c_int
@@ -251,6 +263,49 @@ class Oracle:
                out.ctypes.data, merged, C.byref(loaded), err, 512)
         self._err(rc, err)
         return out, self._collect_merged(archive, merged, L), loaded.value
+
+    def write_session(self, archive: bytes, session_k, session_merged) -> bytes:
+        """write_session (session.cpp:8-24) of the session {k, merged} bound to `archive`."""
+        L = archive_levels(archive)
+        sk = (C.c_int * L)(*session_k)
+        keep = []
+        sm = (C.POINTER(C.c_uint32) * MAX_LEVELS)()
+        for li, m in enumerate(session_merged):
+            if m is not None:
+                a = np.ascontiguousarray(m, dtype=np.uint32)
+                keep.append(a)
+                sm[li] = a.ctypes.data_as(C.POINTER(C.c_uint32))
+        out = C.POINTER(C.c_uint8)()
+        size = C.c_uint64()
+        if self.pfx == "ref_":
+            err = C.create_string_buffer(512)
+            rc = self.lib.ref_write_session(archive, len(archive), sk, sm, C.byref(out), C.byref(size), err, 512)
+            self._err(rc, err)
+        else:
+            counts = (C.c_uint64 * MAX_LEVELS)(*archive_counts(archive))
+            self.lib.orc_write_session(self.info(archive).identity, L, sk, sm, counts, C.byref(out), C.byref(size))
+        data = C.string_at(out, size.value)
+        getattr(self.lib, self.pfx + "free")(out)
+        return data
+
+    def read_session(self, archive: bytes, data: bytes):
+        """read_session (session.cpp:26-61) -> (planes_loaded, merged per level or None)."""
+        L = archive_levels(archive)
+        k = (C.c_int * MAX_LEVELS)()
+        merged = (C.POINTER(C.c_uint32) * MAX_LEVELS)()
+        err = C.create_string_buffer(512)
+        rc = getattr(self.lib, self.pfx + "read_session")(archive, len(archive), data, len(data), k, merged, err, 512)
+        self._err(rc, err)
+        return list(k)[:L], self._collect_merged(archive, merged, L)
+
+    def compute_metrics(self, original: np.ndarray, decoded: np.ndarray):
+        """compute_metrics<T> (pipeline.hpp:354-372) -> (max_error, mse, psnr)."""
+        a, b = np.ascontiguousarray(original), np.ascontiguousarray(decoded)
+        assert a.dtype == b.dtype and a.size == b.size
+        out = (C.c_double * 3)()
+        getattr(self.lib, self.pfx + "compute_metrics")(0 if a.dtype == np.float32 else 1, a.ctypes.data,
+                                                         b.ctypes.data, a.size, out)
+        return tuple(out)
 
     def plan_for_error(self, archive: bytes, max_error: float):
         L = archive_levels(archive)

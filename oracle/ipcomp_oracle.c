@@ -1176,3 +1176,110 @@ int orc_write_session(uint32_t archive_crc, int levels, const int *k, uint32_t *
     *out_size = w.n;
     return E_OK;
 }
+
+/* read_session, session.cpp:26-61 (ByteReader truncation: common.hpp:98; read_block:
+ * backend.cpp:75-86; backend_decode: backend.cpp:55-65).  merged_out[l-1] is malloc'd for
+ * progressive levels, NULL otherwise. */
+int orc_read_session(const uint8_t *archive, uint64_t size, const uint8_t *bytes, uint64_t n, int *k_out,
+                     uint32_t **merged_out, char *err, int errlen) {
+    reader_t rd;
+    int rc = reader_open(&rd, archive, size, err, errlen);
+    if (rc) return rc;
+    const int L = rd.h.levels, lp = rd.h.lp;
+    for (int l = 0; l < ORC_MAX_LEVELS; ++l) merged_out[l] = NULL;
+    const char *trunc = "truncated input while parsing";
+    uint64_t pos = 0;
+#define NEED(k)                                                                         \
+    do {                                                                                \
+        if (n - pos < (uint64_t)(k)) { rc = fail(err, errlen, E_RUNTIME, trunc); goto bad; } \
+    } while (0)
+    NEED(4);
+    if (memcmp(bytes, "IPS1", 4) != 0) { rc = fail(err, errlen, E_RUNTIME, "not a session file: bad magic"); goto bad; }
+    pos = 4;
+    NEED(4);
+    if ((uint32_t)rd_le(bytes + pos, 4) != rd.identity) {
+        rc = fail(err, errlen, E_RUNTIME, "session does not belong to this archive");
+        goto bad;
+    }
+    pos += 4;
+    for (int level = L; level >= 1; --level) {
+        NEED(1);
+        const int k = bytes[pos++];
+        k_out[level - 1] = k;
+        if (k > 32) { rc = fail(err, errlen, E_RUNTIME, "session plane count out of range"); goto bad; }
+        if (level > lp && k != 32) { rc = fail(err, errlen, E_RUNTIME, "session has partial non-progressive level"); goto bad; }
+        NEED(1);
+        const int backend = bytes[pos];
+        pos += 1;
+        if (backend > 1) { rc = fail(err, errlen, E_RUNTIME, "unknown backend id"); goto bad; }
+        NEED(8);
+        const uint64_t raw_bits = rd_le(bytes + pos, 8);
+        pos += 8;
+        NEED(8);
+        const uint64_t plen = rd_le(bytes + pos, 8);
+        pos += 8;
+        NEED(4);
+        const uint32_t crc = (uint32_t)rd_le(bytes + pos, 4);
+        pos += 4;
+        NEED(plen);
+        const uint8_t *payload = bytes + pos;
+        pos += plen;
+        if (orc_crc32(payload, plen) != crc) { rc = fail(err, errlen, E_RUNTIME, "block checksum mismatch"); goto bad; }
+        const uint64_t rb = (raw_bits + 7) / 8;
+        uint8_t *raw = (uint8_t *)malloc(rb ? rb : 1);
+        if (backend == 0) {
+            if (plen != rb) { free(raw); rc = fail(err, errlen, E_RUNTIME, "identity block has wrong length"); goto bad; }
+            memcpy(raw, payload, rb);
+        } else {
+            uLongf dl = (uLongf)rb;
+            uint8_t dummy;
+            const int zrc = uncompress(rb ? raw : &dummy, &dl, payload, (uLong)plen);
+            if (zrc != Z_OK || dl != rb) {
+                free(raw);
+                rc = fail(err, errlen, E_RUNTIME, "deflate backend failed to decompress block");
+                goto bad;
+            }
+        }
+        if (level <= lp) {
+            const uint64_t count = rd.recs[level - 1].count;
+            if (rb != count * 4) { free(raw); rc = fail(err, errlen, E_RUNTIME, "session codeword array has wrong length"); goto bad; }
+            uint32_t *m = (uint32_t *)malloc(count * 4 + 4);
+            for (uint64_t i = 0; i < count; ++i) m[i] = (uint32_t)rd_le(raw + 4 * i, 4);
+            merged_out[level - 1] = m;
+        } else if (rb != 0) {
+            free(raw);
+            rc = fail(err, errlen, E_RUNTIME, "session stores codewords for a non-progressive level");
+            goto bad;
+        }
+        free(raw);
+    }
+    if (pos != n) { rc = fail(err, errlen, E_RUNTIME, "session file has trailing bytes"); goto bad; }
+    return E_OK;
+#undef NEED
+bad:
+    for (int l = 0; l < ORC_MAX_LEVELS; ++l) {
+        free(merged_out[l]);
+        merged_out[l] = NULL;
+    }
+    return rc;
+}
+
+/* compute_metrics<T>, pipeline.hpp:354-372 (left-to-right double sum, std::max/std::min
+ * semantics: a NaN operand never replaces the running value). out = {max_error, mse, psnr} */
+int orc_compute_metrics(int scalar, const void *original, const void *decoded, uint64_t n, double *out) {
+    double maxe = 0.0, lo = INFINITY, hi = -INFINITY, sq = 0.0;
+    for (uint64_t i = 0; i < n; ++i) {
+        const double a = scalar == 0 ? (double)((const float *)original)[i] : ((const double *)original)[i];
+        const double b = scalar == 0 ? (double)((const float *)decoded)[i] : ((const double *)decoded)[i];
+        const double diff = a - b;
+        const double ad = fabs(diff);
+        maxe = maxe < ad ? ad : maxe;
+        sq += diff * diff;
+        lo = a < lo ? a : lo;
+        hi = hi < a ? a : hi;
+    }
+    out[0] = maxe;
+    out[1] = n == 0 ? 0.0 : sq / (double)n;
+    out[2] = out[1] == 0.0 ? INFINITY : 20.0 * log10((hi - lo) / sqrt(out[1]));
+    return E_OK;
+}

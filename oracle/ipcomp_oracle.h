@@ -89,6 +89,10 @@ uint32_t orc_crc32(const uint8_t *p, uint64_t n);
 /* session file (session.cpp) */
 int orc_write_session(uint32_t archive_crc, int levels, const int *k, uint32_t *const *merged,
                       const uint64_t *counts, uint8_t **out, uint64_t *out_size);
+/* compute_metrics (pipeline.hpp:354-372): out = {max_error, mse, psnr} */
+int orc_compute_metrics(int scalar, const void *original, const void *decoded, uint64_t n, double *out);
+int orc_read_session(const uint8_t *archive, uint64_t size, const uint8_t *bytes, uint64_t n, int *k_out,
+                     uint32_t **merged_out, char *err, int errlen);
 
 #ifdef __cplusplus
 }

@@ -12,6 +12,7 @@
 #include <vector>
 
 #include "ipcomp/pipeline.hpp"
+#include "ipcomp/session.hpp"
 
 using namespace ipcomp;
 
@@ -146,6 +147,67 @@ int ref_refine(const uint8_t *archive, uint64_t size, int scalar, const int *ses
         if (scalar == 0) run(float{});
         else run(double{});
     });
+}
+
+// write_session (session.cpp:8-24) of the session {k, merged} bound to `archive`
+int ref_write_session(const uint8_t *archive, uint64_t size, const int *session_k, uint32_t *const *session_merged,
+                      uint8_t **out, uint64_t *out_size, char *err, int errlen) {
+    return guarded(err, errlen, [&] {
+        MemArchive m(archive, size);
+        const auto &h = m.reader.header();
+        RetrievalSession sess;
+        sess.archive_crc = m.reader.identity();
+        sess.level.resize(h.levels);
+        for (int l = 0; l < h.levels; ++l) {
+            sess.level[l].planes_loaded = session_k[l];
+            if (l + 1 <= h.progressive_levels && session_merged[l]) {
+                const auto cnt = m.reader.record(l + 1).count;
+                sess.level[l].merged.assign(session_merged[l], session_merged[l] + cnt);
+            }
+        }
+        std::ostringstream os(std::ios::binary);
+        write_session(os, sess);
+        const std::string b = os.str();
+        *out = static_cast<uint8_t *>(std::malloc(b.size() + 1));
+        std::memcpy(*out, b.data(), b.size());
+        *out_size = b.size();
+    });
+}
+
+// read_session (session.cpp:26-61); merged_out[l] malloc'd for progressive levels
+int ref_read_session(const uint8_t *archive, uint64_t size, const uint8_t *bytes, uint64_t n, int *k_out,
+                     uint32_t **merged_out, char *err, int errlen) {
+    return guarded(err, errlen, [&] {
+        MemArchive m(archive, size);
+        std::string b(reinterpret_cast<const char *>(bytes), n);
+        std::istringstream is(b, std::ios::binary);
+        const RetrievalSession sess = read_session(is, m.reader);
+        for (std::size_t l = 0; l < sess.level.size(); ++l) {
+            k_out[l] = sess.level[l].planes_loaded;
+            const auto &mm = sess.level[l].merged;
+            if (l + 1 > (std::size_t)m.reader.header().progressive_levels) {
+                merged_out[l] = nullptr;
+                continue;
+            }
+            merged_out[l] = static_cast<uint32_t *>(std::malloc(mm.size() * 4 + 4));
+            std::memcpy(merged_out[l], mm.data(), mm.size() * 4);
+        }
+    });
+}
+
+// compute_metrics<T> (pipeline.hpp:354-372)
+int ref_compute_metrics(int scalar, const void *original, const void *decoded, uint64_t n, double *out) {
+    auto run = [&](auto tag) {
+        using T = decltype(tag);
+        const auto m = compute_metrics<T>(std::span<const T>(static_cast<const T *>(original), n),
+                                          std::span<const T>(static_cast<const T *>(decoded), n));
+        out[0] = m.max_error;
+        out[1] = m.mse;
+        out[2] = m.psnr;
+    };
+    if (scalar == 0) run(float{});
+    else run(double{});
+    return 0;
 }
 
 int ref_plan_for_error(const uint8_t *archive, uint64_t size, double max_error, int *k_out, char *err, int errlen) {

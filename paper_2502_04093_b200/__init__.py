@@ -92,6 +92,10 @@ def library() -> C.CDLL:
         "ipcg_session_count": (u64, [vp, i32]),
         "ipcg_session_merged": (i32, [vp, vp, i32, vp, i32]),
         "ipcg_session_free": (None, [vp]),
+        "ipcg_session_write_bound": (u64, [vp]),
+        "ipcg_session_write": (i32, [vp, vp, vp, i32, u64, P(u64)]),
+        "ipcg_session_read": (i32, [vp, vp, vp, u64, i32, P(vp)]),
+        "ipcg_compute_metrics": (i32, [vp, i32, vp, i32, u64, vp, i32, u64, P(dbl), P(dbl), P(dbl)]),
         "ipcg_plan_for_error": (i32, [vp, vp, dbl, P(i32)]),
         "ipcg_plan_for_size": (i32, [vp, vp, u64, P(i32)]),
         "ipcg_bound_for_plan": (dbl, [vp, P(i32)]),
@@ -116,7 +120,8 @@ EXPORTED_SYMBOLS = [
     "ipcg_compress", "ipcg_archive_open", "ipcg_archive_index", "ipcg_archive_size", "ipcg_archive_write",
     "ipcg_archive_payload_bytes_read", "ipcg_archive_free", "ipcg_reconstruct", "ipcg_refine",
     "ipcg_session_create", "ipcg_session_levels", "ipcg_session_archive_crc", "ipcg_session_planes_loaded",
-    "ipcg_session_count", "ipcg_session_merged", "ipcg_session_free", "ipcg_plan_for_error",
+    "ipcg_session_count", "ipcg_session_merged", "ipcg_session_free",
+    "ipcg_session_write_bound", "ipcg_session_write", "ipcg_session_read", "ipcg_compute_metrics", "ipcg_plan_for_error",
     "ipcg_plan_for_size", "ipcg_bound_for_plan", "ipcg_plan_payload_bytes", "ipcg_backend_encode",
     "ipcg_kernel_launches", "ipcg_profile_enable", "ipcg_profile_read", "ipcg_backend_decode",
 ]
@@ -374,12 +379,41 @@ class RetrievalSession:
         reader.ctx.check(library().ipcg_session_create(reader.ctx.h, reader.h, k, arr, C.byref(h)))
         return cls(h, reader.ctx)
 
+    def to_bytes(self) -> bytes:
+        """write_session (session.cpp:8-24); codewords deflated on the GPU."""
+        return write_session(self)
+
     def __del__(self):
         try:
             if getattr(self, "h", None) and _lib is not None:
                 _lib.ipcg_session_free(self.h)
         except Exception:
             pass
+
+
+def write_session(session: RetrievalSession, dst=None) -> bytes | int:
+    """write_session (session.cpp:8-24).  Returns the file bytes, or, with `dst` (a host or
+    device buffer: numpy array / torch tensor), writes into it and returns the size."""
+    lib = library()
+    ctx = session.ctx
+    size = C.c_uint64()
+    if dst is None:
+        buf = np.empty(max(1, int(lib.ipcg_session_write_bound(session.h))), np.uint8)
+        ctx.check(lib.ipcg_session_write(ctx.h, session.h, C.c_void_p(buf.ctypes.data), 0, buf.nbytes,
+                                         C.byref(size)))
+        return buf[:size.value].tobytes()
+    addr, on_dev, nbytes = _ptr(dst)
+    ctx.check(lib.ipcg_session_write(ctx.h, session.h, C.c_void_p(addr), on_dev, nbytes, C.byref(size)))
+    return int(size.value)
+
+
+def read_session(data, reader: "ArchiveReader") -> RetrievalSession:
+    """read_session (session.cpp:26-61): `data` is bytes or a host/device buffer."""
+    addr, on_dev, nbytes = _ptr(data)
+    h = C.c_void_p()
+    reader.ctx.check(library().ipcg_session_read(reader.ctx.h, reader.h, C.c_void_p(addr), nbytes, on_dev,
+                                                 C.byref(h)))
+    return RetrievalSession(h, reader.ctx)
 
 
 @dataclass
@@ -444,6 +478,29 @@ def refine_field(reader: ArchiveReader, session: RetrievalSession, previous, pla
     for l in range(1, reader._ix.progressive_levels + 1):
         visits[l - 1] = 1
     return Retrieved(out, s, ReconstructStats(visits, int(loaded.value)))
+
+
+@dataclass
+class FieldMetrics:
+    """FieldMetrics (pipeline.hpp:49-53)."""
+    max_error: float
+    mse: float
+    psnr: float
+
+
+def compute_metrics(original, decoded, ctx: Context | None = None) -> FieldMetrics:
+    """compute_metrics<T> (pipeline.hpp:354-372) on the GPU; numpy arrays or torch tensors."""
+    ctx = ctx or Context.default()
+    pa, da, na = _ptr(original)
+    pb, db, nb = _ptr(decoded)
+    sa, sb = _scalar_of(original), _scalar_of(decoded)
+    if sa != sb:
+        raise InvalidArgument("metrics inputs differ in scalar type")
+    w = 4 if sa == 0 else 8
+    m, e, p = C.c_double(), C.c_double(), C.c_double()
+    ctx.check(library().ipcg_compute_metrics(ctx.h, sa, C.c_void_p(pa), da, na // w, C.c_void_p(pb), db, nb // w,
+                                             C.byref(m), C.byref(e), C.byref(p)))
+    return FieldMetrics(m.value, e.value, p.value)
 
 
 # ------------------------------------------------------------------ planner

@@ -47,6 +47,8 @@ struct MappedBuf {  // grow-only mapped page-locked staging, one per host thread
 };
 }  // namespace rb
 
+void compute_metrics_device(int scalar, const void *a, const void *b, uint64_t n, double out[3], cudaStream_t st);
+
 void readback(void *dst, const void *src_dev, size_t bytes, cudaStream_t st) {
     if (!bytes) return;
     thread_local rb::MappedBuf mb;
@@ -986,7 +988,7 @@ void retrieve_impl(ipcg_ctx *c, ipcg_archive *a, int scalar, const int *k, void 
             }
             const uint64_t count = ix.records[li].count;
             uint32_t *merged = nullptr;
-            merged = static_cast<uint32_t *>(scratch_get(std::max<uint64_t>(count, 1) * 4, st));
+            merged = static_cast<uint32_t *>(scratch_get(std::max<uint64_t>(count, 1) * 4 + 16, st));
             const uint32_t *min = refine ? prev_sess->merged[li] : nullptr;
             {
                 ProfScope ps("merge", st, count * 4 + (uint64_t)(p.p1 - p.p0) * ((count + 7) / 8));
@@ -1202,7 +1204,7 @@ int ipcg_session_create(ipcg_ctx *c, const ipcg_archive *a, const int *planes_lo
             s->count[l] = a->ix.records[l].count;
             if (l + 1 <= s->lp && merged && merged[l]) {
                 const uint64_t cnt = s->count[l];
-                s->merged[l] = static_cast<uint32_t *>(c->scratch.get(std::max<uint64_t>(cnt, 1) * 4, c->stream));
+                s->merged[l] = static_cast<uint32_t *>(c->scratch.get(std::max<uint64_t>(cnt, 1) * 4 + 16, c->stream));
                 CK(cudaMemcpyAsync(s->merged[l], merged[l], cnt * 4, cudaMemcpyHostToDevice, c->stream));
                 CK(cudaStreamSynchronize(c->stream));
             }
@@ -1241,6 +1243,271 @@ void ipcg_session_free(ipcg_session *s) {
             else cudaFreeAsync(s->merged[l], s->owner);
         }
     delete s;
+}
+
+// ------------------------------------------------------------------ session file
+// write_session / read_session (src/session.cpp:8-61): "IPS1", u32 archive identity, then per
+// level (coarsest first) u8 planes_loaded + one backend block (backend.cpp:67-86) holding the
+// level's merged codewords as u32 little-endian -- the device layout of the session's arrays,
+// so they are deflated (DeflateBatch, zlib-1.3-exact) and inflated in place on the GPU.
+uint64_t ipcg_session_write_bound(const ipcg_session *s) {
+    if (!s) return 0;
+    uint64_t b = 8;
+    for (int l = 0; l < s->levels; ++l) b += 1 + 21 + (s->merged[l] ? s->count[l] * 4 : 0);
+    return b;
+}
+
+int ipcg_session_write(ipcg_ctx *c, const ipcg_session *s, void *dst, int dst_on_device, uint64_t capacity,
+                       uint64_t *size_out) {
+    return guarded(c, [&] {
+        if (!s) throw Error(EINVAL_, "session is null");
+        cudaStream_t st = c->stream;
+        const int L = s->levels;
+        struct Enc {
+            uint8_t be = 0;
+            uint64_t raw = 0, len = 0;
+            uint32_t crc = 0;
+            const uint8_t *payload = nullptr;  // device
+        };
+        std::vector<Enc> enc(L);
+        std::vector<DBuf> keep;  // deflate outputs, alive until the copy-out below
+        for (int l = L; l >= 1; --l) {
+            const uint32_t *m = s->merged[l - 1];
+            if (!m) continue;
+            Enc &e = enc[l - 1];
+            const uint64_t n = s->count[l - 1] * 4;
+            e.raw = n;
+            if (n == 0) continue;  // empty identity block, crc32("") = 0
+            const uint64_t out_stride = round_up(n + 16, 16);
+            keep.emplace_back(out_stride, st);
+            DBuf ws(DeflateBatch::workspace_bytes(1, n), st), be(16, st), ln(16, st), cr(16, st), pl(16, st);
+            const BackendResults res{be.as<uint8_t>(), ln.as<uint64_t>(), cr.as<uint32_t>(), pl.as<const uint8_t *>()};
+            // merged arrays carry >= 16 bytes of padding (session allocations), as DeflateBatch reads padded rows
+            DeflateBatch::run(reinterpret_cast<const uint8_t *>(m), round_up(n, 16), 1, n, keep.back().as<uint8_t>(),
+                              out_stride, ws.p, res, st);
+            readback(&e.be, be.p, 1, st);
+            readback(&e.len, ln.p, 8, st);
+            readback(&e.crc, cr.p, 4, st);
+            readback(&e.payload, pl.p, 8, st);
+        }
+        uint64_t size = 8;
+        for (int l = 0; l < L; ++l) size += 1 + 21 + enc[l].len;
+        if (size_out) *size_out = size;
+        if (!dst || capacity < size) throw Error(EINVAL_, "session buffer too small");
+        std::vector<uint8_t> head(8 + 22 * (size_t)L);
+        auto put = [](uint8_t *p, uint64_t v, int nb) {
+            for (int i = 0; i < nb; ++i) p[i] = (uint8_t)(v >> (8 * i));
+        };
+        std::memcpy(head.data(), "IPS1", 4);
+        put(head.data() + 4, s->archive_crc, 4);
+        struct Piece {
+            const void *src;
+            bool dev;
+            uint64_t len, off;
+        };
+        std::vector<Piece> pieces{{head.data(), false, 8, 0}};
+        uint64_t o = 8;
+        for (int l = L, hi = 0; l >= 1; --l, ++hi) {
+            const Enc &e = enc[l - 1];
+            uint8_t *h = head.data() + 8 + 22 * (size_t)hi;
+            h[0] = (uint8_t)s->k[l - 1];
+            h[1] = e.be;
+            put(h + 2, e.raw * 8, 8);
+            put(h + 10, e.len, 8);
+            put(h + 18, e.crc, 4);
+            pieces.push_back({h, false, 22, o});
+            o += 22;
+            if (e.len) pieces.push_back({e.payload, true, e.len, o});
+            o += e.len;
+        }
+        uint8_t *d = static_cast<uint8_t *>(dst);
+        for (const Piece &pc : pieces) {
+            if (!dst_on_device && !pc.dev) std::memcpy(d + pc.off, pc.src, pc.len);
+            else
+                CK(cudaMemcpyAsync(d + pc.off, pc.src, pc.len,
+                                   pc.dev ? (dst_on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost)
+                                          : cudaMemcpyHostToDevice,
+                                   st));
+        }
+        CK(cudaStreamSynchronize(st));
+    });
+}
+
+int ipcg_session_read(ipcg_ctx *c, const ipcg_archive *a, const void *bytes, uint64_t size, int on_device,
+                      ipcg_session **out) {
+    if (out) *out = nullptr;
+    return guarded(c, [&] {
+        cudaStream_t st = c->stream;
+        const ipcg_index &ix = a->ix;
+        const int L = ix.levels, lp = ix.progressive_levels;
+        const uint8_t *src = static_cast<const uint8_t *>(bytes);
+        // small host reads of the (possibly device-resident) file: the headers only
+        auto fetch = [&](uint64_t off, uint64_t len, uint8_t *h) {
+            if (!on_device) std::memcpy(h, src + off, len);
+            else if (len) CK(cudaMemcpy(h, src + off, len, cudaMemcpyDeviceToHost));
+        };
+        auto rd = [](const uint8_t *p, int nb) {
+            uint64_t v = 0;
+            for (int i = 0; i < nb; ++i) v |= (uint64_t)p[i] << (8 * i);
+            return v;
+        };
+        const char *const trunc = "truncated input while parsing";  // ByteReader (common.hpp:98)
+        uint8_t h[22];
+        if (size < 4) throw Error(ERUNTIME, trunc);
+        fetch(0, 4, h);
+        if (std::memcmp(h, "IPS1", 4) != 0) throw Error(ERUNTIME, "not a session file: bad magic");
+        if (size < 8) throw Error(ERUNTIME, trunc);
+        fetch(4, 4, h);
+        const uint32_t crc = (uint32_t)rd(h, 4);
+        if (crc != ix.identity) throw Error(ERUNTIME, "session does not belong to this archive");
+        // parse every level's header in file order; the first parse error is raised only after
+        // the blocks of the levels before it decoded cleanly (the reference works level by level)
+        struct Blk {
+            int level, k;
+            uint8_t be;
+            uint64_t raw_bits, plen, off;
+            uint32_t crc;
+        };
+        std::vector<Blk> blks;
+        std::string parse_err;
+        uint64_t pos = 8;
+        for (int level = L; level >= 1; --level) {
+            Blk b{level, 0, 0, 0, 0, 0, 0};
+            if (size - pos < 1) { parse_err = trunc; break; }
+            fetch(pos, 1, h);
+            b.k = h[0];
+            pos += 1;
+            if (b.k > 32) { parse_err = "session plane count out of range"; break; }
+            if (level > lp && b.k != 32) { parse_err = "session has partial non-progressive level"; break; }
+            if (size - pos < 1) { parse_err = trunc; break; }
+            fetch(pos, 1, h);
+            if (h[0] > 1) { parse_err = "unknown backend id"; break; }
+            if (size - pos < 21) { parse_err = trunc; break; }
+            fetch(pos, 21, h);
+            b.be = h[0];
+            b.raw_bits = rd(h + 1, 8);
+            b.plen = rd(h + 9, 8);
+            b.crc = (uint32_t)rd(h + 17, 4);
+            pos += 21;
+            if (size - pos < b.plen) { parse_err = trunc; break; }
+            b.off = pos;
+            pos += b.plen;
+            blks.push_back(b);
+        }
+        if (parse_err.empty() && pos != size) parse_err = "session file has trailing bytes";
+        // payload bytes on the device
+        DBuf staged;
+        const uint8_t *dsrc = src;
+        if (!on_device) {
+            staged = DBuf(std::max<uint64_t>(pos, 1), st);
+            CK(cudaMemcpyAsync(staged.p, src, pos, cudaMemcpyHostToDevice, st));
+            dsrc = staged.as<uint8_t>();
+        }
+        const size_t B = blks.size();
+        std::vector<uint32_t> hcrc(B, 0);
+        if (B) {
+            uint64_t maxp = 1;
+            for (const Blk &b : blks) maxp = std::max(maxp, b.plen);
+            std::vector<const uint8_t *> ptrs(B);
+            std::vector<uint64_t> lens(B);
+            for (size_t i = 0; i < B; ++i) ptrs[i] = dsrc + blks[i].off, lens[i] = blks[i].plen;
+            const size_t cw = crc32_batch_workspace((int)B, maxp);
+            DBuf crcws(cw, st), crcs(B * 4, st), pd(B * 8, st), ld(B * 8, st);
+            CK(cudaMemcpyAsync(pd.p, ptrs.data(), B * 8, cudaMemcpyHostToDevice, st));
+            CK(cudaMemcpyAsync(ld.p, lens.data(), B * 8, cudaMemcpyHostToDevice, st));
+            crc32_batch(pd.as<const uint8_t *>(), ld.as<uint64_t>(), (int)B, maxp, crcs.as<uint32_t>(), crcws.p, cw, st);
+            readback(hcrc.data(), crcs.p, B * 4, st);
+        }
+        ipcg_session *ns = new ipcg_session;
+        ns->archive_crc = ix.identity;
+        ns->levels = L;
+        ns->lp = lp;
+        ns->owner = st;
+        ns->pool = &c->scratch;
+        ns->device = c->device;
+        std::vector<DBuf> scratch_out;  // decode targets of blocks whose size is then rejected
+        try {
+            // decode every block (identity: copy, deflate: inflate) into its target
+            std::vector<InflateJob> jobs;
+            std::vector<size_t> job_blk;
+            std::vector<CopyDesc> copies;
+            std::vector<std::string> blk_err(B);
+            for (size_t i = 0; i < B; ++i) {
+                const Blk &b = blks[i];
+                const int li = b.level - 1;
+                ns->k[li] = b.k;
+                ns->count[li] = ix.records[li].count;
+                if (hcrc[i] != b.crc) { blk_err[i] = "block checksum mismatch"; continue; }
+                const uint64_t rb = (b.raw_bits + 7) / 8;
+                if (b.be == 0 && b.plen != rb) { blk_err[i] = "identity block has wrong length"; continue; }
+                const bool fits = b.level <= lp ? rb == ix.records[li].count * 4 : rb == 0;
+                uint8_t *dst = nullptr;
+                if (fits && b.level <= lp) {
+                    const uint64_t cnt = ix.records[li].count;
+                    ns->merged[li] = static_cast<uint32_t *>(scratch_get(std::max<uint64_t>(cnt, 1) * 4 + 16, st));
+                    dst = reinterpret_cast<uint8_t *>(ns->merged[li]);
+                } else if (rb) {
+                    if (rb > (uint64_t(1) << 36)) { blk_err[i] = "std::bad_alloc"; continue; }
+                    scratch_out.emplace_back(rb, st);
+                    dst = scratch_out.back().as<uint8_t>();
+                }
+                if (!fits) blk_err[i] = b.level <= lp ? "session codeword array has wrong length"
+                                                      : "session stores codewords for a non-progressive level";
+                if (!rb) continue;
+                if (b.be == 0) copies.push_back(CopyDesc{dsrc + b.off, (uint64_t)reinterpret_cast<uintptr_t>(dst), rb});
+                else jobs.push_back(InflateJob{dsrc + b.off, b.plen, dst, rb}), job_blk.push_back(i);
+            }
+            if (!copies.empty()) gather(c, copies, nullptr);
+            if (!jobs.empty()) {
+                DevAlloc tmp;
+                DBuf sd(jobs.size() * 4, st);
+                inflate_batch_host(jobs, sd.as<int>(), tmp, st);
+                std::vector<int> js(jobs.size());
+                readback(js.data(), sd.p, jobs.size() * 4, st);
+                for (size_t k = 0; k < jobs.size(); ++k)
+                    if (js[k]) blk_err[job_blk[k]] = "deflate backend failed to decompress block";
+            }
+            CK(cudaStreamSynchronize(st));
+            for (size_t i = 0; i < B; ++i)
+                if (!blk_err[i].empty()) throw Error(ERUNTIME, blk_err[i]);
+            if (!parse_err.empty()) throw Error(ERUNTIME, parse_err);
+        } catch (...) {
+            for (int l = 0; l < IPCG_MAX_LEVELS; ++l)
+                if (ns->merged[l]) scratch_put(ns->merged[l], st);
+            delete ns;
+            throw;
+        }
+        *out = ns;
+    });
+}
+
+// compute_metrics<T> (pipeline.hpp:354-372) on the device (metrics.cu)
+int ipcg_compute_metrics(ipcg_ctx *c, int scalar, const void *original, int original_on_device, uint64_t n_original,
+                         const void *decoded, int decoded_on_device, uint64_t n_decoded, double *max_error,
+                         double *mse, double *psnr) {
+    return guarded(c, [&] {
+        if (scalar != 0 && scalar != 1) throw Error(EINVAL_, "field scalars must be f32 or f64");
+        if (n_original != n_decoded) throw Error(EINVAL_, "metrics inputs differ in size");
+        cudaStream_t st = c->stream;
+        const uint64_t bytes = n_original * (scalar == 0 ? 4 : 8);
+        DBuf ua, ub;
+        const void *a = original, *b = decoded;
+        if (!original_on_device && bytes) {
+            ua = DBuf(bytes, st);
+            CK(cudaMemcpyAsync(ua.p, original, bytes, cudaMemcpyHostToDevice, st));
+            a = ua.p;
+        }
+        if (!decoded_on_device && bytes) {
+            ub = DBuf(bytes, st);
+            CK(cudaMemcpyAsync(ub.p, decoded, bytes, cudaMemcpyHostToDevice, st));
+            b = ub.p;
+        }
+        double r[3];
+        compute_metrics_device(scalar, a, b, n_original, r, st);
+        if (max_error) *max_error = r[0];
+        if (mse) *mse = r[1];
+        if (psnr) *psnr = r[2];
+    });
 }
 
 int ipcg_plan_for_error(ipcg_ctx *c, const ipcg_archive *a, double max_error, int *k_out) {

@@ -2,7 +2,7 @@
 from /root/reference/proj/src by `make -C oracle ref`).
 
 Each case stores the input field, the compression options, the archive bytes the
-reference writes, and SHA-256 digests of the reference's reconstructions for a few
+reference writes, the session file it writes for one plan (.ips), and SHA-256 digests of the reference's reconstructions for a few
 plans (incl. one refine step) plus its planner outputs.  The fixtures pin the C
 restatement (oracle/) and the GPU path without needing the reference tree, which does
 not exist on the GPU box.  Re-run only when the reference changes:
@@ -71,6 +71,10 @@ def main():
         k2 = [min(32, x + 7) if l + 1 <= LP else 32 for l, x in enumerate(k1)]
         v2, _, loaded2 = ref.refine(arch, k1, m1, v1, k2)
         refine = {"k1": k1, "k2": k2, "sha256": hashlib.sha256(v2.tobytes()).hexdigest(), "loaded": int(loaded2)}
+        sess = ref.write_session(arch, k1, m1)  # write_session (session.cpp:8-24) of the k1 session
+        with open(os.path.join(HERE, f"{name}.ips"), "wb") as fh:
+            fh.write(sess)
+        session = {"k": k1, "sha256": hashlib.sha256(sess).hexdigest(), "bytes": len(sess)}
         planner = {}
         for fac in (4.0, 64.0, 4096.0):
             planner[f"error_x{int(fac)}"] = ref.plan_for_error(arch, fac * eb)
@@ -85,7 +89,8 @@ def main():
             fh.write(arch)
         manifest.append({"name": name, "dims": list(dims), "dtype": np.dtype(dtype).name, "eb": eb,
                          "interp": interp, "lp": lp, "archive_sha256": hashlib.sha256(arch).hexdigest(),
-                         "archive_bytes": len(arch), "recon": recon, "refine": refine, "planner": planner})
+                         "archive_bytes": len(arch), "recon": recon, "refine": refine, "planner": planner,
+                         "session": session})
     with open(os.path.join(HERE, "manifest.json"), "w") as fh:
         json.dump(manifest, fh, indent=1)
     print("wrote", len(manifest), "golden cases")

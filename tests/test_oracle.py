@@ -49,6 +49,84 @@ def test_oracle_reproduces_golden_reference_outputs(case, oracle_lib):
             assert got == want_k
 
 
+@pytest.mark.parametrize("case", MANIFEST, ids=[c["name"] for c in MANIFEST])
+def test_oracle_session_file_matches_golden(case, oracle_lib):
+    """write_session / read_session (session.cpp:8-61) against the session file the reference wrote."""
+    arch = open(os.path.join(GOLDEN, case["name"] + ".ipc"), "rb").read()
+    want = open(os.path.join(GOLDEN, case["name"] + ".ips"), "rb").read()
+    sess = case["session"]
+    assert hashlib.sha256(want).hexdigest() == sess["sha256"]
+    f = np.load(os.path.join(GOLDEN, case["name"] + ".input.npy"))
+    _, m, _ = oracle_lib.reconstruct(arch, sess["k"], f.dtype, f.size)
+    assert oracle_lib.write_session(arch, sess["k"], m) == want
+    k, m2 = oracle_lib.read_session(arch, want)
+    assert k == sess["k"]
+    for a, b in zip(m, m2):
+        assert (a is None and b is None) or np.array_equal(a, b)
+
+
+def _session_corruptions(good: bytes):
+    yield good[:3]
+    yield b"XPS1" + good[4:]
+    yield good[:4] + bytes(4) + good[8:]
+    yield good[:-1]
+    yield good + b"\0"
+    yield good[:8] + bytes([33]) + good[9:]   # plane count out of range
+    yield good[:9] + bytes([7]) + good[10:]   # unknown backend id
+    yield good[:20] + bytes([good[20] ^ 1]) + good[21:]  # payload length
+    yield good[:-2] + bytes([good[-2] ^ 0x40]) + good[-1:]  # payload byte -> checksum
+    for cut in (9, 12, 20, 29):
+        yield good[:cut]
+
+
+def test_oracle_metrics_known_answers(oracle_lib):  # test_pipeline.cpp:355-390
+    a = np.array([1.0, 2.0, 3.0])
+    m = oracle_lib.compute_metrics(a, a)
+    assert m[0] == 0.0 and m[1] == 0.0 and np.isinf(m[2])
+    a = np.array([0.0, 10.0, 5.0, 2.5])
+    b = a.copy()
+    b[2] += 0.125
+    m = oracle_lib.compute_metrics(a, b)
+    assert m[0] == 0.125 and m[1] == 0.125 * 0.125 / 4.0
+    assert m[2] == pytest.approx(20.0 * np.log10(10.0 / np.sqrt(0.125 * 0.125 / 4.0)), rel=1e-12)
+
+
+@pytest.mark.skipif(not oracle.ref_available(), reason="oracle/_ref not built (reference tree absent)")
+def test_oracle_metrics_equal_reference(oracle_lib):
+    ref = oracle.load("ref")
+    rng = np.random.default_rng(19)
+    for dt in (np.float32, np.float64):
+        a = rng.uniform(-3, 3, 5000).astype(dt)
+        b = (a + 0.01 * rng.uniform(-3, 3, a.size)).astype(dt)
+        b[11], a[12], b[13] = np.nan, np.inf, -np.inf
+        for x, y in ((a, b), (a[:100], a[:100]), (a[:0], b[:0])):
+            got, want = oracle_lib.compute_metrics(x, y), ref.compute_metrics(x, y)
+            assert np.array_equal(np.array(got), np.array(want), equal_nan=True)
+
+
+@pytest.mark.skipif(not oracle.ref_available(), reason="oracle/_ref not built (reference tree absent)")
+@pytest.mark.parametrize("lp", [0, 2])
+def test_oracle_session_reader_errors_match_reference(lp, oracle_lib):
+    ref = oracle.load("ref")
+    dims = (20, 24, 18)
+    f = synth.smooth_field(dims, 3).astype(np.float32)
+    arch = oracle_lib.compress(f, dims, 1e-3 * float(f.max() - f.min()), 1, lp)
+    L = oracle.archive_levels(arch)
+    k = [5 + 3 * i if i < (lp or L) else 32 for i in range(L)]
+    _, m, _ = oracle_lib.reconstruct(arch, k, np.float32, f.size)
+    good = ref.write_session(arch, k, m)
+    assert oracle_lib.write_session(arch, k, m) == good
+    for bad in _session_corruptions(good):
+        res = []
+        for impl in (oracle_lib, ref):
+            try:
+                impl.read_session(arch, bad)
+                res.append("ok")
+            except oracle.OracleError as e:
+                res.append(str(e))
+        assert res[0] == res[1], (len(bad), res)
+
+
 @pytest.mark.skipif(not oracle.ref_available(), reason="oracle/_ref not built (reference tree absent)")
 @pytest.mark.parametrize("dims,interp,dtype", [((1,), 1, np.float64), ((3, 1), 0, np.float32), ((65,), 1, np.float64),
                                                ((9, 7, 33), 1, np.float32), ((2, 3, 4, 5), 0, np.float64),
