@@ -240,6 +240,39 @@ Retrieved<T> refine_field(ArchiveReader &archive, const RetrievalSession &sessio
     return out;
 }
 
+// write_session / read_session (session.hpp:36-40, session.cpp:8-61): the merged codewords
+// are deflated / inflated on the device
+inline void write_session(std::ostream &out, const RetrievalSession &session,
+                          Context &ctx = Context::default_context()) {
+    std::vector<char> buf(ipcg_session_write_bound(session.get()));
+    std::uint64_t size = 0;
+    ctx.check(ipcg_session_write(ctx.get(), session.get(), buf.data(), 0, buf.size(), &size));
+    out.write(buf.data(), (std::streamsize)size);
+    if (!out) throw std::runtime_error("failed to write session stream");
+}
+inline RetrievalSession read_session(std::istream &in, const ArchiveReader &archive) {
+    std::vector<char> bytes((std::istreambuf_iterator<char>(in)), std::istreambuf_iterator<char>());
+    ipcg_session *s = nullptr;
+    archive.context().check(
+        ipcg_session_read(archive.context().get(), archive.get(), bytes.data(), bytes.size(), 0, &s));
+    return RetrievalSession(s);
+}
+
+// FieldMetrics / compute_metrics<T> (pipeline.hpp:49-53,354-372), one pass on the device
+struct FieldMetrics {
+    double max_error = 0.0;
+    double mse = 0.0;
+    double psnr = 0.0;
+};
+template <class T>
+FieldMetrics compute_metrics(std::span<const T> original, std::span<const T> decoded,
+                             Context &ctx = Context::default_context()) {
+    FieldMetrics m;
+    ctx.check(ipcg_compute_metrics(ctx.get(), detail::scalar_of<T>(), original.data(), 0, original.size(),
+                                   decoded.data(), 0, decoded.size(), &m.max_error, &m.mse, &m.psnr));
+    return m;
+}
+
 // planner.hpp:15-55 over the archive's index (the ErrorModel is the index itself)
 inline const ArchiveReader &build_error_model(const ArchiveReader &a) { return a; }
 inline RetrievalPlan full_plan(const ArchiveReader &a) {

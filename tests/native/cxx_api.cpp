@@ -1,6 +1,7 @@
 // cxx_api.cpp -- TEST PROGRAM: drives include/ipcomp_b200.hpp the way a reference user
 // drives <ipcomp/pipeline.hpp> (compress -> write -> read back from an istream ->
-// plan_for_error -> reconstruct -> refine to the full plan) and writes the archive and
+// plan_for_error -> reconstruct -> refine to the full plan -> session file round trip ->
+// compute_metrics) and writes the archive and
 // both reconstructions to files so tests/test_cxx_api.py can diff them with the oracle.
 //   cxx_api <field.f32> <nx> <ny> <nz> <eb> <max_error> <out_prefix>
 #include <cstdio>
@@ -44,6 +45,16 @@ int main(int argc, char **argv) {
         dump(pre + ".recon", r1.values.data(), r1.values.size() * sizeof(float));
         ib::Retrieved<float> r2 = ib::refine_field<float>(reader, r1.session, r1.values, ib::full_plan(reader));
         dump(pre + ".refine", r2.values.data(), r2.values.size() * sizeof(float));
+        // session file round trip (write_session / read_session), then refine from it
+        std::stringstream sess;
+        ib::write_session(sess, r1.session);
+        const std::string sbytes = sess.str();
+        dump(pre + ".session", sbytes.data(), sbytes.size());
+        const ib::RetrievalSession back = ib::read_session(sess, reader);
+        ib::Retrieved<float> r3 = ib::refine_field<float>(reader, back, r1.values, ib::full_plan(reader));
+        dump(pre + ".refine2", r3.values.data(), r3.values.size() * sizeof(float));
+        const ib::FieldMetrics m = ib::compute_metrics<float>(field, r3.values);
+        std::printf("max_error %.17g mse %.17g psnr %.17g\n", m.max_error, m.mse, m.psnr);
         std::printf("levels %d plan", reader.header().levels);
         for (int k : plan.k) std::printf(" %d", k);
         std::printf(" bytes_read %llu\n", (unsigned long long)reader.payload_bytes_read());
