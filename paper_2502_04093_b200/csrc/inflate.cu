@@ -29,6 +29,9 @@
 #include <cooperative_groups.h>
 namespace cg = cooperative_groups;
 
+#ifndef IPCG_CPW
+#define IPCG_CPW 1
+#endif
 namespace ipcg {
 
 namespace {
@@ -186,6 +189,11 @@ struct Huff {
     uint16_t offs[16];
     uint16_t sym[320];
     uint16_t fast[1 << FASTBITS];  // (len << 12) | symbol, 0 = slow path
+    // k_decode_cands' resolved entries: code length (0 = slow path) | kind << 4 | extra bits
+    // << 6 | value << 16.  lit/len table: kind 0 literal (value = byte), 1 length (value =
+    // base length), 2 end of block / invalid symbol (general path); distance table: kind 1
+    // (value = base distance), 2 invalid.  Code + extra bits fit one refill (9 + 13 < 33).
+    uint32_t fx[1 << FASTBITS];
 };
 
 // build from lengths on the whole warp (lengths already validated)
@@ -224,7 +232,20 @@ __device__ void huff_build(Huff &h, const uint8_t *lens, int n, unsigned lane) {
 
 // the same for a group of G lanes (gl = lane within the group); every lane of the warp
 // calls it (inactive groups pass active = false) so the warp-wide syncs line up
-__device__ void huff_build_group(Huff &h, const uint8_t *lens, int n, unsigned gl, unsigned G, bool active) {
+__device__ __forceinline__ uint32_t fx_entry(uint32_t L, uint32_t sym, bool dist) {
+    uint32_t kind = 2, ext = 0, val = 0;
+    if (dist) {
+        if (sym < 30) kind = 1, ext = kDExt[sym], val = kDBase[sym];
+    } else if (sym < 256) {
+        kind = 0, val = sym;
+    } else if (sym >= 257 && sym < 286) {
+        kind = 1, ext = kLExt[sym - 257], val = kLBase[sym - 257];
+    }
+    return L | kind << 4 | ext << 6 | val << 16;
+}
+
+__device__ void huff_build_group(Huff &h, const uint8_t *lens, int n, unsigned gl, unsigned G, bool active,
+                                 bool dist) {
     if (active && gl == 0) {
         for (int i = 0; i < 16; ++i) h.count[i] = 0;
         for (int i = 0; i < n; ++i) h.count[lens[i]]++;
@@ -243,7 +264,7 @@ __device__ void huff_build_group(Huff &h, const uint8_t *lens, int n, unsigned g
     }
     __syncwarp();
     if (active)
-        for (int i = gl; i < (1 << FASTBITS); i += G) h.fast[i] = 0;
+        for (int i = gl; i < (1 << FASTBITS); i += G) h.fast[i] = 0, h.fx[i] = 0;
     __syncwarp();
     if (active) {
         int total = 0;
@@ -254,7 +275,11 @@ __device__ void huff_build_group(Huff &h, const uint8_t *lens, int n, unsigned g
             if (L > FASTBITS) continue;
             const uint32_t code = h.first[L] + (uint32_t)(t - h.offs[L]);
             const uint32_t rev = __brev(code) >> (32 - L);
-            for (uint32_t e = 0; e < (1u << (FASTBITS - L)); ++e) h.fast[rev | (e << L)] = (uint16_t)((L << 12) | h.sym[t]);
+            const uint32_t fx = fx_entry((uint32_t)L, h.sym[t], dist);
+            for (uint32_t e = 0; e < (1u << (FASTBITS - L)); ++e) {
+                h.fast[rev | (e << L)] = (uint16_t)((L << 12) | h.sym[t]);
+                h.fx[rev | (e << L)] = fx;
+            }
         }
     }
     __syncwarp();
@@ -285,11 +310,14 @@ __device__ __forceinline__ int huff_decode(const Huff &h, Bits &b) {
 struct WBits {
     const uint32_t *w;
     uint64_t nwords;  // words covering [aligned base, src + len)
-    uint64_t wi;      // next word to load
+    uint64_t wi;      // index of the word held in `nxt`
+    uint32_t nxt;     // word wi, loaded one refill ahead so its latency overlaps the decode
     uint64_t buf;
     int cnt;
-    uint64_t pos;     // absolute bit position (relative to the aligned base) of buf bit 0
     uint64_t endbit;  // absolute bit position of the end of the stream
+    // absolute bit position (relative to the aligned base) of buf bit 0: words before wi are
+    // in (or past) the buffer, so it is derived instead of being advanced on every drop
+    __device__ __forceinline__ uint64_t pos() const { return wi * 32 - (uint64_t)cnt; }
     __device__ __forceinline__ void init(const uint8_t *src, uint64_t len, uint64_t bit) {
         const uintptr_t a = reinterpret_cast<uintptr_t>(src);
         const uint64_t off = (uint64_t)(a & 3) * 8;
@@ -298,32 +326,31 @@ struct WBits {
         endbit = off + 8 * len;
         const uint64_t abs = off + bit;
         wi = abs >> 5;
+        nxt = wi < nwords ? __ldg(w + wi) : 0u;
         buf = 0;
         cnt = 0;
-        pos = abs & ~31ull;
         refill();
         refill();
         drop((int)(abs & 31));
     }
     __device__ __forceinline__ void refill() {
         if (cnt <= 32) {
-            const uint64_t v = wi < nwords ? __ldg(w + wi) : 0u;
-            buf |= v << cnt;
+            buf |= (uint64_t)nxt << cnt;
             ++wi;
+            nxt = wi < nwords ? __ldg(w + wi) : 0u;
             cnt += 32;
         }
     }
     __device__ __forceinline__ void drop(int k) {
         buf >>= k;
         cnt -= k;
-        pos += (uint64_t)k;
     }
     __device__ __forceinline__ uint32_t take(int k) {  // k <= cnt
         const uint32_t v = (uint32_t)(buf & ((1ull << k) - 1));
         drop(k);
         return v;
     }
-    __device__ __forceinline__ bool overrun() const { return pos > endbit; }
+    __device__ __forceinline__ bool overrun() const { return pos() > endbit; }
 };
 
 // Huffman decode from the buffer (needs >= 15 valid bits)
@@ -538,7 +565,7 @@ __global__ void __launch_bounds__(256) k_scan(const InflateJob *jobs, const Tabl
 // CPW candidates per warp, one per group of 32/CPW lanes: the decode is inherently
 // sequential per block and every lane of a group does the same work, so packing several
 // blocks into a warp divides the (issue-bound) warp-instruction count.
-constexpr int DWARPS = 4;  // warps per k_decode_cands CTA (static smem: DWARPS * CPW table slots)
+constexpr int DWARPS = 4 / IPCG_CPW;  // warps per k_decode_cands CTA (static smem: DWARPS * CPW table slots)
 
 template <int CPW>
 __global__ void __launch_bounds__(DWARPS * 32) k_decode_cands(const InflateJob *jobs, const Tables *tabs, Cand *cands,
@@ -571,12 +598,12 @@ __global__ void __launch_bounds__(DWARPS * 32) k_decode_cands(const InflateJob *
         if (act && gl == 0)
             for (int i = 0; i < nlen + ndist; ++i) lens_s[slot][i] = lens[i];
         __syncwarp();
-        huff_build_group(lit_s[slot], lens_s[slot], nlen, gl, G, act);
-        huff_build_group(dist_s[slot], lens_s[slot] + nlen, ndist, gl, G, act);
+        huff_build_group(lit_s[slot], lens_s[slot], nlen, gl, G, act, false);
+        huff_build_group(dist_s[slot], lens_s[slot] + nlen, ndist, gl, G, act, true);
         if (act) {  // (no early exits: every lane reaches the syncs below)
         uint32_t *out = pool + ci * (uint64_t)MAXSYM;
         uint32_t ns = 0, nz = 0;
-        uint64_t bytes = 0;
+        uint32_t bytes = 0;  // <= 16383 symbols x 258 bytes
         bool good = true;
         WBits wb;
         wb.init(job.src, job.src_len, b.used);
@@ -598,6 +625,43 @@ __global__ void __launch_bounds__(DWARPS * 32) k_decode_cands(const InflateJob *
             bool eob = false;
             while (ns < seg_end) {
                 wb.refill();  // >= 33 bits: a literal/length code and its extra bits
+                {  // resolved fast-table entries: literals and whole matches in a few instructions
+                    const uint32_t e = lit_s[slot].fx[(uint32_t)wb.buf & ((1u << FASTBITS) - 1)];
+                    const uint32_t kind = (e >> 4) & 3u;
+                    if ((e & 15u) && kind == 0u) {
+                        wb.drop((int)(e & 15u));
+                        const uint32_t sym = e >> 16;
+                        if (gl == 0) out[ns] = sym_lit(sym);
+                        nz |= sym;
+                        ++ns;
+                        ++bytes;
+                        continue;
+                    }
+                    if ((e & 15u) && kind == 1u) {
+                        const uint32_t cl = e & 15u, ext = (e >> 6) & 15u;
+                        const uint32_t len = (e >> 16) + ((uint32_t)(wb.buf >> cl) & ((1u << ext) - 1u));
+                        wb.drop((int)(cl + ext));
+                        wb.refill();
+                        const uint32_t ed = dist_s[slot].fx[(uint32_t)wb.buf & ((1u << FASTBITS) - 1)];
+                        uint32_t d;
+                        if ((ed & 15u) && ((ed >> 4) & 3u) == 1u) {
+                            const uint32_t dcl = ed & 15u, dext = (ed >> 6) & 15u;
+                            d = (ed >> 16) + ((uint32_t)(wb.buf >> dcl) & ((1u << dext) - 1u));
+                            wb.drop((int)(dcl + dext));
+                        } else {
+                            const int ds = huff_decode_w(dist_s[slot], wb);
+                            if (ds < 0 || ds >= 30) {
+                                good = false;
+                                break;
+                            }
+                            d = kDBase[ds] + wb.take(kDExt[ds]);
+                        }
+                        if (gl == 0) out[ns] = sym_match(len, d);
+                        ++ns;
+                        bytes += len;
+                        continue;
+                    }
+                }
                 const int sym = huff_decode_w(lit_s[slot], wb);
                 if (sym < 256) {
                     if (sym < 0) {
@@ -634,7 +698,7 @@ __global__ void __launch_bounds__(DWARPS * 32) k_decode_cands(const InflateJob *
             if (!good || eob) break;
         }
         if (wb.overrun()) good = false;
-        b.used = wb.pos - (uint64_t)(reinterpret_cast<uintptr_t>(job.src) & 3) * 8;
+        b.used = wb.pos() - (uint64_t)(reinterpret_cast<uintptr_t>(job.src) & 3) * 8;
         if (gl == 0) {
             c.ok = good ? 1 : 0;
             c.nzlit = nz != 0;
@@ -1179,7 +1243,7 @@ void inflate_batch_host(const std::vector<InflateJob> &jobs, int *status_dev, De
     {
         ProfScope ps("inflate.decode", st, total_src);
         if (nc) {
-            constexpr int CPW = 1;  // measured: 2 or 4 per warp diverge (literal vs match paths) and lose
+            constexpr int CPW = IPCG_CPW;  // measured: 2 or 4 per warp diverge (literal vs match paths) and lose
             const unsigned g = (unsigned)std::min<uint64_t>((nc + DWARPS * CPW - 1) / (DWARPS * CPW), 148ull * 32);
             k_decode_cands<CPW><<<g, DWARPS * 32, 0, st>>>(jd, td, cands, ncand, cand_cap, pool, ckpt);
             CKL();
