@@ -29,6 +29,9 @@
 #include <cooperative_groups.h>
 namespace cg = cooperative_groups;
 
+#ifndef IPCG_SEG
+#define IPCG_SEG 128
+#endif
 #ifndef IPCG_CPW
 #define IPCG_CPW 1
 #endif
@@ -39,7 +42,7 @@ namespace {
 constexpr int FASTBITS = 9;
 constexpr int MAXSYM = 16400;  // symbols stored per candidate block (zlib blocks: <= 16383)
 constexpr int WARPS = 4;
-constexpr int SEG = 128;                  // symbols per emit segment
+constexpr int SEG = IPCG_SEG;             // symbols per emit segment
 constexpr int NCKPT = MAXSYM / SEG + 2;   // output-offset checkpoints per candidate
 
 // ------------------------------------------------------------------ bit reader

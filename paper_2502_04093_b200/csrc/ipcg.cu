@@ -1000,7 +1000,7 @@ void retrieve_impl(ipcg_ctx *c, ipcg_archive *a, int scalar, const int *k, void 
             {
                 ProfScope psr("recon_pass", st, count * (uint64_t)(4 + 2 * w));
                 for (const PassDesc &pd : G.level[li].passes) {
-                    launch_recon_pass(state, scalar, ix.interp == 1, pd, ix.eb, merged, st);
+                    launch_recon_pass(state, scalar, ix.interp == 1, pd, ix.eb, merged, G.dims[G.nd - 1], st);
                     if (no) launch_outlier_apply(state, scalar, pd, ob, napplied.as<uint64_t>() + li, no, st);
                 }
             }

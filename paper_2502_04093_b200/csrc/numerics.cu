@@ -1,5 +1,6 @@
 // numerics.cu -- sm_100a kernels for prediction, quantization, bitplanes, loss tables,
 // merge and reconstruction.  See numerics.cuh for the reference citations.
+#include <type_traits>
 #include <cub/device/device_radix_sort.cuh>
 
 #include "numerics.cuh"
@@ -448,6 +449,93 @@ __global__ void __launch_bounds__(kBlock) k_recon_pass(T *__restrict__ state, Pa
     }
 }
 
+// Level-1 passes as whole rows of the last axis: one CTA per (row, 256*V-element chunk),
+// 16-byte vector loads and stores.  Targets of a level-1 pass sit at every other element of
+// a row (odd x for the last-axis pass, even x for the others); the thread rewrites the
+// non-target elements of its vector with the values it loaded (no other thread of the pass
+// writes them: they are stencil sources or later passes' targets), so every sector is read
+// and written whole instead of half-used by one-element-per-thread accesses.  The stencil
+// rows of an earlier-axis pass are vector-loaded at the same x (the cubic/linear/copy choice
+// is uniform per row); the last-axis pass stages its chunk plus a 4-element halo in shared
+// memory.  Arithmetic is predict()/reconstruct_value() verbatim.
+constexpr int kRowThreads = 256;
+template <class T, bool Last>
+__global__ void __launch_bounds__(kRowThreads) k_recon_rows(T *__restrict__ state, PassDesc p, uint32_t X,
+                                                            uint32_t x0, double eb, bool cubic,
+                                                            const uint32_t *__restrict__ merged) {
+    using Vec = typename std::conditional<sizeof(T) == 4, float4, double2>::type;
+    constexpr int V = 16 / (int)sizeof(T);
+    constexpr int CH = kRowThreads * V;
+    const uint32_t bz = blockIdx.z, by = blockIdx.y;
+    const uint64_t row = p.start_flat - x0 + (uint64_t)bz * p.step_flat[0] + (uint64_t)by * p.step_flat[1];
+    const uint64_t obase = p.ordinal_base + ((uint64_t)bz * p.cnt[1] + by) * p.cnt[2];
+    const uint32_t xb = blockIdx.x * CH, xs = xb + threadIdx.x * V;
+    const bool in = xs < X;  // X % V == 0
+    T e[V];
+    if (in) {
+        const Vec v = *reinterpret_cast<const Vec *>(state + row + xs);
+        const T *vv = reinterpret_cast<const T *>(&v);
+#pragma unroll
+        for (int k = 0; k < V; ++k) e[k] = vv[k];
+    }
+    if constexpr (Last) {
+        __shared__ T sm[CH + 8];
+        for (int i = (int)threadIdx.x - 4; i < CH + 4; i += kRowThreads) {
+            if (i >= 0 && i < CH) continue;
+            const int64_t x = (int64_t)xb + i;
+            if (x >= 0 && x < (int64_t)X) sm[i + 4] = state[row + x];
+        }
+        if (in) {
+#pragma unroll
+            for (int k = 0; k < V; ++k) sm[threadIdx.x * V + k + 4] = e[k];
+        }
+        __syncthreads();
+        if (!in) return;
+#pragma unroll
+        for (int k = 0; k < V; ++k) {
+            const uint32_t x = xs + k;
+            if ((x & 1u) != x0) continue;
+            const T *c = sm + (x - xb) + 4;  // c[0] = element x
+            T pred;
+            if (cubic && x >= 3 && x + 3 < X) pred = ((T)9 * (c[-1] + c[1]) - (c[-3] + c[3])) / (T)16;
+            else if (x + 1 < X) pred = (c[-1] + c[1]) / (T)2;
+            else pred = c[-1];
+            e[k] = reconstruct_value<T>(pred, eb, (int64_t)from_negabinary(merged[obase + (x >> 1)]));
+        }
+    } else {
+        if (!in) return;
+        const uint64_t coord = p.axis_start + (uint64_t)(p.axis == 0 ? bz : by) * p.axis_step;
+        const uint64_t stp = p.st;
+        const bool cub = cubic && coord >= 3 * p.s && coord + 3 * p.s < p.extent;
+        const bool lin = coord + p.s < p.extent;
+        auto ld = [&](uint64_t f, T *o) {
+            const Vec v = *reinterpret_cast<const Vec *>(state + f);
+            const T *vv = reinterpret_cast<const T *>(&v);
+#pragma unroll
+            for (int k = 0; k < V; ++k) o[k] = vv[k];
+        };
+        T a[V], b[V], c[V], d[V];
+        ld(row + xs - stp, b);
+        if (lin) ld(row + xs + stp, c);
+        if (cub) ld(row + xs - 3 * stp, a), ld(row + xs + 3 * stp, d);
+#pragma unroll
+        for (int k = 0; k < V; ++k) {
+            const uint32_t x = xs + k;
+            if ((x & 1u) != x0) continue;
+            T pred;
+            if (cub) pred = ((T)9 * (b[k] + c[k]) - (a[k] + d[k])) / (T)16;
+            else if (lin) pred = (b[k] + c[k]) / (T)2;
+            else pred = b[k];
+            e[k] = reconstruct_value<T>(pred, eb, (int64_t)from_negabinary(merged[obase + (x >> 1)]));
+        }
+    }
+    Vec v;
+    T *vv = reinterpret_cast<T *>(&v);
+#pragma unroll
+    for (int k = 0; k < V; ++k) vv[k] = e[k];
+    *reinterpret_cast<Vec *>(state + row + xs) = v;
+}
+
 // strictly increasing prefix of in-range ordinals = what the in-order matcher applies
 __global__ void k_outlier_prefix(const uint8_t *block, uint64_t entries, int scalar, uint64_t count, uint64_t *napplied) {
     __shared__ unsigned long long first_bad;
@@ -613,10 +701,35 @@ void launch_merge(const uint32_t *const *rows, const uint32_t *merged_in, uint32
     CKL();
 }
 
+// a level-1 pass whose targets are every other element of whole rows of the last axis
+static bool rows_applicable(const PassDesc &q, uint64_t X, int w, const void *state, uint32_t &x0) {
+    if (q.s != 1 || q.axis < 0 || X < 2 || X % (16 / w) != 0 || (reinterpret_cast<uintptr_t>(state) & 15)) return false;
+    if (q.step_flat[2] != 2 || q.cnt[1] > 65535 || q.cnt[0] > 65535 || X >= (1u << 31)) return false;
+    x0 = (uint32_t)(q.start_flat % X);
+    if (x0 > 1 || q.cnt[2] != (X - x0 + 1) / 2) return false;
+    if (q.axis == 2) return x0 == 1 && q.st == 1;
+    return x0 == 0 && q.st % (16 / w) == 0;  // stencil rows stay 16-byte aligned
+}
+
 void launch_recon_pass(void *state, int scalar, bool cubic, const PassDesc &pd, double eb, const uint32_t *merged,
-                       cudaStream_t st) {
+                       uint64_t row_len, cudaStream_t st) {
     PassDesc q;
     dim3 grid, block;
+    uint32_t x0 = 0;
+    if (pass_box(pd, q, grid, block) && rows_applicable(q, row_len, scalar == 0 ? 4 : 8, state, x0)) {
+        const unsigned ch = kRowThreads * (scalar == 0 ? 4 : 2);
+        const dim3 g((unsigned)((row_len + ch - 1) / ch), (unsigned)q.cnt[1], (unsigned)q.cnt[0]);
+        const uint32_t X = (uint32_t)row_len;
+        if (scalar == 0) {
+            if (q.axis == 2) k_recon_rows<float, true><<<g, kRowThreads, 0, st>>>((float *)state, q, X, x0, eb, cubic, merged);
+            else k_recon_rows<float, false><<<g, kRowThreads, 0, st>>>((float *)state, q, X, x0, eb, cubic, merged);
+        } else {
+            if (q.axis == 2) k_recon_rows<double, true><<<g, kRowThreads, 0, st>>>((double *)state, q, X, x0, eb, cubic, merged);
+            else k_recon_rows<double, false><<<g, kRowThreads, 0, st>>>((double *)state, q, X, x0, eb, cubic, merged);
+        }
+        CKL();
+        return;
+    }
     if (pass_box(pd, q, grid, block)) {
         if (scalar == 0) k_recon_pass<float, true, true><<<grid, block, 0, st>>>((float *)state, q, eb, cubic, merged);
         else k_recon_pass<double, true, true><<<grid, block, 0, st>>>((double *)state, q, eb, cubic, merged);

@@ -50,7 +50,7 @@ void launch_outlier_block(const uint64_t *ord_sorted, const uint64_t *bits_sorte
 void launch_merge(const uint32_t *const *rows, const uint32_t *merged_in, uint32_t *merged_out, uint64_t count, int k0,
                   int k1, cudaStream_t st);
 void launch_recon_pass(void *state, int scalar, bool cubic, const PassDesc &pd, double eb, const uint32_t *merged,
-                       cudaStream_t st);
+                       uint64_t row_len, cudaStream_t st);
 // outlier block bytes (u64 ordinal, T) -> overwrite inside one pass's ordinal range
 void launch_outlier_apply(void *state, int scalar, const PassDesc &pd, const uint8_t *block, const uint64_t *napplied,
                           uint64_t max_entries, cudaStream_t st);

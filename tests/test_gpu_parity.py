@@ -83,7 +83,13 @@ def _widen(rng, k, lp):
 
 @pytest.mark.parametrize("dims,interp,dtype", [((65, 33), 0, np.float64), ((17, 13, 11), 1, np.float64),
                                                ((64, 64, 64), 1, np.float32), ((33,), 1, np.float32),
-                                               ((2, 3, 4, 5), 0, np.float32)])
+                                               ((2, 3, 4, 5), 0, np.float32),
+                                               # whole-row level-1 kernels (last extent a multiple of
+                                               # the 16-byte vector): f64 pairs, f32 quads, rows longer
+                                               # than one 1024-element chunk, 1-D and 2-D boxes
+                                               ((24, 40, 36), 1, np.float64), ((24, 40, 36), 0, np.float64),
+                                               ((6, 10, 2056), 1, np.float32), ((48, 64), 0, np.float32),
+                                               ((4100,), 1, np.float32), ((7, 9, 4), 1, np.float32)])
 def test_reconstruct_and_refine_match_oracle(dims, interp, dtype, oracle_lib, ctx):
     f = _field(dims, 606, dtype)
     eb = _eb(f, 1e-4)
