@@ -465,7 +465,7 @@ ipcg_archive *compress_impl(ipcg_ctx *c, int scalar, const void *values, int on_
         {
             ProfScope ps("quant_pass", st, lg.count * (uint64_t)(2 * w + 4) + lg.count * (uint64_t)w);
             for (const PassDesc &pd : lg.passes)
-                launch_quant_pass(vals, state.p, scalar, cubic, pd, eb, nb, &sd->lowor[li], sink, st);
+                launch_quant_pass(vals, state.p, scalar, cubic, pd, eb, nb, &sd->lowor[li], sink, G.dims[G.nd - 1], st);
         }
         tm.mark("quant");
         tline.mark("q" + std::to_string(level), st);

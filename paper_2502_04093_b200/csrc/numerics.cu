@@ -459,29 +459,66 @@ __global__ void __launch_bounds__(kBlock) k_recon_pass(T *__restrict__ state, Pa
 // is uniform per row); the last-axis pass stages its chunk plus a 4-element halo in shared
 // memory.  Arithmetic is predict()/reconstruct_value() verbatim.
 constexpr int kRowThreads = 256;
-template <class T, bool Last>
-__global__ void __launch_bounds__(kRowThreads) k_recon_rows(T *__restrict__ state, PassDesc p, uint32_t X,
-                                                            uint32_t x0, double eb, bool cubic,
-                                                            const uint32_t *__restrict__ merged) {
+// blockDim = (tx, ty): tx threads cover a chunk of tx*V elements of one row, ty rows per CTA
+// (rows shorter than 256*V elements would otherwise leave threads idle).  Quant: the
+// compress pass (quant_point: predict + quantize + write-back + codeword + outliers);
+// otherwise the reconstruction pass (apply_level).
+struct RowsQuant {
+    const void *values;
+    uint32_t *nb;
+    uint32_t *lowor;
+    OutlierSink sink;
+};
+template <class T, bool Last, bool Quant>
+__global__ void __launch_bounds__(kRowThreads) k_rows(T *__restrict__ state, PassDesc p, uint32_t X, uint32_t x0,
+                                                      double eb, bool cubic, const uint32_t *__restrict__ merged,
+                                                      RowsQuant qz) {
     using Vec = typename std::conditional<sizeof(T) == 4, float4, double2>::type;
     constexpr int V = 16 / (int)sizeof(T);
-    constexpr int CH = kRowThreads * V;
-    const uint32_t bz = blockIdx.z, by = blockIdx.y;
+    const uint32_t tx = blockDim.x, CH = tx * V;
+    const uint32_t bz = blockIdx.z, by = blockIdx.y * blockDim.y + threadIdx.y;
+    const bool rowok = by < p.cnt[1];  // (no early return: barrier / warp reduction below)
     const uint64_t row = p.start_flat - x0 + (uint64_t)bz * p.step_flat[0] + (uint64_t)by * p.step_flat[1];
     const uint64_t obase = p.ordinal_base + ((uint64_t)bz * p.cnt[1] + by) * p.cnt[2];
     const uint32_t xb = blockIdx.x * CH, xs = xb + threadIdx.x * V;
-    const bool in = xs < X;  // X % V == 0
-    T e[V];
-    if (in) {
-        const Vec v = *reinterpret_cast<const Vec *>(state + row + xs);
+    const bool in = rowok && xs < X;  // X % V == 0
+    auto ldv = [&](const T *src, T *o) {
+        const Vec v = *reinterpret_cast<const Vec *>(src);
         const T *vv = reinterpret_cast<const T *>(&v);
 #pragma unroll
-        for (int k = 0; k < V; ++k) e[k] = vv[k];
+        for (int k = 0; k < V; ++k) o[k] = vv[k];
+    };
+    T e[V], val[V];
+    if (in) {
+        ldv(state + row + xs, e);
+        if constexpr (Quant) ldv(static_cast<const T *>(qz.values) + row + xs, val);
     }
+    uint32_t orv = 0;
+    // the target at element k with prediction `pred`
+    auto finish = [&](int k, uint32_t x, T pred) {
+        const uint64_t o = obase + (x >> 1);
+        if constexpr (Quant) {
+            int32_t code;
+            T recon;
+            const bool outl = quantize_residual<T>(val[k], pred, eb, code, recon);
+            e[k] = outl ? val[k] : recon;
+            const uint32_t w = to_negabinary(code);
+            qz.nb[o] = w;
+            orv |= w;
+            if (outl) {
+                const unsigned long long slot = atomicAdd(qz.sink.count, 1ull);
+                qz.sink.ordinal[slot] = o;
+                qz.sink.bits[slot] = bits_of<T>(val[k]);
+            }
+        } else {
+            e[k] = reconstruct_value<T>(pred, eb, (int64_t)from_negabinary(merged[o]));
+        }
+    };
     if constexpr (Last) {
-        __shared__ T sm[CH + 8];
-        for (int i = (int)threadIdx.x - 4; i < CH + 4; i += kRowThreads) {
-            if (i >= 0 && i < CH) continue;
+        extern __shared__ __align__(16) unsigned char rsm[];
+        T *sm = reinterpret_cast<T *>(rsm) + (size_t)threadIdx.y * (CH + 8);
+        if (rowok && threadIdx.x < 8) {  // 4-element halo on each side
+            const int i = threadIdx.x < 4 ? (int)threadIdx.x - 4 : (int)CH + (int)threadIdx.x - 4;
             const int64_t x = (int64_t)xb + i;
             if (x >= 0 && x < (int64_t)X) sm[i + 4] = state[row + x];
         }
@@ -490,34 +527,28 @@ __global__ void __launch_bounds__(kRowThreads) k_recon_rows(T *__restrict__ stat
             for (int k = 0; k < V; ++k) sm[threadIdx.x * V + k + 4] = e[k];
         }
         __syncthreads();
-        if (!in) return;
+        if (in) {
 #pragma unroll
-        for (int k = 0; k < V; ++k) {
-            const uint32_t x = xs + k;
-            if ((x & 1u) != x0) continue;
-            const T *c = sm + (x - xb) + 4;  // c[0] = element x
-            T pred;
-            if (cubic && x >= 3 && x + 3 < X) pred = ((T)9 * (c[-1] + c[1]) - (c[-3] + c[3])) / (T)16;
-            else if (x + 1 < X) pred = (c[-1] + c[1]) / (T)2;
-            else pred = c[-1];
-            e[k] = reconstruct_value<T>(pred, eb, (int64_t)from_negabinary(merged[obase + (x >> 1)]));
+            for (int k = 0; k < V; ++k) {
+                const uint32_t x = xs + k;
+                if ((x & 1u) != x0) continue;
+                const T *c = sm + (x - xb) + 4;  // c[0] = element x
+                T pred;
+                if (cubic && x >= 3 && x + 3 < X) pred = ((T)9 * (c[-1] + c[1]) - (c[-3] + c[3])) / (T)16;
+                else if (x + 1 < X) pred = (c[-1] + c[1]) / (T)2;
+                else pred = c[-1];
+                finish(k, x, pred);
+            }
         }
-    } else {
-        if (!in) return;
+    } else if (in) {
         const uint64_t coord = p.axis_start + (uint64_t)(p.axis == 0 ? bz : by) * p.axis_step;
         const uint64_t stp = p.st;
         const bool cub = cubic && coord >= 3 * p.s && coord + 3 * p.s < p.extent;
         const bool lin = coord + p.s < p.extent;
-        auto ld = [&](uint64_t f, T *o) {
-            const Vec v = *reinterpret_cast<const Vec *>(state + f);
-            const T *vv = reinterpret_cast<const T *>(&v);
-#pragma unroll
-            for (int k = 0; k < V; ++k) o[k] = vv[k];
-        };
         T a[V], b[V], c[V], d[V];
-        ld(row + xs - stp, b);
-        if (lin) ld(row + xs + stp, c);
-        if (cub) ld(row + xs - 3 * stp, a), ld(row + xs + 3 * stp, d);
+        ldv(state + row + xs - stp, b);
+        if (lin) ldv(state + row + xs + stp, c);
+        if (cub) ldv(state + row + xs - 3 * stp, a), ldv(state + row + xs + 3 * stp, d);
 #pragma unroll
         for (int k = 0; k < V; ++k) {
             const uint32_t x = xs + k;
@@ -526,14 +557,20 @@ __global__ void __launch_bounds__(kRowThreads) k_recon_rows(T *__restrict__ stat
             if (cub) pred = ((T)9 * (b[k] + c[k]) - (a[k] + d[k])) / (T)16;
             else if (lin) pred = (b[k] + c[k]) / (T)2;
             else pred = b[k];
-            e[k] = reconstruct_value<T>(pred, eb, (int64_t)from_negabinary(merged[obase + (x >> 1)]));
+            finish(k, x, pred);
         }
     }
-    Vec v;
-    T *vv = reinterpret_cast<T *>(&v);
+    if (in) {
+        Vec v;
+        T *vv = reinterpret_cast<T *>(&v);
 #pragma unroll
-    for (int k = 0; k < V; ++k) vv[k] = e[k];
-    *reinterpret_cast<Vec *>(state + row + xs) = v;
+        for (int k = 0; k < V; ++k) vv[k] = e[k];
+        *reinterpret_cast<Vec *>(state + row + xs) = v;
+    }
+    if constexpr (Quant) {
+        orv = __reduce_or_sync(0xffffffffu, orv);
+        if (lane_id() == 0 && (orv & ~*reinterpret_cast<volatile uint32_t *>(qz.lowor))) atomicOr(qz.lowor, orv);
+    }
 }
 
 // strictly increasing prefix of in-range ordinals = what the in-order matcher applies
@@ -609,10 +646,45 @@ static bool pass_box(const PassDesc &pd, PassDesc &q, dim3 &grid, dim3 &block) {
     return true;
 }
 
+template <bool Quant>
+static void launch_rows(void *state, int scalar, const PassDesc &q, uint32_t X, uint32_t x0, double eb, bool cubic,
+                        const uint32_t *merged, RowsQuant qz, cudaStream_t st) {
+    const int w = scalar == 0 ? 4 : 8, V = 16 / w;
+    const unsigned tx = (unsigned)std::min<uint64_t>(kRowThreads, ((uint64_t)X / V + 31) / 32 * 32);
+    const unsigned ty = kRowThreads / tx;
+    const dim3 blk(tx, ty, 1);
+    const dim3 g((X + tx * V - 1) / (tx * V), (unsigned)((q.cnt[1] + ty - 1) / ty), (unsigned)q.cnt[0]);
+    const size_t smem = q.axis == 2 ? (size_t)ty * (tx * V + 8) * w : 0;
+    if (scalar == 0) {
+        if (q.axis == 2) k_rows<float, true, Quant><<<g, blk, smem, st>>>((float *)state, q, X, x0, eb, cubic, merged, qz);
+        else k_rows<float, false, Quant><<<g, blk, 0, st>>>((float *)state, q, X, x0, eb, cubic, merged, qz);
+    } else {
+        if (q.axis == 2) k_rows<double, true, Quant><<<g, blk, smem, st>>>((double *)state, q, X, x0, eb, cubic, merged, qz);
+        else k_rows<double, false, Quant><<<g, blk, 0, st>>>((double *)state, q, X, x0, eb, cubic, merged, qz);
+    }
+    CKL();
+}
+
+// a level-1 pass whose targets are every other element of whole rows of the last axis
+static bool rows_applicable(const PassDesc &q, uint64_t X, int w, const void *state, uint32_t &x0) {
+    if (q.s != 1 || q.axis < 0 || X < 2 || X % (16 / w) != 0 || (reinterpret_cast<uintptr_t>(state) & 15)) return false;
+    if (q.step_flat[2] != 2 || q.cnt[1] > 65535 || q.cnt[0] > 65535 || X >= (1u << 31)) return false;
+    x0 = (uint32_t)(q.start_flat % X);
+    if (x0 > 1 || q.cnt[2] != (X - x0 + 1) / 2) return false;
+    if (q.axis == 2) return x0 == 1 && q.st == 1;
+    return x0 == 0 && q.st % (16 / w) == 0;  // stencil rows stay 16-byte aligned
+}
+
 void launch_quant_pass(const void *values, void *state, int scalar, bool cubic, const PassDesc &pd, double eb,
-                       uint32_t *nb, uint32_t *lowor, OutlierSink sink, cudaStream_t st) {
+                       uint32_t *nb, uint32_t *lowor, OutlierSink sink, uint64_t row_len, cudaStream_t st) {
     PassDesc q;
     dim3 grid, block;
+    uint32_t x0 = 0;
+    if (pass_box(pd, q, grid, block) && (reinterpret_cast<uintptr_t>(values) & 15) == 0 &&
+        rows_applicable(q, row_len, scalar == 0 ? 4 : 8, state, x0)) {
+        launch_rows<true>(state, scalar, q, (uint32_t)row_len, x0, eb, cubic, nullptr, RowsQuant{values, nb, lowor, sink}, st);
+        return;
+    }
     if (pass_box(pd, q, grid, block)) {
         if (scalar == 0)
             k_quant_pass<float, true, true><<<grid, block, 0, st>>>((const float *)values, (float *)state, q, eb, cubic, nb, lowor, sink);
@@ -701,33 +773,13 @@ void launch_merge(const uint32_t *const *rows, const uint32_t *merged_in, uint32
     CKL();
 }
 
-// a level-1 pass whose targets are every other element of whole rows of the last axis
-static bool rows_applicable(const PassDesc &q, uint64_t X, int w, const void *state, uint32_t &x0) {
-    if (q.s != 1 || q.axis < 0 || X < 2 || X % (16 / w) != 0 || (reinterpret_cast<uintptr_t>(state) & 15)) return false;
-    if (q.step_flat[2] != 2 || q.cnt[1] > 65535 || q.cnt[0] > 65535 || X >= (1u << 31)) return false;
-    x0 = (uint32_t)(q.start_flat % X);
-    if (x0 > 1 || q.cnt[2] != (X - x0 + 1) / 2) return false;
-    if (q.axis == 2) return x0 == 1 && q.st == 1;
-    return x0 == 0 && q.st % (16 / w) == 0;  // stencil rows stay 16-byte aligned
-}
-
 void launch_recon_pass(void *state, int scalar, bool cubic, const PassDesc &pd, double eb, const uint32_t *merged,
                        uint64_t row_len, cudaStream_t st) {
     PassDesc q;
     dim3 grid, block;
     uint32_t x0 = 0;
     if (pass_box(pd, q, grid, block) && rows_applicable(q, row_len, scalar == 0 ? 4 : 8, state, x0)) {
-        const unsigned ch = kRowThreads * (scalar == 0 ? 4 : 2);
-        const dim3 g((unsigned)((row_len + ch - 1) / ch), (unsigned)q.cnt[1], (unsigned)q.cnt[0]);
-        const uint32_t X = (uint32_t)row_len;
-        if (scalar == 0) {
-            if (q.axis == 2) k_recon_rows<float, true><<<g, kRowThreads, 0, st>>>((float *)state, q, X, x0, eb, cubic, merged);
-            else k_recon_rows<float, false><<<g, kRowThreads, 0, st>>>((float *)state, q, X, x0, eb, cubic, merged);
-        } else {
-            if (q.axis == 2) k_recon_rows<double, true><<<g, kRowThreads, 0, st>>>((double *)state, q, X, x0, eb, cubic, merged);
-            else k_recon_rows<double, false><<<g, kRowThreads, 0, st>>>((double *)state, q, X, x0, eb, cubic, merged);
-        }
-        CKL();
+        launch_rows<false>(state, scalar, q, (uint32_t)row_len, x0, eb, cubic, merged, RowsQuant{}, st);
         return;
     }
     if (pass_box(pd, q, grid, block)) {

@@ -29,7 +29,7 @@ struct OutlierSink {
 void launch_range(const void *values, int scalar, uint64_t n, double *scratch /*2*1024*/, double *out2,
                   cudaStream_t st);
 void launch_quant_pass(const void *values, void *state, int scalar, bool cubic, const PassDesc &pd, double eb,
-                       uint32_t *nb, uint32_t *lowor, OutlierSink sink, cudaStream_t st);
+                       uint32_t *nb, uint32_t *lowor, OutlierSink sink, uint64_t row_len, cudaStream_t st);
 void launch_bitplanes(const uint32_t *nb, uint64_t count, uint32_t *planes, uint64_t plane_stride_words,
                       cudaStream_t st);
 void launch_loss_pass(const uint32_t *nb, double *dev, const PassDesc &pd, bool cubic, double unit, int d,
