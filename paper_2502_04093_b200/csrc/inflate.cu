@@ -29,6 +29,12 @@
 #include <cooperative_groups.h>
 namespace cg = cooperative_groups;
 
+#ifndef IPCG_SUBB
+#define IPCG_SUBB 512
+#endif
+#ifndef IPCG_NPH
+#define IPCG_NPH 2
+#endif
 #ifndef IPCG_SEG
 #define IPCG_SEG 128
 #endif
@@ -186,68 +192,39 @@ __device__ bool read_dynamic_header(Bits &b, uint8_t *lens, int &nlen, int &ndis
 }
 
 // ----------------------------------------------------------- fast warp tables
+// k_decode_cands' tables: canonical counts/symbols (codes longer than the table) plus a
+// resolved table indexed by the next BITS stream bits: code length (0 = longer code) |
+// kind << 4 | extra bits << 6 | value << 16.  kind 0 literal (value = byte), 1 length or
+// distance (value = base), 2 end of block, 3 invalid symbol.  A literal/length table of
+// 11 bits leaves almost no code to the canonical loop (which diverges a lane-parallel warp).
+constexpr int LITBITS = 11, DISTBITS = 10;
+template <int BITS>
 struct Huff {
     uint16_t count[16];
     uint16_t first[16];
     uint16_t offs[16];
     uint16_t sym[320];
-    uint16_t fast[1 << FASTBITS];  // (len << 12) | symbol, 0 = slow path
-    // k_decode_cands' resolved entries: code length (0 = slow path) | kind << 4 | extra bits
-    // << 6 | value << 16.  lit/len table: kind 0 literal (value = byte), 1 length (value =
-    // base length), 2 end of block / invalid symbol (general path); distance table: kind 1
-    // (value = base distance), 2 invalid.  Code + extra bits fit one refill (9 + 13 < 33).
-    uint32_t fx[1 << FASTBITS];
+    uint32_t fx[1 << BITS];
 };
 
-// build from lengths on the whole warp (lengths already validated)
-__device__ void huff_build(Huff &h, const uint8_t *lens, int n, unsigned lane) {
-    if (lane == 0) {
-        for (int i = 0; i < 16; ++i) h.count[i] = 0;
-        for (int i = 0; i < n; ++i) h.count[lens[i]]++;
-        h.count[0] = 0;
-        h.offs[1] = 0;
-        for (int l = 1; l < 15; ++l) h.offs[l + 1] = (uint16_t)(h.offs[l] + h.count[l]);
-        uint16_t code = 0;
-        for (int l = 1; l <= 15; ++l) {
-            code = (uint16_t)((code + h.count[l - 1]) << 1);
-            h.first[l] = code;
-        }
-        uint16_t o[16];
-        for (int l = 0; l < 16; ++l) o[l] = h.offs[l];
-        for (int i = 0; i < n; ++i)
-            if (lens[i]) h.sym[o[lens[i]]++] = (uint16_t)i;
-    }
-    __syncwarp();
-    for (int i = lane; i < (1 << FASTBITS); i += 32) h.fast[i] = 0;
-    __syncwarp();
-    int total = 0;
-    for (int l = 1; l <= 15; ++l) total += h.count[l];
-    for (int t = lane; t < total; t += 32) {
-        int L = 1;
-        while (L < 15 && !(t >= h.offs[L] && t < h.offs[L] + h.count[L])) ++L;
-        if (L > FASTBITS) continue;
-        const uint32_t code = h.first[L] + (uint32_t)(t - h.offs[L]);
-        const uint32_t rev = __brev(code) >> (32 - L);
-        for (uint32_t e = 0; e < (1u << (FASTBITS - L)); ++e) h.fast[rev | (e << L)] = (uint16_t)((L << 12) | h.sym[t]);
-    }
-    __syncwarp();
-}
-
-// the same for a group of G lanes (gl = lane within the group); every lane of the warp
-// calls it (inactive groups pass active = false) so the warp-wide syncs line up
 __device__ __forceinline__ uint32_t fx_entry(uint32_t L, uint32_t sym, bool dist) {
-    uint32_t kind = 2, ext = 0, val = 0;
+    uint32_t kind = 3, ext = 0, val = 0;
     if (dist) {
         if (sym < 30) kind = 1, ext = kDExt[sym], val = kDBase[sym];
     } else if (sym < 256) {
         kind = 0, val = sym;
-    } else if (sym >= 257 && sym < 286) {
+    } else if (sym == 256) {
+        kind = 2;
+    } else if (sym < 286) {
         kind = 1, ext = kLExt[sym - 257], val = kLBase[sym - 257];
     }
     return L | kind << 4 | ext << 6 | val << 16;
 }
 
-__device__ void huff_build_group(Huff &h, const uint8_t *lens, int n, unsigned gl, unsigned G, bool active,
+// built by a group of G lanes (gl = lane within the group); every lane of the warp calls it
+// (inactive groups pass active = false) so the warp-wide syncs line up
+template <int BITS>
+__device__ void huff_build_group(Huff<BITS> &h, const uint8_t *lens, int n, unsigned gl, unsigned G, bool active,
                                  bool dist) {
     if (active && gl == 0) {
         for (int i = 0; i < 16; ++i) h.count[i] = 0;
@@ -267,7 +244,7 @@ __device__ void huff_build_group(Huff &h, const uint8_t *lens, int n, unsigned g
     }
     __syncwarp();
     if (active)
-        for (int i = gl; i < (1 << FASTBITS); i += G) h.fast[i] = 0, h.fx[i] = 0;
+        for (int i = gl; i < (1 << BITS); i += G) h.fx[i] = 0;
     __syncwarp();
     if (active) {
         int total = 0;
@@ -275,116 +252,69 @@ __device__ void huff_build_group(Huff &h, const uint8_t *lens, int n, unsigned g
         for (int t = gl; t < total; t += G) {
             int L = 1;
             while (L < 15 && !(t >= h.offs[L] && t < h.offs[L] + h.count[L])) ++L;
-            if (L > FASTBITS) continue;
+            if (L > BITS) continue;
             const uint32_t code = h.first[L] + (uint32_t)(t - h.offs[L]);
             const uint32_t rev = __brev(code) >> (32 - L);
             const uint32_t fx = fx_entry((uint32_t)L, h.sym[t], dist);
-            for (uint32_t e = 0; e < (1u << (FASTBITS - L)); ++e) {
-                h.fast[rev | (e << L)] = (uint16_t)((L << 12) | h.sym[t]);
-                h.fx[rev | (e << L)] = fx;
-            }
+            for (uint32_t e = 0; e < (1u << (BITS - L)); ++e) h.fx[rev | (e << L)] = fx;
         }
     }
     __syncwarp();
 }
 
-__device__ __forceinline__ int huff_decode(const Huff &h, Bits &b) {
-    const uint32_t e = h.fast[b.peek(FASTBITS)];
-    if (e) {
-        b.drop((int)(e >> 12));
-        return (int)(e & 0xfff);
-    }
+// the table entry for the code at the start of bb, the canonical loop for a longer code
+template <int BITS>
+__device__ __forceinline__ uint32_t huff_entry(const Huff<BITS> &h, uint64_t bb, bool dist) {
+    const uint32_t e = h.fx[(uint32_t)bb & ((1u << BITS) - 1)];
+    if (e & 15u) return e;
     int code = 0, first = 0, index = 0;
-    for (int len = 1; len <= 15; ++len) {
-        code |= (int)b.get(1);
-        const int count = h.count[len];
-        if (code - count < first) return h.sym[index + (code - first)];
-        index += count;
-        first += count;
-        first <<= 1;
-        code <<= 1;
-    }
-    return -1;
-}
-
-// ---------------------------------------------------- word-refill bit reader
-// 64-bit buffer refilled 32 bits at a time from 4-byte-aligned words (the stream may start
-// at any byte; words wholly past its last byte read as 0).  Used by the symbol loops.
-struct WBits {
-    const uint32_t *w;
-    uint64_t nwords;  // words covering [aligned base, src + len)
-    uint64_t wi;      // index of the word held in `nxt`
-    uint32_t nxt;     // word wi, loaded one refill ahead so its latency overlaps the decode
-    uint64_t buf;
-    int cnt;
-    uint64_t endbit;  // absolute bit position of the end of the stream
-    // absolute bit position (relative to the aligned base) of buf bit 0: words before wi are
-    // in (or past) the buffer, so it is derived instead of being advanced on every drop
-    __device__ __forceinline__ uint64_t pos() const { return wi * 32 - (uint64_t)cnt; }
-    __device__ __forceinline__ void init(const uint8_t *src, uint64_t len, uint64_t bit) {
-        const uintptr_t a = reinterpret_cast<uintptr_t>(src);
-        const uint64_t off = (uint64_t)(a & 3) * 8;
-        w = reinterpret_cast<const uint32_t *>(a & ~uintptr_t(3));
-        nwords = (off / 8 + len + 3) / 4;
-        endbit = off + 8 * len;
-        const uint64_t abs = off + bit;
-        wi = abs >> 5;
-        nxt = wi < nwords ? __ldg(w + wi) : 0u;
-        buf = 0;
-        cnt = 0;
-        refill();
-        refill();
-        drop((int)(abs & 31));
-    }
-    __device__ __forceinline__ void refill() {
-        if (cnt <= 32) {
-            buf |= (uint64_t)nxt << cnt;
-            ++wi;
-            nxt = wi < nwords ? __ldg(w + wi) : 0u;
-            cnt += 32;
-        }
-    }
-    __device__ __forceinline__ void drop(int k) {
-        buf >>= k;
-        cnt -= k;
-    }
-    __device__ __forceinline__ uint32_t take(int k) {  // k <= cnt
-        const uint32_t v = (uint32_t)(buf & ((1ull << k) - 1));
-        drop(k);
-        return v;
-    }
-    __device__ __forceinline__ bool overrun() const { return pos() > endbit; }
-};
-
-// Huffman decode from the buffer (needs >= 15 valid bits)
-__device__ __forceinline__ int huff_decode_w(const Huff &h, WBits &b) {
-    const uint32_t e = h.fast[b.buf & ((1u << FASTBITS) - 1)];
-    if (e) {
-        b.drop((int)(e >> 12));
-        return (int)(e & 0xfff);
-    }
-    int code = 0, first = 0, index = 0;
-    uint64_t bb = b.buf;
-    for (int len = 1; len <= 15; ++len) {
+    for (int l = 1; l <= 15; ++l) {
         code |= (int)(bb & 1);
         bb >>= 1;
-        const int count = h.count[len];
-        if (code - count < first) {
-            b.drop(len);
-            return h.sym[index + (code - first)];
-        }
+        const int count = h.count[l];
+        if (code - count < first) return fx_entry((uint32_t)l, h.sym[index + (code - first)], dist);
         index += count;
         first += count;
         first <<= 1;
         code <<= 1;
     }
-    return -1;
+    return 0u;  // no code: invalid
 }
 
 // symbol words: literal = byte; match = 1<<31 | len << 16 | dist  (len <= 258, dist <= 32768)
 __device__ __forceinline__ uint32_t sym_lit(uint32_t c) { return c; }
 __device__ __forceinline__ uint32_t sym_match(uint32_t len, uint32_t dist) {
     return 0x80000000u | (len << 16) | (dist - 1);
+}
+
+// One whole deflate symbol (literal, or length + distance with their extra bits) at the start
+// of a 64-bit window.  kind: 0 literal, 1 match, 2 end of block, 3 invalid; nbits = bits used.
+__device__ __forceinline__ uint32_t decode_symbol(const Huff<LITBITS> &lit, const Huff<DISTBITS> &dist, uint64_t bb,
+                                                  uint32_t &kind, uint32_t &nbits, uint32_t &blen) {
+    const uint32_t e = huff_entry(lit, bb, false);
+    const uint32_t k = (e >> 4) & 3u, cl = e & 15u;
+    if (cl == 0u || k >= 2u) {
+        kind = cl == 0u ? 3u : k;
+        nbits = cl;
+        return 0;
+    }
+    if (k == 0u) {
+        kind = 0, nbits = cl, blen = 1;
+        return sym_lit(e >> 16);
+    }
+    const uint32_t ext = (e >> 6) & 15u;
+    const uint32_t len = (e >> 16) + ((uint32_t)(bb >> cl) & ((1u << ext) - 1u));
+    const uint64_t rest = bb >> (cl + ext);
+    const uint32_t ed = huff_entry(dist, rest, true);
+    const uint32_t dcl = ed & 15u;
+    if (dcl == 0u || ((ed >> 4) & 3u) != 1u) {
+        kind = 3;
+        return 0;
+    }
+    const uint32_t dext = (ed >> 6) & 15u;
+    const uint32_t d = (ed >> 16) + ((uint32_t)(rest >> dcl) & ((1u << dext) - 1u));
+    kind = 1, nbits = cl + ext + dcl + dext, blen = len;
+    return sym_match(len, d);
 }
 
 // ------------------------------------------------------------------ state
@@ -568,15 +498,24 @@ __global__ void __launch_bounds__(256) k_scan(const InflateJob *jobs, const Tabl
 // CPW candidates per warp, one per group of 32/CPW lanes: the decode is inherently
 // sequential per block and every lane of a group does the same work, so packing several
 // blocks into a warp divides the (issue-bound) warp-instruction count.
-constexpr int DWARPS = 4 / IPCG_CPW;  // warps per k_decode_cands CTA (static smem: DWARPS * CPW table slots)
+constexpr int SUBB = IPCG_SUBB;      // bits per lane subsequence (lane-parallel candidate decode)
+constexpr int MARKW = SUBB / 32;     // its symbol-start bitmap words
+constexpr int NPH = IPCG_NPH;         // speculative start phases after a loss of synchronisation
+constexpr int DWARPS = 2;  // warps per k_decode_cands CTA (static smem: ~16 KB of tables + bitmaps per warp)
 
 template <int CPW>
 __global__ void __launch_bounds__(DWARPS * 32) k_decode_cands(const InflateJob *jobs, const Tables *tabs, Cand *cands,
                                                            const unsigned long long *ncand_total, uint64_t cand_cap,
                                                            uint32_t *pool, uint32_t *ckpt_pool) {
+    static_assert(CPW == 1, "the speculative decode runs all 32 lanes of a warp on one candidate");
     constexpr unsigned G = 32 / CPW;
-    __shared__ Huff lit_s[DWARPS * CPW], dist_s[DWARPS * CPW];
+    __shared__ Huff<LITBITS> lit_s[DWARPS * CPW];
+    __shared__ Huff<DISTBITS> dist_s[DWARPS * CPW];
     __shared__ uint8_t lens_s[DWARPS * CPW][320];
+    __shared__ uint32_t marks_s[DWARPS][NPH * 32 * MARKW];
+    __shared__ uint32_t li_e1[DWARPS][NPH][32], li_x[DWARPS][NPH][32];  // per lane and phase
+    __shared__ int8_t li_sync[DWARPS][NPH][32];
+    __shared__ uint8_t li_fl[DWARPS][NPH][32];  // 1: path ends in own subsequence, 2: in the next  // symbol-start bitmaps of the lane subsequences
     const unsigned w = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const unsigned sub = lane / G, gl = lane % G, slot = w * CPW + sub;
     const uint64_t n = min((unsigned long long)cand_cap, *ncand_total);
@@ -608,100 +547,193 @@ __global__ void __launch_bounds__(DWARPS * 32) k_decode_cands(const InflateJob *
         uint32_t ns = 0, nz = 0;
         uint32_t bytes = 0;  // <= 16383 symbols x 258 bytes
         bool good = true;
-        WBits wb;
-        wb.init(job.src, job.src_len, b.used);
-        // segments of SEG symbols: the checkpoint and the overrun test once per segment, a
-        // tight decode loop inside (same outcome as testing every symbol: an overrun stays
-        // an overrun, and the final test below catches one inside the last segment)
-        for (;;) {
-            if (ns >= MAXSYM) {  // only an end-of-block may follow MAXSYM symbols
-                wb.refill();
-                if (huff_decode_w(lit_s[slot], wb) != 256) good = false;
-                break;
-            }
-            if (gl == 0) ckpt_pool[ci * NCKPT + ns / SEG] = (uint32_t)bytes;
-            if (wb.overrun()) {
+        // Lane-parallel decode with self-synchronisation.  A round covers 32 subsequences of
+        // SUBB bits from the round's (true) start: lane i decodes subsequence i speculatively
+        // from its first bit, marking its symbol starts in shared memory (P1), then continues
+        // into subsequence i+1 until it meets a start lane i+1 marked (P2: from there the two
+        // paths coincide).  Lane 0 starts on the true path, so by induction every lane whose
+        // left neighbour synchronised is on the true path from its sync point; the round covers
+        // lanes up to the first one without a sync (its true exit is its left neighbour's
+        // continued exit) or the end of block.  P3 decodes each lane's true range counting
+        // symbols and bytes, a warp scan places them, P4 decodes again and writes them (with the
+        // SEG checkpoints).  Canonical Huffman codes resynchronise within a few symbols; a block
+        // that never does still advances >= 2 subsequences per round.
+        const uintptr_t sa = reinterpret_cast<uintptr_t>(job.src);
+        const uint64_t off = (uint64_t)(sa & 3) * 8;
+        const uint32_t *W = reinterpret_cast<const uint32_t *>(sa & ~uintptr_t(3));
+        const uint64_t nwords = (off / 8 + job.src_len + 3) / 4, endbit = off + 8 * job.src_len;
+        auto window = [&](uint64_t P) {
+            const uint64_t k = P >> 5;
+            const uint32_t sh = (uint32_t)(P & 31);
+            const uint32_t w0 = k < nwords ? __ldg(W + k) : 0u, w1 = k + 1 < nwords ? __ldg(W + k + 1) : 0u,
+                           w2 = k + 2 < nwords ? __ldg(W + k + 2) : 0u;
+            return (uint64_t)__funnelshift_r(w0, w1, sh) | ((uint64_t)__funnelshift_r(w1, w2, sh) << 32);
+        };
+        uint32_t *marks = marks_s[w];  // [32 lanes][MARKW words]
+        const uint32_t subb = SUBB;
+        // Periodic streams can keep an off-phase path off-phase forever (a run of one 2-bit
+        // match symbol: a path started one bit late decodes the same symbols shifted).  After a
+        // round that lost synchronisation every lane also runs its subsequence from the next
+        // NPH-1 bit offsets, and a left neighbour may synchronise with any of those paths.
+        int nph = 1;
+        uint64_t base = off + b.used;
+        bool eob = false;
+        while (good && !eob) {
+            if (base > endbit) {  // overrun (the stream reads as zeros past its end)
                 good = false;
                 break;
             }
-            const uint32_t seg_end = min(ns + (uint32_t)SEG, (uint32_t)MAXSYM);
-            bool eob = false;
-            while (ns < seg_end) {
-                wb.refill();  // >= 33 bits: a literal/length code and its extra bits
-                {  // resolved fast-table entries: literals and whole matches in a few instructions
-                    const uint32_t e = lit_s[slot].fx[(uint32_t)wb.buf & ((1u << FASTBITS) - 1)];
-                    const uint32_t kind = (e >> 4) & 3u;
-                    if ((e & 15u) && kind == 0u) {
-                        wb.drop((int)(e & 15u));
-                        const uint32_t sym = e >> 16;
-                        if (gl == 0) out[ns] = sym_lit(sym);
-                        nz |= sym;
-                        ++ns;
-                        ++bytes;
-                        continue;
-                    }
-                    if ((e & 15u) && kind == 1u) {
-                        const uint32_t cl = e & 15u, ext = (e >> 6) & 15u;
-                        const uint32_t len = (e >> 16) + ((uint32_t)(wb.buf >> cl) & ((1u << ext) - 1u));
-                        wb.drop((int)(cl + ext));
-                        wb.refill();
-                        const uint32_t ed = dist_s[slot].fx[(uint32_t)wb.buf & ((1u << FASTBITS) - 1)];
-                        uint32_t d;
-                        if ((ed & 15u) && ((ed >> 4) & 3u) == 1u) {
-                            const uint32_t dcl = ed & 15u, dext = (ed >> 6) & 15u;
-                            d = (ed >> 16) + ((uint32_t)(wb.buf >> dcl) & ((1u << dext) - 1u));
-                            wb.drop((int)(dcl + dext));
-                        } else {
-                            const int ds = huff_decode_w(dist_s[slot], wb);
-                            if (ds < 0 || ds >= 30) {
-                                good = false;
-                                break;
-                            }
-                            d = kDBase[ds] + wb.take(kDExt[ds]);
+            const uint64_t g = base + (uint64_t)gl * subb, gn = g + subb;
+            // P1: speculative decode of my subsequence from nph bit offsets, marking symbol starts;
+            // per phase the exit (or the position of a path-ending symbol) goes to shared memory
+            // relative to `base` (per-phase registers cost the kernel 40 registers)
+            uint32_t nb, bl;
+            for (int ph = 0; ph < nph; ++ph) {
+                uint32_t *mk = marks + (ph * 32 + gl) * MARKW;
+                for (int q = 0; q < MARKW; ++q) mk[q] = 0u;
+                uint64_t p = g + ph;
+                uint32_t k1 = 0;
+                while (p < gn) {
+                    const uint32_t r = (uint32_t)(p - g);
+                    mk[r >> 5] |= 1u << (r & 31);
+                    decode_symbol(lit_s[slot], dist_s[slot], window(p), k1, nb, bl);
+                    if (k1 >= 2u) break;  // this path ends (end of block or invalid code) at p
+                    p += nb;
+                }
+                li_e1[w][ph][gl] = (uint32_t)(p - base);
+                li_fl[w][ph][gl] = k1 >= 2u ? 1 : 0;
+            }
+            __syncwarp();
+            // P2: each phase's path continues into subsequence gl+1 until it meets a symbol start
+            // of one of lane gl+1's paths (from there the two coincide)
+            for (int ph = 0; ph < nph; ++ph) {
+                int hit = -1;
+                uint8_t fl = li_fl[w][ph][gl];
+                uint64_t x = base + li_e1[w][ph][gl];
+                if (gl < 31 && !(fl & 1)) {
+                    const uint64_t g2 = gn + subb;
+                    while (x < g2) {
+                        const uint32_t r = (uint32_t)(x - gn);
+                        for (int q = 0; q < nph && hit < 0; ++q)
+                            if ((marks[(q * 32 + gl + 1) * MARKW + (r >> 5)] >> (r & 31)) & 1u) hit = q;
+                        if (hit >= 0) break;
+                        uint32_t k2;
+                        decode_symbol(lit_s[slot], dist_s[slot], window(x), k2, nb, bl);
+                        if (k2 >= 2u) {
+                            fl |= 2;
+                            break;
                         }
-                        if (gl == 0) out[ns] = sym_match(len, d);
-                        ++ns;
-                        bytes += len;
-                        continue;
+                        x += nb;
                     }
                 }
-                const int sym = huff_decode_w(lit_s[slot], wb);
-                if (sym < 256) {
-                    if (sym < 0) {
-                        good = false;
+                li_x[w][ph][gl] = (uint32_t)(x - base);
+                li_sync[w][ph][gl] = (int8_t)hit;
+                li_fl[w][ph][gl] = fl;
+            }
+            __syncwarp();
+            // resolve the true range [t_i, t_i+1) of every covered lane (uniform loop over shared
+            // memory): lane 0's phase 0 is the true path; lane i+1's true phase is the one lane
+            // i's true path met; a lane whose left neighbour met none is covered by that
+            // neighbour's continuation, and the round ends there
+            uint64_t my_t = 0, my_e = 0;
+            int last = -1;
+            bool lost = false, other = false;
+            {
+                uint64_t t = base;
+                int cur = 0;  // true phase of lane i, or -1: covered by lane i-1's continuation
+                uint64_t prev_x = 0;
+                bool prev_end2 = false;
+                for (int i = 0; i < 32; ++i) {
+                    uint64_t E;
+                    bool stop;
+                    if (cur >= 0) {
+                        E = base + li_e1[w][cur][i];
+                        stop = li_fl[w][cur][i] & 1;
+                        other |= cur != 0;
+                    } else {
+                        E = prev_x;
+                        stop = prev_end2;
+                    }
+                    if (gl == (unsigned)i) my_t = t, my_e = E;
+                    last = i;
+                    t = E;
+                    if (stop) break;  // end of block / invalid code inside lane i
+                    if (cur < 0) {
+                        lost = true;
                         break;
                     }
-                    if (gl == 0) out[ns] = sym_lit((uint32_t)sym);
-                    nz |= (uint32_t)sym;
-                    ++ns;
-                    ++bytes;
-                    continue;
+                    if (i == 31) break;
+                    prev_x = base + li_x[w][cur][i];
+                    prev_end2 = (li_fl[w][cur][i] & 2) != 0;
+                    cur = li_sync[w][cur][i];
                 }
-                if (sym == 256) {
-                    eob = true;
-                    break;
-                }
-                const int li = sym - 257;
-                if (li >= 29) {
-                    good = false;
-                    break;
-                }
-                const uint32_t len = kLBase[li] + wb.take(kLExt[li]);
-                wb.refill();  // >= 33 bits: a distance code and its extra bits
-                const int ds = huff_decode_w(dist_s[slot], wb);
-                if (ds < 0 || ds >= 30) {
-                    good = false;
-                    break;
-                }
-                const uint32_t d = kDBase[ds] + wb.take(kDExt[ds]);
-                if (gl == 0) out[ns] = sym_match(len, d);
-                ++ns;
-                bytes += len;
             }
-            if (!good || eob) break;
+            // speculate the other phases after a round that lost synchronisation within its first
+            // lanes (a phase-locked stream: the round covered almost nothing), and keep doing so
+            // while some lane's true path is one of them; a loss further on costs little
+            nph = ((lost && last < 4) || (nph > 1 && other)) ? NPH : 1;
+            // P3: count my true range (the range of the last covered lane may end at the block's
+            // end-of-block or at an invalid code)
+            const bool mine = (int)gl <= last;
+            uint32_t cnt = 0, byt = 0, kend = 0;
+            uint64_t q = my_t;
+            if (mine) {
+                while (q < my_e || (q == my_e && (int)gl == last)) {
+                    decode_symbol(lit_s[slot], dist_s[slot], window(q), kend, nb, bl);
+                    if (kend >= 2u) {
+                        q += kend == 2u ? nb : 0;
+                        break;
+                    }
+                    ++cnt;
+                    byt += bl;
+                    q += nb;
+                    if (q >= my_e && (int)gl != last) break;
+                    if (q >= my_e) break;
+                }
+            }
+            // the last covered lane tells how the round ended
+            const uint32_t kl = __shfl_sync(0xffffffffu, kend, last);
+            const uint64_t ql = __shfl_sync(0xffffffffu, q, last);
+            uint32_t ci_ = cnt, cb_ = byt;  // exclusive scans of counts and bytes
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const uint32_t a1 = __shfl_up_sync(0xffffffffu, ci_, o), a2 = __shfl_up_sync(0xffffffffu, cb_, o);
+                if ((int)gl >= o) ci_ += a1, cb_ += a2;
+            }
+            const uint32_t tot = __shfl_sync(0xffffffffu, ci_, 31), totb = __shfl_sync(0xffffffffu, cb_, 31);
+            const uint32_t sbase = ns + ci_ - cnt, bbase = bytes + cb_ - byt;
+            // P4: write my symbols (indices past MAXSYM are not stored: the block fails below)
+            if (mine && cnt) {
+                uint64_t r = my_t;
+                uint32_t bsum = bbase;
+                for (uint32_t m = 0; m < cnt; ++m) {
+                    uint32_t kk;
+                    const uint32_t sym = decode_symbol(lit_s[slot], dist_s[slot], window(r), kk, nb, bl);
+                    const uint32_t idx = sbase + m;
+                    if (idx < MAXSYM) {
+                        if (idx % SEG == 0) ckpt_pool[ci * NCKPT + idx / SEG] = bsum;
+                        out[idx] = sym;
+                    }
+                    if (kk == 0u) nz |= sym;
+                    bsum += bl;
+                    r += nb;
+                }
+            }
+            ns += tot;
+            bytes += totb;
+            if (ns > MAXSYM) good = false;  // only an end-of-block may follow MAXSYM symbols
+            if (kl == 3u) good = false;
+            if (kl == 2u) {
+                eob = true;
+                if (ns % SEG == 0 && ns < MAXSYM && gl == 0) ckpt_pool[ci * NCKPT + ns / SEG] = bytes;
+            }
+            base = (kl == 2u) ? ql : __shfl_sync(0xffffffffu, my_e, last);
+            __syncwarp();
         }
-        if (wb.overrun()) good = false;
-        b.used = wb.pos() - (uint64_t)(reinterpret_cast<uintptr_t>(job.src) & 3) * 8;
+        const uint64_t pos = base;
+        nz = __reduce_or_sync(0xffffffffu, nz);
+        if (pos > endbit) good = false;
+        b.used = pos - off;
         if (gl == 0) {
             c.ok = good ? 1 : 0;
             c.nzlit = nz != 0;

@@ -248,3 +248,50 @@ def test_inflate_against_zlib_streams(ctx):
     assert [str(g) for g in got] == ["deflate backend failed to decompress block", "block checksum mismatch",
                                      "deflate backend failed to decompress block",
                                      "deflate backend failed to decompress block", "identity block has wrong length"]
+
+
+def test_inflate_lane_parallel_decode_edge_streams(ctx):
+    """The lane-parallel candidate decode (inflate.cu k_decode_cands) on streams that defeat
+    self-synchronisation: long runs coded as a few-bit repeated match (phase-locked paths),
+    periodic symbol patterns of several periods, near-fixed-length literal codes, a dynamic block
+    of exactly the maximum symbol count, and corruptions deep inside long dynamic blocks."""
+    import zlib
+
+    rng = np.random.default_rng(23)
+    datas = [bytes(3_000_000),                                         # 258-byte dist-1 matches
+             (b"\x01" + bytes(257)) * 6000,                            # run + literal
+             bytes([0, 0, 0, 7]) * 200000,                             # 4-periodic
+             bytes(rng.integers(0, 2, 300000, dtype=np.uint8)),       # 1-bit literal codes
+             bytes(rng.integers(0, 4, 300000, dtype=np.uint8) * 64),  # 2-bit literal codes
+             rng.integers(0, 256, 200000, dtype=np.uint8).tobytes(),   # ~8-bit codes
+             bytes(rng.permutation(np.repeat(np.arange(256, dtype=np.uint8), 64)))]
+    blocks, want = [], []
+    for d in datas:
+        for level, strategy in ((6, zlib.Z_DEFAULT_STRATEGY), (1, zlib.Z_DEFAULT_STRATEGY),
+                                (6, zlib.Z_HUFFMAN_ONLY), (6, zlib.Z_RLE)):
+            c = zlib.compressobj(level, zlib.DEFLATED, 15, 8, strategy)
+            z = c.compress(d) + c.flush()
+            blocks.append((1, z, zlib.crc32(z), len(d)))
+            want.append(d)
+    got = ipc.backend_decode(blocks, ctx=ctx)
+    for g, w in zip(got, want):
+        assert g == w
+    # corruptions at several depths of a long dynamic stream: the error must surface exactly
+    # as zlib reports it (any failure -> the reference's message), never as wrong bytes
+    d = datas[5]
+    z0 = zlib.compress(d, 6)
+    bad = []
+    for frac in (0.01, 0.3, 0.62, 0.97):
+        z = bytearray(z0)
+        z[int(len(z) * frac)] ^= 0x10
+        bad.append((1, bytes(z), zlib.crc32(bytes(z)), len(d)))
+    got = ipc.backend_decode(bad, ctx=ctx)
+    for (be, z, crc, n), g in zip(bad, got):
+        try:
+            ok = zlib.decompress(z) == d
+        except zlib.error:
+            ok = False
+        if ok:
+            assert g == d
+        else:
+            assert str(g) == "deflate backend failed to decompress block"
