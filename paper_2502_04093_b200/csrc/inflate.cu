@@ -1072,6 +1072,29 @@ __device__ __forceinline__ void for_each_set(const uint32_t *bits, uint64_t word
     }
 }
 
+// every set flag, one thread per BYTE: the flag word is a warp broadcast, ptr/dst accesses of a
+// warp are 32 consecutive bytes (a thread per flag WORD made every lane's accesses 32 bytes
+// apart: one sector per lane per access, and run-heavy planes are almost all unresolved)
+// (a warp loads 32 flag words at once and skips the zero ones with a ballot; every thread of
+// the grid must call it: nth is a multiple of 32)
+template <class F>
+__device__ __forceinline__ void for_each_flagged(const uint32_t *bits, uint64_t nbytes, uint64_t tid, uint64_t nth,
+                                                 F &&f) {
+    const uint64_t nwords = (nbytes + 31) / 32;
+    const unsigned lane = (unsigned)(tid & 31);
+    for (uint64_t w0 = (tid >> 5) * 32; w0 < nwords; w0 += (nth >> 5) * 32) {
+        const uint32_t mine = w0 + lane < nwords ? bits[w0 + lane] : 0u;
+        unsigned nz = __ballot_sync(0xffffffffu, mine != 0u);
+        while (nz) {
+            const int k = __ffs(nz) - 1;
+            nz &= nz - 1;
+            const uint32_t word = __shfl_sync(0xffffffffu, mine, k);
+            const uint64_t t = (w0 + (uint64_t)k) * 32 + lane;
+            if ((word >> lane) & 1u) f(t);
+        }
+    }
+}
+
 __global__ void __launch_bounds__(256) k_resolve_all(const InflateJob *jobs, const Tables *tabs, const JobMeta *meta,
                                                     int njobs, unsigned *changed) {
     cg::grid_group grid = cg::this_grid();
@@ -1081,7 +1104,7 @@ __global__ void __launch_bounds__(256) k_resolve_all(const InflateJob *jobs, con
     for (int j = 0; j < njobs; ++j) {
         if (meta[j].status || meta[j].allzero) continue;
         const Tables T = tabs[j];
-        for_each_set(T.flags, (jobs[j].dst_len + 31) / 32, tid, nth, [&](uint64_t t) {
+        for_each_flagged(T.flags, jobs[j].dst_len, tid, nth, [&](uint64_t t) {
             const uint32_t s = T.ptr[t];
             if (flag_get(T.flags, s) && !flag_get(T.mark, s)) atomicOr(&T.mark[s >> 5], 1u << (s & 31));
         });
@@ -1114,7 +1137,7 @@ __global__ void __launch_bounds__(256) k_resolve_all(const InflateJob *jobs, con
         if (meta[j].status || meta[j].allzero) continue;
         const InflateJob job = jobs[j];
         const Tables T = tabs[j];
-        for_each_set(T.flags, (job.dst_len + 31) / 32, tid, nth, [&](uint64_t t) {
+        for_each_flagged(T.flags, job.dst_len, tid, nth, [&](uint64_t t) {
             uint32_t s = T.ptr[t];
             if (flag_get(T.flags, s)) s = T.ptr[s];
             job.dst[t] = job.dst[s];
