@@ -1146,18 +1146,39 @@ __global__ void __launch_bounds__(256) k_resolve_all(const InflateJob *jobs, con
 }
 
 // --------------------------------------------------------------- 6. checks
+// Adler-32 of the output: B = sum_i (n - i) b_i = n A - sum_i i b_i (mod 65521), 16-byte loads
+// from the first 16-byte boundary, dp4a sums and index-weighted sums, one modulo per thread
 __global__ void k_adler(const InflateJob *jobs, JobMeta *meta, unsigned long long *acc) {
     const int j = blockIdx.y;
     if (meta[j].status) return;
     const InflateJob job = jobs[j];
     const uint64_t n = job.dst_len;
-    unsigned long long A = 0, B = 0;
-    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
-        const uint32_t v = job.dst[i];
-        A += v;
-        B += (unsigned long long)((n - i) % 65521u) * v;
+    const uint64_t tid = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x, nth = (uint64_t)gridDim.x * blockDim.x;
+    const uint64_t head0 = (16 - (reinterpret_cast<uintptr_t>(job.dst) & 15)) & 15, head = head0 < n ? head0 : n;
+    const uint64_t nv = (n - head) / 16;
+    unsigned long long A = 0, W = 0;
+    const uint4 *pv = reinterpret_cast<const uint4 *>(job.dst + head);
+    for (uint64_t v = tid; v < nv; v += nth) {
+        const uint4 q = pv[v];
+        const uint32_t w[4] = {q.x, q.y, q.z, q.w};
+        uint32_t s = 0, ws = 0;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            const uint32_t sk = __dp4a(w[k], 0x01010101u, 0u);
+            s += sk;
+            ws += __dp4a(w[k], 0x03020100u, 0u) + 4u * k * sk;
+        }
+        A += s;
+        W += (unsigned long long)(head + 16 * v) * s + ws;
     }
-    B %= 65521u;
+    for (uint64_t i = tid; i < n; i += nth) {  // the unaligned head and the tail
+        if (i >= head && i < head + 16 * nv) continue;
+        const uint32_t b = job.dst[i];
+        A += b;
+        W += (unsigned long long)i * b;
+    }
+    const unsigned long long M = 65521;
+    unsigned long long B = ((n % M) * (A % M) + M - W % M) % M;
     for (int o = 16; o > 0; o >>= 1) {
         A += __shfl_down_sync(0xffffffffu, A, o);
         B += __shfl_down_sync(0xffffffffu, B, o);
@@ -1167,7 +1188,6 @@ __global__ void k_adler(const InflateJob *jobs, JobMeta *meta, unsigned long lon
         atomicAdd(&acc[2 * j + 1], B % 65521u);
     }
 }
-
 __global__ void k_finish(const InflateJob *jobs, int njobs, JobMeta *meta, const unsigned long long *acc, int *status) {
     const int j = blockIdx.x * blockDim.x + threadIdx.x;
     if (j >= njobs) return;
