@@ -1014,6 +1014,9 @@ __global__ void __launch_bounds__(WARPS * 32) k_emit(const InflateJob *jobs, con
             const uint32_t mv = __shfl_sync(0xffffffffu, v, l);
             const uint64_t mo = o + __shfl_sync(0xffffffffu, my_rel, l);
             const uint32_t len = (mv >> 16) & 0x1ff, d = (mv & 0xffff) + 1;
+            // i % d by a reciprocal multiply (exact for i < 2^16: i < len <= 258; d = 1 apart,
+            // whose reciprocal 2^32 does not fit)
+            const uint32_t rcp = 0xffffffffu / d + 1u;
             // every source byte precedes mo, so the lanes of one match never depend on each other;
             // unresolved bytes (sources in earlier segments) get a pointer, and their flag bits
             // are set with one ballot-aggregated atomic per 32 bytes
@@ -1022,7 +1025,7 @@ __global__ void __launch_bounds__(WARPS * 32) k_emit(const InflateJob *jobs, con
                 const bool act = i < len;
                 bool unres = false;
                 if (act) {
-                    const uint64_t src = mo - d + (d < len ? (i % d) : i);
+                    const uint64_t src = mo - d + (d < len ? (d == 1u ? 0u : i - d * __umulhi(i, rcp)) : i);
                     const uint64_t t = mo + i;
                     if (src >= b0) {
                         if (flag_get(T.flags, src)) {
