@@ -390,6 +390,7 @@ __global__ void __launch_bounds__(256) k_merge(const uint32_t *const *__restrict
 // for each word lane c takes bit c of every new plane word (a broadcast load), ORs in the
 // prefix's XOR-encoded digits and solves the recurrence.  One coalesced codeword load and
 // store per word; 4 words per warp iteration for memory-level parallelism.
+constexpr int MF_U = 8;  // plane words (x 32 codewords) per warp per step: loads in flight
 __global__ void __launch_bounds__(256) k_merge_few(const uint32_t *const *__restrict__ rows,
                                                    const uint32_t *__restrict__ merged_in,
                                                    uint32_t *__restrict__ merged_out, uint64_t count, int k0, int k1) {
@@ -402,10 +403,10 @@ __global__ void __launch_bounds__(256) k_merge_few(const uint32_t *const *__rest
 #pragma unroll
     for (int q = 0; q < 8; ++q) r[q] = q < np ? rows[k0 + q] : nullptr;
     const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
-    for (uint64_t w0 = (((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5) * 4; w0 < words; w0 += nwarps * 4) {
-        uint32_t m[4], e[4];
+    for (uint64_t w0 = (((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5) * MF_U; w0 < words; w0 += nwarps * MF_U) {
+        uint32_t m[MF_U], e[MF_U];
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
+        for (int u = 0; u < MF_U; ++u) {
             const uint64_t i = (w0 + u) * 32 + lane;
             m[u] = i < count ? __ldg(merged_in + i) & pre : 0u;
             e[u] = (m[u] ^ (m[u] >> 1) ^ (m[u] >> 2)) & pre;
@@ -414,13 +415,13 @@ __global__ void __launch_bounds__(256) k_merge_few(const uint32_t *const *__rest
         for (int q = 0; q < 8; ++q) {
             if (q >= np) break;
 #pragma unroll
-            for (int u = 0; u < 4; ++u) {
+            for (int u = 0; u < MF_U; ++u) {
                 const uint32_t x = w0 + u < words ? __ldg(r[q] + w0 + u) : 0u;
                 e[u] |= ((x >> lane) & 1u) << (31 - (k0 + q));
             }
         }
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
+        for (int u = 0; u < MF_U; ++u) {
             const uint64_t i = (w0 + u) * 32 + lane;
             if (i < count) merged_out[i] = xor_decode_word(e[u]) & keep;
         }
@@ -764,7 +765,7 @@ void launch_merge(const uint32_t *const *rows, const uint32_t *merged_in, uint32
     const uint64_t words = (count + 31) / 32;
     if (words == 0) return;
     if (merged_in && k0 > 0 && k1 - k0 <= 8) {
-        const unsigned g = (unsigned)std::min<uint64_t>(((words + 3) / 4 + 7) / 8, 148ull * 16);
+        const unsigned g = (unsigned)std::min<uint64_t>(((words + MF_U - 1) / MF_U + 7) / 8, 148ull * 16);
         k_merge_few<<<g, 256, 0, st>>>(rows, merged_in, merged_out, count, k0, k1);
     } else {
         const unsigned g = (unsigned)std::min<uint64_t>(((words + 31) / 32 + 7) / 8, 148ull * 8);
