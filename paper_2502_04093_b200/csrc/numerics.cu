@@ -232,21 +232,31 @@ __device__ __forceinline__ uint32_t warp_transpose32(uint32_t x, unsigned lane) 
 // bitplane.cpp:7-22 split + 44-49 xor: a warp transposes its 32 codewords (lane l: codeword
 // l -> lane 31-p: plane p's word, bit l = codeword l's digit), XORs each plane word with the
 // two planes above it (lanes +1, +2), and the CTA writes the 32 planes x 32 words tile.
+constexpr int BP_G = 4;  // 32-codeword groups per warp (loads in flight per thread)
 __global__ void __launch_bounds__(1024) k_bitplanes(const uint32_t *__restrict__ nb, uint64_t count,
                                                     uint32_t *__restrict__ planes, uint64_t stride) {
-    __shared__ uint32_t tile[32][33];
+    __shared__ uint32_t tile[32][32 * BP_G + 1];
     const unsigned warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const uint64_t word0 = (uint64_t)blockIdx.x * 32;
-    const uint64_t i = (word0 + warp) * 32 + lane;
-    const uint32_t v = i < count ? nb[i] : 0u;
-    const uint32_t b = warp_transpose32(v, lane);  // plane 31 - lane
-    const uint32_t b1 = __shfl_down_sync(0xffffffffu, b, 1), b2 = __shfl_down_sync(0xffffffffu, b, 2);
-    const uint32_t e = b ^ (lane < 31 ? b1 : 0u) ^ (lane < 30 ? b2 : 0u);
-    tile[31 - lane][warp] = e;  // tile[plane][word]
+    const uint64_t word0 = (uint64_t)blockIdx.x * 32 * BP_G;
+    uint32_t v[BP_G];
+#pragma unroll
+    for (int g = 0; g < BP_G; ++g) {
+        const uint64_t i = (word0 + warp + 32 * g) * 32 + lane;
+        v[g] = i < count ? __ldg(nb + i) : 0u;
+    }
+#pragma unroll
+    for (int g = 0; g < BP_G; ++g) {
+        const uint32_t b = warp_transpose32(v[g], lane);  // plane 31 - lane
+        const uint32_t b1 = __shfl_down_sync(0xffffffffu, b, 1), b2 = __shfl_down_sync(0xffffffffu, b, 2);
+        const uint32_t e = b ^ (lane < 31 ? b1 : 0u) ^ (lane < 30 ? b2 : 0u);
+        tile[31 - lane][warp + 32 * g] = e;  // tile[plane][word]
+    }
     __syncthreads();
     const unsigned p = threadIdx.x >> 5, w = threadIdx.x & 31;
     const uint64_t words = (count + 31) / 32;
-    if (word0 + w < words) planes[(uint64_t)p * stride + word0 + w] = tile[p][w];
+#pragma unroll
+    for (int g = 0; g < BP_G; ++g)
+        if (word0 + w + 32 * g < words) planes[(uint64_t)p * stride + word0 + w + 32 * g] = tile[p][w + 32 * g];
 }
 
 }  // namespace
@@ -709,7 +719,7 @@ void launch_quant_pass(const void *values, void *state, int scalar, bool cubic, 
 void launch_bitplanes(const uint32_t *nb, uint64_t count, uint32_t *planes, uint64_t stride, cudaStream_t st) {
     const uint64_t words = (count + 31) / 32;
     if (words == 0) return;
-    const uint64_t blocks = (words + 31) / 32;
+    const uint64_t blocks = (words + 32 * BP_G - 1) / (32 * BP_G);
     k_bitplanes<<<(unsigned)blocks, 1024, 0, st>>>(nb, count, planes, stride);
     CKL();
 }
