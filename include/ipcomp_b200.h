@@ -82,25 +82,63 @@ int ipcg_compress(ipcg_ctx *ctx, int scalar, const void *values, int values_on_d
  * archive held in caller memory (host or device).  The bytes are borrowed, like
  * the reference's istream, and must outlive the handle. */
 int ipcg_archive_open(ipcg_ctx *ctx, const void *bytes, uint64_t size, int on_device, ipcg_archive **out);
+/* ArchiveReader(std::istream&) over a seekable source, as the reference reads its stream
+ * (archive.cpp:117-181): `read` copies `len` bytes at absolute offset `offset` into host
+ * memory `dst` and returns the number of bytes it delivered (fewer = end of source, < 0 =
+ * failure).  Opening reads exactly the index (the header, then each level record in
+ * turn); a retrieval then reads only the blocks its plan names, each once, at
+ * index_bytes + block offset -- the reference's read_range.  `user` and the source must
+ * outlive the handle.  Index errors carry the reference's messages ("truncated archive
+ * index", "not an archive: bad magic", ...); a short block read raises "truncated archive
+ * payload". */
+typedef int64_t (*ipcg_read_fn)(void *user, uint64_t offset, void *dst, uint64_t len);
+int ipcg_archive_open_source(ipcg_ctx *ctx, ipcg_read_fn read, void *user, ipcg_archive **out);
+/* ArchiveReader::read_range (archive.cpp:172-181): `length` payload bytes at payload offset
+ * `offset` into host memory, accounted in payload_bytes_read ("block offset outside
+ * payload" / "truncated archive payload" as the reference). */
+int ipcg_archive_read_range(ipcg_ctx *ctx, ipcg_archive *a, uint64_t offset, uint64_t length, void *dst);
 int ipcg_archive_index(const ipcg_archive *a, ipcg_index *out);
 /* write_archive (src/archive.cpp:72-81): serialized size and copy-out */
 uint64_t ipcg_archive_size(const ipcg_archive *a);
 int ipcg_archive_write(ipcg_ctx *ctx, const ipcg_archive *a, void *dst, int dst_on_device, uint64_t capacity);
+/* bytes [offset, offset + length) of the serialized archive (e.g. the payload alone, for
+ * ArchiveData::payload) into host or device memory; archives opened from a source read them
+ * through it (not accounted as block reads) */
+int ipcg_archive_copy(ipcg_ctx *ctx, const ipcg_archive *a, uint64_t offset, uint64_t length, void *dst,
+                      int dst_on_device);
 /* ArchiveReader::payload_bytes_read (archive.hpp:81) */
 uint64_t ipcg_archive_payload_bytes_read(const ipcg_archive *a);
 void ipcg_archive_free(ipcg_archive *a);
+/* serialize_index (archive.cpp:31-65) of header + records (payload_bytes, index_bytes and
+ * identity are derived, not read); *size_out receives the index size, also when capacity is too
+ * small (IPCG_EINVAL).  Context-free (errors via ipcg_last_error(NULL)). */
+int ipcg_index_serialize(const ipcg_index *ix, uint8_t *dst, uint64_t capacity, uint64_t *size_out);
+/* parse an index held in host memory (the archive's first `size` bytes, payload optional) */
+int ipcg_index_parse(const uint8_t *bytes, uint64_t size, ipcg_index *out);
+/* crc32_bytes (backend.cpp:9-11): zlib's CRC-32, host (archive identity, small blocks) */
+uint32_t ipcg_crc32(const void *bytes, uint64_t len);
+
+/* ReconstructStats (pipeline.hpp:37-40) */
+typedef struct {
+    uint64_t payload_bytes_loaded;
+    int level_visits[IPCG_MAX_LEVELS]; /* [l-1]: times level l was reconstructed */
+} ipcg_retrieve_stats;
 
 /* reconstruct_field<T> (pipeline.hpp:260-287): plan k[levels] (RetrievalPlan,
- * archive.hpp:59-61); out is host or device; *session_out may be NULL. */
+ * archive.hpp:59-61); out is host or device and holds out_count elements (must equal the
+ * grid's point count: IPCG_EINVAL otherwise); *session_out and stats may be NULL. */
 int ipcg_reconstruct(ipcg_ctx *ctx, ipcg_archive *a, int scalar, const int *k, void *out, int out_on_device,
-                     ipcg_session **session_out, uint64_t *payload_bytes_loaded);
+                     uint64_t out_count, ipcg_session **session_out, ipcg_retrieve_stats *stats);
 
-/* refine_field<T> (pipeline.hpp:294-352) */
+/* refine_field<T> (pipeline.hpp:294-352); previous_count / out_count elements, each must
+ * equal the grid's point count ("previous reconstruction has wrong size", pipeline.hpp:303) */
 int ipcg_refine(ipcg_ctx *ctx, ipcg_archive *a, int scalar, const ipcg_session *session, const void *previous,
-                int previous_on_device, const int *k, void *out, int out_on_device, ipcg_session **session_out,
-                uint64_t *payload_bytes_loaded);
+                int previous_on_device, uint64_t previous_count, const int *k, void *out, int out_on_device,
+                uint64_t out_count, ipcg_session **session_out, ipcg_retrieve_stats *stats);
 
-/* RetrievalSession (session.hpp:19-34) */
+/* RetrievalSession (session.hpp:19-34): planes_loaded[levels] (0..32, 32 for levels above
+ * the progressive bound) and merged[l] = host codewords of progressive level l+1 (count of
+ * that level; required when planes_loaded > 0, may be NULL when it is 0) */
 int ipcg_session_create(ipcg_ctx *ctx, const ipcg_archive *a, const int *planes_loaded,
                         const uint32_t *const *merged /* [levels], host, NULL for non-progressive */,
                         ipcg_session **out);
@@ -136,6 +174,37 @@ int ipcg_plan_for_error(ipcg_ctx *ctx, const ipcg_archive *a, double max_error, 
 int ipcg_plan_for_size(ipcg_ctx *ctx, const ipcg_archive *a, uint64_t byte_budget, int *k_out);
 double ipcg_bound_for_plan(const ipcg_archive *a, const int *k);
 uint64_t ipcg_plan_payload_bytes(const ipcg_archive *a, const int *k);
+
+/* ErrorModel / LevelCosts (planner.hpp:13-32): a plain model callers may also build by hand;
+ * the planner below works on it alone (planner.cpp:30-290).  Context-free calls; errors
+ * (IPCG_EINFEASIBLE, IPCG_EINVAL for a malformed model) via ipcg_last_error(NULL). */
+typedef struct {
+    double delta[33];
+    uint64_t plane_bytes[32];
+    uint64_t outlier_bytes;
+    int progressive;
+} ipcg_level_costs;
+typedef struct {
+    int levels, progressive_levels;
+    double eb, amplification;
+    ipcg_level_costs level[IPCG_MAX_LEVELS]; /* [l-1] */
+} ipcg_error_model;
+int ipcg_build_error_model(const ipcg_index *ix, ipcg_error_model *out);
+int ipcg_model_plan_for_error(const ipcg_error_model *m, double max_error, int *k_out);
+int ipcg_model_plan_for_size(const ipcg_error_model *m, uint64_t byte_budget, int *k_out);
+double ipcg_model_bound_for_plan(const ipcg_error_model *m, const int *k);
+uint64_t ipcg_model_plan_payload_bytes(const ipcg_error_model *m, const int *k);
+uint64_t ipcg_model_mandatory_payload_bytes(const ipcg_error_model *m);
+uint64_t ipcg_model_total_payload_bytes(const ipcg_error_model *m);
+
+/* bitplane.cpp:7-68 on the device, for host arrays: 32 plane rows planes[p] of
+ * ceil(count/8) bytes each (bit i of plane p = digit 31-p of codeword i, LSB-first).
+ *   split (+ xor_encode when xor_encode != 0)                    bitplane.cpp:7-22,44-49
+ *   xor_encode (decode = 0) / xor_decode of the first `nplanes` planes (decode = 1), in place
+ *   merge of the first planes_loaded raw planes                  bitplane.cpp:24-38 */
+int ipcg_split(ipcg_ctx *ctx, const uint32_t *codewords, uint64_t count, int xor_encode, uint8_t *const *planes);
+int ipcg_plane_xor(ipcg_ctx *ctx, uint8_t *const *planes, uint64_t count, int nplanes, int decode);
+int ipcg_merge(ipcg_ctx *ctx, const uint8_t *const *planes, uint64_t count, int planes_loaded, uint32_t *codewords);
 
 /* backend_encode (src/backend.cpp:34-53) for `count` equal-length raw planes laid out
  * at raw + i*raw_stride (host or device).  Payloads are written to out_payload

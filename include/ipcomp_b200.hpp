@@ -1,12 +1,10 @@
-// ipcomp_b200.hpp -- header-only C++20 mirror of the reference's public API for the hot
-// path (namespace ipcomp: pipeline.hpp, archive.hpp, planner.hpp, session.hpp, common.hpp
-// under /root/reference/proj/include/ipcomp), implemented over the C-ABI in ipcomp_b200.h.
-//
-// A reference user switches by including this header instead of <ipcomp/pipeline.hpp> and
-// <ipcomp/planner.hpp>, linking libipcomp_b200.so, and using namespace ipcomp_b200 (the
-// names, argument meanings and exception types are the reference's).  Differences, all
-// additive: archives/sessions may stay device-resident, and every call takes an optional
-// Context (one CUDA device + stream; Context::default_context() uses device 0).
+// ipcomp_b200.hpp -- the DEVICE-RESIDENT extension API (namespace ipcomp_b200), header-only
+// over the C-ABI in ipcomp_b200.h.  The source-compatible drop-in for the reference's public
+// API is include/ipcomp/*.hpp (namespace ipcomp; the reference's own acceptance.cpp and unit
+// tests compile against it unchanged).  This header is for callers who keep archives,
+// sessions and fields in HBM across calls: compress_field returns the device-resident archive,
+// sessions keep their merged codewords on the device, and every call takes an explicit
+// Context (one CUDA device + stream).  Names and exception types follow the reference.
 #ifndef IPCOMP_B200_HPP
 #define IPCOMP_B200_HPP
 
@@ -185,6 +183,7 @@ class RetrievalSession {
 
 // pipeline.hpp:37-47
 struct ReconstructStats {
+    std::vector<int> level_visits;
     std::uint64_t payload_bytes_loaded = 0;
 };
 template <class T>
@@ -219,8 +218,11 @@ Retrieved<T> reconstruct_field(ArchiveReader &archive, const RetrievalPlan &plan
     Retrieved<T> out;
     out.values.resize(count);
     ipcg_session *s = nullptr;
+    ipcg_retrieve_stats st{};
     ctx.check(ipcg_reconstruct(ctx.get(), archive.get(), detail::scalar_of<T>(), plan.k.data(), out.values.data(), 0,
-                               &s, &out.stats.payload_bytes_loaded));
+                               out.values.size(), &s, &st));
+    out.stats.payload_bytes_loaded = st.payload_bytes_loaded;
+    out.stats.level_visits.assign(st.level_visits, st.level_visits + archive.header().levels);
     out.session = RetrievalSession(s);
     return out;
 }
@@ -234,8 +236,11 @@ Retrieved<T> refine_field(ArchiveReader &archive, const RetrievalSession &sessio
     Retrieved<T> out;
     out.values.resize(previous.size());
     ipcg_session *s = nullptr;
+    ipcg_retrieve_stats st{};
     ctx.check(ipcg_refine(ctx.get(), archive.get(), detail::scalar_of<T>(), session.get(), previous.data(), 0,
-                          target.k.data(), out.values.data(), 0, &s, &out.stats.payload_bytes_loaded));
+                          previous.size(), target.k.data(), out.values.data(), 0, out.values.size(), &s, &st));
+    out.stats.payload_bytes_loaded = st.payload_bytes_loaded;
+    out.stats.level_visits.assign(st.level_visits, st.level_visits + archive.header().levels);
     out.session = RetrievalSession(s);
     return out;
 }

@@ -56,6 +56,22 @@ class Index(C.Structure):
                 ("records", LevelRecord * MAX_LEVELS)]
 
 
+class RetrieveStats(C.Structure):
+    _fields_ = [("payload_bytes_loaded", C.c_uint64), ("level_visits", C.c_int * MAX_LEVELS)]
+
+
+class LevelCosts(C.Structure):
+    _fields_ = [("delta", C.c_double * 33), ("plane_bytes", C.c_uint64 * 32), ("outlier_bytes", C.c_uint64),
+                ("progressive", C.c_int)]
+
+
+class ErrorModelC(C.Structure):
+    _fields_ = [("levels", C.c_int), ("progressive_levels", C.c_int), ("eb", C.c_double),
+                ("amplification", C.c_double), ("level", LevelCosts * MAX_LEVELS)]
+
+
+READ_FN = C.CFUNCTYPE(C.c_int64, C.c_void_p, C.c_uint64, C.c_void_p, C.c_uint64)
+
 _lib = None
 
 
@@ -78,13 +94,19 @@ def library() -> C.CDLL:
         "ipcg_set_host_async": (i32, [vp, i32]),
         "ipcg_compress": (i32, [vp, i32, vp, i32, P(u64), i32, dbl, i32, i32, u64, P(vp)]),
         "ipcg_archive_open": (i32, [vp, vp, u64, i32, P(vp)]),
+        "ipcg_archive_open_source": (i32, [vp, READ_FN, vp, P(vp)]),
+        "ipcg_archive_read_range": (i32, [vp, vp, u64, u64, vp]),
+        "ipcg_archive_copy": (i32, [vp, vp, u64, u64, vp, i32]),
+        "ipcg_index_serialize": (i32, [P(Index), vp, u64, P(u64)]),
+        "ipcg_index_parse": (i32, [vp, u64, P(Index)]),
+        "ipcg_crc32": (C.c_uint32, [vp, u64]),
         "ipcg_archive_index": (i32, [vp, P(Index)]),
         "ipcg_archive_size": (u64, [vp]),
         "ipcg_archive_write": (i32, [vp, vp, vp, i32, u64]),
         "ipcg_archive_payload_bytes_read": (u64, [vp]),
         "ipcg_archive_free": (None, [vp]),
-        "ipcg_reconstruct": (i32, [vp, vp, i32, P(i32), vp, i32, P(vp), P(u64)]),
-        "ipcg_refine": (i32, [vp, vp, i32, vp, vp, i32, P(i32), vp, i32, P(vp), P(u64)]),
+        "ipcg_reconstruct": (i32, [vp, vp, i32, P(i32), vp, i32, u64, P(vp), P(RetrieveStats)]),
+        "ipcg_refine": (i32, [vp, vp, i32, vp, vp, i32, u64, P(i32), vp, i32, u64, P(vp), P(RetrieveStats)]),
         "ipcg_session_create": (i32, [vp, vp, P(i32), P(P(C.c_uint32)), P(vp)]),
         "ipcg_session_levels": (i32, [vp]),
         "ipcg_session_archive_crc": (C.c_uint32, [vp]),
@@ -100,6 +122,16 @@ def library() -> C.CDLL:
         "ipcg_plan_for_size": (i32, [vp, vp, u64, P(i32)]),
         "ipcg_bound_for_plan": (dbl, [vp, P(i32)]),
         "ipcg_plan_payload_bytes": (u64, [vp, P(i32)]),
+        "ipcg_build_error_model": (i32, [P(Index), P(ErrorModelC)]),
+        "ipcg_model_plan_for_error": (i32, [P(ErrorModelC), dbl, P(i32)]),
+        "ipcg_model_plan_for_size": (i32, [P(ErrorModelC), u64, P(i32)]),
+        "ipcg_model_bound_for_plan": (dbl, [P(ErrorModelC), P(i32)]),
+        "ipcg_model_plan_payload_bytes": (u64, [P(ErrorModelC), P(i32)]),
+        "ipcg_model_mandatory_payload_bytes": (u64, [P(ErrorModelC)]),
+        "ipcg_model_total_payload_bytes": (u64, [P(ErrorModelC)]),
+        "ipcg_split": (i32, [vp, vp, u64, i32, P(C.c_void_p)]),
+        "ipcg_plane_xor": (i32, [vp, P(C.c_void_p), u64, i32, i32]),
+        "ipcg_merge": (i32, [vp, P(C.c_void_p), u64, i32, vp]),
         "ipcg_backend_encode": (i32, [vp, vp, i32, u64, u64, i32, vp, vp, vp, vp, u64]),
         "ipcg_kernel_launches": (u64, [vp]),
         "ipcg_profile_enable": (i32, [vp, i32]),
@@ -118,6 +150,11 @@ EXPORTED_SYMBOLS = [
     "ipcg_ctx_create", "ipcg_ctx_destroy", "ipcg_last_error", "ipcg_set_stream", "ipcg_synchronize",
     "ipcg_set_host_async",
     "ipcg_compress", "ipcg_archive_open", "ipcg_archive_index", "ipcg_archive_size", "ipcg_archive_write",
+    "ipcg_archive_open_source", "ipcg_archive_read_range", "ipcg_archive_copy", "ipcg_index_serialize",
+    "ipcg_index_parse", "ipcg_crc32", "ipcg_build_error_model", "ipcg_model_plan_for_error",
+    "ipcg_model_plan_for_size", "ipcg_model_bound_for_plan", "ipcg_model_plan_payload_bytes",
+    "ipcg_model_mandatory_payload_bytes", "ipcg_model_total_payload_bytes", "ipcg_split", "ipcg_plane_xor",
+    "ipcg_merge",
     "ipcg_archive_payload_bytes_read", "ipcg_archive_free", "ipcg_reconstruct", "ipcg_refine",
     "ipcg_session_create", "ipcg_session_levels", "ipcg_session_archive_crc", "ipcg_session_planes_loaded",
     "ipcg_session_count", "ipcg_session_merged", "ipcg_session_free",
@@ -449,13 +486,14 @@ def reconstruct_field(reader: ArchiveReader, plan, dtype=None, out=None, device:
     scalar = reader._ix.scalar if dtype is None else (0 if np.dtype(dtype) == np.float32 else 1)
     k = _plan_arr(plan, reader.levels)
     out = _out_buffer(reader, out, device)
-    addr, on_dev, _ = _ptr(out)
+    addr, on_dev, nbytes = _ptr(out)
     sess = C.c_void_p()
-    loaded = C.c_uint64()
-    reader.ctx.check(lib.ipcg_reconstruct(reader.ctx.h, reader.h, scalar, k, C.c_void_p(addr), on_dev,
-                                          C.byref(sess) if keep_session else None, C.byref(loaded)))
+    st = RetrieveStats()
+    w = 4 if scalar == 0 else 8
+    reader.ctx.check(lib.ipcg_reconstruct(reader.ctx.h, reader.h, scalar, k, C.c_void_p(addr), on_dev, nbytes // w,
+                                          C.byref(sess) if keep_session else None, C.byref(st)))
     s = RetrievalSession(sess, reader.ctx) if keep_session else None
-    return Retrieved(out, s, ReconstructStats([1] * reader.levels, int(loaded.value)))
+    return Retrieved(out, s, ReconstructStats(list(st.level_visits[: reader.levels]), int(st.payload_bytes_loaded)))
 
 
 def refine_field(reader: ArchiveReader, session: RetrievalSession, previous, plan, out=None,
@@ -463,21 +501,19 @@ def refine_field(reader: ArchiveReader, session: RetrievalSession, previous, pla
     """refine_field<T> (pipeline.hpp:294-352)."""
     lib = library()
     k = _plan_arr(plan, reader.levels)
-    paddr, pdev, _ = _ptr(previous)
+    paddr, pdev, pbytes = _ptr(previous)
     if out is None:
         out = np.empty_like(previous) if isinstance(previous, np.ndarray) else previous.clone()
-    addr, on_dev, _ = _ptr(out)
+    addr, on_dev, nbytes = _ptr(out)
     sess = C.c_void_p()
-    loaded = C.c_uint64()
+    st = RetrieveStats()
     scalar = _scalar_of(previous)
-    reader.ctx.check(lib.ipcg_refine(reader.ctx.h, reader.h, scalar, session.h, C.c_void_p(paddr), pdev, k,
-                                     C.c_void_p(addr), on_dev, C.byref(sess) if keep_session else None,
-                                     C.byref(loaded)))
+    w = 4 if scalar == 0 else 8
+    reader.ctx.check(lib.ipcg_refine(reader.ctx.h, reader.h, scalar, session.h, C.c_void_p(paddr), pdev,
+                                     pbytes // w, k, C.c_void_p(addr), on_dev, nbytes // w,
+                                     C.byref(sess) if keep_session else None, C.byref(st)))
     s = RetrievalSession(sess, reader.ctx) if keep_session else None
-    visits = [0] * reader.levels
-    for l in range(1, reader._ix.progressive_levels + 1):
-        visits[l - 1] = 1
-    return Retrieved(out, s, ReconstructStats(visits, int(loaded.value)))
+    return Retrieved(out, s, ReconstructStats(list(st.level_visits[: reader.levels]), int(st.payload_bytes_loaded)))
 
 
 @dataclass

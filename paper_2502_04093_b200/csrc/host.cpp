@@ -3,6 +3,7 @@
 //   planner:         proj/src/planner.cpp:30-290 (1024 ceiling buckets, knapsack DP)
 #include "host.h"
 
+#include <algorithm>
 #include <cmath>
 #include <cstring>
 #include <limits>
@@ -47,10 +48,23 @@ void check_record(const ipcg_level_record &r) {  // archive.cpp:23-28
         if (!(r.delta[d] >= r.delta[d - 1])) throw Error(ERUNTIME, "loss table must be non-decreasing");
 }
 
+// The reference's IndexParser (archive.cpp:87-113) takes one field at a time from its stream;
+// `more` (optional) appends the next `need` bytes of a seekable source to `buf`, so the index
+// is read field by field and never past its end.
 struct Reader {
     const uint8_t *p;
     uint64_t n, pos = 0;
+    std::vector<uint8_t> *buf = nullptr;
+    const IndexSource *more = nullptr;
     uint64_t get(int nb) {
+        if (n - pos < (uint64_t)nb && more) {
+            const uint64_t need = pos + (uint64_t)nb - n;
+            buf->resize(n + need);
+            const int64_t got = more->read(more->user, n, buf->data() + n, need);
+            n += got > 0 ? std::min<uint64_t>((uint64_t)got, need) : 0;
+            buf->resize(n);
+            p = buf->data();
+        }
         if (n - pos < (uint64_t)nb) throw Error(ERUNTIME, "truncated archive index");
         uint64_t v = 0;
         for (int i = 0; i < nb; ++i) v |= (uint64_t)p[pos + i] << (8 * i);
@@ -108,12 +122,11 @@ std::vector<uint8_t> serialize_index(const ipcg_index &h) {
     return w;
 }
 
-void parse_index(const uint8_t *bytes, uint64_t avail, ipcg_index &h) {
+namespace {
+void parse_index_impl(Reader &r, ipcg_index &h) {
     std::memset(&h, 0, sizeof h);
-    Reader r{bytes, avail};
-    if (avail < 4) throw Error(ERUNTIME, "truncated archive index");
-    if (std::memcmp(bytes, "IPC1", 4) != 0) throw Error(ERUNTIME, "not an archive: bad magic");
-    r.pos = 4;
+    const uint64_t magic = r.get(4);
+    if (magic != 0x31435049ull) throw Error(ERUNTIME, "not an archive: bad magic");  // "IPC1"
     h.version = (uint16_t)r.get(2);
     if (h.version != 1) throw Error(ERUNTIME, "unsupported archive version");
     h.scalar = (uint8_t)r.get(1);
@@ -148,7 +161,8 @@ void parse_index(const uint8_t *bytes, uint64_t avail, ipcg_index &h) {
         check_record(rec);
     }
     h.index_bytes = r.pos;
-    h.identity = crc32_host(bytes, r.pos);
+    h.identity = crc32_host(r.p, r.pos);
+    // archive.cpp:164-169 (the same wrapping u64 sums as the reference)
     uint64_t end = 0;
     for (int l = 0; l < h.levels; ++l) {
         const ipcg_level_record &rec = h.records[l];
@@ -156,6 +170,18 @@ void parse_index(const uint8_t *bytes, uint64_t avail, ipcg_index &h) {
         for (int p = 0; p < 32; ++p) end = std::max(end, rec.plane_offset[p] + rec.plane_length[p]);
     }
     h.payload_bytes = end;
+}
+}  // namespace
+
+void parse_index(const uint8_t *bytes, uint64_t avail, ipcg_index &h) {
+    Reader r{bytes, avail};
+    parse_index_impl(r, h);
+}
+
+void parse_index(const IndexSource &src, ipcg_index &h) {
+    std::vector<uint8_t> buf;
+    Reader r{nullptr, 0, 0, &buf, &src};
+    parse_index_impl(r, h);
 }
 
 void validate_plan(const ipcg_index &h, const int *k) {
@@ -167,16 +193,18 @@ void validate_plan(const ipcg_index &h, const int *k) {
 }
 
 // ------------------------------------------------------------------ planner
+// planner.cpp:30-290 over the plain model (planner.hpp:13-32); the index-based entry points
+// build the model first, as build_error_model does.
 namespace {
 
 constexpr int kBuckets = 1024;
 constexpr int kInfCost = kBuckets + 1;
 
-double amp(const ipcg_index &h) { return h.interp == 1 ? 1.25 : 1.0; }  // predictor.hpp:12
-double weight(const ipcg_index &h, int level) { return std::pow(amp(h), level - 1); }
-uint64_t optional_bytes(const ipcg_index &h, int level, int dropped) {
+double weight(const ipcg_error_model &m, int level) { return std::pow(m.amplification, level - 1); }
+const ipcg_level_costs &at(const ipcg_error_model &m, int level) { return m.level[level - 1]; }
+uint64_t optional_bytes(const ipcg_level_costs &lc, int dropped) {
     uint64_t s = 0;
-    for (int p = 0; p < 32 - dropped; ++p) s += h.records[level - 1].plane_length[p];
+    for (int p = 0; p < 32 - dropped; ++p) s += lc.plane_bytes[p];
     return s;
 }
 
@@ -188,39 +216,66 @@ struct Choice {
 
 }  // namespace
 
-double bound_for_plan(const ipcg_index &h, const int *k) {
-    double sum = 0.0;
-    for (int l = 1; l <= h.levels; ++l) sum += weight(h, l) * h.records[l - 1].delta[32 - k[l - 1]];
-    return sum + h.eb;
+void check_model(const ipcg_error_model &m) {
+    if (m.levels < 0 || m.levels > IPCG_MAX_LEVELS) throw Error(EINVAL_, "error model level count out of range");
+    if (m.progressive_levels < 0 || m.progressive_levels > m.levels)
+        throw Error(EINVAL_, "error model progressive level count out of range");
 }
 
-uint64_t mandatory_payload_bytes(const ipcg_index &h) {
+void build_error_model(const ipcg_index &h, ipcg_error_model &m) {  // planner.cpp:30-45
+    std::memset(&m, 0, sizeof m);
+    m.levels = h.levels;
+    m.progressive_levels = h.progressive_levels;
+    m.eb = h.eb;
+    m.amplification = h.interp == 1 ? 1.25 : 1.0;  // predictor.hpp:12 amplification()
+    for (int l = 0; l < h.levels; ++l) {
+        ipcg_level_costs &lc = m.level[l];
+        std::memcpy(lc.delta, h.records[l].delta, sizeof lc.delta);
+        for (int p = 0; p < 32; ++p) lc.plane_bytes[p] = h.records[l].plane_length[p];
+        lc.outlier_bytes = h.records[l].outlier_length;
+        lc.progressive = l + 1 <= h.progressive_levels;
+    }
+}
+
+double bound_for_plan(const ipcg_error_model &m, const int *k) {
+    double sum = 0.0;
+    for (int l = 1; l <= m.levels; ++l) sum += weight(m, l) * at(m, l).delta[32 - k[l - 1]];
+    return sum + m.eb;
+}
+
+uint64_t mandatory_payload_bytes(const ipcg_error_model &m) {
     uint64_t s = 0;
-    for (int l = 1; l <= h.levels; ++l) {
-        s += h.records[l - 1].outlier_length;
-        if (l > h.progressive_levels) s += optional_bytes(h, l, 0);
+    for (int l = 1; l <= m.levels; ++l) {
+        s += at(m, l).outlier_bytes;
+        if (!at(m, l).progressive) s += optional_bytes(at(m, l), 0);
     }
     return s;
 }
 
-uint64_t plan_payload_bytes(const ipcg_index &h, const int *k) {
-    uint64_t s = mandatory_payload_bytes(h);
-    for (int l = 1; l <= h.progressive_levels; ++l) s += optional_bytes(h, l, 32 - k[l - 1]);
+uint64_t total_payload_bytes(const ipcg_error_model &m) {
+    uint64_t s = 0;
+    for (int l = 1; l <= m.levels; ++l) s += at(m, l).outlier_bytes + optional_bytes(at(m, l), 0);
     return s;
 }
 
-void plan_for_error(const ipcg_index &h, double max_error, int *k) {
-    if (std::isnan(max_error) || max_error < h.eb)
+uint64_t plan_payload_bytes(const ipcg_error_model &m, const int *k) {
+    uint64_t s = mandatory_payload_bytes(m);
+    for (int l = 1; l <= m.progressive_levels; ++l) s += optional_bytes(at(m, l), 32 - k[l - 1]);
+    return s;
+}
+
+void plan_for_error(const ipcg_error_model &m, double max_error, int *k) {
+    if (std::isnan(max_error) || max_error < m.eb)
         throw Error(EINFEASIBLE, "requested error bound is below the archive's compression bound");
-    const double slack = max_error - h.eb;
-    for (int l = 0; l < h.levels; ++l) k[l] = 32;
-    const int lp = h.progressive_levels;
+    const double slack = max_error - m.eb;
+    for (int l = 0; l < m.levels; ++l) k[l] = 32;
+    const int lp = m.progressive_levels;
     if (lp == 0) return;
     std::vector<std::vector<Choice>> cs(lp);
     for (int l = 1; l <= lp; ++l) {
-        const double w = weight(h, l);
+        const double w = weight(m, l);
         for (int d = 0; d <= 32; ++d) {
-            const double e = w * h.records[l - 1].delta[d];
+            const double e = w * at(m, l).delta[d];
             int cost;
             if (e <= 0.0 || std::isinf(slack)) cost = 0;
             else if (slack <= 0.0) cost = kInfCost;
@@ -229,14 +284,14 @@ void plan_for_error(const ipcg_index &h, double max_error, int *k) {
                 cost = units > (double)kInfCost ? kInfCost : (int)units;
             }
             if (cost > kBuckets) continue;
-            const Choice c{d, cost, optional_bytes(h, l, d), e};
+            const Choice c{d, cost, optional_bytes(at(m, l), d), e};
             if (!cs[l - 1].empty() && cs[l - 1].back().cost == cost) cs[l - 1].back() = c;
             else cs[l - 1].push_back(c);
         }
     }
     std::vector<std::vector<uint64_t>> best(lp + 1, std::vector<uint64_t>(kBuckets + 1, 0));
     for (int i = 1; i <= lp; ++i) {
-        const uint64_t base = optional_bytes(h, i, 0);
+        const uint64_t base = optional_bytes(at(m, i), 0);
         for (int e = 0; e <= kBuckets; ++e) {
             uint64_t v = 0;
             bool any = false;
@@ -250,7 +305,7 @@ void plan_for_error(const ipcg_index &h, double max_error, int *k) {
     }
     int e = kBuckets;
     for (int i = lp; i >= 1; --i) {
-        const uint64_t base = optional_bytes(h, i, 0), want = best[i][e];
+        const uint64_t base = optional_bytes(at(m, i), 0), want = best[i][e];
         bool found = false;
         for (auto it = cs[i - 1].rbegin(); it != cs[i - 1].rend(); ++it) {
             if (it->cost > e) continue;
@@ -263,12 +318,12 @@ void plan_for_error(const ipcg_index &h, double max_error, int *k) {
         }
         if (!found) throw Error(ERUNTIME, "plan reconstruction lost the optimum");
     }
-    while (bound_for_plan(h, k) > max_error) {
+    while (bound_for_plan(m, k) > max_error) {
         int worst = -1;
         double worst_err = 0.0;
         for (int l = 1; l <= lp; ++l) {
             const int d = 32 - k[l - 1];
-            const double er = weight(h, l) * h.records[l - 1].delta[d];
+            const double er = weight(m, l) * at(m, l).delta[d];
             if (d > 0 && er > worst_err) worst_err = er, worst = l;
         }
         if (worst < 0) break;
@@ -276,13 +331,13 @@ void plan_for_error(const ipcg_index &h, double max_error, int *k) {
     }
 }
 
-void plan_for_size(const ipcg_index &h, uint64_t byte_budget, int *k) {
-    const uint64_t mandatory = mandatory_payload_bytes(h);
+void plan_for_size(const ipcg_error_model &m, uint64_t byte_budget, int *k) {
+    const uint64_t mandatory = mandatory_payload_bytes(m);
     if (byte_budget < mandatory)
         throw Error(EINFEASIBLE, "byte budget is below the mandatory payload (outliers and non-progressive levels)");
     const uint64_t budget = byte_budget - mandatory;
-    for (int l = 0; l < h.levels; ++l) k[l] = 32;
-    const int lp = h.progressive_levels;
+    for (int l = 0; l < m.levels; ++l) k[l] = 32;
+    const int lp = m.progressive_levels;
     if (lp == 0) return;
     auto cost_of = [&](uint64_t bytes) -> int {
         if (bytes == 0) return 0;
@@ -292,12 +347,12 @@ void plan_for_size(const ipcg_index &h, uint64_t byte_budget, int *k) {
     };
     std::vector<std::vector<Choice>> cs(lp);
     for (int l = 1; l <= lp; ++l) {
-        const double w = weight(h, l);
+        const double w = weight(m, l);
         for (int d = 32; d >= 0; --d) {
-            const uint64_t bytes = optional_bytes(h, l, d);
+            const uint64_t bytes = optional_bytes(at(m, l), d);
             const int cost = cost_of(bytes);
             if (cost > kBuckets) continue;
-            const double e = w * h.records[l - 1].delta[d];
+            const double e = w * at(m, l).delta[d];
             if (!cs[l - 1].empty() && cs[l - 1].back().cost == cost) {
                 if (e < cs[l - 1].back().err) cs[l - 1].back() = Choice{d, cost, bytes, e};
             } else {
@@ -346,5 +401,19 @@ void plan_for_size(const ipcg_index &h, uint64_t byte_budget, int *k) {
         if (!found) throw Error(ERUNTIME, "plan reconstruction lost the optimum");
     }
 }
+
+// index-based entry points
+namespace {
+ipcg_error_model model_of(const ipcg_index &h) {
+    ipcg_error_model m;
+    build_error_model(h, m);
+    return m;
+}
+}  // namespace
+double bound_for_plan(const ipcg_index &h, const int *k) { return bound_for_plan(model_of(h), k); }
+uint64_t plan_payload_bytes(const ipcg_index &h, const int *k) { return plan_payload_bytes(model_of(h), k); }
+uint64_t mandatory_payload_bytes(const ipcg_index &h) { return mandatory_payload_bytes(model_of(h)); }
+void plan_for_error(const ipcg_index &h, double max_error, int *k) { plan_for_error(model_of(h), max_error, k); }
+void plan_for_size(const ipcg_index &h, uint64_t budget, int *k) { plan_for_size(model_of(h), budget, k); }
 
 }  // namespace ipcg

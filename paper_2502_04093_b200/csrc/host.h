@@ -19,9 +19,25 @@ constexpr uint64_t kMaxIndexBytes = 12 + 32 + 20 + IPCG_MAX_LEVELS * 808;
 // ArchiveReader constructor (archive.cpp:117-170): parses `avail` bytes, fills ix
 // (including index_bytes, identity, derived payload_bytes)
 void parse_index(const uint8_t *bytes, uint64_t avail, ipcg_index &ix);
+// the same over a seekable source, reading the index field by field (never past its end)
+struct IndexSource {
+    ipcg_read_fn read;
+    void *user;
+};
+void parse_index(const IndexSource &src, ipcg_index &ix);
 
 void validate_plan(const ipcg_index &ix, const int *k);  // archive.cpp:202-211
 
+// planner.cpp:30-290 on the plain model (planner.hpp:13-32)
+void check_model(const ipcg_error_model &m);
+void build_error_model(const ipcg_index &ix, ipcg_error_model &m);
+double bound_for_plan(const ipcg_error_model &m, const int *k);
+uint64_t plan_payload_bytes(const ipcg_error_model &m, const int *k);
+uint64_t mandatory_payload_bytes(const ipcg_error_model &m);
+uint64_t total_payload_bytes(const ipcg_error_model &m);
+void plan_for_error(const ipcg_error_model &m, double max_error, int *k);
+void plan_for_size(const ipcg_error_model &m, uint64_t budget, int *k);
+// the same from an index (build_error_model first)
 double bound_for_plan(const ipcg_index &ix, const int *k);
 uint64_t plan_payload_bytes(const ipcg_index &ix, const int *k);
 uint64_t mandatory_payload_bytes(const ipcg_index &ix);

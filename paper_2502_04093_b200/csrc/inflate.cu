@@ -328,6 +328,7 @@ struct JobMeta {
     uint32_t nseg;       // emit segments over all blocks
     uint32_t nfallback;  // blocks the chain decoded itself (fixed, stored excluded, unmatched dynamic)
     uint64_t fb_syms;    // their symbols
+    int bad;             // a match reached before the start of the output (k_emit)
 };
 
 struct Cand {
@@ -960,13 +961,17 @@ __global__ void k_fill_zero(const InflateJob *jobs, const JobMeta *meta) {
 // -------------------------------------------------------------------- 4. emit
 __device__ __forceinline__ bool flag_get(const uint32_t *f, uint64_t i) { return (f[i >> 5] >> (i & 31)) & 1u; }
 
-__global__ void __launch_bounds__(WARPS * 32) k_emit(const InflateJob *jobs, const Tables *tabs, const JobMeta *meta,
+__global__ void __launch_bounds__(WARPS * 32) k_emit(const InflateJob *jobs, const Tables *tabs, JobMeta *meta,
                                                    const uint32_t *pool, const uint32_t *ckpt_pool) {
     // one warp per emit segment (SEG symbols of one block, output offset from the
-    // candidate's checkpoints); copies reaching before the segment become pointers
+    // candidate's checkpoints); copies reaching before the segment become pointers.
+    // A match whose distance exceeds the bytes written before it is zlib's "invalid distance
+    // too far back": the job fails (meta.bad) and nothing is written for it.  All-zero jobs
+    // (filled by k_fill_zero) still run their first 32 KiB of output here, check only.
     const int j = blockIdx.y;
-    const JobMeta &jm = meta[j];
-    if (jm.status || jm.allzero) return;
+    JobMeta &jm = meta[j];
+    if (jm.status) return;
+    const bool check_only = jm.allzero != 0;
     const unsigned w = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const uint64_t gs = (uint64_t)blockIdx.x * WARPS + w;
     if (gs >= jm.nseg) return;
@@ -981,6 +986,7 @@ __global__ void __launch_bounds__(WARPS * 32) k_emit(const InflateJob *jobs, con
     const Blk blk = T.blocks[lo];
     const uint32_t seg = (uint32_t)(gs - blk.seg_base);
     uint8_t *dst = job.dst;
+    if (check_only && blk.type == 0) return;
     if (blk.type == 0) {
         for (uint64_t i = lane; i < blk.out_len; i += 32) dst[blk.out_off + i] = job.src[blk.src + i];
         return;
@@ -988,6 +994,7 @@ __global__ void __launch_bounds__(WARPS * 32) k_emit(const InflateJob *jobs, con
     // a block without checkpoints (decoded by the chain itself) is one segment of any length
     const uint32_t s_begin = seg * SEG, s_end = blk.nseg == 1 ? blk.nsyms : min(blk.nsyms, s_begin + SEG);
     const uint64_t b0 = blk.out_off + (seg ? ckpt_pool[blk.ckpt * NCKPT + seg] : 0);
+    if (check_only && b0 >= 32768) return;  // no distance reaches past 32 KiB of output
     const uint32_t *syms = blk.type == 1 ? pool + blk.src : T.fallback + blk.src;
     uint64_t o = b0;
     // 32 symbols per step: output offsets by a warp prefix sum, literals written in parallel,
@@ -1005,7 +1012,7 @@ __global__ void __launch_bounds__(WARPS * 32) k_emit(const InflateJob *jobs, con
             if ((int)lane >= off) incl += t;
         }
         const uint32_t my_rel = incl - mylen;
-        if (valid && !ismatch) dst[o + my_rel] = (uint8_t)v;
+        if (valid && !ismatch && !check_only) dst[o + my_rel] = (uint8_t)v;
         __syncwarp();
         unsigned mm = __ballot_sync(0xffffffffu, ismatch);
         while (mm) {
@@ -1014,6 +1021,11 @@ __global__ void __launch_bounds__(WARPS * 32) k_emit(const InflateJob *jobs, con
             const uint32_t mv = __shfl_sync(0xffffffffu, v, l);
             const uint64_t mo = o + __shfl_sync(0xffffffffu, my_rel, l);
             const uint32_t len = (mv >> 16) & 0x1ff, d = (mv & 0xffff) + 1;
+            if ((uint64_t)d > mo) {  // warp-uniform
+                if (lane == 0) atomicOr(&jm.bad, 1);
+                continue;
+            }
+            if (check_only) continue;
             // i % d by a reciprocal multiply (exact for i < 2^16: i < len <= 258; d = 1 apart,
             // whose reciprocal 2^32 does not fit)
             const uint32_t rcp = 0xffffffffu / d + 1u;
@@ -1195,6 +1207,7 @@ __global__ void k_finish(const InflateJob *jobs, int njobs, JobMeta *meta, const
     const int j = blockIdx.x * blockDim.x + threadIdx.x;
     if (j >= njobs) return;
     JobMeta &m = meta[j];
+    if (m.bad) m.status = 1;
     if (!m.status) {
         const uint64_t n = jobs[j].dst_len;
         const uint32_t a = (uint32_t)((1 + acc[2 * j]) % 65521u), b = (uint32_t)((acc[2 * j + 1] + n) % 65521u);

@@ -82,6 +82,8 @@ struct ipcg_ctx {
     std::string err;
     void *pinned = nullptr;
     size_t pinned_cap = 0;
+    void *src_pinned = nullptr;  // staging of block reads from a seekable archive source
+    size_t src_pinned_cap = 0;
     // host-async mode (ipcg_set_host_async): a retrieval's device->host copy of its values
     // runs on `copy` from a ring of device output buffers, so the next call's kernels (and
     // its host->device uploads: PCIe is full duplex) overlap it
@@ -108,6 +110,8 @@ struct ipcg_archive {
     ScratchPool *pool = nullptr;   // the creating context's pool `owned` returns to
     uint64_t payload_read = 0;
     int device = 0;
+    ipcg_read_fn read = nullptr;  // seekable source (ipcg_archive_open_source): bytes == nullptr
+    void *user = nullptr;
 };
 
 struct ipcg_session {
@@ -659,16 +663,45 @@ __global__ void k_compare(const CopyDesc *pairs, int n, int *diff) {
         }
 }
 
+// offs[2i] = block offset, offs[2i+1] = block length (a block shorter than its 21-byte header
+// copies only its own bytes; the host length checks then reject it)
 __global__ void k_copy_headers(const uint8_t *src, const uint64_t *offs, int n, uint8_t *dst) {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
-    for (int k = 0; k < 21; ++k) dst[i * 21 + k] = src[offs[i] + k];
+    const uint64_t len = offs[2 * i + 1] < 21 ? offs[2 * i + 1] : 21;
+    for (uint64_t k = 0; k < len; ++k) dst[i * 21 + k] = src[offs[2 * i] + k];
+}
+
+// read `len` bytes at absolute archive offset `off` through a seekable source
+void source_read(const ipcg_archive *a, uint64_t off, void *dst, uint64_t len, const char *short_msg) {
+    uint64_t done = 0;
+    while (done < len) {
+        const int64_t got = a->read(a->user, off + done, static_cast<uint8_t *>(dst) + done, len - done);
+        if (got <= 0) throw Error(ERUNTIME, short_msg);
+        done += std::min<uint64_t>((uint64_t)got, len - done);
+    }
+}
+
+void *src_pinned(ipcg_ctx *c, size_t bytes) {
+    if (bytes > c->src_pinned_cap) {
+        if (c->src_pinned) {
+            CK(cudaStreamSynchronize(c->stream));  // earlier uploads from it have landed
+            CK(cudaFreeHost(c->src_pinned));
+        }
+        c->src_pinned = nullptr;
+        const size_t cap = std::max<size_t>(bytes, 1 << 20);
+        CK(cudaMallocHost(&c->src_pinned, cap));
+        c->src_pinned_cap = cap;
+    }
+    return c->src_pinned;
 }
 
 void retrieve_impl(ipcg_ctx *c, ipcg_archive *a, int scalar, const int *k, void *out, int out_on_dev,
-                   const ipcg_session *prev_sess, const void *previous, int prev_on_dev, ipcg_session **sess_out,
-                   uint64_t *loaded) {
+                   uint64_t out_count, const ipcg_session *prev_sess, const void *previous, int prev_on_dev,
+                   uint64_t prev_count, ipcg_session **sess_out, ipcg_retrieve_stats *stats) {
     PhaseTimer tm;
+    if (!a) throw Error(EINVAL_, "archive is null");
+    if (!k) throw Error(EINVAL_, "plan is null");
     const ipcg_index &ix = a->ix;
     if (ix.scalar != scalar) throw Error(EINVAL_, "scalar kind does not match archive");
     validate_plan(ix, k);
@@ -682,6 +715,8 @@ void retrieve_impl(ipcg_ctx *c, ipcg_archive *a, int scalar, const int *k, void 
     const int L = ix.levels;
     const int w = scalar == 0 ? 4 : 8;
     const uint64_t n = G.n;
+    if (refine && (prev_count != n || !previous)) throw Error(EINVAL_, "previous reconstruction has wrong size");
+    if (out_count != n || !out) throw Error(EINVAL_, "output buffer has wrong size");
     if (refine) {
         for (int level = 1; level <= L; ++level)
             if (k[level - 1] < prev_sess->k[level - 1])
@@ -697,9 +732,13 @@ void retrieve_impl(ipcg_ctx *c, ipcg_archive *a, int scalar, const int *k, void 
     std::vector<LevelPlan> lv(L);
     std::vector<PlaneRef> refs;
     uint64_t read = 0;
+    // overflow-safe forms of read_range's checks (archive.cpp:173,178); a source's size is only
+    // known when a read comes up short
     auto range_ok = [&](uint64_t off, uint64_t len) {
-        if (off + len > ix.payload_bytes) throw Error(ERUNTIME, "block offset outside payload");
-        if (ix.index_bytes + off + len > a->size) throw Error(ERUNTIME, "truncated archive payload");
+        if (len > ix.payload_bytes || off > ix.payload_bytes - len) throw Error(ERUNTIME, "block offset outside payload");
+        if (a->read) return;
+        if (a->size < ix.index_bytes || len > a->size - ix.index_bytes || off > a->size - ix.index_bytes - len)
+            throw Error(ERUNTIME, "truncated archive payload");
     };
     std::vector<std::pair<uint64_t, uint64_t>> spans;  // payload-relative (off, len) in read order
     for (int level = L; level >= 1; --level) {
@@ -711,7 +750,8 @@ void retrieve_impl(ipcg_ctx *c, ipcg_archive *a, int scalar, const int *k, void 
         p.p1 = k[li];
         if (!p.active) continue;
         if (refine) {
-            if (prev_sess->count[li] != r.count) throw Error(ERUNTIME, "session codeword array has wrong length");
+            if (prev_sess->count[li] != r.count || (p.p0 > 0 && !prev_sess->merged[li]))
+                throw Error(ERUNTIME, "session codeword array has wrong length");
         } else if (r.count != G.level[li].count) {
             throw Error(ERUNTIME, "level point count does not match its dimensions");
         }
@@ -722,7 +762,8 @@ void retrieve_impl(ipcg_ctx *c, ipcg_archive *a, int scalar, const int *k, void 
             read += r.plane_length[q];
         }
         const uint64_t e = 8 + (uint64_t)w;
-        if (r.outlier_length != r.outlier_count * e) throw Error(ERUNTIME, "outlier block length does not match its count");
+        if (r.outlier_length % e != 0 || r.outlier_length / e != r.outlier_count)
+            throw Error(ERUNTIME, "outlier block length does not match its count");
         range_ok(r.outlier_offset, r.outlier_length);
         spans.push_back({r.outlier_offset, r.outlier_length});
         read += r.outlier_length;
@@ -739,20 +780,21 @@ void retrieve_impl(ipcg_ctx *c, ipcg_archive *a, int scalar, const int *k, void 
         for (size_t i = 0; i < spans.size(); ++i) src_off[i] = spans[i].first;
         if (!refs.empty()) {
             // plane spans are every span except each level's trailing outlier block
-            std::vector<uint64_t> hoffs;
+            std::vector<uint64_t> hoffs;  // (offset, length) per plane block
             size_t si = 0;
             for (int level = L; level >= 1; --level) {
                 const LevelPlan &p = lv[level - 1];
                 if (!p.active) continue;
-                for (int q = p.p0; q < p.p1; ++q) hoffs.push_back(src_off[si++]);
+                for (int q = p.p0; q < p.p1; ++q, ++si) hoffs.push_back(src_off[si]), hoffs.push_back(spans[si].second);
                 ++si;  // outlier
             }
-            DBuf ho(hoffs.size() * 8, st), hd(hoffs.size() * 21, st);
+            const size_t nh = hoffs.size() / 2;
+            DBuf ho(hoffs.size() * 8, st), hd(nh * 21, st);
             uint64_t *hp = static_cast<uint64_t *>(pinned(c, hoffs.size() * 8));
             std::memcpy(hp, hoffs.data(), hoffs.size() * 8);
             CK(cudaMemcpyAsync(ho.p, hp, hoffs.size() * 8, cudaMemcpyHostToDevice, st));
-            k_copy_headers<<<(unsigned)((hoffs.size() + 127) / 128), 128, 0, st>>>(src_dev, ho.as<uint64_t>(),
-                                                                                (int)hoffs.size(), hd.as<uint8_t>());
+            k_copy_headers<<<(unsigned)((nh + 127) / 128), 128, 0, st>>>(src_dev, ho.as<uint64_t>(), (int)nh,
+                                                                        hd.as<uint8_t>());
             CKL();
             readback(headers.data(), hd.p, headers.size(), st);
         }
@@ -761,8 +803,11 @@ void retrieve_impl(ipcg_ctx *c, ipcg_archive *a, int scalar, const int *k, void 
         // adjacent in the archive (a level's planes and its outlier block) go as one copy,
         // which is a DMA from page-locked memory and a driver-pipelined copy otherwise.  The
         // call returns only after the stream drains, so the buffer is not read after return.
+        // A seekable source is read span by span (the reference's read_range order) into
+        // page-locked staging, each span's upload overlapping the next span's read.
         stage = DBuf(std::max<uint64_t>(staged, 1), st);
-        const uint8_t *hb = a->bytes + ix.index_bytes;
+        uint8_t *sp = a->read ? static_cast<uint8_t *>(src_pinned(c, std::max<uint64_t>(staged, 1))) : nullptr;
+        const uint8_t *hb = a->read ? sp : a->bytes + ix.index_bytes;
         uint64_t o = 0;
         for (size_t i = 0; i < spans.size();) {
             size_t e = i + 1;
@@ -772,7 +817,12 @@ void retrieve_impl(ipcg_ctx *c, ipcg_archive *a, int scalar, const int *k, void 
                 ++e;
             }
             const uint64_t len = spans[e - 1].first + spans[e - 1].second - spans[i].first;
-            if (len) CK(cudaMemcpyAsync(stage.as<uint8_t>() + o, hb + spans[i].first, len, cudaMemcpyHostToDevice, st));
+            const uint8_t *from = hb + spans[i].first;
+            if (a->read) {
+                source_read(a, ix.index_bytes + spans[i].first, sp + o, len, "truncated archive payload");
+                from = sp + o;
+            }
+            if (len) CK(cudaMemcpyAsync(stage.as<uint8_t>() + o, from, len, cudaMemcpyHostToDevice, st));
             o += len;
             i = e;
         }
@@ -781,7 +831,8 @@ void retrieve_impl(ipcg_ctx *c, ipcg_archive *a, int scalar, const int *k, void 
             const LevelPlan &p = lv[level - 1];
             if (!p.active) continue;
             for (int q = p.p0; q < p.p1; ++q, ++ri, ++si)  // (a short block fails the length checks below)
-                std::memcpy(&headers[ri * 21], hb + spans[si].first, std::min<uint64_t>(21, spans[si].second));
+                std::memcpy(&headers[ri * 21], a->read ? sp + src_off[si] : hb + spans[si].first,
+                            std::min<uint64_t>(21, spans[si].second));
             ++si;
         }
         src_dev = stage.as<uint8_t>();
@@ -1025,7 +1076,11 @@ void retrieve_impl(ipcg_ctx *c, ipcg_archive *a, int scalar, const int *k, void 
         delete ns;
         throw;
     }
-    if (loaded) *loaded = read;
+    if (stats) {
+        std::memset(stats, 0, sizeof *stats);
+        stats->payload_bytes_loaded = read;
+        for (int l = 0; l < L; ++l) stats->level_visits[l] = lv[l].active ? 1 : 0;  // pipeline.hpp:275,346
+    }
     if (sess_out) *sess_out = ns;
     else {
         for (int l = 0; l < IPCG_MAX_LEVELS; ++l)
@@ -1080,6 +1135,7 @@ void ipcg_ctx_destroy(ipcg_ctx *c) {
     c->scratch.release_all(c->own_stream);
     if (c->own_stream) cudaStreamSynchronize(c->own_stream);
     if (c->pinned) cudaFreeHost(c->pinned);
+    if (c->src_pinned) cudaFreeHost(c->src_pinned);
     for (cudaStream_t s : c->side) cudaStreamDestroy(s);
     for (cudaStream_t s : c->loss) cudaStreamDestroy(s);
     for (cudaEvent_t e : c->events) cudaEventDestroy(e);
@@ -1144,16 +1200,107 @@ int ipcg_archive_open(ipcg_ctx *c, const void *bytes, uint64_t size, int on_devi
     });
 }
 
+int ipcg_archive_open_source(ipcg_ctx *c, ipcg_read_fn read, void *user, ipcg_archive **out) {
+    if (out) *out = nullptr;
+    return guarded(c, [&] {
+        if (!read || !out) throw Error(EINVAL_, "archive source needs a read function");
+        ipcg_archive *a = new ipcg_archive;
+        try {
+            parse_index(IndexSource{read, user}, a->ix);
+        } catch (...) {
+            delete a;
+            throw;
+        }
+        a->read = read;
+        a->user = user;
+        a->size = a->ix.index_bytes + a->ix.payload_bytes;  // as the index describes it
+        a->device = c ? c->device : 0;
+        *out = a;
+    });
+}
+
+int ipcg_archive_read_range(ipcg_ctx *c, ipcg_archive *a, uint64_t off, uint64_t len, void *dst) {
+    return guarded(c, [&] {
+        const ipcg_index &ix = a->ix;
+        if (len > ix.payload_bytes || off > ix.payload_bytes - len) throw Error(ERUNTIME, "block offset outside payload");
+        if (len && !dst) throw Error(EINVAL_, "read_range: null destination");
+        if (a->read) {
+            source_read(a, ix.index_bytes + off, dst, len, "truncated archive payload");
+        } else {
+            if (a->size < ix.index_bytes || len > a->size - ix.index_bytes || off > a->size - ix.index_bytes - len)
+                throw Error(ERUNTIME, "truncated archive payload");
+            if (!len) {
+            } else if (a->on_device) {
+                CK(cudaMemcpyAsync(dst, a->bytes + ix.index_bytes + off, len, cudaMemcpyDeviceToHost, c->stream));
+                CK(cudaStreamSynchronize(c->stream));
+            } else {
+                std::memcpy(dst, a->bytes + ix.index_bytes + off, len);
+            }
+        }
+        a->payload_read += len;
+    });
+}
+
+int ipcg_archive_copy(ipcg_ctx *c, const ipcg_archive *a, uint64_t off, uint64_t len, void *dst, int dst_on_device) {
+    return guarded(c, [&] {
+        if (!len) return;
+        if (!dst) throw Error(EINVAL_, "archive copy: null destination");
+        if (a->read) {
+            if (dst_on_device) {
+                void *h = pinned(c, len);
+                source_read(a, off, h, len, "truncated archive");
+                CK(cudaMemcpyAsync(dst, h, len, cudaMemcpyHostToDevice, c->stream));
+                CK(cudaStreamSynchronize(c->stream));
+            } else {
+                source_read(a, off, dst, len, "truncated archive");
+            }
+            return;
+        }
+        if (len > a->size || off > a->size - len) throw Error(EINVAL_, "archive copy outside the archive");
+        if (!a->on_device && !dst_on_device) {
+            std::memcpy(dst, a->bytes + off, len);
+            return;
+        }
+        const cudaMemcpyKind kind = a->on_device ? (dst_on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost)
+                                                 : cudaMemcpyHostToDevice;
+        CK(cudaMemcpyAsync(dst, a->bytes + off, len, kind, c->stream));
+        CK(cudaStreamSynchronize(c->stream));
+    });
+}
+
 int ipcg_archive_index(const ipcg_archive *a, ipcg_index *out) {
     if (!a || !out) return IPCG_EINVAL;
     *out = a->ix;
     return IPCG_OK;
 }
 
+int ipcg_index_serialize(const ipcg_index *ix, uint8_t *dst, uint64_t capacity, uint64_t *size_out) {
+    return guarded(nullptr, [&] {
+        if (!ix) throw Error(EINVAL_, "index is null");
+        if (ix->levels > IPCG_MAX_LEVELS) throw Error(EINVAL_, "archive has more levels than supported");
+        const std::vector<uint8_t> b = serialize_index(*ix);
+        if (size_out) *size_out = b.size();
+        if (!dst || capacity < b.size()) throw Error(EINVAL_, "index buffer too small");
+        std::memcpy(dst, b.data(), b.size());
+    });
+}
+
+int ipcg_index_parse(const uint8_t *bytes, uint64_t size, ipcg_index *out) {
+    return guarded(nullptr, [&] {
+        if (!out || (size && !bytes)) throw Error(EINVAL_, "index_parse: null argument");
+        parse_index(bytes, size, *out);
+    });
+}
+
+uint32_t ipcg_crc32(const void *bytes, uint64_t len) {
+    return len ? crc32_host(static_cast<const uint8_t *>(bytes), len) : 0u;
+}
+
 uint64_t ipcg_archive_size(const ipcg_archive *a) { return a ? a->size : 0; }
 
 int ipcg_archive_write(ipcg_ctx *c, const ipcg_archive *a, void *dst, int dst_on_device, uint64_t capacity) {
     return guarded(c, [&] {
+        if (a->read) throw Error(EINVAL_, "archive opened from a source: copy it with ipcg_archive_copy");
         if (capacity < a->size) throw Error(EINVAL_, "destination too small for the archive");
         const cudaMemcpyKind kind = a->on_device ? (dst_on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost)
                                                  : (dst_on_device ? cudaMemcpyHostToDevice : cudaMemcpyHostToHost);
@@ -1175,39 +1322,61 @@ void ipcg_archive_free(ipcg_archive *a) {
 }
 
 int ipcg_reconstruct(ipcg_ctx *c, ipcg_archive *a, int scalar, const int *k, void *out, int out_on_device,
-                     ipcg_session **session_out, uint64_t *loaded) {
-    if (session_out) *session_out = nullptr;
-    return guarded(c, [&] { retrieve_impl(c, a, scalar, k, out, out_on_device, nullptr, nullptr, 0, session_out, loaded); });
-}
-
-int ipcg_refine(ipcg_ctx *c, ipcg_archive *a, int scalar, const ipcg_session *s, const void *previous, int prev_on_dev,
-                const int *k, void *out, int out_on_device, ipcg_session **session_out, uint64_t *loaded) {
+                     uint64_t out_count, ipcg_session **session_out, ipcg_retrieve_stats *stats) {
     if (session_out) *session_out = nullptr;
     return guarded(c, [&] {
-        if (!s) throw Error(EINVAL_, "refinement needs a session");
-        retrieve_impl(c, a, scalar, k, out, out_on_device, s, previous, prev_on_dev, session_out, loaded);
+        retrieve_impl(c, a, scalar, k, out, out_on_device, out_count, nullptr, nullptr, 0, 0, session_out, stats);
     });
 }
 
+int ipcg_refine(ipcg_ctx *c, ipcg_archive *a, int scalar, const ipcg_session *s, const void *previous, int prev_on_dev,
+                uint64_t previous_count, const int *k, void *out, int out_on_device, uint64_t out_count,
+                ipcg_session **session_out, ipcg_retrieve_stats *stats) {
+    if (session_out) *session_out = nullptr;
+    return guarded(c, [&] {
+        if (!s) throw Error(EINVAL_, "refinement needs a session");
+        retrieve_impl(c, a, scalar, k, out, out_on_device, out_count, s, previous, prev_on_dev, previous_count,
+                      session_out, stats);
+    });
+}
+
+// RetrievalSession from host data (session.hpp:19-34), validated the way a refinement would use
+// it: plane counts in 0..32, 32 above the progressive bound, codewords for every progressive
+// level that has planes loaded
 int ipcg_session_create(ipcg_ctx *c, const ipcg_archive *a, const int *planes_loaded, const uint32_t *const *merged,
                         ipcg_session **out) {
+    if (out) *out = nullptr;
     return guarded(c, [&] {
+        if (!a || !planes_loaded || !out) throw Error(EINVAL_, "session_create: null argument");
+        const int L = a->ix.levels, lp = a->ix.progressive_levels;
+        for (int l = 0; l < L; ++l) {
+            const int kk = planes_loaded[l];
+            if (kk < 0 || kk > 32) throw Error(EINVAL_, "plane index out of range");
+            if (l + 1 > lp && kk != 32) throw Error(EINVAL_, "non-progressive levels must load all planes");
+            if (l + 1 <= lp && kk > 0 && !(merged && merged[l]))
+                throw Error(ERUNTIME, "session codeword array has wrong length");
+        }
         ipcg_session *s = new ipcg_session;
         s->archive_crc = a->ix.identity;
-        s->levels = a->ix.levels;
-        s->lp = a->ix.progressive_levels;
+        s->levels = L;
+        s->lp = lp;
         s->owner = c->stream;
         s->pool = &c->scratch;
         s->device = c->device;
-        for (int l = 0; l < s->levels; ++l) {
-            s->k[l] = planes_loaded[l];
-            s->count[l] = a->ix.records[l].count;
-            if (l + 1 <= s->lp && merged && merged[l]) {
-                const uint64_t cnt = s->count[l];
-                s->merged[l] = static_cast<uint32_t *>(c->scratch.get(std::max<uint64_t>(cnt, 1) * 4 + 16, c->stream));
-                CK(cudaMemcpyAsync(s->merged[l], merged[l], cnt * 4, cudaMemcpyHostToDevice, c->stream));
-                CK(cudaStreamSynchronize(c->stream));
+        try {
+            for (int l = 0; l < L; ++l) {
+                s->k[l] = planes_loaded[l];
+                s->count[l] = a->ix.records[l].count;
+                if (l + 1 <= lp && merged && merged[l]) {
+                    const uint64_t cnt = s->count[l];
+                    s->merged[l] = static_cast<uint32_t *>(c->scratch.get(std::max<uint64_t>(cnt, 1) * 4 + 16, c->stream));
+                    CK(cudaMemcpyAsync(s->merged[l], merged[l], cnt * 4, cudaMemcpyHostToDevice, c->stream));
+                }
             }
+            CK(cudaStreamSynchronize(c->stream));
+        } catch (...) {
+            ipcg_session_free(s);
+            throw;
         }
         *out = s;
     });
@@ -1519,6 +1688,30 @@ int ipcg_plan_for_size(ipcg_ctx *c, const ipcg_archive *a, uint64_t budget, int 
 double ipcg_bound_for_plan(const ipcg_archive *a, const int *k) { return bound_for_plan(a->ix, k); }
 uint64_t ipcg_plan_payload_bytes(const ipcg_archive *a, const int *k) { return plan_payload_bytes(a->ix, k); }
 
+int ipcg_build_error_model(const ipcg_index *ix, ipcg_error_model *out) {
+    return guarded(nullptr, [&] {
+        if (!ix || !out) throw Error(EINVAL_, "build_error_model: null argument");
+        if (ix->levels > IPCG_MAX_LEVELS) throw Error(EINVAL_, "archive has more levels than supported");
+        build_error_model(*ix, *out);
+    });
+}
+int ipcg_model_plan_for_error(const ipcg_error_model *m, double max_error, int *k_out) {
+    return guarded(nullptr, [&] {
+        check_model(*m);
+        plan_for_error(*m, max_error, k_out);
+    });
+}
+int ipcg_model_plan_for_size(const ipcg_error_model *m, uint64_t budget, int *k_out) {
+    return guarded(nullptr, [&] {
+        check_model(*m);
+        plan_for_size(*m, budget, k_out);
+    });
+}
+double ipcg_model_bound_for_plan(const ipcg_error_model *m, const int *k) { return bound_for_plan(*m, k); }
+uint64_t ipcg_model_plan_payload_bytes(const ipcg_error_model *m, const int *k) { return plan_payload_bytes(*m, k); }
+uint64_t ipcg_model_mandatory_payload_bytes(const ipcg_error_model *m) { return mandatory_payload_bytes(*m); }
+uint64_t ipcg_model_total_payload_bytes(const ipcg_error_model *m) { return total_payload_bytes(*m); }
+
 int ipcg_backend_encode(ipcg_ctx *c, const uint8_t *raw, int raw_on_device, uint64_t plane_bytes, uint64_t raw_stride,
                         int count, uint8_t *backend, uint64_t *length, uint32_t *crc, uint8_t *out_payload,
                         uint64_t out_capacity) {
@@ -1607,6 +1800,70 @@ int ipcg_backend_decode(ipcg_ctx *c, const uint8_t *payloads, const uint64_t *pa
                 if (js[k]) status[job_of[k]] = 2;
         }
         CK(cudaMemcpyAsync(out, dout.p, tout, cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
+    });
+}
+
+// ---------------------------------------------------------- bitplane API
+// split / xor_encode / xor_decode / merge (bitplane.cpp:7-59) on host plane arrays: staged
+// through 32 device word rows (16-byte aligned, zero-padded past the plane's bytes)
+namespace {
+struct PlaneRows {
+    DBuf buf;
+    uint64_t stride = 0, nbytes = 0;
+    PlaneRows(uint64_t count, cudaStream_t st) {
+        nbytes = (count + 7) / 8;
+        stride = round_up(std::max<uint64_t>((count + 31) / 32, 1), 4);
+        buf = DBuf(32 * stride * 4, st);
+        CK(cudaMemsetAsync(buf.p, 0, 32 * stride * 4, st));
+    }
+    uint32_t *row(int p) const { return buf.as<uint32_t>() + (uint64_t)p * stride; }
+    void upload(const uint8_t *const *planes, int np, cudaStream_t st) {
+        for (int p = 0; p < np; ++p)
+            if (nbytes) CK(cudaMemcpyAsync(row(p), planes[p], nbytes, cudaMemcpyHostToDevice, st));
+    }
+    void download(uint8_t *const *planes, int np, cudaStream_t st) {
+        for (int p = 0; p < np; ++p)
+            if (nbytes) CK(cudaMemcpyAsync(planes[p], row(p), nbytes, cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
+    }
+};
+}  // namespace
+
+int ipcg_split(ipcg_ctx *c, const uint32_t *codewords, uint64_t count, int xor_encode, uint8_t *const *planes) {
+    return guarded(c, [&] {
+        if (!planes || (count && !codewords)) throw Error(EINVAL_, "split: null argument");
+        cudaStream_t st = c->stream;
+        PlaneRows r(count, st);
+        DBuf codes(std::max<uint64_t>(count, 1) * 4, st);
+        if (count) CK(cudaMemcpyAsync(codes.p, codewords, count * 4, cudaMemcpyHostToDevice, st));
+        launch_split(codes.as<uint32_t>(), count, r.row(0), r.stride, xor_encode != 0, st);
+        r.download(planes, 32, st);
+    });
+}
+
+int ipcg_plane_xor(ipcg_ctx *c, uint8_t *const *planes, uint64_t count, int np, int decode) {
+    return guarded(c, [&] {
+        if (np < 0 || np > 32) throw Error(EINVAL_, "plane count out of range");
+        if (!planes) throw Error(EINVAL_, "plane_xor: null argument");
+        cudaStream_t st = c->stream;
+        PlaneRows r(count, st);
+        r.upload(planes, np, st);
+        launch_plane_xor(r.row(0), r.stride, count, np, decode != 0, st);
+        r.download(planes, np, st);
+    });
+}
+
+int ipcg_merge(ipcg_ctx *c, const uint8_t *const *planes, uint64_t count, int k, uint32_t *codewords) {
+    return guarded(c, [&] {
+        if (k < 0 || k > 32) throw Error(EINVAL_, "plane count out of range");
+        if ((k && !planes) || (count && !codewords)) throw Error(EINVAL_, "merge: null argument");
+        cudaStream_t st = c->stream;
+        PlaneRows r(count, st);
+        r.upload(planes, k, st);
+        DBuf out(std::max<uint64_t>(count, 1) * 4, st);
+        launch_merge_raw(r.row(0), r.stride, count, k, out.as<uint32_t>(), st);
+        if (count) CK(cudaMemcpyAsync(codewords, out.p, count * 4, cudaMemcpyDeviceToHost, st));
         CK(cudaStreamSynchronize(st));
     });
 }

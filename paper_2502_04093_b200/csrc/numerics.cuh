@@ -58,4 +58,10 @@ void launch_outlier_apply(void *state, int scalar, const PassDesc &pd, const uin
 void launch_outlier_prefix(const uint8_t *block, uint64_t entries, int scalar, uint64_t count, uint64_t *napplied,
                            cudaStream_t st);
 
+// bitplane.cpp:7-59 as standalone operations on 32 word rows (bitops.cu)
+void launch_split(const uint32_t *codes, uint64_t count, uint32_t *rows, uint64_t stride, bool xor_encode,
+                  cudaStream_t st);
+void launch_plane_xor(uint32_t *rows, uint64_t stride, uint64_t count, int np, bool decode, cudaStream_t st);
+void launch_merge_raw(const uint32_t *rows, uint64_t stride, uint64_t count, int k, uint32_t *out, cudaStream_t st);
+
 }  // namespace ipcg

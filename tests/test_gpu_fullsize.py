@@ -2,8 +2,10 @@
 256x384x384 f64, 64^3), on the seeded synthetic fields bench.py uses.
 
 Exact: the whole archive is byte-identical to the compiled reference (oracle/_ref, the
-unmodified reference's own multi-threaded CPU code) and, for every retrieval target of the
-config, the reconstruction equals the reference's bit for bit.  Size-independent
+unmodified reference's own multi-threaded CPU code); for EVERY retrieval target of every config
+(cfg2's four, cfg5's six, cfg3's bitrates incl. the non-fill partial plans) the reconstruction
+and the session's merged codewords equal the reference's bit for bit, and every refine step
+equals the reference's refine_field from the same session.  Size-independent
 properties on top (the reference's acceptance criteria, acceptance.cpp:80-104): a full
 retrieval meets the point-wise bound; every planned retrieval's measured error is within
 bound_for_plan, which is within the requested target; a refine chain lands bit-identical
@@ -62,12 +64,20 @@ def test_full_size_config(cfg, ctx):
             assert bound <= t * rng, (cfg, t, bound)
         else:
             assert ipc.plan_payload_bytes(reader, plan) <= int(t * n / 8)
+        want = want_merged = None
+        if ref is not None:  # every target of every config, against the reference's own code
+            want, want_merged, _ = ref.reconstruct(arch, plan.k, f.dtype, n)
+            assert fresh.values.cpu().numpy().tobytes() == want.tobytes(), (cfg, kind, t)
+            for l in range(1, reader.header().progressive_levels + 1):
+                assert np.array_equal(fresh.session.merged(l), want_merged[l - 1]), (cfg, kind, t, l)
         if prev is not None and all(a >= b for a, b in zip(plan.k, prev.session.planes_loaded())):
             refined = ipc.refine_field(reader, prev.session, prev.values, plan)
             assert torch.equal(_bits(refined.values), _bits(fresh.values)), (cfg, kind, t)
-        if ref is not None and (cfg in (1, 3, 4) or (cfg == 5 and (kind, t) == plans[-1][:2])):
-            want, _, _ = ref.reconstruct(arch, plan.k, f.dtype, n)
-            assert fresh.values.cpu().numpy().tobytes() == want.tobytes(), (cfg, kind, t)
+            if ref is not None:  # the reference's refine_field from the previous step's session
+                pk = prev.session.planes_loaded()
+                pm = [prev.session.merged(l) for l in range(1, reader.levels + 1)]
+                got_ref, _, _ = ref.refine(arch, pk, pm, prev.values.cpu().numpy(), plan.k)
+                assert refined.values.cpu().numpy().tobytes() == got_ref.tobytes(), (cfg, kind, t)
         prev = fresh
 
 
@@ -84,6 +94,7 @@ def test_cfg3_nonfill_range_variant(ctx):
     eb = 1e-3 * float(f[ok].max() - f[ok].min())
     ft = torch.from_numpy(f).cuda()
     reader = ipc.compress_field(ft, dims, eb, c["interp"], ctx=ctx)
+    arch = reader.to_bytes()
     n = f.size
     prev_bytes = -1
     mandatory = ipc.plan_payload_bytes(
@@ -95,6 +106,9 @@ def test_cfg3_nonfill_range_variant(ctx):
             assert int(b * n / 8) < mandatory
             continue
         got = ipc.reconstruct_field(reader, plan, device=True, keep_session=False)
+        if oracle.ref_available():  # partial bitrate plans, bit for bit against the reference
+            want, _, _ = oracle.load("ref").reconstruct(arch, plan.k, f.dtype, n)
+            assert got.values.cpu().numpy().tobytes() == want.tobytes(), b
         loaded = got.stats.payload_bytes_loaded
         assert loaded == ipc.plan_payload_bytes(reader, plan) >= prev_bytes
         prev_bytes = loaded
@@ -104,4 +118,4 @@ def test_cfg3_nonfill_range_variant(ctx):
         ulp = float(np.spacing(np.float32(np.abs(f[ok]).max())))
         assert ipc.compute_metrics(ft, got.values, ctx=ctx).max_error <= ipc.bound_for_plan(reader, plan) + 4 * ulp
     if oracle.ref_available():
-        assert reader.to_bytes() == oracle.load("ref").compress(f, dims, eb, c["interp"])
+        assert arch == oracle.load("ref").compress(f, dims, eb, c["interp"])
