@@ -217,6 +217,24 @@ def run_ours(args, ws, rank, local):
     comp["archive_bytes"] = archive_bytes
     comp["compression_ratio"] = round(nbytes / archive_bytes, 3)
 
+    # SURVEY.md §8(d) canonical algorithmic bytes (each stage's distinct HBM inputs and outputs
+    # once per element): compress (4w + 20) n + P, retrieval of plan k  P_k + 2 R_k + (8 + 2w) n
+    # with R_k = sum_l k_l ceil(count_l / 8) the decoded plane bytes
+    peak, peak_src = measured_peak()
+    P = reader.header().payload_bytes
+    counts = [int(reader.record(l).count) for l in range(1, reader.levels + 1)]
+    pipeline = {"compress": {"ms": round(nbytes / comp["compress_gbs"] / 1e6, 3),
+                             "algorithmic_bytes": (4 * w + 20) * n + P}}
+    for rel in rels:
+        plan = ipc.plan_for_error(reader, rel * rng)
+        Rk = sum(k * ((cnt + 7) // 8) for k, cnt in zip(plan.k, counts))
+        pipeline[f"retrieve rel {rel}"] = {"ms": round(nbytes / fresh[str(rel)] / 1e6, 3),
+                                           "algorithmic_bytes": ipc.plan_payload_bytes(reader, plan) + 2 * Rk
+                                           + (8 + 2 * w) * n}
+    for v in pipeline.values():
+        v["achieved"] = round(v["algorithmic_bytes"] / (v["ms"] / 1e3) / 1e9, 2)
+        v["frac"] = round(v["achieved"] / peak, 5)
+
     # roofline of the dominant kernel family, from CUDA events around each family.  This extra
     # step runs with the profiler on, which keeps compress on one stream (in the timed steps
     # each level's lossless stage overlaps the others), so family spans are not inflated.
@@ -229,8 +247,9 @@ def run_ours(args, ws, rank, local):
     prof = ctx.profile_read()
     ctx.profile(False)
     step_ms = p0.elapsed_time(p1)
-    peak, peak_src = measured_peak()
     top = max(prof.items(), key=lambda kv: kv[1]["ms"])
+    # families record §8(d)-canonical bytes: a deflate.* family the 32 x ceil(count/8) plane
+    # bytes it consumes, the loss table the 4-byte codes it reads, and so on
     achieved = top[1]["bytes"] / (top[1]["ms"] / 1e3) / 1e9 if top[1]["ms"] > 0 else 0.0
 
     def gbs(fam):
@@ -246,15 +265,19 @@ def run_ours(args, ws, rank, local):
             hbm[fam] = {"ms": round(prof[fam]["ms"], 3), "achieved": round(g, 1), "frac": round(g / peak, 4)}
     # measured DRAM traffic of the dominant family (ncu, one compress = one step's launches)
     traffic, traffic_src = None, None
-    tp = os.path.join(ROOT, "profiles", "r01_traffic.json")
-    if os.path.exists(tp):
-        tj = json.load(open(tp)).get(top[0])
+    for tp in (os.path.join(ROOT, "profiles", "r02_traffic.json"), os.path.join(ROOT, "profiles", "r01_traffic.json")):
+        tj = json.load(open(tp)).get(top[0]) if os.path.exists(tp) else None
         if tj:
             traffic, traffic_src = int(tj["dram_bytes"]), tj["source"]
+            break
     roofline = {"bound": "hbm", "kernel": top[0], "achieved": round(achieved, 2), "peak": peak,
                 "unit": "GB/s", "frac": round(achieved / peak, 5), "traffic": traffic,
                 "traffic_basis": "bytes per step for the family (same basis as achieved)", "traffic_source": traffic_src,
                 "algorithmic_bytes": int(top[1]["bytes"]),
+                "traffic_over_algorithmic": round(traffic / top[1]["bytes"], 3) if traffic and top[1]["bytes"] else None,
+                "pipeline": pipeline,
+                "pipeline_basis": "SURVEY.md 8(d): compress (4w+20)n + P; retrieve P_k + 2R_k + (8+2w)n; "
+                                  "device-resident single calls, CUDA events",
                 "share_of_step": round(top[1]["ms"] / step_ms, 4) if step_ms else None,
                 "peak_source": peak_src,
                 "family_timing": "CUDA events per family in one profiled step run serially "
@@ -318,12 +341,7 @@ def run_ours(args, ws, rank, local):
             "scaling": "weak", "vs_baseline": None, "dtype": "f32" if w == 4 else "f64",
             "data": "synthetic: seeded Gaussian random field P(k)~k^-11/3 by FFT synthesis, normalised to [0,1] "
                     "(stands in for the paper's SDRBench fields)",
-            "config": {"workload": f"cfg{args.config}: {'x'.join(map(str, dims))} {np.dtype(f.dtype).name} "
-                                   f"{'cubic' if c['interp'] else 'linear'} rel eb {c['rel_eb']}; step = compress + "
-                                   f"progressive retrieve rel {rels[0]} then refine {rels[1:]}",
-                       "dims": list(dims), "rel_eb": c["rel_eb"], "abs_eb": eb,
-                       "l2": f"inputs {nbytes >> 20} MiB > 126 MB L2 (no flush needed)",
-                       "parallelism": f"replicas x{ws}"},
+            "config": workload_config(args.config, dims, f, eb, ws),
             "e2e": e2e, "roofline": roofline, "cpu_baseline": cpu, "gpu_launches": int(launches),
             "clocks": clk.summary(), "detail": comp,
         }
@@ -331,10 +349,20 @@ def run_ours(args, ws, rank, local):
 
 
 # ------------------------------------------------------------ CPU reference
-def _sample(f, dims, frac_dims=(128, 256, 256)):
+def _sample(f, dims, frac_dims=(256, 256, 256)):
     d = tuple(min(a, b) for a, b in zip(dims, frac_dims)) if len(dims) == 3 else dims
     v = f.reshape(dims)[tuple(slice(0, x) for x in d)]
     return np.ascontiguousarray(v).reshape(-1), d
+
+
+def cpu_model():
+    try:
+        for ln in open("/proc/cpuinfo"):
+            if ln.startswith("model name"):
+                return ln.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
 
 
 def reference_cycle(ref, v, d, c, eb, rels):
@@ -354,44 +382,54 @@ def reference_cycle(ref, v, d, c, eb, rels):
     return time.perf_counter() - t0, len(arch)
 
 
-def cpu_baseline(cfg, f, dims, c):
+def _load_ref():
+    import oracle
+
     try:
-        import oracle
-
-        ref = oracle.load("ref")
-        kind = "reference"
+        return oracle.load("ref"), "reference"
     except Exception:
-        import oracle
+        return oracle.load("oracle"), "port"
 
-        ref = oracle.load("oracle")
-        kind = "port"
-    v, d = _sample(f, dims)
-    eb = synth.abs_eb(v, c["rel_eb"])
-    threads = int(os.environ.get("IPCOMP_THREADS", "0")) or min(os.cpu_count() or 1, 16)
-    t, _ = reference_cycle(ref, v, d, c, eb, retrieval_targets(cfg))
-    return {"value": round(v.nbytes / t / 1e9, 5), "unit": "GB/s", "cores": threads, "kind": kind,
-            "sample": f"compress + progressive retrieve chain of a {'x'.join(map(str, d))} sub-volume "
-                      f"({v.nbytes >> 20} MiB) of the same field, one run, {t:.1f} s"}
+
+def cpu_baseline(cfg, f, dims, c):
+    """the reference's CPU compress + retrieve chain on this box's cores --
+    the FULL field with IPCOMP_THREADS unset (min(nproc, 16) workers, parallel.hpp:15-22), and a
+    sub-volume with IPCOMP_THREADS=1."""
+    ref, kind = _load_ref()
+    rels = retrieval_targets(cfg)
+    saved = os.environ.pop("IPCOMP_THREADS", None)
+    threads = min(os.cpu_count() or 1, 16)
+    eb = synth.abs_eb(f, c["rel_eb"])
+    v = np.ascontiguousarray(f).reshape(-1)
+    t_full, _ = reference_cycle(ref, v, dims, c, eb, rels)
+    vs, ds = _sample(f, dims, (128, 128, 128))
+    os.environ["IPCOMP_THREADS"] = "1"
+    t_one, _ = reference_cycle(ref, vs, ds, c, synth.abs_eb(vs, c["rel_eb"]), rels)
+    os.environ.pop("IPCOMP_THREADS")
+    if saved is not None:
+        os.environ["IPCOMP_THREADS"] = saved
+    return {"value": round(v.nbytes / t_full / 1e9, 5), "unit": "GB/s", "cores": threads, "kind": kind,
+            "sample": f"the full {'x'.join(map(str, dims))} field ({v.nbytes >> 20} MiB): compress + progressive "
+                      f"retrieve chain, IPCOMP_THREADS unset ({threads} workers), one run, {t_full:.1f} s",
+            "single_thread": {"value": round(vs.nbytes / t_one / 1e9, 6), "unit": "GB/s", "cores": 1,
+                              "sample": f"{'x'.join(map(str, ds))} sub-volume ({vs.nbytes >> 20} MiB), "
+                                        f"IPCOMP_THREADS=1, one run, {t_one:.1f} s"},
+            "cpu_model": cpu_model(), "nproc": os.cpu_count()}
 
 
 def run_reference(args, ws, rank):
+    """The reference arm: the reference's own CPU code (oracle/_ref) on this box's host cores,
+    every step a bounded sample (a 256^3 sub-volume) of our arm's workload."""
     if rank != 0:
         return
-    import oracle
-
     c = synth.CONFIGS[args.config]
     dims = tuple(int(x) for x in args.dims.split("x")) if args.dims else c["dims"]
-    try:
-        ref = oracle.load("ref")
-        kind = "reference"
-    except Exception:
-        ref = oracle.load("oracle")
-        kind = "port"
-    threads = os.cpu_count() or 1
-    os.environ["IPCOMP_THREADS"] = str(threads)
+    ref, kind = _load_ref()
+    threads = min(os.cpu_count() or 1, 16)
+    os.environ.pop("IPCOMP_THREADS", None)  # the reference's default worker count
     f = synth.make_field(args.config, seed=0, dims=dims, device="cpu")
     v, d = _sample(f, dims)
-    eb = synth.abs_eb(v, c["rel_eb"])
+    eb = synth.abs_eb(f, c["rel_eb"])  # the workload's eb (range of the whole field)
     rels = retrieval_targets(args.config)
     for _ in range(args.warmup):
         reference_cycle(ref, v, d, c, eb, rels)
@@ -402,16 +440,28 @@ def run_reference(args, ws, rank):
     total = sum(times)
     value = v.nbytes * args.steps / total / 1e9
     sample = (f"each step: compress + progressive retrieve chain of a {'x'.join(map(str, d))} sub-volume "
-              f"({v.nbytes >> 20} MiB) of the cfg{args.config} field")
+              f"({v.nbytes >> 20} MiB) of the cfg{args.config} field, same eb and targets")
     line = {"metric": METRIC, "value": round(value, 5), "unit": "GB/s", "n_gpus": ws, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": round(1e3 * total / args.steps, 3), "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f32" if f.itemsize == 4 else "f64",
-            "data": "synthetic", "impl": "reference",
-            "config": {"workload": f"cfg{args.config}: {'x'.join(map(str, dims))} (sampled)", "dims": list(dims)},
+            "data": "synthetic", "impl": "reference", "config": workload_config(args.config, dims, f, eb, ws),
+            "sampled": True,
             "cpu_baseline": {"value": round(value, 5), "unit": "GB/s", "cores": threads, "kind": kind,
-                             "sample": sample},
+                             "sample": sample, "cpu_model": cpu_model(), "nproc": os.cpu_count()},
             "e2e": {"value": round(value, 5), "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
+
+
+def workload_config(cfg, dims, f, eb, ws):
+    c = synth.CONFIGS[cfg]
+    rels = retrieval_targets(cfg)
+    nbytes = f.size * f.itemsize
+    return {"workload": f"cfg{cfg}: {'x'.join(map(str, dims))} {np.dtype(f.dtype).name} "
+                        f"{'cubic' if c['interp'] else 'linear'} rel eb {c['rel_eb']}; step = compress + "
+                        f"progressive retrieve rel {rels[0]} then refine {rels[1:]}",
+            "dims": list(dims), "rel_eb": c["rel_eb"], "abs_eb": eb,
+            "l2": f"inputs {nbytes >> 20} MiB > 126 MB L2 (no flush needed)",
+            "parallelism": f"replicas x{ws}"}
 
 
 def main():

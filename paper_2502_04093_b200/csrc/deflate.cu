@@ -1185,7 +1185,7 @@ void DeflateBatch::run(const uint8_t *in, uint64_t in_stride, int S, uint64_t n,
             attr = true;
         }
         {
-        ProfScope ps1("deflate.prevlinks", st, (uint64_t)S * n * 3);
+        ProfScope ps1("deflate.prevlinks", st, (uint64_t)S * n);
         static int span_env = getenv("IPCG_PL_SPAN") ? atoi(getenv("IPCG_PL_SPAN")) : 0;
         int span = span_env;
         if (span <= 0) {
@@ -1201,7 +1201,7 @@ void DeflateBatch::run(const uint8_t *in, uint64_t in_stride, int S, uint64_t n,
         CKL();
         }
         {
-        ProfScope ps2("deflate.match", st, (uint64_t)S * n * 11);
+        ProfScope ps2("deflate.match", st, (uint64_t)S * n);
         if (n < (1ull << 31))
             k_match<false><<<dim3(grid_for(n, 256, 4096), S), 256, 0, st>>>(in, in_stride, n, w.meta, w.prevd, w.rec);
         else
@@ -1210,7 +1210,7 @@ void DeflateBatch::run(const uint8_t *in, uint64_t in_stride, int S, uint64_t n,
         }
         if (after_match) CK(cudaEventRecord(after_match, st));
         {
-        ProfScope ps3("deflate.anchor", st, (uint64_t)S * n * 8);
+        ProfScope ps3("deflate.anchor", st, (uint64_t)S * n);
         k_anchor<<<dim3((unsigned)((n + TILE - 1) / TILE), S), 256, 0, st>>>(n, w.meta, w.rec, w.nchunks, w.first_anchor);
         CKL();
         const dim3 bg((unsigned)((w.nseg + 1 + 255) / 256), S);
@@ -1223,13 +1223,13 @@ void DeflateBatch::run(const uint8_t *in, uint64_t in_stride, int S, uint64_t n,
         CKL();
         }
         {
-        ProfScope ps3("deflate.sim", st, (uint64_t)S * n * 8);
+        ProfScope ps3("deflate.sim", st, (uint64_t)S * n);
         k_sim<<<dim3((unsigned)((w.nchunks + 255) / 256), S), 256, 0, st>>>(n, w.meta, w.rec, w.nchunks, w.bnd,
                                                                               w.nbreak, w.exit4, w.cnt4);
         CKL();
         }
         {
-        ProfScope ps3("deflate.resolve", st, (uint64_t)S * w.nchunks * 8);
+        ProfScope ps3("deflate.resolve", st, (uint64_t)S * n);
         const dim3 sg((unsigned)((w.nseg + 1 + 255) / 256), S);
         k_seg_compose<<<sg, 256, 0, st>>>(w.meta, w.nchunks, w.nseg, w.exit4, w.cnt4, w.seg_exit4, w.seg_cnt4);
         CKL();
@@ -1241,21 +1241,21 @@ void DeflateBatch::run(const uint8_t *in, uint64_t in_stride, int S, uint64_t n,
         CKL();
         }
         {
-        ProfScope ps3("deflate.emit_syms", st, (uint64_t)S * n * 12);
+        ProfScope ps3("deflate.emit_syms", st, (uint64_t)S * n);
         k_emit_syms<<<dim3((unsigned)((w.nchunks + 255) / 256), S), 256, 0, st>>>(in, in_stride, n, w.meta, w.rec, w.nchunks, w.bnd, w.nbreak, w.entry, w.symoff, w.syms, w.maxb, w.blk_top, w.blk_start, w.runs, w.nruns);
         CKL();
         k_emit_runs<<<148 * 4, 256, 0, st>>>(n, w.rec, w.syms, w.maxb, w.blk_top, w.blk_start, w.runs, w.nruns);
         CKL();
         }
         {
-        ProfScope ps4("deflate.blocks", st, (uint64_t)S * n * 4);
+        ProfScope ps4("deflate.blocks", st, (uint64_t)S * n);
         k_plan<<<dim3((unsigned)w.maxb, S), 32, 0, st>>>(n, w.meta, w.syms, w.maxb, w.blk_top, w.blk_start, w.trees);
         CKL();
         k_layout<<<S, 32, 0, st>>>(n, w.meta, S, w.maxb, w.trees, w.blk_bitpos);
         CKL();
         }
         {
-        ProfScope ps5("deflate.emit", st, (uint64_t)S * n * 4);
+        ProfScope ps5("deflate.emit", st, (uint64_t)S * n);
         k_zero_out<<<dim3(grid_for(n / 8 + 2, 256, 512), S), 256, 0, st>>>(n, w.meta, out, out_stride);
         CKL();
         k_emit<<<dim3((unsigned)w.maxb, S), 256, 0, st>>>(in, in_stride, n, w.meta, w.syms, w.maxb, w.blk_start, w.trees, w.blk_bitpos, out, out_stride);
