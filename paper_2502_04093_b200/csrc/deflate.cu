@@ -68,9 +68,33 @@ struct Work {
     uint32_t *crc_part;
     uint32_t *crc_tab;
     uint64_t nchunks, nseg, maxb, ncrc;
+    // on-demand parse (streams < 2^31 bytes): per-position visit words, the chunk walks'
+    // symbols and loop-top offsets (all three alias `rec`, which only the wide path uses)
+    uint16_t *od_vis, *od_spos;
+    uint32_t *od_ssym;
+    struct OdChunk *od_chunks;
+    uint64_t od_nch;
+    uint32_t od_C;
 };
 
 constexpr uint64_t SEG = 32;  // chunks per resolve segment
+
+// one chunk of the on-demand parse (deflate_core.cuh Walker): its walk from (start, A), the
+// continuation from the walk's exit, and its place on the true parse
+struct OdChunk {
+    uint32_t nsym;                        // symbols of the chunk's own walk
+    uint32_t ex_p, ex_tag, ex_pl, ex_pd;  // the walk's exit state (first loop top past the chunk)
+    uint32_t nxt;                         // chunk whose walk the continuation joins (od_nch: stream end)
+    uint32_t nidx;                        // ... at that walk's symbol index; the final tag at the end
+    uint32_t ncont;                       // symbols the continuation emits before it joins
+    uint32_t adopted, aidx;               // on the true parse; its first own symbol on it
+    uint64_t aoff, coff;                  // output offsets of the adopted own symbols / the continuation
+};
+
+static uint32_t od_chunk_size() {
+    static const uint32_t c = getenv("IPCG_OD_CHUNK") ? (uint32_t)atoi(getenv("IPCG_OD_CHUNK")) : 1024u;
+    return c < 64 ? 64u : c > 8192 ? 8192u : c;
+}
 
 Work carve(void *ws, int S, uint64_t n, size_t *size_out = nullptr) {
     Bump b{static_cast<uint8_t *>(ws)};
@@ -84,6 +108,12 @@ Work carve(void *ws, int S, uint64_t n, size_t *size_out = nullptr) {
     w.nruns = b.take<unsigned long long>(1);
     w.prevd = b.take<uint16_t>((size_t)S * n);
     w.rec = b.take<uint64_t>((size_t)S * n);
+    w.od_C = od_chunk_size();
+    w.od_nch = (n + w.od_C - 1) / w.od_C;
+    w.od_vis = reinterpret_cast<uint16_t *>(w.rec);
+    w.od_spos = w.od_vis + (size_t)S * n;
+    w.od_ssym = reinterpret_cast<uint32_t *>(w.od_spos + (size_t)S * n);  // 4-byte aligned: 4Sn bytes in
+    w.od_chunks = b.take<OdChunk>((size_t)S * w.od_nch);
     w.first_anchor = b.take<uint64_t>((size_t)S * w.nchunks);
     w.nbreak = b.take<uint32_t>((size_t)S * (w.nchunks + 1));
     w.bnd = b.take<uint64_t>((size_t)S * (w.nchunks + 1));
@@ -796,6 +826,204 @@ __global__ void __launch_bounds__(256) k_emit_runs(uint64_t n, const uint64_t *r
     }
 }
 
+
+// ------------------------------------------------------- on-demand parse (n < 2^31)
+// deflate_core.cuh's Walker: the lazy parse searches longest_match only at the loop tops it
+// visits, with the one chain limit it needs.  (1) k_od_walk: a thread per chunk walks the parse
+// from (chunk start, A), stamping every visited state in od_vis and buffering its symbols;
+// (2) k_od_sync: a thread per chunk continues its walk past the chunk end until it reaches a
+// state the walk of the chunk it is in also visited -- from there both agree; (3) k_od_chain:
+// a warp per stream follows the joins from chunk 0 (the true start), giving each adopted chunk
+// its output offsets; (4) k_od_place: a warp per adopted chunk copies its symbols from the join
+// point and re-walks its continuation.  Pinned to zlib by tests/native/zmodel.cpp
+// (zmodel_compress_od, the same functions run sequentially).
+__global__ void __launch_bounds__(128) k_od_walk(const uint8_t *in, uint64_t in_stride, uint32_t n,
+                                                const StreamMeta *meta, const uint16_t *prevd_all, uint32_t C,
+                                                uint32_t nch, uint16_t *vis_all, uint32_t *ssym_all,
+                                                uint16_t *spos_all, OdChunk *chunks_all) {
+    const int j = blockIdx.y;
+    if (!meta[j].active) return;
+    const uint32_t k = blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= nch) return;
+    const uint8_t *inj = in + (uint64_t)j * in_stride;
+    const uint16_t *pvj = prevd_all + (uint64_t)j * n;
+    asm volatile("" : "+l"(inj), "+l"(pvj));
+    const InWords words{inj};
+    const PrevD32 prev{pvj};
+    uint16_t *vis = vis_all + (uint64_t)j * n;
+    uint32_t *ssym = ssym_all + (uint64_t)j * n;
+    uint16_t *spos = spos_all + (uint64_t)j * n;
+    const uint32_t b0 = k * C, b1 = min(n, b0 + C);
+    Walker w{b0, TAG_A, 0, 0};
+    uint32_t cnt = 0;
+    while (w.p < b1) {
+        const uint32_t p = w.p;
+        vis[p] = vis_pack(w.tag, cnt);
+        const uint32_t sym = walker_step(w, n, words, prev);
+        if (sym != NOSYM) {
+            ssym[b0 + cnt] = sym;
+            spos[b0 + cnt] = (uint16_t)(p - b0);
+            ++cnt;
+        }
+    }
+    OdChunk &c = chunks_all[(uint64_t)j * nch + k];
+    c.nsym = cnt;
+    c.ex_p = w.p, c.ex_tag = w.tag, c.ex_pl = w.pl, c.ex_pd = w.pd;
+}
+
+// the continuation of a chunk walk: from its exit state until a visited state (or the stream
+// end); emits into syms (with block bookkeeping) when given, counts otherwise
+template <bool EMIT>
+__device__ uint32_t od_follow(Walker w, uint32_t n, uint32_t C, uint32_t nch, const InWords &words, const PrevD32 &prev,
+                              const uint16_t *vis, uint32_t &nxt, uint32_t &idx, uint32_t *syms, uint64_t g,
+                              uint64_t *btop, uint64_t *bstart) {
+    uint32_t cnt = 0;
+    for (;;) {
+        if (w.p >= n) {
+            nxt = nch;
+            idx = w.tag;
+            return cnt;
+        }
+        const uint16_t v = vis[w.p];
+        if (vis_match(v, w.tag)) {
+            nxt = w.p / C;
+            idx = vis_symidx(v);
+            return cnt;
+        }
+        const uint32_t p = w.p;
+        const uint32_t sym = walker_step(w, n, words, prev);
+        if (sym != NOSYM) {
+            if (EMIT) {
+                syms[g] = sym;
+                if (g % BLOCK_SYMS == 0) bstart[g / BLOCK_SYMS] = (uint64_t)p - 1;
+                if (g % BLOCK_SYMS == BLOCK_SYMS - 1) btop[g / BLOCK_SYMS] = (uint64_t)p;
+                ++g;
+            }
+            ++cnt;
+        }
+    }
+}
+
+__global__ void __launch_bounds__(128) k_od_sync(const uint8_t *in, uint64_t in_stride, uint32_t n,
+                                                const StreamMeta *meta, const uint16_t *prevd_all, uint32_t C,
+                                                uint32_t nch, const uint16_t *vis_all, OdChunk *chunks_all) {
+    const int j = blockIdx.y;
+    if (!meta[j].active) return;
+    const uint32_t k = blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= nch) return;
+    const uint8_t *inj = in + (uint64_t)j * in_stride;
+    const uint16_t *pvj = prevd_all + (uint64_t)j * n;
+    asm volatile("" : "+l"(inj), "+l"(pvj));
+    const InWords words{inj};
+    const PrevD32 prev{pvj};
+    OdChunk &c = chunks_all[(uint64_t)j * nch + k];
+    uint32_t nxt, idx;
+    c.ncont = od_follow<false>(Walker{c.ex_p, c.ex_tag, c.ex_pl, c.ex_pd}, n, C, nch, words, prev,
+                               vis_all + (uint64_t)j * n, nxt, idx, nullptr, 0, nullptr, nullptr);
+    c.nxt = nxt, c.nidx = idx;
+}
+
+// a warp per stream follows the joins 32 chunks at a time: a run of chunks each joining its
+// successor is resolved by one warp scan; a join that skips chunks starts the next run
+__global__ void __launch_bounds__(32) k_od_chain(const uint8_t *in, uint64_t in_stride, uint32_t n, StreamMeta *meta,
+                                                uint32_t nch, OdChunk *chunks_all, uint32_t *syms_all, uint64_t maxb,
+                                                uint64_t *blk_start_all) {
+    const int j = blockIdx.x;
+    StreamMeta &m = meta[j];
+    if (!m.active) return;
+    const unsigned lane = threadIdx.x;
+    OdChunk *ch = chunks_all + (uint64_t)j * nch;
+    uint32_t a = 0, idx = 0, final_tag = TAG_A;
+    uint64_t off = 0;
+    for (uint32_t w0 = 0; w0 < nch; w0 += 32) {
+        const uint32_t k = w0 + lane;
+        const bool in_range = k < nch;
+        uint32_t nxt = in_range ? ch[k].nxt : nch, nidx = in_range ? ch[k].nidx : 0;
+        const uint32_t nsym = in_range ? ch[k].nsym : 0, ncont = in_range ? ch[k].ncont : 0;
+        unsigned adopted = 0;
+        while (a < w0 + 32 && a < nch) {
+            const unsigned la = a - w0;
+            const unsigned brk = __ballot_sync(0xffffffffu, lane >= la && in_range && (nxt != k + 1 || nxt == nch));
+            const unsigned lb = brk ? (unsigned)(__ffs(brk) - 1) : 31u;  // last lane of the run
+            const bool run = lane >= la && lane <= lb && in_range;
+            const uint32_t prev_nidx = __shfl_up_sync(0xffffffffu, nidx, 1);
+            const uint32_t my_idx = lane == la ? idx : prev_nidx;
+            const uint64_t contrib = run ? (uint64_t)(nsym - my_idx) + ncont : 0;
+            uint64_t incl = contrib;
+            for (int o = 1; o < 32; o <<= 1) {
+                const uint64_t t = __shfl_up_sync(0xffffffffu, incl, o);
+                if ((int)lane >= o) incl += t;
+            }
+            if (run) {
+                OdChunk &c = ch[k];
+                c.adopted = 1;
+                c.aidx = my_idx;
+                c.aoff = off + incl - contrib;
+                c.coff = c.aoff + (nsym - my_idx);
+            }
+            adopted |= __ballot_sync(0xffffffffu, run);
+            off += __shfl_sync(0xffffffffu, incl, 31);
+            idx = __shfl_sync(0xffffffffu, nidx, lb);
+            a = __shfl_sync(0xffffffffu, nxt, lb);
+        }
+        if (in_range && !((adopted >> lane) & 1u)) ch[k].adopted = 0;
+        if (a >= nch) {  // the run reached the stream end: its last chunk carries the final tag
+            final_tag = idx;
+            // remaining chunks (if any) are jumped over
+            for (uint32_t r = w0 + 32 + lane; r < nch; r += 32) ch[r].adopted = 0;
+            break;
+        }
+    }
+    if (lane == 0) {
+        m.S_loop = off;
+        m.final_tag = (int)final_tag;
+        const bool fin = final_tag != TAG_A && n > 0;
+        m.nsyms = off + (fin ? 1 : 0);
+        m.nblocks = off / BLOCK_SYMS + 1;
+        uint64_t *bs = blk_start_all + (uint64_t)j * maxb;
+        if (fin) {
+            syms_all[(uint64_t)j * (n + 1) + off] = sym_literal(in[(uint64_t)j * in_stride + n - 1]);
+            if (off % BLOCK_SYMS == 0) bs[off / BLOCK_SYMS] = n - 1;
+        }
+        if (m.nsyms == (m.nblocks - 1) * BLOCK_SYMS) bs[m.nblocks - 1] = n;  // empty final block
+    }
+}
+
+__global__ void __launch_bounds__(128) k_od_place(const uint8_t *in, uint64_t in_stride, uint32_t n,
+                                                 const StreamMeta *meta, const uint16_t *prevd_all, uint32_t C,
+                                                 uint32_t nch, const uint16_t *vis_all, const uint32_t *ssym_all,
+                                                 const uint16_t *spos_all, const OdChunk *chunks_all,
+                                                 uint32_t *syms_all, uint64_t maxb, uint64_t *blk_top_all,
+                                                 uint64_t *blk_start_all) {
+    const int j = blockIdx.y;
+    if (!meta[j].active) return;
+    const uint32_t k = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    const unsigned lane = threadIdx.x & 31;
+    if (k >= nch) return;
+    const OdChunk c = chunks_all[(uint64_t)j * nch + k];
+    if (!c.adopted) return;
+    uint32_t *syms = syms_all + (uint64_t)j * (n + 1);
+    uint64_t *btop = blk_top_all + (uint64_t)j * maxb, *bstart = blk_start_all + (uint64_t)j * maxb;
+    const uint32_t b0 = k * C;
+    const uint32_t *ssym = ssym_all + (uint64_t)j * n + b0;
+    const uint16_t *spos = spos_all + (uint64_t)j * n + b0;
+    for (uint32_t i = c.aidx + lane; i < c.nsym; i += 32) {
+        const uint64_t g = c.aoff + (i - c.aidx);
+        const uint64_t p = (uint64_t)b0 + spos[i];
+        syms[g] = ssym[i];
+        if (g % BLOCK_SYMS == 0) bstart[g / BLOCK_SYMS] = p - 1;
+        if (g % BLOCK_SYMS == BLOCK_SYMS - 1) btop[g / BLOCK_SYMS] = p;
+    }
+    if (lane == 0 && c.ncont) {
+        const uint8_t *inj = in + (uint64_t)j * in_stride;
+        const InWords words{inj};
+        const PrevD32 prev{prevd_all + (uint64_t)j * n};
+        uint32_t nxt, idx;
+        od_follow<true>(Walker{c.ex_p, c.ex_tag, c.ex_pl, c.ex_pd}, n, C, nch, words, prev, vis_all + (uint64_t)j * n,
+                        nxt, idx, syms, c.coff, btop, bstart);
+    }
+}
+
 // ------------------------------------------------------------ 8. block plans
 // zlib's tree construction (build_tree/gen_bitlen/gen_codes) is a sequential chain of
 // dependent shared-memory operations.  A one-warp CTA per block: the warp tallies the
@@ -1200,52 +1428,81 @@ void DeflateBatch::run(const uint8_t *in, uint64_t in_stride, int S, uint64_t n,
         k_prevlinks<<<dim3((unsigned)((nblk + span * PL_WARPS - 1) / (span * PL_WARPS)), S), PL_WARPS * 32, smem, st>>>(in, in_stride, n, w.meta, w.prevd, span);
         CKL();
         }
+        static const bool od_off = getenv("IPCG_DEFLATE_ALLPOS") != nullptr;  // dev: the all-position search
+        if (n < (1ull << 31) && !od_off) {
+            const uint32_t nch = (uint32_t)w.od_nch;
+            {
+            ProfScope ps2("deflate.walk", st, (uint64_t)S * n);
+            CK(cudaMemsetAsync(w.od_vis, 0, (size_t)S * n * sizeof(uint16_t), st));
+            k_od_walk<<<dim3((nch + 127) / 128, S), 128, 0, st>>>(in, in_stride, (uint32_t)n, w.meta, w.prevd, w.od_C,
+                                                                  nch, w.od_vis, w.od_ssym, w.od_spos, w.od_chunks);
+            CKL();
+            }
+            if (after_match) CK(cudaEventRecord(after_match, st));
+            {
+            ProfScope ps3("deflate.sync", st, (uint64_t)S * n);
+            k_od_sync<<<dim3((nch + 127) / 128, S), 128, 0, st>>>(in, in_stride, (uint32_t)n, w.meta, w.prevd, w.od_C,
+                                                                  nch, w.od_vis, w.od_chunks);
+            CKL();
+            k_od_chain<<<S, 32, 0, st>>>(in, in_stride, (uint32_t)n, w.meta, nch, w.od_chunks, w.syms, w.maxb,
+                                         w.blk_start);
+            CKL();
+            }
+            {
+            ProfScope ps3("deflate.place", st, (uint64_t)S * n);
+            k_od_place<<<dim3((nch + 3) / 4, S), 128, 0, st>>>(in, in_stride, (uint32_t)n, w.meta, w.prevd, w.od_C, nch,
+                                                               w.od_vis, w.od_ssym, w.od_spos, w.od_chunks, w.syms,
+                                                               w.maxb, w.blk_top, w.blk_start);
+            CKL();
+            }
+        } else {
         {
-        ProfScope ps2("deflate.match", st, (uint64_t)S * n);
-        if (n < (1ull << 31))
-            k_match<false><<<dim3(grid_for(n, 256, 4096), S), 256, 0, st>>>(in, in_stride, n, w.meta, w.prevd, w.rec);
-        else
-            k_match<true><<<dim3(grid_for(n, 256, 4096), S), 256, 0, st>>>(in, in_stride, n, w.meta, w.prevd, w.rec);
-        CKL();
-        }
-        if (after_match) CK(cudaEventRecord(after_match, st));
-        {
-        ProfScope ps3("deflate.anchor", st, (uint64_t)S * n);
-        k_anchor<<<dim3((unsigned)((n + TILE - 1) / TILE), S), 256, 0, st>>>(n, w.meta, w.rec, w.nchunks, w.first_anchor);
-        CKL();
-        const dim3 bg((unsigned)((w.nseg + 1 + 255) / 256), S);
-        k_bounds_seg<<<bg, 256, 0, st>>>(w.meta, w.nchunks, w.nseg, w.first_anchor, w.seg_symoff, w.seg_cnt4);
-        CKL();
-        k_bounds_scan<<<S, 32, 0, st>>>(n, w.meta, w.nchunks, w.nseg, w.seg_symoff, w.seg_cnt4);
-        CKL();
-        k_bounds_expand<<<bg, 256, 0, st>>>(n, w.meta, w.nchunks, w.nseg, w.first_anchor, w.seg_symoff, w.seg_cnt4,
-                                            w.bnd, w.nbreak);
-        CKL();
-        }
-        {
-        ProfScope ps3("deflate.sim", st, (uint64_t)S * n);
-        k_sim<<<dim3((unsigned)((w.nchunks + 255) / 256), S), 256, 0, st>>>(n, w.meta, w.rec, w.nchunks, w.bnd,
-                                                                              w.nbreak, w.exit4, w.cnt4);
-        CKL();
-        }
-        {
-        ProfScope ps3("deflate.resolve", st, (uint64_t)S * n);
-        const dim3 sg((unsigned)((w.nseg + 1 + 255) / 256), S);
-        k_seg_compose<<<sg, 256, 0, st>>>(w.meta, w.nchunks, w.nseg, w.exit4, w.cnt4, w.seg_exit4, w.seg_cnt4);
-        CKL();
-        k_resolve<<<S, 32, 0, st>>>(in, in_stride, n, w.meta, w.nseg, w.seg_exit4, w.seg_cnt4, w.seg_entry,
-                                    w.seg_symoff, w.syms, w.maxb, w.blk_start);
-        CKL();
-        k_seg_expand<<<sg, 256, 0, st>>>(w.meta, w.nchunks, w.nseg, w.exit4, w.cnt4, w.seg_entry, w.seg_symoff,
-                                         w.entry, w.symoff);
-        CKL();
-        }
-        {
-        ProfScope ps3("deflate.emit_syms", st, (uint64_t)S * n);
-        k_emit_syms<<<dim3((unsigned)((w.nchunks + 255) / 256), S), 256, 0, st>>>(in, in_stride, n, w.meta, w.rec, w.nchunks, w.bnd, w.nbreak, w.entry, w.symoff, w.syms, w.maxb, w.blk_top, w.blk_start, w.runs, w.nruns);
-        CKL();
-        k_emit_runs<<<148 * 4, 256, 0, st>>>(n, w.rec, w.syms, w.maxb, w.blk_top, w.blk_start, w.runs, w.nruns);
-        CKL();
+            ProfScope ps2("deflate.match", st, (uint64_t)S * n);
+            if (n < (1ull << 31))
+                k_match<false><<<dim3(grid_for(n, 256, 4096), S), 256, 0, st>>>(in, in_stride, n, w.meta, w.prevd, w.rec);
+            else
+                k_match<true><<<dim3(grid_for(n, 256, 4096), S), 256, 0, st>>>(in, in_stride, n, w.meta, w.prevd, w.rec);
+            CKL();
+            }
+            if (after_match) CK(cudaEventRecord(after_match, st));
+            {
+            ProfScope ps3("deflate.anchor", st, (uint64_t)S * n);
+            k_anchor<<<dim3((unsigned)((n + TILE - 1) / TILE), S), 256, 0, st>>>(n, w.meta, w.rec, w.nchunks, w.first_anchor);
+            CKL();
+            const dim3 bg((unsigned)((w.nseg + 1 + 255) / 256), S);
+            k_bounds_seg<<<bg, 256, 0, st>>>(w.meta, w.nchunks, w.nseg, w.first_anchor, w.seg_symoff, w.seg_cnt4);
+            CKL();
+            k_bounds_scan<<<S, 32, 0, st>>>(n, w.meta, w.nchunks, w.nseg, w.seg_symoff, w.seg_cnt4);
+            CKL();
+            k_bounds_expand<<<bg, 256, 0, st>>>(n, w.meta, w.nchunks, w.nseg, w.first_anchor, w.seg_symoff, w.seg_cnt4,
+                                                w.bnd, w.nbreak);
+            CKL();
+            }
+            {
+            ProfScope ps3("deflate.sim", st, (uint64_t)S * n);
+            k_sim<<<dim3((unsigned)((w.nchunks + 255) / 256), S), 256, 0, st>>>(n, w.meta, w.rec, w.nchunks, w.bnd,
+                                                                                  w.nbreak, w.exit4, w.cnt4);
+            CKL();
+            }
+            {
+            ProfScope ps3("deflate.resolve", st, (uint64_t)S * n);
+            const dim3 sg((unsigned)((w.nseg + 1 + 255) / 256), S);
+            k_seg_compose<<<sg, 256, 0, st>>>(w.meta, w.nchunks, w.nseg, w.exit4, w.cnt4, w.seg_exit4, w.seg_cnt4);
+            CKL();
+            k_resolve<<<S, 32, 0, st>>>(in, in_stride, n, w.meta, w.nseg, w.seg_exit4, w.seg_cnt4, w.seg_entry,
+                                        w.seg_symoff, w.syms, w.maxb, w.blk_start);
+            CKL();
+            k_seg_expand<<<sg, 256, 0, st>>>(w.meta, w.nchunks, w.nseg, w.exit4, w.cnt4, w.seg_entry, w.seg_symoff,
+                                             w.entry, w.symoff);
+            CKL();
+            }
+            {
+            ProfScope ps3("deflate.emit_syms", st, (uint64_t)S * n);
+            k_emit_syms<<<dim3((unsigned)((w.nchunks + 255) / 256), S), 256, 0, st>>>(in, in_stride, n, w.meta, w.rec, w.nchunks, w.bnd, w.nbreak, w.entry, w.symoff, w.syms, w.maxb, w.blk_top, w.blk_start, w.runs, w.nruns);
+            CKL();
+            k_emit_runs<<<148 * 4, 256, 0, st>>>(n, w.rec, w.syms, w.maxb, w.blk_top, w.blk_start, w.runs, w.nruns);
+            CKL();
+            }
         }
         {
         ProfScope ps4("deflate.blocks", st, (uint64_t)S * n);

@@ -213,7 +213,8 @@ struct Walk32 {
 };
 
 template <class Words, class Prev>
-HD bool walk32_start(uint32_t p, uint32_t n, const Words &w, const Prev &prevd, Walk32 &s, uint64_t &rec) {
+HD bool walk32_start(uint32_t p, uint32_t n, const Words &w, const Prev &prevd, Walk32 &s, uint64_t &rec,
+                     int max_chain = MAX_CHAIN) {
     rec = 0;
     if (p + MIN_MATCH > n) return true;
     const uint32_t d0 = prevd(p);
@@ -240,7 +241,7 @@ HD bool walk32_start(uint32_t p, uint32_t n, const Words &w, const Prev &prevd, 
                 uint32_t r = p - 1;
                 while (r >= floor_ + 1 && w.byte(r - 1) == v) --r;
                 i += (int)(p - 1 - r);
-                if (i >= MAX_CHAIN) {
+                if (i >= max_chain) {
                     rec = mrec_pack(best, bestd, best, bestd, flag);
                     return true;
                 }
@@ -250,7 +251,7 @@ HD bool walk32_start(uint32_t p, uint32_t n, const Words &w, const Prev &prevd, 
     }
     const uint32_t dq = prevd(from);
     // (from == limit is possible here: the head candidate may sit at exactly MAX_DIST)
-    if (dq == 0 || from - dq <= limit || i >= MAX_CHAIN) {
+    if (dq == 0 || from - dq <= limit || i >= max_chain) {
         rec = mrec_pack(best, bestd, best, bestd, flag);
         return true;
     }
@@ -265,7 +266,8 @@ HD bool walk32_start(uint32_t p, uint32_t n, const Words &w, const Prev &prevd, 
 // every chained candidate).  Candidates up to 32 and beyond run as two phases so the
 // chain-32 snapshot is taken once instead of every step.
 template <class Words, class Prev>
-HD bool walk32_run(uint32_t n, const Words &w, const Prev &prevd, Walk32 &s, int budget, uint64_t &rec) {
+HD bool walk32_run(uint32_t n, const Words &w, const Prev &prevd, Walk32 &s, int budget, uint64_t &rec,
+                   int max_chain = MAX_CHAIN) {
     const uint32_t p = s.p;
     const uint32_t maxlen = n - p < (uint32_t)MAX_MATCH ? n - p : (uint32_t)MAX_MATCH;
     const uint32_t nice = n - p < (uint32_t)NICE_LENGTH ? n - p : (uint32_t)NICE_LENGTH;
@@ -298,7 +300,7 @@ HD bool walk32_run(uint32_t n, const Words &w, const Prev &prevd, Walk32 &s, int
         if (dq - 1u >= q - lim1 || i >= stop) {
             if (stop == 32) {
                 l32 = best, d32 = bestd;
-                if (i == 32 && dq - 1u < q - lim1) {  // phase 2: candidates 33..MAX_CHAIN
+                if (max_chain > 32 && i == 32 && dq - 1u < q - lim1) {  // phase 2: candidates 33..MAX_CHAIN
                     stop = MAX_CHAIN;
                     q -= dq;
                     ++i;
@@ -408,6 +410,74 @@ HD bool sym_is_match(uint32_t s) { return (s & 0x80000000u) != 0; }
 HD uint32_t sym_lc(uint32_t s) { return (s >> 16) & 0xff; }     // len - 3
 HD uint32_t sym_dist1(uint32_t s) { return s & 0xffff; }        // dist - 1
 HD uint32_t sym_bytes(uint32_t s) { return sym_is_match(s) ? sym_lc(s) + 3 : 1; }
+
+// ------------------------------------------------------- on-demand lazy parse
+// The lazy parse (deflate_slow) needs longest_match only at the loop tops it visits, and only
+// with one chain limit: 128, or 32 once prev_length >= good_length (zlib's chain_length >>= 2).
+// A Walker runs the parse from any state, searching on demand; a state is (loop top p, tag) --
+// the pending match of a C tag is the search result at p-1 with that tag's chain, so two walkers
+// in the same (p, tag) continue identically.  The GPU runs one walker per chunk from (chunk
+// start, A) and joins each chunk's walk onto the previous one's where the latter reaches a state
+// the former visited (deflate.cu: k_od_walk / k_od_sync / k_od_chain / k_od_place).
+struct Match {
+    uint32_t len, dist, flag;
+};
+
+template <class Words, class Prev>
+HD Match match_on_demand(uint32_t p, uint32_t n, const Words &w, const Prev &prevd, int chain) {
+    Walk32 s;
+    uint64_t rec;
+    if (!walk32_start(p, n, w, prevd, s, rec, chain)) walk32_run(n, w, prevd, s, 1 << 30, rec, chain);
+    return chain == 32 ? Match{mrec_l32(rec), mrec_d32(rec), mrec_flag(rec)}
+                       : Match{mrec_l128(rec), mrec_d128(rec), mrec_flag(rec)};
+}
+
+constexpr uint32_t NOSYM = 0xFFFFFFFFu;
+
+struct Walker {
+    uint32_t p, tag, pl, pd;  // loop top, tag, pending match (tags C128 / C32)
+};
+
+// one iteration of deflate_slow's loop from state s (the decisions of parse_step, the match at
+// p searched here); returns the symbol it emits or NOSYM
+template <class Words, class Prev>
+HD uint32_t walker_step(Walker &s, uint32_t n, const Words &w, const Prev &prevd) {
+    const uint32_t p = s.p;
+    const bool pending = s.tag == TAG_C128 || s.tag == TAG_C32;
+    const uint32_t pl = pending ? s.pl : 2u;
+    uint32_t ml = 2, md = 0;
+    uint32_t ktag = TAG_C128;
+    if (p + MIN_MATCH <= n && pl < (uint32_t)MAX_LAZY) {
+        const int chain = pl >= (uint32_t)GOOD_LENGTH ? 32 : MAX_CHAIN;
+        const Match m = match_on_demand(p, n, w, prevd, chain);
+        if (m.len != 0 && !(m.flag && tail_slide_nil((int64_t)p, (int64_t)n))) {
+            ktag = chain == 32 ? TAG_C32 : TAG_C128;
+            if (m.len > pl) {
+                ml = m.len, md = m.dist;
+                if (ml == (uint32_t)MIN_MATCH && md > (uint32_t)TOO_FAR) ml = 2;
+            } else {
+                ml = pl;
+            }
+        }
+    }
+    if (pl >= (uint32_t)MIN_MATCH && ml <= pl) {
+        const uint32_t sym = sym_match(pl, s.pd);
+        s.p = p - 1 + pl;
+        s.tag = TAG_A;
+        return sym;
+    }
+    const uint32_t sym = s.tag != TAG_A ? sym_literal(w.byte(p - 1)) : NOSYM;
+    s.p = p + 1;
+    s.tag = ml >= (uint32_t)MIN_MATCH ? ktag : (uint32_t)TAG_B;
+    s.pl = ml, s.pd = md;
+    return sym;
+}
+
+// visit word of a chunk walk at position p: bit 15 visited, bits 13-14 tag, bits 0-12 the number
+// of symbols the walk emitted before that state (chunks of at most 8192 positions)
+HD uint16_t vis_pack(uint32_t tag, uint32_t symidx) { return (uint16_t)(0x8000u | (tag << 13) | symidx); }
+HD bool vis_match(uint16_t v, uint32_t tag) { return (v >> 13) == (0x4u | tag); }
+HD uint32_t vis_symidx(uint16_t v) { return v & 0x1fffu; }
 
 // ------------------------------------------------------------ static tables
 HD int ilog2(uint32_t v) {

@@ -11,6 +11,7 @@
 // atomicMax on the IEEE bits of a non-negative double (exact, order-free).
 #include <algorithm>
 #include <cstdio>
+#include <cstdlib>
 #include <type_traits>
 
 #include "numerics.cuh"
@@ -160,10 +161,279 @@ __global__ void __launch_bounds__(LT_THREADS) k_loss_fused(const uint32_t *__res
 }
 
 
+// ---------------------------------------------------------------------------------------
+// k_loss_lines: the same replay for levels of 1-3 dimensions (leading axes padded with extent
+// 1), with every deviation value in registers.  On a level's lattice (coordinates in units of
+// the level stride) the passes are: over x (x odd, y, z even), over y (y odd, z even), over z
+// (z odd).  Their sources are always points of coarser levels or of EARLIER passes, so:
+//   pass-x value  v0 = 0 + own                      (its sources are coarser: deviation 0)
+//   pass-y value  v1 = pred_y(v0 at y+-1, y+-3) + own  (v0 = 0 at even x)
+//   pass-z value  v2 = pred_z(E at z+-1, z+-3) + own   (E = v1 / v0 / 0 at even z)
+// i.e. every value is a 2-deep stencil of codewords.  A warp owns one x, a segment of z and a
+// range of y rows: lane l holds the even-z indices S+2l, S+2l+1 (E values) and the odd-z
+// targets of the same indices; pass-z sources of the neighbours come by shuffle, pass-y sources
+// from a 4-row register window of v0 walked down the y rows.  Dropped-digit counts go two at a
+// time; the codewords of a task are re-read per pair (L2-resident).  No shared memory, no
+// barriers.  Owned indices per segment: [S+1, S+62) (61 of the 64 held), S = 61k - 1.
+struct LossLines {
+    int Mx, My, Mz;                  // lattice extents
+    uint32_t cey, coy, cez, coz;     // even / odd lattice counts along y, z
+    uint32_t cox;                    // odd count along x
+    uint64_t b0, b1, b2;             // ordinal bases of the passes over x, y, z
+    uint32_t nseg, rows_per_task, nyr;
+    uint64_t ntasks;
+};
+
+constexpr int LL_WARPS = 8;
+
+// (double)v for |v| < 2^51 by the 2^52 + 2^51 bias: an integer add and one DADD on the FP64 pipe
+// instead of an I2F.F64 on the conversion unit (same value: both are exact)
+__device__ __forceinline__ double i2d_exact(int64_t v) {
+    return __longlong_as_double(v + 0x4338000000000000ll) - 6755399441055744.0;
+}
+// own = unit * (double)(from_negabinary(w & ~m) - from_negabinary(w)) (pipeline.hpp:104-106)
+__device__ __forceinline__ double own_dev(uint32_t w, uint32_t m, double unit) {
+    return unit * i2d_exact((int64_t)from_nb(w & ~m) - (int64_t)from_nb(w));
+}
+
+template <bool Cubic>
+__device__ __forceinline__ double pred4(double a, double b, double c, double d, int cls) {
+    // predict_cubic / predict_linear / copy (predictor.hpp:16-38); x/16 and x/2 are exact scalings
+    return cls == 0 ? (9.0 * (b + c) - (a + d)) * 0.0625 : cls == 1 ? (b + c) * 0.5 : b;
+}
+
+__device__ __forceinline__ int edge_class(bool cubic, int c, int M) {
+    return (cubic && c >= 3 && c + 3 < M) ? 0 : (c + 1 < M) ? 1 : 2;
+}
+
+__device__ __forceinline__ void fold_max(double v, double &m) { m = (m < v) ? v : m; }
+
+// u64 max of a non-negative double across the warp (bit patterns order like the values)
+__device__ __forceinline__ unsigned long long warp_max_bits(double v) {
+    const unsigned long long b = (unsigned long long)__double_as_longlong(v);
+    const unsigned hi = (unsigned)(b >> 32), lo = (unsigned)b;
+    const unsigned mh = __reduce_max_sync(0xffffffffu, hi);
+    const unsigned ml = __reduce_max_sync(0xffffffffu, hi == mh ? lo : 0u);
+    return ((unsigned long long)mh << 32) | ml;
+}
+
+// one task of k_loss_lines for one pair of dropped-digit counts (masks ma, mb); XODD: the
+// task's x is odd (pass-x points exist in it), ZCUBIC: every target of the warp has the
+// interior (cubic) class along z.  Returns the lane's running maxima in mxa / mxb.
+struct LaneCtx {
+    const uint32_t *r0, *r1, *r2;  // this x's rows of the pass-x / pass-y / pass-z boxes, + e0
+    int e0;                        // first E index held by the lane
+    bool eok0, eok1, own0, own1, tok0, tok1;
+    int zc0, zc1;                  // z edge classes of the lane's two targets
+};
+
+template <bool Cubic, bool ZCUBIC>
+__device__ __forceinline__ void pass_z(const LaneCtx &L, double E0, double E1, uint32_t c20, uint32_t c21, uint32_t m,
+                                       double unit, double &mx) {
+    // target e reads E at e-1, e, e+1, e+2 (lane-1's second, own two, lane+1's two)
+    const double left = __shfl_up_sync(0xffffffffu, E1, 1);
+    const double r0 = __shfl_down_sync(0xffffffffu, E0, 1);
+    const double r1 = __shfl_down_sync(0xffffffffu, E1, 1);
+    double p0, p1;
+    if (ZCUBIC) {
+        p0 = (9.0 * (E0 + E1) - (left + r0)) * 0.0625;
+        p1 = (9.0 * (E1 + r0) - (E0 + r1)) * 0.0625;
+    } else {
+        p0 = pred4<Cubic>(left, E0, E1, r0, L.zc0);
+        p1 = pred4<Cubic>(E0, E1, r0, r1, L.zc1);
+    }
+    const double va = p0 + own_dev(c20, m, unit), vb = p1 + own_dev(c21, m, unit);
+    if (L.tok0) fold_max(fabs(va), mx);
+    if (L.tok1) fold_max(fabs(vb), mx);
+}
+
+template <bool Cubic, bool XODD, bool ZCUBIC>
+__device__ void loss_task(const LaneCtx &L, const LossLines &g, uint32_t p0, uint32_t p1, uint32_t ma, uint32_t mb,
+                          bool two, double unit, double &mxa, double &mxb) {
+    const uint32_t cez = g.cez, coz = g.coz;
+    // v0 window over even rows q-1 .. q+2 of pair q: [row][z][d]
+    double w[4][2][2];
+    auto v0 = [&](int q, double (&o)[2][2]) {
+        uint32_t c[2] = {0u, 0u};
+        const bool rq = XODD && q >= 0 && (uint32_t)q < g.cey;
+        if (rq && L.eok0) c[0] = __ldg(L.r0 + (uint64_t)q * cez);
+        if (rq && L.eok1) c[1] = __ldg(L.r0 + (uint64_t)q * cez + 1);
+#pragma unroll
+        for (int k = 0; k < 2; ++k) {
+            const bool ok = rq && (k ? L.eok1 : L.eok0);
+            o[k][0] = ok ? own_dev(c[k], ma, unit) : 0.0;
+            o[k][1] = ok ? own_dev(c[k], mb, unit) : 0.0;
+        }
+    };
+    if (XODD) {
+        v0((int)p0 - 1, w[0]);
+        v0((int)p0, w[1]);
+        v0((int)p0 + 1, w[2]);
+    }
+    for (uint32_t p = p0; p < p1; ++p) {
+        const int yo = 2 * (int)p + 1;
+        const bool has_odd = yo < g.My;
+        uint32_t c1[2] = {0u, 0u}, c2e[2] = {0u, 0u}, c2o[2] = {0u, 0u};
+        const uint32_t *q1 = L.r1 + (uint64_t)p * cez, *q2 = L.r2 + (uint64_t)(2 * p) * coz;
+        if (has_odd && L.eok0) c1[0] = __ldg(q1);
+        if (has_odd && L.eok1) c1[1] = __ldg(q1 + 1);
+        if (L.tok0) c2e[0] = __ldg(q2);
+        if (L.tok1) c2e[1] = __ldg(q2 + 1);
+        if (has_odd && L.tok0) c2o[0] = __ldg(q2 + coz);
+        if (has_odd && L.tok1) c2o[1] = __ldg(q2 + coz + 1);
+        if (XODD) v0((int)p + 2, w[3]);
+        // row y = 2p: E = v0 (pass-x points at odd x, coarser points at even x)
+#pragma unroll
+        for (int t = 0; t < 2; ++t) {
+            if (!two && t) break;
+            double &mx = t ? mxb : mxa;
+            const uint32_t m = t ? mb : ma;
+            const double E0 = XODD ? w[1][0][t] : 0.0, E1 = XODD ? w[1][1][t] : 0.0;
+            if (XODD) {
+                if (L.eok0 && L.own0) fold_max(fabs(E0), mx);
+                if (L.eok1 && L.own1) fold_max(fabs(E1), mx);
+            }
+            pass_z<Cubic, ZCUBIC>(L, E0, E1, c2e[0], c2e[1], m, unit, mx);
+        }
+        // row y = 2p + 1: E = v1 = pred_y(v0 window) + own (at even x the window is all zero:
+        // pred = +0 exactly, and +0 + own == own)
+        if (has_odd) {
+            const int ycls = edge_class(Cubic, yo, g.My);
+#pragma unroll
+            for (int t = 0; t < 2; ++t) {
+                if (!two && t) break;
+                double &mx = t ? mxb : mxa;
+                const uint32_t m = t ? mb : ma;
+                double E0 = own_dev(c1[0], m, unit), E1 = own_dev(c1[1], m, unit);
+                if (XODD) {
+                    double p0v, p1v;
+                    if (ycls == 0) {
+                        p0v = (9.0 * (w[1][0][t] + w[2][0][t]) - (w[0][0][t] + w[3][0][t])) * 0.0625;
+                        p1v = (9.0 * (w[1][1][t] + w[2][1][t]) - (w[0][1][t] + w[3][1][t])) * 0.0625;
+                    } else {
+                        p0v = pred4<Cubic>(w[0][0][t], w[1][0][t], w[2][0][t], w[3][0][t], ycls);
+                        p1v = pred4<Cubic>(w[0][1][t], w[1][1][t], w[2][1][t], w[3][1][t], ycls);
+                    }
+                    E0 = p0v + E0;
+                    E1 = p1v + E1;
+                }
+                if (L.eok0 && L.own0) fold_max(fabs(E0), mx);
+                if (L.eok1 && L.own1) fold_max(fabs(E1), mx);
+                pass_z<Cubic, ZCUBIC>(L, E0, E1, c2o[0], c2o[1], m, unit, mx);
+            }
+        }
+        if (XODD) {
+#pragma unroll
+            for (int k = 0; k < 2; ++k)
+#pragma unroll
+                for (int t = 0; t < 2; ++t) w[0][k][t] = w[1][k][t], w[1][k][t] = w[2][k][t], w[2][k][t] = w[3][k][t];
+        }
+    }
+}
+
+template <bool Cubic>
+__global__ void __launch_bounds__(LL_WARPS * 32, 3) k_loss_lines(const uint32_t *__restrict__ nb, LossLines g,
+                                                              double unit, const uint32_t *lowor,
+                                                              unsigned long long *raw) {
+    const uint32_t lo = *lowor;
+    if (lo == 0) return;
+    const int d0 = __ffs((int)lo), hb = 31 - __clz(lo), dmax = hb + 1 < 32 ? hb + 1 : 32;
+    const unsigned lane = threadIdx.x & 31;
+    for (uint64_t task = (uint64_t)blockIdx.x * LL_WARPS + (threadIdx.x >> 5); task < g.ntasks;
+         task += (uint64_t)gridDim.x * LL_WARPS) {
+        const uint32_t yr = (uint32_t)(task % g.nyr);
+        const uint32_t seg = (uint32_t)((task / g.nyr) % g.nseg);
+        const int x = (int)(task / ((uint64_t)g.nyr * g.nseg));
+        const uint32_t p0 = yr * g.rows_per_task, p1 = min(p0 + g.rows_per_task, g.cey);  // row pairs
+        const int S = (int)seg * 61 - 1;
+        LaneCtx L;
+        L.e0 = S + 2 * (int)lane;
+        const int e1 = L.e0 + 1;
+        L.eok0 = L.e0 >= 0 && (uint32_t)L.e0 < g.cez;
+        L.eok1 = (uint32_t)e1 < g.cez;
+        L.own0 = L.e0 >= S + 1 && L.e0 < S + 62;
+        L.own1 = e1 < S + 62;
+        L.tok0 = L.own0 && L.e0 >= 0 && (uint32_t)L.e0 < g.coz;
+        L.tok1 = L.own1 && (uint32_t)e1 < g.coz;
+        L.zc0 = edge_class(Cubic, 2 * L.e0 + 1, g.Mz);
+        L.zc1 = edge_class(Cubic, 2 * e1 + 1, g.Mz);
+        const int eb = L.e0 < 0 ? 0 : L.e0;  // row pointers are only dereferenced where e0 >= 0
+        L.r0 = nb + g.b0 + (uint64_t)(x >> 1) * g.cey * g.cez + eb;
+        L.r1 = nb + g.b1 + (uint64_t)x * g.coy * g.cez + eb;
+        L.r2 = nb + g.b2 + (uint64_t)x * g.My * g.coz + eb;
+        if (L.e0 < 0) {  // (lane 0 of the first segment: its e0 = -1 holds nothing, e1 = 0 sits at +0)
+            L.r0 -= 1, L.r1 -= 1, L.r2 -= 1;
+        }
+        const bool zcubic = __all_sync(0xffffffffu, !(L.tok0 || L.tok1) || ((!L.tok0 || L.zc0 == 0) && (!L.tok1 || L.zc1 == 0)));
+        const bool xodd = x & 1;
+        for (int da = d0; da <= dmax; da += 2) {
+            const int db = da + 1 <= dmax ? da + 1 : da;
+            const uint32_t ma = da == 32 ? 0xFFFFFFFFu : ((1u << da) - 1u);
+            const uint32_t mb = db == 32 ? 0xFFFFFFFFu : ((1u << db) - 1u);
+            const bool two = db != da;
+            double mxa = 0.0, mxb = 0.0;
+            if (xodd) {
+                if (zcubic) loss_task<Cubic, true, true>(L, g, p0, p1, ma, mb, two, unit, mxa, mxb);
+                else loss_task<Cubic, true, false>(L, g, p0, p1, ma, mb, two, unit, mxa, mxb);
+            } else {
+                if (zcubic) loss_task<Cubic, false, true>(L, g, p0, p1, ma, mb, two, unit, mxa, mxb);
+                else loss_task<Cubic, false, false>(L, g, p0, p1, ma, mb, two, unit, mxa, mxb);
+            }
+            const unsigned long long ba = warp_max_bits(mxa), bb = warp_max_bits(mxb);
+            if (lane == 0) {
+                if (ba) atomicMax(&raw[da], ba);
+                if (bb && two) atomicMax(&raw[db], bb);
+            }
+        }
+    }
+}
+
+// the level as a padded 3-D lattice, or false (4-D grids, the coarsest level)
+bool loss_lines_geom(const Geometry &G, int level, LossLines &g) {
+    if (level == G.levels || G.nd > 3) return false;
+    const LevelGeom &lg = G.level[level - 1];
+    const uint64_t s = uint64_t(1) << (level - 1);
+    int M[3] = {1, 1, 1};
+    for (int i = 0; i < G.nd; ++i) {
+        const uint64_t m = (G.dims[i] + s - 1) / s;
+        if (m > (1u << 30)) return false;
+        M[3 - G.nd + i] = (int)m;
+    }
+    g = LossLines{};
+    g.Mx = M[0], g.My = M[1], g.Mz = M[2];
+    g.cox = (uint32_t)(M[0] / 2);
+    g.cey = (uint32_t)((M[1] + 1) / 2), g.coy = (uint32_t)(M[1] / 2);
+    g.cez = (uint32_t)((M[2] + 1) / 2), g.coz = (uint32_t)(M[2] / 2);
+    for (const PassDesc &pd : lg.passes) {
+        const int a = pd.axis + (3 - G.nd);
+        if (a == 0) g.b0 = pd.ordinal_base;
+        else if (a == 1) g.b1 = pd.ordinal_base;
+        else if (a == 2) g.b2 = pd.ordinal_base;
+    }
+    g.nseg = (std::max(g.cez, g.coz) + 60) / 61;
+    // rows per task: enough tasks to fill the GPU a few times over, at least 16 row pairs each
+    const uint64_t lines = (uint64_t)g.Mx * g.nseg;
+    const uint64_t want = (uint64_t)num_sms() * 64 * 4;
+    uint32_t nyr = (uint32_t)std::max<uint64_t>(1, std::min<uint64_t>((want + lines - 1) / lines, (g.cey + 15) / 16));
+    g.rows_per_task = (g.cey + nyr - 1) / nyr;
+    g.nyr = (g.cey + g.rows_per_task - 1) / g.rows_per_task;
+    g.ntasks = lines * g.nyr;
+    return true;
+}
+
 }  // namespace
 
 bool launch_loss_fused(const uint32_t *nb, const Geometry &G, int level, bool cubic, double unit,
                        const uint32_t *lowor, unsigned long long *raw, cudaStream_t st) {
+    static const bool lines_off = getenv("IPCG_LOSS_TILES") != nullptr;  // dev: the smem-tile kernel
+    LossLines ll;
+    if (!lines_off && loss_lines_geom(G, level, ll)) {
+        const unsigned grid = (unsigned)std::min<uint64_t>((ll.ntasks + LL_WARPS - 1) / LL_WARPS, (uint64_t)num_sms() * 16);
+        if (cubic) k_loss_lines<true><<<grid, LL_WARPS * 32, 0, st>>>(nb, ll, unit, lowor, raw);
+        else k_loss_lines<false><<<grid, LL_WARPS * 32, 0, st>>>(nb, ll, unit, lowor, raw);
+        CKL();
+        return true;
+    }
     static const int tiles[5][4] = {{0, 0, 0, 0}, {2048, 1, 1, 1}, {32, 64, 1, 1}, {4, 16, 32, 1}, {1, 4, 8, 16}};
     TileGeom g;
     uint64_t ntiles, region;

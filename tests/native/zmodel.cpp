@@ -46,100 +46,12 @@ struct Stats {
 
 }  // namespace
 
-extern "C" int zmodel_compress(const uint8_t *in, uint64_t n, int chunk, uint8_t *out, uint64_t cap,
-                               uint64_t *out_len, uint64_t *stats) {
-    struct HostBytes {
-        const uint8_t *in;
-        uint32_t operator()(int64_t i) const { return in[i]; }
-        int64_t match_len(int64_t a, int64_t b, int64_t maxlen) const {
-            int64_t len = 0;
-            while (len < maxlen && in[a + len] == in[b + len]) ++len;
-            return len;
-        }
-    } bytes{in};
-    // 1. hash-chain links
-    std::vector<uint16_t> prevd(n + 1, 0);
-    {
-        std::vector<int64_t> head(1 << 15, -1);
-        for (int64_t p = 0; p + MIN_MATCH <= (int64_t)n; ++p) {
-            const uint32_t h = hash3(in[p], in[p + 1], in[p + 2]);
-            const int64_t q = head[h];
-            prevd[p] = (q >= 0 && p - q < WSIZE) ? (uint16_t)(p - q) : 0;
-            head[h] = p;
-        }
-    }
-    auto prevfn = [&](int64_t i) -> uint32_t { return prevd[i]; };
-    // 2. match records (the GPU's fast form; zmodel_match_check pins it to match_search)
-    std::vector<uint64_t> rec(n + 1, 0);
-    const HostWords words{in, n};
-    for (int64_t p = 0; p < (int64_t)n; ++p) rec[p] = match_search32((uint32_t)p, (uint32_t)n, words, prevfn);
-    // 3. anchors: no match found at q < p can reach past p
-    std::vector<uint8_t> anchor(n + 1, 0);
-    {
-        int64_t reach = 0;
-        for (int64_t p = 0; p <= (int64_t)n; ++p) {
-            anchor[p] = reach <= p;
-            if (p < (int64_t)n) {
-                const int64_t r = p + (int64_t)(mrec_l128(rec[p]) ? mrec_l128(rec[p]) : 1);
-                if (r > reach) reach = r;
-            }
-        }
-    }
-    const int64_t CH = chunk > 0 ? chunk : 4096;
-    const int64_t nchunks = ((int64_t)n + CH - 1) / CH;
-    std::vector<int64_t> bnd(nchunks + 1);
-    bnd[nchunks] = (int64_t)n;
-    for (int64_t k = nchunks - 1; k >= 0; --k) {  // first anchor >= k*CH (suffix-min)
-        int64_t b = bnd[k + 1];
-        for (int64_t p = k * CH; p < (k + 1) * CH && p < (int64_t)n; ++p)
-            if (anchor[p]) {
-                b = p;
-                break;
-            }
-        bnd[k] = b;
-    }
-    bnd[0] = 0;
-    // 4. per chunk, the exit tag for each entry tag
-    auto run_chunk = [&](int64_t b0, int64_t b1, int tag, std::vector<uint32_t> *syms, int64_t *loop_tops) {
-        int64_t p = b0;
-        uint64_t count = 0;
-        while (p < b1) {
-            const Step s = parse_step(p, tag, (int64_t)n, rec[p], p > 0 ? rec[p - 1] : 0, bytes);
-            if (s.emit) {
-                const uint32_t sym = s.emit == 2 ? sym_match(s.len, s.dist) : sym_literal(s.len);
-                if (syms) syms->push_back(sym);
-                if (loop_tops) loop_tops[syms->size() - 1] = p;
-                ++count;
-            }
-            p = s.next_p;
-            tag = s.next_tag;
-        }
-        if (p != b1) return -1;  // anchors guarantee exact exit
-        return tag;
-    };
-    std::vector<uint8_t> exits(nchunks * 4, 0);
-    for (int64_t k = 0; k < nchunks; ++k) {
-        if (bnd[k] >= bnd[k + 1]) {
-            for (int t = 0; t < 4; ++t) exits[k * 4 + t] = (uint8_t)t;  // empty chunk: identity
-            continue;
-        }
-        for (int t = 0; t < 4; ++t) {
-            const int e = run_chunk(bnd[k], bnd[k + 1], t, nullptr, nullptr);
-            if (e < 0) return -10;
-            exits[k * 4 + t] = (uint8_t)e;
-        }
-    }
-    // 5. resolve entry tags (a scan of 4->4 maps)
-    std::vector<int> entry(nchunks + 1);
-    entry[0] = TAG_A;
-    for (int64_t k = 0; k < nchunks; ++k) entry[k + 1] = exits[k * 4 + entry[k]];
-    // 6. emit symbols from the true entries; remember each symbol's loop top
-    std::vector<uint32_t> syms;
-    std::vector<int64_t> tops(n + 2);
-    for (int64_t k = 0; k < nchunks; ++k)
-        if (bnd[k] < bnd[k + 1]) run_chunk(bnd[k], bnd[k + 1], entry[k], &syms, tops.data());
+// blocks of 16383 symbols, Huffman plans, bits, Adler-32 (shared by both parse models)
+static int emit_stream(const uint8_t *in, uint64_t n, std::vector<uint32_t> &syms, std::vector<int64_t> &tops,
+                       int final_tag, int64_t nchunks, uint8_t *out, uint64_t cap, uint64_t *out_len,
+                       uint64_t *stats) {
     const uint64_t S_loop = syms.size();
-    const bool final_lit = entry[nchunks] != TAG_A && n > 0;
+    const bool final_lit = final_tag != TAG_A && n > 0;
     if (final_lit) {
         syms.push_back(sym_literal(in[n - 1]));
         tops[syms.size() - 1] = (int64_t)n;
@@ -246,6 +158,101 @@ extern "C" int zmodel_compress(const uint8_t *in, uint64_t n, int chunk, uint8_t
     return 0;
 }
 
+extern "C" int zmodel_compress(const uint8_t *in, uint64_t n, int chunk, uint8_t *out, uint64_t cap,
+                               uint64_t *out_len, uint64_t *stats) {
+    struct HostBytes {
+        const uint8_t *in;
+        uint32_t operator()(int64_t i) const { return in[i]; }
+        int64_t match_len(int64_t a, int64_t b, int64_t maxlen) const {
+            int64_t len = 0;
+            while (len < maxlen && in[a + len] == in[b + len]) ++len;
+            return len;
+        }
+    } bytes{in};
+    // 1. hash-chain links
+    std::vector<uint16_t> prevd(n + 1, 0);
+    {
+        std::vector<int64_t> head(1 << 15, -1);
+        for (int64_t p = 0; p + MIN_MATCH <= (int64_t)n; ++p) {
+            const uint32_t h = hash3(in[p], in[p + 1], in[p + 2]);
+            const int64_t q = head[h];
+            prevd[p] = (q >= 0 && p - q < WSIZE) ? (uint16_t)(p - q) : 0;
+            head[h] = p;
+        }
+    }
+    auto prevfn = [&](int64_t i) -> uint32_t { return prevd[i]; };
+    // 2. match records (the GPU's fast form; zmodel_match_check pins it to match_search)
+    std::vector<uint64_t> rec(n + 1, 0);
+    const HostWords words{in, n};
+    for (int64_t p = 0; p < (int64_t)n; ++p) rec[p] = match_search32((uint32_t)p, (uint32_t)n, words, prevfn);
+    // 3. anchors: no match found at q < p can reach past p
+    std::vector<uint8_t> anchor(n + 1, 0);
+    {
+        int64_t reach = 0;
+        for (int64_t p = 0; p <= (int64_t)n; ++p) {
+            anchor[p] = reach <= p;
+            if (p < (int64_t)n) {
+                const int64_t r = p + (int64_t)(mrec_l128(rec[p]) ? mrec_l128(rec[p]) : 1);
+                if (r > reach) reach = r;
+            }
+        }
+    }
+    const int64_t CH = chunk > 0 ? chunk : 4096;
+    const int64_t nchunks = ((int64_t)n + CH - 1) / CH;
+    std::vector<int64_t> bnd(nchunks + 1);
+    bnd[nchunks] = (int64_t)n;
+    for (int64_t k = nchunks - 1; k >= 0; --k) {  // first anchor >= k*CH (suffix-min)
+        int64_t b = bnd[k + 1];
+        for (int64_t p = k * CH; p < (k + 1) * CH && p < (int64_t)n; ++p)
+            if (anchor[p]) {
+                b = p;
+                break;
+            }
+        bnd[k] = b;
+    }
+    bnd[0] = 0;
+    // 4. per chunk, the exit tag for each entry tag
+    auto run_chunk = [&](int64_t b0, int64_t b1, int tag, std::vector<uint32_t> *syms, int64_t *loop_tops) {
+        int64_t p = b0;
+        uint64_t count = 0;
+        while (p < b1) {
+            const Step s = parse_step(p, tag, (int64_t)n, rec[p], p > 0 ? rec[p - 1] : 0, bytes);
+            if (s.emit) {
+                const uint32_t sym = s.emit == 2 ? sym_match(s.len, s.dist) : sym_literal(s.len);
+                if (syms) syms->push_back(sym);
+                if (loop_tops) loop_tops[syms->size() - 1] = p;
+                ++count;
+            }
+            p = s.next_p;
+            tag = s.next_tag;
+        }
+        if (p != b1) return -1;  // anchors guarantee exact exit
+        return tag;
+    };
+    std::vector<uint8_t> exits(nchunks * 4, 0);
+    for (int64_t k = 0; k < nchunks; ++k) {
+        if (bnd[k] >= bnd[k + 1]) {
+            for (int t = 0; t < 4; ++t) exits[k * 4 + t] = (uint8_t)t;  // empty chunk: identity
+            continue;
+        }
+        for (int t = 0; t < 4; ++t) {
+            const int e = run_chunk(bnd[k], bnd[k + 1], t, nullptr, nullptr);
+            if (e < 0) return -10;
+            exits[k * 4 + t] = (uint8_t)e;
+        }
+    }
+    // 5. resolve entry tags (a scan of 4->4 maps)
+    std::vector<int> entry(nchunks + 1);
+    entry[0] = TAG_A;
+    for (int64_t k = 0; k < nchunks; ++k) entry[k + 1] = exits[k * 4 + entry[k]];
+    // 6. emit symbols from the true entries; remember each symbol's loop top
+    std::vector<uint32_t> syms;
+    std::vector<int64_t> tops(n + 2);
+    for (int64_t k = 0; k < nchunks; ++k)
+        if (bnd[k] < bnd[k + 1]) run_chunk(bnd[k], bnd[k + 1], entry[k], &syms, tops.data());
+    return emit_stream(in, n, syms, tops, entry[nchunks], nchunks, out, cap, out_len, stats);
+}
+
 extern "C" uint32_t zmodel_crc_combine(uint32_t crc1, uint32_t crc2, uint64_t len2) { return crc_combine(crc1, crc2, len2); }
 
 // match_search32 (the GPU's form) against the reference-shaped match_search at every
@@ -334,4 +341,104 @@ extern "C" void zmodel_parse_visits(const uint8_t *in, uint64_t n, uint64_t *out
     out3[0] = visits;
     out3[1] = vsteps;
     out3[2] = allsteps;
+}
+
+// The on-demand chunked parse, run sequentially exactly as the GPU's k_od_* kernels run it in
+// parallel: (1) one walker per chunk from (chunk start, A), recording each visited state and
+// the symbols it emits; (2) from each chunk walk's exit state, a continuation walk until it
+// reaches a state the walk of the chunk it is in visited (sync); (3) from chunk 0, follow the
+// syncs: the true parse is chunk 0's walk, its continuation, the synced chunk's walk from the
+// sync state, ...; (4) place the adopted symbols (re-walking the continuations).
+extern "C" int zmodel_compress_od(const uint8_t *in, uint64_t n, int chunk, uint8_t *out, uint64_t cap,
+                                  uint64_t *out_len, uint64_t *stats) {
+    std::vector<uint16_t> prevd(n + 1, 0);
+    {
+        std::vector<int64_t> head(1 << 15, -1);
+        for (int64_t p = 0; p + MIN_MATCH <= (int64_t)n; ++p) {
+            const uint32_t h = hash3(in[p], in[p + 1], in[p + 2]);
+            const int64_t q = head[h];
+            prevd[p] = (q >= 0 && p - q < WSIZE) ? (uint16_t)(p - q) : 0;
+            head[h] = p;
+        }
+    }
+    auto prevfn = [&](uint32_t i) -> uint32_t { return prevd[i]; };
+    const HostWords words{in, n};
+    const uint64_t C = chunk > 0 ? (uint64_t)chunk : 1024;
+    if (C > 8192) return -20;
+    const uint64_t nch = (n + C - 1) / C;
+    auto b = [&](uint64_t k) { return std::min<uint64_t>(k * C, n); };
+    // 1. chunk walks
+    std::vector<uint16_t> vis(n + 1, 0), spos(n + 1, 0);
+    std::vector<uint32_t> ssym(n + 1, 0), nsym(nch, 0);
+    std::vector<Walker> ex(nch);
+    for (uint64_t k = 0; k < nch; ++k) {
+        Walker w{(uint32_t)b(k), TAG_A, 0, 0};
+        uint32_t cnt = 0;
+        while (w.p < b(k + 1)) {
+            const uint32_t p = w.p;
+            vis[p] = vis_pack(w.tag, cnt);
+            const uint32_t sym = walker_step(w, (uint32_t)n, words, prevfn);
+            if (sym != NOSYM) {
+                ssym[b(k) + cnt] = sym;
+                spos[b(k) + cnt] = (uint16_t)(p - b(k));
+                ++cnt;
+            }
+        }
+        nsym[k] = cnt;
+        ex[k] = w;
+    }
+    // 2. continuations until they meet a visited state
+    std::vector<uint64_t> nxt(nch), nidx(nch, 0), ncont(nch, 0);
+    std::vector<int> fin(nch, TAG_A);
+    auto follow = [&](Walker w, uint64_t &c, uint32_t &idx, std::vector<uint32_t> *syms, std::vector<int64_t> *tops) {
+        uint64_t cnt = 0;
+        for (;;) {
+            if (w.p >= n) {
+                c = nch;
+                idx = w.tag;  // the final tag
+                return cnt;
+            }
+            c = w.p / C;
+            const uint16_t v = vis[w.p];
+            if (vis_match(v, w.tag)) {
+                idx = vis_symidx(v);
+                return cnt;
+            }
+            const uint32_t p = w.p;
+            const uint32_t sym = walker_step(w, (uint32_t)n, words, prevfn);
+            if (sym != NOSYM) {
+                if (syms) syms->push_back(sym), tops->push_back(p);
+                ++cnt;
+            }
+        }
+    };
+    uint64_t cont_steps = 0;
+    for (uint64_t k = 0; k < nch; ++k) {
+        uint64_t c;
+        uint32_t idx;
+        ncont[k] = follow(ex[k], c, idx, nullptr, nullptr);
+        nxt[k] = c;
+        if (c == nch) fin[k] = (int)idx;
+        else nidx[k] = idx;
+        cont_steps += ncont[k];
+    }
+    // 3. the adopted chain; 4. placement
+    std::vector<uint32_t> syms;
+    std::vector<int64_t> tops;
+    int final_tag = TAG_A;
+    uint64_t a = 0, idx = 0, adopted = 0;
+    while (a < nch) {
+        ++adopted;
+        for (uint64_t i = idx; i < nsym[a]; ++i) syms.push_back(ssym[b(a) + i]), tops.push_back((int64_t)(b(a) + spos[b(a) + i]));
+        uint64_t c;
+        uint32_t id;
+        follow(ex[a], c, id, &syms, &tops);
+        if (c == nch) final_tag = (int)id;
+        else idx = id;
+        a = c;
+    }
+    tops.resize(syms.size() + 2);
+    const int rc = emit_stream(in, n, syms, tops, final_tag, (int64_t)nch, out, cap, out_len, stats);
+    if (stats) stats[0] = adopted, stats[1] = cont_steps;
+    return rc;
 }

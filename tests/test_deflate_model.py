@@ -28,12 +28,15 @@ def zmodel():
     lib.zmodel_crc_combine.restype = C.c_uint32
     lib.zmodel_crc_combine.argtypes = [C.c_uint32, C.c_uint32, C.c_uint64]
 
-    def run(data: bytes, chunk: int = 2048) -> bytes:
+    lib.zmodel_compress_od.argtypes = lib.zmodel_compress.argtypes
+
+    def run(data: bytes, chunk: int = 2048, ondemand: bool = False) -> bytes:
         cap = 2 * len(data) + 1024
         out = C.create_string_buffer(cap)
         n = C.c_uint64()
         st = (C.c_uint64 * 6)()
-        assert lib.zmodel_compress(data, len(data), chunk, out, cap, C.byref(n), st) == 0
+        f = lib.zmodel_compress_od if ondemand else lib.zmodel_compress
+        assert f(data, len(data), chunk, out, cap, C.byref(n), st) == 0
         return out.raw[: n.value]
 
     run.lib = lib
@@ -66,8 +69,13 @@ CASES = list(_cases())
 
 @pytest.mark.parametrize("name,data", CASES, ids=[c[0] for c in CASES])
 def test_model_equals_zlib_level6(zmodel, name, data):
-    assert zmodel(data) == zlib.compress(data, 6)
-    assert zmodel(data, chunk=257) == zlib.compress(data, 6)
+    want = zlib.compress(data, 6)
+    assert zmodel(data) == want
+    assert zmodel(data, chunk=257) == want
+    # the on-demand chunked parse (what the GPU runs for streams < 2^31 bytes), with chunk sizes
+    # that put joins inside matches, across several chunks and at the stream end
+    for ch in (64, 300, 1024, 8192):
+        assert zmodel(data, chunk=ch, ondemand=True) == want, ch
 
 
 def test_model_on_real_bitplanes(zmodel, oracle_lib):
@@ -81,7 +89,9 @@ def test_model_on_real_bitplanes(zmodel, oracle_lib):
             for p in range(32):
                 raw = lt.xor_planes[p].tobytes()
                 if raw:
-                    assert zmodel(raw) == zlib.compress(raw, 6), (cfg, lt.count, p)
+                    want = zlib.compress(raw, 6)
+                    assert zmodel(raw) == want, (cfg, lt.count, p)
+                    assert zmodel(raw, chunk=1024, ondemand=True) == want, (cfg, lt.count, p)
 
 
 def test_crc_combine(zmodel):
