@@ -75,6 +75,10 @@ struct Work {
     struct OdChunk *od_chunks;
     uint64_t od_nch;
     uint32_t od_C;
+    // next byte-change position at or after each 64-byte group (suffix minimum): run lengths in
+    // O(1) for the continuation walks' run jumps
+    uint32_t *od_chg;
+    uint64_t od_ng;
 };
 
 constexpr uint64_t SEG = 32;  // chunks per resolve segment
@@ -92,8 +96,8 @@ struct OdChunk {
 };
 
 static uint32_t od_chunk_size() {
-    static const uint32_t c = getenv("IPCG_OD_CHUNK") ? (uint32_t)atoi(getenv("IPCG_OD_CHUNK")) : 1024u;
-    return c < 64 ? 64u : c > 8192 ? 8192u : c;
+    static const uint32_t c = getenv("IPCG_OD_CHUNK") ? (uint32_t)atoi(getenv("IPCG_OD_CHUNK")) : 64u;
+    return c < 16 ? 16u : c > 8192 ? 8192u : c;
 }
 
 Work carve(void *ws, int S, uint64_t n, size_t *size_out = nullptr) {
@@ -114,6 +118,8 @@ Work carve(void *ws, int S, uint64_t n, size_t *size_out = nullptr) {
     w.od_spos = w.od_vis + (size_t)S * n;
     w.od_ssym = reinterpret_cast<uint32_t *>(w.od_spos + (size_t)S * n);  // 4-byte aligned: 4Sn bytes in
     w.od_chunks = b.take<OdChunk>((size_t)S * w.od_nch);
+    w.od_ng = (n + 63) / 64;
+    w.od_chg = b.take<uint32_t>((size_t)S * (w.od_ng + 1));
     w.first_anchor = b.take<uint64_t>((size_t)S * w.nchunks);
     w.nbreak = b.take<uint32_t>((size_t)S * (w.nchunks + 1));
     w.bnd = b.take<uint64_t>((size_t)S * (w.nchunks + 1));
@@ -174,7 +180,7 @@ struct PrevD32 {
 // 4-byte words of a stream whose base is 16-byte aligned and whose row is padded to 16
 // bytes, so a word whose first byte is < n is always inside the allocation.
 struct InWords {
-    const uint8_t *p;
+    const uint8_t *p;  // stream base
     __device__ __forceinline__ uint32_t word(uint32_t k) const { return __ldg(reinterpret_cast<const uint32_t *>(p) + k); }
     __device__ __forceinline__ uint32_t byte(uint32_t i) const { return __ldg(p + i); }
     __device__ __forceinline__ const uint8_t *at(uint32_t off) const { return p + off; }
@@ -871,13 +877,81 @@ __global__ void __launch_bounds__(128) k_od_walk(const uint8_t *in, uint64_t in_
     c.ex_p = w.p, c.ex_tag = w.tag, c.ex_pl = w.pl, c.ex_pd = w.pd;
 }
 
-// the continuation of a chunk walk: from its exit state until a visited state (or the stream
-// end); emits into syms (with block bookkeeping) when given, counts otherwise
-template <bool EMIT>
-__device__ uint32_t od_follow(Walker w, uint32_t n, uint32_t C, uint32_t nch, const InWords &words, const PrevD32 &prev,
-                              const uint16_t *vis, uint32_t &nxt, uint32_t &idx, uint32_t *syms, uint64_t g,
-                              uint64_t *btop, uint64_t *bstart) {
-    uint32_t cnt = 0;
+// Byte runs: first position y in each 64-byte group with in[y] != in[y-1] (or ~0), then the suffix
+// minimum over groups, so next_change(x) -- the end of the run containing x-1 -- costs one group
+// scan and one load.
+__global__ void __launch_bounds__(256) k_od_chg(const uint8_t *in, uint64_t in_stride, uint32_t n, const StreamMeta *meta,
+                                               uint64_t ng, uint32_t *chg_all) {
+    const int j = blockIdx.y;
+    if (!meta[j].active) return;
+    const uint64_t g = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+    if (g >= ng) return;
+    const uint8_t *p = in + (uint64_t)j * in_stride;
+    const uint32_t a = (uint32_t)g * 64, e = min(n, a + 64);
+    uint32_t first = 0xffffffffu;
+    for (uint32_t y = a < 1 ? 1 : a; y < e; ++y)
+        if (__ldg(p + y) != __ldg(p + y - 1)) {
+            first = y;
+            break;
+        }
+    chg_all[(uint64_t)j * (ng + 1) + g] = first;
+}
+
+__global__ void __launch_bounds__(1024) k_od_chg_suffix(uint32_t n, const StreamMeta *meta, uint64_t ng,
+                                                       uint32_t *chg_all) {
+    const int j = blockIdx.x;
+    if (!meta[j].active) return;
+    uint32_t *chg = chg_all + (uint64_t)j * (ng + 1);
+    __shared__ uint32_t wmin[32];
+    __shared__ uint32_t carry;
+    if (threadIdx.x == 0) carry = n, chg[ng] = n;
+    __syncthreads();
+    const unsigned lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    for (int64_t t0 = ((int64_t)ng - 1) / 1024 * 1024; t0 >= 0; t0 -= 1024) {
+        const uint64_t g = (uint64_t)t0 + threadIdx.x;
+        uint32_t v = g < ng ? chg[g] : 0xffffffffu;
+        for (int o = 1; o < 32; o <<= 1) {  // suffix min inside the warp
+            const uint32_t x = __shfl_down_sync(0xffffffffu, v, o);
+            if (lane + o < 32) v = min(v, x);
+        }
+        if (lane == 0) wmin[warp] = v;
+        __syncthreads();
+        uint32_t after = carry;  // minimum over later warps of this tile and later tiles
+        for (unsigned w2 = warp + 1; w2 < 32; ++w2) after = min(after, wmin[w2]);
+        v = min(v, after);
+        if (g < ng) chg[g] = min(v, n);
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            uint32_t m = carry;
+            for (int w2 = 0; w2 < 32; ++w2) m = min(m, wmin[w2]);
+            carry = m;
+        }
+        __syncthreads();
+    }
+}
+
+// first y >= x with in[y] != in[y-1] (n if none)
+__device__ __forceinline__ uint32_t next_change(const uint8_t *p, uint32_t n, const uint32_t *chg, uint32_t x) {
+    if (x >= n) return n;
+    const uint32_t g = x / 64, e = min(n, g * 64 + 64);
+    for (uint32_t y = x < 1 ? 1 : x; y < e; ++y)
+        if (__ldg(p + y) != __ldg(p + y - 1)) return y;
+    return chg[g + 1];
+}
+
+// The continuation of a chunk walk: from its exit state until a state the walk of the chunk it
+// is in visited (or the stream end).  Inside a byte run the parse is periodic: at (p, A) with
+// in[p-1] == in[p] and R bytes of the run left from p, the search finds (258, 1) and the next
+// state emits match(258, 1) and lands on (p + 258, A) -- floor(R / 258) such cycles are taken at
+// once (no sync check at the skipped states: a later join is still exact, only later).  EMIT
+// places the symbols (with the block bookkeeping); a warp (LANES = 32) walks redundantly and
+// writes the symbols of a jump in parallel.
+template <bool EMIT, int LANES>
+__device__ uint64_t od_follow(Walker w, uint32_t n, uint32_t C, uint32_t nch, const InWords &words, const PrevD32 &prev,
+                              const uint16_t *vis, const uint32_t *chg, uint32_t &nxt, uint32_t &idx, uint32_t *syms,
+                              uint64_t g, uint64_t *btop, uint64_t *bstart) {
+    const unsigned lane = LANES == 1 ? 0u : (threadIdx.x & 31);
+    uint64_t cnt = 0;
     for (;;) {
         if (w.p >= n) {
             nxt = nch;
@@ -891,12 +965,34 @@ __device__ uint32_t od_follow(Walker w, uint32_t n, uint32_t C, uint32_t nch, co
             return cnt;
         }
         const uint32_t p = w.p;
+        if (w.tag == TAG_A && p >= 1 && p + 516 <= n && words.byte(p - 1) == words.byte(p) &&
+            words.byte(p + 257) == words.byte(p) && words.byte(p + 515) == words.byte(p)) {
+            const uint32_t R = next_change(words.p, n, chg, p + 1) - p;
+            const uint32_t m = R / (uint32_t)MAX_MATCH;
+            if (m >= 2) {
+                if (EMIT) {
+                    const uint32_t sym = sym_match(MAX_MATCH, 1);
+                    for (uint32_t i = lane; i < m; i += LANES) {
+                        const uint64_t gi = g + i, top = (uint64_t)p + 1 + (uint64_t)MAX_MATCH * i;
+                        syms[gi] = sym;
+                        if (gi % BLOCK_SYMS == 0) bstart[gi / BLOCK_SYMS] = top - 1;
+                        if (gi % BLOCK_SYMS == BLOCK_SYMS - 1) btop[gi / BLOCK_SYMS] = top;
+                    }
+                    g += m;
+                }
+                cnt += m;
+                w.p = p + (uint32_t)MAX_MATCH * m;  // tag stays A
+                continue;
+            }
+        }
         const uint32_t sym = walker_step(w, n, words, prev);
         if (sym != NOSYM) {
             if (EMIT) {
-                syms[g] = sym;
-                if (g % BLOCK_SYMS == 0) bstart[g / BLOCK_SYMS] = (uint64_t)p - 1;
-                if (g % BLOCK_SYMS == BLOCK_SYMS - 1) btop[g / BLOCK_SYMS] = (uint64_t)p;
+                if (lane == 0) {
+                    syms[g] = sym;
+                    if (g % BLOCK_SYMS == 0) bstart[g / BLOCK_SYMS] = (uint64_t)p - 1;
+                    if (g % BLOCK_SYMS == BLOCK_SYMS - 1) btop[g / BLOCK_SYMS] = (uint64_t)p;
+                }
                 ++g;
             }
             ++cnt;
@@ -906,7 +1002,8 @@ __device__ uint32_t od_follow(Walker w, uint32_t n, uint32_t C, uint32_t nch, co
 
 __global__ void __launch_bounds__(128) k_od_sync(const uint8_t *in, uint64_t in_stride, uint32_t n,
                                                 const StreamMeta *meta, const uint16_t *prevd_all, uint32_t C,
-                                                uint32_t nch, const uint16_t *vis_all, OdChunk *chunks_all) {
+                                                uint32_t nch, const uint16_t *vis_all, const uint32_t *chg_all,
+                                                uint64_t ng, OdChunk *chunks_all) {
     const int j = blockIdx.y;
     if (!meta[j].active) return;
     const uint32_t k = blockIdx.x * blockDim.x + threadIdx.x;
@@ -918,8 +1015,9 @@ __global__ void __launch_bounds__(128) k_od_sync(const uint8_t *in, uint64_t in_
     const PrevD32 prev{pvj};
     OdChunk &c = chunks_all[(uint64_t)j * nch + k];
     uint32_t nxt, idx;
-    c.ncont = od_follow<false>(Walker{c.ex_p, c.ex_tag, c.ex_pl, c.ex_pd}, n, C, nch, words, prev,
-                               vis_all + (uint64_t)j * n, nxt, idx, nullptr, 0, nullptr, nullptr);
+    c.ncont = (uint32_t)od_follow<false, 1>(Walker{c.ex_p, c.ex_tag, c.ex_pl, c.ex_pd}, n, C, nch, words, prev,
+                                            vis_all + (uint64_t)j * n, chg_all + (uint64_t)j * (ng + 1), nxt, idx,
+                                            nullptr, 0, nullptr, nullptr);
     c.nxt = nxt, c.nidx = idx;
 }
 
@@ -992,9 +1090,9 @@ __global__ void __launch_bounds__(32) k_od_chain(const uint8_t *in, uint64_t in_
 __global__ void __launch_bounds__(128) k_od_place(const uint8_t *in, uint64_t in_stride, uint32_t n,
                                                  const StreamMeta *meta, const uint16_t *prevd_all, uint32_t C,
                                                  uint32_t nch, const uint16_t *vis_all, const uint32_t *ssym_all,
-                                                 const uint16_t *spos_all, const OdChunk *chunks_all,
-                                                 uint32_t *syms_all, uint64_t maxb, uint64_t *blk_top_all,
-                                                 uint64_t *blk_start_all) {
+                                                 const uint16_t *spos_all, const uint32_t *chg_all, uint64_t ng,
+                                                 const OdChunk *chunks_all, uint32_t *syms_all, uint64_t maxb,
+                                                 uint64_t *blk_top_all, uint64_t *blk_start_all) {
     const int j = blockIdx.y;
     if (!meta[j].active) return;
     const uint32_t k = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
@@ -1014,13 +1112,14 @@ __global__ void __launch_bounds__(128) k_od_place(const uint8_t *in, uint64_t in
         if (g % BLOCK_SYMS == 0) bstart[g / BLOCK_SYMS] = p - 1;
         if (g % BLOCK_SYMS == BLOCK_SYMS - 1) btop[g / BLOCK_SYMS] = p;
     }
-    if (lane == 0 && c.ncont) {
+    if (c.ncont) {  // the whole warp walks the continuation (a run jump's symbols go out in parallel)
         const uint8_t *inj = in + (uint64_t)j * in_stride;
         const InWords words{inj};
         const PrevD32 prev{prevd_all + (uint64_t)j * n};
         uint32_t nxt, idx;
-        od_follow<true>(Walker{c.ex_p, c.ex_tag, c.ex_pl, c.ex_pd}, n, C, nch, words, prev, vis_all + (uint64_t)j * n,
-                        nxt, idx, syms, c.coff, btop, bstart);
+        od_follow<true, 32>(Walker{c.ex_p, c.ex_tag, c.ex_pl, c.ex_pd}, n, C, nch, words, prev,
+                            vis_all + (uint64_t)j * n, chg_all + (uint64_t)j * (ng + 1), nxt, idx, syms, c.coff, btop,
+                            bstart);
     }
 }
 
@@ -1434,6 +1533,11 @@ void DeflateBatch::run(const uint8_t *in, uint64_t in_stride, int S, uint64_t n,
             {
             ProfScope ps2("deflate.walk", st, (uint64_t)S * n);
             CK(cudaMemsetAsync(w.od_vis, 0, (size_t)S * n * sizeof(uint16_t), st));
+            k_od_chg<<<dim3((unsigned)((w.od_ng + 255) / 256), S), 256, 0, st>>>(in, in_stride, (uint32_t)n, w.meta,
+                                                                             w.od_ng, w.od_chg);
+            CKL();
+            k_od_chg_suffix<<<S, 1024, 0, st>>>((uint32_t)n, w.meta, w.od_ng, w.od_chg);
+            CKL();
             k_od_walk<<<dim3((nch + 127) / 128, S), 128, 0, st>>>(in, in_stride, (uint32_t)n, w.meta, w.prevd, w.od_C,
                                                                   nch, w.od_vis, w.od_ssym, w.od_spos, w.od_chunks);
             CKL();
@@ -1442,7 +1546,7 @@ void DeflateBatch::run(const uint8_t *in, uint64_t in_stride, int S, uint64_t n,
             {
             ProfScope ps3("deflate.sync", st, (uint64_t)S * n);
             k_od_sync<<<dim3((nch + 127) / 128, S), 128, 0, st>>>(in, in_stride, (uint32_t)n, w.meta, w.prevd, w.od_C,
-                                                                  nch, w.od_vis, w.od_chunks);
+                                                                  nch, w.od_vis, w.od_chg, w.od_ng, w.od_chunks);
             CKL();
             k_od_chain<<<S, 32, 0, st>>>(in, in_stride, (uint32_t)n, w.meta, nch, w.od_chunks, w.syms, w.maxb,
                                          w.blk_start);
@@ -1451,8 +1555,8 @@ void DeflateBatch::run(const uint8_t *in, uint64_t in_stride, int S, uint64_t n,
             {
             ProfScope ps3("deflate.place", st, (uint64_t)S * n);
             k_od_place<<<dim3((nch + 3) / 4, S), 128, 0, st>>>(in, in_stride, (uint32_t)n, w.meta, w.prevd, w.od_C, nch,
-                                                               w.od_vis, w.od_ssym, w.od_spos, w.od_chunks, w.syms,
-                                                               w.maxb, w.blk_top, w.blk_start);
+                                                               w.od_vis, w.od_ssym, w.od_spos, w.od_chg, w.od_ng,
+                                                               w.od_chunks, w.syms, w.maxb, w.blk_top, w.blk_start);
             CKL();
             }
         } else {

@@ -405,6 +405,20 @@ extern "C" int zmodel_compress_od(const uint8_t *in, uint64_t n, int chunk, uint
                 return cnt;
             }
             const uint32_t p = w.p;
+            // the GPU's run jump (deflate.cu od_follow): floor(R / 258) periodic match(258, 1) cycles
+            if (w.tag == TAG_A && p >= 1 && p + 516 <= n && in[p - 1] == in[p] && in[p + 257] == in[p] &&
+                in[p + 515] == in[p]) {
+                uint64_t e = p + 1;
+                while (e < n && in[e] == in[e - 1]) ++e;
+                const uint64_t m = (e - p) / MAX_MATCH;
+                if (m >= 2) {
+                    for (uint64_t i = 0; i < m; ++i)
+                        if (syms) syms->push_back(sym_match(MAX_MATCH, 1)), tops->push_back((int64_t)(p + 1 + MAX_MATCH * i));
+                    cnt += m;
+                    w.p = (uint32_t)(p + MAX_MATCH * m);
+                    continue;
+                }
+            }
             const uint32_t sym = walker_step(w, (uint32_t)n, words, prevfn);
             if (sym != NOSYM) {
                 if (syms) syms->push_back(sym), tops->push_back(p);

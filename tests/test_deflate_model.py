@@ -54,6 +54,8 @@ def _cases():
         yield f"runs{n}", np.repeat(rng.integers(0, 3, n // 50 + 1, dtype=np.uint8),
                                     rng.integers(1, 300, n // 50 + 1))[:n].tobytes()
         yield f"text{n}", (b"the quick brown fox %d jumps over " * (n // 30 + 1))[:n]
+        yield f"longruns{n}", np.repeat(rng.integers(0, 4, n // 500 + 1, dtype=np.uint8),
+                                        rng.integers(1, 5000, n // 500 + 1))[:n].tobytes()
     # window-slide boundaries: tail slides with the head exactly at MAX_DIST
     for k in range(3):
         base = 32768 * k + 65536
