@@ -23,9 +23,10 @@ constexpr int PL_WARPS = 3;  // prevlink warps per CTA (64 KiB head table each)
 constexpr int CRC_CHUNK = 4096;
 
 struct StreamMeta {
-    unsigned long long nonzero, adA, adB;
+    unsigned long long nonzero, adA, adB, zeros;
     uint32_t adler;
     int active, rep, final_tag;
+    int od;  // parsed by the on-demand walkers (sparse streams) instead of the all-position search
     unsigned long long S_loop, nsyms, nblocks, total_bits, comp_len;
 };
 
@@ -79,9 +80,16 @@ struct Work {
     // O(1) for the continuation walks' run jumps
     uint32_t *od_chg;
     uint64_t od_ng;
+    uint64_t *od_cbuf;  // OD_CB continuation symbols (sym | loop top << 32) per chunk
+    uint4 *od_link;     // per chunk (nxt, nidx, nsym, ncont), packed for the path resolution
+    struct OdSc *od_sc; // per chunk as a superchunk entry (k_od_sc_jump)
+    uint4 *od_entry;    // per superchunk: the path's entry (chunk, join index, output offset)
+    uint64_t od_nsc;
 };
 
 constexpr uint64_t SEG = 32;  // chunks per resolve segment
+constexpr int OD_CB = 4;      // continuation symbols buffered per chunk by k_od_sync
+constexpr int OD_SC = 1024;   // chunks per superchunk of the path resolution
 
 // one chunk of the on-demand parse (deflate_core.cuh Walker): its walk from (start, A), the
 // continuation from the walk's exit, and its place on the true parse
@@ -92,6 +100,7 @@ struct OdChunk {
     uint32_t nidx;                        // ... at that walk's symbol index; the final tag at the end
     uint32_t ncont;                       // symbols the continuation emits before it joins
     uint32_t adopted, aidx;               // on the true parse; its first own symbol on it
+    uint32_t cbuf_ok;                     // the continuation's symbols are in od_cbuf (no re-walk)
     uint64_t aoff, coff;                  // output offsets of the adopted own symbols / the continuation
 };
 
@@ -114,10 +123,15 @@ Work carve(void *ws, int S, uint64_t n, size_t *size_out = nullptr) {
     w.rec = b.take<uint64_t>((size_t)S * n);
     w.od_C = od_chunk_size();
     w.od_nch = (n + w.od_C - 1) / w.od_C;
-    w.od_vis = reinterpret_cast<uint16_t *>(w.rec);
-    w.od_spos = w.od_vis + (size_t)S * n;
-    w.od_ssym = reinterpret_cast<uint32_t *>(w.od_spos + (size_t)S * n);  // 4-byte aligned: 4Sn bytes in
+    w.od_vis = b.take<uint16_t>((size_t)S * n);
+    w.od_spos = b.take<uint16_t>((size_t)S * n);
+    w.od_ssym = b.take<uint32_t>((size_t)S * n);
     w.od_chunks = b.take<OdChunk>((size_t)S * w.od_nch);
+    w.od_cbuf = b.take<uint64_t>((size_t)S * w.od_nch * OD_CB);
+    w.od_link = b.take<uint4>((size_t)S * w.od_nch);
+    w.od_nsc = (w.od_nch + OD_SC - 1) / OD_SC;
+    w.od_sc = b.take<OdSc>((size_t)S * w.od_nsc * OD_SC);
+    w.od_entry = b.take<uint4>((size_t)S * w.od_nsc);
     w.od_ng = (n + 63) / 64;
     w.od_chg = b.take<uint32_t>((size_t)S * (w.od_ng + 1));
     w.first_anchor = b.take<uint64_t>((size_t)S * w.nchunks);
@@ -194,7 +208,7 @@ struct InWords {
 __global__ void k_scan(const uint8_t *in, uint64_t in_stride, uint64_t n, StreamMeta *meta) {
     const int j = blockIdx.y;
     const uint8_t *p = in + (uint64_t)j * in_stride;
-    unsigned long long nz = 0, A = 0, W = 0;
+    unsigned long long nz = 0, A = 0, W = 0, zc = 0;  // zc: zero bytes x 8 (vcmpeq4 sets 8 bits per byte)
     const uint64_t nv = n / 16;
     const uint4 *pv = reinterpret_cast<const uint4 *>(p);
     for (uint64_t v = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; v < nv; v += (uint64_t)gridDim.x * blockDim.x) {
@@ -208,12 +222,15 @@ __global__ void k_scan(const uint8_t *in, uint64_t in_stride, uint64_t n, Stream
             ws += __dp4a(w[k], 0x03020100u, 0u) + 4u * k * sk;
         }
         nz |= q.x | q.y | q.z | q.w;
+        zc += __popc(__vcmpeq4(q.x, 0u)) + __popc(__vcmpeq4(q.y, 0u)) + __popc(__vcmpeq4(q.z, 0u)) +
+              __popc(__vcmpeq4(q.w, 0u));
         A += s;
         W += (unsigned long long)(16 * v) * s + ws;
     }
     for (uint64_t i = nv * 16 + blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
         const uint32_t b = p[i];
         nz |= b;
+        zc += b == 0 ? 8u : 0u;
         A += b;
         W += (unsigned long long)i * b;
     }
@@ -223,15 +240,17 @@ __global__ void k_scan(const uint8_t *in, uint64_t in_stride, uint64_t n, Stream
     for (int o = 16; o > 0; o >>= 1) {
         A += __shfl_down_sync(0xffffffffu, A, o);
         B += __shfl_down_sync(0xffffffffu, B, o);
+        zc += __shfl_down_sync(0xffffffffu, zc, o);
     }
     if ((threadIdx.x & 31) == 0) {
+        atomicAdd(&meta[j].zeros, zc / 8);
         if (nz) atomicOr(&meta[j].nonzero, 1ull);
         atomicAdd(&meta[j].adA, A);
         atomicAdd(&meta[j].adB, B % 65521u);
     }
 }
 
-__global__ void k_select(StreamMeta *meta, int S, uint64_t n) {
+__global__ void k_select(StreamMeta *meta, int S, uint64_t n, int od_mode, int od_zeros_pct) {
     if (threadIdx.x != 0 || blockIdx.x != 0) return;
     int rep = -1;
     for (int j = 0; j < S; ++j)
@@ -243,6 +262,10 @@ __global__ void k_select(StreamMeta *meta, int S, uint64_t n) {
         StreamMeta &m = meta[j];
         m.rep = rep;
         m.active = (m.nonzero || j == rep) && n > 0;
+        // on-demand parse for sparse streams: mostly zero bytes means long matches, and the lazy
+        // parse then visits few of the positions the all-position search would cover (measured
+        // on cfg2 level-1 planes: 92% zeros -> 14% of the search work)
+        m.od = od_mode == 1 || (od_mode == 0 && m.zeros * 100 >= (unsigned long long)n * od_zeros_pct);
         const uint32_t a = (uint32_t)((1 + m.adA) % 65521u);
         const uint32_t b = (uint32_t)((m.adB + n) % 65521u);
         m.adler = (b << 16) | a;
@@ -365,7 +388,7 @@ template <bool WIDE>  // WIDE: streams of 2^31 bytes or more (64-bit positions)
 __global__ void __launch_bounds__(256) k_match(const uint8_t *in, uint64_t in_stride, uint64_t n,
                                               const StreamMeta *meta, const uint16_t *prevd_all, uint64_t *rec_all) {
     const int j = blockIdx.y;
-    if (!meta[j].active) return;
+    if (!meta[j].active || meta[j].od) return;
     uint64_t *rec = rec_all + (uint64_t)j * n;
     if constexpr (!WIDE) {
         // the stream bases go through an empty asm so the compiler keeps them in registers
@@ -393,7 +416,7 @@ constexpr int TILE = 2048;
 __global__ void __launch_bounds__(256) k_anchor(uint64_t n, const StreamMeta *meta, const uint64_t *rec_all,
                                                uint64_t nchunks, uint64_t *first_anchor) {
     const int j = blockIdx.y;
-    if (!meta[j].active) return;
+    if (!meta[j].active || meta[j].od) return;
     const uint64_t c0 = (uint64_t)blockIdx.x * TILE;
     if (c0 >= n) return;
     const uint64_t *rec = rec_all + (uint64_t)j * n;
@@ -461,7 +484,7 @@ __global__ void __launch_bounds__(256) k_bounds_seg(const StreamMeta *meta, uint
                                                    const uint64_t *first_anchor, uint64_t *segv_all,
                                                    uint32_t *segnb_all) {
     const int j = blockIdx.y;
-    if (!meta[j].active) return;
+    if (!meta[j].active || meta[j].od) return;
     const uint64_t g = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (g >= nseg) return;
     const uint64_t *fa = first_anchor + (uint64_t)j * nchunks;
@@ -482,7 +505,7 @@ __global__ void __launch_bounds__(256) k_bounds_seg(const StreamMeta *meta, uint
 __global__ void k_bounds_scan(uint64_t n, const StreamMeta *meta, uint64_t nchunks, uint64_t nseg, uint64_t *segv_all,
                               uint32_t *segnb_all) {
     const int j = blockIdx.x;
-    if (!meta[j].active) return;
+    if (!meta[j].active || meta[j].od) return;
     const unsigned lane = threadIdx.x;
     uint64_t *segv = segv_all + (uint64_t)j * nseg;
     uint32_t *segnb = segnb_all + (uint64_t)j * nseg;
@@ -511,7 +534,7 @@ __global__ void __launch_bounds__(256) k_bounds_expand(uint64_t n, const StreamM
                                                       const uint64_t *segv_all, const uint32_t *segnb_all,
                                                       uint64_t *bnd_all, uint32_t *nbreak_all) {
     const int j = blockIdx.y;
-    if (!meta[j].active) return;
+    if (!meta[j].active || meta[j].od) return;
     const uint64_t g = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (g > nseg) return;
     uint64_t *bnd = bnd_all + (uint64_t)j * (nchunks + 1);
@@ -573,7 +596,7 @@ __global__ void __launch_bounds__(256) k_sim(uint64_t n, const StreamMeta *meta,
                                             uint64_t nchunks, const uint64_t *bnd_all,
                                             const uint32_t *nbreak_all, uint8_t *exit4, uint32_t *cnt4) {
     const int j = blockIdx.y;
-    if (!meta[j].active) return;
+    if (!meta[j].active || meta[j].od) return;
     const uint64_t k = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (k >= nchunks) return;
     const RecG R{rec_all + (uint64_t)j * n};
@@ -643,7 +666,7 @@ __global__ void __launch_bounds__(256) k_seg_compose(const StreamMeta *meta, uin
                                                     const uint8_t *exit4_all, const uint32_t *cnt4_all,
                                                     uint8_t *seg_exit4_all, uint32_t *seg_cnt4_all) {
     const int j = blockIdx.y;
-    if (!meta[j].active) return;
+    if (!meta[j].active || meta[j].od) return;
     const uint64_t g = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (g >= nseg) return;
     const uint8_t *ex = exit4_all + (uint64_t)j * nchunks * 4;
@@ -670,7 +693,7 @@ __global__ void __launch_bounds__(256) k_seg_expand(const StreamMeta *meta, uint
                                                    const uint8_t *seg_entry_all, const uint64_t *seg_symoff_all,
                                                    uint8_t *entry_all, uint64_t *symoff_all) {
     const int j = blockIdx.y;
-    if (!meta[j].active) return;
+    if (!meta[j].active || meta[j].od) return;
     const uint64_t g = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (g > nseg) return;
     uint8_t *entry = entry_all + (uint64_t)j * (nchunks + 1);
@@ -706,7 +729,7 @@ __global__ void k_resolve(const uint8_t *in, uint64_t in_stride, uint64_t n, Str
                           uint32_t *syms_all, uint64_t maxb, uint64_t *blk_start_all) {
     const int j = blockIdx.x;
     StreamMeta &m = meta[j];
-    if (!m.active) return;
+    if (!m.active || m.od) return;
     const unsigned lane = threadIdx.x;
     const uint8_t *ex = exit4_all + (uint64_t)j * nchunks * 4;
     const uint32_t *cn = cnt4_all + (uint64_t)j * nchunks * 4;
@@ -767,7 +790,7 @@ __global__ void __launch_bounds__(256) k_emit_syms(const uint8_t *in, uint64_t i
                                                   uint64_t *blk_start_all, RunTask *runs,
                                                   unsigned long long *nruns) {
     const int j = blockIdx.y;
-    if (!meta[j].active) return;
+    if (!meta[j].active || meta[j].od) return;
     const uint64_t k = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (k >= nchunks) return;
     const RecG R{rec_all + (uint64_t)j * n};
@@ -848,7 +871,7 @@ __global__ void __launch_bounds__(128) k_od_walk(const uint8_t *in, uint64_t in_
                                                 uint32_t nch, uint16_t *vis_all, uint32_t *ssym_all,
                                                 uint16_t *spos_all, OdChunk *chunks_all) {
     const int j = blockIdx.y;
-    if (!meta[j].active) return;
+    if (!meta[j].active || !meta[j].od) return;
     const uint32_t k = blockIdx.x * blockDim.x + threadIdx.x;
     if (k >= nch) return;
     const uint8_t *inj = in + (uint64_t)j * in_stride;
@@ -877,13 +900,21 @@ __global__ void __launch_bounds__(128) k_od_walk(const uint8_t *in, uint64_t in_
     c.ex_p = w.p, c.ex_tag = w.tag, c.ex_pl = w.pl, c.ex_pd = w.pd;
 }
 
+// block bookkeeping of output symbol g emitted at loop top `top`: 32-bit index arithmetic (streams
+// on the on-demand path are < 2^31 bytes, so symbol indices are too)
+__device__ __forceinline__ void blk_mark(uint64_t g, uint64_t top, uint64_t *bstart, uint64_t *btop) {
+    const uint32_t g32 = (uint32_t)g, q = g32 / (uint32_t)BLOCK_SYMS, r = g32 - q * (uint32_t)BLOCK_SYMS;
+    if (r == 0) bstart[q] = top - 1;
+    if (r == (uint32_t)BLOCK_SYMS - 1) btop[q] = top;
+}
+
 // Byte runs: first position y in each 64-byte group with in[y] != in[y-1] (or ~0), then the suffix
 // minimum over groups, so next_change(x) -- the end of the run containing x-1 -- costs one group
 // scan and one load.
 __global__ void __launch_bounds__(256) k_od_chg(const uint8_t *in, uint64_t in_stride, uint32_t n, const StreamMeta *meta,
                                                uint64_t ng, uint32_t *chg_all) {
     const int j = blockIdx.y;
-    if (!meta[j].active) return;
+    if (!meta[j].active || !meta[j].od) return;
     const uint64_t g = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
     if (g >= ng) return;
     const uint8_t *p = in + (uint64_t)j * in_stride;
@@ -900,7 +931,7 @@ __global__ void __launch_bounds__(256) k_od_chg(const uint8_t *in, uint64_t in_s
 __global__ void __launch_bounds__(1024) k_od_chg_suffix(uint32_t n, const StreamMeta *meta, uint64_t ng,
                                                        uint32_t *chg_all) {
     const int j = blockIdx.x;
-    if (!meta[j].active) return;
+    if (!meta[j].active || !meta[j].od) return;
     uint32_t *chg = chg_all + (uint64_t)j * (ng + 1);
     __shared__ uint32_t wmin[32];
     __shared__ uint32_t carry;
@@ -949,19 +980,23 @@ __device__ __forceinline__ uint32_t next_change(const uint8_t *p, uint32_t n, co
 template <bool EMIT, int LANES>
 __device__ uint64_t od_follow(Walker w, uint32_t n, uint32_t C, uint32_t nch, const InWords &words, const PrevD32 &prev,
                               const uint16_t *vis, const uint32_t *chg, uint32_t &nxt, uint32_t &idx, uint32_t *syms,
-                              uint64_t g, uint64_t *btop, uint64_t *bstart) {
+                              uint64_t g, uint64_t *btop, uint64_t *bstart, uint64_t *cbuf = nullptr,
+                              uint32_t *cbuf_ok = nullptr) {
     const unsigned lane = LANES == 1 ? 0u : (threadIdx.x & 31);
     uint64_t cnt = 0;
+    bool buf_ok = cbuf != nullptr;
     for (;;) {
         if (w.p >= n) {
             nxt = nch;
             idx = w.tag;
+            if (cbuf_ok) *cbuf_ok = buf_ok;
             return cnt;
         }
         const uint16_t v = vis[w.p];
         if (vis_match(v, w.tag)) {
             nxt = w.p / C;
             idx = vis_symidx(v);
+            if (cbuf_ok) *cbuf_ok = buf_ok;
             return cnt;
         }
         const uint32_t p = w.p;
@@ -973,13 +1008,12 @@ __device__ uint64_t od_follow(Walker w, uint32_t n, uint32_t C, uint32_t nch, co
                 if (EMIT) {
                     const uint32_t sym = sym_match(MAX_MATCH, 1);
                     for (uint32_t i = lane; i < m; i += LANES) {
-                        const uint64_t gi = g + i, top = (uint64_t)p + 1 + (uint64_t)MAX_MATCH * i;
-                        syms[gi] = sym;
-                        if (gi % BLOCK_SYMS == 0) bstart[gi / BLOCK_SYMS] = top - 1;
-                        if (gi % BLOCK_SYMS == BLOCK_SYMS - 1) btop[gi / BLOCK_SYMS] = top;
+                        syms[g + i] = sym;
+                        blk_mark(g + i, (uint64_t)p + 1 + (uint64_t)MAX_MATCH * i, bstart, btop);
                     }
                     g += m;
                 }
+                buf_ok = false;
                 cnt += m;
                 w.p = p + (uint32_t)MAX_MATCH * m;  // tag stays A
                 continue;
@@ -990,10 +1024,13 @@ __device__ uint64_t od_follow(Walker w, uint32_t n, uint32_t C, uint32_t nch, co
             if (EMIT) {
                 if (lane == 0) {
                     syms[g] = sym;
-                    if (g % BLOCK_SYMS == 0) bstart[g / BLOCK_SYMS] = (uint64_t)p - 1;
-                    if (g % BLOCK_SYMS == BLOCK_SYMS - 1) btop[g / BLOCK_SYMS] = (uint64_t)p;
+                    blk_mark(g, p, bstart, btop);
                 }
                 ++g;
+            }
+            if (buf_ok) {
+                if (cnt < OD_CB) cbuf[cnt] = (uint64_t)sym | ((uint64_t)p << 32);
+                else buf_ok = false;
             }
             ++cnt;
         }
@@ -1003,9 +1040,10 @@ __device__ uint64_t od_follow(Walker w, uint32_t n, uint32_t C, uint32_t nch, co
 __global__ void __launch_bounds__(128) k_od_sync(const uint8_t *in, uint64_t in_stride, uint32_t n,
                                                 const StreamMeta *meta, const uint16_t *prevd_all, uint32_t C,
                                                 uint32_t nch, const uint16_t *vis_all, const uint32_t *chg_all,
-                                                uint64_t ng, OdChunk *chunks_all) {
+                                                uint64_t ng, OdChunk *chunks_all, uint64_t *cbuf_all,
+                                                uint4 *link_all) {
     const int j = blockIdx.y;
-    if (!meta[j].active) return;
+    if (!meta[j].active || !meta[j].od) return;
     const uint32_t k = blockIdx.x * blockDim.x + threadIdx.x;
     if (k >= nch) return;
     const uint8_t *inj = in + (uint64_t)j * in_stride;
@@ -1017,32 +1055,124 @@ __global__ void __launch_bounds__(128) k_od_sync(const uint8_t *in, uint64_t in_
     uint32_t nxt, idx;
     c.ncont = (uint32_t)od_follow<false, 1>(Walker{c.ex_p, c.ex_tag, c.ex_pl, c.ex_pd}, n, C, nch, words, prev,
                                             vis_all + (uint64_t)j * n, chg_all + (uint64_t)j * (ng + 1), nxt, idx,
-                                            nullptr, 0, nullptr, nullptr);
+                                            nullptr, 0, nullptr, nullptr,
+                                            cbuf_all + ((uint64_t)j * nch + k) * OD_CB, &c.cbuf_ok);
     c.nxt = nxt, c.nidx = idx;
+    link_all[(uint64_t)j * nch + k] = make_uint4(nxt, idx, c.nsym, c.ncont);  // what k_od_chain reads
 }
 
-// a warp per stream follows the joins 32 chunks at a time: a run of chunks each joining its
-// successor is resolved by one warp scan; a join that skips chunks starts the next run
-__global__ void __launch_bounds__(32) k_od_chain(const uint8_t *in, uint64_t in_stride, uint32_t n, StreamMeta *meta,
-                                                uint32_t nch, OdChunk *chunks_all, uint32_t *syms_all, uint64_t maxb,
-                                                uint64_t *blk_start_all) {
-    const int j = blockIdx.x;
+// The true parse as a path through the chunks: chunk 0, then the chunk its continuation joins
+// (nxt), and so on; an adopted chunk a contributes its own symbols from its join index (nidx of
+// its predecessor) plus its continuation's.  Resolved in three steps:
+//   k_od_sc_jump  a CTA per superchunk of 1024 chunks: for every possible entry chunk, by
+//                 pointer doubling in shared memory, the first path node past the superchunk,
+//                 the last node inside it and the symbol count along the way
+//   k_od_sc_walk  a thread per stream chains the superchunk entries (1024x fewer steps)
+//   k_od_sc_mark  a warp per superchunk walks its part of the path (32 chunks per step when
+//                 consecutive chunks join their successors) and writes each chunk's offsets
+struct OdSc {            // per superchunk entry chunk: where the path through it leads
+    uint32_t exit;       // first path node past the superchunk (od_nch: the stream end)
+    uint32_t exit_idx;   // nidx of the last node inside (the final tag at the stream end)
+    uint64_t total;      // sum over the nodes inside of nsym + ncont - (join index), entry's excluded
+};
+
+__global__ void __launch_bounds__(OD_SC) k_od_sc_jump(const StreamMeta *meta, uint32_t nch, uint32_t nsc,
+                                                     const uint4 *link_all, OdSc *sc_all) {
+    const int j = blockIdx.y;
+    if (!meta[j].active || !meta[j].od) return;
+    const uint32_t s0 = blockIdx.x * OD_SC, k = s0 + threadIdx.x;
+    __shared__ uint32_t J[2][OD_SC], last[2][OD_SC];
+    __shared__ unsigned long long W[2][OD_SC];
+    const uint4 l = k < nch ? link_all[(uint64_t)j * nch + k] : make_uint4(nch, 0, 0, 0);
+    const bool inside = l.x < s0 + OD_SC && l.x < nch;
+    const uint32_t t = threadIdx.x;
+    J[0][t] = inside ? l.x - s0 : 0xffffffffu;
+    W[0][t] = (unsigned long long)l.z + l.w - (inside ? l.y : 0u);
+    last[0][t] = t;
+    __syncthreads();
+    int c = 0;
+    for (int r = 0; r < 10; ++r) {
+        const uint32_t jj = J[c][t];
+        if (jj != 0xffffffffu) {
+            J[c ^ 1][t] = J[c][jj];
+            W[c ^ 1][t] = W[c][t] + W[c][jj];
+            last[c ^ 1][t] = last[c][jj];
+        } else {
+            J[c ^ 1][t] = jj, W[c ^ 1][t] = W[c][t], last[c ^ 1][t] = last[c][t];
+        }
+        __syncthreads();
+        c ^= 1;
+    }
+    if (k < nch) {
+        const uint32_t lk = s0 + last[c][t];
+        const uint4 ll = link_all[(uint64_t)j * nch + lk];
+        sc_all[(uint64_t)j * nsc * OD_SC + k] = OdSc{ll.x, ll.y, W[c][t]};
+    }
+}
+
+// per stream: the path's entry (chunk, join index, output offset) of every superchunk it enters
+__global__ void k_od_sc_walk(const uint8_t *in, uint64_t in_stride, uint32_t n, StreamMeta *meta, int S, uint32_t nch,
+                             uint32_t nsc, const OdSc *sc_all, uint4 *entry_all, uint32_t *syms_all, uint64_t maxb,
+                             uint64_t *blk_start_all) {
+    const int j = blockIdx.x * blockDim.x + threadIdx.x;
+    if (j >= S) return;
     StreamMeta &m = meta[j];
-    if (!m.active) return;
-    const unsigned lane = threadIdx.x;
-    OdChunk *ch = chunks_all + (uint64_t)j * nch;
-    uint32_t a = 0, idx = 0, final_tag = TAG_A;
+    if (!m.active || !m.od) return;
+    const OdSc *sc = sc_all + (uint64_t)j * nsc * OD_SC;
+    uint4 *entry = entry_all + (uint64_t)j * nsc;
+    uint32_t a = 0, idx = 0, s_next = 0;
     uint64_t off = 0;
-    for (uint32_t w0 = 0; w0 < nch; w0 += 32) {
+    while (a < nch) {
+        const uint32_t s = a / OD_SC;
+        for (; s_next < s; ++s_next) entry[s_next] = make_uint4(0xffffffffu, 0, 0, 0);  // jumped over
+        entry[s] = make_uint4(a, idx, (uint32_t)off, (uint32_t)(off >> 32));
+        s_next = s + 1;
+        const OdSc e = sc[a];
+        off += e.total - idx;
+        idx = e.exit_idx;
+        a = e.exit;
+    }
+    for (; s_next < nsc; ++s_next) entry[s_next] = make_uint4(0xffffffffu, 0, 0, 0);
+    const uint32_t final_tag = idx;
+    m.S_loop = off;
+    m.final_tag = (int)final_tag;
+    const bool fin = final_tag != TAG_A && n > 0;
+    m.nsyms = off + (fin ? 1 : 0);
+    m.nblocks = off / BLOCK_SYMS + 1;
+    uint64_t *bs = blk_start_all + (uint64_t)j * maxb;
+    if (fin) {
+        syms_all[(uint64_t)j * (n + 1) + off] = sym_literal(in[(uint64_t)j * in_stride + n - 1]);
+        if (off % BLOCK_SYMS == 0) bs[off / BLOCK_SYMS] = n - 1;
+    }
+    if (m.nsyms == (m.nblocks - 1) * BLOCK_SYMS) bs[m.nblocks - 1] = n;  // empty final block
+}
+
+// a warp per superchunk: from its entry, runs of chunks joining their successors resolve 32 at a
+// time by a warp scan; a join that skips chunks starts the next run
+__global__ void __launch_bounds__(128) k_od_sc_mark(const StreamMeta *meta, uint32_t nch, uint32_t nsc,
+                                                   const uint4 *link_all, const uint4 *entry_all, OdChunk *chunks_all) {
+    const int j = blockIdx.y;
+    if (!meta[j].active || !meta[j].od) return;
+    const uint32_t s = blockIdx.x * 4 + (threadIdx.x >> 5);
+    if (s >= nsc) return;
+    const unsigned lane = threadIdx.x & 31;
+    OdChunk *ch = chunks_all + (uint64_t)j * nch;
+    const uint4 *link = link_all + (uint64_t)j * nch;
+    const uint4 en = entry_all[(uint64_t)j * nsc + s];
+    const uint32_t s0 = s * OD_SC, s1 = min(nch, s0 + OD_SC);
+    uint32_t a = en.x, idx = en.y;
+    uint64_t off = ((uint64_t)en.w << 32) | en.z;
+    if (en.x == 0xffffffffu) a = s1;  // not on the path: every chunk is jumped over
+    for (uint32_t w0 = s0; w0 < s1; w0 += 32) {
         const uint32_t k = w0 + lane;
-        const bool in_range = k < nch;
-        uint32_t nxt = in_range ? ch[k].nxt : nch, nidx = in_range ? ch[k].nidx : 0;
-        const uint32_t nsym = in_range ? ch[k].nsym : 0, ncont = in_range ? ch[k].ncont : 0;
+        const bool in_range = k < s1;
+        const uint4 cur = in_range ? link[k] : make_uint4(nch, 0, 0, 0);
+        const uint32_t nxt = cur.x, nidx = cur.y, nsym = cur.z, ncont = cur.w;
         unsigned adopted = 0;
-        while (a < w0 + 32 && a < nch) {
+        while (a < w0 + 32 && a < s1) {
             const unsigned la = a - w0;
             const unsigned brk = __ballot_sync(0xffffffffu, lane >= la && in_range && (nxt != k + 1 || nxt == nch));
-            const unsigned lb = brk ? (unsigned)(__ffs(brk) - 1) : 31u;  // last lane of the run
+            const unsigned lb = brk ? (unsigned)(__ffs(brk) - 1) : 31u;
             const bool run = lane >= la && lane <= lb && in_range;
             const uint32_t prev_nidx = __shfl_up_sync(0xffffffffu, nidx, 1);
             const uint32_t my_idx = lane == la ? idx : prev_nidx;
@@ -1065,25 +1195,6 @@ __global__ void __launch_bounds__(32) k_od_chain(const uint8_t *in, uint64_t in_
             a = __shfl_sync(0xffffffffu, nxt, lb);
         }
         if (in_range && !((adopted >> lane) & 1u)) ch[k].adopted = 0;
-        if (a >= nch) {  // the run reached the stream end: its last chunk carries the final tag
-            final_tag = idx;
-            // remaining chunks (if any) are jumped over
-            for (uint32_t r = w0 + 32 + lane; r < nch; r += 32) ch[r].adopted = 0;
-            break;
-        }
-    }
-    if (lane == 0) {
-        m.S_loop = off;
-        m.final_tag = (int)final_tag;
-        const bool fin = final_tag != TAG_A && n > 0;
-        m.nsyms = off + (fin ? 1 : 0);
-        m.nblocks = off / BLOCK_SYMS + 1;
-        uint64_t *bs = blk_start_all + (uint64_t)j * maxb;
-        if (fin) {
-            syms_all[(uint64_t)j * (n + 1) + off] = sym_literal(in[(uint64_t)j * in_stride + n - 1]);
-            if (off % BLOCK_SYMS == 0) bs[off / BLOCK_SYMS] = n - 1;
-        }
-        if (m.nsyms == (m.nblocks - 1) * BLOCK_SYMS) bs[m.nblocks - 1] = n;  // empty final block
     }
 }
 
@@ -1091,10 +1202,11 @@ __global__ void __launch_bounds__(128) k_od_place(const uint8_t *in, uint64_t in
                                                  const StreamMeta *meta, const uint16_t *prevd_all, uint32_t C,
                                                  uint32_t nch, const uint16_t *vis_all, const uint32_t *ssym_all,
                                                  const uint16_t *spos_all, const uint32_t *chg_all, uint64_t ng,
-                                                 const OdChunk *chunks_all, uint32_t *syms_all, uint64_t maxb,
-                                                 uint64_t *blk_top_all, uint64_t *blk_start_all) {
+                                                 const OdChunk *chunks_all, const uint64_t *cbuf_all,
+                                                 uint32_t *syms_all, uint64_t maxb, uint64_t *blk_top_all,
+                                                 uint64_t *blk_start_all) {
     const int j = blockIdx.y;
-    if (!meta[j].active) return;
+    if (!meta[j].active || !meta[j].od) return;
     const uint32_t k = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
     const unsigned lane = threadIdx.x & 31;
     if (k >= nch) return;
@@ -1109,10 +1221,15 @@ __global__ void __launch_bounds__(128) k_od_place(const uint8_t *in, uint64_t in
         const uint64_t g = c.aoff + (i - c.aidx);
         const uint64_t p = (uint64_t)b0 + spos[i];
         syms[g] = ssym[i];
-        if (g % BLOCK_SYMS == 0) bstart[g / BLOCK_SYMS] = p - 1;
-        if (g % BLOCK_SYMS == BLOCK_SYMS - 1) btop[g / BLOCK_SYMS] = p;
+        blk_mark(g, p, bstart, btop);
     }
-    if (c.ncont) {  // the whole warp walks the continuation (a run jump's symbols go out in parallel)
+    if (c.ncont && c.cbuf_ok) {
+        if (lane < c.ncont) {
+            const uint64_t e = cbuf_all[((uint64_t)j * nch + k) * OD_CB + lane];
+            syms[c.coff + lane] = (uint32_t)e;
+            blk_mark(c.coff + lane, e >> 32, bstart, btop);
+        }
+    } else if (c.ncont) {  // the whole warp walks the continuation (a run jump's symbols go out in parallel)
         const uint8_t *inj = in + (uint64_t)j * in_stride;
         const InWords words{inj};
         const PrevD32 prev{prevd_all + (uint64_t)j * n};
@@ -1501,7 +1618,9 @@ void DeflateBatch::run(const uint8_t *in, uint64_t in_stride, int S, uint64_t n,
         CKL();
         }
     }
-    k_select<<<1, 32, 0, st>>>(w.meta, S, n);
+    static const int od_mode = getenv("IPCG_OD_MODE") ? atoi(getenv("IPCG_OD_MODE")) : 0;  // dev: 1 all, 2 none
+    static const int od_pct = getenv("IPCG_OD_ZEROS") ? atoi(getenv("IPCG_OD_ZEROS")) : 85;  // dev: threshold
+    k_select<<<1, 32, 0, st>>>(w.meta, S, n, n < (1ull << 31) ? od_mode : 2, od_pct);
     CKL();
     if (n > 0) {
         const uint64_t nblk = (n + WSIZE - 1) / WSIZE;
@@ -1527,8 +1646,9 @@ void DeflateBatch::run(const uint8_t *in, uint64_t in_stride, int S, uint64_t n,
         k_prevlinks<<<dim3((unsigned)((nblk + span * PL_WARPS - 1) / (span * PL_WARPS)), S), PL_WARPS * 32, smem, st>>>(in, in_stride, n, w.meta, w.prevd, span);
         CKL();
         }
-        static const bool od_off = getenv("IPCG_DEFLATE_ALLPOS") != nullptr;  // dev: the all-position search
-        if (n < (1ull << 31) && !od_off) {
+        // sparse streams (meta.od, k_select) take the on-demand parse, the others the all-position
+        // search; each kernel below skips the streams of the other path
+        if (n < (1ull << 31)) {
             const uint32_t nch = (uint32_t)w.od_nch;
             {
             ProfScope ps2("deflate.walk", st, (uint64_t)S * n);
@@ -1546,20 +1666,31 @@ void DeflateBatch::run(const uint8_t *in, uint64_t in_stride, int S, uint64_t n,
             {
             ProfScope ps3("deflate.sync", st, (uint64_t)S * n);
             k_od_sync<<<dim3((nch + 127) / 128, S), 128, 0, st>>>(in, in_stride, (uint32_t)n, w.meta, w.prevd, w.od_C,
-                                                                  nch, w.od_vis, w.od_chg, w.od_ng, w.od_chunks);
+                                                                  nch, w.od_vis, w.od_chg, w.od_ng, w.od_chunks,
+                                                                  w.od_cbuf, w.od_link);
             CKL();
-            k_od_chain<<<S, 32, 0, st>>>(in, in_stride, (uint32_t)n, w.meta, nch, w.od_chunks, w.syms, w.maxb,
-                                         w.blk_start);
+            }
+            {
+            ProfScope ps3c("deflate.chain", st, (uint64_t)S * n);
+            const unsigned nsc = (unsigned)w.od_nsc;
+            k_od_sc_jump<<<dim3(nsc, S), OD_SC, 0, st>>>(w.meta, nch, nsc, w.od_link, w.od_sc);
+            CKL();
+            k_od_sc_walk<<<(S + 31) / 32, 32, 0, st>>>(in, in_stride, (uint32_t)n, w.meta, S, nch, nsc, w.od_sc,
+                                                      w.od_entry, w.syms, w.maxb, w.blk_start);
+            CKL();
+            k_od_sc_mark<<<dim3((nsc + 3) / 4, S), 128, 0, st>>>(w.meta, nch, nsc, w.od_link, w.od_entry, w.od_chunks);
             CKL();
             }
             {
             ProfScope ps3("deflate.place", st, (uint64_t)S * n);
             k_od_place<<<dim3((nch + 3) / 4, S), 128, 0, st>>>(in, in_stride, (uint32_t)n, w.meta, w.prevd, w.od_C, nch,
                                                                w.od_vis, w.od_ssym, w.od_spos, w.od_chg, w.od_ng,
-                                                               w.od_chunks, w.syms, w.maxb, w.blk_top, w.blk_start);
+                                                               w.od_chunks, w.od_cbuf, w.syms, w.maxb, w.blk_top,
+                                                               w.blk_start);
             CKL();
             }
-        } else {
+        }
+        {
         {
             ProfScope ps2("deflate.match", st, (uint64_t)S * n);
             if (n < (1ull << 31))
