@@ -1264,17 +1264,31 @@ __global__ void __launch_bounds__(32) k_plan(uint64_t n, const StreamMeta *meta,
     const uint32_t *syms = syms_all + (uint64_t)j * (n + 1);
     const uint64_t s0 = b * BLOCK_SYMS, s1 = min((uint64_t)m.nsyms, (uint64_t)(s0 + BLOCK_SYMS));
     // 8 symbols per lane in flight before tallying (one dependent load per iteration left the
-    // warp waiting on global latency 512 times per block)
-    for (uint64_t base = s0; base < s1; base += 32 * 8) {
+    // warp waiting on global latency 512 times per block); a warp-uniform code (sparse planes:
+    // runs of literal 0 or of 258-byte matches) is added once instead of by 32 serialised atomics
+    const uint32_t cnt = (uint32_t)(s1 - s0);
+    const uint32_t *sb = syms + s0;
+    for (uint32_t base = 0; base < cnt; base += 32 * 8) {
         uint32_t v[8];
 #pragma unroll
         for (int k = 0; k < 8; ++k) {
-            const uint64_t i = base + (uint64_t)k * 32 + lane;
-            v[k] = i < s1 ? __ldg(syms + i) : 0xFFFFFFFFu;
+            const uint32_t i = base + (uint32_t)k * 32 + lane;
+            v[k] = i < cnt ? __ldg(sb + i) : 0xFFFFFFFFu;
         }
 #pragma unroll
         for (int k = 0; k < 8; ++k) {
             const uint32_t s = v[k];
+            if (__all_sync(0xffffffffu, s == __shfl_sync(0xffffffffu, s, 0))) {
+                if (lane == 0 && s != 0xFFFFFFFFu) {
+                    if (sym_is_match(s)) {
+                        atomicAdd(&lf[length_code(sym_lc(s)) + 257], 32u);
+                        atomicAdd(&df[dist_code(sym_dist1(s))], 32u);
+                    } else {
+                        atomicAdd(&lf[s], 32u);
+                    }
+                }
+                continue;
+            }
             if (s == 0xFFFFFFFFu) continue;
             if (sym_is_match(s)) {
                 atomicAdd(&lf[length_code(sym_lc(s)) + 257], 1u);

@@ -480,10 +480,14 @@ HD bool vis_match(uint16_t v, uint32_t tag) { return (v >> 13) == (0x4u | tag); 
 HD uint32_t vis_symidx(uint16_t v) { return v & 0x1fffu; }
 
 // ------------------------------------------------------------ static tables
-HD int ilog2(uint32_t v) {
+HD int ilog2(uint32_t v) {  // v >= 1
+#if defined(__CUDA_ARCH__)
+    return 31 - __clz((int)v);
+#else
     int r = 0;
     while (v >>= 1) ++r;
     return r;
+#endif
 }
 HD uint32_t length_code(uint32_t lc) {  // _length_code[len-3]
     if (lc < 8) return lc;
