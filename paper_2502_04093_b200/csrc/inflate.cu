@@ -439,8 +439,10 @@ __global__ void __launch_bounds__(256) k_validate(const InflateJob *jobs, const 
     }
 }
 
-__global__ void __launch_bounds__(256) k_scan(const InflateJob *jobs, const Tables *tabs, JobMeta *meta,
-                                             Survivor *surv, unsigned long long *nsurv, uint64_t surv_cap) {
+__global__ void __launch_bounds__(256) k_scan(const InflateJob *jobs, int njobs, const uint64_t *tile_off,
+                                             const Tables *tabs, JobMeta *meta, Survivor *surv,
+                                             unsigned long long *nsurv, uint64_t surv_cap) {
+    // persistent CTAs over every (job, tile): the 4096-entry Kraft table is built once per CTA
     __shared__ uint16_t kraft4[4096];  // sum of 128 >> l over four 3-bit lengths (0 = unused)
     __shared__ __align__(16) uint8_t tile[SCAN_TILE + SCAN_HALO];
     for (int i = threadIdx.x; i < 4096; i += blockDim.x) {
@@ -451,10 +453,18 @@ __global__ void __launch_bounds__(256) k_scan(const InflateJob *jobs, const Tabl
         }
         kraft4[i] = (uint16_t)k;
     }
-    const int j = blockIdx.y;
-    const InflateJob job = jobs[j];
+    const uint64_t total = tile_off[njobs];
     const uint32_t *tw = reinterpret_cast<const uint32_t *>(tile);
-    for (uint64_t t0 = (uint64_t)blockIdx.x * SCAN_TILE; t0 < job.src_len; t0 += (uint64_t)gridDim.x * SCAN_TILE) {
+    for (uint64_t g = blockIdx.x; g < total; g += gridDim.x) {
+        int lo = 0, hi = njobs - 1;  // job of tile g: last j with tile_off[j] <= g
+        while (lo < hi) {
+            const int mid = (lo + hi + 1) / 2;
+            if (tile_off[mid] <= g) lo = mid;
+            else hi = mid - 1;
+        }
+        const int j = lo;
+        const InflateJob job = jobs[j];
+        const uint64_t t0 = (g - tile_off[j]) * SCAN_TILE;
         __syncthreads();
         for (int i = threadIdx.x; i < SCAN_TILE + SCAN_HALO; i += blockDim.x)
             tile[i] = t0 + i < job.src_len ? job.src[t0 + i] : 0;
@@ -473,8 +483,8 @@ __global__ void __launch_bounds__(256) k_scan(const InflateJob *jobs, const Tabl
             if (ok) {
                 // code-length lengths: bits 17 .. 17 + 3*ncode of the window; complete code only
                 const int ncode = (int)((f0 >> 13) & 15) + 4;
-                const uint64_t lo = (uint64_t)f0 | ((uint64_t)f1 << 32);
-                uint64_t cl = (lo >> 17) | ((uint64_t)f2 << 47);  // 57 bits = 19 fields
+                const uint64_t lo2 = (uint64_t)f0 | ((uint64_t)f1 << 32);
+                uint64_t cl = (lo2 >> 17) | ((uint64_t)f2 << 47);  // 57 bits = 19 fields
                 cl &= (1ull << (3 * ncode)) - 1;
                 const uint32_t kraft = (uint32_t)kraft4[cl & 4095] + kraft4[(cl >> 12) & 4095] +
                                        kraft4[(cl >> 24) & 4095] + kraft4[(cl >> 36) & 4095] +
@@ -1111,34 +1121,56 @@ __device__ __forceinline__ void for_each_flagged(const uint32_t *bits, uint64_t 
 }
 
 __global__ void __launch_bounds__(256) k_resolve_all(const InflateJob *jobs, const Tables *tabs, const JobMeta *meta,
-                                                    int njobs, unsigned *changed) {
+                                                    int njobs, unsigned *changed, uint64_t *mlist, uint64_t mcap,
+                                                    unsigned long long *mcount) {
     cg::grid_group grid = cg::this_grid();
     const uint64_t tid = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
     const uint64_t nth = (uint64_t)gridDim.x * blockDim.x;
-    // A
+    // A: mark every unresolved byte some pointer targets, and list it once (job << 40 | byte)
     for (int j = 0; j < njobs; ++j) {
         if (meta[j].status || meta[j].allzero) continue;
         const Tables T = tabs[j];
         for_each_flagged(T.flags, jobs[j].dst_len, tid, nth, [&](uint64_t t) {
             const uint32_t s = T.ptr[t];
-            if (flag_get(T.flags, s) && !flag_get(T.mark, s)) atomicOr(&T.mark[s >> 5], 1u << (s & 31));
+            if (flag_get(T.flags, s) && !flag_get(T.mark, s)) {
+                const uint32_t bit = 1u << (s & 31);
+                if (!(atomicOr(&T.mark[s >> 5], bit) & bit)) {
+                    const unsigned long long i = atomicAdd(mcount, 1ull);
+                    if (i < mcap) mlist[i] = ((uint64_t)j << 40) | s;
+                }
+            }
         });
     }
     grid.sync();
-    // B
+    // B: pointer jumping on the listed bytes only (the marked set, closed under ptr), a grid
+    // barrier per round; the full mark bitmaps are scanned only if the list overflowed
+    const unsigned long long M = *(volatile unsigned long long *)mcount;
     for (int round = 0;; ++round) {
         if (tid == 0) changed[(round + 1) % 3] = 0;  // its last reader finished before the previous sync
         bool any = false;
-        for (int j = 0; j < njobs; ++j) {
-            if (meta[j].status || meta[j].allzero) continue;
-            const Tables T = tabs[j];
-            for_each_set(T.mark, (jobs[j].dst_len + 31) / 32, tid, nth, [&](uint64_t t) {
-                const uint32_t s = T.ptr[t];
-                if (flag_get(T.flags, s)) {
-                    T.ptr[t] = T.ptr[s];
+        if (M <= mcap) {
+            for (uint64_t i = tid; i < M; i += nth) {
+                const uint64_t e = mlist[i];
+                const Tables T = tabs[e >> 40];
+                const uint32_t t = (uint32_t)(e & 0xffffffffffull);
+                const uint32_t sp = T.ptr[t];
+                if (flag_get(T.flags, sp)) {
+                    T.ptr[t] = T.ptr[sp];
                     any = true;
                 }
-            });
+            }
+        } else {
+            for (int j = 0; j < njobs; ++j) {
+                if (meta[j].status || meta[j].allzero) continue;
+                const Tables T = tabs[j];
+                for_each_set(T.mark, (jobs[j].dst_len + 31) / 32, tid, nth, [&](uint64_t t) {
+                    const uint32_t sp = T.ptr[t];
+                    if (flag_get(T.flags, sp)) {
+                        T.ptr[t] = T.ptr[sp];
+                        any = true;
+                    }
+                });
+            }
         }
         if (__any_sync(0xffffffffu, any) && (threadIdx.x & 31) == 0) atomicOr(&changed[round % 3], 1u);
         grid.sync();
@@ -1147,7 +1179,8 @@ __global__ void __launch_bounds__(256) k_resolve_all(const InflateJob *jobs, con
             break;
         }
     }
-    // C
+    grid.sync();
+    // C: resolve every unresolved byte in one step (its target is resolved or listed)
     for (int j = 0; j < njobs; ++j) {
         if (meta[j].status || meta[j].allzero) continue;
         const InflateJob job = jobs[j];
@@ -1296,19 +1329,23 @@ void inflate_batch_host(const std::vector<InflateJob> &jobs, int *status_dev, De
     const uint64_t cand_cap = total_src / 256 + 64 * (uint64_t)n;
     // small tables: jobs, offs, caps, tabs, meta, counters
     const size_t jb = n * sizeof(InflateJob), ob = n * 8, cb = n * 4 * 8, tb = n * sizeof(Tables),
-                 mb = n * sizeof(JobMeta);
-    uint8_t *small = static_cast<uint8_t *>(alloc.get(jb + ob + cb + tb + mb + 16 * n + 64 + 1024, st));
+                 mb = n * sizeof(JobMeta), sb = (n + 1) * 8;
+    uint8_t *small = static_cast<uint8_t *>(alloc.get(jb + ob + cb + sb + tb + mb + 16 * n + 64 + 1024, st));
     InflateJob *jd = reinterpret_cast<InflateJob *>(small);
     uint64_t *od = reinterpret_cast<uint64_t *>(small + jb);
     uint64_t *cd = reinterpret_cast<uint64_t *>(small + jb + ob);
-    Tables *td = reinterpret_cast<Tables *>(((uintptr_t)(small + jb + ob + cb) + 15) & ~uintptr_t(15));
+    uint64_t *tiles_d = reinterpret_cast<uint64_t *>(small + jb + ob + cb);  // scan tiles: prefix per job
+    Tables *td = reinterpret_cast<Tables *>(((uintptr_t)(small + jb + ob + cb + sb) + 15) & ~uintptr_t(15));
     JobMeta *md = reinterpret_cast<JobMeta *>(((uintptr_t)(td + n) + 15) & ~uintptr_t(15));
     unsigned long long *acc = reinterpret_cast<unsigned long long *>(((uintptr_t)(md + n) + 15) & ~uintptr_t(15));
     unsigned long long *ncand = acc + 2 * n;
-    std::vector<uint8_t> host(jb + ob + cb);
+    std::vector<uint8_t> host(jb + ob + cb + sb);
     std::memcpy(host.data(), jobs.data(), jb);
     std::memcpy(host.data() + jb, P.offs.data(), ob);
     std::memcpy(host.data() + jb + ob, P.caps.data(), cb);
+    std::vector<uint64_t> tiles(n + 1, 0);
+    for (int q = 0; q < n; ++q) tiles[q + 1] = tiles[q] + (jobs[q].src_len + SCAN_TILE - 1) / SCAN_TILE;
+    std::memcpy(host.data() + jb + ob + cb, tiles.data(), sb);
     CK(cudaMemcpyAsync(small, host.data(), host.size(), cudaMemcpyHostToDevice, st));
     CK(cudaMemsetAsync(md, 0, (uint8_t *)(ncand + 1) - (uint8_t *)md, st));
     uint8_t *arena = static_cast<uint8_t *>(alloc.get(P.arena + 256, st));
@@ -1323,8 +1360,8 @@ void inflate_batch_host(const std::vector<InflateJob> &jobs, int *status_dev, De
     CKL();
     {
         ProfScope ps("inflate.scan", st, total_src);
-        k_scan<<<dim3(grid_for((max_src + SCAN_TILE - 1) / SCAN_TILE, 1, 4096), n), 256, 0, st>>>(jd, td, md, surv,
-                                                                                             nsurv, surv_cap);
+        k_scan<<<(unsigned)std::max<uint64_t>(1, std::min<uint64_t>(tiles[n], (uint64_t)num_sms() * 8)), 256, 0, st>>>(
+            jd, n, tiles_d, td, md, surv, nsurv, surv_cap);
         CKL();
         k_validate<<<148 * 8, 256, 0, st>>>(jd, td, md, surv, nsurv, surv_cap, cands, ncand, cand_cap);
         CKL();
@@ -1382,8 +1419,11 @@ void inflate_batch_host(const std::vector<InflateJob> &jobs, int *status_dev, De
         }
         {
             ProfScope ps3("inflate.resolve", st, max_dst * n / 8);
-            unsigned *changed = static_cast<unsigned *>(alloc.get(4 * sizeof(unsigned), st));
-            CK(cudaMemsetAsync(changed, 0, 4 * sizeof(unsigned), st));
+            unsigned *changed = static_cast<unsigned *>(alloc.get(4 * sizeof(unsigned) + 8, st));
+            unsigned long long *mcount = reinterpret_cast<unsigned long long *>(changed + 4);
+            CK(cudaMemsetAsync(changed, 0, 4 * sizeof(unsigned) + 8, st));
+            uint64_t mcap = std::max<uint64_t>(1 << 20, max_dst * (uint64_t)n / 32);  // marked bytes listed
+            uint64_t *mlist = static_cast<uint64_t *>(alloc.get(mcap * 8, st));
             static int coop_blocks = 0;
             if (!coop_blocks) {
                 int dev = 0, sms = 0, per = 0;
@@ -1393,13 +1433,17 @@ void inflate_batch_host(const std::vector<InflateJob> &jobs, int *status_dev, De
                 coop_blocks = sms * std::max(1, std::min(per, 4));
             }
             int nj = n;
-            void *args[] = {(void *)&jd, (void *)&td, (void *)&md, (void *)&nj, (void *)&changed};
+            void *args[] = {(void *)&jd, (void *)&td, (void *)&md, (void *)&nj, (void *)&changed, (void *)&mlist,
+                            (void *)&mcap, (void *)&mcount};
             CK(cudaLaunchCooperativeKernel((const void *)k_resolve_all, dim3(coop_blocks), dim3(256), args, 0, st));
             CKL();
             if (getenv("IPCG_DEBUG_INFLATE")) {
                 unsigned hr[4];
+                unsigned long long hm = 0;
                 CK(cudaStreamSynchronize(st));
                 CK(cudaMemcpy(hr, changed, sizeof(hr), cudaMemcpyDeviceToHost));
+                CK(cudaMemcpy(&hm, mcount, 8, cudaMemcpyDeviceToHost));
+                fprintf(stderr, "inflate: %llu listed (marked) bytes\n", hm);
                 uint64_t unres = 0;
                 std::vector<Tables> ht(n);
                 CK(cudaMemcpy(ht.data(), td, n * sizeof(Tables), cudaMemcpyDeviceToHost));
