@@ -24,6 +24,7 @@
 #include <cstdlib>
 
 #include "../../include/ipcomp_b200.h"
+#include "assemble.cuh"
 #include "deflate.cuh"
 #include "grid.h"
 #include "host.h"
@@ -407,26 +408,20 @@ ipcg_archive *compress_impl(ipcg_ctx *c, int scalar, const void *values, int on_
     DBuf state(n * w, st), dev(n * 8, st);
     CK(cudaMemsetAsync(state.p, 0, n * w, st));
     CK(cudaMemsetAsync(dev.p, 0, n * 8, st));
-    // small per-call device state
-    struct Small {
-        double rng[2];
-        uint32_t lowor[IPCG_MAX_LEVELS];
-        unsigned long long raw[IPCG_MAX_LEVELS][33];
-        double delta[IPCG_MAX_LEVELS][33];
-        unsigned long long ocount[IPCG_MAX_LEVELS];
-        uint8_t backend[IPCG_MAX_LEVELS][32];
-        uint64_t length[IPCG_MAX_LEVELS][32];
-        uint32_t crc[IPCG_MAX_LEVELS][32];
-        const uint8_t *payload[IPCG_MAX_LEVELS][32];
-        double range_part[2 * 1024];
-    };
+    // small per-call device state (assemble.cuh)
+    using Small = AsmSmall;
     DBuf small(sizeof(Small), st);
     tm.mark("setup");
     Timeline tline;
     tline.mark("start", st);
     Small *sd = small.as<Small>();
     CK(cudaMemsetAsync(small.p, 0, sizeof(Small), st));
-    DBuf ord(n * 8, st), bits(n * 8, st);
+    // outliers: a bitmap over each level's ordinals and the exact values by ordinal
+    uint64_t flag_words = 0;
+    std::vector<uint64_t> fbase(L);
+    for (int li = 0; li < L; ++li) fbase[li] = flag_words, flag_words += (G.level[li].count + 31) / 32;
+    DBuf bits(n * 8, st), oflags(std::max<uint64_t>(flag_words, 1) * 4, st);
+    CK(cudaMemsetAsync(oflags.p, 0, std::max<uint64_t>(flag_words, 1) * 4, st));
     {
         ProfScope ps("range", st, n * w);
         launch_range(vals, scalar, n, sd->range_part, sd->rng, st);
@@ -465,7 +460,7 @@ ipcg_archive *compress_impl(ipcg_ctx *c, int scalar, const void *values, int on_
         outs[li] = DBuf(32 * out_stride[li], st);
         tm.mark("alloc_l");
         uint32_t *nb = nbs[li].as<uint32_t>();
-        const OutlierSink sink{&sd->ocount[li], ord.as<uint64_t>() + sink_base[li], bits.as<uint64_t>() + sink_base[li]};
+        const OutlierSink sink{&sd->ocount[li], oflags.as<uint32_t>() + fbase[li], bits.as<uint64_t>() + sink_base[li]};
         {
             ProfScope ps("quant_pass", st, lg.count * (uint64_t)(2 * w + 4) + lg.count * (uint64_t)w);
             for (const PassDesc &pd : lg.passes)
@@ -526,118 +521,60 @@ ipcg_archive *compress_impl(ipcg_ctx *c, int scalar, const void *values, int on_
             stream_dep(c, side_stream(c, 1 + (size_t)li), st);
         }
     }
-    Small *sh = static_cast<Small *>(pinned(c, sizeof(Small)));
     tm.mark("enqueue");
-    readback(sh, small.p, sizeof(Small), st);
-    tline.print();
-    Small hs;
-    std::memcpy(&hs, sh, sizeof(Small));
-    tm.mark("gpu_wait");
-
-    // index (pipeline.hpp:158-217 + archive.cpp:31-65)
-    ipcg_index ix{};
-    ix.version = 1;
-    ix.scalar = (uint8_t)scalar;
-    ix.interp = (uint8_t)interp;
-    ix.ndims = (uint8_t)nd;
-    for (int i = 0; i < nd; ++i) ix.dims[i] = dims[i];
-    ix.eb = eb;
-    ix.range = hs.rng[1] - hs.rng[0];
-    ix.levels = (uint8_t)L;
-    ix.progressive_levels = (uint8_t)lp;
-    ix.anchor_cap = (uint8_t)cap;
-    uint64_t cursor = 0;
-    for (int level = L; level >= 1; --level) {
-        const int li = level - 1;
-        ipcg_level_record &r = ix.records[li];
-        r.count = G.level[li].count;
-        for (int d = 0; d < 33; ++d) r.delta[d] = hs.delta[li][d];
-        r.outlier_offset = cursor;
-        r.outlier_count = hs.ocount[li];
-        r.outlier_length = hs.ocount[li] * (uint64_t)(8 + w);
-        cursor += r.outlier_length;
-        for (int p = 0; p < 32; ++p) {
-            r.plane_offset[p] = cursor;
-            r.plane_length[p] = 21 + hs.length[li][p];
-            cursor += r.plane_length[p];
-        }
+    // the archive, assembled on the device (assemble.cu): offsets by a device prefix sum, index,
+    // block headers, payload gather, outlier blocks compacted in ordinal order.  One readback at
+    // the end (the finished index); the host parses it like the reference's reader.
+    AsmParams P{};
+    P.scalar = scalar, P.interp = interp, P.nd = nd, P.levels = L, P.lp = lp, P.cap = (int)(uint8_t)cap;
+    for (int i = 0; i < nd; ++i) P.dims[i] = dims[i];
+    P.eb = eb;
+    for (int li = 0; li < L; ++li) P.count[li] = G.level[li].count;
+    std::vector<const uint32_t *> ofl(L);
+    std::vector<const uint64_t *> obt(L);
+    uint64_t max_tiles = 1;
+    for (int li = 0; li < L; ++li) {
+        ofl[li] = oflags.as<uint32_t>() + fbase[li];
+        obt[li] = bits.as<uint64_t>() + sink_base[li];
+        max_tiles = std::max<uint64_t>(max_tiles, ((G.level[li].count + 31) / 32 + 8191) / 8192);
     }
-    ix.payload_bytes = cursor;
-    const std::vector<uint8_t> index = serialize_index(ix);
-    ix.index_bytes = index.size();
-    ix.identity = crc32_host(index.data(), index.size());
-    const uint64_t total = index.size() + cursor;
-    tm.mark("index");
-
+    DBuf descs((size_t)L * 32 * sizeof(AsmDesc), st), aout(sizeof(AsmOut), st), tiles(max_tiles * 4, st);
     ipcg_archive *a = new ipcg_archive;
     a->device = c->device;
-    // stream-ordered: a cudaMalloc/cudaFree pair per call would synchronize the device
-    a->owned = static_cast<uint8_t *>(c->scratch.get(std::max<uint64_t>(total, 1), st));
     a->owner = st;
     a->pool = &c->scratch;
-    a->bytes = a->owned;
-    a->size = total;
     a->on_device = true;
-    a->ix = ix;
-    tm.mark("alloc");
-    // index + block headers staged in one pinned blob, payloads copied device-to-device
-    std::vector<uint8_t> blob(index.begin(), index.end());
-    std::vector<CopyDesc> descs;
-    std::vector<std::pair<uint64_t, uint64_t>> blob_spans;  // (blob offset, archive offset, len) for headers
-    blob_spans.push_back({0, 0});
-    const uint64_t payload0 = index.size();
-    for (int level = L; level >= 1; --level) {
-        const int li = level - 1;
-        const ipcg_level_record &r = ix.records[li];
-        for (int p = 0; p < 32; ++p) {
-            const uint64_t hb = blob.size();
-            const uint64_t len = hs.length[li][p];
-            uint8_t h[21];
-            h[0] = hs.backend[li][p];
-            for (int i = 0; i < 8; ++i) h[1 + i] = (uint8_t)(r.count >> (8 * i));
-            for (int i = 0; i < 8; ++i) h[9 + i] = (uint8_t)(len >> (8 * i));
-            for (int i = 0; i < 4; ++i) h[17 + i] = (uint8_t)(hs.crc[li][p] >> (8 * i));
-            blob.insert(blob.end(), h, h + 21);
-            descs.push_back(CopyDesc{nullptr, payload0 + r.plane_offset[p], 21});
-            blob_spans.push_back({hb, 21});
-            descs.push_back(CopyDesc{hs.payload[li][p], payload0 + r.plane_offset[p] + 21, len});
-        }
+    uint64_t capacity = asm_capacity(P);
+    AsmOut ho{};
+    for (int attempt = 0; attempt < 2; ++attempt) {
+        // stream-ordered pool memory: a cudaMalloc/cudaFree pair per call would synchronize the device
+        a->owned = static_cast<uint8_t *>(c->scratch.get(std::max<uint64_t>(capacity, 1), st));
+        launch_assemble(P, sd, a->owned, capacity, descs.as<AsmDesc>(), aout.as<AsmOut>(), ofl.data(), obt.data(),
+                        tiles.as<uint32_t>(), st);
+        readback(&ho, aout.p, sizeof(AsmOut), st);
+        tline.print();
+        if (ho.fits) break;
+        c->scratch.put(a->owned);  // more outliers than the 1/64 allowance: assemble again at the exact size
+        a->owned = nullptr;
+        capacity = ho.total;
     }
-    DBuf blob_d(blob.size(), st);
-    uint8_t *bh = static_cast<uint8_t *>(pinned(c, blob.size()));
-    std::memcpy(bh, blob.data(), blob.size());
-    CK(cudaMemcpyAsync(blob_d.p, bh, blob.size(), cudaMemcpyHostToDevice, st));
-    // index copy
-    std::vector<CopyDesc> all;
-    all.push_back(CopyDesc{blob_d.as<uint8_t>(), 0, index.size()});
-    size_t hi = 1;
-    for (CopyDesc &d : descs) {
-        if (!d.src) {
-            d.src = blob_d.as<uint8_t>() + blob_spans[hi].first;
-            ++hi;
-        }
-        all.push_back(d);
+    if (!ho.fits) {
+        delete a;
+        throw Error(ERUNTIME, "archive assembly overflow");
     }
-    CK(cudaStreamSynchronize(st));  // pinned blob consumed before reuse
-    gather(c, all, a->owned);
-    tm.mark("gather");
-    // outlier blocks, sorted by ordinal (pipeline.hpp:185-188)
-    uint64_t maxo = 0;
-    for (int l = 0; l < L; ++l) maxo = std::max<uint64_t>(maxo, hs.ocount[l]);
-    if (maxo) {
-        const size_t tb = sort_outliers_temp_bytes(maxo);
-        DBuf temp(tb, st), os(maxo * 8, st), bs(maxo * 8, st);
-        for (int level = L; level >= 1; --level) {
-            const int li = level - 1;
-            if (!hs.ocount[li]) continue;
-            const OutlierSink sink{&sd->ocount[li], ord.as<uint64_t>() + sink_base[li], bits.as<uint64_t>() + sink_base[li]};
-            launch_sort_outliers(sink, hs.ocount[li], os.as<uint64_t>(), bs.as<uint64_t>(), temp.p, tb, st);
-            launch_outlier_block(os.as<uint64_t>(), bs.as<uint64_t>(), &sd->ocount[li], scalar,
-                                 a->owned + payload0 + ix.records[li].outlier_offset, st);
-        }
+    tm.mark("assemble");
+    std::vector<uint8_t> index(ho.index_bytes);
+    readback(index.data(), a->owned, index.size(), st);
+    try {
+        parse_index(index.data(), index.size(), a->ix);  // also the identity (crc32 of the index)
+    } catch (...) {
+        c->scratch.put(a->owned);
+        delete a;
+        throw;
     }
-    CK(cudaStreamSynchronize(st));
-    tm.mark("outliers");
+    a->bytes = a->owned;
+    a->size = ho.total;
+    tm.mark("index");
     return a;
 }
 

@@ -1,7 +1,6 @@
 // numerics.cu -- sm_100a kernels for prediction, quantization, bitplanes, loss tables,
 // merge and reconstruction.  See numerics.cuh for the reference citations.
 #include <type_traits>
-#include <cub/device/device_radix_sort.cuh>
 
 #include "numerics.cuh"
 
@@ -203,9 +202,10 @@ __device__ __forceinline__ void quant_point(const T *__restrict__ values, T *__r
         nb[p.ordinal_base + i] = w;
         orv |= w;
         if (outl) {
-            const unsigned long long slot = atomicAdd(sink.count, 1ull);
-            sink.ordinal[slot] = p.ordinal_base + i;
-            sink.bits[slot] = bits_of<T>(v);
+            const uint64_t o = p.ordinal_base + i;
+            atomicAdd(sink.count, 1ull);
+            atomicOr(&sink.flags[o >> 5], 1u << (o & 31));
+            sink.bits[o] = bits_of<T>(v);
         }
     }
 }
@@ -327,19 +327,6 @@ __global__ void k_loss_finalize(const unsigned long long *rawbits, const uint32_
 }
 
 // ------------------------------------------------------------- outlier block
-// (u64 ordinal, T) pairs in ordinal order (pipeline.hpp:126-136)
-__global__ void k_outlier_block(const uint64_t *ord, const uint64_t *bits, const unsigned long long *count, int scalar,
-                                uint8_t *out) {
-    const uint64_t n = *count;
-    const int w = scalar == 0 ? 4 : 8, e = 8 + w;
-    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
-        uint8_t *dst = out + i * (uint64_t)e;
-        const uint64_t o = ord[i], b = bits[i];
-        for (int k = 0; k < 8; ++k) dst[k] = (uint8_t)(o >> (8 * k));
-        for (int k = 0; k < w; ++k) dst[8 + k] = (uint8_t)(b >> (8 * k));
-    }
-}
-
 // ------------------------------------------------------------------- merge
 // xor_decode + merge (bitplane.cpp:24-59), and refine's digit folding with the XOR
 // prefix taken from already-merged codewords (pipeline.hpp:328-339).  A CTA takes 32
@@ -517,9 +504,9 @@ __global__ void __launch_bounds__(kRowThreads) k_rows(T *__restrict__ state, Pas
             qz.nb[o] = w;
             orv |= w;
             if (outl) {
-                const unsigned long long slot = atomicAdd(qz.sink.count, 1ull);
-                qz.sink.ordinal[slot] = o;
-                qz.sink.bits[slot] = bits_of<T>(val[k]);
+                atomicAdd(qz.sink.count, 1ull);
+                atomicOr(&qz.sink.flags[o >> 5], 1u << (o & 31));
+                qz.sink.bits[o] = bits_of<T>(val[k]);
             }
         } else {
             e[k] = reconstruct_value<T>(pred, eb, (int64_t)from_negabinary(merged[o]));
@@ -747,26 +734,6 @@ void launch_zero_pass(double *dev, const PassDesc &pd, cudaStream_t st) {
 
 void launch_loss_finalize(const unsigned long long *rawbits, const uint32_t *lowor, double *delta, cudaStream_t st) {
     k_loss_finalize<<<1, 32, 0, st>>>(rawbits, lowor, delta);
-    CKL();
-}
-
-size_t sort_outliers_temp_bytes(uint64_t capacity) {
-    size_t bytes = 0;
-    cub::DeviceRadixSort::SortPairs(nullptr, bytes, (const uint64_t *)nullptr, (uint64_t *)nullptr,
-                                    (const uint64_t *)nullptr, (uint64_t *)nullptr, (int)capacity);
-    return bytes;
-}
-
-void launch_sort_outliers(OutlierSink sink, uint64_t count, uint64_t *ord_sorted, uint64_t *bits_sorted, void *temp,
-                          size_t temp_bytes, cudaStream_t st) {
-    if (count == 0) return;
-    CK(cub::DeviceRadixSort::SortPairs(temp, temp_bytes, sink.ordinal, ord_sorted, sink.bits, bits_sorted, (int)count,
-                                       0, 64, st));
-}
-
-void launch_outlier_block(const uint64_t *ord_sorted, const uint64_t *bits_sorted, const unsigned long long *count,
-                          int scalar, uint8_t *out, cudaStream_t st) {
-    k_outlier_block<<<64, 256, 0, st>>>(ord_sorted, bits_sorted, count, scalar, out);
     CKL();
 }
 

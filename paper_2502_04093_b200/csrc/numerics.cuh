@@ -19,9 +19,12 @@ __host__ __device__ __forceinline__ uint32_t to_negabinary(int32_t q) {
 }
 __host__ __device__ __forceinline__ int32_t from_negabinary(uint32_t w) { return (int32_t)((w ^ kNbMask) - kNbMask); }
 
+// a level's escaped points (pipeline.hpp:184-188): flags bit o = the point of ordinal o is an
+// outlier, bits[o] = its exact value's bit pattern; count totals them.  The outlier block is
+// compacted in ordinal order from the bitmap (assemble.cu), so no sort is needed.
 struct OutlierSink {
     unsigned long long *count;
-    uint64_t *ordinal;
+    uint32_t *flags;
     uint64_t *bits;
 };
 
@@ -40,11 +43,6 @@ void launch_zero_pass(double *dev, const PassDesc &pd, cudaStream_t st);
 bool launch_loss_fused(const uint32_t *nb, const Geometry &G, int level, bool cubic, double unit,
                        const uint32_t *lowor, unsigned long long *raw, cudaStream_t st);
 void launch_loss_finalize(const unsigned long long *rawbits, const uint32_t *lowor, double *delta, cudaStream_t st);
-void launch_sort_outliers(OutlierSink sink, uint64_t count, uint64_t *ord_sorted, uint64_t *bits_sorted,
-                          void *temp, size_t temp_bytes, cudaStream_t st);
-size_t sort_outliers_temp_bytes(uint64_t capacity);
-void launch_outlier_block(const uint64_t *ord_sorted, const uint64_t *bits_sorted, const unsigned long long *count,
-                          int scalar, uint8_t *out, cudaStream_t st);
 
 // rows: device array of 32 plane-row pointers (rows[p] used for k0 <= p < k1)
 void launch_merge(const uint32_t *const *rows, const uint32_t *merged_in, uint32_t *merged_out, uint64_t count, int k0,
