@@ -1639,11 +1639,8 @@ void DeflateBatch::run(const uint8_t *in, uint64_t in_stride, int S, uint64_t n,
     if (n > 0) {
         const uint64_t nblk = (n + WSIZE - 1) / WSIZE;
         const size_t smem = (size_t)PL_WARPS * 32768 * sizeof(uint16_t);
-        static bool attr = false;
-        if (!attr) {
+        if (first_on_device<1>())
             CK(cudaFuncSetAttribute(k_prevlinks, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-            attr = true;
-        }
         {
         ProfScope ps1("deflate.prevlinks", st, (uint64_t)S * n);
         static int span_env = getenv("IPCG_PL_SPAN") ? atoi(getenv("IPCG_PL_SPAN")) : 0;

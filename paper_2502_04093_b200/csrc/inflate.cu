@@ -1424,13 +1424,12 @@ void inflate_batch_host(const std::vector<InflateJob> &jobs, int *status_dev, De
             CK(cudaMemsetAsync(changed, 0, 4 * sizeof(unsigned) + 8, st));
             uint64_t mcap = std::max<uint64_t>(1 << 20, max_dst * (uint64_t)n / 32);  // marked bytes listed
             uint64_t *mlist = static_cast<uint64_t *>(alloc.get(mcap * 8, st));
-            static int coop_blocks = 0;
+            static int coop_cache[64] = {0};  // per device
+            int &coop_blocks = coop_cache[current_device() & 63];
             if (!coop_blocks) {
-                int dev = 0, sms = 0, per = 0;
-                CK(cudaGetDevice(&dev));
-                CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+                int per = 0;
                 CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_resolve_all, 256, 0));
-                coop_blocks = sms * std::max(1, std::min(per, 4));
+                coop_blocks = num_sms() * std::max(1, std::min(per, 4));
             }
             int nj = n;
             void *args[] = {(void *)&jd, (void *)&td, (void *)&md, (void *)&nj, (void *)&changed, (void *)&mlist,

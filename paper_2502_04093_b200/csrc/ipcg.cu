@@ -80,6 +80,8 @@ struct ipcg_ctx {
     std::vector<cudaEvent_t> events;
     size_t events_used = 0;
     ScratchPool scratch;  // per-call device scratch, reused across calls (also archive/session memory)
+    Profiler prof;        // per-family timing (ipcg_profile_enable)
+    unsigned long long launches = 0;  // kernels this context launched (ipcg_kernel_launches)
     std::string err;
     void *pinned = nullptr;
     size_t pinned_cap = 0;
@@ -252,10 +254,21 @@ thread_local std::string g_host_err;  // errors of context-free (host-only) call
 template <class F>
 int guarded(ipcg_ctx *c, F &&f) {
     std::string &err = c ? c->err : g_host_err;
-    struct Bind {  // this call's scratch pool
+    struct Bind {  // this call's scratch pool, profiler and launch counter
         ScratchPool *prev;
-        explicit Bind(ipcg_ctx *c) : prev(current_scratch()) { current_scratch() = c ? &c->scratch : nullptr; }
-        ~Bind() { current_scratch() = prev; }
+        Profiler *prev_prof;
+        unsigned long long *prev_launches;
+        explicit Bind(ipcg_ctx *c)
+            : prev(current_scratch()), prev_prof(current_profiler()), prev_launches(current_launches()) {
+            current_scratch() = c ? &c->scratch : nullptr;
+            current_profiler() = c ? &c->prof : nullptr;
+            current_launches() = c ? &c->launches : nullptr;
+        }
+        ~Bind() {
+            current_scratch() = prev;
+            current_profiler() = prev_prof;
+            current_launches() = prev_launches;
+        }
     } bind(c);
     try {
         if (c) CK(cudaSetDevice(c->device));
@@ -1805,12 +1818,12 @@ int ipcg_merge(ipcg_ctx *c, const uint8_t *const *planes, uint64_t count, int k,
     });
 }
 
-uint64_t ipcg_kernel_launches(const ipcg_ctx *) { return launch_counter(); }
+uint64_t ipcg_kernel_launches(const ipcg_ctx *c) { return c ? c->launches : launch_counter(); }
 
 int ipcg_profile_enable(ipcg_ctx *c, int enable) {
     return guarded(c, [&] {
         CK(cudaStreamSynchronize(c->stream));
-        Profiler &p = profiler();
+        Profiler &p = c->prof;
         for (auto &r : p.recs) p.pool.push_back(r.a), p.pool.push_back(r.b);
         p.recs.clear();
         p.enabled = enable != 0;
@@ -1821,7 +1834,7 @@ int ipcg_profile_enable(ipcg_ctx *c, int enable) {
 int ipcg_profile_read(ipcg_ctx *c, char *json, uint64_t capacity) {
     return guarded(c, [&] {
         CK(cudaStreamSynchronize(c->stream));
-        Profiler &p = profiler();
+        Profiler &p = c->prof;
         std::vector<std::string> names;
         std::vector<double> ms;
         std::vector<uint64_t> cnt, bytes;

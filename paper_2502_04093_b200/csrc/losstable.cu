@@ -439,11 +439,9 @@ bool launch_loss_fused(const uint32_t *nb, const Geometry &G, int level, bool cu
     uint64_t ntiles, region;
     if (!tile_geom(G, level, tiles, g, ntiles, region)) return false;
     const size_t smem = region * (2 * 8 + 4 + 2) + 64;
-    static bool attr = false;
-    if (!attr) {
+    if (first_on_device<2>()) {
         CK(cudaFuncSetAttribute(k_loss_fused<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
         CK(cudaFuncSetAttribute(k_loss_fused<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-        attr = true;
     }
     if (cubic) k_loss_fused<true><<<(unsigned)ntiles, LT_THREADS, smem, st>>>(nb, g, unit, lowor, raw);
     else k_loss_fused<false><<<(unsigned)ntiles, LT_THREADS, smem, st>>>(nb, g, unit, lowor, raw);

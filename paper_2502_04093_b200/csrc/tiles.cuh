@@ -1,5 +1,5 @@
 // tiles.cuh -- box-plus-halo tiling of one level's lattice, shared by the fused loss-table
-// (losstable.cu) and reconstruction (recon_fused.cu) kernels.  A CTA owns a box of the
+// kernel (losstable.cu, 4-D grids and the smem-tile variant).  A CTA owns a box of the
 // level's lattice (coordinates in units of the level stride s) plus a 3-point halo along
 // every axis after the first; pass j is evaluated on the box widened by the halo along the
 // axes > j, so every level point is produced by exactly one box.

@@ -28,10 +28,31 @@ struct Error : std::runtime_error {
         cudaError_t _e = (x);                                          \
         if (_e != cudaSuccess) ::ipcg::throw_cuda(_e, #x, __FILE__, __LINE__); \
     } while (0)
-// every kernel launch goes through CKL(): checks the launch and counts it
+// every kernel launch goes through CKL(): checks the launch and counts it on the counter of
+// the context whose API call runs on this thread (ipcg_kernel_launches); a process-wide one
+// outside any call
+inline unsigned long long *&current_launches() {
+    thread_local unsigned long long *p = nullptr;
+    return p;
+}
 inline unsigned long long &launch_counter() {
-    static unsigned long long c = 0;
-    return c;
+    static unsigned long long global = 0;
+    unsigned long long *c = current_launches();
+    return c ? *c : global;
+}
+inline int current_device() {
+    int d = 0;
+    cudaGetDevice(&d);
+    return d;
+}
+// true the first time it is called for the current device (per-device one-time setup such as
+// cudaFuncSetAttribute, which applies to the device current when it is called)
+template <int Slot>
+inline bool first_on_device() {
+    static unsigned long long mask = 0;  // devices 0..63
+    const unsigned long long bit = 1ull << (current_device() & 63);
+    const bool first = !(__atomic_fetch_or(&mask, bit, __ATOMIC_RELAXED) & bit);
+    return first;
 }
 #define CKL()                              \
     do {                                   \
@@ -67,9 +88,15 @@ struct Profiler {
         return e;
     }
 };
-inline Profiler &profiler() {
-    static Profiler p;
+// the profiler of the context whose API call runs on this thread (a process-wide one otherwise)
+inline Profiler *&current_profiler() {
+    thread_local Profiler *p = nullptr;
     return p;
+}
+inline Profiler &profiler() {
+    static Profiler global;
+    Profiler *p = current_profiler();
+    return p ? *p : global;
 }
 struct ProfScope {
     int idx = -1;
@@ -150,15 +177,16 @@ struct DevAlloc {
     }
 };
 
-// SM count of the current device (cached; one device per process, see include/ipcomp_b200.h)
+// SM count of the current device (cached per device)
 inline int num_sms() {
-    static int sms = [] {
-        int dev = 0, v = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
-        return v > 0 ? v : 148;
-    }();
-    return sms;
+    static int cache[64] = {0};
+    const int dev = current_device() & 63;
+    if (!cache[dev]) {
+        int v = 0;
+        cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, current_device());
+        cache[dev] = v > 0 ? v : 148;
+    }
+    return cache[dev];
 }
 
 inline unsigned grid_for(uint64_t n, unsigned block, unsigned cap = 148u * 32u) {
