@@ -135,6 +135,15 @@ def barrier(ws: int):
         dist.barrier()
 
 
+def refine_plan(reader, session, target):
+    """plan_for_error's plan for `target`, never dropping a plane the session holds (planner plans
+    for decreasing targets are usually but not necessarily nested; refine_field requires it)"""
+    import paper_2502_04093_b200 as ipc
+
+    k = ipc.plan_for_error(reader, target).k
+    return ipc.RetrievalPlan([max(a, b) for a, b in zip(k, session.planes_loaded())])
+
+
 def retrieval_targets(cfg: int):
     return synth.CONFIGS[cfg]["retrieve"].get("rel", [1e-2])
 
@@ -163,7 +172,7 @@ def run_ours(args, ws, rank, local):
         rng = reader.header().range
         out = ipc.reconstruct_field(reader, ipc.plan_for_error(reader, rels[0] * rng), device=True)
         for rel in rels[1:]:
-            out = ipc.refine_field(reader, out.session, out.values, ipc.plan_for_error(reader, rel * rng))
+            out = ipc.refine_field(reader, out.session, out.values, refine_plan(reader, out.session, rel * rng))
         return reader, out
 
     # correctness guard on the benchmarked workload itself: full-fidelity bound holds
@@ -303,7 +312,7 @@ def run_ours(args, ws, rank, local):
             rng_ = rh.header().range
             o = ipc.reconstruct_field(rh, ipc.plan_for_error(rh, rels[0] * rng_), out=host_out)
             for rel in rels[1:]:
-                o = ipc.refine_field(rh, o.session, host_out, ipc.plan_for_error(rh, rel * rng_), out=host_out)
+                o = ipc.refine_field(rh, o.session, host_out, refine_plan(rh, o.session, rel * rng_), out=host_out)
             h2d = nbytes + rh.payload_bytes_read()
             d2h = size + nbytes * len(rels)
             return o
@@ -365,18 +374,19 @@ def cpu_model():
     return "unknown"
 
 
-def reference_cycle(ref, v, d, c, eb, rels):
-    """compress + progressive retrieve chain with the reference's own CPU code."""
+def reference_cycle(ref, v, d, c, eb, rels, rng=None):
+    """compress + progressive retrieve chain with the reference's own CPU code; retrieval targets
+    are rel x rng (the workload field's range when v is a sample of it, else v's archive range)."""
     t0 = time.perf_counter()
     arch = ref.compress(v, d, eb, c["interp"])
-    import oracle
+    if rng is None:
+        import oracle
 
-    info = oracle.load("oracle").info(arch)
-    rng = info.range
+        rng = oracle.load("oracle").info(arch).range
     k = ref.plan_for_error(arch, rels[0] * rng)
     vals, merged, _ = ref.reconstruct(arch, k, v.dtype, v.size)
     for rel in rels[1:]:
-        k2 = ref.plan_for_error(arch, rel * rng)
+        k2 = [max(a, b) for a, b in zip(ref.plan_for_error(arch, rel * rng), k)]  # as bench's refine_plan
         vals, merged, _ = ref.refine(arch, k, merged, vals, k2)
         k = k2
     return time.perf_counter() - t0, len(arch)
@@ -431,11 +441,12 @@ def run_reference(args, ws, rank):
     v, d = _sample(f, dims)
     eb = synth.abs_eb(f, c["rel_eb"])  # the workload's eb (range of the whole field)
     rels = retrieval_targets(args.config)
+    rng = float(f.max()) - float(f.min())
     for _ in range(args.warmup):
-        reference_cycle(ref, v, d, c, eb, rels)
+        reference_cycle(ref, v, d, c, eb, rels, rng)
     times = []
     for _ in range(args.steps):
-        t, _ = reference_cycle(ref, v, d, c, eb, rels)
+        t, _ = reference_cycle(ref, v, d, c, eb, rels, rng)
         times.append(t)
     total = sum(times)
     value = v.nbytes * args.steps / total / 1e9
