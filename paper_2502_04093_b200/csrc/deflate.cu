@@ -1619,7 +1619,8 @@ void crc32_batch(const uint8_t *const *ptrs, const uint64_t *lens, int S, uint64
 }
 
 void DeflateBatch::run(const uint8_t *in, uint64_t in_stride, int S, uint64_t n, uint8_t *out, uint64_t out_stride,
-                       void *workspace, BackendResults res, cudaStream_t st, cudaEvent_t after_match) {
+                       void *workspace, BackendResults res, cudaStream_t st, cudaEvent_t after_match,
+                       cudaStream_t side, cudaEvent_t fork, cudaEvent_t join) {
     if ((in_stride & 15) || (reinterpret_cast<uintptr_t>(in) & 15))
         throw Error(EINVAL_, "deflate input rows must be 16-byte aligned with a 16-byte multiple stride");
     Work w = carve(workspace, S, n);
@@ -1659,42 +1660,47 @@ void DeflateBatch::run(const uint8_t *in, uint64_t in_stride, int S, uint64_t n,
         }
         // sparse streams (meta.od, k_select) take the on-demand parse, the others the all-position
         // search; each kernel below skips the streams of the other path
+        const bool forked = side && fork && join && n < (1ull << 31);
+        const cudaStream_t ost = forked ? side : st;  // the on-demand parse's stream
+        if (forked) {
+            CK(cudaEventRecord(fork, st));
+            CK(cudaStreamWaitEvent(side, fork, 0));
+        }
         if (n < (1ull << 31)) {
             const uint32_t nch = (uint32_t)w.od_nch;
             {
-            ProfScope ps2("deflate.walk", st, (uint64_t)S * n);
-            CK(cudaMemsetAsync(w.od_vis, 0, (size_t)S * n * sizeof(uint16_t), st));
-            k_od_chg<<<dim3((unsigned)((w.od_ng + 255) / 256), S), 256, 0, st>>>(in, in_stride, (uint32_t)n, w.meta,
+            ProfScope ps2("deflate.walk", ost, (uint64_t)S * n);
+            CK(cudaMemsetAsync(w.od_vis, 0, (size_t)S * n * sizeof(uint16_t), ost));
+            k_od_chg<<<dim3((unsigned)((w.od_ng + 255) / 256), S), 256, 0, ost>>>(in, in_stride, (uint32_t)n, w.meta,
                                                                              w.od_ng, w.od_chg);
             CKL();
-            k_od_chg_suffix<<<S, 1024, 0, st>>>((uint32_t)n, w.meta, w.od_ng, w.od_chg);
+            k_od_chg_suffix<<<S, 1024, 0, ost>>>((uint32_t)n, w.meta, w.od_ng, w.od_chg);
             CKL();
-            k_od_walk<<<dim3((nch + 127) / 128, S), 128, 0, st>>>(in, in_stride, (uint32_t)n, w.meta, w.prevd, w.od_C,
+            k_od_walk<<<dim3((nch + 127) / 128, S), 128, 0, ost>>>(in, in_stride, (uint32_t)n, w.meta, w.prevd, w.od_C,
                                                                   nch, w.od_vis, w.od_ssym, w.od_spos, w.od_chunks);
             CKL();
             }
-            if (after_match) CK(cudaEventRecord(after_match, st));
             {
-            ProfScope ps3("deflate.sync", st, (uint64_t)S * n);
-            k_od_sync<<<dim3((nch + 127) / 128, S), 128, 0, st>>>(in, in_stride, (uint32_t)n, w.meta, w.prevd, w.od_C,
+            ProfScope ps3("deflate.sync", ost, (uint64_t)S * n);
+            k_od_sync<<<dim3((nch + 127) / 128, S), 128, 0, ost>>>(in, in_stride, (uint32_t)n, w.meta, w.prevd, w.od_C,
                                                                   nch, w.od_vis, w.od_chg, w.od_ng, w.od_chunks,
                                                                   w.od_cbuf, w.od_link);
             CKL();
             }
             {
-            ProfScope ps3c("deflate.chain", st, (uint64_t)S * n);
+            ProfScope ps3c("deflate.chain", ost, (uint64_t)S * n);
             const unsigned nsc = (unsigned)w.od_nsc;
-            k_od_sc_jump<<<dim3(nsc, S), OD_SC, 0, st>>>(w.meta, nch, nsc, w.od_link, w.od_sc);
+            k_od_sc_jump<<<dim3(nsc, S), OD_SC, 0, ost>>>(w.meta, nch, nsc, w.od_link, w.od_sc);
             CKL();
-            k_od_sc_walk<<<(S + 31) / 32, 32, 0, st>>>(in, in_stride, (uint32_t)n, w.meta, S, nch, nsc, w.od_sc,
+            k_od_sc_walk<<<(S + 31) / 32, 32, 0, ost>>>(in, in_stride, (uint32_t)n, w.meta, S, nch, nsc, w.od_sc,
                                                       w.od_entry, w.syms, w.maxb, w.blk_start);
             CKL();
-            k_od_sc_mark<<<dim3((nsc + 3) / 4, S), 128, 0, st>>>(w.meta, nch, nsc, w.od_link, w.od_entry, w.od_chunks);
+            k_od_sc_mark<<<dim3((nsc + 3) / 4, S), 128, 0, ost>>>(w.meta, nch, nsc, w.od_link, w.od_entry, w.od_chunks);
             CKL();
             }
             {
-            ProfScope ps3("deflate.place", st, (uint64_t)S * n);
-            k_od_place<<<dim3((nch + 3) / 4, S), 128, 0, st>>>(in, in_stride, (uint32_t)n, w.meta, w.prevd, w.od_C, nch,
+            ProfScope ps3("deflate.place", ost, (uint64_t)S * n);
+            k_od_place<<<dim3((nch + 3) / 4, S), 128, 0, ost>>>(in, in_stride, (uint32_t)n, w.meta, w.prevd, w.od_C, nch,
                                                                w.od_vis, w.od_ssym, w.od_spos, w.od_chg, w.od_ng,
                                                                w.od_chunks, w.od_cbuf, w.syms, w.maxb, w.blk_top,
                                                                w.blk_start);
@@ -1749,6 +1755,10 @@ void DeflateBatch::run(const uint8_t *in, uint64_t in_stride, int S, uint64_t n,
             k_emit_runs<<<148 * 4, 256, 0, st>>>(n, w.rec, w.syms, w.maxb, w.blk_top, w.blk_start, w.runs, w.nruns);
             CKL();
             }
+        }
+        if (forked) {
+            CK(cudaEventRecord(join, side));
+            CK(cudaStreamWaitEvent(st, join, 0));
         }
         {
         ProfScope ps4("deflate.blocks", st, (uint64_t)S * n);

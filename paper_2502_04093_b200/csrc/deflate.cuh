@@ -23,8 +23,12 @@ struct DeflateBatch {
     static size_t workspace_bytes(int S, uint64_t n);
     // after_match (optional): recorded on `st` once the match search is enqueued, so a caller
     // can start other work when the throughput-bound phases are over
+    // side (optional): a second stream the on-demand parse of the sparse streams runs on, concurrent
+    // with the all-position search of the others on `st` (joined before the block plans); fork/join
+    // are two caller-owned events
     static void run(const uint8_t *in, uint64_t in_stride, int S, uint64_t n, uint8_t *out, uint64_t out_stride,
-                    void *workspace, BackendResults res, cudaStream_t st, cudaEvent_t after_match = nullptr);
+                    void *workspace, BackendResults res, cudaStream_t st, cudaEvent_t after_match = nullptr,
+                    cudaStream_t side = nullptr, cudaEvent_t fork = nullptr, cudaEvent_t join = nullptr);
 };
 
 // standalone CRC-32 (zlib polynomial) of S (ptr, len) device ranges

@@ -77,6 +77,7 @@ struct ipcg_ctx {
     cudaStream_t own_stream = nullptr;
     std::vector<cudaStream_t> side;  // fork targets (per-level chains)
     std::vector<cudaStream_t> loss;  // per-level loss-table streams (highest priority)
+    std::vector<cudaStream_t> odside;  // per-level streams of the deflate on-demand parse
     std::vector<cudaEvent_t> events;
     size_t events_used = 0;
     ScratchPool scratch;  // per-call device scratch, reused across calls (also archive/session memory)
@@ -189,6 +190,17 @@ cudaStream_t loss_stream(ipcg_ctx *c, size_t i) {
         c->loss.push_back(s);
     }
     return c->loss[i];
+}
+
+// level li's on-demand-parse stream (level 1, throughput-bound, at the lowest priority like its
+// main deflate chain; the latency-bound coarser levels at the highest)
+cudaStream_t od_stream(ipcg_ctx *c, size_t li) {
+    while (c->odside.size() <= li) {
+        cudaStream_t s;
+        CK(cudaStreamCreateWithPriority(&s, cudaStreamNonBlocking, prio_for(c->odside.size() == 0)));
+        c->odside.push_back(s);
+    }
+    return c->odside[li];
 }
 
 // an event from the context's pool (reused across calls: a wait captures the event's
@@ -495,8 +507,10 @@ ipcg_archive *compress_impl(ipcg_ctx *c, int scalar, const void *values, int on_
             tline.ev.push_back({"m" + std::to_string(level), after_match});
         }
         const BackendResults res{sd->backend[li], sd->length[li], sd->crc[li], sd->payload[li]};
+        cudaStream_t os = serial ? nullptr : od_stream(c, (size_t)li);
         DeflateBatch::run(planes[li].as<uint8_t>(), plane_stride[li] * 4, 32, pb[li], outs[li].as<uint8_t>(),
-                          out_stride[li], wss[li].p, res, ds, after_match);
+                          out_stride[li], wss[li].p, res, ds, after_match, os, os ? pool_event(c) : nullptr,
+                          os ? pool_event(c) : nullptr);
         tline.mark("d" + std::to_string(level), ds);
         // loss table (measure_loss_table): replay per dropped-digit count d, on the level's own
         // highest-priority stream, started once this level's match search is done so it
@@ -1082,12 +1096,14 @@ void ipcg_ctx_destroy(ipcg_ctx *c) {
     if (c->stream) cudaStreamSynchronize(c->stream);
     for (cudaStream_t s : c->side) cudaStreamSynchronize(s);
     for (cudaStream_t s : c->loss) cudaStreamSynchronize(s);
+    for (cudaStream_t s : c->odside) cudaStreamSynchronize(s);
     c->scratch.release_all(c->own_stream);
     if (c->own_stream) cudaStreamSynchronize(c->own_stream);
     if (c->pinned) cudaFreeHost(c->pinned);
     if (c->src_pinned) cudaFreeHost(c->src_pinned);
     for (cudaStream_t s : c->side) cudaStreamDestroy(s);
     for (cudaStream_t s : c->loss) cudaStreamDestroy(s);
+    for (cudaStream_t s : c->odside) cudaStreamDestroy(s);
     for (cudaEvent_t e : c->events) cudaEventDestroy(e);
     if (c->own_stream) cudaStreamDestroy(c->own_stream);
     delete c;
