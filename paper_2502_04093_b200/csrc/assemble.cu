@@ -9,6 +9,8 @@
 namespace ipcg {
 namespace {
 
+constexpr uint64_t ASM_PIECE_H = 64 << 10;  // gather piece (k_asm_gather)
+
 __device__ __forceinline__ void put_le(uint8_t *p, uint64_t v, int nb) {
     for (int i = 0; i < nb; ++i) p[i] = (uint8_t)(v >> (8 * i));
 }
@@ -84,35 +86,50 @@ __global__ void k_asm_layout(AsmParams P, const AsmSmall *sm, uint8_t *arch, uin
         put_le(h + 17, sm->crc[li][p], 4);
         descs[li * 32 + p] = AsmDesc{sm->payload[li][p], index_bytes + off[li][1 + p] + 21, sm->length[li][p]};
     }
+    // piece prefix over the descriptors (level-major, plane order) for k_asm_gather
+    __syncwarp();
+    if (lane == 0) {
+        uint64_t acc = 0;
+        for (int d = 0; d < L * 32; ++d) {
+            out->pieces[d] = acc;
+            acc += (sm->length[d / 32][d % 32] + ASM_PIECE_H - 1) / ASM_PIECE_H;
+        }
+        out->pieces[L * 32] = acc;
+    }
 }
 
-// payload copies: every CTA walks the descriptors, taking its share of each one's 64 KiB pieces
-// (word-aligned destination stores, funnel-shifted source words as k_gather does)
+// payload copies: 64 KiB pieces of all descriptors numbered consecutively (piece prefix from
+// k_asm_layout), one CTA per piece in a grid-stride loop; word-aligned destination stores of
+// funnel-shifted source words, as k_gather does
+constexpr uint64_t ASM_PIECE = ASM_PIECE_H;
 __global__ void __launch_bounds__(256) k_asm_gather(const AsmDesc *descs, int nd, const AsmOut *out, uint8_t *arch) {
     if (!out->fits) return;
-    constexpr uint64_t PIECE = 64 << 10;
-    for (int d = 0; d < nd; ++d) {
-        const AsmDesc c = descs[d];
-        const uint64_t np = (c.len + PIECE - 1) / PIECE;
-        for (uint64_t q = blockIdx.x; q < np; q += gridDim.x) {
-            const uint64_t a = q * PIECE, len = min(PIECE, c.len - a);
-            uint8_t *o = arch + c.dst + a;
-            const uint8_t *s = c.src + a;
-            const uint64_t head = min(len, (uint64_t)((4 - ((uintptr_t)o & 3)) & 3));
-            if (threadIdx.x < head) o[threadIdx.x] = s[threadIdx.x];
-            const uint8_t *s2 = s + head;
-            uint8_t *o2 = o + head;
-            const uint64_t rem = len - head, nw = rem / 4;
-            const unsigned sh = (unsigned)((uintptr_t)s2 & 3) * 8;
-            const uint32_t *sw = reinterpret_cast<const uint32_t *>((uintptr_t)s2 & ~uintptr_t(3));
-            uint32_t *ow = reinterpret_cast<uint32_t *>(o2);
-            if (sh == 0) {
-                for (uint64_t k = threadIdx.x; k < nw; k += blockDim.x) ow[k] = sw[k];
-            } else {
-                for (uint64_t k = threadIdx.x; k < nw; k += blockDim.x) ow[k] = __funnelshift_r(sw[k], sw[k + 1], sh);
-            }
-            for (uint64_t k = nw * 4 + threadIdx.x; k < rem; k += blockDim.x) o2[k] = s2[k];
+    const uint64_t total = out->pieces[nd];
+    for (uint64_t g = blockIdx.x; g < total; g += gridDim.x) {
+        int lo = 0, hi = nd - 1;  // descriptor of piece g: last d with pieces[d] <= g
+        while (lo < hi) {
+            const int mid = (lo + hi + 1) / 2;
+            if (out->pieces[mid] <= g) lo = mid;
+            else hi = mid - 1;
         }
+        const AsmDesc c = descs[lo];
+        const uint64_t a = (g - out->pieces[lo]) * ASM_PIECE, len = min(ASM_PIECE, c.len - a);
+        uint8_t *o = arch + c.dst + a;
+        const uint8_t *s = c.src + a;
+        const uint64_t head = min(len, (uint64_t)((4 - ((uintptr_t)o & 3)) & 3));
+        if (threadIdx.x < head) o[threadIdx.x] = s[threadIdx.x];
+        const uint8_t *s2 = s + head;
+        uint8_t *o2 = o + head;
+        const uint64_t rem = len - head, nw = rem / 4;
+        const unsigned sh = (unsigned)((uintptr_t)s2 & 3) * 8;
+        const uint32_t *sw = reinterpret_cast<const uint32_t *>((uintptr_t)s2 & ~uintptr_t(3));
+        uint32_t *ow = reinterpret_cast<uint32_t *>(o2);
+        if (sh == 0) {
+            for (uint64_t k = threadIdx.x; k < nw; k += blockDim.x) ow[k] = sw[k];
+        } else {
+            for (uint64_t k = threadIdx.x; k < nw; k += blockDim.x) ow[k] = __funnelshift_r(sw[k], sw[k + 1], sh);
+        }
+        for (uint64_t k = nw * 4 + threadIdx.x; k < rem; k += blockDim.x) o2[k] = s2[k];
     }
 }
 
@@ -221,7 +238,7 @@ void launch_assemble(const AsmParams &P, const AsmSmall *sm, uint8_t *arch, uint
                      cudaStream_t st) {
     k_asm_layout<<<1, 32, 0, st>>>(P, sm, arch, capacity, descs, out);
     CKL();
-    k_asm_gather<<<(unsigned)num_sms() * 4, 256, 0, st>>>(descs, P.levels * 32, out, arch);
+    k_asm_gather<<<(unsigned)num_sms() * 8, 256, 0, st>>>(descs, P.levels * 32, out, arch);
     CKL();
     for (int li = 0; li < P.levels; ++li) {
         const uint64_t words = (P.count[li] + 31) / 32, ntiles = (words + OT_WORDS - 1) / OT_WORDS;

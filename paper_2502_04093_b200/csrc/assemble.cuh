@@ -39,6 +39,7 @@ struct AsmOut {
     uint64_t total, index_bytes;
     uint64_t outlier_dst[IPCG_MAX_LEVELS];
     int fits;
+    uint64_t pieces[IPCG_MAX_LEVELS * 32 + 1];  // gather pieces before each descriptor
 };
 
 // worst-case archive size for the device assembly (outliers capped at 1/64 of each level)
