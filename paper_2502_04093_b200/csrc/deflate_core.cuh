@@ -556,30 +556,32 @@ struct BlockTrees {
 
 // zlib's heap orders nodes by smaller(n, m) = freq[n] < freq[m] || (freq[n] == freq[m] &&
 // depth[n] <= depth[m]), i.e. (freq, depth) compared lexicographically with ties counting as
-// "smaller".  Heap entries pack freq << 18 | depth << 10 | node so one load gives the whole
-// key (depth is zlib's uch and wraps the same way).  heap[heap_max..] then holds the nodes
-// in zlib's order for gen_bitlen.
+// "smaller".  Heap entries pack freq << 17 | depth << 10 | node into 32 bits so one load gives
+// the whole key: a block's frequencies sum to at most 16384 (16383 symbols + END_BLOCK), and a
+// Huffman tree over a total weight <= 16384 is at most ~21 levels deep, so zlib's uch depth never
+// reaches the 7 bits kept here.  heap[heap_max..] then holds the nodes in zlib's order for
+// gen_bitlen.
 struct TreeScratch {
     uint16_t freq[HEAP_SIZE];     // leaf frequencies (input; forced leaves set to 1)
     uint16_t dad_len[HEAP_SIZE];  // zlib's dl union: Dad during build, Len after gen_bitlen
-    uint64_t heap[HEAP_SIZE];
+    uint32_t heap[HEAP_SIZE];
     uint16_t bl_count[MAX_BITS + 1];
     int heap_len, heap_max;
 };
 
-HD uint64_t hmake(uint64_t freq, uint32_t depth, int node) {
-    return (freq << 18) | ((uint64_t)(depth & 0xff) << 10) | (uint64_t)node;
+HD uint32_t hmake(uint32_t freq, uint32_t depth, int node) {
+    return (freq << 17) | ((depth & 0x7f) << 10) | (uint32_t)node;
 }
-HD uint64_t hkey(uint64_t e) { return e >> 10; }
-HD int hnode(uint64_t e) { return (int)(e & 1023); }
+HD uint32_t hkey(uint32_t e) { return e >> 10; }
+HD int hnode(uint32_t e) { return (int)(e & 1023); }
 
 HD void pqdownheap(TreeScratch &t, int k) {
-    const uint64_t v = t.heap[k];
+    const uint32_t v = t.heap[k];
     int j = k << 1;
     while (j <= t.heap_len) {
-        uint64_t hj = t.heap[j];
+        uint32_t hj = t.heap[j];
         if (j < t.heap_len) {
-            const uint64_t hj1 = t.heap[j + 1];
+            const uint32_t hj1 = t.heap[j + 1];
             if (hkey(hj1) <= hkey(hj)) j++, hj = hj1;
         }
         if (hkey(v) <= hkey(hj)) break;
@@ -617,15 +619,15 @@ HD int build_tree(TreeScratch &t, int kind, int elems, uint8_t *len_out, uint16_
     for (int n = t.heap_len / 2; n >= 1; n--) pqdownheap(t, n);
     int node = elems;
     do {
-        const uint64_t en = t.heap[1];  // pqremove
+        const uint32_t en = t.heap[1];  // pqremove
         t.heap[1] = t.heap[t.heap_len--];
         pqdownheap(t, 1);
-        const uint64_t em = t.heap[1];
+        const uint32_t em = t.heap[1];
         t.heap[--t.heap_max] = en;
         t.heap[--t.heap_max] = em;
-        const uint32_t dn = (uint32_t)(en >> 10) & 0xff, dm = (uint32_t)(em >> 10) & 0xff;
+        const uint32_t dn = (en >> 10) & 0x7f, dm = (em >> 10) & 0x7f;
         t.dad_len[hnode(en)] = t.dad_len[hnode(em)] = (uint16_t)node;
-        t.heap[1] = hmake((en >> 18) + (em >> 18), (dn >= dm ? dn : dm) + 1, node++);
+        t.heap[1] = hmake((en >> 17) + (em >> 17), (dn >= dm ? dn : dm) + 1, node++);
         pqdownheap(t, 1);
     } while (t.heap_len >= 2);
     t.heap[--t.heap_max] = t.heap[1];
