@@ -1635,7 +1635,12 @@ void DeflateBatch::run(const uint8_t *in, uint64_t in_stride, int S, uint64_t n,
     }
     static const int od_mode = getenv("IPCG_OD_MODE") ? atoi(getenv("IPCG_OD_MODE")) : 0;  // dev: 1 all, 2 none
     static const int od_pct = getenv("IPCG_OD_ZEROS") ? atoi(getenv("IPCG_OD_ZEROS")) : 85;  // dev: threshold
-    k_select<<<1, 32, 0, st>>>(w.meta, S, n, n < (1ull << 31) ? od_mode : 2, od_pct);
+    // the on-demand parse pays off on large sparse streams; on small ones (< 1 MiB: coarse levels,
+    // small fields) its serial chunk walks and continuations are latency the all-position search
+    // does not have
+    const int mode = n >= (1ull << 31) ? 2 : (od_mode == 0 && n < (1u << 20)) ? 2 : od_mode;
+    const bool od_possible = mode != 2;  // else no stream takes the on-demand parse: skip its launches
+    k_select<<<1, 32, 0, st>>>(w.meta, S, n, mode, od_pct);
     CKL();
     if (n > 0) {
         const uint64_t nblk = (n + WSIZE - 1) / WSIZE;
@@ -1660,13 +1665,13 @@ void DeflateBatch::run(const uint8_t *in, uint64_t in_stride, int S, uint64_t n,
         }
         // sparse streams (meta.od, k_select) take the on-demand parse, the others the all-position
         // search; each kernel below skips the streams of the other path
-        const bool forked = side && fork && join && n < (1ull << 31);
+        const bool forked = side && fork && join && od_possible;
         const cudaStream_t ost = forked ? side : st;  // the on-demand parse's stream
         if (forked) {
             CK(cudaEventRecord(fork, st));
             CK(cudaStreamWaitEvent(side, fork, 0));
         }
-        if (n < (1ull << 31)) {
+        if (od_possible) {
             const uint32_t nch = (uint32_t)w.od_nch;
             {
             ProfScope ps2("deflate.walk", ost, (uint64_t)S * n);
