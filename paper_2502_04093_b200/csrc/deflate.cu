@@ -20,7 +20,7 @@ namespace {
 
 constexpr int CH = DeflateBatch::CH;
 constexpr int PL_WARPS = 3;  // prevlink warps per CTA (64 KiB head table each)
-constexpr int CRC_CHUNK = 4096;
+constexpr int CRC_CHUNK = 1024;  // bytes per thread (4 KiB left the 30 MB of a refine's identity planes at ~7K threads)
 
 struct StreamMeta {
     unsigned long long nonzero, adA, adB, zeros;
