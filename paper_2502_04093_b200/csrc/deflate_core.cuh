@@ -261,11 +261,16 @@ HD bool walk32_start(uint32_t p, uint32_t n, const Words &w, const Prev &prevd, 
 
 // scan_end1 / scan_end (only meaningful while MIN_MATCH <= best; best < nice <= maxlen holds
 // in the loop).  Both quick-reject bytes of q are loaded unconditionally through
-// qb = stream + best - 1 (at best == 0 they are q, q+1 and unused).  The chain ends when the
-// link is NIL or leaves the window: dq - 1 >= q - lim1 (unsigned; dq <= q and q >= lim1 for
-// every chained candidate).  Candidates up to 32 and beyond run as two phases so the
-// chain-32 snapshot is taken once instead of every step.
-template <class Words, class Prev>
+// qb = stream + best - 1.  While best == 0 they are q, q+1, checked against p, p+1: a chained
+// candidate has p's hash, and hash3 keeps all 8 bits of the third byte once the first two are
+// fixed, so equal first two bytes mean a match of >= MIN_MATCH, and any other candidate's
+// compare could not set best (it would be < MIN_MATCH).  (Comparing every candidate while
+// best == 0 made the compare loop, run by ~5 lanes of 32, 45% of k_match's instructions.)
+// The chain ends when the link is NIL or leaves the window: dq - 1 >= q - lim1 (unsigned;
+// dq <= q and q >= lim1 for every chained candidate).  Candidates up to 32 and beyond run as
+// two phases so the chain-32 snapshot is taken once instead of every step.  BUDGETED: stop
+// after `budget` candidates (resumable walks); the one-pass search compiles the check out.
+template <bool BUDGETED = true, class Words, class Prev>
 HD bool walk32_run(uint32_t n, const Words &w, const Prev &prevd, Walk32 &s, int budget, uint64_t &rec,
                    int max_chain = MAX_CHAIN) {
     const uint32_t p = s.p;
@@ -274,17 +279,17 @@ HD bool walk32_run(uint32_t n, const Words &w, const Prev &prevd, Walk32 &s, int
     const uint32_t lim1 = (p > (uint32_t)MAX_DIST ? p - (uint32_t)MAX_DIST : 0u) + 1u;
     uint32_t q = s.q, best = s.best, bestd = s.bestd, l32 = s.l32, d32 = s.d32;
     int i = s.i;
-    uint32_t e0 = best ? w.byte(p + best - 1) : 0u, e1 = best ? w.byte(p + best) : 0u;
+    uint32_t e0 = w.byte(p + (best ? best - 1 : 0u)), e1 = w.byte(p + (best ? best : 1u));
     const uint8_t *qb = w.at(best ? best - 1 : 0u);
     int stop = i <= 32 ? 32 : MAX_CHAIN;
     for (;;) {
-        if (budget-- <= 0) {
+        if (BUDGETED && budget-- <= 0) {
             s.q = q, s.best = best, s.bestd = bestd, s.l32 = l32, s.d32 = d32, s.i = i;
             return false;
         }
         const uint32_t dq = prevd(q);
         const uint32_t x0 = ldg_byte(qb + q), x1 = ldg_byte(qb + q + 1);
-        if (best == 0 || (x0 == e0 && x1 == e1)) {
+        if (x0 == e0 && x1 == e1) {
             const uint32_t len = match_len32(w, n, p, q, maxlen);
             if (len >= (uint32_t)MIN_MATCH && len > best) {
                 best = len, bestd = p - q;
@@ -321,7 +326,7 @@ HD uint64_t match_search32(uint32_t p, uint32_t n, const Words &w, const Prev &p
     Walk32 s;
     uint64_t rec;
     if (walk32_start(p, n, w, prevd, s, rec)) return rec;
-    walk32_run(n, w, prevd, s, 1 << 30, rec);
+    walk32_run<false>(n, w, prevd, s, 0, rec);
     return rec;
 }
 
@@ -427,7 +432,7 @@ template <class Words, class Prev>
 HD Match match_on_demand(uint32_t p, uint32_t n, const Words &w, const Prev &prevd, int chain) {
     Walk32 s;
     uint64_t rec;
-    if (!walk32_start(p, n, w, prevd, s, rec, chain)) walk32_run(n, w, prevd, s, 1 << 30, rec, chain);
+    if (!walk32_start(p, n, w, prevd, s, rec, chain)) walk32_run<false>(n, w, prevd, s, 0, rec, chain);
     return chain == 32 ? Match{mrec_l32(rec), mrec_d32(rec), mrec_flag(rec)}
                        : Match{mrec_l128(rec), mrec_d128(rec), mrec_flag(rec)};
 }
