@@ -329,6 +329,7 @@ struct JobMeta {
     uint32_t nfallback;  // blocks the chain decoded itself (fixed, stored excluded, unmatched dynamic)
     uint64_t fb_syms;    // their symbols
     int bad;             // a match reached before the start of the output (k_emit)
+    int ranked;          // block table built by k_rank (k_chain skips the job)
 };
 
 struct Cand {
@@ -340,6 +341,7 @@ struct Cand {
     int ok;
     int nzlit;   // some literal is non-zero
     int bfinal;  // BFINAL bit of this block's header
+    int rounds;  // lane-parallel decode rounds (diagnostics)
     int next;    // candidate starting at end_bit, -1 if none (set by k_decode_cands)
 };
 
@@ -589,7 +591,9 @@ __global__ void __launch_bounds__(DWARPS * 32) k_decode_cands(const InflateJob *
         int nph = 1;
         uint64_t base = off + b.used;
         bool eob = false;
+        int nrounds = 0;
         while (good && !eob) {
+            ++nrounds;
             if (base > endbit) {  // overrun (the stream reads as zeros past its end)
                 good = false;
                 break;
@@ -751,6 +755,7 @@ __global__ void __launch_bounds__(DWARPS * 32) k_decode_cands(const InflateJob *
             c.end_bit = b.used;
             c.nsyms = ns;
             c.out_bytes = bytes;
+            c.rounds = nrounds;
             // link to the candidate that starts where this block ends (the chain follows it)
             int nx = -1;
             const Tables T = tabs[c.job];
@@ -815,9 +820,143 @@ __device__ bool chain_decode_block(Bits &b, int type, uint32_t *fb, uint64_t fca
     }
 }
 
+// The common case of the chain, in parallel: every block of every stream is a dynamic block
+// whose candidate decoded ok, so a stream's blocks are the candidate list from the one at bit 16
+// (after the zlib header) along `next` to a BFINAL candidate.  One CTA ranks all candidates by
+// pointer jumping (suffix sums of output bytes, emit segments, block counts; the 2^l-th
+// successors kept per level), then a thread per block of each complete stream finds its node by
+// the binary expansion of its rank and writes its Blk; k_chain walks only the streams left over
+// (stored/fixed/unmatched blocks, or chains of 2^RANK_L blocks or more).  The walk this replaces
+// cost ~0.45 ms for a 900-block stream: one dependent L2 round trip per block.
+constexpr int RANK_L = 16;
+struct RankWs {
+    int *nx[2];
+    int *tm[2];
+    uint64_t *sb[2];
+    uint32_t *ss[2], *sn[2];
+    uint8_t *sz[2];
+    int *jump;  // [RANK_L][nc]
+};
+
+__global__ void __launch_bounds__(1024) k_rank(const InflateJob *jobs, int njobs, const Tables *tabs, JobMeta *meta,
+                                              const Cand *cands, uint32_t nc, RankWs W) {
+    const unsigned tid = threadIdx.x, nth = blockDim.x;
+    for (uint32_t c = tid; c < nc; c += nth) {
+        const Cand &k = cands[c];
+        const int nx = (k.ok && !k.bfinal && k.next >= 0 && (uint32_t)k.next < nc && cands[k.next].ok) ? k.next : -1;
+        W.nx[0][c] = nx;
+        W.tm[0][c] = (int)c;
+        W.sb[0][c] = k.ok ? k.out_bytes : 0;
+        W.ss[0][c] = k.nsyms > 0 ? (k.nsyms + SEG - 1) / SEG : 1;
+        W.sn[0][c] = 1;
+        W.sz[0][c] = k.nzlit ? 1 : 0;
+    }
+    __shared__ int more;
+    int cur = 0;
+    for (int l = 0; l < RANK_L; ++l) {
+        if (tid == 0) more = 0;
+        __syncthreads();
+        const int o = cur ^ 1;
+        for (uint32_t c = tid; c < nc; c += nth) {
+            const int nx = W.nx[cur][c];
+            W.jump[(size_t)l * nc + c] = nx;
+            if (nx >= 0) {
+                W.nx[o][c] = W.nx[cur][nx];
+                W.tm[o][c] = W.tm[cur][nx];
+                W.sb[o][c] = W.sb[cur][c] + W.sb[cur][nx];
+                W.ss[o][c] = W.ss[cur][c] + W.ss[cur][nx];
+                W.sn[o][c] = W.sn[cur][c] + W.sn[cur][nx];
+                W.sz[o][c] = W.sz[cur][c] | W.sz[cur][nx];
+                more = 1;
+            } else {
+                W.nx[o][c] = -1;
+                W.tm[o][c] = W.tm[cur][c];
+                W.sb[o][c] = W.sb[cur][c];
+                W.ss[o][c] = W.ss[cur][c];
+                W.sn[o][c] = W.sn[cur][c];
+                W.sz[o][c] = W.sz[cur][c];
+            }
+        }
+        __syncthreads();
+        cur = o;
+        if (!more) {
+            for (int l2 = l + 1; l2 < RANK_L; ++l2)
+                for (uint32_t c = tid; c < nc; c += nth) W.jump[(size_t)l2 * nc + c] = -1;
+            break;
+        }
+        __syncthreads();  // `more` is reset only after every thread read it
+    }
+    __syncthreads();
+    // per stream: its head, and whether the ranked list is the whole stream
+    for (int j = 0; j < njobs; ++j) {
+        __shared__ int head, ok;
+        if (tid == 0) {
+            head = -1, ok = 0;
+            const InflateJob job = jobs[j];
+            const Tables T = tabs[j];
+            bool hdr = job.src_len >= 2 && !meta[j].overflow;
+            if (hdr) {
+                const uint32_t cmf = job.src[0], flg = job.src[1];
+                hdr = ((cmf << 8) | flg) % 31 == 0 && (cmf & 15) == 8 && (cmf >> 4) + 8 <= 15 && !(flg & 0x20);
+            }
+            if (hdr) {
+                const unsigned long long key = 16 + 1;
+                uint64_t sl = hslot(key, T.hcap);
+                for (uint64_t probe = 0; probe < T.hcap; ++probe, sl = (sl + 1) & (T.hcap - 1)) {
+                    const unsigned long long kk = T.hash[sl];
+                    if (kk == 0ull) break;
+                    if (kk == key) {
+                        head = (int)T.hval[sl];
+                        break;
+                    }
+                }
+            }
+            if (head >= 0 && (uint32_t)head < nc && cands[head].ok && W.nx[cur][head] < 0) {
+                const int term = W.tm[cur][head];
+                const Cand &tc = cands[term];
+                const uint64_t e = tc.end_bit, bp = (e + 7) >> 3;
+                if (tc.bfinal && W.sn[cur][head] <= T.bcap && W.sb[cur][head] == job.dst_len && bp + 4 <= job.src_len) {
+                    ok = 1;
+                    JobMeta &m = meta[j];
+                    m.adler_want = ((uint32_t)job.src[bp] << 24) | ((uint32_t)job.src[bp + 1] << 16) |
+                                   ((uint32_t)job.src[bp + 2] << 8) | job.src[bp + 3];
+                    m.nblocks = W.sn[cur][head];
+                    m.allzero = !W.sz[cur][head];
+                    m.nseg = W.ss[cur][head];
+                    m.ranked = 1;
+                }
+            }
+        }
+        __syncthreads();
+        if (ok) {
+            const Tables T = tabs[j];
+            const uint32_t N = W.sn[cur][head];
+            const uint64_t B = W.sb[cur][head];
+            const uint32_t SS = W.ss[cur][head];
+            for (uint32_t r = tid; r < N; r += nth) {
+                int node = head;
+                for (int l = 0; l < RANK_L && node >= 0; ++l)
+                    if ((r >> l) & 1u) node = W.jump[(size_t)l * nc + node];
+                const Cand &c = cands[node];
+                Blk blk;
+                blk.type = 1;
+                blk.nsyms = c.nsyms;
+                blk.src = (uint64_t)node * MAXSYM;
+                blk.out_off = B - W.sb[cur][node];
+                blk.out_len = c.out_bytes;
+                blk.nseg = c.nsyms > 0 ? (c.nsyms + SEG - 1) / SEG : 1;
+                blk.seg_base = SS - W.ss[cur][node];
+                blk.ckpt = (uint64_t)node;
+                T.blocks[r] = blk;
+            }
+        }
+        __syncthreads();
+    }
+}
+
 __global__ void k_chain(const InflateJob *jobs, int njobs, const Tables *tabs, JobMeta *meta, const Cand *cands) {
     const int j = blockIdx.x * blockDim.x + threadIdx.x;
-    if (j >= njobs) return;
+    if (j >= njobs || meta[j].ranked) return;
     const InflateJob job = jobs[j];
     const Tables T = tabs[j];
     JobMeta &m = meta[j];
@@ -1120,46 +1259,136 @@ __device__ __forceinline__ void for_each_flagged(const uint32_t *bits, uint64_t 
     }
 }
 
+__device__ __forceinline__ unsigned long long gtimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
+
+// CTA-aggregated append: returns the first of `n` list slots claimed for this thread (one global
+// atomic per CTA; every thread of the CTA must call it)
+__device__ __forceinline__ unsigned long long cta_append(unsigned n, unsigned long long *ctr, unsigned *s_cnt,
+                                                        unsigned long long *s_base) {
+    const unsigned lane = threadIdx.x & 31;
+    unsigned incl = n;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const unsigned v = __shfl_up_sync(0xffffffffu, incl, o);
+        if ((int)lane >= o) incl += v;
+    }
+    if (threadIdx.x == 0) *s_cnt = 0;
+    __syncthreads();
+    unsigned woff = 0;
+    if (lane == 31 && incl) woff = atomicAdd(s_cnt, incl);
+    woff = __shfl_sync(0xffffffffu, woff, 31);
+    __syncthreads();
+    if (threadIdx.x == 0) *s_base = *s_cnt ? atomicAdd(ctr, (unsigned long long)*s_cnt) : 0ull;
+    __syncthreads();
+    return *s_base + woff + (incl - n);
+}
+
 __global__ void __launch_bounds__(256) k_resolve_all(const InflateJob *jobs, const Tables *tabs, const JobMeta *meta,
                                                     int njobs, unsigned *changed, uint64_t *mlist, uint64_t mcap,
                                                     unsigned long long *mcount) {
     cg::grid_group grid = cg::this_grid();
     const uint64_t tid = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
     const uint64_t nth = (uint64_t)gridDim.x * blockDim.x;
-    // A: mark every unresolved byte some pointer targets, and list it once (job << 40 | byte)
+    if (tid == 0) mcount[7] = gtimer();
+    // A1: mark every unresolved byte some pointer targets (lanes of a warp that point at the byte
+    // the previous lane points at -- the bytes of one run -- leave the atomic to that lane)
+    const unsigned lane = threadIdx.x & 31;
+    __shared__ unsigned s_cnt;
+    __shared__ unsigned long long s_base;
     for (int j = 0; j < njobs; ++j) {
         if (meta[j].status || meta[j].allzero) continue;
         const Tables T = tabs[j];
-        for_each_flagged(T.flags, jobs[j].dst_len, tid, nth, [&](uint64_t t) {
-            const uint32_t s = T.ptr[t];
-            if (flag_get(T.flags, s) && !flag_get(T.mark, s)) {
-                const uint32_t bit = 1u << (s & 31);
-                if (!(atomicOr(&T.mark[s >> 5], bit) & bit)) {
-                    const unsigned long long i = atomicAdd(mcount, 1ull);
-                    if (i < mcap) mlist[i] = ((uint64_t)j << 40) | s;
+        const uint64_t nwords = (jobs[j].dst_len + 31) / 32;
+        for (uint64_t w0 = (tid >> 5) * 32; w0 < nwords; w0 += (nth >> 5) * 32) {
+            const uint32_t mine = w0 + lane < nwords ? T.flags[w0 + lane] : 0u;
+            unsigned nz = __ballot_sync(0xffffffffu, mine != 0u);
+            while (nz) {  // four flag words per step, loads interleaved (see C)
+                constexpr int U = 4;
+                uint32_t sp[U];
+                bool f[U];
+#pragma unroll
+                for (int u = 0; u < U; ++u) {
+                    const int k = nz ? __ffs(nz) - 1 : 0;
+                    const uint32_t word = __shfl_sync(0xffffffffu, mine, k);
+                    f[u] = nz && ((word >> lane) & 1u);
+                    nz &= nz - 1;
+                    sp[u] = f[u] ? T.ptr[(w0 + (uint64_t)k) * 32 + lane] : ~0u;
                 }
+                bool c[U];
+#pragma unroll
+                for (int u = 0; u < U; ++u) {
+                    const uint32_t up = __shfl_up_sync(0xffffffffu, sp[u], 1);
+                    c[u] = f[u] && (lane == 0 || up != sp[u]);
+                }
+#pragma unroll
+                for (int u = 0; u < U; ++u) c[u] = c[u] && flag_get(T.flags, sp[u]) && !flag_get(T.mark, sp[u]);
+#pragma unroll
+                for (int u = 0; u < U; ++u)
+                    if (c[u]) atomicOr(&T.mark[sp[u] >> 5], 1u << (sp[u] & 31));
             }
-        });
+        }
     }
     grid.sync();
-    // B: pointer jumping on the listed bytes only (the marked set, closed under ptr), a grid
-    // barrier per round; the full mark bitmaps are scanned only if the list overflowed
-    const unsigned long long M = *(volatile unsigned long long *)mcount;
-    for (int round = 0;; ++round) {
-        if (tid == 0) changed[(round + 1) % 3] = 0;  // its last reader finished before the previous sync
-        bool any = false;
-        if (M <= mcap) {
-            for (uint64_t i = tid; i < M; i += nth) {
-                const uint64_t e = mlist[i];
-                const Tables T = tabs[e >> 40];
-                const uint32_t t = (uint32_t)(e & 0xffffffffffull);
-                const uint32_t sp = T.ptr[t];
-                if (flag_get(T.flags, sp)) {
-                    T.ptr[t] = T.ptr[sp];
-                    any = true;
-                }
+    // A2: list the marked bytes (job << 40 | byte): a CTA-uniform pass over the mark words, one
+    // list atomic per CTA step (one per warp, or per byte, serialised on the counter)
+    for (int j = 0; j < njobs; ++j) {
+        if (meta[j].status || meta[j].allzero) continue;
+        const Tables T = tabs[j];
+        const uint64_t nwords = (jobs[j].dst_len + 31) / 32;
+        for (uint64_t b0 = (uint64_t)blockIdx.x * blockDim.x; b0 < nwords; b0 += nth) {
+            const uint64_t wi = b0 + threadIdx.x;
+            const uint32_t mw = wi < nwords ? T.mark[wi] : 0u;
+            const unsigned long long at = cta_append(__popc(mw), mcount, &s_cnt, &s_base);
+            uint32_t x = mw;
+            for (unsigned long long i = at; x; ++i) {
+                const int b = __ffs(x) - 1;
+                x &= x - 1;
+                if (i < mcap) mlist[i] = ((uint64_t)j << 40) | (wi * 32 + (uint64_t)b);
             }
-        } else {
+        }
+    }
+    grid.sync();
+    const unsigned long long M0 = *(volatile unsigned long long *)mcount;
+    unsigned long long *stamp = mcount + 4;  // diagnostics: globaltimer after A, B, C
+    if (tid == 0) stamp[0] = gtimer();
+    if (M0 <= mcap) {
+        unsigned long long *cnt = mcount + 1;  // three rotating survivor counters
+        uint64_t *cur = mlist, *nxt = mlist + mcap;
+        unsigned long long M = M0;
+        for (int round = 0; M; ++round) {
+            if (tid == 0) cnt[(round + 1) % 3] = 0;  // its last reader finished before the previous sync
+            for (uint64_t b0 = (uint64_t)blockIdx.x * blockDim.x; b0 < M; b0 += nth) {
+                const uint64_t i = b0 + threadIdx.x;
+                bool keep = false;
+                uint64_t e = 0;
+                if (i < M) {
+                    e = cur[i];
+                    const Tables T = tabs[e >> 40];
+                    const uint32_t t = (uint32_t)(e & 0xffffffffffull);
+                    const uint32_t sp = T.ptr[t];
+                    if (flag_get(T.flags, sp)) {
+                        const uint32_t np = T.ptr[sp];
+                        T.ptr[t] = np;
+                        keep = flag_get(T.flags, np);
+                    }
+                }
+                const unsigned long long at = cta_append(keep ? 1u : 0u, &cnt[round % 3], &s_cnt, &s_base);
+                if (keep) nxt[at] = e;
+            }
+            grid.sync();
+            M = *(volatile unsigned long long *)&cnt[round % 3];
+            uint64_t *tmp = cur;
+            cur = nxt, nxt = tmp;
+            if (M == 0 && tid == 0) changed[3] = (unsigned)round + 1;  // rounds run (diagnostics)
+        }
+    } else {
+        for (int round = 0;; ++round) {
+            if (tid == 0) changed[(round + 1) % 3] = 0;  // its last reader finished before the previous sync
+            bool any = false;
             for (int j = 0; j < njobs; ++j) {
                 if (meta[j].status || meta[j].allzero) continue;
                 const Tables T = tabs[j];
@@ -1171,26 +1400,58 @@ __global__ void __launch_bounds__(256) k_resolve_all(const InflateJob *jobs, con
                     }
                 });
             }
-        }
-        if (__any_sync(0xffffffffu, any) && (threadIdx.x & 31) == 0) atomicOr(&changed[round % 3], 1u);
-        grid.sync();
-        if (*(volatile unsigned *)&changed[round % 3] == 0) {
-            if (tid == 0) changed[3] = (unsigned)round + 1;  // rounds run (diagnostics)
-            break;
+            if (__any_sync(0xffffffffu, any) && lane == 0) atomicOr(&changed[round % 3], 1u);
+            grid.sync();
+            if (*(volatile unsigned *)&changed[round % 3] == 0) {
+                if (tid == 0) changed[3] = (unsigned)round + 1;  // rounds run (diagnostics)
+                break;
+            }
         }
     }
     grid.sync();
-    // C: resolve every unresolved byte in one step (its target is resolved or listed)
+    if (tid == 0) stamp[1] = gtimer();
+    // C: resolve every unresolved byte in one step (its target is resolved or listed); four flag
+    // words per step with their loads interleaved (the chain ptr -> flag -> ptr -> value is
+    // latency-bound one word at a time)
     for (int j = 0; j < njobs; ++j) {
         if (meta[j].status || meta[j].allzero) continue;
         const InflateJob job = jobs[j];
         const Tables T = tabs[j];
-        for_each_flagged(T.flags, job.dst_len, tid, nth, [&](uint64_t t) {
-            uint32_t s = T.ptr[t];
-            if (flag_get(T.flags, s)) s = T.ptr[s];
-            job.dst[t] = job.dst[s];
-        });
+        const uint64_t nwords = (job.dst_len + 31) / 32;
+        for (uint64_t w0 = (tid >> 5) * 32; w0 < nwords; w0 += (nth >> 5) * 32) {
+            const uint32_t mine = w0 + lane < nwords ? T.flags[w0 + lane] : 0u;
+            unsigned nz = __ballot_sync(0xffffffffu, mine != 0u);
+            while (nz) {
+                constexpr int U = 4;
+                uint64_t t[U];
+                uint32_t sp[U];
+                bool f[U];
+#pragma unroll
+                for (int u = 0; u < U; ++u) {
+                    const int k = nz ? __ffs(nz) - 1 : 0;
+                    const uint32_t word = __shfl_sync(0xffffffffu, mine, k);
+                    f[u] = nz && ((word >> lane) & 1u);
+                    nz &= nz - 1;
+                    t[u] = (w0 + (uint64_t)k) * 32 + lane;
+                    sp[u] = f[u] ? T.ptr[t[u]] : 0u;
+                }
+                bool g[U];
+#pragma unroll
+                for (int u = 0; u < U; ++u) g[u] = f[u] && flag_get(T.flags, sp[u]);
+#pragma unroll
+                for (int u = 0; u < U; ++u)
+                    if (g[u]) sp[u] = T.ptr[sp[u]];
+                uint8_t v[U];
+#pragma unroll
+                for (int u = 0; u < U; ++u) v[u] = f[u] ? job.dst[sp[u]] : 0;
+#pragma unroll
+                for (int u = 0; u < U; ++u)
+                    if (f[u]) job.dst[t[u]] = v[u];
+            }
+        }
     }
+    grid.sync();
+    if (tid == 0) stamp[2] = gtimer();
 }
 
 // --------------------------------------------------------------- 6. checks
@@ -1379,6 +1640,22 @@ void inflate_batch_host(const std::vector<InflateJob> &jobs, int *status_dev, De
             k_decode_cands<CPW><<<g, DWARPS * 32, 0, st>>>(jd, td, cands, ncand, cand_cap, pool, ckpt);
             CKL();
         }
+        if (nc && nc <= (1u << 20)) {
+            RankWs W;
+            uint8_t *rw = static_cast<uint8_t *>(alloc.get(nc * (2 * (4 + 4 + 8 + 4 + 4 + 1) + 4 * RANK_L) + 256, st));
+            auto take = [&](size_t b) { uint8_t *q = rw; rw += (b + 15) & ~size_t(15); return q; };
+            for (int h = 0; h < 2; ++h) {
+                W.nx[h] = reinterpret_cast<int *>(take(nc * 4));
+                W.tm[h] = reinterpret_cast<int *>(take(nc * 4));
+                W.sb[h] = reinterpret_cast<uint64_t *>(take(nc * 8));
+                W.ss[h] = reinterpret_cast<uint32_t *>(take(nc * 4));
+                W.sn[h] = reinterpret_cast<uint32_t *>(take(nc * 4));
+                W.sz[h] = take(nc);
+            }
+            W.jump = reinterpret_cast<int *>(take(nc * 4 * RANK_L));
+            k_rank<<<1, 1024, 0, st>>>(jd, n, td, md, cands, (uint32_t)nc, W);
+            CKL();
+        }
         k_chain<<<(n + 31) / 32, 32, 0, st>>>(jd, n, td, md, cands);
         CKL();
     }
@@ -1392,7 +1669,10 @@ void inflate_batch_host(const std::vector<InflateJob> &jobs, int *status_dev, De
             std::vector<Cand> hcands(nc);
             CK(cudaMemcpy(hcands.data(), cands, nc * sizeof(Cand), cudaMemcpyDeviceToHost));
             uint64_t ok = 0, okn = 0, badn = 0, hist[6] = {0, 0, 0, 0, 0, 0};
+            uint64_t rsum = 0, rmax = 0, bits_sum = 0;
             for (const Cand &cc : hcands) {
+                rsum += cc.rounds, rmax = std::max<uint64_t>(rmax, cc.rounds);
+                bits_sum += cc.end_bit > cc.hdr_bit ? cc.end_bit - cc.hdr_bit : 0;
                 if (cc.ok) ++ok, okn += cc.nsyms;
                 else badn += cc.nsyms;
                 const uint32_t v = cc.nsyms;
@@ -1400,7 +1680,9 @@ void inflate_batch_host(const std::vector<InflateJob> &jobs, int *status_dev, De
             }
             unsigned long long hs = 0;
             CK(cudaMemcpy(&hs, nsurv, 8, cudaMemcpyDeviceToHost));
-            fprintf(stderr, "inflate: %llu survivors of %llu bit offsets\n", hs, (unsigned long long)total_src * 8);
+            fprintf(stderr, "inflate: %llu survivors of %llu bit offsets; decode rounds mean %.1f max %llu, bits/cand %.0f\n", hs,
+                    (unsigned long long)total_src * 8, nc ? (double)rsum / nc : 0.0, (unsigned long long)rmax,
+                    nc ? (double)bits_sum / nc : 0.0);
             fprintf(stderr, "inflate: %d jobs, %llu candidates (%llu ok, syms ok %llu bad %llu) nsyms hist 0:%llu <16:%llu <256:%llu <4k:%llu <16k:%llu >=16k:%llu\n",
                     n, (unsigned long long)nc, (unsigned long long)ok, (unsigned long long)okn, (unsigned long long)badn,
                     (unsigned long long)hist[0], (unsigned long long)hist[1], (unsigned long long)hist[2],
@@ -1419,17 +1701,17 @@ void inflate_batch_host(const std::vector<InflateJob> &jobs, int *status_dev, De
         }
         {
             ProfScope ps3("inflate.resolve", st, max_dst * n / 8);
-            unsigned *changed = static_cast<unsigned *>(alloc.get(4 * sizeof(unsigned) + 8, st));
-            unsigned long long *mcount = reinterpret_cast<unsigned long long *>(changed + 4);
-            CK(cudaMemsetAsync(changed, 0, 4 * sizeof(unsigned) + 8, st));
+            unsigned *changed = static_cast<unsigned *>(alloc.get(4 * sizeof(unsigned) + 8 * 8, st));
+            unsigned long long *mcount = reinterpret_cast<unsigned long long *>(changed + 4);  // + 3 round counters
+            CK(cudaMemsetAsync(changed, 0, 4 * sizeof(unsigned) + 8 * 8, st));
             uint64_t mcap = std::max<uint64_t>(1 << 20, max_dst * (uint64_t)n / 32);  // marked bytes listed
-            uint64_t *mlist = static_cast<uint64_t *>(alloc.get(mcap * 8, st));
+            uint64_t *mlist = static_cast<uint64_t *>(alloc.get(2 * mcap * 8, st));  // two halves (compaction)
             static int coop_cache[64] = {0};  // per device
             int &coop_blocks = coop_cache[current_device() & 63];
             if (!coop_blocks) {
                 int per = 0;
                 CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_resolve_all, 256, 0));
-                coop_blocks = num_sms() * std::max(1, std::min(per, 4));
+                coop_blocks = num_sms() * std::max(1, std::min(per, getenv("IPCG_RES_CTAS") ? atoi(getenv("IPCG_RES_CTAS")) : 8));
             }
             int nj = n;
             void *args[] = {(void *)&jd, (void *)&td, (void *)&md, (void *)&nj, (void *)&changed, (void *)&mlist,
@@ -1442,7 +1724,10 @@ void inflate_batch_host(const std::vector<InflateJob> &jobs, int *status_dev, De
                 CK(cudaStreamSynchronize(st));
                 CK(cudaMemcpy(hr, changed, sizeof(hr), cudaMemcpyDeviceToHost));
                 CK(cudaMemcpy(&hm, mcount, 8, cudaMemcpyDeviceToHost));
-                fprintf(stderr, "inflate: %llu listed (marked) bytes\n", hm);
+                unsigned long long stp[4];
+                CK(cudaMemcpy(stp, mcount + 4, sizeof(stp), cudaMemcpyDeviceToHost));
+                fprintf(stderr, "inflate: %llu listed (marked) bytes; resolve A %.3f B %.3f C %.3f ms\n", hm,
+                        (stp[0] - stp[3]) * 1e-6, (stp[1] - stp[0]) * 1e-6, (stp[2] - stp[1]) * 1e-6);
                 uint64_t unres = 0;
                 std::vector<Tables> ht(n);
                 CK(cudaMemcpy(ht.data(), td, n * sizeof(Tables), cudaMemcpyDeviceToHost));
