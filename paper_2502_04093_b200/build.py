@@ -23,6 +23,7 @@ INCLUDE = os.path.join(os.path.dirname(HERE), "include")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVFLAGS = ["-std=c++17", *ARCH, "-O3", "-lineinfo", "-fmad=false", "-prec-div=true", "-prec-sqrt=true",
            "-ftz=false", "--extended-lambda", "-Xcompiler", "-fPIC,-ffp-contract=off", f"-I{INCLUDE}"]
+NVFLAGS += os.environ.get("IPCG_NVCC_EXTRA", "").split()  # dev: variant builds (tools/variants.sh)
 PER_FILE: dict = {}  # per-file extra nvcc flags
 
 

@@ -197,13 +197,19 @@ __device__ bool read_dynamic_header(Bits &b, uint8_t *lens, int &nlen, int &ndis
 // kind << 4 | extra bits << 6 | value << 16.  kind 0 literal (value = byte), 1 length or
 // distance (value = base), 2 end of block, 3 invalid symbol.  A literal/length table of
 // 11 bits leaves almost no code to the canonical loop (which diverges a lane-parallel warp).
-constexpr int LITBITS = 11, DISTBITS = 10;
+#ifndef IPCG_DISTBITS
+#define IPCG_DISTBITS 8
+#endif
+#ifndef IPCG_STAGE
+#define IPCG_STAGE 1
+#endif
+constexpr int LITBITS = 11, DISTBITS = IPCG_DISTBITS;
 template <int BITS>
 struct Huff {
     uint16_t count[16];
     uint16_t first[16];
     uint16_t offs[16];
-    uint16_t sym[320];
+    uint16_t sym[BITS == LITBITS ? 320 : 32];  // canonical symbol order (lit/len: 288 + slack; distance: 30 + slack)
     uint32_t fx[1 << BITS];
 };
 
@@ -529,6 +535,10 @@ __global__ void __launch_bounds__(DWARPS * 32) k_decode_cands(const InflateJob *
     __shared__ uint32_t li_e1[DWARPS][NPH][32], li_x[DWARPS][NPH][32];  // per lane and phase
     __shared__ int8_t li_sync[DWARPS][NPH][32];
     __shared__ uint8_t li_fl[DWARPS][NPH][32];  // 1: path ends in own subsequence, 2: in the next  // symbol-start bitmaps of the lane subsequences
+    // the round's bits (32 subsequences + the reach of the last symbols), staged once per round:
+    // the per-symbol window loads were the decode's top stall (L1 misses on the critical path)
+    constexpr int STG = IPCG_STAGE ? 32 * SUBB / 32 + 8 : 4;
+    __shared__ uint32_t stg_s[DWARPS][STG];
     const unsigned w = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const unsigned sub = lane / G, gl = lane % G, slot = w * CPW + sub;
     const uint64_t n = min((unsigned long long)cand_cap, *ncand_total);
@@ -575,11 +585,19 @@ __global__ void __launch_bounds__(DWARPS * 32) k_decode_cands(const InflateJob *
         const uint64_t off = (uint64_t)(sa & 3) * 8;
         const uint32_t *W = reinterpret_cast<const uint32_t *>(sa & ~uintptr_t(3));
         const uint64_t nwords = (off / 8 + job.src_len + 3) / 4, endbit = off + 8 * job.src_len;
+        uint32_t *stg = stg_s[w];
+        uint64_t k0 = 0;  // first staged word
         auto window = [&](uint64_t P) {
             const uint64_t k = P >> 5;
             const uint32_t sh = (uint32_t)(P & 31);
-            const uint32_t w0 = k < nwords ? __ldg(W + k) : 0u, w1 = k + 1 < nwords ? __ldg(W + k + 1) : 0u,
-                           w2 = k + 2 < nwords ? __ldg(W + k + 2) : 0u;
+            uint32_t w0, w1, w2;
+            const uint64_t rel = k - k0;
+            if (IPCG_STAGE && k >= k0 && rel + 2 < (uint64_t)STG) {
+                w0 = stg[rel], w1 = stg[rel + 1], w2 = stg[rel + 2];
+            } else {
+                w0 = k < nwords ? __ldg(W + k) : 0u, w1 = k + 1 < nwords ? __ldg(W + k + 1) : 0u,
+                w2 = k + 2 < nwords ? __ldg(W + k + 2) : 0u;
+            }
             return (uint64_t)__funnelshift_r(w0, w1, sh) | ((uint64_t)__funnelshift_r(w1, w2, sh) << 32);
         };
         uint32_t *marks = marks_s[w];  // [32 lanes][MARKW words]
@@ -599,6 +617,12 @@ __global__ void __launch_bounds__(DWARPS * 32) k_decode_cands(const InflateJob *
                 break;
             }
             const uint64_t g = base + (uint64_t)gl * subb, gn = g + subb;
+            k0 = base >> 5;
+            if (IPCG_STAGE) {
+                __syncwarp();  // the previous round's readers are done
+                for (int i = (int)gl; i < STG; i += 32) stg[i] = k0 + i < nwords ? __ldg(W + k0 + i) : 0u;
+                __syncwarp();
+            }
             // P1: speculative decode of my subsequence from nph bit offsets, marking symbol starts;
             // per phase the exit (or the position of a path-ending symbol) goes to shared memory
             // relative to `base` (per-phase registers cost the kernel 40 registers)
