@@ -162,10 +162,19 @@ __device__ bool read_dynamic_header(Bits &b, uint8_t *lens, int &nlen, int &ndis
     if (!canon_build(scratch, cll, 19, 0)) return false;
     int idx = 0;
     uint8_t prev = 0;
+    // Kraft sums of the two codes so far (units of 2^-15): an over-subscribed code is rejected by
+    // inflate_table anyway (canon_build below), so stop reading at once -- random bit offsets
+    // that pass the scan's filters mostly fail here, about halfway through their lengths
+    uint32_t kl = 0, kd = 0;
     while (idx < nlen + ndist) {
         const int sym = canon_decode(scratch, b);
         if (sym < 0) return false;
         if (sym < 16) {
+            if (sym) {
+                if (idx < nlen) kl += 32768u >> sym;
+                else kd += 32768u >> sym;
+                if (kl > 32768u || kd > 32768u) return false;
+            }
             lens[idx++] = (uint8_t)sym;
             prev = (uint8_t)sym;
             continue;
@@ -182,6 +191,12 @@ __device__ bool read_dynamic_header(Bits &b, uint8_t *lens, int &nlen, int &ndis
             rep = 11 + (int)b.get(7);
         }
         if (idx + rep > nlen + ndist) return false;
+        if (v) {
+            const int inl = idx < nlen ? min(rep, nlen - idx) : 0;
+            kl += (uint32_t)inl * (32768u >> v);
+            kd += (uint32_t)(rep - inl) * (32768u >> v);
+            if (kl > 32768u || kd > 32768u) return false;
+        }
         for (int r = 0; r < rep; ++r) lens[idx + r] = v;
         prev = v;
         idx += rep;
@@ -429,6 +444,99 @@ __device__ __forceinline__ void scan_offset(const InflateJob &job, const Tables 
     meta[j].overflow = 1;
 }
 
+// zlib's acceptance of a dynamic header at `bit` (BFINAL at bit), as a filter in front of
+// scan_offset: the same rules as read_dynamic_header + canon_build (complete code-length code,
+// repeat and length-count rules, end-of-block code present, no over-subscribed lit/len or
+// distance code, incomplete only as a single 1-bit code, no read past the stream end), but on
+// Kraft sums and maximum lengths instead of length arrays, with the code-length code decoded
+// through a 128-entry table (`tab`, this thread's slice of shared memory) and the bits read from
+// aligned words.  Rejects only what the full check rejects; the ~1% that pass are re-read in full.
+__device__ bool quick_header_ok(const InflateJob &job, uint64_t bit, uint8_t *tab) {
+    const uintptr_t sa = reinterpret_cast<uintptr_t>(job.src);
+    const uint64_t off = (uint64_t)(sa & 3) * 8;
+    const uint32_t *W = reinterpret_cast<const uint32_t *>(sa & ~uintptr_t(3));
+    const uint64_t nwords = (off / 8 + job.src_len + 3) / 4;
+    auto window = [&](uint64_t P) {  // 64 stream bits from absolute (word-aligned-base) bit P
+        const uint64_t k = P >> 5;
+        const uint32_t sh = (uint32_t)(P & 31);
+        const uint32_t w0 = k < nwords ? __ldg(W + k) : 0u, w1 = k + 1 < nwords ? __ldg(W + k + 1) : 0u,
+                       w2 = k + 2 < nwords ? __ldg(W + k + 2) : 0u;
+        return (uint64_t)__funnelshift_r(w0, w1, sh) | ((uint64_t)__funnelshift_r(w1, w2, sh) << 32);
+    };
+    uint64_t p = off + bit + 3;
+    uint64_t v = window(p);
+    const int nlen = (int)(v & 31) + 257, ndist = (int)((v >> 5) & 31) + 1, ncode = (int)((v >> 10) & 15) + 4;
+    if (nlen > 286 || ndist > 30) return false;
+    p += 14;
+    v = window(p);
+    uint8_t cll[19];
+#pragma unroll
+    for (int i = 0; i < 19; ++i) cll[i] = 0;
+    for (int i = 0; i < ncode; ++i) cll[kOrder[i]] = (uint8_t)((v >> (3 * i)) & 7);
+    p += 3 * (uint64_t)ncode;
+    uint32_t cnt[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+#pragma unroll
+    for (int i = 0; i < 19; ++i) cnt[cll[i]]++;
+    int left = 1;
+#pragma unroll
+    for (int l = 1; l <= 7; ++l) {
+        left = (left << 1) - (int)cnt[l];
+        if (left < 0) return false;
+    }
+    if (left != 0) return false;  // incomplete (or empty) code-length code
+    // canonical codes -> reversed-bit table of (symbol | length << 5)
+    uint32_t next[8];
+    next[1] = 0;
+#pragma unroll
+    for (int l = 1; l < 7; ++l) next[l + 1] = (next[l] + cnt[l]) << 1;
+    for (int sym = 0; sym < 19; ++sym) {
+        const int L = cll[sym];
+        if (!L) continue;
+        const uint32_t code = next[L]++;
+        const uint32_t rev = __brev(code) >> (32 - L);
+        for (uint32_t e = 0; e < (1u << (7 - L)); ++e) tab[rev | (e << L)] = (uint8_t)(sym | L << 5);
+    }
+    const int total = nlen + ndist;
+    int idx = 0, prevl = 0, maxl = 0, maxd = 0;
+    uint32_t kl = 0, kd = 0;
+    bool eob = false;
+    while (idx < total) {
+        v = window(p);
+        const uint32_t e = tab[v & 127];
+        const int L = e >> 5, sym = e & 31;
+        v >>= L;
+        p += (uint64_t)L;
+        int rep, val;
+        if (sym < 16) {
+            rep = 1, val = sym;
+        } else if (sym == 16) {
+            if (idx == 0) return false;
+            rep = 3 + (int)(v & 3), val = prevl, p += 2;
+        } else if (sym == 17) {
+            rep = 3 + (int)(v & 7), val = 0, p += 3;
+        } else {
+            rep = 11 + (int)(v & 127), val = 0, p += 7;
+        }
+        if (idx + rep > total) return false;
+        if (val) {
+            const int inl = idx < nlen ? min(rep, nlen - idx) : 0;
+            if (inl) {
+                kl += (uint32_t)inl * (32768u >> val), maxl = max(maxl, val);
+                if (idx <= 256 && 256 < idx + inl) eob = true;
+            }
+            if (rep - inl) kd += (uint32_t)(rep - inl) * (32768u >> val), maxd = max(maxd, val);
+            if (kl > 32768u || kd > 32768u) return false;
+        }
+        prevl = val;
+        idx += rep;
+    }
+    if (!eob) return false;
+    if (p - off > 8 * job.src_len) return false;  // read past the stream end
+    if (kl < 32768u && maxl != 1) return false;    // incomplete lit/len code
+    if (kd < 32768u && maxd > 1) return false;     // incomplete distance code (none at all is accepted)
+    return true;
+}
+
 // survivors of the cheap filters, validated by k_validate with every lane busy (validating
 // in place left 31 lanes waiting on the one running zlib's header decode)
 struct Survivor {
@@ -440,9 +548,11 @@ __global__ void __launch_bounds__(256) k_validate(const InflateJob *jobs, const 
                                                  const Survivor *surv, const unsigned long long *nsurv,
                                                  uint64_t surv_cap, Cand *cands, unsigned long long *ncand_total,
                                                  uint64_t cand_cap) {
+    __shared__ uint8_t qtab[256][128];
     const uint64_t ns = min((unsigned long long)surv_cap, *nsurv);
     for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < ns; i += (uint64_t)gridDim.x * blockDim.x) {
         const Survivor sv = surv[i];
+        if (!quick_header_ok(jobs[sv.job], sv.bit, qtab[threadIdx.x])) continue;
         scan_offset(jobs[sv.job], tabs[sv.job], meta, sv.job, cands, ncand_total, cand_cap, sv.bit);
     }
 }
