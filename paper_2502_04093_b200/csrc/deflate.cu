@@ -9,7 +9,6 @@
 //   CRC-32 (chunked + GF(2) combine).
 // All-zero planes (most high planes) are compressed once per batch and shared.
 #include <cstdlib>
-#include <cub/block/block_radix_sort.cuh>
 #include "deflate.cuh"
 #include "deflate_core.cuh"
 
@@ -376,145 +375,6 @@ __global__ void __launch_bounds__(PL_WARPS * 32) k_prevlinks(const uint8_t *in, 
                 prevd[q] = (uint16_t)(hs[k] < 0x10000u && e != sent && d < (uint32_t)WSIZE ? d : 0u);
             }
         }
-    }
-}
-
-// Sorted prevlinks: the same links without the serial head-table walk.  prevd[q] is the
-// distance to the previous position with the same hash (what zlib's prev[] chain yields,
-// k_prevlinks above) when it is < WSIZE, else 0.  A CTA owns a span of PLS_SUB sub-tiles of
-// PLS_T positions and walks them in order, after a warm-up over the WSIZE bytes before the
-// span.  Per sub-tile it sorts the positions by (hash, position) in shared memory (CUB block
-// radix sort; positions start in order and the sort is stable, so only the 15 hash bits are
-// sorted): a position's sorted predecessor with the same hash is its link, and a hash's first
-// position in the sub-tile links to the hash's last position so far, kept in a shared-memory
-// table of absolute positions (updated after the lookups).
-constexpr int PLS_THREADS = 1024, PLS_ITEMS = 16, PLS_T = PLS_THREADS * PLS_ITEMS;
-constexpr int PLS_WARM = WSIZE / PLS_T;  // warm-up sub-tiles
-using PlSort = cub::BlockRadixSort<uint32_t, PLS_THREADS, PLS_ITEMS, cub::NullType, 5, false>;
-constexpr size_t PLS_SORT_BYTES =
-    sizeof(typename PlSort::TempStorage) > PLS_T * sizeof(uint16_t) ? sizeof(typename PlSort::TempStorage)
-                                                                    : PLS_T * sizeof(uint16_t);
-constexpr size_t PLS_SMEM = 32768 * sizeof(uint32_t) + ((PLS_SORT_BYTES + 15) & ~size_t(15)) +
-                            2 * PLS_THREADS * sizeof(uint32_t);
-
-__device__ __forceinline__ void pl_span_item(const uint8_t *in, uint64_t in_stride, uint32_t n, int j,
-                                             uint16_t *prevd_all, uint64_t own0, int span, uint8_t *plsm) {
-    uint32_t *last = reinterpret_cast<uint32_t *>(plsm);                    // [hash] -> last position + 1 (0: none)
-    uint8_t *sortmem = plsm + 32768 * sizeof(uint32_t);                     // sort temp, then the sub-tile's links
-    uint16_t *pv = reinterpret_cast<uint16_t *>(sortmem);
-    uint32_t *efirst = reinterpret_cast<uint32_t *>(sortmem + ((PLS_SORT_BYTES + 15) & ~size_t(15)));
-    uint32_t *elast = efirst + PLS_THREADS;
-    const unsigned tid = threadIdx.x;
-    const uint8_t *p = in + (uint64_t)j * in_stride;
-    uint16_t *prevd = prevd_all + (uint64_t)j * n;
-    const uint32_t own_end = (uint32_t)min((uint64_t)n, own0 + (uint64_t)span * PLS_T);
-    for (int k = tid; k < 32768; k += PLS_THREADS) last[k] = 0u;
-    const uint32_t start = own0 >= (uint64_t)WSIZE ? (uint32_t)own0 - WSIZE : 0u;
-    constexpr uint32_t NONE = ~0u;
-    for (uint32_t t0 = start; t0 < own_end; t0 += PLS_T) {
-        const uint32_t len = min((uint32_t)PLS_T, n - t0);
-        const uint32_t o0 = tid * PLS_ITEMS;
-        // 18 bytes from o0 (rows are 16-byte aligned and padded: a 16-byte word that starts
-        // below n is inside the row)
-        uint32_t wv[8];
-#pragma unroll
-        for (int k = 0; k < 2; ++k) {
-            const uint32_t q = t0 + o0 + 16 * k;
-            const uint4 v = q < n ? __ldg(reinterpret_cast<const uint4 *>(p + q)) : make_uint4(0, 0, 0, 0);
-            wv[4 * k] = v.x, wv[4 * k + 1] = v.y, wv[4 * k + 2] = v.z, wv[4 * k + 3] = v.w;
-        }
-        uint32_t keys[PLS_ITEMS];
-#pragma unroll
-        for (int i = 0; i < PLS_ITEMS; ++i) {
-            const uint32_t a = (wv[i >> 2] >> (8 * (i & 3))) & 0xff,
-                           b = (wv[(i + 1) >> 2] >> (8 * ((i + 1) & 3))) & 0xff,
-                           c = (wv[(i + 2) >> 2] >> (8 * ((i + 2) & 3))) & 0xff;
-            const bool valid = (uint64_t)t0 + o0 + i + MIN_MATCH <= n;
-            // invalid positions (the stream's last two, and past its end) are the sub-tile's
-            // highest offsets, so sorting them under hash 0x7fff never makes one a valid link
-            keys[i] = ((valid ? hash3(a, b, c) : 0x7fffu) << 15) | (o0 + i);
-        }
-        __syncthreads();  // the previous sub-tile's pv/edge readers are done
-        PlSort(*reinterpret_cast<typename PlSort::TempStorage *>(sortmem)).Sort(keys, 15, 30);
-        __syncthreads();
-        efirst[tid] = keys[0];
-        elast[tid] = keys[PLS_ITEMS - 1];
-        __syncthreads();
-        uint32_t prevk = tid ? elast[tid - 1] : NONE;
-        // lookups (the table still holds the previous sub-tiles' last positions)
-#pragma unroll
-        for (int i = 0; i < PLS_ITEMS; ++i) {
-            const uint32_t k = keys[i], h = k >> 15, off = k & 0x7fff, q = t0 + off;
-            uint32_t d = 0;
-            if (off < len && (uint64_t)q + MIN_MATCH <= n) {
-                if (prevk != NONE && (prevk >> 15) == h) {
-                    d = off - (prevk & 0x7fff);
-                } else {
-                    const uint32_t e = last[h];
-                    if (e && q - (e - 1) < (uint32_t)WSIZE) d = q - (e - 1);
-                }
-            }
-            if (off < len) pv[off] = (uint16_t)d;
-            prevk = k;
-        }
-        __syncthreads();
-        // table updates: each hash's last valid position in the sub-tile
-#pragma unroll
-        for (int i = 0; i < PLS_ITEMS; ++i) {
-            const uint32_t k = keys[i], h = k >> 15, off = k & 0x7fff;
-            const uint32_t nextk = i + 1 < PLS_ITEMS ? keys[i + 1] : (tid + 1 < PLS_THREADS ? efirst[tid + 1] : NONE);
-            if ((uint64_t)t0 + off + MIN_MATCH <= n && (nextk == NONE || (nextk >> 15) != h)) last[h] = t0 + off + 1;
-        }
-        if (t0 < own0) continue;  // warm-up
-        uint16_t *dst = prevd + t0;
-        if (len == PLS_T && (reinterpret_cast<uintptr_t>(dst) & 15) == 0) {
-            uint4 *d4 = reinterpret_cast<uint4 *>(dst);
-            const uint4 *s4 = reinterpret_cast<const uint4 *>(pv);
-            for (int k = tid; k < PLS_T / 8; k += PLS_THREADS) d4[k] = s4[k];
-        } else {
-            for (uint32_t k = tid; k < len; k += PLS_THREADS) dst[k] = pv[k];
-        }
-    }
-}
-
-// Persistent: one CTA per SM takes (active stream, span) items round-robin; the span length is
-// chosen on the device from the number of active streams (the warm-up against the waves).
-__global__ void __launch_bounds__(PLS_THREADS, 1) k_pl_span(const uint8_t *in, uint64_t in_stride, uint32_t n,
-                                                           const StreamMeta *meta, int S, uint16_t *prevd_all) {
-    extern __shared__ __align__(16) uint8_t plsm[];
-    __shared__ int item_stream;
-    const unsigned tid = threadIdx.x, lane = tid & 31;
-    int nact = 0;
-    for (int b = 0; b < S; b += 32) nact += __popc(__ballot_sync(0xffffffffu, b + (int)lane < S && meta[b + lane].active));
-    if (nact == 0) return;
-    const uint32_t nsub = (n + PLS_T - 1) / PLS_T;
-    int span = 1;
-    {
-        double best = 1e300;
-        for (int s = 1; s <= 64; s *= 2) {
-            const uint64_t items = (uint64_t)nact * ((nsub + s - 1) / s);
-            const double tt = (double)((items + gridDim.x - 1) / gridDim.x) * (double)(min((uint32_t)s, nsub) + PLS_WARM);
-            if (tt < best - 1e-9) best = tt, span = s;
-        }
-    }
-    const uint32_t per = (nsub + span - 1) / span;
-    for (uint64_t item = blockIdx.x; item < (uint64_t)nact * per; item += gridDim.x) {
-        const int r = (int)(item / per);
-        if (tid < 32) {  // the r-th active stream
-            int seen = 0;
-            for (int b = 0; b < S; b += 32) {
-                const unsigned m = __ballot_sync(0xffffffffu, b + (int)lane < S && meta[b + lane].active);
-                if (seen + __popc(m) > r) {
-                    if (lane == 0) item_stream = b + __fns(m, 0, r - seen + 1);
-                    break;
-                }
-                seen += __popc(m);
-            }
-        }
-        __syncthreads();
-        const int j = item_stream;
-        pl_span_item(in, in_stride, n, j, prevd_all, (uint64_t)(item % per) * span * PLS_T, span, plsm);
-        __syncthreads();
     }
 }
 
@@ -1800,16 +1660,8 @@ void DeflateBatch::run(const uint8_t *in, uint64_t in_stride, int S, uint64_t n,
                 if (t < best - 1e-9) best = t, span = s;
             }
         }
-        static const int pl_mode = getenv("IPCG_PL_MODE") ? atoi(getenv("IPCG_PL_MODE")) : 0;  // dev: 1 serial
-        if (pl_mode == 1 || n >= (1ull << 31)) {
-            k_prevlinks<<<dim3((unsigned)((nblk + span * PL_WARPS - 1) / (span * PL_WARPS)), S), PL_WARPS * 32, smem, st>>>(in, in_stride, n, w.meta, w.prevd, span);
-            CKL();
-        } else {
-            if (first_on_device<3>())
-                CK(cudaFuncSetAttribute(k_pl_span, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)PLS_SMEM));
-            k_pl_span<<<num_sms(), PLS_THREADS, PLS_SMEM, st>>>(in, in_stride, (uint32_t)n, w.meta, S, w.prevd);
-            CKL();
-        }
+        k_prevlinks<<<dim3((unsigned)((nblk + span * PL_WARPS - 1) / (span * PL_WARPS)), S), PL_WARPS * 32, smem, st>>>(in, in_stride, n, w.meta, w.prevd, span);
+        CKL();
         }
         // sparse streams (meta.od, k_select) take the on-demand parse, the others the all-position
         // search; each kernel below skips the streams of the other path
