@@ -174,11 +174,18 @@ static int prio_for(bool low) {
     CK(cudaDeviceGetStreamPriorityRange(&least, &greatest));
     return low ? least : greatest;
 }
+// dev: IPCG_PRIO_MODE=1 inverts the lossless streams (level 1 highest, coarser levels lowest),
+// 2 puts every lossless stream at the default priority
+static int lossless_prio(bool level1) {
+    static const int mode = getenv("IPCG_PRIO_MODE") ? atoi(getenv("IPCG_PRIO_MODE")) : 0;
+    if (mode == 2) return 0;
+    return prio_for(mode == 1 ? !level1 : level1);
+}
 
 cudaStream_t side_stream(ipcg_ctx *c, size_t i) {
     while (c->side.size() <= i) {
         cudaStream_t s;
-        CK(cudaStreamCreateWithPriority(&s, cudaStreamNonBlocking, prio_for(c->side.size() == 1)));
+        CK(cudaStreamCreateWithPriority(&s, cudaStreamNonBlocking, lossless_prio(c->side.size() == 1)));
         c->side.push_back(s);
     }
     return c->side[i];
@@ -206,7 +213,7 @@ cudaStream_t quant_stream(ipcg_ctx *c) {
 cudaStream_t od_stream(ipcg_ctx *c, size_t li) {
     while (c->odside.size() <= li) {
         cudaStream_t s;
-        CK(cudaStreamCreateWithPriority(&s, cudaStreamNonBlocking, prio_for(c->odside.size() == 0)));
+        CK(cudaStreamCreateWithPriority(&s, cudaStreamNonBlocking, lossless_prio(c->odside.size() == 0)));
         c->odside.push_back(s);
     }
     return c->odside[li];
@@ -322,29 +329,31 @@ struct CopyDesc {
     uint64_t len;
 };
 
-__global__ void k_gather(const CopyDesc *d, int nd, uint8_t *dst) {
+__global__ void __launch_bounds__(512) k_gather(const CopyDesc *d, int nd, uint8_t *dst) {
     const int i = blockIdx.x;
     if (i >= nd) return;
     const CopyDesc c = d[i];
     uint8_t *o = dst + c.dst_off;
     const uint8_t *s = c.src;
     uint64_t len = c.len;
-    // bytes until the destination is 4-byte aligned, then aligned 32-bit stores whose source
-    // words are funnel-shifted from aligned loads (archive payloads start at arbitrary bytes),
-    // then the tail bytes
-    const uint64_t head = min(len, (uint64_t)((4 - ((uintptr_t)o & 3)) & 3));
+    // bytes until the destination is 16-byte aligned (plane rows are), then 16-byte stores whose
+    // source words are funnel-shifted from aligned 4-byte loads (archive payloads start at
+    // arbitrary bytes), then the tail bytes
+    const uint64_t head = min(len, (uint64_t)((16 - ((uintptr_t)o & 15)) & 15));
     if (threadIdx.x < head) o[threadIdx.x] = s[threadIdx.x];
     o += head, s += head, len -= head;
-    const uint64_t nw = len / 4;
+    const uint64_t nv = len / 16;
     const unsigned sh = (unsigned)((uintptr_t)s & 3) * 8;
     const uint32_t *sw = reinterpret_cast<const uint32_t *>((uintptr_t)s & ~uintptr_t(3));
-    uint32_t *ow = reinterpret_cast<uint32_t *>(o);
-    if (sh == 0) {
-        for (uint64_t k = threadIdx.x; k < nw; k += blockDim.x) ow[k] = sw[k];
-    } else {
-        for (uint64_t k = threadIdx.x; k < nw; k += blockDim.x) ow[k] = __funnelshift_r(sw[k], sw[k + 1], sh);
+    uint4 *ov = reinterpret_cast<uint4 *>(o);
+    for (uint64_t k = threadIdx.x; k < nv; k += blockDim.x) {
+        const uint32_t *q = sw + 4 * k;
+        const uint32_t w0 = __ldg(q), w1 = __ldg(q + 1), w2 = __ldg(q + 2), w3 = __ldg(q + 3);
+        const uint32_t w4 = sh ? __ldg(q + 4) : 0u;  // only read when the source is unaligned
+        ov[k] = make_uint4(__funnelshift_r(w0, w1, sh), __funnelshift_r(w1, w2, sh), __funnelshift_r(w2, w3, sh),
+                           __funnelshift_r(w3, w4, sh));
     }
-    for (uint64_t k = nw * 4 + threadIdx.x; k < len; k += blockDim.x) o[k] = s[k];
+    for (uint64_t k = nv * 16 + threadIdx.x; k < len; k += blockDim.x) o[k] = s[k];
 }
 
 // dst == nullptr: dst_off are absolute device addresses
@@ -352,7 +361,7 @@ void gather(ipcg_ctx *c, std::vector<CopyDesc> descs, uint8_t *dst) {
     // split long copies so every SM participates
     std::vector<CopyDesc> pieces;
     pieces.reserve(descs.size());
-    const uint64_t piece = 256 << 10;
+    const uint64_t piece = 64 << 10;
     for (const CopyDesc &d : descs)
         for (uint64_t o = 0; o < d.len; o += piece)
             pieces.push_back(CopyDesc{d.src + o, d.dst_off + o, std::min(piece, d.len - o)});
@@ -361,7 +370,7 @@ void gather(ipcg_ctx *c, std::vector<CopyDesc> descs, uint8_t *dst) {
     CopyDesc *h = static_cast<CopyDesc *>(pinned(c, pieces.size() * sizeof(CopyDesc)));
     std::memcpy(h, pieces.data(), pieces.size() * sizeof(CopyDesc));
     CK(cudaMemcpyAsync(dd.p, h, pieces.size() * sizeof(CopyDesc), cudaMemcpyHostToDevice, c->stream));
-    k_gather<<<(unsigned)pieces.size(), 256, 0, c->stream>>>(dd.as<CopyDesc>(), (int)pieces.size(), dst);
+    k_gather<<<(unsigned)pieces.size(), 512, 0, c->stream>>>(dd.as<CopyDesc>(), (int)pieces.size(), dst);
     CKL();
     CK(cudaStreamSynchronize(c->stream));  // the pinned staging is reused by the next call
 }

@@ -383,44 +383,66 @@ __global__ void __launch_bounds__(256) k_merge(const uint32_t *const *__restrict
     }
 }
 
-// Refinement step adding few planes (k1 - k0 <= 8) on top of merged codewords: no transpose;
-// for each word lane c takes bit c of every new plane word (a broadcast load), ORs in the
-// prefix's XOR-encoded digits and solves the recurrence.  One coalesced codeword load and
-// store per word; 4 words per warp iteration for memory-level parallelism.
-constexpr int MF_U = 8;  // plane words (x 32 codewords) per warp per step: loads in flight
+// Refinement step adding few planes (k1 - k0 <= 8) on top of merged codewords: no transpose.
+// A thread takes MF_V groups of 4 consecutive codewords (16-byte loads and stores of the merged
+// codes); the 4 digits of each new plane come from one plane word shared by 8 neighbouring
+// threads (an L1 broadcast).  The prefix's XOR-encoded digits are OR-ed in and the recurrence
+// solved per codeword.
+#ifndef IPCG_MFV
+#define IPCG_MFV 4
+#endif
+constexpr int MF_V = IPCG_MFV;
+__device__ __forceinline__ uint4 merge_few4(uint4 m, const uint32_t *const *r, int np, int k0, uint64_t w,
+                                            unsigned b, uint32_t pre, uint32_t keep) {
+    uint32_t e[4] = {m.x & pre, m.y & pre, m.z & pre, m.w & pre};
+#pragma unroll
+    for (int j = 0; j < 4; ++j) e[j] = (e[j] ^ (e[j] >> 1) ^ (e[j] >> 2)) & pre;
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+        if (q >= np) break;
+        const uint32_t nib = (__ldg(r[q] + w) >> b) & 15u;
+        const int sh = 31 - (k0 + q);
+#pragma unroll
+        for (int j = 0; j < 4; ++j) e[j] |= ((nib >> j) & 1u) << sh;
+    }
+    return make_uint4(xor_decode_word(e[0]) & keep, xor_decode_word(e[1]) & keep, xor_decode_word(e[2]) & keep,
+                      xor_decode_word(e[3]) & keep);
+}
+
 __global__ void __launch_bounds__(256) k_merge_few(const uint32_t *const *__restrict__ rows,
                                                    const uint32_t *__restrict__ merged_in,
                                                    uint32_t *__restrict__ merged_out, uint64_t count, int k0, int k1) {
-    const unsigned lane = threadIdx.x & 31;
-    const uint64_t words = (count + 31) / 32;
     const uint32_t pre = k0 == 0 ? 0u : ~0u << (32 - k0);
     const uint32_t keep = k1 >= 32 ? ~0u : ~0u << (32 - k1);
     const int np = k1 - k0;
     const uint32_t *r[8];
 #pragma unroll
     for (int q = 0; q < 8; ++q) r[q] = q < np ? rows[k0 + q] : nullptr;
-    const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
-    for (uint64_t w0 = (((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5) * MF_U; w0 < words; w0 += nwarps * MF_U) {
-        uint32_t m[MF_U], e[MF_U];
+    const uint64_t g0 = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) * MF_V;  // first 4-codeword group
+    const uint64_t full = count / 4;  // whole groups
+    uint4 m[MF_V];
 #pragma unroll
-        for (int u = 0; u < MF_U; ++u) {
-            const uint64_t i = (w0 + u) * 32 + lane;
-            m[u] = i < count ? __ldg(merged_in + i) & pre : 0u;
-            e[u] = (m[u] ^ (m[u] >> 1) ^ (m[u] >> 2)) & pre;
-        }
+    for (int v = 0; v < MF_V; ++v) {
+        const uint64_t g = g0 + v;
+        m[v] = g < full && merged_in ? __ldg(reinterpret_cast<const uint4 *>(merged_in) + g) : make_uint4(0, 0, 0, 0);
+    }
 #pragma unroll
-        for (int q = 0; q < 8; ++q) {
-            if (q >= np) break;
-#pragma unroll
-            for (int u = 0; u < MF_U; ++u) {
-                const uint32_t x = w0 + u < words ? __ldg(r[q] + w0 + u) : 0u;
-                e[u] |= ((x >> lane) & 1u) << (31 - (k0 + q));
+    for (int v = 0; v < MF_V; ++v) {
+        const uint64_t g = g0 + v;
+        if (g < full) {
+            reinterpret_cast<uint4 *>(merged_out)[g] = merge_few4(m[v], r, np, k0, g / 8, (unsigned)(g % 8) * 4, pre, keep);
+        } else if (g == full && count % 4) {  // tail group
+            uint4 t = make_uint4(0, 0, 0, 0);
+            const uint64_t i0 = g * 4;
+            if (merged_in) {
+                t.x = merged_in[i0];
+                if (i0 + 1 < count) t.y = merged_in[i0 + 1];
+                if (i0 + 2 < count) t.z = merged_in[i0 + 2];
             }
-        }
-#pragma unroll
-        for (int u = 0; u < MF_U; ++u) {
-            const uint64_t i = (w0 + u) * 32 + lane;
-            if (i < count) merged_out[i] = xor_decode_word(e[u]) & keep;
+            const uint4 o = merge_few4(t, r, np, k0, g / 8, (unsigned)(g % 8) * 4, pre, keep);
+            merged_out[i0] = o.x;
+            if (i0 + 1 < count) merged_out[i0 + 1] = o.y;
+            if (i0 + 2 < count) merged_out[i0 + 2] = o.z;
         }
     }
 }
@@ -742,10 +764,13 @@ void launch_merge(const uint32_t *const *rows, const uint32_t *merged_in, uint32
     const uint64_t words = (count + 31) / 32;
     if (words == 0) return;
     if (merged_in && k0 > 0 && k1 - k0 <= 8) {
-        const unsigned g = (unsigned)std::min<uint64_t>(((words + MF_U - 1) / MF_U + 7) / 8, 148ull * 16);
+        const uint64_t groups = count / 4 + 1;  // + the tail group
+        const unsigned g = (unsigned)((groups + 256 * MF_V - 1) / (256 * MF_V));
         k_merge_few<<<g, 256, 0, st>>>(rows, merged_in, merged_out, count, k0, k1);
     } else {
-        const unsigned g = (unsigned)std::min<uint64_t>(((words + 31) / 32 + 7) / 8, 148ull * 8);
+        // a warp per 32 plane words, no grid-stride loop: the scheduler keeps replacing finished
+        // warps, so loads stay in flight (a capped grid serialised load -> transpose -> store per warp)
+        const unsigned g = (unsigned)(((words + 31) / 32 + 7) / 8);
         k_merge<<<g, 256, 0, st>>>(rows, merged_in, merged_out, count, k0, k1);
     }
     CKL();
