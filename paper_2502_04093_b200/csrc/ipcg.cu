@@ -904,21 +904,42 @@ void retrieve_impl(ipcg_ctx *c, ipcg_archive *a, int scalar, const int *k, void 
         CK(cudaMemcpyAsync(pd.p, hp, R * 8, cudaMemcpyHostToDevice, st));
         CK(cudaMemcpyAsync(ld.p, hp + R * 8, R * 8, cudaMemcpyHostToDevice, st));
         CK(cudaStreamSynchronize(st));  // pinned ptr/len table consumed
+        // CRC-32 of every payload on a side stream, concurrent with the copies and the inflate
+        // (which validate everything they read and never fault on corrupt input); the checks
+        // run after the inflate in backend_decode's order -- every checksum, then identity
+        // lengths, then the inflate status -- so the reported error is unchanged
+        c->events_used = 0;
+        const cudaStream_t cs = profiler().enabled ? st : side_stream(c, 0);
+        if (cs != st) stream_dep(c, st, cs);
         {
             uint64_t cb = 0;
             for (uint64_t x : lens) cb += x;
-            ProfScope ps("crc_check", st, cb);
-            crc32_batch(pd.as<const uint8_t *>(), ld.as<uint64_t>(), (int)R, maxp, crcs.as<uint32_t>(), crcws.p, cw, st);
+            ProfScope ps("crc_check", cs, cb);
+            crc32_batch(pd.as<const uint8_t *>(), ld.as<uint64_t>(), (int)R, maxp, crcs.as<uint32_t>(), crcws.p, cw, cs);
         }
-        std::vector<uint32_t> hcrc(R);
-        readback(hcrc.data(), crcs.p, R * 4, st);
-        for (size_t i = 0; i < R; ++i)
-            if (hcrc[i] != refs[i].crc) throw Error(ERUNTIME, "block checksum mismatch");
+        struct JoinOnExit {  // an exception before check_crcs still orders the CRC's buffers' release
+            ipcg_ctx *c;
+            cudaStream_t from, to;
+            ~JoinOnExit() {
+                if (from != to) {
+                    cudaEvent_t e = pool_event(c);
+                    cudaEventRecord(e, from);
+                    cudaStreamWaitEvent(to, e, 0);
+                }
+            }
+        } join_crc{c, cs, st};
+        auto check_crcs = [&] {
+            if (cs != st) stream_dep(c, cs, st);
+            std::vector<uint32_t> hcrc(R);
+            readback(hcrc.data(), crcs.p, R * 4, st);
+            for (size_t i = 0; i < R; ++i)
+                if (hcrc[i] != refs[i].crc) throw Error(ERUNTIME, "block checksum mismatch");
+            for (size_t i = 0; i < R; ++i) {
+                const uint64_t pbytes = (ix.records[refs[i].level - 1].count + 7) / 8;
+                if (refs[i].backend == 0 && refs[i].plen != pbytes) throw Error(ERUNTIME, "identity block has wrong length");
+            }
+        };
     tm.mark("crc");
-        for (size_t i = 0; i < R; ++i) {
-            const uint64_t pbytes = (ix.records[refs[i].level - 1].count + 7) / 8;
-            if (refs[i].backend == 0 && refs[i].plen != pbytes) throw Error(ERUNTIME, "identity block has wrong length");
-        }
         if (!copies.empty()) gather(c, copies, nullptr);
     tm.mark("copies");
         // identical deflate payloads (typically the all-zero high planes) decode once:
@@ -966,10 +987,13 @@ void retrieve_impl(ipcg_ctx *c, ipcg_archive *a, int scalar, const int *k, void 
                 ProfScope ps("inflate", st, ib);
                 inflate_batch_host(todo, sd.as<int>(), tmp, st);
             }
+            check_crcs();
             std::vector<int> status(todo.size());
             readback(status.data(), sd.p, todo.size() * 4, st);
             for (int s : status)
                 if (s) throw Error(ERUNTIME, "deflate backend failed to decompress block");
+        } else {
+            check_crcs();
         }
     tm.mark("inflate");
     }
