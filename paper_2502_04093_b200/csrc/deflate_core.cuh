@@ -567,9 +567,9 @@ struct BlockTrees {
 // reaches the 7 bits kept here.  heap[heap_max..] then holds the nodes in zlib's order for
 // gen_bitlen.
 struct TreeScratch {
+    alignas(8) uint32_t heap[HEAP_SIZE + 1];  // 8-byte aligned, one spare entry: pqdownheap reads child pairs
     uint16_t freq[HEAP_SIZE];     // leaf frequencies (input; forced leaves set to 1)
     uint16_t dad_len[HEAP_SIZE];  // zlib's dl union: Dad during build, Len after gen_bitlen
-    uint32_t heap[HEAP_SIZE];
     uint16_t bl_count[MAX_BITS + 1];
     int heap_len, heap_max;
 };
@@ -580,16 +580,22 @@ HD uint32_t hmake(uint32_t freq, uint32_t depth, int node) {
 HD uint32_t hkey(uint32_t e) { return e >> 10; }
 HD int hnode(uint32_t e) { return (int)(e & 1023); }
 
+// (the two children heap[j], heap[j+1] -- j even -- come in one 8-byte load; keys compare as
+// e | 1023, the node bits set, which orders like e >> 10; heap_len stays in a register.  The
+// k_plan tree builds are issue-bound and this loop was over half of their instructions.)
+struct alignas(8) HeapPair {
+    uint32_t x, y;
+};
 HD void pqdownheap(TreeScratch &t, int k) {
     const uint32_t v = t.heap[k];
+    const uint32_t vk = v | 1023u;
+    const int len = t.heap_len;
     int j = k << 1;
-    while (j <= t.heap_len) {
-        uint32_t hj = t.heap[j];
-        if (j < t.heap_len) {
-            const uint32_t hj1 = t.heap[j + 1];
-            if (hkey(hj1) <= hkey(hj)) j++, hj = hj1;
-        }
-        if (hkey(v) <= hkey(hj)) break;
+    while (j <= len) {
+        const HeapPair c = *reinterpret_cast<const HeapPair *>(&t.heap[j]);  // heap[j + 1] unused when j == len
+        uint32_t hj = c.x;
+        if (j < len && (c.y | 1023u) <= (c.x | 1023u)) j++, hj = c.y;
+        if (vk <= (hj | 1023u)) break;
         t.heap[k] = hj;
         k = j;
         j <<= 1;
