@@ -1244,6 +1244,47 @@ __global__ void k_fill_zero(const InflateJob *jobs, const JobMeta *meta) {
 // -------------------------------------------------------------------- 4. emit
 __device__ __forceinline__ bool flag_get(const uint32_t *f, uint64_t i) { return (f[i >> 5] >> (i & 31)) & 1u; }
 
+// bytes [mo, tend) all repeat byte mo-1 (distance-1 matches); every lane calls it
+__device__ __forceinline__ void emit_run(const Tables &T, uint8_t *dst, uint64_t mo, uint64_t tend, uint64_t b0,
+                                         unsigned lane) {
+    const uint64_t s = mo - 1;
+    bool unres = true;
+    uint32_t P = (uint32_t)s;
+    uint8_t val = 0;
+    if (s >= b0) {
+        if (flag_get(T.flags, s)) P = T.ptr[s];
+        else unres = false, val = dst[s];
+    }
+    if (unres) {
+        // 16-byte stores from the first index whose address is 16-byte aligned
+        const uint64_t pb = reinterpret_cast<uintptr_t>(T.ptr) / 4;  // ptr is 4-byte aligned
+        const uint64_t a = min(tend, ((pb + mo + 3) & ~(uint64_t)3) - pb), be = (pb + tend) & ~(uint64_t)3;
+        const uint64_t b = be > pb + a ? be - pb : a;
+        for (uint64_t x = mo + lane; x < a; x += 32) T.ptr[x] = P;
+        const uint4 PP = make_uint4(P, P, P, P);
+        uint4 *p4 = reinterpret_cast<uint4 *>(T.ptr + a);
+        for (uint64_t x = lane; x < (b - a) / 4; x += 32) p4[x] = PP;
+        for (uint64_t x = b + lane; x < tend; x += 32) T.ptr[x] = P;
+        // flag bits: partial words at the ends by atomics (their other bits belong to other
+        // symbols, possibly other warps' segments), whole words stored
+        const uint64_t fa = min(tend, (mo + 31) & ~(uint64_t)31), fb = max(fa, tend & ~(uint64_t)31);
+        if (lane == 0 && mo < fa) atomicOr(&T.flags[mo >> 5], ((1u << (uint32_t)(fa - mo)) - 1u) << (mo & 31));
+        for (uint64_t w = fa / 32 + lane; w < fb / 32; w += 32) T.flags[w] = 0xffffffffu;
+        if (lane == 1 && fb < tend) atomicOr(&T.flags[fb >> 5], (1u << (uint32_t)(tend - fb)) - 1u);
+    } else {
+        const uint64_t db = reinterpret_cast<uintptr_t>(dst);
+        const uint64_t a = min(tend, ((db + mo + 15) & ~(uint64_t)15) - db), be = (db + tend) & ~(uint64_t)15;
+        const uint64_t b = be > db + a ? be - db : a;
+        for (uint64_t x = mo + lane; x < a; x += 32) dst[x] = val;
+        const uint32_t w4 = (uint32_t)val * 0x01010101u;
+        const uint4 VV = make_uint4(w4, w4, w4, w4);
+        uint4 *d4 = reinterpret_cast<uint4 *>(dst + a);
+        for (uint64_t x = lane; x < (b - a) / 16; x += 32) d4[x] = VV;
+        for (uint64_t x = b + lane; x < tend; x += 32) dst[x] = val;
+    }
+    __syncwarp();
+}
+
 __global__ void __launch_bounds__(WARPS * 32) k_emit(const InflateJob *jobs, const Tables *tabs, JobMeta *meta,
                                                    const uint32_t *pool, const uint32_t *ckpt_pool) {
     // one warp per emit segment (SEG symbols of one block, output offset from the
@@ -1298,12 +1339,25 @@ __global__ void __launch_bounds__(WARPS * 32) k_emit(const InflateJob *jobs, con
         if (valid && !ismatch && !check_only) dst[o + my_rel] = (uint8_t)v;
         __syncwarp();
         unsigned mm = __ballot_sync(0xffffffffu, ismatch);
+        const unsigned r1 = __ballot_sync(0xffffffffu, ismatch && (v & 0xffffu) == 0u);  // distance-1 matches
         while (mm) {
             const int l = __ffs(mm) - 1;
-            mm &= mm - 1;
             const uint32_t mv = __shfl_sync(0xffffffffu, v, l);
             const uint64_t mo = o + __shfl_sync(0xffffffffu, my_rel, l);
             const uint32_t len = (mv >> 16) & 0x1ff, d = (mv & 0xffff) + 1;
+            if (d == 1u && mo >= 1 && !check_only) {
+                // a run: consecutive distance-1 matches (lanes l .. e-1) all repeat the byte before
+                // the first, so the whole run is one fill -- of its value when that byte is
+                // resolved, else of its pointer with the flag bits set -- in 16-byte stores (the
+                // per-match byte loop was the emit's latency on run-heavy planes)
+                const unsigned above = ~r1 & (0xffffffffu << l);
+                const int e = above ? __ffs(above) - 1 : 32;
+                mm &= e == 32 ? 0u : (0xffffffffu << e);
+                const uint64_t tend = o + __shfl_sync(0xffffffffu, incl, e - 1);
+                emit_run(T, dst, mo, tend, b0, lane);
+                continue;
+            }
+            mm &= mm - 1;
             if ((uint64_t)d > mo) {  // warp-uniform
                 if (lane == 0) atomicOr(&jm.bad, 1);
                 continue;
@@ -1669,6 +1723,7 @@ __global__ void k_setup(const InflateJob *jobs, int njobs, Tables *tabs, uint8_t
     a += T.bcap * sizeof(Blk);
     T.fallback = reinterpret_cast<uint32_t *>(a);
     a += T.fcap * 4;
+    a = reinterpret_cast<uint8_t *>(((uintptr_t)a + 15) & ~uintptr_t(15));  // k_emit's run fills store 16 bytes
     T.ptr = reinterpret_cast<uint32_t *>(a);
     tabs[j] = T;
 }
