@@ -1286,18 +1286,29 @@ __device__ __forceinline__ void emit_run(const Tables &T, uint8_t *dst, uint64_t
 }
 
 __global__ void __launch_bounds__(WARPS * 32) k_emit(const InflateJob *jobs, const Tables *tabs, JobMeta *meta,
-                                                   const uint32_t *pool, const uint32_t *ckpt_pool) {
+                                                   const uint32_t *pool, const uint32_t *ckpt_pool, const uint64_t *segoff,
+                                                   int njobs) {
     // one warp per emit segment (SEG symbols of one block, output offset from the
     // candidate's checkpoints); copies reaching before the segment become pointers.
     // A match whose distance exceeds the bytes written before it is zlib's "invalid distance
     // too far back": the job fails (meta.bad) and nothing is written for it.  All-zero jobs
     // (filled by k_fill_zero) still run their first 32 KiB of output here, check only.
-    const int j = blockIdx.y;
+    // the grid covers the segments of every job back to back (segoff: their prefix sums; a
+    // (segment, job) grid left ~95% of a cfg2 retrieval's CTAs with nothing to do)
+    const unsigned w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint64_t gg = (uint64_t)blockIdx.x * WARPS + w;
+    if (gg >= segoff[njobs]) return;
+    int jl = 0, jh = njobs - 1;  // last job with segoff[j] <= gg
+    while (jl < jh) {
+        const int mid = (jl + jh + 1) / 2;
+        if (segoff[mid] <= gg) jl = mid;
+        else jh = mid - 1;
+    }
+    const int j = jl;
     JobMeta &jm = meta[j];
     if (jm.status) return;
     const bool check_only = jm.allzero != 0;
-    const unsigned w = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const uint64_t gs = (uint64_t)blockIdx.x * WARPS + w;
+    const uint64_t gs = gg - segoff[j];
     if (gs >= jm.nseg) return;
     const InflateJob job = jobs[j];
     const Tables T = tabs[j];
@@ -1365,7 +1376,7 @@ __global__ void __launch_bounds__(WARPS * 32) k_emit(const InflateJob *jobs, con
             if (check_only) continue;
             // i % d by a reciprocal multiply (exact for i < 2^16: i < len <= 258; d = 1 apart,
             // whose reciprocal 2^32 does not fit)
-            const uint32_t rcp = 0xffffffffu / d + 1u;
+            const uint32_t rcp = (d > 1u && d < len) ? 0xffffffffu / d + 1u : 0u;  // (an integer division: only when used)
             // every source byte precedes mo, so the lanes of one match never depend on each other;
             // unresolved bytes (sources in earlier segments) get a pointer, and their flag bits
             // are set with one ballot-aggregated atomic per 32 bytes
@@ -1883,7 +1894,12 @@ void inflate_batch_host(const std::vector<InflateJob> &jobs, int *status_dev, De
         }
         {
             ProfScope ps2("inflate.emit_blocks", st, max_dst * n);
-            k_emit<<<dim3((unsigned)((maxseg + WARPS - 1) / WARPS), n), WARPS * 32, 0, st>>>(jd, td, md, pool, ckpt);
+            std::vector<uint64_t> so(n + 1, 0);
+            for (int q = 0; q < n; ++q) so[q + 1] = so[q] + (hm[q].status ? 0 : hm[q].nseg);
+            uint64_t *sod = static_cast<uint64_t *>(alloc.get((n + 1) * 8, st));
+            CK(cudaMemcpyAsync(sod, so.data(), (n + 1) * 8, cudaMemcpyHostToDevice, st));
+            if (so[n])
+                k_emit<<<(unsigned)((so[n] + WARPS - 1) / WARPS), WARPS * 32, 0, st>>>(jd, td, md, pool, ckpt, sod, n);
             CKL();
             k_fill_zero<<<dim3(grid_for(max_dst / 16 + 1, 256, 512), n), 256, 0, st>>>(jd, md);
             CKL();
