@@ -218,7 +218,10 @@ __device__ bool read_dynamic_header(Bits &b, uint8_t *lens, int &nlen, int &ndis
 #ifndef IPCG_STAGE
 #define IPCG_STAGE 1
 #endif
-constexpr int LITBITS = 11, DISTBITS = IPCG_DISTBITS;
+#ifndef IPCG_LITBITS
+#define IPCG_LITBITS 11
+#endif
+constexpr int LITBITS = IPCG_LITBITS, DISTBITS = IPCG_DISTBITS;
 template <int BITS>
 struct Huff {
     uint16_t count[16];
@@ -640,14 +643,20 @@ __global__ void __launch_bounds__(DWARPS * 32) k_decode_cands(const InflateJob *
     constexpr unsigned G = 32 / CPW;
     __shared__ Huff<LITBITS> lit_s[DWARPS * CPW];
     __shared__ Huff<DISTBITS> dist_s[DWARPS * CPW];
-    __shared__ uint8_t lens_s[DWARPS * CPW][320];
     __shared__ uint32_t marks_s[DWARPS][NPH * 32 * MARKW];
     __shared__ uint32_t li_e1[DWARPS][NPH][32], li_x[DWARPS][NPH][32];  // per lane and phase
     __shared__ int8_t li_sync[DWARPS][NPH][32];
+    __shared__ int8_t li_skip[DWARPS][NPH][32];    // 1: the continuation met lane gl+2's path (gl+1 covered)
+    __shared__ uint32_t li_x1[DWARPS][NPH][32];    // its first symbol start in lane gl+2's subsequence
+    // symbol counts and output bytes: of the P1 path (n1, b1), of the whole continuation (nc, bc)
+    // and of its part before lane gl+2's subsequence (nx, bx) -- P3 counts a lane's true range
+    // from these instead of decoding it again
+    __shared__ uint16_t li_n1[DWARPS][NPH][32], li_nc[DWARPS][NPH][32], li_nx[DWARPS][NPH][32];
+    __shared__ uint32_t li_b1[DWARPS][NPH][32], li_bc[DWARPS][NPH][32], li_bx[DWARPS][NPH][32];
     __shared__ uint8_t li_fl[DWARPS][NPH][32];  // 1: path ends in own subsequence, 2: in the next  // symbol-start bitmaps of the lane subsequences
     // the round's bits (32 subsequences + the reach of the last symbols), staged once per round:
     // the per-symbol window loads were the decode's top stall (L1 misses on the critical path)
-    constexpr int STG = IPCG_STAGE ? 32 * SUBB / 32 + 8 : 4;
+    constexpr int STG = IPCG_STAGE ? 32 * SUBB / 32 + 8 : 80;  // (>= 80 words: the code lengths live here first)
     __shared__ uint32_t stg_s[DWARPS][STG];
     const unsigned w = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const unsigned sub = lane / G, gl = lane % G, slot = w * CPW + sub;
@@ -671,10 +680,12 @@ __global__ void __launch_bounds__(DWARPS * 32) k_decode_cands(const InflateJob *
             }
         }
         if (act && gl == 0)
-            for (int i = 0; i < nlen + ndist; ++i) lens_s[slot][i] = lens[i];
+            for (int i = 0; i < nlen + ndist; ++i) reinterpret_cast<uint8_t *>(stg_s[slot])[i] = lens[i];
         __syncwarp();
-        huff_build_group(lit_s[slot], lens_s[slot], nlen, gl, G, act, false);
-        huff_build_group(dist_s[slot], lens_s[slot] + nlen, ndist, gl, G, act, true);
+        // (the code lengths sit in the staging buffer until the tables are built)
+        huff_build_group(lit_s[slot], reinterpret_cast<const uint8_t *>(stg_s[slot]), nlen, gl, G, act, false);
+        huff_build_group(dist_s[slot], reinterpret_cast<const uint8_t *>(stg_s[slot]) + nlen, ndist, gl, G, act, true);
+        __syncwarp();
         if (act) {  // (no early exits: every lane reaches the syncs below)
         uint32_t *out = pool + ci * (uint64_t)MAXSYM;
         uint32_t ns = 0, nz = 0;
@@ -741,30 +752,45 @@ __global__ void __launch_bounds__(DWARPS * 32) k_decode_cands(const InflateJob *
                 uint32_t *mk = marks + (ph * 32 + gl) * MARKW;
                 for (int q = 0; q < MARKW; ++q) mk[q] = 0u;
                 uint64_t p = g + ph;
-                uint32_t k1 = 0;
+                uint32_t k1 = 0, c1 = 0, b1 = 0;
                 while (p < gn) {
                     const uint32_t r = (uint32_t)(p - g);
                     mk[r >> 5] |= 1u << (r & 31);
                     decode_symbol(lit_s[slot], dist_s[slot], window(p), k1, nb, bl);
                     if (k1 >= 2u) break;  // this path ends (end of block or invalid code) at p
+                    ++c1, b1 += bl;
                     p += nb;
                 }
                 li_e1[w][ph][gl] = (uint32_t)(p - base);
                 li_fl[w][ph][gl] = k1 >= 2u ? 1 : 0;
+                li_n1[w][ph][gl] = (uint16_t)c1;
+                li_b1[w][ph][gl] = b1;
             }
             __syncwarp();
             // P2: each phase's path continues into subsequence gl+1 until it meets a symbol start
             // of one of lane gl+1's paths (from there the two coincide)
+            // (a path that has not met lane gl+1's within its subsequence goes on through lane
+            // gl+2's: blocks of long match symbols -- extra bits resynchronise slowly -- lost the
+            // round at such lanes and took ~2x the rounds of their bit length)
             for (int ph = 0; ph < nph; ++ph) {
-                int hit = -1;
+                int hit = -1, skip = 0;
+                uint64_t x1 = 0;
+                uint32_t cc = 0, cb = 0, cx = 0, bx = 0;
                 uint8_t fl = li_fl[w][ph][gl];
                 uint64_t x = base + li_e1[w][ph][gl];
                 if (gl < 31 && !(fl & 1)) {
-                    const uint64_t g2 = gn + subb;
-                    while (x < g2) {
-                        const uint32_t r = (uint32_t)(x - gn);
-                        for (int q = 0; q < nph && hit < 0; ++q)
-                            if ((marks[(q * 32 + gl + 1) * MARKW + (r >> 5)] >> (r & 31)) & 1u) hit = q;
+                    const uint64_t g2 = gn + subb, g3 = gl < 30 ? g2 + subb : g2;
+                    while (x < g3) {
+                        if (x < g2) {
+                            const uint32_t r = (uint32_t)(x - gn);
+                            for (int q = 0; q < nph && hit < 0; ++q)
+                                if ((marks[(q * 32 + gl + 1) * MARKW + (r >> 5)] >> (r & 31)) & 1u) hit = q;
+                        } else {
+                            if (!x1) x1 = x, cx = cc, bx = cb;
+                            const uint32_t r = (uint32_t)(x - g2);
+                            for (int q = 0; q < nph && hit < 0; ++q)
+                                if ((marks[(q * 32 + gl + 2) * MARKW + (r >> 5)] >> (r & 31)) & 1u) hit = q, skip = 1;
+                        }
                         if (hit >= 0) break;
                         uint32_t k2;
                         decode_symbol(lit_s[slot], dist_s[slot], window(x), k2, nb, bl);
@@ -772,12 +798,17 @@ __global__ void __launch_bounds__(DWARPS * 32) k_decode_cands(const InflateJob *
                             fl |= 2;
                             break;
                         }
+                        ++cc, cb += bl;
                         x += nb;
                     }
                 }
                 li_x[w][ph][gl] = (uint32_t)(x - base);
                 li_sync[w][ph][gl] = (int8_t)hit;
+                li_skip[w][ph][gl] = (int8_t)skip;
+                li_x1[w][ph][gl] = (uint32_t)((x1 ? x1 : x) - base);
                 li_fl[w][ph][gl] = fl;
+                li_nc[w][ph][gl] = (uint16_t)cc, li_bc[w][ph][gl] = cb;
+                li_nx[w][ph][gl] = (uint16_t)(x1 ? cx : cc), li_bx[w][ph][gl] = x1 ? bx : cb;
             }
             __syncwarp();
             // resolve the true range [t_i, t_i+1) of every covered lane (uniform loop over shared
@@ -785,13 +816,24 @@ __global__ void __launch_bounds__(DWARPS * 32) k_decode_cands(const InflateJob *
             // i's true path met; a lane whose left neighbour met none is covered by that
             // neighbour's continuation, and the round ends there
             uint64_t my_t = 0, my_e = 0;
+            // how P3 counts my range: on my P1 path of phase my_ph from my_sp (continuation symbols
+            // my_pc/my_pb before it), or (my_ph < 0) wholly the left neighbour's continuation
+            int my_ph = -1;
+            uint64_t my_sp = 0;
+            uint32_t my_pc = 0, my_pb = 0;
             int last = -1;
             bool lost = false, other = false;
             {
                 uint64_t t = base;
-                int cur = 0;  // true phase of lane i, or -1: covered by lane i-1's continuation
+                int cur = 0;          // true phase of lane i, or -1: covered by lane i-1's continuation
+                int next_phase = -1;  // for a covered lane: the phase of lane i+1 its coverer met (-1: none)
                 uint64_t prev_x = 0;
                 bool prev_end2 = false;
+                uint64_t sp = base;      // lane i's sync point on its P1 path (cur >= 0)
+                uint32_t pc = 0, pb = 0;  // true symbols/bytes of lane i before sp (cur >= 0), or all of
+                                         // its range (cur < 0)
+                uint64_t nsp = 0;        // after a covered lane: the sync point / counts of the next
+                uint32_t npc = 0, npb = 0;
                 for (int i = 0; i < 32; ++i) {
                     uint64_t E;
                     bool stop;
@@ -803,18 +845,40 @@ __global__ void __launch_bounds__(DWARPS * 32) k_decode_cands(const InflateJob *
                         E = prev_x;
                         stop = prev_end2;
                     }
-                    if (gl == (unsigned)i) my_t = t, my_e = E;
+                    if (gl == (unsigned)i) my_t = t, my_e = E, my_ph = cur, my_sp = sp, my_pc = pc, my_pb = pb;
                     last = i;
                     t = E;
                     if (stop) break;  // end of block / invalid code inside lane i
                     if (cur < 0) {
-                        lost = true;
-                        break;
+                        if (next_phase < 0) {
+                            lost = true;
+                            break;
+                        }
+                        cur = next_phase;  // lane i+1 on the path lane i-1's continuation met
+                        next_phase = -1;
+                        sp = nsp, pc = npc, pb = npb;
+                        continue;
                     }
                     if (i == 31) break;
-                    prev_x = base + li_x[w][cur][i];
-                    prev_end2 = (li_fl[w][cur][i] & 2) != 0;
-                    cur = li_sync[w][cur][i];
+                    const int hit = li_sync[w][cur][i];
+                    const bool sk = hit >= 0 && li_skip[w][cur][i];
+                    if (sk) {
+                        // lane i+1 is covered up to the continuation's first symbol in lane i+2's
+                        // subsequence, where lane i+2's path `hit` takes over
+                        prev_x = base + li_x1[w][cur][i];
+                        prev_end2 = false;
+                        next_phase = hit;
+                        nsp = base + li_x[w][cur][i];
+                        npc = li_nc[w][cur][i] - li_nx[w][cur][i], npb = li_bc[w][cur][i] - li_bx[w][cur][i];
+                        pc = li_nx[w][cur][i], pb = li_bx[w][cur][i];
+                    } else {
+                        prev_x = base + li_x[w][cur][i];
+                        prev_end2 = (li_fl[w][cur][i] & 2) != 0;
+                        next_phase = -1;
+                        sp = prev_x;  // (hit: lane i+1's sync point; none: lane i+1 is covered)
+                        pc = li_nc[w][cur][i], pb = li_bc[w][cur][i];
+                    }
+                    cur = hit >= 0 && !sk ? hit : -1;
                 }
             }
             // speculate the other phases after a round that lost synchronisation within its first
@@ -822,11 +886,37 @@ __global__ void __launch_bounds__(DWARPS * 32) k_decode_cands(const InflateJob *
             // while some lane's true path is one of them; a loss further on costs little
             nph = ((lost && last < 4) || (nph > 1 && other)) ? NPH : 1;
             // P3: count my true range (the range of the last covered lane may end at the block's
-            // end-of-block or at an invalid code)
+            // end-of-block or at an invalid code).  From the counts P1/P2 kept: a lane on its P1
+            // path takes the continuation symbols before its sync point plus its P1 symbols from
+            // there (P1's prefix before the sync point -- a few symbols -- decoded again); a
+            // covered lane takes its coverer's continuation counts.  An empty last range (an
+            // end-of-block right at its start) is decoded as before.
             const bool mine = (int)gl <= last;
             uint32_t cnt = 0, byt = 0, kend = 0;
             uint64_t q = my_t;
-            if (mine) {
+            bool counted = false;
+            if (mine && !(my_t == my_e && (int)gl == last)) {
+                if (my_ph < 0) {
+                    cnt = my_pc, byt = my_pb, q = my_e, counted = true;
+                } else {
+                    uint64_t pp = g + (uint64_t)my_ph;
+                    uint32_t c0 = 0, b0c = 0;
+                    while (pp < my_sp) {
+                        uint32_t kk;
+                        decode_symbol(lit_s[slot], dist_s[slot], window(pp), kk, nb, bl);
+                        if (kk >= 2u) break;
+                        ++c0, b0c += bl;
+                        pp += nb;
+                    }
+                    if (pp == my_sp) {
+                        cnt = my_pc + li_n1[w][my_ph][gl] - c0;
+                        byt = my_pb + li_b1[w][my_ph][gl] - b0c;
+                        q = my_e, counted = true;
+                    }
+                }
+            }
+            if (mine && !counted) {
+                cnt = 0, byt = 0, q = my_t;
                 while (q < my_e || (q == my_e && (int)gl == last)) {
                     decode_symbol(lit_s[slot], dist_s[slot], window(q), kend, nb, bl);
                     if (kend >= 2u) {
@@ -1880,6 +1970,14 @@ void inflate_batch_host(const std::vector<InflateJob> &jobs, int *status_dev, De
             }
             unsigned long long hs = 0;
             CK(cudaMemcpy(&hs, nsurv, 8, cudaMemcpyDeviceToHost));
+            {
+                std::vector<std::pair<int, uint64_t>> rb;
+                for (const Cand &cc : hcands) rb.push_back({cc.rounds, cc.end_bit > cc.hdr_bit ? cc.end_bit - cc.hdr_bit : 0});
+                std::sort(rb.begin(), rb.end());
+                fprintf(stderr, "inflate: slowest candidates (rounds, bits, syms):");
+                for (size_t q = rb.size() > 8 ? rb.size() - 8 : 0; q < rb.size(); ++q) fprintf(stderr, " (%d, %llu)", rb[q].first, (unsigned long long)rb[q].second);
+                fprintf(stderr, "\n");
+            }
             fprintf(stderr, "inflate: %llu survivors of %llu bit offsets; decode rounds mean %.1f max %llu, bits/cand %.0f\n", hs,
                     (unsigned long long)total_src * 8, nc ? (double)rsum / nc : 0.0, (unsigned long long)rmax,
                     nc ? (double)bits_sum / nc : 0.0);
