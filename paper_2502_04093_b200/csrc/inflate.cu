@@ -407,17 +407,9 @@ __device__ __forceinline__ uint64_t hslot(uint64_t key, uint64_t cap) {
 constexpr int SCAN_TILE = 256 * 4;  // bytes per tile: 4 per thread = 32 bit offsets
 constexpr int SCAN_HALO = 16;       // a header's fixed part spans < 80 bits
 
-__device__ __forceinline__ void scan_offset(const InflateJob &job, const Tables &T, JobMeta *meta, int j,
+__device__ __forceinline__ void list_candidate(const InflateJob &job, const Tables &T, JobMeta *meta, int j,
                                             Cand *cands, unsigned long long *ncand_total, uint64_t cand_cap,
                                             uint64_t bit) {
-    Bits b;
-    b.init(job.src, job.src_len, bit + 3);
-    uint8_t lens[320];
-    Canon cs;
-    int nlen, ndist;
-    if (!read_dynamic_header(b, lens, nlen, ndist, cs)) return;
-    Canon cl;
-    if (!canon_build(cl, lens, nlen, 1) || !canon_build(cl, lens + nlen, ndist, 2)) return;
     const unsigned long long ci = atomicAdd(ncand_total, 1ull);
     if (ci >= cand_cap) {
         meta[j].overflow = 1;
@@ -555,8 +547,12 @@ __global__ void __launch_bounds__(256) k_validate(const InflateJob *jobs, const 
     const uint64_t ns = min((unsigned long long)surv_cap, *nsurv);
     for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < ns; i += (uint64_t)gridDim.x * blockDim.x) {
         const Survivor sv = surv[i];
+        // quick_header_ok is zlib's acceptance rule itself (same predicate as read_dynamic_header +
+        // canon_build), so an accepted header is listed directly; k_decode_cands reads it in full
+        // again and would still reject it (ok = 0).  (The full read here was a one-thread serial
+        // tail: ~0.4 ms per retrieval for the ~2000 real block headers.)
         if (!quick_header_ok(jobs[sv.job], sv.bit, qtab[threadIdx.x])) continue;
-        scan_offset(jobs[sv.job], tabs[sv.job], meta, sv.job, cands, ncand_total, cand_cap, sv.bit);
+        list_candidate(jobs[sv.job], tabs[sv.job], meta, sv.job, cands, ncand_total, cand_cap, sv.bit);
     }
 }
 
@@ -593,33 +589,32 @@ __global__ void __launch_bounds__(256) k_scan(const InflateJob *jobs, int njobs,
         const uint64_t byte0 = t0 + 4 * threadIdx.x;
         const uint32_t W0 = tw[threadIdx.x], W1 = tw[threadIdx.x + 1], W2 = tw[threadIdx.x + 2],
                        W3 = tw[threadIdx.x + 3];
-        const unsigned lane = threadIdx.x & 31;
-        for (int k = 0; k < 32; ++k) {  // warp-convergent: survivors appended with one atomic per warp
-            const uint64_t bit = byte0 * 8 + (uint64_t)k;
+        // the fixed-position filters for all 32 offsets at once (bit k of each mask is offset k):
+        // BTYPE = 2 (bit k+1 clear, bit k+2 set), HLIT <= 29 and HDIST <= 29 (not bits k+4..k+7,
+        // resp. k+9..k+12, all set); the Kraft sum of the code-length code only for the ~22% left
+        // (the per-offset test made this kernel issue-bound)
+        const uint64_t X = (uint64_t)W0 | ((uint64_t)W1 << 32);
+        uint32_t m = (uint32_t)((~(X >> 1)) & (X >> 2) & ~((X >> 4) & (X >> 5) & (X >> 6) & (X >> 7)) &
+                                ~((X >> 9) & (X >> 10) & (X >> 11) & (X >> 12)));
+        const uint64_t bit0 = byte0 * 8, nbits = job.src_len * 8;
+        if (bit0 < 16) m &= 0xffffffffu << (uint32_t)(16 - bit0);  // offsets >= 16 (after the zlib header)
+        if (bit0 + 32 > nbits) m &= nbits <= bit0 ? 0u : (1u << (uint32_t)(nbits - bit0)) - 1u;
+        while (m) {
+            const int k = __ffs(m) - 1;
+            m &= m - 1;
             const uint32_t f0 = __funnelshift_r(W0, W1, k), f1 = __funnelshift_r(W1, W2, k),
                            f2 = __funnelshift_r(W2, W3, k);
-            // BFINAL(1) BTYPE(2)=2 HLIT(5)<=29 HDIST(5)<=29 HCLEN(4)
-            bool ok = bit >= 16 && bit < job.src_len * 8 && ((f0 >> 1) & 3) == 2 && ((f0 >> 3) & 31) <= 29 &&
-                      ((f0 >> 8) & 31) <= 29;
-            if (ok) {
-                // code-length lengths: bits 17 .. 17 + 3*ncode of the window; complete code only
-                const int ncode = (int)((f0 >> 13) & 15) + 4;
-                const uint64_t lo2 = (uint64_t)f0 | ((uint64_t)f1 << 32);
-                uint64_t cl = (lo2 >> 17) | ((uint64_t)f2 << 47);  // 57 bits = 19 fields
-                cl &= (1ull << (3 * ncode)) - 1;
-                const uint32_t kraft = (uint32_t)kraft4[cl & 4095] + kraft4[(cl >> 12) & 4095] +
-                                       kraft4[(cl >> 24) & 4095] + kraft4[(cl >> 36) & 4095] +
-                                       kraft4[(cl >> 48) & 511];
-                ok = kraft == 128;
-            }
-            const unsigned m = __ballot_sync(0xffffffffu, ok);
-            if (!m) continue;
-            unsigned long long base = 0;
-            if (lane == (unsigned)__ffs(m) - 1) base = atomicAdd(nsurv, (unsigned long long)__popc(m));
-            base = __shfl_sync(0xffffffffu, base, __ffs(m) - 1);
-            if (ok) {
-                const unsigned long long si = base + __popc(m & ((1u << lane) - 1u));
-                if (si < surv_cap) surv[si] = Survivor{bit, j};
+            // code-length lengths: bits 17 .. 17 + 3*ncode of the window; complete code only
+            const int ncode = (int)((f0 >> 13) & 15) + 4;
+            const uint64_t lo2 = (uint64_t)f0 | ((uint64_t)f1 << 32);
+            uint64_t cl = (lo2 >> 17) | ((uint64_t)f2 << 47);  // 57 bits = 19 fields
+            cl &= (1ull << (3 * ncode)) - 1;
+            const uint32_t kraft = (uint32_t)kraft4[cl & 4095] + kraft4[(cl >> 12) & 4095] +
+                                   kraft4[(cl >> 24) & 4095] + kraft4[(cl >> 36) & 4095] +
+                                   kraft4[(cl >> 48) & 511];
+            if (kraft == 128) {  // rare (~1 in 1100 offsets): one atomic each
+                const unsigned long long si = atomicAdd(nsurv, 1ull);
+                if (si < surv_cap) surv[si] = Survivor{bit0 + (uint64_t)k, j};
                 else meta[j].overflow = 1;
             }
         }
@@ -1060,6 +1055,8 @@ struct RankWs {
     uint32_t *ss[2], *sn[2];
     uint8_t *sz[2];
     int *jump;  // [RANK_L][nc]
+    int *jhead;         // [njobs]: head candidate of a ranked stream, -1 otherwise
+    uint64_t *jpre;     // [njobs + 1]: prefix sums of the ranked streams' block counts
 };
 
 __global__ void __launch_bounds__(1024) k_rank(const InflateJob *jobs, int njobs, const Tables *tabs, JobMeta *meta,
@@ -1111,70 +1108,84 @@ __global__ void __launch_bounds__(1024) k_rank(const InflateJob *jobs, int njobs
         __syncthreads();  // `more` is reset only after every thread read it
     }
     __syncthreads();
-    // per stream: its head, and whether the ranked list is the whole stream
-    for (int j = 0; j < njobs; ++j) {
-        __shared__ int head, ok;
-        if (tid == 0) {
-            head = -1, ok = 0;
-            const InflateJob job = jobs[j];
-            const Tables T = tabs[j];
-            bool hdr = job.src_len >= 2 && !meta[j].overflow;
-            if (hdr) {
-                const uint32_t cmf = job.src[0], flg = job.src[1];
-                hdr = ((cmf << 8) | flg) % 31 == 0 && (cmf & 15) == 8 && (cmf >> 4) + 8 <= 15 && !(flg & 0x20);
-            }
-            if (hdr) {
-                const unsigned long long key = 16 + 1;
-                uint64_t sl = hslot(key, T.hcap);
-                for (uint64_t probe = 0; probe < T.hcap; ++probe, sl = (sl + 1) & (T.hcap - 1)) {
-                    const unsigned long long kk = T.hash[sl];
-                    if (kk == 0ull) break;
-                    if (kk == key) {
-                        head = (int)T.hval[sl];
-                        break;
-                    }
-                }
-            }
-            if (head >= 0 && (uint32_t)head < nc && cands[head].ok && W.nx[cur][head] < 0) {
-                const int term = W.tm[cur][head];
-                const Cand &tc = cands[term];
-                const uint64_t e = tc.end_bit, bp = (e + 7) >> 3;
-                if (tc.bfinal && W.sn[cur][head] <= T.bcap && W.sb[cur][head] == job.dst_len && bp + 4 <= job.src_len) {
-                    ok = 1;
-                    JobMeta &m = meta[j];
-                    m.adler_want = ((uint32_t)job.src[bp] << 24) | ((uint32_t)job.src[bp + 1] << 16) |
-                                   ((uint32_t)job.src[bp + 2] << 8) | job.src[bp + 3];
-                    m.nblocks = W.sn[cur][head];
-                    m.allzero = !W.sz[cur][head];
-                    m.nseg = W.ss[cur][head];
-                    m.ranked = 1;
+    // per stream (a thread each): its head, and whether the ranked list is the whole stream
+    for (int j = (int)tid; j < njobs; j += (int)nth) {
+        int head = -1;
+        bool ok = false;
+        const InflateJob job = jobs[j];
+        const Tables T = tabs[j];
+        bool hdr = job.src_len >= 2 && !meta[j].overflow;
+        if (hdr) {
+            const uint32_t cmf = job.src[0], flg = job.src[1];
+            hdr = ((cmf << 8) | flg) % 31 == 0 && (cmf & 15) == 8 && (cmf >> 4) + 8 <= 15 && !(flg & 0x20);
+        }
+        if (hdr) {
+            const unsigned long long key = 16 + 1;
+            uint64_t sl = hslot(key, T.hcap);
+            for (uint64_t probe = 0; probe < T.hcap; ++probe, sl = (sl + 1) & (T.hcap - 1)) {
+                const unsigned long long kk = T.hash[sl];
+                if (kk == 0ull) break;
+                if (kk == key) {
+                    head = (int)T.hval[sl];
+                    break;
                 }
             }
         }
-        __syncthreads();
-        if (ok) {
-            const Tables T = tabs[j];
-            const uint32_t N = W.sn[cur][head];
-            const uint64_t B = W.sb[cur][head];
-            const uint32_t SS = W.ss[cur][head];
-            for (uint32_t r = tid; r < N; r += nth) {
-                int node = head;
-                for (int l = 0; l < RANK_L && node >= 0; ++l)
-                    if ((r >> l) & 1u) node = W.jump[(size_t)l * nc + node];
-                const Cand &c = cands[node];
-                Blk blk;
-                blk.type = 1;
-                blk.nsyms = c.nsyms;
-                blk.src = (uint64_t)node * MAXSYM;
-                blk.out_off = B - W.sb[cur][node];
-                blk.out_len = c.out_bytes;
-                blk.nseg = c.nsyms > 0 ? (c.nsyms + SEG - 1) / SEG : 1;
-                blk.seg_base = SS - W.ss[cur][node];
-                blk.ckpt = (uint64_t)node;
-                T.blocks[r] = blk;
+        if (head >= 0 && (uint32_t)head < nc && cands[head].ok && W.nx[cur][head] < 0) {
+            const int term = W.tm[cur][head];
+            const Cand &tc = cands[term];
+            const uint64_t e = tc.end_bit, bp = (e + 7) >> 3;
+            if (tc.bfinal && W.sn[cur][head] <= T.bcap && W.sb[cur][head] == job.dst_len && bp + 4 <= job.src_len) {
+                ok = true;
+                JobMeta &m = meta[j];
+                m.adler_want = ((uint32_t)job.src[bp] << 24) | ((uint32_t)job.src[bp + 1] << 16) |
+                               ((uint32_t)job.src[bp + 2] << 8) | job.src[bp + 3];
+                m.nblocks = W.sn[cur][head];
+                m.allzero = !W.sz[cur][head];
+                m.nseg = W.ss[cur][head];
+                m.ranked = 1;
             }
         }
-        __syncthreads();
+        W.jhead[j] = ok ? head : -1;
+    }
+    __syncthreads();
+    if (tid == 0) {  // (streams are few: a serial prefix)
+        uint64_t acc = 0;
+        for (int j = 0; j < njobs; ++j) {
+            W.jpre[j] = acc;
+            if (W.jhead[j] >= 0) acc += W.sn[cur][W.jhead[j]];
+        }
+        W.jpre[njobs] = acc;
+    }
+    __syncthreads();
+    // a thread per block of every ranked stream: its node by the binary expansion of its rank
+    const uint64_t total = W.jpre[njobs];
+    for (uint64_t idx = tid; idx < total; idx += nth) {
+        int jl = 0, jh = njobs - 1;  // last stream with jpre <= idx
+        while (jl < jh) {
+            const int mid = (jl + jh + 1) / 2;
+            if (W.jpre[mid] <= idx) jl = mid;
+            else jh = mid - 1;
+        }
+        const int head = W.jhead[jl];
+        const uint32_t r = (uint32_t)(idx - W.jpre[jl]);
+        const Tables T = tabs[jl];
+        const uint64_t B = W.sb[cur][head];
+        const uint32_t SS = W.ss[cur][head];
+        int node = head;
+        for (int l = 0; l < RANK_L && node >= 0; ++l)
+            if ((r >> l) & 1u) node = W.jump[(size_t)l * nc + node];
+        const Cand &c = cands[node];
+        Blk blk;
+        blk.type = 1;
+        blk.nsyms = c.nsyms;
+        blk.src = (uint64_t)node * MAXSYM;
+        blk.out_off = B - W.sb[cur][node];
+        blk.out_len = c.out_bytes;
+        blk.nseg = c.nsyms > 0 ? (c.nsyms + SEG - 1) / SEG : 1;
+        blk.seg_base = SS - W.ss[cur][node];
+        blk.ckpt = (uint64_t)node;
+        T.blocks[r] = blk;
     }
 }
 
@@ -1932,7 +1943,7 @@ void inflate_batch_host(const std::vector<InflateJob> &jobs, int *status_dev, De
         }
         if (nc && nc <= (1u << 20)) {
             RankWs W;
-            uint8_t *rw = static_cast<uint8_t *>(alloc.get(nc * (2 * (4 + 4 + 8 + 4 + 4 + 1) + 4 * RANK_L) + 256, st));
+            uint8_t *rw = static_cast<uint8_t *>(alloc.get(nc * (2 * (4 + 4 + 8 + 4 + 4 + 1) + 4 * RANK_L) + (size_t)n * 12 + 512, st));
             auto take = [&](size_t b) { uint8_t *q = rw; rw += (b + 15) & ~size_t(15); return q; };
             for (int h = 0; h < 2; ++h) {
                 W.nx[h] = reinterpret_cast<int *>(take(nc * 4));
@@ -1943,6 +1954,8 @@ void inflate_batch_host(const std::vector<InflateJob> &jobs, int *status_dev, De
                 W.sz[h] = take(nc);
             }
             W.jump = reinterpret_cast<int *>(take(nc * 4 * RANK_L));
+            W.jhead = reinterpret_cast<int *>(take((size_t)n * 4));
+            W.jpre = reinterpret_cast<uint64_t *>(take((size_t)(n + 1) * 8));
             k_rank<<<1, 1024, 0, st>>>(jd, n, td, md, cands, (uint32_t)nc, W);
             CKL();
         }
