@@ -36,7 +36,7 @@ namespace cg = cooperative_groups;
 #define IPCG_NPH 2
 #endif
 #ifndef IPCG_SEG
-#define IPCG_SEG 128
+#define IPCG_SEG 512
 #endif
 #ifndef IPCG_CPW
 #define IPCG_CPW 1
