@@ -117,6 +117,9 @@ struct ipcg_archive {
     int device = 0;
     ipcg_read_fn read = nullptr;  // seekable source (ipcg_archive_open_source): bytes == nullptr
     void *user = nullptr;
+    // device archives: the 21-byte header of every plane block, [level-1][plane], read back once
+    // on the first retrieval (the archive is immutable) instead of per call
+    std::vector<uint8_t> hdr_all;
 };
 
 struct ipcg_session {
@@ -367,12 +370,11 @@ void gather(ipcg_ctx *c, std::vector<CopyDesc> descs, uint8_t *dst) {
             pieces.push_back(CopyDesc{d.src + o, d.dst_off + o, std::min(piece, d.len - o)});
     if (pieces.empty()) return;
     DBuf dd(pieces.size() * sizeof(CopyDesc), c->stream);
-    CopyDesc *h = static_cast<CopyDesc *>(pinned(c, pieces.size() * sizeof(CopyDesc)));
-    std::memcpy(h, pieces.data(), pieces.size() * sizeof(CopyDesc));
-    CK(cudaMemcpyAsync(dd.p, h, pieces.size() * sizeof(CopyDesc), cudaMemcpyHostToDevice, c->stream));
+    // from pageable memory: the driver stages it before returning, so no stream sync is needed
+    // to reuse `pieces` (a pinned staging buffer cost a sync per call)
+    CK(cudaMemcpyAsync(dd.p, pieces.data(), pieces.size() * sizeof(CopyDesc), cudaMemcpyHostToDevice, c->stream));
     k_gather<<<(unsigned)pieces.size(), 512, 0, c->stream>>>(dd.as<CopyDesc>(), (int)pieces.size(), dst);
     CKL();
-    CK(cudaStreamSynchronize(c->stream));  // the pinned staging is reused by the next call
 }
 
 // ---------------------------------------------------------------- compress
@@ -766,24 +768,32 @@ void retrieve_impl(ipcg_ctx *c, ipcg_archive *a, int scalar, const int *k, void 
         src_dev = a->bytes + ix.index_bytes;
         for (size_t i = 0; i < spans.size(); ++i) src_off[i] = spans[i].first;
         if (!refs.empty()) {
-            // plane spans are every span except each level's trailing outlier block
-            std::vector<uint64_t> hoffs;  // (offset, length) per plane block
-            size_t si = 0;
+            if (a->hdr_all.empty()) {  // every plane block's header, once per archive
+                std::vector<uint64_t> hoffs;  // (offset, length) per plane block, [level-1][plane]
+                for (int li = 0; li < L; ++li)
+                    for (int q = 0; q < 32; ++q) {
+                        const uint64_t off = ix.records[li].plane_offset[q], len = ix.records[li].plane_length[q];
+                        const bool ok = len <= ix.payload_bytes && off <= ix.payload_bytes - len;
+                        hoffs.push_back(ok ? off : 0), hoffs.push_back(ok ? len : 0);
+                    }
+                const size_t nh = hoffs.size() / 2;
+                DBuf ho(hoffs.size() * 8, st), hd(nh * 21, st);
+                CK(cudaMemcpyAsync(ho.p, hoffs.data(), hoffs.size() * 8, cudaMemcpyHostToDevice, st));
+                CK(cudaMemsetAsync(hd.p, 0, nh * 21, st));
+                k_copy_headers<<<(unsigned)((nh + 127) / 128), 128, 0, st>>>(src_dev, ho.as<uint64_t>(), (int)nh,
+                                                                            hd.as<uint8_t>());
+                CKL();
+                std::vector<uint8_t> all(nh * 21);
+                readback(all.data(), hd.p, all.size(), st);
+                a->hdr_all.swap(all);
+            }
+            size_t ri = 0;
             for (int level = L; level >= 1; --level) {
                 const LevelPlan &p = lv[level - 1];
                 if (!p.active) continue;
-                for (int q = p.p0; q < p.p1; ++q, ++si) hoffs.push_back(src_off[si]), hoffs.push_back(spans[si].second);
-                ++si;  // outlier
+                for (int q = p.p0; q < p.p1; ++q, ++ri)
+                    std::memcpy(&headers[ri * 21], &a->hdr_all[((size_t)(level - 1) * 32 + q) * 21], 21);
             }
-            const size_t nh = hoffs.size() / 2;
-            DBuf ho(hoffs.size() * 8, st), hd(nh * 21, st);
-            uint64_t *hp = static_cast<uint64_t *>(pinned(c, hoffs.size() * 8));
-            std::memcpy(hp, hoffs.data(), hoffs.size() * 8);
-            CK(cudaMemcpyAsync(ho.p, hp, hoffs.size() * 8, cudaMemcpyHostToDevice, st));
-            k_copy_headers<<<(unsigned)((nh + 127) / 128), 128, 0, st>>>(src_dev, ho.as<uint64_t>(), (int)nh,
-                                                                        hd.as<uint8_t>());
-            CKL();
-            readback(headers.data(), hd.p, headers.size(), st);
         }
     } else {
         // straight from the caller's buffer (no host-side staging copy): spans that are
@@ -898,12 +908,9 @@ void retrieve_impl(ipcg_ctx *c, ipcg_archive *a, int scalar, const int *k, void 
         }
         const size_t cw = crc32_batch_workspace((int)R, maxp);
         DBuf crcws(cw, st), crcs(R * 4, st), pd(R * 8, st), ld(R * 8, st);
-        uint8_t *hp = static_cast<uint8_t *>(pinned(c, R * 16));
-        std::memcpy(hp, ptrs.data(), R * 8);
-        std::memcpy(hp + R * 8, lens.data(), R * 8);
-        CK(cudaMemcpyAsync(pd.p, hp, R * 8, cudaMemcpyHostToDevice, st));
-        CK(cudaMemcpyAsync(ld.p, hp + R * 8, R * 8, cudaMemcpyHostToDevice, st));
-        CK(cudaStreamSynchronize(st));  // pinned ptr/len table consumed
+        // (pageable sources: staged by the driver on return, no stream sync)
+        CK(cudaMemcpyAsync(pd.p, ptrs.data(), R * 8, cudaMemcpyHostToDevice, st));
+        CK(cudaMemcpyAsync(ld.p, lens.data(), R * 8, cudaMemcpyHostToDevice, st));
         // CRC-32 of every payload on a side stream, concurrent with the copies and the inflate
         // (which validate everything they read and never fault on corrupt input); the checks
         // run after the inflate in backend_decode's order -- every checksum, then identity
@@ -1003,7 +1010,6 @@ void retrieve_impl(ipcg_ctx *c, ipcg_archive *a, int scalar, const int *k, void 
         for (int l = 0; l < L; ++l)
             for (int q = 0; q < 32; ++q) flat[(size_t)l * 32 + q] = rows[l][q];
         CK(cudaMemcpyAsync(rows_d.p, flat.data(), flat.size() * sizeof(void *), cudaMemcpyHostToDevice, st));
-        CK(cudaStreamSynchronize(st));
     }
     tm.mark("rows");
     // ---- merge + reconstruct, coarsest first
