@@ -1013,9 +1013,41 @@ __device__ bool chain_decode_block(Bits &b, int type, uint32_t *fb, uint64_t fca
     } else {
         if (!read_dynamic_header(b, lens, nlen, ndist, cs)) return false;
     }
-    if (!canon_build(lit, lens, nlen, 1) || !canon_build(dist, lens + nlen, ndist, 2)) return false;
     nsyms = 0;
     bytes = 0;
+    if (type == 1) {
+        // the fixed codes by arithmetic on the bit-reversed next 7/8/9 bits (the canonical
+        // bit-at-a-time loop cost ~1 us per symbol here, on small fields' critical path)
+        for (;;) {
+            const uint32_t v = b.peek(9);
+            const uint32_t c7 = __brev(v) >> 25, c8 = __brev(v) >> 24, c9 = __brev(v) >> 23;
+            int sym;
+            if (c7 <= 23u) sym = 256 + (int)c7, b.drop(7);
+            else if (c8 >= 48u && c8 <= 191u) sym = (int)c8 - 48, b.drop(8);
+            else if (c8 >= 192u && c8 <= 199u) sym = 280 + (int)c8 - 192, b.drop(8);
+            else sym = 144 + (int)c9 - 400, b.drop(9);
+            if (b.overrun()) return false;
+            if (sym == 256) return true;
+            if (fused >= fcap) return false;
+            if (sym < 256) {
+                fb[fused++] = sym_lit((uint32_t)sym);
+                ++nsyms;
+                ++bytes;
+                continue;
+            }
+            const int li = sym - 257;
+            if (li >= 29) return false;
+            const uint32_t len = kLBase[li] + b.get(kLExt[li]);
+            const int ds = (int)(__brev(b.peek(5)) >> 27);
+            b.drop(5);
+            if (ds >= 30) return false;
+            const uint32_t d = kDBase[ds] + b.get(kDExt[ds]);
+            fb[fused++] = sym_match(len, d);
+            ++nsyms;
+            bytes += len;
+        }
+    }
+    if (!canon_build(lit, lens, nlen, 1) || !canon_build(dist, lens + nlen, ndist, 2)) return false;
     for (;;) {
         const int sym = canon_decode(lit, b);
         if (sym < 0 || b.overrun()) return false;
@@ -1190,8 +1222,10 @@ __global__ void __launch_bounds__(1024) k_rank(const InflateJob *jobs, int njobs
 }
 
 __global__ void k_chain(const InflateJob *jobs, int njobs, const Tables *tabs, JobMeta *meta, const Cand *cands) {
-    const int j = blockIdx.x * blockDim.x + threadIdx.x;
-    if (j >= njobs || meta[j].ranked) return;
+    // a warp per stream (lane 0): the serial walks and fallback decodes of different streams must
+    // not share a warp, where their divergent loops would run one after another
+    const int j = blockIdx.x;
+    if (threadIdx.x != 0 || j >= njobs || meta[j].ranked) return;
     const InflateJob job = jobs[j];
     const Tables T = tabs[j];
     JobMeta &m = meta[j];
@@ -1959,7 +1993,7 @@ void inflate_batch_host(const std::vector<InflateJob> &jobs, int *status_dev, De
             k_rank<<<1, 1024, 0, st>>>(jd, n, td, md, cands, (uint32_t)nc, W);
             CKL();
         }
-        k_chain<<<(n + 31) / 32, 32, 0, st>>>(jd, n, td, md, cands);
+        k_chain<<<n, 32, 0, st>>>(jd, n, td, md, cands);
         CKL();
     }
     {
