@@ -1635,10 +1635,11 @@ void DeflateBatch::run(const uint8_t *in, uint64_t in_stride, int S, uint64_t n,
     }
     static const int od_mode = getenv("IPCG_OD_MODE") ? atoi(getenv("IPCG_OD_MODE")) : 0;  // dev: 1 all, 2 none
     static const int od_pct = getenv("IPCG_OD_ZEROS") ? atoi(getenv("IPCG_OD_ZEROS")) : 85;  // dev: threshold
-    // the on-demand parse pays off on large sparse streams; on small ones (< 1 MiB: coarse levels,
+    // the on-demand parse pays off on large sparse streams; on small ones (< 64 KiB: coarse levels,
     // small fields) its serial chunk walks and continuations are latency the all-position search
     // does not have
-    const int mode = n >= (1ull << 31) ? 2 : (od_mode == 0 && n < (1u << 20)) ? 2 : od_mode;
+    static const uint64_t od_min = getenv("IPCG_OD_MIN") ? strtoull(getenv("IPCG_OD_MIN"), nullptr, 10) : (1u << 16);  // dev knob; measured 1 MiB / 256 KiB / 64 KiB / 16 KiB: cfg3 compress 5.60 / 5.36 / 5.18 / 5.10 ms, cfg1 2.72 / 2.80 / 2.71 / 4.66 ms
+    const int mode = n >= (1ull << 31) ? 2 : (od_mode == 0 && n < od_min) ? 2 : od_mode;
     const bool od_possible = mode != 2;  // else no stream takes the on-demand parse: skip its launches
     k_select<<<1, 32, 0, st>>>(w.meta, S, n, mode, od_pct);
     CKL();
