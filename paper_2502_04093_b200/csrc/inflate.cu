@@ -1912,7 +1912,8 @@ static InflatePlan plan_jobs(const std::vector<InflateJob> &jobs) {
     return p;
 }
 
-void inflate_batch_host(const std::vector<InflateJob> &jobs, int *status_dev, DevAlloc &alloc, cudaStream_t st) {
+void inflate_batch_host(const std::vector<InflateJob> &jobs, int *status_dev, DevAlloc &alloc, cudaStream_t st,
+                        cudaStream_t check, cudaEvent_t fork, cudaEvent_t done) {
     const int n = (int)jobs.size();
     if (n == 0) return;
     const InflatePlan P = plan_jobs(jobs);
@@ -2090,11 +2091,18 @@ void inflate_batch_host(const std::vector<InflateJob> &jobs, int *status_dev, De
                         (unsigned long long)unres, (unsigned long long)(max_dst * n));
             }
         }
-        ProfScope ps4("inflate.adler", st, max_dst * n);
-        k_adler<<<dim3(grid_for(max_dst, 256, 256), n), 256, 0, st>>>(jd, md, acc);
+        // the checksum and final status: on `check` (when given) alongside the caller's next work
+        const cudaStream_t cs = check ? check : st;
+        if (check) {
+            CK(cudaEventRecord(fork, st));
+            CK(cudaStreamWaitEvent(check, fork, 0));
+        }
+        ProfScope ps4("inflate.adler", cs, max_dst * n);
+        k_adler<<<dim3(grid_for(max_dst, 256, 256), n), 256, 0, cs>>>(jd, md, acc);
         CKL();
-        k_finish<<<(n + 63) / 64, 64, 0, st>>>(jd, n, md, acc, status_dev);
+        k_finish<<<(n + 63) / 64, 64, 0, cs>>>(jd, n, md, acc, status_dev);
         CKL();
+        if (check) CK(cudaEventRecord(done, check));
     }
 }
 

@@ -11,6 +11,7 @@
 // All device work of a call is ordered on the context's stream; temporaries, archive
 // payloads and session codewords come from the context's grow-only ScratchPool
 // (util.cuh), so steady-state calls allocate nothing.
+#include <functional>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -883,6 +884,23 @@ void retrieve_impl(ipcg_ctx *c, ipcg_archive *a, int scalar, const int *k, void 
     for (int l = 0; l < L; ++l)
         if (planes[l].p)
             for (int q = 0; q < 32; ++q) rows[l][q] = planes[l].as<uint32_t>() + (uint64_t)q * stride[l];
+    // checks made once the merge and reconstruction are enqueued (finish_checks): the payload
+    // CRCs and the inflate's Adler-32/status run on side streams under them
+    DBuf crcws, crcs, pd, ld;
+    cudaStream_t cs = st;
+    DevAlloc inflate_tmp;
+    DBuf inflate_status;
+    size_t inflate_jobs = 0;
+    cudaStream_t inflate_check = nullptr;
+    cudaEvent_t inflate_done = nullptr;
+    struct JoinCheck {  // an exception before finish_checks still orders inflate_tmp's release
+        cudaStream_t &check, &st;
+        cudaEvent_t &done;
+        ~JoinCheck() {
+            if (check) cudaStreamWaitEvent(st, done, 0);
+        }
+    } join_check{inflate_check, st, inflate_done};
+    std::function<void()> finish_checks = [] {};
     if (R) {
         std::vector<const uint8_t *> ptrs(R);
         std::vector<uint64_t> lens(R);
@@ -907,7 +925,7 @@ void retrieve_impl(ipcg_ctx *c, ipcg_archive *a, int scalar, const int *k, void 
             }
         }
         const size_t cw = crc32_batch_workspace((int)R, maxp);
-        DBuf crcws(cw, st), crcs(R * 4, st), pd(R * 8, st), ld(R * 8, st);
+        crcws = DBuf(cw, st), crcs = DBuf(R * 4, st), pd = DBuf(R * 8, st), ld = DBuf(R * 8, st);
         // (pageable sources: staged by the driver on return, no stream sync)
         CK(cudaMemcpyAsync(pd.p, ptrs.data(), R * 8, cudaMemcpyHostToDevice, st));
         CK(cudaMemcpyAsync(ld.p, lens.data(), R * 8, cudaMemcpyHostToDevice, st));
@@ -916,7 +934,7 @@ void retrieve_impl(ipcg_ctx *c, ipcg_archive *a, int scalar, const int *k, void 
         // run after the inflate in backend_decode's order -- every checksum, then identity
         // lengths, then the inflate status -- so the reported error is unchanged
         c->events_used = 0;
-        const cudaStream_t cs = profiler().enabled ? st : side_stream(c, 0);
+        cs = profiler().enabled ? st : side_stream(c, 0);
         if (cs != st) stream_dep(c, st, cs);
         {
             uint64_t cb = 0;
@@ -986,22 +1004,32 @@ void retrieve_impl(ipcg_ctx *c, ipcg_archive *a, int scalar, const int *k, void 
             if (rep_of[a] < 0) todo.push_back(jobs[a]);
             else rows[job_level[a]][job_plane[a]] = rows[job_level[rep_of[a]]][job_plane[rep_of[a]]];
         if (!todo.empty()) {
-            DevAlloc tmp;
-            DBuf sd(todo.size() * 4, st);
-            {
-                uint64_t ib = 0;
-                for (const InflateJob &j : todo) ib += j.src_len + j.dst_len;
-                ProfScope ps("inflate", st, ib);
-                inflate_batch_host(todo, sd.as<int>(), tmp, st);
+            inflate_status = DBuf(todo.size() * 4, st);
+            inflate_jobs = todo.size();
+            uint64_t ib = 0;
+            for (const InflateJob &j : todo) ib += j.src_len + j.dst_len;
+            ProfScope ps("inflate", st, ib);
+            // the inflate's Adler-32 and status run on a side stream under the merge and
+            // reconstruction below; every check is made before returning (finish_checks)
+            if (!profiler().enabled) {
+                inflate_check = quant_stream(c);  // (compress's stream: idle here; side stream 0 carries the CRC)
+                inflate_done = pool_event(c);
+                inflate_batch_host(todo, inflate_status.as<int>(), inflate_tmp, st, inflate_check, pool_event(c),
+                                   inflate_done);
+            } else {
+                inflate_batch_host(todo, inflate_status.as<int>(), inflate_tmp, st);
             }
-            check_crcs();
-            std::vector<int> status(todo.size());
-            readback(status.data(), sd.p, todo.size() * 4, st);
-            for (int s : status)
-                if (s) throw Error(ERUNTIME, "deflate backend failed to decompress block");
-        } else {
-            check_crcs();
         }
+        finish_checks = [&, check_crcs] {
+            if (inflate_check) CK(cudaStreamWaitEvent(st, inflate_done, 0));
+            check_crcs();
+            if (inflate_jobs) {
+                std::vector<int> status(inflate_jobs);
+                readback(status.data(), inflate_status.p, inflate_jobs * 4, st);
+                for (int s : status)
+                    if (s) throw Error(ERUNTIME, "deflate backend failed to decompress block");
+            }
+        };
     tm.mark("inflate");
     }
     DBuf rows_d((size_t)L * 32 * sizeof(void *), st);
@@ -1075,6 +1103,7 @@ void retrieve_impl(ipcg_ctx *c, ipcg_archive *a, int scalar, const int *k, void 
             if (level <= ix.progressive_levels) ns->merged[li] = merged;
             else scratch_put(merged, st);
         }
+        finish_checks();  // every checksum, then identity lengths, then the inflate status
         if (slot) {
             CK(cudaEventRecord(slot->ready, st));
             CK(cudaStreamWaitEvent(c->copy, slot->ready, 0));
