@@ -567,7 +567,7 @@ struct BlockTrees {
 // reaches the 7 bits kept here.  heap[heap_max..] then holds the nodes in zlib's order for
 // gen_bitlen.
 struct TreeScratch {
-    alignas(8) uint32_t heap[HEAP_SIZE + 1];  // 8-byte aligned, one spare entry: pqdownheap reads child pairs
+    alignas(16) uint32_t heap[HEAP_SIZE + 4];  // 16-byte aligned, spare entries: pqdownheap reads child pairs and grandchild quads
     uint16_t freq[HEAP_SIZE];     // leaf frequencies (input; forced leaves set to 1)
     uint16_t dad_len[HEAP_SIZE];  // zlib's dl union: Dad during build, Len after gen_bitlen
     uint16_t bl_count[MAX_BITS + 1];
@@ -586,19 +586,37 @@ HD int hnode(uint32_t e) { return (int)(e & 1023); }
 struct alignas(8) HeapPair {
     uint32_t x, y;
 };
+struct alignas(16) HeapQuad {
+    uint32_t x, y, z, w;
+};
+// The two children heap[j], heap[j+1] (j even) come in one 8-byte load, and the four
+// grandchildren heap[2j .. 2j+3] are loaded (one 16-byte load) while this level compares, so the
+// chain of dependent shared-memory loads is one per two levels; keys compare as e | 1023 (the
+// node bits set), which orders like e >> 10; heap_len stays in a register.  The k_plan tree
+// builds are latency/issue-bound and this loop was over half of their instructions.
 HD void pqdownheap(TreeScratch &t, int k) {
     const uint32_t v = t.heap[k];
     const uint32_t vk = v | 1023u;
     const int len = t.heap_len;
     int j = k << 1;
-    while (j <= len) {
-        const HeapPair c = *reinterpret_cast<const HeapPair *>(&t.heap[j]);  // heap[j + 1] unused when j == len
-        uint32_t hj = c.x;
-        if (j < len && (c.y | 1023u) <= (c.x | 1023u)) j++, hj = c.y;
-        if (vk <= (hj | 1023u)) break;
-        t.heap[k] = hj;
-        k = j;
-        j <<= 1;
+    if (j <= len) {
+        const HeapPair c0 = *reinterpret_cast<const HeapPair *>(&t.heap[j]);  // heap[j + 1] unused when j == len
+        uint32_t cx = c0.x, cy = c0.y;
+        for (;;) {
+            const int g = j << 1;  // grandchildren: heap[g .. g+3] (children of j and j+1)
+            HeapQuad q{0u, 0u, 0u, 0u};
+            if (g <= len) q = *reinterpret_cast<const HeapQuad *>(&t.heap[g]);
+            uint32_t hj = cx;
+            int jj = j;
+            if (j < len && (cy | 1023u) <= (cx | 1023u)) jj = j + 1, hj = cy;
+            if (vk <= (hj | 1023u)) break;
+            t.heap[k] = hj;
+            k = jj;
+            j = k << 1;
+            if (j > len) break;
+            if (jj == (g >> 1)) cx = q.x, cy = q.y;
+            else cx = q.z, cy = q.w;
+        }
     }
     t.heap[k] = v;
 }
