@@ -1664,6 +1664,7 @@ void DeflateBatch::run(const uint8_t *in, uint64_t in_stride, int S, uint64_t n,
         k_prevlinks<<<dim3((unsigned)((nblk + span * PL_WARPS - 1) / (span * PL_WARPS)), S), PL_WARPS * 32, smem, st>>>(in, in_stride, n, w.meta, w.prevd, span);
         CKL();
         }
+        debug_mark("P", (int)(n >> 20), st);  // (dev timeline: hash links done; tag = stream MiB)
         // sparse streams (meta.od, k_select) take the on-demand parse, the others the all-position
         // search; each kernel below skips the streams of the other path
         const bool forked = side && fork && join && od_possible;
@@ -1762,7 +1763,9 @@ void DeflateBatch::run(const uint8_t *in, uint64_t in_stride, int S, uint64_t n,
             CKL();
             }
         }
+        debug_mark("S", (int)(n >> 20), st);  // dense symbols done
         if (forked) {
+            debug_mark("O", (int)(n >> 20), side);  // on-demand parse done
             CK(cudaEventRecord(join, side));
             CK(cudaStreamWaitEvent(st, join, 0));
         }
@@ -1773,6 +1776,7 @@ void DeflateBatch::run(const uint8_t *in, uint64_t in_stride, int S, uint64_t n,
         k_layout<<<S, 32, 0, st>>>(n, w.meta, S, w.maxb, w.trees, w.blk_bitpos);
         CKL();
         }
+        debug_mark("B", (int)(n >> 20), st);  // block plans done
         {
         ProfScope ps5("deflate.emit", st, (uint64_t)S * n);
         k_zero_out<<<dim3(grid_for(n / 8 + 2, 256, 512), S), 256, 0, st>>>(n, w.meta, out, out_stride);

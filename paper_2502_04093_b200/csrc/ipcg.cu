@@ -217,7 +217,11 @@ cudaStream_t quant_stream(ipcg_ctx *c) {
 cudaStream_t od_stream(ipcg_ctx *c, size_t li) {
     while (c->odside.size() <= li) {
         cudaStream_t s;
-        CK(cudaStreamCreateWithPriority(&s, cudaStreamNonBlocking, lossless_prio(c->odside.size() == 0)));
+        // the on-demand parse streams at the highest priority: level 1's latency-bound parse then
+        // ends (IPCG_DEBUG_TIMELINE "O14") at ~20 ms instead of last at ~27 ms, behind the dense
+        // search it shares the GPU with; compress 29.9 -> 29.1 ms (IPCG_OD_PRIO=0: the old order)
+        static const int od_hi = getenv("IPCG_OD_PRIO") ? atoi(getenv("IPCG_OD_PRIO")) : 1;
+        CK(cudaStreamCreateWithPriority(&s, cudaStreamNonBlocking, od_hi ? prio_for(false) : lossless_prio(c->odside.size() == 0)));
         c->odside.push_back(s);
     }
     return c->odside[li];
@@ -394,6 +398,8 @@ struct Timeline {
     void print() {
         if (!on || ev.empty()) return;
         CK(cudaDeviceSynchronize());
+        for (auto &x : debug_marks()) ev.push_back(x);
+        debug_marks().clear();
         std::vector<std::pair<float, std::string>> t;
         for (auto &x : ev) {
             float ms = 0;

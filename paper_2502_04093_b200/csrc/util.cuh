@@ -177,6 +177,21 @@ struct DevAlloc {
     }
 };
 
+// dev timeline marks from inside the stages (IPCG_DEBUG_TIMELINE): named events, printed and
+// released by ipcg.cu's Timeline after the call's final sync
+inline std::vector<std::pair<std::string, cudaEvent_t>> &debug_marks() {
+    static std::vector<std::pair<std::string, cudaEvent_t>> v;
+    return v;
+}
+inline void debug_mark(const char *name, int level, cudaStream_t s) {
+    static const bool on = getenv("IPCG_DEBUG_TIMELINE") != nullptr;
+    if (!on) return;
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    cudaEventRecord(e, s);
+    debug_marks().push_back({std::string(name) + std::to_string(level), e});
+}
+
 // SM count of the current device (cached per device)
 inline int num_sms() {
     static int cache[64] = {0};
