@@ -80,6 +80,7 @@ struct ipcg_ctx {
     std::vector<cudaStream_t> loss;  // per-level loss-table streams (highest priority)
     std::vector<cudaStream_t> odside;  // per-level streams of the deflate on-demand parse
     cudaStream_t quant = nullptr;      // compress's prediction/quantization chain (highest priority)
+    cudaStream_t h2d = nullptr;        // compress's upload of a host field
     std::vector<cudaEvent_t> events;
     size_t events_used = 0;
     ScratchPool scratch;  // per-call device scratch, reused across calls (also archive/session memory)
@@ -454,7 +455,6 @@ ipcg_archive *compress_impl(ipcg_ctx *c, int scalar, const void *values, int on_
     const void *vals = values;
     if (!on_dev) {
         vals_buf = DBuf(n * w, st);
-        CK(cudaMemcpyAsync(vals_buf.p, values, n * w, cudaMemcpyHostToDevice, st));
         vals = vals_buf.p;
     }
     DBuf state(n * w, st), dev(n * 8, st);
@@ -478,10 +478,56 @@ ipcg_archive *compress_impl(ipcg_ctx *c, int scalar, const void *values, int on_
     c->events_used = 0;
     const cudaStream_t qs = serial0 ? st : quant_stream(c);
     if (qs != st) stream_dep(c, st, qs);
-    {
+    // A host field is uploaded in two parts: first the rows whose leading coordinates are all even
+    // -- every point the levels coarser than 1 read or write lies in them (their strides are >= 2
+    // on every axis) -- then the rest, so the coarse levels' quantization and lossless stages run
+    // while ~3/4 of the field is still crossing PCIe; level 1 and the range wait for all of it.
+    cudaEvent_t all_ready = nullptr;
+    if (!on_dev) {
+        if (serial0) {
+            CK(cudaMemcpyAsync(vals_buf.p, values, n * w, cudaMemcpyHostToDevice, st));
+        } else {
+            if (!c->h2d) CK(cudaStreamCreateWithFlags(&c->h2d, cudaStreamNonBlocking));
+            const cudaStream_t hs = c->h2d;
+            stream_dep(c, st, hs);  // the buffer's stream-ordered allocation
+            const bool split = L >= 2 && (nd == 2 || nd == 3) && dims[0] >= 2;
+            uint8_t *dst = vals_buf.as<uint8_t>();
+            const uint8_t *src = static_cast<const uint8_t *>(values);
+            if (split) {
+                const size_t rowb = (size_t)dims[nd - 1] * w;
+                const size_t Y = nd == 3 ? (size_t)dims[1] : (size_t)dims[0], Z = nd == 3 ? (size_t)dims[0] : 1;
+                auto rows3d = [&](size_t off, size_t height) {  // rows y = off, off+2, ... of every even z
+                    if (!height) return;
+                    cudaMemcpy3DParms m{};
+                    m.srcPtr = make_cudaPitchedPtr(const_cast<uint8_t *>(src) + off * rowb, 2 * rowb, rowb, Y);
+                    m.dstPtr = make_cudaPitchedPtr(dst + off * rowb, 2 * rowb, rowb, Y);
+                    m.extent = make_cudaExtent(rowb, height, nd == 3 ? (Z + 1) / 2 : 1);
+                    m.kind = cudaMemcpyHostToDevice;
+                    CK(cudaMemcpy3DAsync(&m, hs));
+                };
+                rows3d(0, (Y + 1) / 2);  // coarse rows: even y (and even z)
+                cudaEvent_t coarse = pool_event(c);
+                CK(cudaEventRecord(coarse, hs));
+                CK(cudaStreamWaitEvent(qs, coarse, 0));
+                rows3d(1, Y / 2);  // odd y of even z
+                if (nd == 3 && Z >= 2) {  // odd z slabs
+                    const size_t slab = Y * rowb;
+                    CK(cudaMemcpy2DAsync(dst + slab, 2 * slab, src + slab, 2 * slab, slab, Z / 2, cudaMemcpyHostToDevice, hs));
+                }
+            } else {
+                CK(cudaMemcpyAsync(dst, src, n * w, cudaMemcpyHostToDevice, hs));
+            }
+            all_ready = pool_event(c);
+            CK(cudaEventRecord(all_ready, hs));
+            if (!split) CK(cudaStreamWaitEvent(qs, all_ready, 0));
+            if (qs != st) CK(cudaStreamWaitEvent(st, all_ready, 0));  // (st joins qs later anyway)
+        }
+    }
+    auto range_once = [&] {
         ProfScope ps("range", qs, n * w);
         launch_range(vals, scalar, n, sd->range_part, sd->rng, qs);
-    }
+    };
+    if (!all_ready) range_once();
 
     // (Forking each level's lossless stage and the loss tables onto side streams was
     // measured: no gain -- level 1's kernels saturate the GPU, so overlap only hides the
@@ -503,6 +549,10 @@ ipcg_archive *compress_impl(ipcg_ctx *c, int scalar, const void *values, int on_
     for (int level = L; level >= 1; --level) {
         const LevelGeom &lg = G.level[level - 1];
         const int li = level - 1;
+        if (level == 1 && all_ready) {  // the whole field is on the device
+            CK(cudaStreamWaitEvent(qs, all_ready, 0));
+            range_once();
+        }
         sink_base[li] = base;
         base += lg.count;
         pb[li] = (lg.count + 7) / 8;
@@ -1186,6 +1236,7 @@ void ipcg_ctx_destroy(ipcg_ctx *c) {
     for (cudaStream_t s : c->loss) cudaStreamSynchronize(s);
     for (cudaStream_t s : c->odside) cudaStreamSynchronize(s);
     if (c->quant) cudaStreamSynchronize(c->quant);
+    if (c->h2d) cudaStreamSynchronize(c->h2d);
     c->scratch.release_all(c->own_stream);
     if (c->own_stream) cudaStreamSynchronize(c->own_stream);
     if (c->pinned) cudaFreeHost(c->pinned);
@@ -1194,6 +1245,7 @@ void ipcg_ctx_destroy(ipcg_ctx *c) {
     for (cudaStream_t s : c->loss) cudaStreamDestroy(s);
     for (cudaStream_t s : c->odside) cudaStreamDestroy(s);
     if (c->quant) cudaStreamDestroy(c->quant);
+    if (c->h2d) cudaStreamDestroy(c->h2d);
     for (cudaEvent_t e : c->events) cudaEventDestroy(e);
     if (c->own_stream) cudaStreamDestroy(c->own_stream);
     delete c;
