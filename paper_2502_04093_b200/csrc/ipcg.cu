@@ -769,6 +769,7 @@ void retrieve_impl(ipcg_ctx *c, ipcg_archive *a, int scalar, const int *k, void 
                 throw Error(EINVAL_, "refinement plan must not drop planes the session already loaded");
     }
     cudaStream_t st = c->stream;
+    c->events_used = 0;  // this call's events (the previous call has drained)
     // ---- plan the block reads (read_range accounting, archive.cpp:172-200)
     struct LevelPlan {
         int p0, p1;
@@ -815,6 +816,7 @@ void retrieve_impl(ipcg_ctx *c, ipcg_archive *a, int scalar, const int *k, void 
         read += r.outlier_length;
     }
     // ---- bring the blocks to the device
+    cudaEvent_t stage_def = nullptr, stage_all = nullptr;  // two-phase host staging (below)
     uint64_t staged = 0;
     for (auto &s : spans) staged += s.second;
     DBuf stage;
@@ -862,23 +864,54 @@ void retrieve_impl(ipcg_ctx *c, ipcg_archive *a, int scalar, const int *k, void 
         stage = DBuf(std::max<uint64_t>(staged, 1), st);
         uint8_t *sp = a->read ? static_cast<uint8_t *>(src_pinned(c, std::max<uint64_t>(staged, 1))) : nullptr;
         const uint8_t *hb = a->read ? sp : a->bytes + ix.index_bytes;
+        // From a caller's buffer the spans upload on the context's h2d stream in two rounds: the
+        // deflate-coded plane blocks first (the inflate starts on them), then the identity planes
+        // and outlier blocks, whose upload runs under the inflate.
+        const bool two_phase = !a->read && !profiler().enabled;
+        std::vector<uint8_t> is_plane(spans.size(), 0);
+        {
+            size_t si = 0;
+            for (int level = L; level >= 1; --level) {
+                if (!lv[level - 1].active) continue;
+                for (int q = lv[level - 1].p0; q < lv[level - 1].p1; ++q) is_plane[si++] = 1;
+                ++si;  // outlier block
+            }
+        }
+        auto deflate_span = [&](size_t i) { return is_plane[i] && spans[i].second >= 1 && hb[spans[i].first] == 1; };
+        cudaStream_t hs = st;
+        if (two_phase) {
+            if (!c->h2d) CK(cudaStreamCreateWithFlags(&c->h2d, cudaStreamNonBlocking));
+            hs = c->h2d;
+            stream_dep(c, st, hs);  // the stage buffer's stream-ordered allocation
+        }
         uint64_t o = 0;
-        for (size_t i = 0; i < spans.size();) {
-            size_t e = i + 1;
-            src_off[i] = o;
-            while (e < spans.size() && spans[e].first == spans[e - 1].first + spans[e - 1].second) {
-                src_off[e] = o + (spans[e].first - spans[i].first);
-                ++e;
+        for (size_t i = 0; i < spans.size(); ++i) src_off[i] = o, o += spans[i].second;
+        for (int phase = two_phase ? 0 : 1; phase < 2; ++phase) {
+            // phase 0: deflate plane blocks; phase 1: the rest (everything when not two-phase)
+            for (size_t i = 0; i < spans.size();) {
+                const bool mine = !two_phase || (phase == 0) == deflate_span(i);
+                if (!mine) {
+                    ++i;
+                    continue;
+                }
+                size_t e = i + 1;
+                while (e < spans.size() && spans[e].first == spans[e - 1].first + spans[e - 1].second &&
+                       (!two_phase || (phase == 0) == deflate_span(e)))
+                    ++e;
+                const uint64_t len = spans[e - 1].first + spans[e - 1].second - spans[i].first;
+                const uint8_t *from = hb + spans[i].first;
+                if (a->read) {
+                    source_read(a, ix.index_bytes + spans[i].first, sp + src_off[i], len, "truncated archive payload");
+                    from = sp + src_off[i];
+                }
+                if (len) CK(cudaMemcpyAsync(stage.as<uint8_t>() + src_off[i], from, len, cudaMemcpyHostToDevice, hs));
+                i = e;
             }
-            const uint64_t len = spans[e - 1].first + spans[e - 1].second - spans[i].first;
-            const uint8_t *from = hb + spans[i].first;
-            if (a->read) {
-                source_read(a, ix.index_bytes + spans[i].first, sp + o, len, "truncated archive payload");
-                from = sp + o;
+            if (two_phase) {
+                cudaEvent_t ev = pool_event(c);
+                CK(cudaEventRecord(ev, hs));
+                (phase == 0 ? stage_def : stage_all) = ev;
             }
-            if (len) CK(cudaMemcpyAsync(stage.as<uint8_t>() + o, from, len, cudaMemcpyHostToDevice, st));
-            o += len;
-            i = e;
         }
         size_t si = 0, ri = 0;
         for (int level = L; level >= 1; --level) {
@@ -989,9 +1022,9 @@ void retrieve_impl(ipcg_ctx *c, ipcg_archive *a, int scalar, const int *k, void 
         // (which validate everything they read and never fault on corrupt input); the checks
         // run after the inflate in backend_decode's order -- every checksum, then identity
         // lengths, then the inflate status -- so the reported error is unchanged
-        c->events_used = 0;
         cs = profiler().enabled ? st : side_stream(c, 0);
         if (cs != st) stream_dep(c, st, cs);
+        if (stage_all) CK(cudaStreamWaitEvent(cs, stage_all, 0));
         {
             uint64_t cb = 0;
             for (uint64_t x : lens) cb += x;
@@ -1021,8 +1054,8 @@ void retrieve_impl(ipcg_ctx *c, ipcg_archive *a, int scalar, const int *k, void 
             }
         };
     tm.mark("crc");
-        if (!copies.empty()) gather(c, copies, nullptr);
     tm.mark("copies");
+        if (stage_def) CK(cudaStreamWaitEvent(st, stage_def, 0));
         // identical deflate payloads (typically the all-zero high planes) decode once:
         // same (length, crc, plane size) and byte-equal on the device -> alias the row
         std::vector<int> rep_of(jobs.size(), -1);
@@ -1076,6 +1109,9 @@ void retrieve_impl(ipcg_ctx *c, ipcg_archive *a, int scalar, const int *k, void 
                 inflate_batch_host(todo, inflate_status.as<int>(), inflate_tmp, st);
             }
         }
+        // identity planes: their upload (second staging round) ran under the inflate
+        if (stage_all) CK(cudaStreamWaitEvent(st, stage_all, 0));
+        if (!copies.empty()) gather(c, copies, nullptr);
         finish_checks = [&, check_crcs] {
             if (inflate_check) CK(cudaStreamWaitEvent(st, inflate_done, 0));
             check_crcs();
@@ -1088,6 +1124,7 @@ void retrieve_impl(ipcg_ctx *c, ipcg_archive *a, int scalar, const int *k, void 
         };
     tm.mark("inflate");
     }
+    if (stage_all) CK(cudaStreamWaitEvent(st, stage_all, 0));  // outlier blocks (and no planes at all)
     DBuf rows_d((size_t)L * 32 * sizeof(void *), st);
     {
         std::vector<const uint32_t *> flat((size_t)L * 32, nullptr);
