@@ -51,24 +51,47 @@ struct MappedBuf {  // grow-only mapped page-locked staging, one per host thread
 
 void compute_metrics_device(int scalar, const void *a, const void *b, uint64_t n, double out[3], cudaStream_t st);
 
-void readback(void *dst, const void *src_dev, size_t bytes, cudaStream_t st) {
-    if (!bytes) return;
+// several device ranges read back behind one stream synchronization
+struct RbPart {
+    void *dst;
+    const void *src;
+    size_t bytes;
+};
+void readback_parts(const RbPart *parts, int np, cudaStream_t st) {
+    size_t total = 0;
+    for (int i = 0; i < np; ++i) total += (parts[i].bytes + 15) & ~size_t(15);
+    if (!total) return;
     thread_local rb::MappedBuf mb;
-    if (bytes > mb.cap) {
+    if (total > mb.cap) {
         CK(cudaStreamSynchronize(st));
         if (mb.h) CK(cudaFreeHost(mb.h));
         mb.h = nullptr;
-        const size_t cap = std::max<size_t>(bytes, 64 << 10);
+        const size_t cap = std::max<size_t>(total, 64 << 10);
         CK(cudaHostAlloc(&mb.h, cap, cudaHostAllocMapped));
         mb.cap = cap;
     }
     void *d = nullptr;
     CK(cudaHostGetDevicePointer(&d, mb.h, 0));
-    rb::k_readback<<<(unsigned)std::min<size_t>((bytes + 255) / 256, 64), 256, 0, st>>>(
-        static_cast<const uint8_t *>(src_dev), static_cast<uint8_t *>(d), bytes);
-    CKL();
+    size_t off = 0;
+    for (int i = 0; i < np; ++i) {
+        const size_t b = parts[i].bytes;
+        if (b) {
+            rb::k_readback<<<(unsigned)std::min<size_t>((b + 255) / 256, 64), 256, 0, st>>>(
+                static_cast<const uint8_t *>(parts[i].src), static_cast<uint8_t *>(d) + off, b);
+            CKL();
+        }
+        off += (b + 15) & ~size_t(15);
+    }
     CK(cudaStreamSynchronize(st));
-    std::memcpy(dst, mb.h, bytes);
+    off = 0;
+    for (int i = 0; i < np; ++i) {
+        std::memcpy(parts[i].dst, static_cast<uint8_t *>(mb.h) + off, parts[i].bytes);
+        off += (parts[i].bytes + 15) & ~size_t(15);
+    }
+}
+void readback(void *dst, const void *src_dev, size_t bytes, cudaStream_t st) {
+    const RbPart p{dst, src_dev, bytes};
+    readback_parts(&p, 1, st);
 }
 }  // namespace ipcg
 
@@ -105,6 +128,23 @@ struct ipcg_ctx {
     size_t ring_next = 0;
     cudaEvent_t copy_tail = nullptr;  // the last copy enqueued
     bool copy_pending = false;
+    // compress graphs (compress_entry): a device-resident field of a shape seen before replays
+    // the whole captured kernel sequence of its compress with one launch
+    struct CGraph {
+        int scalar, nd, interp, lp;
+        uint64_t dims[4], cap, eb_bits;
+        int state = 0;        // 0 seen once (its scratch tallied), 1 captured, 2 not capturable
+        size_t need = 0;      // scratch bytes one compress of this shape requests
+        uint8_t *slab = nullptr;  // input slot + every scratch block the captured calls use
+        cudaGraphExec_t exec = nullptr;
+        void *aout = nullptr;     // AsmOut in the slab
+        uint8_t *arch = nullptr;  // assembled archive in the slab
+        unsigned long long nlaunch = 0;
+        uint64_t used = 0;
+    };
+    std::vector<CGraph> graphs;
+    uint64_t graph_clock = 0;
+    cudaStream_t capture = nullptr;  // graphs are captured on this stream
 };
 
 struct ipcg_archive {
@@ -435,8 +475,19 @@ struct PhaseTimer {
     }
 };
 
+// what a captured compress leaves for its replays (compress graphs, below)
+struct CaptureOut {
+    AsmOut *aout = nullptr;
+    uint8_t *arch = nullptr;
+    uint64_t capacity = 0;
+};
+
+// index bytes of an archive (host.cpp serialize_index: 12-byte preamble, dims, 20 bytes of
+// header fields, 808 bytes per level)
+inline uint64_t index_bytes_for(int nd, int levels) { return 12 + 8 * (uint64_t)nd + 20 + 808 * (uint64_t)levels; }
+
 ipcg_archive *compress_impl(ipcg_ctx *c, int scalar, const void *values, int on_dev, const uint64_t *dims, int nd,
-                            double eb, int interp, int lp_opt, uint64_t cap) {
+                            double eb, int interp, int lp_opt, uint64_t cap, CaptureOut *capture = nullptr) {
     PhaseTimer tm;
     validate_dims(dims, nd);
     if (scalar != 0 && scalar != 1) throw Error(EINVAL_, "field scalars must be f32 or f64");
@@ -655,25 +706,34 @@ ipcg_archive *compress_impl(ipcg_ctx *c, int scalar, const void *values, int on_
     a->on_device = true;
     uint64_t capacity = asm_capacity(P);
     AsmOut ho{};
+    // the index's size is fixed by the shape: it comes back with the assembly result, behind
+    // the call's one synchronization
+    std::vector<uint8_t> index(index_bytes_for(nd, L));
     for (int attempt = 0; attempt < 2; ++attempt) {
         // stream-ordered pool memory: a cudaMalloc/cudaFree pair per call would synchronize the device
         a->owned = static_cast<uint8_t *>(c->scratch.get(std::max<uint64_t>(capacity, 1), st));
         launch_assemble(P, sd, a->owned, capacity, descs.as<AsmDesc>(), aout.as<AsmOut>(), ofl.data(), obt.data(),
                         tiles.as<uint32_t>(), st);
-        readback(&ho, aout.p, sizeof(AsmOut), st);
+        if (capture) {  // enqueue only: the replays read the results back
+            capture->aout = aout.as<AsmOut>();
+            capture->arch = a->owned;
+            capture->capacity = capacity;
+            delete a;
+            return nullptr;
+        }
+        const RbPart parts[2] = {{&ho, aout.p, sizeof(AsmOut)}, {index.data(), a->owned, index.size()}};
+        readback_parts(parts, 2, st);
         tline.print();
         if (ho.fits) break;
         c->scratch.put(a->owned);  // more outliers than the 1/64 allowance: assemble again at the exact size
         a->owned = nullptr;
         capacity = ho.total;
     }
-    if (!ho.fits) {
+    if (!ho.fits || ho.index_bytes != index.size()) {
         delete a;
         throw Error(ERUNTIME, "archive assembly overflow");
     }
     tm.mark("assemble");
-    std::vector<uint8_t> index(ho.index_bytes);
-    readback(index.data(), a->owned, index.size(), st);
     try {
         parse_index(index.data(), index.size(), a->ix);  // also the identity (crc32 of the index)
     } catch (...) {
@@ -684,6 +744,137 @@ ipcg_archive *compress_impl(ipcg_ctx *c, int scalar, const void *values, int on_
     a->bytes = a->owned;
     a->size = ho.total;
     tm.mark("index");
+    return a;
+}
+
+// ------------------------------------------------------------ compress graphs
+// A small field's compress is bound by the host: ~230 launches, events and stream forks take
+// ~0.9 ms to enqueue on cfg1 (64^3), while level 1's chain waits for them.  A device-resident
+// field whose shape, error bound and options were compressed before replays that call's
+// kernel sequence as one CUDA graph: the first call runs normally and tallies its scratch
+// requests, the second is captured (multi-stream: the side, loss-table and parse streams join
+// the capture through their events; per-node priorities kept) with every scratch block carved
+// from a slab the graph owns, and every later call copies the field into the slab's input slot,
+// launches the graph and reads back the assembly result and index behind one synchronization.
+// The archive is then copied out of the slab into a block of its own.
+constexpr uint64_t kGraphMaxBytes = 128ull << 20;  // fields up to 128 MiB (their slab: ~120 B/point)
+constexpr size_t kGraphsKept = 4;
+
+void free_graph(ipcg_ctx::CGraph &g) {
+    if (g.exec) cudaGraphExecDestroy(g.exec);
+    if (g.slab) cudaFree(g.slab);
+    g.exec = nullptr, g.slab = nullptr;
+}
+
+ipcg_archive *compress_entry(ipcg_ctx *c, int scalar, const void *values, int on_dev, const uint64_t *dims, int nd,
+                             double eb, int interp, int lp, uint64_t cap) {
+    static const bool off = getenv("IPCG_NO_GRAPH") != nullptr;  // dev A/B knob
+    const int w = scalar == 0 ? 4 : 8;
+    uint64_t n = 1;
+    bool shape_ok = nd >= 1 && nd <= 4 && (scalar == 0 || scalar == 1);
+    for (int i = 0; shape_ok && i < nd; ++i) shape_ok = dims[i] >= 1 && dims[i] <= kGraphMaxBytes, n *= dims[i];
+    const bool eligible = !off && on_dev && shape_ok && n * w <= kGraphMaxBytes && !profiler().enabled &&
+                          !getenv("IPCG_DEBUG_TIMELINE") && std::isfinite(eb) && eb > 0.0;
+    if (!eligible) return compress_impl(c, scalar, values, on_dev, dims, nd, eb, interp, lp, cap);
+    uint64_t eb_bits;
+    std::memcpy(&eb_bits, &eb, 8);
+    ipcg_ctx::CGraph *g = nullptr;
+    for (auto &x : c->graphs) {
+        bool same = x.scalar == scalar && x.nd == nd && x.interp == interp && x.lp == lp && x.cap == cap &&
+                    x.eb_bits == eb_bits;
+        for (int i = 0; same && i < nd; ++i) same = x.dims[i] == dims[i];
+        if (same) g = &x;
+    }
+    if (!g) {  // first sight: a normal call, tallying its scratch requests
+        const size_t t0 = c->scratch.tally;
+        ipcg_archive *a = compress_impl(c, scalar, values, on_dev, dims, nd, eb, interp, lp, cap);
+        if (c->graphs.size() >= kGraphsKept) {  // evict the least recently used
+            auto lru = std::min_element(c->graphs.begin(), c->graphs.end(),
+                                        [](const auto &a1, const auto &b1) { return a1.used < b1.used; });
+            if (lru->slab) CK(cudaStreamSynchronize(c->stream));
+            free_graph(*lru);
+            c->graphs.erase(lru);
+        }
+        ipcg_ctx::CGraph ng{};
+        ng.scalar = scalar, ng.nd = nd, ng.interp = interp, ng.lp = lp, ng.cap = cap, ng.eb_bits = eb_bits;
+        for (int i = 0; i < nd; ++i) ng.dims[i] = dims[i];
+        ng.need = c->scratch.tally - t0;
+        ng.used = ++c->graph_clock;
+        c->graphs.push_back(ng);
+        return a;
+    }
+    g->used = ++c->graph_clock;
+    if (g->state == 2) return compress_impl(c, scalar, values, on_dev, dims, nd, eb, interp, lp, cap);
+    const uint64_t in_bytes = (n * w + 255) & ~uint64_t(255);
+    if (g->state == 0) {  // second sight: capture
+        g->state = 2;  // unless the capture below succeeds
+        const size_t arena = g->need + (g->need >> 4) + (1u << 20);
+        void *slab = nullptr;
+        if (cudaMalloc(&slab, in_bytes + arena) != cudaSuccess) {
+            cudaGetLastError();
+            return compress_impl(c, scalar, values, on_dev, dims, nd, eb, interp, lp, cap);
+        }
+        g->slab = static_cast<uint8_t *>(slab);
+        if (!c->capture) CK(cudaStreamCreateWithFlags(&c->capture, cudaStreamNonBlocking));
+        const cudaStream_t real = c->stream;
+        const unsigned long long l0 = c->launches;
+        c->stream = c->capture;
+        c->scratch.arena = g->slab + in_bytes, c->scratch.arena_cap = arena, c->scratch.arena_off = 0;
+        c->scratch.arena_over = false;
+        CaptureOut co;
+        bool ok = cudaStreamBeginCapture(c->capture, cudaStreamCaptureModeRelaxed) == cudaSuccess;
+        cudaGraph_t graph = nullptr;
+        if (ok) {
+            try {
+                compress_impl(c, scalar, g->slab, 1, dims, nd, eb, interp, lp, cap, &co);
+            } catch (...) {
+                ok = false;
+            }
+            ok = cudaStreamEndCapture(c->capture, &graph) == cudaSuccess && ok;
+        }
+        ok = ok && !c->scratch.arena_over && co.aout && graph;
+        c->stream = real;
+        c->scratch.arena = nullptr;
+        g->nlaunch = c->launches - l0;
+        c->launches = l0;
+        if (ok) ok = cudaGraphInstantiateWithFlags(&g->exec, graph, cudaGraphInstantiateFlagUseNodePriority) == cudaSuccess;
+        if (graph) cudaGraphDestroy(graph);
+        cudaGetLastError();  // a failed capture leaves its error here; the call falls back
+        if (!ok) {
+            free_graph(*g);
+            return compress_impl(c, scalar, values, on_dev, dims, nd, eb, interp, lp, cap);
+        }
+        g->aout = co.aout, g->arch = co.arch;
+        g->state = 1;
+    }
+    // replay
+    const cudaStream_t st = c->stream;
+    CK(cudaMemcpyAsync(g->slab, values, n * w, cudaMemcpyDeviceToDevice, st));
+    CK(cudaGraphLaunch(g->exec, st));
+    c->launches += g->nlaunch;
+    const Geometry G = make_geometry(dims, nd, max_levels_for_cap(cap));
+    AsmOut ho{};
+    std::vector<uint8_t> index(index_bytes_for(nd, G.levels));
+    const RbPart parts[2] = {{&ho, g->aout, sizeof(AsmOut)}, {index.data(), g->arch, index.size()}};
+    readback_parts(parts, 2, st);
+    if (!ho.fits || ho.index_bytes != index.size())  // more outliers than the slab's assembly allows
+        return compress_impl(c, scalar, values, on_dev, dims, nd, eb, interp, lp, cap);
+    ipcg_archive *a = new ipcg_archive;
+    a->device = c->device;
+    a->owner = st;
+    a->pool = &c->scratch;
+    a->on_device = true;
+    try {
+        parse_index(index.data(), index.size(), a->ix);
+        a->owned = static_cast<uint8_t *>(c->scratch.get(std::max<uint64_t>(ho.total, 1), st));
+        CK(cudaMemcpyAsync(a->owned, g->arch, ho.total, cudaMemcpyDeviceToDevice, st));
+    } catch (...) {
+        if (a->owned) c->scratch.put(a->owned);
+        delete a;
+        throw;
+    }
+    a->bytes = a->owned;
+    a->size = ho.total;
     return a;
 }
 
@@ -1274,6 +1465,9 @@ void ipcg_ctx_destroy(ipcg_ctx *c) {
     for (cudaStream_t s : c->odside) cudaStreamSynchronize(s);
     if (c->quant) cudaStreamSynchronize(c->quant);
     if (c->h2d) cudaStreamSynchronize(c->h2d);
+    if (c->capture) cudaStreamSynchronize(c->capture);
+    for (auto &g : c->graphs) free_graph(g);
+    if (c->capture) cudaStreamDestroy(c->capture);
     c->scratch.release_all(c->own_stream);
     if (c->own_stream) cudaStreamSynchronize(c->own_stream);
     if (c->pinned) cudaFreeHost(c->pinned);
@@ -1318,7 +1512,7 @@ int ipcg_set_host_async(ipcg_ctx *c, int enable) {
 
 int ipcg_compress(ipcg_ctx *c, int scalar, const void *values, int on_dev, const uint64_t *dims, int nd, double eb,
                   int interp, int lp, uint64_t cap, ipcg_archive **out) {
-    return guarded(c, [&] { *out = compress_impl(c, scalar, values, on_dev, dims, nd, eb, interp, lp, cap); });
+    return guarded(c, [&] { *out = compress_entry(c, scalar, values, on_dev, dims, nd, eb, interp, lp, cap); });
 }
 
 int ipcg_archive_open(ipcg_ctx *c, const void *bytes, uint64_t size, int on_device, ipcg_archive **out) {

@@ -119,12 +119,31 @@ struct ProfScope {
 // the context's stream, so a block returned by one call is reused, stream-ordered, by the
 // next.  (cudaMallocAsync of multi-GB buffers per call was measured blocking the host for
 // up to 200 ms whenever the CUDA pool had to map memory again, leaving the GPU idle.)
+//
+// Graph capture (ipcg.cu, compress graphs): while `arena` is set every request is carved from
+// that caller-owned slab by a bump pointer and never returned, so the captured kernels keep
+// valid addresses for every replay; `tally` sums a call's (rounded) requests -- the slab size
+// the next call of the same shape needs.
 struct ScratchPool {
     std::multimap<size_t, void *> free_;
     std::unordered_map<void *, size_t> size_;
+    uint8_t *arena = nullptr;
+    size_t arena_cap = 0, arena_off = 0;
+    bool arena_over = false;
+    size_t tally = 0;
     void *get(size_t bytes, cudaStream_t st) {
         bytes = (bytes + 255) & ~size_t(255);
         if (bytes == 0) bytes = 256;
+        tally += bytes;
+        if (arena) {
+            if (arena_off + bytes > arena_cap) {  // the capture is discarded (never launched)
+                arena_over = true;
+                return arena;
+            }
+            void *p = arena + arena_off;
+            arena_off += bytes;
+            return p;
+        }
         auto it = free_.lower_bound(bytes);
         if (it != free_.end() && it->first <= bytes + bytes / 4 + (size_t(1) << 20)) {
             void *p = it->second;
@@ -137,6 +156,7 @@ struct ScratchPool {
         return p;
     }
     void put(void *p) {
+        if (arena) return;
         if (p) free_.emplace(size_.at(p), p);
     }
     void release_all(cudaStream_t st) {  // caller has synchronized
