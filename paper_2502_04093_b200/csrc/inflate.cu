@@ -367,7 +367,15 @@ struct Cand {
     int bfinal;  // BFINAL bit of this block's header
     int rounds;  // lane-parallel decode rounds (diagnostics)
     int next;    // candidate starting at end_bit, -1 if none (set by k_decode_cands)
+    uint32_t t_hdr, t_tab, t_dec;  // ns: header read, table build, symbol decode (diagnostics)
+    uint32_t t_ph[6];              // IPCG_DTIME builds: ns in stage, P1, P2, range resolve, P3, P4
 };
+
+__device__ __forceinline__ unsigned long long gtimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
 
 struct Blk {
     int type;        // 0 stored, 1 symbols (candidate or fallback)
@@ -628,6 +636,11 @@ __global__ void __launch_bounds__(256) k_scan(const InflateJob *jobs, int njobs,
 constexpr int SUBB = IPCG_SUBB;      // bits per lane subsequence (lane-parallel candidate decode)
 constexpr int MARKW = SUBB / 32;     // its symbol-start bitmap words
 constexpr int NPH = IPCG_NPH;         // speculative start phases after a loss of synchronisation
+#ifdef IPCG_DTIME
+#define DT_MARK(i) do { const unsigned long long t_ = gtimer(); dt[i] += (uint32_t)(t_ - dtl); dtl = t_; } while (0)
+#else
+#define DT_MARK(i) do { } while (0)
+#endif
 constexpr int DWARPS = 2;  // warps per k_decode_cands CTA (static smem: ~16 KB of tables + bitmaps per warp)
 
 template <int CPW>
@@ -665,6 +678,7 @@ __global__ void __launch_bounds__(DWARPS * 32) k_decode_cands(const InflateJob *
         Bits b;
         int nlen = 0, ndist = 0;
         uint8_t lens[320];
+        const unsigned long long tm0 = gtimer();
         if (act) {
             b.init(job.src, job.src_len, c.hdr_bit + 3);
             Canon cs;
@@ -677,10 +691,12 @@ __global__ void __launch_bounds__(DWARPS * 32) k_decode_cands(const InflateJob *
         if (act && gl == 0)
             for (int i = 0; i < nlen + ndist; ++i) reinterpret_cast<uint8_t *>(stg_s[slot])[i] = lens[i];
         __syncwarp();
+        const unsigned long long tm1 = gtimer();
         // (the code lengths sit in the staging buffer until the tables are built)
         huff_build_group(lit_s[slot], reinterpret_cast<const uint8_t *>(stg_s[slot]), nlen, gl, G, act, false);
         huff_build_group(dist_s[slot], reinterpret_cast<const uint8_t *>(stg_s[slot]) + nlen, ndist, gl, G, act, true);
         __syncwarp();
+        const unsigned long long tm2 = gtimer();
         if (act) {  // (no early exits: every lane reaches the syncs below)
         uint32_t *out = pool + ci * (uint64_t)MAXSYM;
         uint32_t ns = 0, nz = 0;
@@ -726,6 +742,10 @@ __global__ void __launch_bounds__(DWARPS * 32) k_decode_cands(const InflateJob *
         uint64_t base = off + b.used;
         bool eob = false;
         int nrounds = 0;
+#ifdef IPCG_DTIME
+        uint32_t dt[6] = {0, 0, 0, 0, 0, 0};
+        unsigned long long dtl = gtimer();
+#endif
         while (good && !eob) {
             ++nrounds;
             if (base > endbit) {  // overrun (the stream reads as zeros past its end)
@@ -739,6 +759,7 @@ __global__ void __launch_bounds__(DWARPS * 32) k_decode_cands(const InflateJob *
                 for (int i = (int)gl; i < STG; i += 32) stg[i] = k0 + i < nwords ? __ldg(W + k0 + i) : 0u;
                 __syncwarp();
             }
+            DT_MARK(0);
             // P1: speculative decode of my subsequence from nph bit offsets, marking symbol starts;
             // per phase the exit (or the position of a path-ending symbol) goes to shared memory
             // relative to `base` (per-phase registers cost the kernel 40 registers)
@@ -762,6 +783,7 @@ __global__ void __launch_bounds__(DWARPS * 32) k_decode_cands(const InflateJob *
                 li_b1[w][ph][gl] = b1;
             }
             __syncwarp();
+            DT_MARK(1);
             // P2: each phase's path continues into subsequence gl+1 until it meets a symbol start
             // of one of lane gl+1's paths (from there the two coincide)
             // (a path that has not met lane gl+1's within its subsequence goes on through lane
@@ -806,6 +828,7 @@ __global__ void __launch_bounds__(DWARPS * 32) k_decode_cands(const InflateJob *
                 li_nx[w][ph][gl] = (uint16_t)(x1 ? cx : cc), li_bx[w][ph][gl] = x1 ? bx : cb;
             }
             __syncwarp();
+            DT_MARK(2);
             // resolve the true range [t_i, t_i+1) of every covered lane (uniform loop over shared
             // memory): lane 0's phase 0 is the true path; lane i+1's true phase is the one lane
             // i's true path met; a lane whose left neighbour met none is covered by that
@@ -880,6 +903,7 @@ __global__ void __launch_bounds__(DWARPS * 32) k_decode_cands(const InflateJob *
             // lanes (a phase-locked stream: the round covered almost nothing), and keep doing so
             // while some lane's true path is one of them; a loss further on costs little
             nph = ((lost && last < 4) || (nph > 1 && other)) ? NPH : 1;
+            DT_MARK(3);
             // P3: count my true range (the range of the last covered lane may end at the block's
             // end-of-block or at an invalid code).  From the counts P1/P2 kept: a lane on its P1
             // path takes the continuation symbols before its sync point plus its P1 symbols from
@@ -925,6 +949,8 @@ __global__ void __launch_bounds__(DWARPS * 32) k_decode_cands(const InflateJob *
                     if (q >= my_e) break;
                 }
             }
+            __syncwarp();
+            DT_MARK(4);
             // the last covered lane tells how the round ended
             const uint32_t kl = __shfl_sync(0xffffffffu, kend, last);
             const uint64_t ql = __shfl_sync(0xffffffffu, q, last);
@@ -963,6 +989,7 @@ __global__ void __launch_bounds__(DWARPS * 32) k_decode_cands(const InflateJob *
             }
             base = (kl == 2u) ? ql : __shfl_sync(0xffffffffu, my_e, last);
             __syncwarp();
+            DT_MARK(5);
         }
         const uint64_t pos = base;
         nz = __reduce_or_sync(0xffffffffu, nz);
@@ -975,6 +1002,10 @@ __global__ void __launch_bounds__(DWARPS * 32) k_decode_cands(const InflateJob *
             c.nsyms = ns;
             c.out_bytes = bytes;
             c.rounds = nrounds;
+            c.t_hdr = (uint32_t)(tm1 - tm0), c.t_tab = (uint32_t)(tm2 - tm1), c.t_dec = (uint32_t)(gtimer() - tm2);
+#ifdef IPCG_DTIME
+            for (int i = 0; i < 6; ++i) c.t_ph[i] = dt[i];
+#endif
             // link to the candidate that starts where this block ends (the chain follows it)
             int nx = -1;
             const Tables T = tabs[c.job];
@@ -1593,12 +1624,6 @@ __device__ __forceinline__ void for_each_flagged(const uint32_t *bits, uint64_t 
     }
 }
 
-__device__ __forceinline__ unsigned long long gtimer() {
-    unsigned long long t;
-    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
-    return t;
-}
-
 // CTA-aggregated append: returns the first of `n` list slots claimed for this thread (one global
 // atomic per CTA; every thread of the CTA must call it)
 __device__ __forceinline__ unsigned long long cta_append(unsigned n, unsigned long long *ctr, unsigned *s_cnt,
@@ -2025,6 +2050,20 @@ void inflate_batch_host(const std::vector<InflateJob> &jobs, int *status_dev, De
                 fprintf(stderr, "inflate: slowest candidates (rounds, bits, syms):");
                 for (size_t q = rb.size() > 8 ? rb.size() - 8 : 0; q < rb.size(); ++q) fprintf(stderr, " (%d, %llu)", rb[q].first, (unsigned long long)rb[q].second);
                 fprintf(stderr, "\n");
+                std::vector<const Cand *> byt;
+                for (const Cand &cc : hcands) byt.push_back(&cc);
+                std::sort(byt.begin(), byt.end(), [](const Cand *a, const Cand *b) { return a->t_hdr + a->t_tab + a->t_dec > b->t_hdr + b->t_tab + b->t_dec; });
+                fprintf(stderr, "inflate: slowest candidates by time (hdr us, tables us, decode us, rounds, syms):");
+                for (size_t q = 0; q < byt.size() && q < 6; ++q)
+                    fprintf(stderr, " (%.1f, %.1f, %.1f, %d, %u)", byt[q]->t_hdr * 1e-3, byt[q]->t_tab * 1e-3, byt[q]->t_dec * 1e-3, byt[q]->rounds, byt[q]->nsyms);
+#ifdef IPCG_DTIME
+                fprintf(stderr, "\ninflate: their decode phases (stage, P1, P2, ranges, P3, P4 us):");
+                for (size_t q = 0; q < byt.size() && q < 6; ++q)
+                    fprintf(stderr, " (%.1f, %.1f, %.1f, %.1f, %.1f, %.1f)", byt[q]->t_ph[0] * 1e-3, byt[q]->t_ph[1] * 1e-3, byt[q]->t_ph[2] * 1e-3, byt[q]->t_ph[3] * 1e-3, byt[q]->t_ph[4] * 1e-3, byt[q]->t_ph[5] * 1e-3);
+#endif
+                double sh = 0, stb = 0, sd = 0;
+                for (const Cand &cc : hcands) sh += cc.t_hdr, stb += cc.t_tab, sd += cc.t_dec;
+                fprintf(stderr, "\ninflate: candidate time sums: hdr %.3f ms, tables %.3f ms, decode %.3f ms\n", sh * 1e-6, stb * 1e-6, sd * 1e-6);
             }
             fprintf(stderr, "inflate: %llu survivors of %llu bit offsets; decode rounds mean %.1f max %llu, bits/cand %.0f\n", hs,
                     (unsigned long long)total_src * 8, nc ? (double)rsum / nc : 0.0, (unsigned long long)rmax,
