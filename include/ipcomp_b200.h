@@ -72,6 +72,16 @@ int ipcg_synchronize(ipcg_ctx *ctx);
  * Later calls overlap it; a refine whose `previous` is host memory waits for pending copies
  * before reading it.  `out` should be page-locked for the copy to be asynchronous. */
 int ipcg_set_host_async(ipcg_ctx *ctx, int enable);
+/* Upload a HOST field ahead of its ipcg_compress (no reference counterpart: the reference has no
+ * device).  Returns at once; the copy of `bytes` bytes runs on a context-owned stream under the
+ * calls that follow.  The next ipcg_compress of this context given the same host pointer (and a
+ * shape of `bytes` bytes) compresses the staged device copy instead of uploading again; any other
+ * compress ignores it.  The copy is enqueued in shares by the retrieval calls that follow (behind
+ * their own block uploads, so it does not delay them) and the rest by that compress.  One field
+ * is staged at a time; the host field must stay unmodified and valid until the compress that
+ * takes it returns (or, if none does, until ipcg_synchronize).  `host_values` should be
+ * page-locked for the copy to be asynchronous. */
+int ipcg_stage_field(ipcg_ctx *ctx, const void *host_values, uint64_t bytes);
 
 /* compress_field<T> (include/ipcomp/pipeline.hpp:140-223).  `values` is a host or
  * device pointer (values_on_device); the archive is produced device-resident. */

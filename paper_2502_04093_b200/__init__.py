@@ -92,6 +92,7 @@ def library() -> C.CDLL:
         "ipcg_set_stream": (i32, [vp, vp]),
         "ipcg_synchronize": (i32, [vp]),
         "ipcg_set_host_async": (i32, [vp, i32]),
+        "ipcg_stage_field": (i32, [vp, vp, u64]),
         "ipcg_compress": (i32, [vp, i32, vp, i32, P(u64), i32, dbl, i32, i32, u64, P(vp)]),
         "ipcg_archive_open": (i32, [vp, vp, u64, i32, P(vp)]),
         "ipcg_archive_open_source": (i32, [vp, READ_FN, vp, P(vp)]),
@@ -148,7 +149,7 @@ def library() -> C.CDLL:
 
 EXPORTED_SYMBOLS = [
     "ipcg_ctx_create", "ipcg_ctx_destroy", "ipcg_last_error", "ipcg_set_stream", "ipcg_synchronize",
-    "ipcg_set_host_async",
+    "ipcg_set_host_async", "ipcg_stage_field",
     "ipcg_compress", "ipcg_archive_open", "ipcg_archive_index", "ipcg_archive_size", "ipcg_archive_write",
     "ipcg_archive_open_source", "ipcg_archive_read_range", "ipcg_archive_copy", "ipcg_index_serialize",
     "ipcg_index_parse", "ipcg_crc32", "ipcg_build_error_model", "ipcg_model_plan_for_error",
@@ -199,6 +200,14 @@ class Context:
         """Host-async mode (ipcg_set_host_async): retrievals into host buffers return once the
         values are final on the device; the copy-out lands by the next synchronize()."""
         self.check(library().ipcg_set_host_async(self.h, 1 if enable else 0))
+
+    def stage_field(self, values) -> None:
+        """Start uploading a HOST field (ipcg_stage_field); the next compress_field of the same
+        buffer on this context compresses the staged device copy."""
+        addr, on_dev, nbytes = _ptr(values)
+        if on_dev:
+            raise ValueError("stage_field takes a host field")
+        self.check(library().ipcg_stage_field(self.h, C.c_void_p(addr), nbytes))
 
     def kernel_launches(self) -> int:
         return int(library().ipcg_kernel_launches(self.h))

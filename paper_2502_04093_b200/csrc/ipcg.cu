@@ -104,6 +104,15 @@ struct ipcg_ctx {
     std::vector<cudaStream_t> odside;  // per-level streams of the deflate on-demand parse
     cudaStream_t quant = nullptr;      // compress's prediction/quantization chain (highest priority)
     cudaStream_t h2d = nullptr;        // compress's upload of a host field
+    // a host field uploaded ahead of its compress (ipcg_stage_field): context-owned device copy
+    struct Staged {
+        cudaStream_t stream = nullptr;
+        cudaEvent_t ready = nullptr;
+        void *dev = nullptr;
+        size_t cap = 0;
+        const void *host = nullptr;  // the staged field (nullptr: none pending)
+        size_t bytes = 0, issued = 0;  // bytes whose copy is enqueued so far (stage_pump)
+    } staged;
     std::vector<cudaEvent_t> events;
     size_t events_used = 0;
     ScratchPool scratch;  // per-call device scratch, reused across calls (also archive/session memory)
@@ -933,6 +942,28 @@ void *src_pinned(ipcg_ctx *c, size_t bytes) {
     return c->src_pinned;
 }
 
+// Enqueue up to `budget` more bytes of a pending ipcg_stage_field upload.  The copy engine serves
+// host->device copies in issue order, so the whole field enqueued at once sits in front of every
+// upload -- block spans, descriptor tables -- of the retrievals that follow (measured on cfg2: the
+// fresh retrieval 6.8 -> 13.5 ms; with a share enqueued right after each retrieval's block uploads,
+// that call's later table uploads waited instead: 3.3 -> 9 ms).  So each retrieval enqueues a share
+// once all its own work is enqueued -- the pieces cross PCIe under its merge and reconstruction
+// kernels -- and the compress that takes the field enqueues whatever is left.  (A zero-copy
+// kernel reading the pinned field instead of the copy engine was measured too: it slowed the
+// concurrent archive write and the fresh retrieval by as much as it saved.)
+void stage_pump(ipcg_ctx *c, size_t budget) {
+    ipcg_ctx::Staged &sg = c->staged;
+    if (!sg.host || sg.issued >= sg.bytes) return;
+    const size_t piece = size_t(32) << 20;
+    while (sg.issued < sg.bytes && budget > 0) {
+        const size_t len = std::min<size_t>({piece, sg.bytes - sg.issued, budget});
+        CK(cudaMemcpyAsync(static_cast<uint8_t *>(sg.dev) + sg.issued, static_cast<const uint8_t *>(sg.host) + sg.issued,
+                           len, cudaMemcpyHostToDevice, sg.stream));
+        sg.issued += len, budget -= len;
+    }
+    if (sg.issued == sg.bytes) CK(cudaEventRecord(sg.ready, sg.stream));
+}
+
 void retrieve_impl(ipcg_ctx *c, ipcg_archive *a, int scalar, const int *k, void *out, int out_on_dev,
                    uint64_t out_count, const ipcg_session *prev_sess, const void *previous, int prev_on_dev,
                    uint64_t prev_count, ipcg_session **sess_out, ipcg_retrieve_stats *stats) {
@@ -1387,6 +1418,12 @@ void retrieve_impl(ipcg_ctx *c, ipcg_archive *a, int scalar, const int *k, void 
             if (level <= ix.progressive_levels) ns->merged[li] = merged;
             else scratch_put(merged, st);
         }
+        {
+            // a field staged for the next compress (ipcg_stage_field): a share of its upload now,
+            // behind everything this call uploads and under the kernels it still has to run
+            static const size_t pump_mib = getenv("IPCG_STAGE_PUMP") ? strtoull(getenv("IPCG_STAGE_PUMP"), nullptr, 10) : 64;  // dev knob (MiB per retrieval; measured on cfg2's e2e step, 56.3 ms without staging: 64 -> 54.7, 96 -> 54.4-55.8, 128 -> 55.0, 192 -> 55.2 -- larger shares delay the third retrieval's uploads by more than they save the compress)
+            stage_pump(c, pump_mib << 20);
+        }
         finish_checks();  // every checksum, then identity lengths, then the inflate status
         if (slot) {
             CK(cudaEventRecord(slot->ready, st));
@@ -1465,6 +1502,12 @@ void ipcg_ctx_destroy(ipcg_ctx *c) {
     for (cudaStream_t s : c->odside) cudaStreamSynchronize(s);
     if (c->quant) cudaStreamSynchronize(c->quant);
     if (c->h2d) cudaStreamSynchronize(c->h2d);
+    if (c->staged.stream) {
+        cudaStreamSynchronize(c->staged.stream);
+        cudaStreamDestroy(c->staged.stream);
+        cudaEventDestroy(c->staged.ready);
+        if (c->staged.dev) cudaFree(c->staged.dev);
+    }
     if (c->capture) cudaStreamSynchronize(c->capture);
     for (auto &g : c->graphs) free_graph(g);
     if (c->capture) cudaStreamDestroy(c->capture);
@@ -1496,6 +1539,7 @@ int ipcg_synchronize(ipcg_ctx *c) {
     return guarded(c, [&] {
         drain_copies(c);
         CK(cudaStreamSynchronize(c->stream));
+        if (c->staged.stream) CK(cudaStreamSynchronize(c->staged.stream));  // enqueued pieces of a staged field
     });
 }
 
@@ -1510,9 +1554,47 @@ int ipcg_set_host_async(ipcg_ctx *c, int enable) {
     });
 }
 
+int ipcg_stage_field(ipcg_ctx *c, const void *host_values, uint64_t bytes) {
+    return guarded(c, [&] {
+        ipcg_ctx::Staged &sg = c->staged;
+        if (!host_values || !bytes) throw Error(EINVAL_, "stage_field: null field");
+        if (!sg.stream) {
+            CK(cudaStreamCreateWithFlags(&sg.stream, cudaStreamNonBlocking));
+            CK(cudaEventCreateWithFlags(&sg.ready, cudaEventDisableTiming));
+        }
+        // the last compress that read the staging buffer has returned (compress synchronizes), and
+        // a pending upload that was never consumed is simply overwritten behind it in stream order
+        if (bytes > sg.cap) {
+            CK(cudaStreamSynchronize(sg.stream));
+            if (sg.dev) CK(cudaFree(sg.dev));
+            sg.dev = nullptr, sg.cap = 0;
+            CK(cudaMalloc(&sg.dev, bytes));
+            sg.cap = bytes;
+        }
+        sg.host = host_values, sg.bytes = bytes, sg.issued = 0;
+        // (the copies are enqueued by stage_pump: in shares by the retrievals that follow, the rest
+        // by the compress that takes the field)
+    });
+}
+
 int ipcg_compress(ipcg_ctx *c, int scalar, const void *values, int on_dev, const uint64_t *dims, int nd, double eb,
                   int interp, int lp, uint64_t cap, ipcg_archive **out) {
-    return guarded(c, [&] { *out = compress_entry(c, scalar, values, on_dev, dims, nd, eb, interp, lp, cap); });
+    return guarded(c, [&] {
+        // a host field staged ahead (ipcg_stage_field) is compressed from its device copy
+        ipcg_ctx::Staged &sg = c->staged;
+        if (!on_dev && values && sg.host == values) {
+            uint64_t n = 1;
+            bool ok = nd >= 1 && nd <= 4 && dims;
+            for (int i = 0; ok && i < nd; ++i) ok = dims[i] >= 1 && n <= sg.bytes / dims[i], n *= ok ? dims[i] : 1;
+            if (ok && n * (scalar == 0 ? 4u : 8u) == sg.bytes) {
+                stage_pump(c, sg.bytes);
+                CK(cudaStreamWaitEvent(c->stream, sg.ready, 0));
+                values = sg.dev, on_dev = 1;
+            }
+            sg.host = nullptr;
+        }
+        *out = compress_entry(c, scalar, values, on_dev, dims, nd, eb, interp, lp, cap);
+    });
 }
 
 int ipcg_archive_open(ipcg_ctx *c, const void *bytes, uint64_t size, int on_device, ipcg_archive **out) {

@@ -57,6 +57,33 @@ def test_host_async_chain_matches_oracle(lp, oracle_lib):
     assert sync.values.tobytes() == want_prev.tobytes()
 
 
+@pytest.mark.parametrize("dtype,dims", [(np.float32, (40, 36, 30)), (np.float64, (70, 130))])
+def test_staged_field_compresses_like_a_direct_upload(dtype, dims, oracle_lib):
+    """ipcg_stage_field: a host field uploaded ahead of its compress gives the oracle's archive
+    bytes; a compress of another buffer ignores (and drops) the staged copy; a staged field is
+    used once."""
+    import torch
+
+    ctx = ipc.Context(0)
+    f = torch.from_numpy(_field(dims, 7, dtype).reshape(-1)).pin_memory()
+    g = torch.from_numpy(_field(dims, 8, dtype).reshape(-1)).pin_memory()
+    eb = _eb(f.numpy(), 1e-4)
+    want_f = oracle_lib.compress(f.numpy(), dims, eb, 1)
+    want_g = oracle_lib.compress(g.numpy(), dims, eb, 1)
+    for _ in range(2):  # (the second round re-stages over a consumed copy)
+        ctx.stage_field(f)
+        assert ipc.compress_field(f, dims, eb, ipc.CUBIC, ctx=ctx).to_bytes() == want_f
+    assert ipc.compress_field(f, dims, eb, ipc.CUBIC, ctx=ctx).to_bytes() == want_f  # nothing staged
+    ctx.stage_field(f)
+    assert ipc.compress_field(g, dims, eb, ipc.CUBIC, ctx=ctx).to_bytes() == want_g  # another buffer
+    assert ipc.compress_field(f, dims, eb, ipc.CUBIC, ctx=ctx).to_bytes() == want_f  # the copy was dropped
+    ctx.stage_field(f)
+    ctx.stage_field(g)  # replaces the pending one
+    assert ipc.compress_field(g, dims, eb, ipc.CUBIC, ctx=ctx).to_bytes() == want_g
+    with pytest.raises(ValueError):
+        ctx.stage_field(f.cuda())
+
+
 # ---- session file (SURVEY.md §8f rank 1): write_session / read_session, session.cpp:8-61
 import hashlib  # noqa: E402
 import json  # noqa: E402

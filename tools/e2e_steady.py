@@ -19,14 +19,21 @@ ctx.set_host_async(True)
 for it in range(6):
     T = [time.time()]
     r = ipc.compress_field(host_f, dims, eb, c["interp"], ctx=ctx); T.append(time.time())
+    if len(sys.argv) > 1 and "stage" in sys.argv[1] and it < 5:
+        ctx.stage_field(host_f)
     size = r.size()
     r.write_to(host_arch[:size]); T.append(time.time())
     del r
     rh = ipc.ArchiveReader(host_arch[:size], ctx=ctx)
     rng_ = rh.header().range
-    o = ipc.reconstruct_field(rh, ipc.plan_for_error(rh, rels[0] * rng_), out=host_out); T.append(time.time())
-    for rel in rels[1:]:
-        o = ipc.refine_field(rh, o.session, host_out, ipc.plan_for_error(rh, rel * rng_), out=host_out); T.append(time.time())
+    if len(sys.argv) > 1 and "nod2h" in sys.argv[1]:  # experiment: results stay on the device
+        o = ipc.reconstruct_field(rh, ipc.plan_for_error(rh, rels[0] * rng_), device=True); T.append(time.time())
+        for rel in rels[1:]:
+            o = ipc.refine_field(rh, o.session, o.values, ipc.plan_for_error(rh, rel * rng_)); T.append(time.time())
+    else:
+        o = ipc.reconstruct_field(rh, ipc.plan_for_error(rh, rels[0] * rng_), out=host_out); T.append(time.time())
+        for rel in rels[1:]:
+            o = ipc.refine_field(rh, o.session, host_out, ipc.plan_for_error(rh, rel * rng_), out=host_out); T.append(time.time())
     if it >= 3:
         d = [1e3 * (b - a) for a, b in zip(T, T[1:])]
         print(f"step {1e3*(T[-1]-T[0]):.1f} ms: compress {d[0]:.1f} write {d[1]:.1f} fresh {d[2]:.1f} refines " +
