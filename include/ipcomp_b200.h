@@ -202,6 +202,11 @@ typedef struct {
 int ipcg_build_error_model(const ipcg_index *ix, ipcg_error_model *out);
 int ipcg_model_plan_for_error(const ipcg_error_model *m, double max_error, int *k_out);
 int ipcg_model_plan_for_size(const ipcg_error_model *m, uint64_t byte_budget, int *k_out);
+/* The same planners (planner.cpp:125-290) as one GPU launch on the context's stream: by_size = 0
+ * plans for `max_error` (plan_for_error), 1 for `byte_budget` (plan_for_size).  Plans, error
+ * kinds and messages are the host planner's; the host calls above stay the default. */
+int ipcg_model_plan_device(ipcg_ctx *ctx, const ipcg_error_model *m, int by_size, double max_error,
+                           uint64_t byte_budget, int *k_out);
 double ipcg_model_bound_for_plan(const ipcg_error_model *m, const int *k);
 uint64_t ipcg_model_plan_payload_bytes(const ipcg_error_model *m, const int *k);
 uint64_t ipcg_model_mandatory_payload_bytes(const ipcg_error_model *m);

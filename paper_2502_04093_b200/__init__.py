@@ -126,6 +126,7 @@ def library() -> C.CDLL:
         "ipcg_build_error_model": (i32, [P(Index), P(ErrorModelC)]),
         "ipcg_model_plan_for_error": (i32, [P(ErrorModelC), dbl, P(i32)]),
         "ipcg_model_plan_for_size": (i32, [P(ErrorModelC), u64, P(i32)]),
+        "ipcg_model_plan_device": (i32, [vp, P(ErrorModelC), i32, dbl, u64, P(i32)]),
         "ipcg_model_bound_for_plan": (dbl, [P(ErrorModelC), P(i32)]),
         "ipcg_model_plan_payload_bytes": (u64, [P(ErrorModelC), P(i32)]),
         "ipcg_model_mandatory_payload_bytes": (u64, [P(ErrorModelC)]),
@@ -153,7 +154,7 @@ EXPORTED_SYMBOLS = [
     "ipcg_compress", "ipcg_archive_open", "ipcg_archive_index", "ipcg_archive_size", "ipcg_archive_write",
     "ipcg_archive_open_source", "ipcg_archive_read_range", "ipcg_archive_copy", "ipcg_index_serialize",
     "ipcg_index_parse", "ipcg_crc32", "ipcg_build_error_model", "ipcg_model_plan_for_error",
-    "ipcg_model_plan_for_size", "ipcg_model_bound_for_plan", "ipcg_model_plan_payload_bytes",
+    "ipcg_model_plan_for_size", "ipcg_model_plan_device", "ipcg_model_bound_for_plan", "ipcg_model_plan_payload_bytes",
     "ipcg_model_mandatory_payload_bytes", "ipcg_model_total_payload_bytes", "ipcg_split", "ipcg_plane_xor",
     "ipcg_merge",
     "ipcg_archive_payload_bytes_read", "ipcg_archive_free", "ipcg_reconstruct", "ipcg_refine",
@@ -568,6 +569,30 @@ def plan_for_size(model: ArchiveReader, byte_budget: int) -> RetrievalPlan:
     k = (C.c_int * model.levels)()
     model.ctx.check(library().ipcg_plan_for_size(model.ctx.h, model.h, int(byte_budget), k))
     return RetrievalPlan(list(k))
+
+
+def error_model_c(reader: ArchiveReader) -> ErrorModelC:
+    """The plain ErrorModel (planner.hpp:13-32) of an archive's index."""
+    m = ErrorModelC()
+    reader.ctx.check(library().ipcg_build_error_model(C.byref(reader._ix), C.byref(m)))
+    return m
+
+
+def plan_on_device(model, *, max_error: float | None = None, byte_budget: int | None = None,
+                   ctx: Context | None = None) -> RetrievalPlan:
+    """plan_for_error / plan_for_size as one GPU launch (ipcg_model_plan_device, SURVEY §8f rank 4);
+    `model` is an ArchiveReader or an ErrorModelC.  Same plans and errors as the host planner."""
+    if (max_error is None) == (byte_budget is None):
+        raise ValueError("give exactly one of max_error and byte_budget")
+    if isinstance(model, ArchiveReader):
+        ctx = ctx or model.ctx
+        model = error_model_c(model)
+    ctx = ctx or Context.default()
+    k = (C.c_int * MAX_LEVELS)()
+    by_size = byte_budget is not None
+    ctx.check(library().ipcg_model_plan_device(ctx.h, C.byref(model), 1 if by_size else 0,
+                                               0.0 if by_size else float(max_error), int(byte_budget or 0), k))
+    return RetrievalPlan(list(k)[:model.levels])
 
 
 def bound_for_plan(model: ArchiveReader, plan) -> float:

@@ -37,6 +37,10 @@ uint64_t mandatory_payload_bytes(const ipcg_error_model &m);
 uint64_t total_payload_bytes(const ipcg_error_model &m);
 void plan_for_error(const ipcg_error_model &m, double max_error, int *k);
 void plan_for_size(const ipcg_error_model &m, uint64_t budget, int *k);
+// the same two planners as one single-CTA launch (planner.cu); identical plans and errors.
+// (cuda_runtime's cudaStream_t: declared as the opaque pointer it is to keep this header host-only)
+void plan_on_device(const ipcg_error_model &m, int mode, double max_error, uint64_t budget, int *k,
+                    struct CUstream_st *stream);
 // the same from an index (build_error_model first)
 double bound_for_plan(const ipcg_index &ix, const int *k);
 uint64_t plan_payload_bytes(const ipcg_index &ix, const int *k);

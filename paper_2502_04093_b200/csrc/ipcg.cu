@@ -2122,6 +2122,14 @@ int ipcg_model_plan_for_error(const ipcg_error_model *m, double max_error, int *
         plan_for_error(*m, max_error, k_out);
     });
 }
+int ipcg_model_plan_device(ipcg_ctx *c, const ipcg_error_model *m, int by_size, double max_error, uint64_t byte_budget,
+                           int *k_out) {
+    return guarded(c, [&] {
+        if (!c || !m || !k_out) throw Error(EINVAL_, "plan_device: null argument");
+        plan_on_device(*m, by_size ? 1 : 0, max_error, byte_budget, k_out, c->stream);
+        ++c->launches;
+    });
+}
 int ipcg_model_plan_for_size(const ipcg_error_model *m, uint64_t budget, int *k_out) {
     return guarded(nullptr, [&] {
         check_model(*m);

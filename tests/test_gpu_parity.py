@@ -156,6 +156,82 @@ def test_planner_matches_oracle(oracle_lib, ctx):
         ipc.plan_for_error(reader, eb * 0.5)
 
 
+def _host_plan(m, *, max_error=None, byte_budget=None):
+    k = (ipc.C.c_int * ipc.MAX_LEVELS)()
+    lib = ipc.library()
+    if byte_budget is None:
+        rc = lib.ipcg_model_plan_for_error(ipc.C.byref(m), float(max_error), k)
+    else:
+        rc = lib.ipcg_model_plan_for_size(ipc.C.byref(m), int(byte_budget), k)
+    if rc:
+        return rc, (lib.ipcg_last_error(None) or b"").decode(), None
+    return 0, "", list(k)[:m.levels]
+
+
+def _device_plan(ctx, m, **kw):
+    try:
+        return 0, "", ipc.plan_on_device(m, ctx=ctx, **kw).k
+    except ipc.InfeasibleRequest as e:
+        return 4, str(e), None
+    except RuntimeError as e:
+        return 2, str(e), None
+
+
+def test_device_planner_matches_host_and_oracle(oracle_lib, ctx):
+    """plan_for_error / plan_for_size as one GPU launch (planner.cu) give the
+    host planner's plans (and the oracle's), error kinds and messages."""
+    for dims, dtype, interp, lp in [((33, 29, 17), np.float64, 0, 0), ((40, 36, 30), np.float32, 1, 0),
+                                    ((70, 130), np.float32, 1, 2), ((9,), np.float32, 0, 0)]:
+        f = _field(dims, 42, dtype)
+        eb = _eb(f, 1e-4)
+        arch = oracle_lib.compress(f, dims, eb, interp, lp)
+        reader = ipc.ArchiveReader(arch, ctx=ctx)
+        for factor in (1.0, 1.5, 4.0, 64.0, 1024.0, 65536.0, 1e30, float("inf")):
+            assert ipc.plan_on_device(reader, max_error=factor * eb).k == oracle_lib.plan_for_error(arch, factor * eb)
+        for bad in (eb * 0.5, float("nan")):
+            with pytest.raises(ipc.InfeasibleRequest, match="below the archive's compression bound"):
+                ipc.plan_on_device(reader, max_error=bad)
+        total = oracle_lib.plan_payload_bytes(arch, [32] * reader.levels)
+        m = ipc.error_model_c(reader)
+        for b in [0, 1, total // 7, total // 3, total // 2, int(total * 0.9), total - 1, total, 2 * total, 2**63]:
+            rc, msg, want = _host_plan(m, byte_budget=b)
+            drc, dmsg, got = _device_plan(ctx, m, byte_budget=b)
+            assert (drc, got) == (rc, want), (dims, b)
+            if rc:
+                assert dmsg == msg
+            else:
+                assert got == oracle_lib.plan_for_size(arch, b)
+
+
+def test_device_planner_random_models(ctx):
+    """Hand-built ErrorModels (planner.hpp:13-32): ties between choices, zero-length planes,
+    zero deltas, a single level, 16 levels -- device plans equal the host planner's."""
+    rng = np.random.default_rng(5)
+    for case in range(60):
+        m = ipc.ErrorModelC()
+        m.levels = int(rng.integers(1, ipc.MAX_LEVELS + 1))
+        m.progressive_levels = int(rng.integers(0, m.levels + 1))
+        m.eb = float(10.0 ** rng.uniform(-9, 0))
+        m.amplification = float(rng.choice([1.0, 1.25]))
+        for l in range(m.levels):
+            lc = m.level[l]
+            steps = rng.choice([0.0, 1.0, 2.0], size=32, p=[0.3, 0.4, 0.3]) * 10.0 ** rng.uniform(-9, 1)
+            d = np.concatenate([[0.0], np.cumsum(steps)])  # non-decreasing, with plateaus (ties)
+            for i in range(33):
+                lc.delta[i] = float(d[i])
+            pb = rng.integers(0, 1 << int(rng.integers(1, 28)), size=32) * rng.choice([0, 1], size=32, p=[0.2, 0.8])
+            for i in range(32):
+                lc.plane_bytes[i] = int(pb[i])
+            lc.outlier_bytes = int(rng.integers(0, 1000))
+            lc.progressive = 1 if l + 1 <= m.progressive_levels else 0
+        total = int(ipc.library().ipcg_model_total_payload_bytes(ipc.C.byref(m)))
+        for q in range(6):
+            target = m.eb * float(10.0 ** rng.uniform(-0.3, 12))
+            assert _device_plan(ctx, m, max_error=target) == _host_plan(m, max_error=target), (case, q)
+            b = int(rng.integers(0, max(2, 2 * total)))
+            assert _device_plan(ctx, m, byte_budget=b) == _host_plan(m, byte_budget=b), (case, q, b)
+
+
 def test_backend_encode_matches_zlib(ctx):
     import zlib
 
