@@ -47,6 +47,7 @@ def parse():
     ap.add_argument("--dims", default=None, help="override dims, e.g. 256x256x256 (parity/debug only)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-stage", action="store_true", help="e2e without staging the next step's field (A/B)")
     return ap.parse_args()
 
 
@@ -333,7 +334,7 @@ def run_ours(args, ws, rank, local):
         g0, g1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         g0.record(stream)
         for i in range(args.steps):
-            step_host(stage_next=i + 1 < args.steps)
+            step_host(stage_next=i + 1 < args.steps and not args.no_stage)
         ctx.synchronize()
         g1.record(stream)
         torch.cuda.synchronize()

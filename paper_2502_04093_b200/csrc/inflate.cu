@@ -629,6 +629,111 @@ __global__ void __launch_bounds__(256) k_scan(const InflateJob *jobs, int njobs,
     }
 }
 
+// read_dynamic_header for k_decode_cands: the same acceptance rules and the same lens[], but the
+// header's words staged in shared memory by the warp first (one coalesced load instead of a byte
+// refill every few symbols) and the code-length code decoded through a 128-entry table instead of
+// zlib's bit-at-a-time canonical loop (20-135 us -> a few us per block on the retrievals' critical
+// path).  Every lane runs it on the same block (uniform; shared-memory writes are the same value
+// from every lane).  hw: HDRW words, tab: 128 bytes, lens: >= 320 bytes, all shared and warp-private.
+// `used` returns the bit position after the header, relative to the stream's first byte.
+constexpr int HDRW = 160;  // 14 + 57 + 316 symbols x (7 + 7) bits = 4495 bits at most, + alignment + window reach
+__device__ bool read_dynamic_header_warp(const InflateJob &job, uint64_t bit, uint32_t *hw, uint8_t *tab, uint8_t *lens,
+                                         int &nlen, int &ndist, uint64_t &used, unsigned lane) {
+    const uintptr_t sa = reinterpret_cast<uintptr_t>(job.src);
+    const uint64_t off = (uint64_t)(sa & 3) * 8;
+    const uint32_t *W = reinterpret_cast<const uint32_t *>(sa & ~uintptr_t(3));
+    const uint64_t nwords = (off / 8 + job.src_len + 3) / 4;
+    const uint64_t p0 = off + bit, k0 = p0 >> 5;
+    __syncwarp();
+    for (int i = (int)lane; i < HDRW; i += 32) hw[i] = k0 + i < nwords ? __ldg(W + k0 + i) : 0u;
+    __syncwarp();
+    uint32_t r = (uint32_t)(p0 & 31);  // bit position relative to the first staged word
+    auto window = [&](uint32_t q) {
+        const uint32_t k = q >> 5, sh = q & 31;
+        return (uint64_t)__funnelshift_r(hw[k], hw[k + 1], sh) | ((uint64_t)__funnelshift_r(hw[k + 1], hw[k + 2], sh) << 32);
+    };
+    uint64_t v = window(r);
+    nlen = (int)(v & 31) + 257, ndist = (int)((v >> 5) & 31) + 1;
+    const int ncode = (int)((v >> 10) & 15) + 4;
+    if (nlen > 286 || ndist > 30) return false;
+    r += 14;
+    v = window(r);
+    uint8_t cll[19];
+#pragma unroll
+    for (int i = 0; i < 19; ++i) cll[i] = 0;
+    for (int i = 0; i < ncode; ++i) cll[kOrder[i]] = (uint8_t)((v >> (3 * i)) & 7);
+    r += 3 * (uint32_t)ncode;
+    uint32_t cnt[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+#pragma unroll
+    for (int i = 0; i < 19; ++i) cnt[cll[i]]++;
+    int left = 1;
+#pragma unroll
+    for (int l = 1; l <= 7; ++l) {
+        left = (left << 1) - (int)cnt[l];
+        if (left < 0) return false;
+    }
+    if (left != 0) return false;  // incomplete or empty code-length code (inflate_table rejects both here)
+    uint32_t next[8];
+    next[1] = 0;
+#pragma unroll
+    for (int l = 1; l < 7; ++l) next[l + 1] = (next[l] + cnt[l]) << 1;
+    for (int sym = 0; sym < 19; ++sym) {
+        const int L = cll[sym];
+        if (!L) continue;
+        const uint32_t code = next[L]++;
+        const uint32_t rev = __brev(code) >> (32 - L);
+        for (uint32_t e = 0; e < (1u << (7 - L)); ++e) tab[rev | (e << L)] = (uint8_t)(sym | L << 5);
+    }
+    __syncwarp();
+    const int total = nlen + ndist;
+    int idx = 0;
+    uint8_t prev = 0;
+    uint32_t kl = 0, kd = 0;  // Kraft sums (units of 2^-15): an over-subscribed code is rejected at once
+    while (idx < total) {
+        v = window(r);
+        const uint32_t e = tab[v & 127];
+        const int L = e >> 5, sym = e & 31;
+        v >>= L;
+        r += (uint32_t)L;
+        if (sym < 16) {
+            if (sym) {
+                if (idx < nlen) kl += 32768u >> sym;
+                else kd += 32768u >> sym;
+                if (kl > 32768u || kd > 32768u) return false;
+            }
+            lens[idx++] = (uint8_t)sym;
+            prev = (uint8_t)sym;
+            continue;
+        }
+        int rep;
+        uint8_t val = 0;
+        if (sym == 16) {
+            if (idx == 0) return false;
+            val = prev;
+            rep = 3 + (int)(v & 3), r += 2;
+        } else if (sym == 17) {
+            rep = 3 + (int)(v & 7), r += 3;
+        } else {
+            rep = 11 + (int)(v & 127), r += 7;
+        }
+        if (idx + rep > total) return false;
+        if (val) {
+            const int inl = idx < nlen ? min(rep, nlen - idx) : 0;
+            kl += (uint32_t)inl * (32768u >> val);
+            kd += (uint32_t)(rep - inl) * (32768u >> val);
+            if (kl > 32768u || kd > 32768u) return false;
+        }
+        for (int q = 0; q < rep; ++q) lens[idx + q] = val;
+        prev = val;
+        idx += rep;
+    }
+    __syncwarp();
+    if (lens[256] == 0) return false;
+    used = (k0 << 5) + r - off;
+    if (used > 8 * job.src_len) return false;  // read past the stream end
+    return true;
+}
+
 // ------------------------------------------------------------ 2. candidates
 // CPW candidates per warp, one per group of 32/CPW lanes: the decode is inherently
 // sequential per block and every lane of a group does the same work, so packing several
@@ -675,21 +780,20 @@ __global__ void __launch_bounds__(DWARPS * 32) k_decode_cands(const InflateJob *
         Cand dummy;
         Cand &c = act ? cands[ci] : dummy;
         const InflateJob job = jobs[act ? c.job : 0];
-        Bits b;
         int nlen = 0, ndist = 0;
-        uint8_t lens[320];
+        uint64_t used = 0;  // bits of the stream consumed so far (from its first byte)
         const unsigned long long tm0 = gtimer();
-        if (act) {
-            b.init(job.src, job.src_len, c.hdr_bit + 3);
-            Canon cs;
-            const bool ok = read_dynamic_header(b, lens, nlen, ndist, cs);  // identical on the group's lanes
-            if (!ok) {
+        {
+            // the header's code lengths land in the staging buffer (the tables are built from
+            // there); the header words and the code-length table borrow the mark bitmaps
+            uint32_t *hw = marks_s[w];
+            const bool ok = act && read_dynamic_header_warp(job, c.hdr_bit + 3, hw, reinterpret_cast<uint8_t *>(hw + HDRW),
+                                                            reinterpret_cast<uint8_t *>(stg_s[slot]), nlen, ndist, used, lane);
+            if (act && !ok) {
                 if (gl == 0) c.ok = 0;
                 act = false;
             }
         }
-        if (act && gl == 0)
-            for (int i = 0; i < nlen + ndist; ++i) reinterpret_cast<uint8_t *>(stg_s[slot])[i] = lens[i];
         __syncwarp();
         const unsigned long long tm1 = gtimer();
         // (the code lengths sit in the staging buffer until the tables are built)
@@ -719,16 +823,19 @@ __global__ void __launch_bounds__(DWARPS * 32) k_decode_cands(const InflateJob *
         const uint64_t nwords = (off / 8 + job.src_len + 3) / 4, endbit = off + 8 * job.src_len;
         uint32_t *stg = stg_s[w];
         uint64_t k0 = 0;  // first staged word
+        // 64 stream bits from absolute bit P >= the round's first staged bit: the position relative
+        // to the staged words in 32-bit arithmetic (a round spans < 2^16 bits; the 64-bit word
+        // index, bounds and shifts were ~20 of the ~45 instructions before each table lookup)
+        uint32_t kb32 = 0;  // low word of the first staged bit's position (k0 << 5)
         auto window = [&](uint64_t P) {
-            const uint64_t k = P >> 5;
-            const uint32_t sh = (uint32_t)(P & 31);
+            const uint32_t q = (uint32_t)P - kb32, k = q >> 5, sh = q & 31;
             uint32_t w0, w1, w2;
-            const uint64_t rel = k - k0;
-            if (IPCG_STAGE && k >= k0 && rel + 2 < (uint64_t)STG) {
-                w0 = stg[rel], w1 = stg[rel + 1], w2 = stg[rel + 2];
+            if (IPCG_STAGE && k < (uint32_t)(STG - 2)) {
+                w0 = stg[k], w1 = stg[k + 1], w2 = stg[k + 2];
             } else {
-                w0 = k < nwords ? __ldg(W + k) : 0u, w1 = k + 1 < nwords ? __ldg(W + k + 1) : 0u,
-                w2 = k + 2 < nwords ? __ldg(W + k + 2) : 0u;
+                const uint64_t kk = k0 + k;
+                w0 = kk < nwords ? __ldg(W + kk) : 0u, w1 = kk + 1 < nwords ? __ldg(W + kk + 1) : 0u,
+                w2 = kk + 2 < nwords ? __ldg(W + kk + 2) : 0u;
             }
             return (uint64_t)__funnelshift_r(w0, w1, sh) | ((uint64_t)__funnelshift_r(w1, w2, sh) << 32);
         };
@@ -739,7 +846,7 @@ __global__ void __launch_bounds__(DWARPS * 32) k_decode_cands(const InflateJob *
         // round that lost synchronisation every lane also runs its subsequence from the next
         // NPH-1 bit offsets, and a left neighbour may synchronise with any of those paths.
         int nph = 1;
-        uint64_t base = off + b.used;
+        uint64_t base = off + used;
         bool eob = false;
         int nrounds = 0;
 #ifdef IPCG_DTIME
@@ -754,6 +861,7 @@ __global__ void __launch_bounds__(DWARPS * 32) k_decode_cands(const InflateJob *
             }
             const uint64_t g = base + (uint64_t)gl * subb, gn = g + subb;
             k0 = base >> 5;
+            kb32 = (uint32_t)(k0 << 5);
             if (IPCG_STAGE) {
                 __syncwarp();  // the previous round's readers are done
                 for (int i = (int)gl; i < STG; i += 32) stg[i] = k0 + i < nwords ? __ldg(W + k0 + i) : 0u;
@@ -994,11 +1102,11 @@ __global__ void __launch_bounds__(DWARPS * 32) k_decode_cands(const InflateJob *
         const uint64_t pos = base;
         nz = __reduce_or_sync(0xffffffffu, nz);
         if (pos > endbit) good = false;
-        b.used = pos - off;
+        used = pos - off;
         if (gl == 0) {
             c.ok = good ? 1 : 0;
             c.nzlit = nz != 0;
-            c.end_bit = b.used;
+            c.end_bit = used;
             c.nsyms = ns;
             c.out_bytes = bytes;
             c.rounds = nrounds;
@@ -1009,7 +1117,7 @@ __global__ void __launch_bounds__(DWARPS * 32) k_decode_cands(const InflateJob *
             // link to the candidate that starts where this block ends (the chain follows it)
             int nx = -1;
             const Tables T = tabs[c.job];
-            const unsigned long long key = b.used + 1;
+            const unsigned long long key = used + 1;
             uint64_t sl = hslot(key, T.hcap);
             for (uint64_t probe = 0; probe < T.hcap; ++probe, sl = (sl + 1) & (T.hcap - 1)) {
                 const unsigned long long k = T.hash[sl];
