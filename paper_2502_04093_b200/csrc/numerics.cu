@@ -763,7 +763,9 @@ void launch_merge(const uint32_t *const *rows, const uint32_t *merged_in, uint32
                   int k1, cudaStream_t st) {
     const uint64_t words = (count + 31) / 32;
     if (words == 0) return;
-    if (merged_in && k0 > 0 && k1 - k0 <= 8) {
+    // few planes -- a refinement step on merged codewords, or a fresh merge of a coarse plan (k0 = 0,
+    // no prefix to read) -- skip the 32 x 32 bit transpose
+    if (k1 - k0 <= 8 && ((merged_in && k0 > 0) || (!merged_in && k0 == 0))) {
         const uint64_t groups = count / 4 + 1;  // + the tail group
         const unsigned g = (unsigned)((groups + 256 * MF_V - 1) / (256 * MF_V));
         k_merge_few<<<g, 256, 0, st>>>(rows, merged_in, merged_out, count, k0, k1);
