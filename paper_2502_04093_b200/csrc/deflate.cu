@@ -384,9 +384,14 @@ __global__ void __launch_bounds__(PL_WARPS * 32) k_prevlinks(const uint8_t *in, 
 // staging the tile in shared memory (the walk is latency-, not bandwidth-bound: 70 ms vs
 // 43 ms) and a per-lane state machine that refills idle lanes (87 ms: neighbouring
 // positions have similar chain lengths, so the extra state costs more than divergence).
-template <bool WIDE>  // WIDE: streams of 2^31 bytes or more (64-bit positions)
-__global__ void __launch_bounds__(256) k_match(const uint8_t *in, uint64_t in_stride, uint64_t n,
-                                              const StreamMeta *meta, const uint16_t *prevd_all, uint64_t *rec_all) {
+// A CTA takes a contiguous chunk of `chunk` positions (tile after tile of blockDim positions), so
+// its lookups stay inside one slowly sliding window -- 32 KiB of bytes + 64 KiB of links -- that
+// lives in L1; a grid-stride loop moved every CTA to a new window each iteration (ncu: 59% L1 hits,
+// two thirds of the stall samples on the L2 round trips of the scattered link / byte loads).
+template <bool WIDE, int BLOCK>  // WIDE: streams of 2^31 bytes or more (64-bit positions)
+__global__ void __launch_bounds__(BLOCK) k_match(const uint8_t *in, uint64_t in_stride, uint64_t n,
+                                                const StreamMeta *meta, const uint16_t *prevd_all, uint64_t *rec_all,
+                                                uint32_t chunk) {
     const int j = blockIdx.y;
     if (!meta[j].active || meta[j].od) return;
     uint64_t *rec = rec_all + (uint64_t)j * n;
@@ -398,13 +403,13 @@ __global__ void __launch_bounds__(256) k_match(const uint8_t *in, uint64_t in_st
         asm volatile("" : "+l"(inj), "+l"(pvj));
         const InWords words{inj};
         const PrevD32 prev{pvj};
-        for (uint32_t p = blockIdx.x * blockDim.x + threadIdx.x; p < (uint32_t)n; p += gridDim.x * blockDim.x)
-            rec[p] = match_search32(p, (uint32_t)n, words, prev);
+        const uint32_t p0 = blockIdx.x * chunk, p1 = (uint32_t)min((uint64_t)p0 + chunk, n);
+        for (uint32_t p = p0 + threadIdx.x; p < p1; p += BLOCK) rec[p] = match_search32(p, (uint32_t)n, words, prev);
     } else {
         const InBytes bytes{in + (uint64_t)j * in_stride};
         const PrevD prev{prevd_all + (uint64_t)j * n};
-        for (uint64_t p = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; p < n; p += (uint64_t)gridDim.x * blockDim.x)
-            rec[p] = match_search((int64_t)p, (int64_t)n, bytes, prev);
+        const uint64_t p0 = (uint64_t)blockIdx.x * chunk, p1 = min(p0 + chunk, n);
+        for (uint64_t p = p0 + threadIdx.x; p < p1; p += BLOCK) rec[p] = match_search((int64_t)p, (int64_t)n, bytes, prev);
     }
 }
 
@@ -1717,10 +1722,25 @@ void DeflateBatch::run(const uint8_t *in, uint64_t in_stride, int S, uint64_t n,
         {
         {
             ProfScope ps2("deflate.match", st, (uint64_t)S * n);
-            if (n < (1ull << 31))
-                k_match<false><<<dim3(grid_for(n, 256, 4096), S), 256, 0, st>>>(in, in_stride, n, w.meta, w.prevd, w.rec);
+            static const int mblock = getenv("IPCG_MATCH_BLOCK") ? atoi(getenv("IPCG_MATCH_BLOCK")) : 512;  // dev knobs (measured on cfg2, deflate.match per compress: block x chunk 1024 x 4096 / 16384 / 65536: 8.00 / 7.29 / 7.17 ms; 512: 7.21 / 7.11 / 7.45; 256: 7.94 / 8.42 / 10.15; the grid-stride loop: 7.84)
+            static const uint32_t mchunk = getenv("IPCG_MATCH_CHUNK") ? (uint32_t)atoi(getenv("IPCG_MATCH_CHUNK")) : 16384u;
+            // chunks of at least a tile, and enough of them for every SM on small streams
+            uint32_t chunk = mchunk;
+            while (chunk > (uint32_t)mblock && (n + chunk - 1) / chunk < (uint64_t)num_sms() * 2) chunk /= 2;
+            const dim3 mg((unsigned)((n + chunk - 1) / chunk), S);
+            if (first_on_device<7>() && !getenv("IPCG_MATCH_NOCARVE")) {  // all of the SM's L1/shared array as L1
+                CK(cudaFuncSetAttribute(k_match<false, 256>, cudaFuncAttributePreferredSharedMemoryCarveout, 0));
+                CK(cudaFuncSetAttribute(k_match<false, 512>, cudaFuncAttributePreferredSharedMemoryCarveout, 0));
+                CK(cudaFuncSetAttribute(k_match<false, 1024>, cudaFuncAttributePreferredSharedMemoryCarveout, 0));
+            }
+            if (n >= (1ull << 31))
+                k_match<true, 256><<<mg, 256, 0, st>>>(in, in_stride, n, w.meta, w.prevd, w.rec, chunk);
+            else if (mblock == 256)
+                k_match<false, 256><<<mg, 256, 0, st>>>(in, in_stride, n, w.meta, w.prevd, w.rec, chunk);
+            else if (mblock == 512)
+                k_match<false, 512><<<mg, 512, 0, st>>>(in, in_stride, n, w.meta, w.prevd, w.rec, chunk);
             else
-                k_match<true><<<dim3(grid_for(n, 256, 4096), S), 256, 0, st>>>(in, in_stride, n, w.meta, w.prevd, w.rec);
+                k_match<false, 1024><<<mg, 1024, 0, st>>>(in, in_stride, n, w.meta, w.prevd, w.rec, chunk);
             CKL();
             }
             if (after_match) CK(cudaEventRecord(after_match, st));
