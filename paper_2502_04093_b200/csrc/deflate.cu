@@ -378,6 +378,104 @@ __global__ void __launch_bounds__(PL_WARPS * 32) k_prevlinks(const uint8_t *in, 
     }
 }
 
+// Two warps per head table.  With one warp per table (three per SM) the kernel runs at one warp's
+// dependent-issue latency: ~100 instructions per 32 positions of which only the head-table
+// read/write chain is serial.  Here warps A and B of a pair take alternate batches of a span: each
+// prepares its batch (bytes, hashes, match_any) and stores its links on its own, and only the
+// chain (and the window sweep) is a critical section handed back and forth with two named
+// barriers (bar.arrive by the warp that leaves it, bar.sync by the one that enters).
+__device__ __forceinline__ void pl_bar_sync(int id) { asm volatile("bar.sync %0, 64;" ::"r"(id) : "memory"); }
+__device__ __forceinline__ void pl_bar_arrive(int id) {
+    __threadfence_block();
+    asm volatile("bar.arrive %0, 64;" ::"r"(id) : "memory");
+}
+
+template <int NW>  // warps per head table
+__global__ void __launch_bounds__(PL_WARPS * NW * 32) k_prevlinks_pair(const uint8_t *in, uint64_t in_stride, uint64_t n,
+                                                                     const StreamMeta *meta, uint16_t *prevd_all, int span) {
+    extern __shared__ uint16_t heads[];
+    const int j = blockIdx.y;
+    if (!meta[j].active) return;
+    const unsigned warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const unsigned pair = warp / NW, par = warp % NW;  // table of the group; warp `par` takes batches par, par + NW, ...
+    const uint64_t out0 = ((uint64_t)blockIdx.x * PL_WARPS + pair) * (uint64_t)span * WSIZE;
+    if (out0 >= n) return;  // (both warps of the pair)
+    uint16_t *head = heads + (size_t)pair * 32768;
+    // barrier "warp g of the group left the chain": 1 + NW * group + g
+    const int bar_mine = 1 + NW * (int)pair + (int)par, bar_prev = 1 + NW * (int)pair + (int)((par + NW - 1) % NW);
+    if (par == 0) {
+        for (int i = lane; i < 32768; i += 32) head[i] = 0x8000;  // S_0
+        __syncwarp();
+    }
+    const uint8_t *p = in + (uint64_t)j * in_stride;
+    uint16_t *prevd = prevd_all + (uint64_t)j * n;
+    const uint64_t base = out0 == 0 ? 0 : out0 - WSIZE;
+    const uint64_t end = min(n, out0 + (uint64_t)span * WSIZE);
+    constexpr int AHEAD = 16;
+    constexpr uint64_t BATCH = 32 * AHEAD;
+    uint32_t b0[AHEAD], bx[AHEAD];  // byte at q; lanes 0,1: byte at q + 32
+    auto fetch = [&](uint64_t pos0) {
+#pragma unroll
+        for (int k = 0; k < AHEAD; ++k) {
+            const uint64_t q = pos0 + 32 * k + lane;
+            b0[k] = q < n ? __ldg(p + q) : 0u;
+            bx[k] = (lane < 2 && q + 32 < n) ? __ldg(p + q + 32) : 0u;
+        }
+    };
+    const uint64_t first = base + par * BATCH;
+    if (first < end) fetch(first);
+    const unsigned lt_mask = (1u << lane) - 1u;
+    for (uint64_t pos0 = first; pos0 < end; pos0 += NW * BATCH) {
+        const uint32_t rel0 = (uint32_t)(pos0 - base);
+        uint32_t hs[AHEAD], mk[AHEAD];
+#pragma unroll
+        for (int k = 0; k < AHEAD; ++k) {
+            const uint64_t q = pos0 + 32 * k + lane;
+            const uint32_t v1 = __shfl_sync(0xffffffffu, b0[k], (lane + 1) & 31);
+            const uint32_t e1 = __shfl_sync(0xffffffffu, bx[k], (lane + 1) & 31);
+            const uint32_t v2 = __shfl_sync(0xffffffffu, b0[k], (lane + 2) & 31);
+            const uint32_t e2 = __shfl_sync(0xffffffffu, bx[k], (lane + 2) & 31);
+            const uint32_t c1 = lane == 31 ? e1 : v1, c2 = lane >= 30 ? e2 : v2;
+            const bool valid = q + MIN_MATCH <= n && q < end;
+            hs[k] = valid ? hash3(b0[k], c1, c2) : (0x10000u + lane);
+        }
+        if (pos0 + NW * BATCH < end) fetch(pos0 + NW * BATCH);
+#pragma unroll
+        for (int k = 0; k < AHEAD; ++k) mk[k] = __match_any_sync(0xffffffffu, hs[k]);
+        // ---- the critical section: every batch but the first waits for the previous one's
+        if (pos0 != base) pl_bar_sync(bar_prev);
+        // the sentinel of this batch's window W = rel0 / WSIZE is ((W - 1) * WSIZE) mod 65536; the
+        // batch that opens a window sweeps the table (from the previous window's sentinel)
+        const uint32_t W = rel0 / (uint32_t)WSIZE;
+        uint32_t sent = ((W - 1u) * (uint32_t)WSIZE) & 0xFFFFu;
+        if (rel0 != 0 && (rel0 & (WSIZE - 1)) == 0) sent = prevlinks_sweep(head, lane, rel0, ((W - 2u) * (uint32_t)WSIZE) & 0xFFFFu);
+        uint32_t prel[AHEAD];
+#pragma unroll
+        for (int k = 0; k < AHEAD; ++k) {
+            const uint32_t h = hs[k];
+            const bool valid = h < 0x10000u;
+            const uint32_t rel = (uint32_t)(pos0 + 32 * k + lane - base);
+            const unsigned lower = mk[k] & lt_mask;
+            prel[k] = sent;
+            if (lower) prel[k] = rel - (lane - (31u - __clz(lower)));
+            else if (valid) prel[k] = head[h];
+            __syncwarp();
+            if (valid && lane == 31u - __clz(mk[k])) head[h] = (uint16_t)rel;
+            __syncwarp();
+        }
+        pl_bar_arrive(bar_mine);
+        // ---- links of the batch
+#pragma unroll
+        for (int k = 0; k < AHEAD; ++k) {
+            const uint64_t q = pos0 + 32 * k + lane;
+            if (q >= out0 && q < end) {
+                const uint32_t e = prel[k] & 0xFFFF, d = ((uint32_t)(q - base) - e) & 0xFFFF;
+                prevd[q] = (uint16_t)(hs[k] < 0x10000u && e != sent && d < (uint32_t)WSIZE ? d : 0u);
+            }
+        }
+    }
+}
+
 // ------------------------------------------------------------ 3. match search
 // One thread per position runs zlib's longest_match for chain limits 128 and 32 (one
 // walk, the 32-limit result snapshotted on the way).  Measured alternatives that lost:
@@ -1666,7 +1764,23 @@ void DeflateBatch::run(const uint8_t *in, uint64_t in_stride, int S, uint64_t n,
                 if (t < best - 1e-9) best = t, span = s;
             }
         }
-        k_prevlinks<<<dim3((unsigned)((nblk + span * PL_WARPS - 1) / (span * PL_WARPS)), S), PL_WARPS * 32, smem, st>>>(in, in_stride, n, w.meta, w.prevd, span);
+        // dev A/B knob: warps per head table (0: the one-warp kernel).  Measured on cfg2, deflate.prevlinks
+        // per compress: 1 warp 5.34 ms, 2 warps 3.75-3.80, 3 warps 3.58, 4 warps 6.5 (the hand-offs
+        // then cost more than the overlap gains); compress 27.4 -> 25.5 ms with 2
+        static const int pl_pair = getenv("IPCG_PL_PAIR") ? atoi(getenv("IPCG_PL_PAIR")) : 2;
+        const dim3 plg((unsigned)((nblk + span * PL_WARPS - 1) / (span * PL_WARPS)), S);
+        if (pl_pair) {
+            if (first_on_device<8>()) {
+                CK(cudaFuncSetAttribute(k_prevlinks_pair<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+                CK(cudaFuncSetAttribute(k_prevlinks_pair<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+                CK(cudaFuncSetAttribute(k_prevlinks_pair<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+            }
+            if (pl_pair == 3) k_prevlinks_pair<3><<<plg, PL_WARPS * 96, smem, st>>>(in, in_stride, n, w.meta, w.prevd, span);
+            else if (pl_pair == 4) k_prevlinks_pair<4><<<plg, PL_WARPS * 128, smem, st>>>(in, in_stride, n, w.meta, w.prevd, span);
+            else k_prevlinks_pair<2><<<plg, PL_WARPS * 64, smem, st>>>(in, in_stride, n, w.meta, w.prevd, span);
+        } else {
+            k_prevlinks<<<plg, PL_WARPS * 32, smem, st>>>(in, in_stride, n, w.meta, w.prevd, span);
+        }
         CKL();
         }
         debug_mark("P", (int)(n >> 20), st);  // (dev timeline: hash links done; tag = stream MiB)
