@@ -712,6 +712,8 @@ __global__ void __launch_bounds__(256) k_sim(uint64_t n, const StreamMeta *meta,
     uint32_t C[4], D[4];
 #pragma unroll
     for (int t = 0; t < 4; ++t) P[t] = b0, T[t] = t, A[t] = t, C[t] = 0, D[t] = 0;
+    int64_t cp = -1;  // the last record loaded (see k_emit_syms)
+    uint64_t cr = 0;
     for (;;) {
         int w = -1;
         int64_t p = INT64_MAX;
@@ -727,7 +729,11 @@ __global__ void __launch_bounds__(256) k_sim(uint64_t n, const StreamMeta *meta,
         if (m > 0) {
             np = p + MAX_MATCH * m, nt = TAG_A, cw += (uint32_t)m;
         } else {
-            const Step s = parse_step(p, tag, (int64_t)n, R(p), p > 0 ? R(p - 1) : 0ull, bytes);
+            const bool pending = tag == TAG_C128 || tag == TAG_C32;
+            const uint64_t rpm1 = !pending || p == 0 ? 0ull : cp == p - 1 ? cr : R(p - 1);
+            const uint64_t rp = cp == p ? cr : R(p);
+            cp = p, cr = rp;
+            const Step s = parse_step(p, tag, (int64_t)n, rp, rpm1, bytes);
             np = s.next_p, nt = s.next_tag, cw += s.emit != 0;
         }
         int u = -1;
@@ -908,6 +914,11 @@ __global__ void __launch_bounds__(256) k_emit_syms(const uint8_t *in, uint64_t i
     uint64_t g = symoff_all[(uint64_t)j * nchunks + k];
     const uint32_t *nbreak = nbreak_all + (uint64_t)j * (nchunks + 1);
     int64_t p = (int64_t)b0;
+    // the record at p-1 is only read under a pending match (tags C*), and it is then the record
+    // the previous step loaded: kept in a register (the lanes of a warp walk chunks 2 KiB apart,
+    // so every record load is 32 separate L1 accesses)
+    int64_t cp = -1;
+    uint64_t cr = 0;
     while (p < (int64_t)b1) {
         const int64_t m = periodic_run(p, tag, n, nbreak);
         if (m > 64) {  // long stretch: hand it to k_emit_runs
@@ -927,7 +938,11 @@ __global__ void __launch_bounds__(256) k_emit_syms(const uint8_t *in, uint64_t i
             p += MAX_MATCH * m;
             continue;
         }
-        const Step s = parse_step(p, tag, (int64_t)n, R(p), p > 0 ? R(p - 1) : 0ull, bytes);
+        const bool pending = tag == TAG_C128 || tag == TAG_C32;
+        const uint64_t rpm1 = !pending || p == 0 ? 0ull : cp == p - 1 ? cr : R(p - 1);
+        const uint64_t rp = R(p);
+        cp = p, cr = rp;
+        const Step s = parse_step(p, tag, (int64_t)n, rp, rpm1, bytes);
         if (s.emit) {
             syms[g] = s.emit == 2 ? sym_match(s.len, s.dist) : sym_literal(s.len);
             if (g % BLOCK_SYMS == 0) bstart[g / BLOCK_SYMS] = (uint64_t)p - 1;
