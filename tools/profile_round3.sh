@@ -16,7 +16,7 @@ python tools/config_table.py > $O/configs.jsonl 2> $O/configs.err
 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $O/launches.csv \
     python bench.py --steps 2 --warmup 3 --no-cpu-baseline --no-e2e > /dev/null 2>&1
 python tools/launch_summary.py $O/launches.csv > $O/launches_summary.txt
-for spec in "k_match 6" "k_prevlinks_pair 6" "k_plan 6" "k_od_walk 5" "k_emit_syms 6" "k_sim 6" "k_loss_lines 5" \
+for spec in "k_match 6" "k_prevlinks_pair 6" "k_plan 6" "k_od_walk 2" "k_emit_syms 6" "k_sim 6" "k_loss_lines 5" \
             "k_bitplanes 6" "k_rows 2" "k_rows 5" "k_decode_cands 0" "k_resolve_all 0" "k_validate 0" "k_merge 6"; do
   set -- $spec
   timeout 600 ncu --set full --clock-control none --import-source on -k regex:^$1\$ --launch-skip $2 -c 1 \
