@@ -183,6 +183,22 @@ struct InBytes {
         return len;
     }
 };
+// InBytes for a thread that walks a stream forward (k_emit_syms: the lanes of a warp walk chunks
+// 256 bytes apart, so every byte load is 32 separate L1 accesses): the aligned 8 bytes holding
+// the last byte asked for stay in a register.  (Rows are 8-byte aligned and padded to 16 bytes.)
+struct InBytesCached {
+    const uint8_t *p;
+    mutable int64_t base = -8;
+    mutable uint64_t w = 0;
+    __device__ __forceinline__ uint32_t operator()(int64_t i) const {
+        const int64_t b = i & ~int64_t(7);
+        if (b != base) {
+            base = b;
+            w = __ldg(reinterpret_cast<const uint64_t *>(p + b));
+        }
+        return (uint32_t)(w >> (8 * (unsigned)(i - b))) & 0xffu;
+    }
+};
 struct PrevD {
     const uint16_t *p;
     __device__ __forceinline__ uint32_t operator()(int64_t i) const { return __ldg(p + i); }
@@ -906,7 +922,7 @@ __global__ void __launch_bounds__(256) k_emit_syms(const uint8_t *in, uint64_t i
     const uint64_t *bnd = bnd_all + (uint64_t)j * (nchunks + 1);
     const uint64_t b0 = bnd[k], b1 = bnd[k + 1];
     if (b0 >= b1) return;
-    const InBytes bytes{in + (uint64_t)j * in_stride};
+    const InBytesCached bytes{in + (uint64_t)j * in_stride};
     uint32_t *syms = syms_all + (uint64_t)j * (n + 1);
     uint64_t *btop = blk_top_all + (uint64_t)j * maxb;
     uint64_t *bstart = blk_start_all + (uint64_t)j * maxb;
