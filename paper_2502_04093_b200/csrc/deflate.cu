@@ -928,6 +928,7 @@ __global__ void __launch_bounds__(256) k_emit_syms(const uint8_t *in, uint64_t i
     uint64_t *bstart = blk_start_all + (uint64_t)j * maxb;
     int tag = entry_all[(uint64_t)j * (nchunks + 1) + k];
     uint64_t g = symoff_all[(uint64_t)j * nchunks + k];
+    uint64_t g0 = g;  // first symbol of the current stretch this thread writes itself
     const uint32_t *nbreak = nbreak_all + (uint64_t)j * (nchunks + 1);
     int64_t p = (int64_t)b0;
     // the record at p-1 is only read under a pending match (tags C*), and it is then the record
@@ -935,19 +936,49 @@ __global__ void __launch_bounds__(256) k_emit_syms(const uint8_t *in, uint64_t i
     // so every record load is 32 separate L1 accesses)
     int64_t cp = -1;
     uint64_t cr = 0;
+    // symbols leave in 16-byte stores: four consecutive ones gathered in registers once g is a
+    // multiple of 4 (every symbol of [g0, g_end) is this thread's; the lanes' symbol ranges lie
+    // ~1 KiB apart, so a 4-byte store per symbol was 32 separate L1 accesses per step)
+    uint32_t sb0 = 0, sb1 = 0, sb2 = 0;
+    const uint64_t ao = (reinterpret_cast<uintptr_t>(syms) >> 2) & 3;  // groups by address (a stream's symbols start at any word)
+    auto flush = [&](uint64_t ge) {  // the partial group before ge, if it began in this thread's stretch
+        const unsigned r = (unsigned)((ge + ao) & 3);
+        const uint64_t gb = ge - r;
+        if (r && ge >= g0 + r) {
+            syms[gb] = sb0;
+            if (r > 1) syms[gb + 1] = sb1;
+            if (r > 2) syms[gb + 2] = sb2;
+        }
+    };
+    auto put = [&](uint64_t gi, uint32_t v) {
+        const unsigned r = (unsigned)((gi + ao) & 3);
+        if (r == 0) sb0 = v;
+        else if (r == 1) sb1 = v;
+        else if (r == 2) sb2 = v;
+        else if (gi >= g0 + 3) {
+            *reinterpret_cast<uint4 *>(syms + gi - 3) = make_uint4(sb0, sb1, sb2, v);
+            return;
+        } else {
+            syms[gi] = v;
+            return;
+        }
+        if (gi < g0 + r) syms[gi] = v;  // before the stretch's first whole group: stored at once
+    };
     while (p < (int64_t)b1) {
         const int64_t m = periodic_run(p, tag, n, nbreak);
         if (m > 64) {  // long stretch: hand it to k_emit_runs
             const unsigned long long t = atomicAdd(nruns, 1ull);
             runs[t] = RunTask{(uint64_t)p, g, (uint64_t)m, j};
+            flush(g);  // (k_emit_runs writes the stretch's symbols: a new stretch of own symbols follows)
             g += (uint64_t)m;
+            g0 = g;
             p += MAX_MATCH * m;
             continue;
         }
         if (m > 0) {
             for (int64_t i = 0; i < m; ++i, ++g) {
                 const int64_t a = p + MAX_MATCH * i;
-                syms[g] = sym_match(MAX_MATCH, mrec_d128(R(a)));
+                put(g, sym_match(MAX_MATCH, mrec_d128(R(a))));
                 if (g % BLOCK_SYMS == 0) bstart[g / BLOCK_SYMS] = (uint64_t)a;
                 if (g % BLOCK_SYMS == BLOCK_SYMS - 1) btop[g / BLOCK_SYMS] = (uint64_t)a + 1;
             }
@@ -960,7 +991,7 @@ __global__ void __launch_bounds__(256) k_emit_syms(const uint8_t *in, uint64_t i
         cp = p, cr = rp;
         const Step s = parse_step(p, tag, (int64_t)n, rp, rpm1, bytes);
         if (s.emit) {
-            syms[g] = s.emit == 2 ? sym_match(s.len, s.dist) : sym_literal(s.len);
+            put(g, s.emit == 2 ? sym_match(s.len, s.dist) : sym_literal(s.len));
             if (g % BLOCK_SYMS == 0) bstart[g / BLOCK_SYMS] = (uint64_t)p - 1;
             if (g % BLOCK_SYMS == BLOCK_SYMS - 1) btop[g / BLOCK_SYMS] = (uint64_t)p;
             ++g;
@@ -968,6 +999,7 @@ __global__ void __launch_bounds__(256) k_emit_syms(const uint8_t *in, uint64_t i
         p = s.next_p;
         tag = s.next_tag;
     }
+    flush(g);  // the last, partial group
 }
 
 __global__ void __launch_bounds__(256) k_emit_runs(uint64_t n, const uint64_t *rec_all, uint32_t *syms_all,
